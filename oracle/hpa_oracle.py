@@ -1,0 +1,227 @@
+"""Plain, slow, obviously-correct fp64 oracle for hybrid paged attention.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py). Citations: `P:Lnnn` is a
+line of the paper text, `S:Lnnn` a line of SPEC.md, `§8(c) Ax` a
+reading listed in SURVEY.md §8(c) and DESIGN.md "Readings of the paper".
+"""
+from __future__ import annotations
+
+import math
+from typing import Dict, List, Optional, Tuple
+
+import numpy as np
+
+META_LATENT_BIT = 1 << 15  # export-table encoding: bit 15 = latent page, low bits = valid rows
+
+
+def kv_cache_bytes(num_layers: int, num_kv_heads: int, head_dim: int, seq_len: int,
+                   elem_bytes: int) -> int:
+    """KV size = 2 x L x H_kv x d_h x N x bytes.
+
+    PAPER.md P:L232-235 (§3 "KV cache cost", Eq. KV size); the factor 2 is K and V.
+    """
+    return 2 * num_layers * num_kv_heads * head_dim * seq_len * elem_bytes
+
+
+class _Segment:
+    """One segment of a sequence: a run of TOKEN rows or one LATENT set.
+
+    P:L251: "two types of KV cache": regular (prefix + dynamic) KV and the
+    compressed KV of meta latent tokens, both stored in blocks.
+    K, V: fp64 arrays [L][n][H_kv][d] holding the exact bf16 values.
+    """
+
+    def __init__(self, kind: str, set_id: int, k: np.ndarray, v: np.ndarray):
+        self.kind = kind
+        self.set_id = set_id
+        self.k = k
+        self.v = v
+
+    @property
+    def rows(self) -> int:
+        return self.k.shape[1]
+
+
+class OracleCache:
+    """Independent model of the hybrid paged cache at the level of logical rows.
+
+    It never looks at pages; it only records, per sequence, the ordered list of
+    segments that the op log produces. Rules:
+      * append extends the trailing TOKEN segment, or opens a new one after a
+        LATENT set (§8(b) "Append");
+      * install with set_id = -1 appends a new LATENT set at the end; set ids are
+        a per-sequence counter starting at 0 (reading "set ids");
+      * install with an existing set_id replaces that set's rows in place in the
+        logical order ("updatable memory", §8(c) A13);
+      * remove drops the set; release drops the sequence.
+    """
+
+    def __init__(self, num_layers: int, num_q_heads: int, num_kv_heads: int, head_dim: int,
+                 page_size: int):
+        if num_q_heads % num_kv_heads != 0:
+            raise ValueError("num_q_heads must be a multiple of num_kv_heads (S:L25)")
+        self.L = num_layers
+        self.Hq = num_q_heads
+        self.Hkv = num_kv_heads
+        self.d = head_dim
+        self.P = page_size
+        self.seqs: Dict[int, List[_Segment]] = {}
+        self.next_set: Dict[int, int] = {}
+
+    # -- op log ---------------------------------------------------------------
+    def create_seq(self, seq_id: int) -> None:
+        self.seqs[seq_id] = []
+        self.next_set[seq_id] = 0
+
+    def release(self, seq_id: int) -> None:
+        del self.seqs[seq_id]
+        del self.next_set[seq_id]
+
+    def append(self, seq_id: int, k: np.ndarray, v: np.ndarray) -> None:
+        """k, v: [L][n][H_kv][d] (values of the bf16 inputs)."""
+        k = np.asarray(k, dtype=np.float64)
+        v = np.asarray(v, dtype=np.float64)
+        segs = self.seqs[seq_id]
+        if segs and segs[-1].kind == "token":
+            last = segs[-1]
+            last.k = np.concatenate([last.k, k], axis=1)
+            last.v = np.concatenate([last.v, v], axis=1)
+        else:
+            segs.append(_Segment("token", -1, k.copy(), v.copy()))
+
+    def install(self, seq_id: int, set_id: int, kv: np.ndarray) -> int:
+        """kv: [L][2][m][H_kv][d] (SPEC CompressedMemory payload)."""
+        kv = np.asarray(kv, dtype=np.float64)
+        k = kv[:, 0].copy()
+        v = kv[:, 1].copy()
+        segs = self.seqs[seq_id]
+        if set_id < 0:
+            set_id = self.next_set[seq_id]
+            self.next_set[seq_id] += 1
+            segs.append(_Segment("latent", set_id, k, v))
+            return set_id
+        for s in segs:
+            if s.kind == "latent" and s.set_id == set_id:
+                s.k, s.v = k, v
+                return set_id
+        raise KeyError(f"unknown latent set {set_id}")
+
+    def remove(self, seq_id: int, set_id: int) -> None:
+        segs = self.seqs[seq_id]
+        for i, s in enumerate(segs):
+            if s.kind == "latent" and s.set_id == set_id:
+                del segs[i]
+                return
+        raise KeyError(f"unknown latent set {set_id}")
+
+    # -- views ----------------------------------------------------------------
+    def seq_len(self, seq_id: int) -> int:
+        return sum(s.rows for s in self.seqs[seq_id])
+
+    def latent_rows(self, seq_id: int) -> int:
+        return sum(s.rows for s in self.seqs[seq_id] if s.kind == "latent")
+
+    def logical_kv(self, seq_id: int, layer: int) -> Tuple[np.ndarray, np.ndarray]:
+        """Gather route 1: concatenate segments in order -> K, V [H_kv][Lb][d]."""
+        segs = self.seqs[seq_id]
+        if not segs:
+            z = np.zeros((self.Hkv, 0, self.d))
+            return z, z.copy()
+        k = np.concatenate([s.k[layer] for s in segs], axis=0)  # [Lb][H_kv][d]
+        v = np.concatenate([s.v[layer] for s in segs], axis=0)
+        return k.transpose(1, 0, 2).copy(), v.transpose(1, 0, 2).copy()
+
+    def expected_table(self, seq_id: int) -> List[Tuple[str, int, int]]:
+        """Expected block-table entries (kind, valid_rows, pos0) for this sequence."""
+        return expected_table([(s.kind, s.rows) for s in self.seqs[seq_id]], self.P)
+
+
+def expected_table(segments: List[Tuple[str, int]], page_size: int) -> List[Tuple[str, int, int]]:
+    """Block-table entries implied by an ordered segment list.
+
+    SURVEY §8(a) a1 / DESIGN.md reading A7: every segment starts on a fresh page,
+    only the last page of a segment may be partial, and pos0 of an entry (the
+    logical index of its row 0) is the sum of valid_rows over earlier entries.
+    """
+    out = []
+    pos = 0
+    for kind, rows in segments:
+        left = rows
+        while left > 0:
+            take = min(page_size, left)
+            out.append((kind, take, pos))
+            pos += take
+            left -= take
+    return out
+
+
+def gather_physical(k_pool: np.ndarray, v_pool: np.ndarray, pages: List[int],
+                    meta: List[int], layer: int) -> Tuple[np.ndarray, np.ndarray]:
+    """Gather route 2: walk the block table in order and
+    take rows 0..valid_rows-1 of pool[layer][page][h] for each entry.
+
+    k_pool, v_pool: [L][NP][H_kv][P][d] (the device pool layout).
+    meta: export-table encoding (bit 15 latent, low 15 bits valid_rows).
+    Returns K, V [H_kv][Lb][d].
+    """
+    ks, vs = [], []
+    for page, m in zip(pages, meta):
+        valid = m & (META_LATENT_BIT - 1)
+        ks.append(k_pool[layer, page, :, :valid, :])
+        vs.append(v_pool[layer, page, :, :valid, :])
+    if not ks:
+        h, d = k_pool.shape[2], k_pool.shape[4]
+        z = np.zeros((h, 0, d))
+        return z, z.copy()
+    return np.concatenate(ks, axis=1), np.concatenate(vs, axis=1)
+
+
+def attend(q: np.ndarray, k_log: np.ndarray, v_log: np.ndarray, scale: float) -> np.ndarray:
+    """fp64 softmax attention of the last Tq logical rows.
+
+    q: [Tq][Hq][d]; k_log, v_log: [H_kv][Lb][d]; returns o [Tq][Hq][d].
+    Query row t sits at logical index i = Lb - Tq + t and sees keys j <= i
+    (reading A1: mask by logical index in block-table order, bottom-right).
+    q-head hq reads kv-head floor(hq / G), G = Hq / H_kv (reading A6).
+      s_j = scale * sum_d q[t,hq,d] K[h,j,d];  p_j = exp(s_j - max_j s_j);
+      o   = sum_j p_j V[h,j] / sum_j p_j.
+    Decode is Tq = 1; chunked prefill is Tq = C.
+    """
+    q = np.asarray(q, dtype=np.float64)
+    k_log = np.asarray(k_log, dtype=np.float64)
+    v_log = np.asarray(v_log, dtype=np.float64)
+    tq, hq_n, d = q.shape
+    hkv, lb, _ = k_log.shape
+    if tq > lb or lb == 0:
+        raise ValueError("need 1 <= Tq <= Lb (reading A11)")
+    group = hq_n // hkv
+    out = np.zeros((tq, hq_n, d), dtype=np.float64)
+    for hq in range(hq_n):
+        h = hq // group
+        for t in range(tq):
+            i = lb - tq + t
+            keys = k_log[h, : i + 1]          # [i+1][d]
+            vals = v_log[h, : i + 1]
+            s = scale * (keys @ q[t, hq])      # K q^T orientation
+            p = np.exp(s - s.max())
+            out[t, hq] = (p @ vals) / p.sum()
+    return out
+
+
+def decode_reference(cache: OracleCache, seq_id: int, layer: int, q: np.ndarray,
+                     scale: float) -> np.ndarray:
+    """Decode: the query is the last logical row (reading A8). q: [Hq][d]."""
+    k, v = cache.logical_kv(seq_id, layer)
+    return attend(np.asarray(q)[None], k, v, scale)[0]
+
+
+def prefill_reference(cache: OracleCache, seq_id: int, layer: int, q: np.ndarray,
+                      scale: float) -> np.ndarray:
+    """Chunked prefill: queries are the last Tq logical rows. q: [Tq][Hq][d]."""
+    k, v = cache.logical_kv(seq_id, layer)
+    return attend(q, k, v, scale)
+
+
+def default_scale(head_dim: int) -> float:
+    """Reading A5: softmax scale 1/sqrt(d) when the caller passes none."""
+    return 1.0 / math.sqrt(head_dim)

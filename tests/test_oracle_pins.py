@@ -1,0 +1,282 @@
+"""Pins for the CPU oracle against things other than itself (CPU only).
+
+Each test names what fixes the expected value: a number printed by the paper,
+a closed form, a library routine (torch SDPA) with an explicit mask, or a
+pure-Python brute force written independently of oracle/hpa_oracle.py.
+"""
+import math
+import os
+import random
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import OracleCache, attend, expected_table, gather_physical, kv_cache_bytes
+from oracle.hpa_oracle import META_LATENT_BIT
+from workloads import Draw, Shape, tiny_decode
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def f64(t):
+    return t.to(torch.float64).numpy()
+
+
+def build_cache(shape: Shape, script, seed=0, v_scale=1.0):
+    """Drive an OracleCache with a list of ("latent", m) / ("tokens", n) segments."""
+    c = OracleCache(shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim,
+                    shape.page_size)
+    c.create_seq(0)
+    d = Draw(seed)
+    for kind, n in script:
+        if kind == "latent":
+            c.install(0, -1, f64(d.latent(shape, n, v_scale)))
+        else:
+            k, v = d.tokens(shape, n, v_scale)
+            c.append(0, f64(k), f64(v))
+    return c, d
+
+
+# --------------------------------------------------------------------------- paper numbers
+def test_kv_bytes_matches_paper_golden():
+    """P:L232-240 (§3 KV cache cost): 114688 B/token for Qwen3-1.7B, 14 MiB for m=128."""
+    rows = 0
+    with open(os.path.join(GOLDEN, "kv_bytes_paper.txt")) as f:
+        for line in f:
+            line = line.split("#")[0].strip()
+            if not line:
+                continue
+            L, h, d, n, b, exp = map(int, line.split())
+            assert kv_cache_bytes(L, h, d, n, b) == exp
+            rows += 1
+    assert rows == 5
+    assert kv_cache_bytes(28, 8, 128, 1024, 2) == 112 * 1024 * 1024
+    assert kv_cache_bytes(28, 8, 128, 128, 2) == 14 * 1024 * 1024
+
+
+# --------------------------------------------------------------------------- brute force
+def _brute_force(q, k, v, scale):
+    """Pure-Python triple loop (no numpy), bottom-right causal, hq -> hq // G."""
+    tq, hq_n, d = len(q), len(q[0]), len(q[0][0])
+    hkv, lb = len(k), len(k[0])
+    g = hq_n // hkv
+    out = [[[0.0] * d for _ in range(hq_n)] for _ in range(tq)]
+    for t in range(tq):
+        last = lb - tq + t
+        for hq in range(hq_n):
+            h = hq // g
+            scores = []
+            for j in range(last + 1):
+                acc = 0.0
+                for x in range(d):
+                    acc += q[t][hq][x] * k[h][j][x]
+                scores.append(acc * scale)
+            mx = max(scores)
+            w = [math.exp(s - mx) for s in scores]
+            tot = sum(w)
+            for x in range(d):
+                out[t][hq][x] = sum(w[j] * v[h][j][x] for j in range(last + 1)) / tot
+    return out
+
+
+@pytest.mark.parametrize("variant", ["a", "b", "c"])
+def test_tiny_config_vs_bruteforce(variant):
+    """BASELINE.json configs[0] (tiny decode; b: partial latent page; c: prefill)."""
+    w = tiny_decode(variant)
+    c, d = build_cache(w.shape, w.seqs[0].segments)
+    q = f64(d.queries(w.shape, w.seqs[0].q_len))
+    k, v = c.logical_kv(0, 0)
+    got = attend(q, k, v, w.shape.scale)
+    ref = np.array(_brute_force(q.tolist(), k.tolist(), v.tolist(), w.shape.scale))
+    assert np.max(np.abs(got - ref)) <= 1e-12
+
+
+# --------------------------------------------------------------------------- library routine
+@pytest.mark.parametrize("tq,lb,hq,hkv,d", [(1, 64, 2, 1, 64), (16, 64, 2, 1, 64),
+                                            (7, 300, 8, 2, 32), (33, 100, 4, 4, 16)])
+def test_vs_torch_sdpa_explicit_bottom_right_mask(tq, lb, hq, hkv, d):
+    """torch SDPA in fp64 with an explicit boolean bottom-right mask (is_causal is
+    top-left aligned when Lq != Lk) and repeat_kv GQA."""
+    g = torch.Generator().manual_seed(tq * 1000 + lb)
+    q = torch.randn(tq, hq, d, generator=g, dtype=torch.float64)
+    k = torch.randn(hkv, lb, d, generator=g, dtype=torch.float64)
+    v = torch.randn(hkv, lb, d, generator=g, dtype=torch.float64)
+    scale = 1.0 / math.sqrt(d)
+    got = attend(q.numpy(), k.numpy(), v.numpy(), scale)
+    rows = torch.arange(tq)[:, None] + (lb - tq)
+    mask = torch.arange(lb)[None, :] <= rows                       # [tq][lb]
+    kk = k.repeat_interleave(hq // hkv, dim=0)                      # [hq][lb][d]
+    vv = v.repeat_interleave(hq // hkv, dim=0)
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        q.transpose(0, 1), kk, vv, attn_mask=mask, scale=scale).transpose(0, 1)
+    assert np.max(np.abs(got - ref.numpy())) <= 1e-12
+
+
+# --------------------------------------------------------------------------- closed forms
+def test_uniform_v_gives_v():
+    """All visible V rows equal v -> o = v."""
+    rng = np.random.default_rng(0)
+    k = rng.standard_normal((2, 50, 16))
+    v = np.broadcast_to(rng.standard_normal((2, 1, 16)), (2, 50, 16)).copy()
+    q = rng.standard_normal((5, 4, 16))
+    o = attend(q, k, v, 0.25)
+    for hq in range(4):
+        assert np.max(np.abs(o[:, hq] - v[hq // 2, 0])) <= 1e-12
+
+
+def test_equal_keys_give_mean_of_visible_v():
+    """All visible K rows equal -> uniform weights -> o = mean of the visible V rows."""
+    rng = np.random.default_rng(1)
+    k = np.broadcast_to(rng.standard_normal((1, 1, 8)), (1, 40, 8)).copy()
+    v = rng.standard_normal((1, 40, 8))
+    q = rng.standard_normal((3, 2, 8))
+    o = attend(q, k, v, 0.3)
+    for t in range(3):
+        i = 40 - 3 + t
+        assert np.max(np.abs(o[t, 0] - v[0, : i + 1].mean(axis=0))) <= 1e-12
+
+
+def test_single_row_and_zero_query():
+    rng = np.random.default_rng(2)
+    k = rng.standard_normal((1, 1, 8))
+    v = rng.standard_normal((1, 1, 8))
+    assert np.max(np.abs(attend(rng.standard_normal((1, 1, 8)), k, v, 1.0)[0, 0] - v[0, 0])) == 0
+    k = rng.standard_normal((1, 30, 8))
+    v = rng.standard_normal((1, 30, 8))
+    o = attend(np.zeros((1, 1, 8)), k, v, 1.0)                   # q = 0 -> mean of V
+    assert np.max(np.abs(o[0, 0] - v[0].mean(axis=0))) <= 1e-12
+
+
+def test_gqa_mapping_constant_v_per_kv_head():
+    """kv-head h holds constant V = h+1 -> q-head hq must return floor(hq/G)+1 (A6)."""
+    rng = np.random.default_rng(3)
+    hkv, g, lb, d = 4, 3, 20, 8
+    k = rng.standard_normal((hkv, lb, d))
+    v = np.stack([np.full((lb, d), h + 1.0) for h in range(hkv)])
+    o = attend(rng.standard_normal((2, hkv * g, d)), k, v, 0.5)
+    for hq in range(hkv * g):
+        assert np.max(np.abs(o[:, hq] - (hq // g + 1.0))) <= 1e-12
+
+
+def test_mask_perturbation_beyond_causal_bound():
+    """Perturbing keys/values beyond each row's causal bound leaves that row unchanged."""
+    rng = np.random.default_rng(4)
+    k = rng.standard_normal((1, 30, 8))
+    v = rng.standard_normal((1, 30, 8))
+    q = rng.standard_normal((10, 2, 8))
+    base = attend(q, k, v, 0.4)
+    k2, v2 = k.copy(), v.copy()
+    k2[:, 25:] += 100.0
+    v2[:, 25:] -= 50.0
+    pert = attend(q, k2, v2, 0.4)
+    # rows t with i = 20 + t <= 24 see only keys < 25
+    assert np.array_equal(base[:5], pert[:5])
+    assert not np.allclose(base[5:], pert[5:])
+
+
+def test_chunk_equals_sequential_decodes():
+    """Causal consistency: prefill of C rows = C decodes on growing prefixes."""
+    rng = np.random.default_rng(5)
+    k = rng.standard_normal((2, 40, 16))
+    v = rng.standard_normal((2, 40, 16))
+    q = rng.standard_normal((8, 4, 16))
+    full = attend(q, k, v, 0.25)
+    for t in range(8):
+        lb = 40 - 8 + t + 1
+        dec = attend(q[t:t + 1], k[:, :lb], v[:, :lb], 0.25)
+        assert np.max(np.abs(full[t] - dec[0])) <= 1e-12
+
+
+# --------------------------------------------------------------------------- paging
+def _place(cache: OracleCache, seq: int, num_pages: int, rng: random.Random, L: int):
+    """Independent test-side placement: random physical page per table entry."""
+    tab = cache.expected_table(seq)
+    pages = rng.sample(range(num_pages), len(tab))
+    P, h, d = cache.P, cache.Hkv, cache.d
+    kp = np.full((L, num_pages, h, P, d), 7.0)   # finite junk in unused rows
+    vp = np.full((L, num_pages, h, P, d), -3.0)
+    for layer in range(L):
+        k, v = cache.logical_kv(seq, layer)
+        for (kind, valid, pos0), pg in zip(tab, pages):
+            kp[layer, pg, :, :valid] = k[:, pos0:pos0 + valid]
+            vp[layer, pg, :, :valid] = v[:, pos0:pos0 + valid]
+    meta = [valid | (META_LATENT_BIT if kind == "latent" else 0) for kind, valid, _ in tab]
+    return kp, vp, pages, meta
+
+
+def test_paged_equals_contiguous_under_random_permutations():
+    """Route 2 (physical dump + table) == route 1 (model) bitwise for several
+    random physical placements, and attention over it is identical."""
+    shape = Shape(2, 4, 2, 16, 16)
+    script = [("latent", 128), ("latent", 8), ("tokens", 37), ("latent", 20), ("tokens", 5)]
+    c, d = build_cache(shape, script)
+    q = f64(d.queries(shape, 1))
+    outs = []
+    for trial in range(4):
+        kp, vp, pages, meta = _place(c, 0, 64, random.Random(trial), 2)
+        for layer in range(2):
+            k1, v1 = c.logical_kv(0, layer)
+            k2, v2 = gather_physical(kp, vp, pages, meta, layer)
+            assert np.array_equal(k1, k2) and np.array_equal(v1, v2)
+        outs.append(attend(q, *gather_physical(kp, vp, pages, meta, 1), shape.scale))
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
+
+
+def test_expected_table_structure():
+    """Every segment starts on a fresh page; only its last page may be partial;
+    pos0 = prefix sum of valid_rows; kinds follow the op log (reading A7)."""
+    tab = expected_table([("latent", 128), ("latent", 8), ("token", 37), ("latent", 20)], 16)
+    valid = [v for _, v, _ in tab]
+    assert valid == [16] * 8 + [8] + [16, 16, 5] + [16, 4]
+    assert [p for _, _, p in tab] == list(np.cumsum([0] + valid[:-1]))
+    assert [k for k, _, _ in tab] == ["latent"] * 9 + ["token"] * 3 + ["latent"] * 2
+    # m=8, B=16 -> 1 compressed block; n=17, B=16 -> 2 blocks
+    assert len(expected_table([("latent", 8)], 16)) == 1
+    assert len(expected_table([("token", 17)], 16)) == 2
+
+
+def test_uncompressed_replacement_equals_plain_causal_attention():
+    """Replacing a latent set by the document's N uncompressed token rows gives
+    plain causal attention over the contiguous [doc, rest] (library SDPA)."""
+    shape = Shape(1, 4, 2, 32, 16)
+    c, d = build_cache(shape, [("latent", 128), ("tokens", 50)])
+    doc = f64(d.latent(shape, 300))          # "uncompressed" doc rows, N=300
+    c.install(0, 0, doc)                     # replace set 0 (different row count)
+    k, v = c.logical_kv(0, 0)
+    assert k.shape[1] == 350
+    q = f64(d.queries(shape, 3))
+    got = attend(q, k, v, shape.scale)
+    kk = torch.from_numpy(np.concatenate([doc[0, 0].transpose(1, 0, 2), k[:, 300:]], axis=1))
+    vv = torch.from_numpy(np.concatenate([doc[0, 1].transpose(1, 0, 2), v[:, 300:]], axis=1))
+    mask = torch.arange(350)[None, :] <= (torch.arange(3)[:, None] + 347)
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        torch.from_numpy(q).transpose(0, 1), kk.repeat_interleave(2, 0), vv.repeat_interleave(2, 0),
+        attn_mask=mask, scale=shape.scale).transpose(0, 1)
+    assert np.max(np.abs(got - ref.numpy())) <= 1e-12
+
+
+def test_replacement_is_o1_and_leaves_token_rows_untouched():
+    """O(1) update: replacing a latent set changes only that set's rows."""
+    shape = Shape(1, 2, 1, 16, 16)
+    c, d = build_cache(shape, [("latent", 128), ("tokens", 100), ("latent", 128), ("tokens", 9)])
+    k0, v0 = c.logical_kv(0, 0)
+    c.install(0, 1, f64(d.latent(shape, 128)))
+    k1, v1 = c.logical_kv(0, 0)
+    assert np.array_equal(k0[:, :228], k1[:, :228]) and np.array_equal(k0[:, 356:], k1[:, 356:])
+    assert not np.array_equal(k0[:, 228:356], k1[:, 228:356])
+    assert c.latent_rows(0) == 256  # per-doc rows = m regardless of document length
+
+
+def test_set_ids_and_remove():
+    shape = Shape(1, 2, 1, 16, 16)
+    c, d = build_cache(shape, [("latent", 16), ("latent", 32)])
+    assert [s.set_id for s in c.seqs[0]] == [0, 1]
+    c.remove(0, 0)
+    assert c.install(0, -1, f64(d.latent(shape, 4))) == 2
+    assert [(s.kind, s.rows) for s in c.seqs[0]] == [("latent", 32), ("latent", 4)]
+    with pytest.raises(KeyError):
+        c.remove(0, 7)
+    with pytest.raises(ValueError):
+        attend(np.zeros((3, 1, 4)), np.zeros((1, 2, 4)), np.zeros((1, 2, 4)), 1.0)
