@@ -1,0 +1,176 @@
+/*
+ * hpa.h -- C ABI of the B200-native hybrid paged attention (HPA) library.
+ *
+ * What it implements: PAPER.md §3 "Hybrid paged attention for LLM serving"
+ * (P:L248-251): vLLM-style paged attention whose blocks hold two kinds of KV
+ * cache -- regular (prefix + dynamic) token KV and the compressed KV of the
+ * meta latent tokens -- "store[d] ... into the corresponding blocks".
+ * HPA computes ordinary causal softmax attention over the *logical* KV
+ * sequence (block-table order); paging and the latent/token tag change storage
+ * and update cost, not the math.
+ *
+ * Conventions for every call:
+ *   - All calls return hpa_status_t; no C++ exception crosses the ABI.
+ *     hpa_last_error() returns a thread-local message for the last failure.
+ *   - "device" pointers are CUDA device addresses on the cache's device
+ *     (e.g. torch.Tensor.data_ptr()); they must be 16-byte aligned and
+ *     contiguous in the documented layout. "host" pointers are CPU memory.
+ *   - The caller owns q / k / v / out / payload buffers; the cache owns its K/V
+ *     pools, block tables and staging. Device work is enqueued on the caller's
+ *     stream (`stream` is a cudaStream_t, NULL = legacy default stream); all
+ *     calls on one cache must use the same stream or be ordered by the caller.
+ *     Input buffers may be reused once the stream has passed the call.
+ *   - Host metadata (allocator, tables) is updated synchronously; the device
+ *     copy of the tables is updated stream-ordered before the next kernel.
+ *   - One cache = one owner thread; calls on a cache are not
+ *     thread-safe. Different caches (e.g. one per GPU) are independent.
+ *   - Failure atomicity: a call that returns an error leaves the cache
+ *     unchanged (HPA_ERR_OUT_OF_PAGES is the "backpressure" signal of S:L388).
+ *   - bf16 everywhere (KV bytes = 2); fp32 accumulation.
+ */
+#ifndef HPA_H_
+#define HPA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hpa_cache hpa_cache_t;
+typedef void* hpa_stream_t; /* a cudaStream_t */
+
+typedef enum {
+  HPA_OK = 0,
+  HPA_ERR_INVALID_ARG = 1,   /* bad shape / layer / length / alignment / duplicate seq / q_len > seq_len */
+  HPA_ERR_OUT_OF_PAGES = 2,  /* pool exhausted; cache left unchanged (S:L388 backpressure) */
+  HPA_ERR_SEQ_CAPACITY = 3,  /* a sequence would exceed max_pages_per_seq */
+  HPA_ERR_UNKNOWN_SEQ = 4,
+  HPA_ERR_UNKNOWN_SET = 5,
+  HPA_ERR_CUDA = 6,          /* message carries the cudaError string */
+  HPA_ERR_UNSUPPORTED = 7    /* head_dim not in {64,128}, page_size not in {16,32,64,128,256},
+                                G = Hq/H_kv > 16, or device is not sm_100 */
+} hpa_status_t;
+
+/* Cache configuration. Invariant: num_q_heads % num_kv_heads == 0. */
+typedef struct {
+  int32_t num_layers;        /* L: layers held in the pool (one pool for all layers) */
+  int32_t num_q_heads;       /* Hq */
+  int32_t num_kv_heads;      /* H_kv (8 for Qwen3) */
+  int32_t head_dim;          /* d: 64 or 128 */
+  int32_t page_size;         /* P rows per page: 16, 32, 64, 128 or 256 (reading A15) */
+  int32_t num_pages;         /* NP physical pages, shared by all layers */
+  int32_t max_seqs;          /* sequence slots; seq ids are 0..max_seqs-1 */
+  int32_t max_pages_per_seq; /* block-table row length */
+  int32_t device;            /* CUDA ordinal */
+  uint64_t placement_seed;   /* 0: free list in page order; else a seeded shuffle of the
+                                free list (physical placement is then a random permutation,
+                                SURVEY §8(d) "Physical pages") */
+} hpa_config_t;
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* hpa_last_error(void);
+const char* hpa_status_string(hpa_status_t s);
+
+/* KV size = 2 x L x H_kv x d_h x N x bytes (§3 Eq. "KV size").
+ * hpa_kv_bytes(28, 8, 128, 1, 2) == 114688. Pure host arithmetic. */
+uint64_t hpa_kv_bytes(int64_t num_layers, int64_t num_kv_heads, int64_t head_dim,
+                      int64_t seq_len, int64_t elem_bytes);
+
+/* ---------------------------------------------------------------- lifecycle
+ * Allocates K and V pools, each bf16 [L][NP][H_kv][P][d] (zero-filled), plus
+ * device block tables (page id, pos0, meta per entry; seq_len; entry count).
+ * "pre-allocating KV cache in the device memory and partitioning them into
+ * fixed-size non-continuous blocks". */
+hpa_status_t hpa_cache_create(const hpa_config_t* cfg, hpa_cache_t** out);
+hpa_status_t hpa_cache_destroy(hpa_cache_t* c);
+
+/* Device pool base pointers and the byte size of ONE pool (introspection / tests). */
+hpa_status_t hpa_cache_pools(hpa_cache_t* c, void** k_pool, void** v_pool, uint64_t* pool_bytes);
+
+/* Allocator state: free pages, pages referenced by at least one table, live sequences. */
+hpa_status_t hpa_cache_stats(hpa_cache_t* c, int32_t* free_pages, int32_t* used_pages,
+                             int32_t* live_seqs);
+
+/* Creates an empty sequence; *seq_id receives the lowest free slot. */
+hpa_status_t hpa_seq_create(hpa_cache_t* c, int32_t* seq_id);
+/* Drops a sequence and decrements the refcount of each of its pages. */
+hpa_status_t hpa_seq_release(hpa_cache_t* c, int32_t seq_id);
+
+/* ---------------------------------------------------------------- append
+ * The paper's "store ... into the corresponding blocks" op for regular KV
+ * (P:L251). Appends n_new[i] token rows to sequence seq_ids[i] for i < n_seqs.
+ * k, v: device bf16 [L][sum(n_new)][H_kv][d], rows of the sequences in call
+ * order. Each sequence's trailing TOKEN segment is extended (its last page is
+ * filled first); if the sequence ends with a LATENT set (or is empty) a new
+ * TOKEN segment starts on a fresh page. Allocation is all-or-nothing across the
+ * call. seq_ids must be distinct. One kernel launch (+ one H2D metadata copy). */
+hpa_status_t hpa_append_kv(hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids /*host*/,
+                           const int32_t* n_new /*host*/, const void* k, const void* v,
+                           hpa_stream_t stream);
+
+/* ---------------------------------------------------------------- latent sets (a3)
+ * Installs or replaces a latent-memory page set: the m_rows-row compressed KV of
+ * a document/history ("compressed ... KV cache with O(1) length is used as
+ * the updatable memory").
+ * kv: device bf16 [L][2][m_rows][H_kv][d] (K then V per layer).
+ * set_id == -1: append a new LATENT set at the end of the sequence (new segment
+ *   on fresh pages); set ids are a per-sequence counter starting at 0.
+ * set_id >= 0: replace that set. Same page count ceil(m/P): the set's pages are
+ *   rewritten in place; otherwise its pages are freed/allocated and the
+ *   sequence's table is spliced (later entries' pos0 shift). Token pages are
+ *   never touched (O(1) update). *set_id_out (may be NULL) receives the id. */
+hpa_status_t hpa_latent_set_install(hpa_cache_t* c, int32_t seq_id, int32_t set_id,
+                                    int32_t m_rows, const void* kv, hpa_stream_t stream,
+                                    int32_t* set_id_out);
+/* Batched form: n installs (distinct seq_ids), one kernel launch. kv_ptrs[i] is a
+ * device pointer to payload i ([L][2][m_rows[i]][H_kv][d]); set_ids_out may be NULL. */
+hpa_status_t hpa_latent_set_install_batch(hpa_cache_t* c, int32_t n, const int32_t* seq_ids,
+                                          const int32_t* set_ids, const int32_t* m_rows,
+                                          const void* const* kv_ptrs, hpa_stream_t stream,
+                                          int32_t* set_ids_out);
+/* Removes a latent set (frees its pages, splices the table). */
+hpa_status_t hpa_latent_set_remove(hpa_cache_t* c, int32_t seq_id, int32_t set_id);
+
+/* ---------------------------------------------------------------- attention (a4-a6)
+ * Decode (a4 + a5): for each listed sequence the query is its LAST logical row
+ * (its KV must already be appended; reading A8), so every stored row is visible.
+ * q: device bf16 [n_seqs][Hq][d]; out: device bf16 [n_seqs][Hq][d].
+ * out[b][hq] = softmax(scale * K_log[h] q^T) V_log[h], h = floor(hq / G).
+ * softmax_scale <= 0 selects 1/sqrt(d) (reading A5). Split-KV over pages +
+ * LSE combine; the split count depends only on the batch's page counts. */
+hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
+                        const void* q, void* out, float softmax_scale, hpa_stream_t stream);
+
+/* Chunked prefill (a6): queries of sequence i are its LAST q_lens[i] logical
+ * rows (1 <= q_lens[i] <= seq_len; their KV appended first). Query row t sits at
+ * logical index i = seq_len - q_len + t and attends keys j <= i (bottom-right
+ * causal; reading A1). q, out: device bf16 [sum(q_lens)][Hq][d] (varlen, in call
+ * order). tcgen05/TMEM/TMA kernel. */
+hpa_status_t hpa_prefill(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
+                         const int32_t* q_lens /*host*/, const void* q, void* out,
+                         float softmax_scale, hpa_stream_t stream);
+
+/* ---------------------------------------------------------------- introspection / tests
+ * Host-side sequence summary. */
+hpa_status_t hpa_seq_info(hpa_cache_t* c, int32_t seq_id, int32_t* len, int32_t* n_pages,
+                          int32_t* n_latent_rows);
+/* Gathers the logical K and V of (layer, seq) into device bf16 [H_kv][len][d]
+ * (one kernel; bit-exact copy of the stored rows in block-table order). */
+hpa_status_t hpa_export_logical_kv(hpa_cache_t* c, int32_t layer, int32_t seq_id, void* k_out,
+                                   void* v_out, hpa_stream_t stream);
+/* Host copy of a sequence's block table: pages[i], pos0[i] (logical index of the
+ * entry's row 0 = sum of earlier valid_rows) and meta[i] (bit 15 = latent page,
+ * low 15 bits = valid_rows) for i < *n_out <= cap. */
+hpa_status_t hpa_export_table(hpa_cache_t* c, int32_t seq_id, int32_t* pages, int32_t* pos0,
+                              uint16_t* meta, int32_t cap, int32_t* n_out);
+/* Testing / tuning hook: force the decode split count (0 = planner). */
+hpa_status_t hpa_set_decode_splits(hpa_cache_t* c, int32_t splits);
+/* Number of kernels this cache has launched so far (bench "gpu_launches"). */
+hpa_status_t hpa_launch_count(hpa_cache_t* c, uint64_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HPA_H_ */

@@ -1,0 +1,205 @@
+"""`Cache`: Python handle over one hpa_cache_t (one GPU). Marshalling only."""
+from __future__ import annotations
+
+import ctypes
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from ._lib import LIB, HPAConfig, c_i32, c_vp, check
+
+
+def _i32(xs) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(xs, dtype=np.int32).reshape(-1))
+
+
+def _p32(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def _stream(device: int, stream) -> c_vp:
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return c_vp(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+class _CAI:
+    """Zero-copy __cuda_array_interface__ view of cache-owned device memory."""
+
+    def __init__(self, ptr: int, shape, typestr: str = "<i2"):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 2, "strides": None}
+
+
+class Cache:
+    """Hybrid paged KV cache on one B200 (include/hpa.h, hpa_cache_create).
+
+    Pools: K and V, each bf16 [L][num_pages][H_kv][P][d]; block tables on the
+    device; allocator + segment lists on the host.
+    """
+
+    def __init__(self, num_layers: int, num_q_heads: int, num_kv_heads: int, head_dim: int,
+                 page_size: int, num_pages: int, max_seqs: int, max_pages_per_seq: int,
+                 device: int = 0, placement_seed: int = 0):
+        self.cfg = HPAConfig(num_layers, num_q_heads, num_kv_heads, head_dim, page_size, num_pages,
+                             max_seqs, max_pages_per_seq, device, placement_seed)
+        self.device = device
+        self.L, self.Hq, self.Hkv, self.d, self.P = (num_layers, num_q_heads, num_kv_heads,
+                                                      head_dim, page_size)
+        self.num_pages = num_pages
+        h = c_vp()
+        check(LIB.hpa_cache_create(ctypes.byref(self.cfg), ctypes.byref(h)))
+        self._h = h
+
+    # ------------------------------------------------------------------ lifecycle
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            check(LIB.hpa_cache_destroy(self._h))
+            self._h = c_vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def seq_create(self) -> int:
+        s = c_i32()
+        check(LIB.hpa_seq_create(self._h, ctypes.byref(s)))
+        return s.value
+
+    def seq_release(self, seq: int) -> None:
+        check(LIB.hpa_seq_release(self._h, seq))
+
+    def stats(self) -> Tuple[int, int, int]:
+        f, u, l = c_i32(), c_i32(), c_i32()
+        check(LIB.hpa_cache_stats(self._h, ctypes.byref(f), ctypes.byref(u), ctypes.byref(l)))
+        return f.value, u.value, l.value
+
+    # ------------------------------------------------------------------ checks
+    def _dev_tensor(self, t: torch.Tensor, name: str, shape=None) -> int:
+        if not isinstance(t, torch.Tensor) or t.device.type != "cuda" or t.device.index != self.device:
+            raise ValueError(f"{name} must be a CUDA tensor on cuda:{self.device}")
+        if t.dtype != torch.bfloat16:
+            raise ValueError(f"{name} must be bf16")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        if shape is not None and tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+        return t.data_ptr()
+
+    # ------------------------------------------------------------------ a2: append
+    def append_kv(self, seq_ids: Sequence[int], n_new: Sequence[int], k: torch.Tensor,
+                  v: torch.Tensor, stream=None) -> None:
+        """k, v: bf16 [L][sum(n_new)][H_kv][d] on the cache's device (hpa_append_kv)."""
+        ids, ns = _i32(seq_ids), _i32(n_new)
+        if ids.size != ns.size:
+            raise ValueError("seq_ids and n_new differ in length")
+        shape = (self.L, int(ns.sum()), self.Hkv, self.d)
+        kp = self._dev_tensor(k, "k", shape)
+        vp = self._dev_tensor(v, "v", shape)
+        check(LIB.hpa_append_kv(self._h, ids.size, _p32(ids), _p32(ns), c_vp(kp), c_vp(vp),
+                                _stream(self.device, stream)))
+
+    # ------------------------------------------------------------------ a3: latent sets
+    def latent_install(self, seq: int, set_id: int, kv: torch.Tensor, stream=None) -> int:
+        """kv: bf16 [L][2][m][H_kv][d]; set_id = -1 appends a new set. Returns the set id."""
+        m = kv.shape[2]
+        p = self._dev_tensor(kv, "kv", (self.L, 2, m, self.Hkv, self.d))
+        out = c_i32()
+        check(LIB.hpa_latent_set_install(self._h, seq, set_id, m, c_vp(p),
+                                         _stream(self.device, stream), ctypes.byref(out)))
+        return out.value
+
+    def latent_install_batch(self, seq_ids: Sequence[int], set_ids: Sequence[int],
+                             kvs: Sequence[torch.Tensor], stream=None) -> List[int]:
+        """One launch for many installs; kvs[i] bf16 [L][2][m_i][H_kv][d]."""
+        ids, sids = _i32(seq_ids), _i32(set_ids)
+        ms = _i32([kv.shape[2] for kv in kvs])
+        ptrs = (c_vp * len(kvs))(*[self._dev_tensor(kv, "kv", (self.L, 2, kv.shape[2], self.Hkv, self.d))
+                                   for kv in kvs])
+        out = np.zeros(len(kvs), dtype=np.int32)
+        check(LIB.hpa_latent_set_install_batch(self._h, ids.size, _p32(ids), _p32(sids), _p32(ms), ptrs,
+                                               _stream(self.device, stream), _p32(out)))
+        return out.tolist()
+
+    def latent_remove(self, seq: int, set_id: int) -> None:
+        check(LIB.hpa_latent_set_remove(self._h, seq, set_id))
+
+    # ------------------------------------------------------------------ a4-a6: attention
+    def decode(self, layer: int, seq_ids: Sequence[int], q: torch.Tensor,
+               out: Optional[torch.Tensor] = None, scale: float = 0.0, stream=None) -> torch.Tensor:
+        """q: bf16 [n][Hq][d] -> out bf16 [n][Hq][d] (hpa_decode)."""
+        ids = seq_ids if isinstance(seq_ids, np.ndarray) and seq_ids.dtype == np.int32 else _i32(seq_ids)
+        shape = (ids.size, self.Hq, self.d)
+        qp = self._dev_tensor(q, "q", shape)
+        if out is None:
+            out = torch.empty(shape, dtype=torch.bfloat16, device=q.device)
+        op = self._dev_tensor(out, "out", shape)
+        check(LIB.hpa_decode(self._h, layer, ids.size, _p32(ids), c_vp(qp), c_vp(op), float(scale),
+                             _stream(self.device, stream)))
+        return out
+
+    def prefill(self, layer: int, seq_ids: Sequence[int], q_lens: Sequence[int], q: torch.Tensor,
+                out: Optional[torch.Tensor] = None, scale: float = 0.0, stream=None) -> torch.Tensor:
+        """q: bf16 [sum(q_lens)][Hq][d] -> out (hpa_prefill); bottom-right causal."""
+        ids, ql = _i32(seq_ids), _i32(q_lens)
+        shape = (int(ql.sum()), self.Hq, self.d)
+        qp = self._dev_tensor(q, "q", shape)
+        if out is None:
+            out = torch.empty(shape, dtype=torch.bfloat16, device=q.device)
+        op = self._dev_tensor(out, "out", shape)
+        check(LIB.hpa_prefill(self._h, layer, ids.size, _p32(ids), _p32(ql), c_vp(qp), c_vp(op),
+                              float(scale), _stream(self.device, stream)))
+        return out
+
+    # ------------------------------------------------------------------ introspection
+    def seq_info(self, seq: int) -> Tuple[int, int, int]:
+        a, b, c = c_i32(), c_i32(), c_i32()
+        check(LIB.hpa_seq_info(self._h, seq, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value
+
+    def export_logical_kv(self, layer: int, seq: int, stream=None) -> Tuple[torch.Tensor, torch.Tensor]:
+        n, _, _ = self.seq_info(seq)
+        k = torch.empty((self.Hkv, n, self.d), dtype=torch.bfloat16, device=f"cuda:{self.device}")
+        v = torch.empty_like(k)
+        if n:
+            check(LIB.hpa_export_logical_kv(self._h, layer, seq, c_vp(k.data_ptr()), c_vp(v.data_ptr()),
+                                            _stream(self.device, stream)))
+        return k, v
+
+    def export_table(self, seq: int):
+        _, n, _ = self.seq_info(seq)
+        pages = np.zeros(n, np.int32)
+        pos0 = np.zeros(n, np.int32)
+        meta = np.zeros(n, np.uint16)
+        cnt = c_i32()
+        check(LIB.hpa_export_table(self._h, seq, _p32(pages), _p32(pos0),
+                                   meta.ctypes.data_as(ctypes.POINTER(ctypes.c_uint16)), n,
+                                   ctypes.byref(cnt)))
+        return pages, pos0, meta
+
+    def pools(self) -> Tuple[torch.Tensor, torch.Tensor]:
+        """Zero-copy views of the K and V pools, bf16 [L][NP][H_kv][P][d]."""
+        kp, vp, nb = c_vp(), c_vp(), ctypes.c_uint64()
+        check(LIB.hpa_cache_pools(self._h, ctypes.byref(kp), ctypes.byref(vp), ctypes.byref(nb)))
+        shape = (self.L, self.num_pages, self.Hkv, self.P, self.d)
+        dev = torch.device(f"cuda:{self.device}")
+        k = torch.as_tensor(_CAI(kp.value, shape), device=dev).view(torch.bfloat16)
+        v = torch.as_tensor(_CAI(vp.value, shape), device=dev).view(torch.bfloat16)
+        return k, v
+
+    def set_decode_splits(self, splits: int) -> None:
+        check(LIB.hpa_set_decode_splits(self._h, splits))
+
+    def launch_count(self) -> int:
+        n = ctypes.c_uint64()
+        check(LIB.hpa_launch_count(self._h, ctypes.byref(n)))
+        return n.value

@@ -1,0 +1,334 @@
+// decode.cu -- hybrid paged decode attention for sm_100a (SURVEY §8(a) a4 + a5).
+//
+// What it computes (§3 HPA; reading A1/A8):
+// for each request b and kv-head h, the G = Hq/H_kv query heads of its LAST
+// logical row attend every stored row of the block table (latent and token
+// pages alike -- the kernel is kind-agnostic):
+//   o[b][hq] = sum_j softmax_j(scale * q.K_log[h][j]) V_log[h][j],  h = hq / G.
+//
+// Design (B200-first, HBM-bound; roofline in DESIGN.md "Kernels"):
+//  * grid (split, kv-head, request); one CTA = 1 TMA producer warp + NCONS
+//    consumer warps. The producer walks the split's block-table entries and
+//    streams 16-row page chunks of K and V (2 x 4 KB at d=128) into an
+//    NST-deep shared-memory ring with 2-D TMA (128-B swizzle), completion on
+//    per-slot mbarriers. Chunk i goes to consumer warp i % NCONS.
+//  * each consumer runs mma.sync m16n8k16 (bf16 -> fp32) with the GQA group
+//    packed into the M dimension (rows 0..G-1 valid), an online softmax in the
+//    log2 domain (ex2.approx), and P rounded to bf16 for the PV product.
+//  * consumers merge their (m, l, O) through shared memory; with one split the
+//    CTA writes bf16 output directly, otherwise fp32 partials + LSE for the
+//    combine kernel (a5).
+//  * rows >= valid_rows of a partial page are masked to -inf; the pool is
+//    zero-initialised so those rows are always finite (0 * finite = 0).
+#include "hpa_kernels.h"
+#include "ptx.cuh"
+#include <cuda_bf16.h>
+#include <math_constants.h>
+
+namespace hpa {
+namespace {
+
+constexpr int kChunk = 16;  // rows per pipeline chunk (one m16n8k16 K-step of keys)
+constexpr int kNCons = 4;   // consumer warps per CTA
+constexpr int kNSt = 8;     // ring depth
+
+template <int D>
+struct DecodeSmem {
+  static constexpr int kHalves = D / 64;
+  static constexpr int kTileBytes = kChunk * D * 2;   // one 16-row K or V chunk
+  static constexpr int kStageBytes = 2 * kTileBytes;
+  static constexpr int kQBytes = 16 * D * 2;
+  static constexpr int kBytes = 1024 + kNSt * kStageBytes + kQBytes + 2 * kNSt * 8 + kNSt * 4;
+};
+
+template <int D>
+__global__ void __launch_bounds__((kNCons + 1) * 32, 3)
+decode_split_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                    const DecodeArgs a) {
+  using L = DecodeSmem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stages = smem;
+  uint8_t* qs = smem + kNSt * L::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(qs + L::kQBytes);
+  uint64_t* empty = full + kNSt;
+  volatile int32_t* cmeta = reinterpret_cast<int32_t*>(empty + kNSt);
+
+  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int seq = a.seq_rows[b];
+  const int G = a.G;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kNSt; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+  }
+  // q rows of this kv-head's group -> swizzled smem tile [16][D]; rows >= G are 0.
+  {
+    const __nv_bfloat16* qg = static_cast<const __nv_bfloat16*>(a.q) + (int64_t(b) * a.Hq + int64_t(h) * G) * D;
+    for (int i = threadIdx.x; i < 16 * (D / 8); i += blockDim.x) {
+      const int row = i / (D / 8), c = i % (D / 8);
+      int4 val = make_int4(0, 0, 0, 0);
+      if (row < G) val = *reinterpret_cast<const int4*>(qg + row * D + c * 8);
+      *reinterpret_cast<int4*>(qs + (c >> 3) * 2048 + sw128(row, c & 7)) = val;
+    }
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const int ne = a.t.n_entries[seq];
+      const int e0 = int(int64_t(split) * ne / a.splits);
+      const int e1 = int(int64_t(split + 1) * ne / a.splits);
+      const int32_t* bt = a.t.block_table + int64_t(seq) * a.t.max_pages;
+      const int32_t* mt = a.t.meta + int64_t(seq) * a.t.max_pages;
+      uint32_t i = 0;
+      for (int e = e0; e < e1; ++e) {
+        const int page = bt[e];
+        const int valid = mt[e] & kMetaRowsMask;
+        const int rowbase = ((a.layer * a.NP + page) * a.Hkv + h) * a.P;
+        for (int sub = 0; sub * kChunk < valid; ++sub, ++i) {
+          const int slot = i % kNSt;
+          if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
+          cmeta[slot] = min(kChunk, valid - sub * kChunk);
+          mbar_arrive_expect_tx(&full[slot], L::kStageBytes);
+          uint8_t* kd = stages + slot * L::kStageBytes;
+          uint8_t* vd = kd + L::kTileBytes;
+#pragma unroll
+          for (int hf = 0; hf < L::kHalves; ++hf) {
+            tma_load_2d(kd + hf * 2048, &tm_k, &full[slot], hf * 64, rowbase + sub * kChunk);
+            tma_load_2d(vd + hf * 2048, &tm_v, &full[slot], hf * 64, rowbase + sub * kChunk);
+          }
+        }
+      }
+      for (int c = 0; c < kNCons; ++c, ++i) {  // one end-of-work sentinel per consumer
+        const int slot = i % kNSt;
+        if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
+        cmeta[slot] = -1;
+        mbar_arrive(&full[slot]);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int cw = warp - 1;
+  uint32_t qa[D / 16][4];
+#pragma unroll
+  for (int ks = 0; ks < D / 16; ++ks) {
+    const int mi = lane >> 3;
+    const int row = (lane & 7) + (mi & 1) * 8;
+    const int kc = ks * 2 + (mi >> 1);
+    ldsm_x4(smem_u32(qs + (kc >> 3) * 2048 + sw128(row, kc & 7)), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
+  }
+  float o[D / 8][4];
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m_r[2] = {-CUDART_INF_F, -CUDART_INF_F};
+  float l_r[2] = {0.f, 0.f};
+  const float sl2 = a.scale_log2;
+
+  for (uint32_t i = cw;; i += kNCons) {
+    const int slot = i % kNSt;
+    mbar_wait(&full[slot], (i / kNSt) & 1);
+    const int nvalid = cmeta[slot];
+    if (nvalid < 0) break;
+    const uint8_t* kt = stages + slot * L::kStageBytes;
+    const uint8_t* vt = kt + L::kTileBytes;
+
+    // S = Q K^T : 16 x 16
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks) {
+      const int mi = lane >> 3;
+      const int n = (mi >> 1) * 8 + (lane & 7);
+      const int kc = ks * 2 + (mi & 1);
+      uint32_t b00, b01, b10, b11;
+      ldsm_x4(smem_u32(kt + (kc >> 3) * 2048 + sw128(n, kc & 7)), b00, b01, b10, b11);
+      mma_bf16_16816(s[0], qa[ks], b00, b01);
+      mma_bf16_16816(s[1], qa[ks], b10, b11);
+    }
+    // online softmax (log2 domain)
+    float x[2][4];
+    float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int col = j * 8 + 2 * (lane & 3) + (e & 1);
+        x[j][e] = col < nvalid ? s[j][e] * sl2 : -CUDART_INF_F;
+      }
+      mx0 = fmaxf(mx0, fmaxf(x[j][0], x[j][1]));
+      mx1 = fmaxf(mx1, fmaxf(x[j][2], x[j][3]));
+    }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float mn0 = fmaxf(m_r[0], mx0), mn1 = fmaxf(m_r[1], mx1);
+    const float al0 = fast_exp2(m_r[0] - mn0), al1 = fast_exp2(m_r[1] - mn1);
+    m_r[0] = mn0;
+    m_r[1] = mn1;
+    float p[2][4];
+    float ps0 = 0.f, ps1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      p[j][0] = fast_exp2(x[j][0] - mn0);
+      p[j][1] = fast_exp2(x[j][1] - mn0);
+      p[j][2] = fast_exp2(x[j][2] - mn1);
+      p[j][3] = fast_exp2(x[j][3] - mn1);
+      ps0 += p[j][0] + p[j][1];
+      ps1 += p[j][2] + p[j][3];
+    }
+    l_r[0] = l_r[0] * al0 + ps0;
+    l_r[1] = l_r[1] * al1 + ps1;
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n) {
+      o[n][0] *= al0;
+      o[n][1] *= al0;
+      o[n][2] *= al1;
+      o[n][3] *= al1;
+    }
+    uint32_t pa[4];
+    pa[0] = pack_bf16(p[0][0], p[0][1]);
+    pa[1] = pack_bf16(p[0][2], p[0][3]);
+    pa[2] = pack_bf16(p[1][0], p[1][1]);
+    pa[3] = pack_bf16(p[1][2], p[1][3]);
+    // O += P V : 16 x D
+#pragma unroll
+    for (int dp = 0; dp < D / 16; ++dp) {
+      const int mi = lane >> 3;
+      const int key = (mi & 1) * 8 + (lane & 7);
+      const int dc = dp * 2 + (mi >> 1);
+      uint32_t v0, v1, v2, v3;
+      ldsm_x4_t(smem_u32(vt + (dc >> 3) * 2048 + sw128(key, dc & 7)), v0, v1, v2, v3);
+      mma_bf16_16816(o[2 * dp], pa, v0, v1);
+      mma_bf16_16816(o[2 * dp + 1], pa, v2, v3);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+  }
+  l_r[0] += __shfl_xor_sync(0xffffffffu, l_r[0], 1);
+  l_r[0] += __shfl_xor_sync(0xffffffffu, l_r[0], 2);
+  l_r[1] += __shfl_xor_sync(0xffffffffu, l_r[1], 1);
+  l_r[1] += __shfl_xor_sync(0xffffffffu, l_r[1], 2);
+
+  // ---------------------------------------------- merge the consumers' states
+  constexpr int kNT = kNCons * 32;
+  named_bar_sync(1, kNT);  // every consumer is done with the ring
+  float* mo = reinterpret_cast<float*>(stages);        // [NCONS][G][D]
+  float* mm = mo + kNCons * G * D;                       // [NCONS][G]
+  float* ml = mm + kNCons * G;                           // [NCONS][G]
+  {
+    const int g0 = lane >> 2, g1 = g0 + 8;
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n) {
+      const int dcol = n * 8 + 2 * (lane & 3);
+      if (g0 < G) {
+        mo[(cw * G + g0) * D + dcol] = o[n][0];
+        mo[(cw * G + g0) * D + dcol + 1] = o[n][1];
+      }
+      if (g1 < G) {
+        mo[(cw * G + g1) * D + dcol] = o[n][2];
+        mo[(cw * G + g1) * D + dcol + 1] = o[n][3];
+      }
+    }
+    if ((lane & 3) == 0) {
+      if (g0 < G) { mm[cw * G + g0] = m_r[0]; ml[cw * G + g0] = l_r[0]; }
+      if (g1 < G) { mm[cw * G + g1] = m_r[1]; ml[cw * G + g1] = l_r[1]; }
+    }
+  }
+  named_bar_sync(1, kNT);
+  const int tid = threadIdx.x - 32;
+  for (int idx = tid; idx < G * D; idx += kNT) {
+    const int g = idx / D, dcol = idx % D;
+    float M = -CUDART_INF_F;
+#pragma unroll
+    for (int c = 0; c < kNCons; ++c) M = fmaxf(M, mm[c * G + g]);
+    float Ls = 0.f, Os = 0.f;
+    if (M != -CUDART_INF_F) {
+#pragma unroll
+      for (int c = 0; c < kNCons; ++c) {
+        const float w = fast_exp2(mm[c * G + g] - M);
+        Ls += w * ml[c * G + g];
+        Os += w * mo[(c * G + g) * D + dcol];
+      }
+    }
+    const int hq = h * G + g;
+    if (a.splits == 1) {
+      static_cast<__nv_bfloat16*>(a.out)[(int64_t(b) * a.Hq + hq) * D + dcol] = __float2bfloat16_rn(Os / Ls);
+    } else {
+      const int64_t pi = (int64_t(b) * a.Hq + hq) * a.splits + split;
+      a.o_part[pi * D + dcol] = Ls > 0.f ? Os / Ls : 0.f;
+      if (dcol == 0) a.lse_part[pi] = Ls > 0.f ? M + __log2f(Ls) : -CUDART_INF_F;
+    }
+  }
+}
+
+// a5: O = sum_s 2^(lse_s - LSE) O_s, LSE = log2 sum_s 2^lse_s  (fp32).
+template <int D>
+__global__ void __launch_bounds__(D) combine_kernel(const float* __restrict__ o_part,
+                                                    const float* __restrict__ lse, __nv_bfloat16* out,
+                                                    int S) {
+  const int64_t bh = blockIdx.x;
+  const float* ls = lse + bh * S;
+  float M = -CUDART_INF_F;
+  for (int s = 0; s < S; ++s) M = fmaxf(M, ls[s]);
+  float W = 0.f, acc = 0.f;
+  for (int s = 0; s < S; ++s) {
+    const float w = ls[s] == -CUDART_INF_F ? 0.f : fast_exp2(ls[s] - M);
+    W += w;
+    acc += w * o_part[(bh * S + s) * D + threadIdx.x];
+  }
+  out[bh * D + threadIdx.x] = __float2bfloat16_rn(acc / W);
+}
+
+template <int D>
+cudaError_t launch_decode_d(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,
+                            cudaStream_t s, int* launches) {
+  const int smem = DecodeSmem<D>::kBytes;
+  dim3 grid(a.splits, a.Hkv, a.n_seqs);
+  decode_split_kernel<D><<<grid, (kNCons + 1) * 32, smem, s>>>(tm_k, tm_v, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  ++*launches;
+  if (a.splits > 1) {
+    combine_kernel<D><<<a.n_seqs * a.Hq, D, 0, s>>>(a.o_part, a.lse_part,
+                                                    static_cast<__nv_bfloat16*>(a.out), a.splits);
+    e = cudaGetLastError();
+    ++*launches;
+  }
+  return e;
+}
+
+}  // namespace
+
+cudaError_t decode_init_attributes() {
+  cudaError_t e = cudaFuncSetAttribute(decode_split_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       DecodeSmem<128>::kBytes);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(decode_split_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              DecodeSmem<64>::kBytes);
+}
+
+int decode_ctas_per_sm(int32_t D, int32_t /*G*/) {
+  const int smem = (D == 64 ? DecodeSmem<64>::kBytes : DecodeSmem<128>::kBytes) + 1024;
+  int by_smem = (228 * 1024) / smem;
+  return by_smem < 3 ? by_smem : 3;
+}
+
+cudaError_t launch_decode(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,
+                          int32_t D, cudaStream_t s, int* launches) {
+  if (a.n_seqs == 0) return cudaSuccess;
+  if (D == 128) return launch_decode_d<128>(tm_k, tm_v, a, s, launches);
+  if (D == 64) return launch_decode_d<64>(tm_k, tm_v, a, s, launches);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hpa

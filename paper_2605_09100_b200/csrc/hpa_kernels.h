@@ -1,0 +1,95 @@
+// hpa_kernels.h -- internal interface between the host runtime (runtime.cpp)
+// and the CUDA kernels. Not part of the public ABI (see include/hpa.h).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace hpa {
+
+// Device block-table entry meta word: bits 0..15 valid_rows, bit 30 latent.
+constexpr int32_t kMetaLatent = 1 << 30;
+constexpr int32_t kMetaRowsMask = 0xffff;
+
+// Device metadata arena (one int32 allocation), sliced as:
+//   block_table [max_seqs][max_pages]  physical page id per entry
+//   pos0        [max_seqs][max_pages]  logical index of the entry's row 0
+//   meta        [max_seqs][max_pages]  valid_rows | latent bit
+//   seq_len     [max_seqs]
+//   n_entries   [max_seqs]
+struct DevTables {
+  int32_t* block_table;
+  int32_t* pos0;
+  int32_t* meta;
+  int32_t* seq_len;
+  int32_t* n_entries;
+  int32_t max_pages;
+};
+
+// One (index, value) write into the metadata arena.
+struct WordWrite {
+  int32_t idx;
+  int32_t val;
+};
+
+// One scatter record: n_rows rows of K and V, copied for every layer into the
+// pool slots slots[slot_off .. slot_off + n_rows) (slot = page * P + row).
+struct ScatterRecord {
+  const void* k;      // bf16, element (l, r, h, x) at k + l*stride_l + r*stride_r + h*d + x
+  const void* v;
+  int64_t stride_l;   // elements
+  int64_t stride_r;   // elements
+  int32_t n_rows;
+  int32_t slot_off;
+};
+
+struct PoolGeom {
+  void* k_pool;  // bf16 [L][NP][H_kv][P][d]
+  void* v_pool;
+  int32_t L, NP, Hkv, P, D;
+};
+
+// Metadata writes + row scatter in one launch (append / install / apply).
+cudaError_t launch_scatter(const PoolGeom& g, int32_t* arena, const WordWrite* words,
+                           int32_t n_words, const ScatterRecord* recs, int32_t n_recs,
+                           const int32_t* slots, int64_t max_rows_per_rec, cudaStream_t s);
+
+// Logical K/V export of one (layer, seq): out bf16 [H_kv][len][d].
+cudaError_t launch_export(const PoolGeom& g, DevTables t, int32_t layer, int32_t seq,
+                          int32_t n_entries_host, void* k_out, void* v_out, cudaStream_t s);
+
+struct DecodeArgs {
+  DevTables t;
+  const int32_t* seq_rows;  // [n_seqs] device
+  const void* q;            // bf16 [n][Hq][d]
+  void* out;                // bf16 [n][Hq][d]
+  float* o_part;            // fp32 [n][Hq][S][d]   (S > 1)
+  float* lse_part;          // fp32 [n][Hq][S]      (log2 domain)
+  int32_t n_seqs, Hq, Hkv, G, P, NP, layer, splits;
+  float scale_log2;         // softmax_scale * log2(e)
+};
+// tm_k / tm_v: 2-D tensor maps over the pools viewed as [L*NP*H_kv*P][d],
+// box {64, 16}, 128-B swizzle.
+cudaError_t launch_decode(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,
+                          int32_t D, cudaStream_t s, int* launches);
+int decode_ctas_per_sm(int32_t D, int32_t G);
+// Per-device one-time setup (dynamic smem opt-in); call with the device current.
+cudaError_t decode_init_attributes();
+cudaError_t prefill_init_attributes();
+
+struct PrefillArgs {
+  DevTables t;
+  const int32_t* seq_rows;  // [n] device
+  const int32_t* q_len;     // [n] device
+  const int32_t* q_off;     // [n] device: first row of sequence i in q / out
+  void* out;                // bf16 [sum q][Hq][d]
+  int32_t n_seqs, Hq, Hkv, G, P, NP, layer, max_q_len;
+  float scale_log2;
+};
+// tm_q: 3-D map over q [sum q][Hq][d] with box {64, 1, 128};
+// tm_k / tm_v: 2-D maps over the pools with box {64, min(P,128)}.
+cudaError_t launch_prefill(const CUtensorMap& tm_q, const CUtensorMap& tm_k,
+                           const CUtensorMap& tm_v, const PrefillArgs& a, int32_t D,
+                           cudaStream_t s, int* launches);
+
+}  // namespace hpa

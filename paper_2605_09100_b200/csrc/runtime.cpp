@@ -1,0 +1,965 @@
+// runtime.cpp -- host runtime of the HPA library and the C ABI (include/hpa.h).
+//
+// Host side of SURVEY §8(a) a1 (page pool + hybrid block table):
+//  * PageAllocator: free-list stack + refcounts over NP physical pages shared by
+//    all layers ("pre-allocating KV cache ... fixed-size non-continuous blocks",
+//    PAPER.md P:L250). Optional seeded shuffle of the free list so physical
+//    placement is a random permutation.
+//  * Seq: ordered segment list {TOKEN | LATENT(set_id)}; each segment starts on
+//    a fresh page and only its last page may be partial (reading A7).
+//    Host mirror of the table row: page id, pos0 (= prefix sum of valid rows,
+//    the logical index of the entry's row 0) and meta (valid_rows | latent).
+//  * Every mutation is checked first and applied only if it can complete
+//    (failure atomicity; HPA_ERR_OUT_OF_PAGES = S:L388 backpressure).
+//  * Device table updates are queued as (index, value) word writes and shipped
+//    through a pinned staging ring with ONE H2D copy per call; the scatter
+//    kernel applies them in the same launch that copies the K/V rows.
+#include "../../include/hpa.h"
+#include "hpa_kernels.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <string>
+#include <vector>
+
+using namespace hpa;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+hpa_status_t fail(hpa_status_t s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+hpa_status_t cuda_fail(cudaError_t e, const char* what) {
+  return fail(HPA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define HPA_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda,
+// so the library also loads on hosts without a driver).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 map over `rows` x `cols` (row-major), box {64, box_rows}, 128-B swizzle.
+bool make_map_2d(CUtensorMap* m, void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 3-D bf16 map over q [tokens][Hq][d]: box {64, 1, box_tok}, 128-B swizzle.
+bool make_map_q(CUtensorMap* m, const void* base, uint64_t tokens, uint64_t heads, uint64_t d,
+                uint32_t box_tok) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {d, heads, tokens};
+  cuuint64_t strides[2] = {d * 2, heads * d * 2};
+  cuuint32_t box[3] = {64, 1, box_tok};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+uint64_t splitmix64(uint64_t& x) {
+  uint64_t z = (x += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// ------------------------------------------------------------------ allocator
+class PageAllocator {
+ public:
+  void init(int32_t num_pages, uint64_t seed) {
+    refcnt_.assign(num_pages, 0);
+    free_.resize(num_pages);
+    for (int32_t i = 0; i < num_pages; ++i) free_[i] = num_pages - 1 - i;  // pop_back -> page 0 first
+    if (seed != 0) {
+      uint64_t st = seed;
+      for (int32_t i = num_pages - 1; i > 0; --i) {
+        int32_t j = int32_t(splitmix64(st) % uint64_t(i + 1));
+        std::swap(free_[i], free_[j]);
+      }
+    }
+  }
+  int32_t num_free() const { return int32_t(free_.size()); }
+  int32_t num_pages() const { return int32_t(refcnt_.size()); }
+  // caller checked num_free() >= n
+  void alloc(int32_t n, std::vector<int32_t>& out) {
+    for (int32_t i = 0; i < n; ++i) {
+      int32_t p = free_.back();
+      free_.pop_back();
+      refcnt_[p] = 1;
+      out.push_back(p);
+    }
+  }
+  void release(int32_t p) {
+    if (--refcnt_[p] == 0) free_.push_back(p);
+  }
+  int32_t refcount(int32_t p) const { return refcnt_[p]; }
+
+ private:
+  std::vector<int32_t> free_;
+  std::vector<int32_t> refcnt_;
+};
+
+struct Segment {
+  bool latent;
+  int32_t set_id;  // -1 for token segments
+  int32_t rows;
+  std::vector<int32_t> pages;
+};
+
+struct Seq {
+  bool live = false;
+  int32_t next_set = 0;
+  std::vector<Segment> segs;
+  // host mirror of the table row (rebuilt from segs)
+  std::vector<int32_t> pages, pos0, meta;
+  int32_t len = 0;
+  int32_t chunks = 0;  // number of 16-row decode chunks
+};
+
+// Pinned host staging ring mirrored by a device ring of the same size: an
+// upload copies [off, off+n) host -> device; the region is reused only after
+// the event recorded behind the consuming kernel has completed.
+class StagingRing {
+ public:
+  cudaError_t init(size_t cap) {
+    cap_ = cap;
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&host_), cap, cudaHostAllocDefault);
+    if (e != cudaSuccess) return e;
+    return cudaMalloc(reinterpret_cast<void**>(&dev_), cap);
+  }
+  void destroy() {
+    for (auto& f : inflight_) cudaEventDestroy(f.ev);
+    for (auto ev : pool_) cudaEventDestroy(ev);
+    inflight_.clear();
+    pool_.clear();
+    if (host_) cudaFreeHost(host_);
+    if (dev_) cudaFree(dev_);
+    host_ = dev_ = nullptr;
+  }
+  size_t cap() const { return cap_; }
+  // Returns the offset of a free region of n bytes (n <= cap).
+  size_t reserve(size_t n) {
+    n = (n + 255) & ~size_t(255);
+    if (head_ + n > cap_) head_ = 0;
+    const size_t lo = head_, hi = head_ + n;
+    while (!inflight_.empty() && cudaEventQuery(inflight_.front().ev) == cudaSuccess) pop_front();
+    for (auto it = inflight_.begin(); it != inflight_.end();) {
+      if (it->lo < hi && lo < it->hi) {
+        cudaEventSynchronize(it->ev);
+        pool_.push_back(it->ev);
+        it = inflight_.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    head_ = hi;
+    return lo;
+  }
+  char* host(size_t off) { return host_ + off; }
+  char* dev(size_t off) { return dev_ + off; }
+  cudaError_t upload(size_t off, size_t n, cudaStream_t s) {
+    return cudaMemcpyAsync(dev_ + off, host_ + off, n, cudaMemcpyHostToDevice, s);
+  }
+  cudaError_t commit(size_t off, size_t n, cudaStream_t s) {
+    cudaEvent_t ev;
+    if (!pool_.empty()) {
+      ev = pool_.back();
+      pool_.pop_back();
+    } else {
+      cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaEventRecord(ev, s);
+    inflight_.push_back({off, off + ((n + 255) & ~size_t(255)), ev});
+    return e;
+  }
+
+ private:
+  struct Flight {
+    size_t lo, hi;
+    cudaEvent_t ev;
+  };
+  void pop_front() {
+    pool_.push_back(inflight_.front().ev);
+    inflight_.pop_front();
+  }
+  char* host_ = nullptr;
+  char* dev_ = nullptr;
+  size_t cap_ = 0, head_ = 0;
+  std::deque<Flight> inflight_;
+  std::vector<cudaEvent_t> pool_;
+};
+
+// Serialises heterogeneous arrays into one staging upload.
+struct Blob {
+  std::vector<char> bytes;
+  template <class T>
+  size_t add(const T* p, size_t n) {
+    size_t off = (bytes.size() + 15) & ~size_t(15);
+    bytes.resize(off + n * sizeof(T));
+    if (n) std::memcpy(bytes.data() + off, p, n * sizeof(T));
+    return off;
+  }
+};
+
+}  // namespace
+
+struct hpa_cache {
+  hpa_config_t cfg{};
+  PageAllocator alloc;
+  std::vector<Seq> seqs;
+  int32_t live = 0;
+  // device
+  void* k_pool = nullptr;
+  void* v_pool = nullptr;
+  uint64_t pool_bytes = 0;
+  int32_t* arena = nullptr;
+  DevTables dt{};
+  CUtensorMap tm_k_dec{}, tm_v_dec{}, tm_k_pre{}, tm_v_pre{};
+  StagingRing ring;
+  std::vector<WordWrite> pending;  // device table writes not yet shipped
+  // decode batch cache
+  std::vector<int32_t> batch_host;
+  int32_t* batch_dev = nullptr;
+  int32_t batch_cap = 0;
+  // decode partials
+  float* o_part = nullptr;
+  float* lse_part = nullptr;
+  size_t part_elems = 0;
+  int32_t forced_splits = 0;
+  int num_sms = 148;
+  uint64_t launches = 0;
+
+  int64_t idx(int32_t seq, int32_t e) const { return int64_t(seq) * cfg.max_pages_per_seq + e; }
+  int64_t off_pos0() const { return int64_t(cfg.max_seqs) * cfg.max_pages_per_seq; }
+  int64_t off_meta() const { return 2 * off_pos0(); }
+  int64_t off_len() const { return 3 * off_pos0(); }
+  int64_t off_nent() const { return off_len() + cfg.max_seqs; }
+
+  PoolGeom geom() const {
+    return PoolGeom{k_pool, v_pool, cfg.num_layers, cfg.num_pages, cfg.num_kv_heads, cfg.page_size,
+                    cfg.head_dim};
+  }
+
+  // Rebuilds the host mirror of seq `s` from its segments and queues device
+  // writes for entries [from_entry, n) plus seq_len / n_entries.
+  void rebuild(int32_t s, int32_t from_entry) {
+    Seq& q = seqs[s];
+    const int32_t P = cfg.page_size;
+    std::vector<int32_t> pages, pos0, meta;
+    int32_t pos = 0, chunks = 0;
+    for (const Segment& g : q.segs) {
+      int32_t left = g.rows;
+      for (int32_t pg : g.pages) {
+        int32_t take = std::min(P, left);
+        pages.push_back(pg);
+        pos0.push_back(pos);
+        meta.push_back(take | (g.latent ? kMetaLatent : 0));
+        chunks += (take + 15) / 16;
+        pos += take;
+        left -= take;
+      }
+    }
+    const int32_t n = int32_t(pages.size());
+    from_entry = std::max(0, std::min(from_entry, n));
+    // first entry that differs from the previous mirror (cheap diff)
+    int32_t first = from_entry;
+    while (first < n && first < int32_t(q.pages.size()) && q.pages[first] == pages[first] &&
+           q.pos0[first] == pos0[first] && q.meta[first] == meta[first])
+      ++first;
+    for (int32_t e = first; e < n; ++e) {
+      pending.push_back({int32_t(idx(s, e)), pages[e]});
+      pending.push_back({int32_t(off_pos0() + idx(s, e)), pos0[e]});
+      pending.push_back({int32_t(off_meta() + idx(s, e)), meta[e]});
+    }
+    if (q.len != pos || int32_t(q.pages.size()) != n) {
+      pending.push_back({int32_t(off_len() + s), pos});
+      pending.push_back({int32_t(off_nent() + s), n});
+    }
+    q.pages.swap(pages);
+    q.pos0.swap(pos0);
+    q.meta.swap(meta);
+    q.len = pos;
+    q.chunks = chunks;
+  }
+};
+
+namespace {
+
+hpa_status_t check_seq(hpa_cache_t* c, int32_t s) {
+  if (s < 0 || s >= c->cfg.max_seqs || !c->seqs[s].live)
+    return fail(HPA_ERR_UNKNOWN_SEQ, "unknown sequence %d", s);
+  return HPA_OK;
+}
+
+int32_t seq_entries(const Seq& q) { return int32_t(q.pages.size()); }
+
+// Ships pending word writes (+ optional scatter records/slots) in one upload and
+// one scatter launch on `s`.
+hpa_status_t ship(hpa_cache_t* c, cudaStream_t s, const std::vector<ScatterRecord>& recs,
+                  const std::vector<int32_t>& slots, int64_t max_rows) {
+  if (c->pending.empty() && recs.empty()) return HPA_OK;
+  // The scatter kernel applies words in parallel, so each index may appear at
+  // most once: keep the LAST queued write per index (program order).
+  if (c->pending.size() > 1) {
+    std::stable_sort(c->pending.begin(), c->pending.end(),
+                     [](const WordWrite& x, const WordWrite& y) { return x.idx < y.idx; });
+    size_t w = 0;
+    for (size_t r = 0; r < c->pending.size(); ++r) {
+      if (w > 0 && c->pending[w - 1].idx == c->pending[r].idx) c->pending[w - 1] = c->pending[r];
+      else c->pending[w++] = c->pending[r];
+    }
+    c->pending.resize(w);
+  }
+  Blob b;
+  const size_t o_words = b.add(c->pending.data(), c->pending.size());
+  const size_t o_recs = b.add(recs.data(), recs.size());
+  const size_t o_slots = b.add(slots.data(), slots.size());
+  if (b.bytes.size() > c->ring.cap())
+    return fail(HPA_ERR_INVALID_ARG, "metadata upload of %zu bytes exceeds staging capacity %zu",
+                b.bytes.size(), c->ring.cap());
+  const size_t off = c->ring.reserve(b.bytes.size());
+  std::memcpy(c->ring.host(off), b.bytes.data(), b.bytes.size());
+  HPA_CUDA(c->ring.upload(off, b.bytes.size(), s));
+  char* d = c->ring.dev(off);
+  HPA_CUDA(launch_scatter(c->geom(), c->arena, reinterpret_cast<const WordWrite*>(d + o_words),
+                          int32_t(c->pending.size()), reinterpret_cast<const ScatterRecord*>(d + o_recs),
+                          int32_t(recs.size()), reinterpret_cast<const int32_t*>(d + o_slots), max_rows, s));
+  c->launches += 1;
+  HPA_CUDA(c->ring.commit(off, b.bytes.size(), s));
+  c->pending.clear();
+  return HPA_OK;
+}
+
+// Device copy of the batch's seq rows (re-uploaded only when the list changes).
+hpa_status_t upload_batch(hpa_cache_t* c, int32_t n, const int32_t* seq_ids, cudaStream_t s) {
+  if (int32_t(c->batch_host.size()) == n && std::equal(seq_ids, seq_ids + n, c->batch_host.begin()))
+    return HPA_OK;
+  if (n > c->batch_cap) {
+    if (c->batch_dev) cudaFree(c->batch_dev);
+    c->batch_cap = std::max(n, 1024);
+    HPA_CUDA(cudaMalloc(&c->batch_dev, size_t(c->batch_cap) * 4));
+  }
+  const size_t off = c->ring.reserve(size_t(n) * 4);
+  std::memcpy(c->ring.host(off), seq_ids, size_t(n) * 4);
+  HPA_CUDA(cudaMemcpyAsync(c->batch_dev, c->ring.host(off), size_t(n) * 4, cudaMemcpyHostToDevice, s));
+  HPA_CUDA(c->ring.commit(off, size_t(n) * 4, s));
+  c->batch_host.assign(seq_ids, seq_ids + n);
+  return HPA_OK;
+}
+
+// Split planner: splits depend only on the batch's table sizes (never on
+// physical placement). Minimises the wave-quantised time of equal-length
+// units plus a small per-split cost.
+int32_t plan_splits(hpa_cache_t* c, int32_t n, int32_t max_entries, int32_t max_chunks) {
+  if (c->forced_splits > 0) return std::max(1, std::min(c->forced_splits, std::max(1, max_entries)));
+  const int64_t units = int64_t(n) * c->cfg.num_kv_heads;
+  const int64_t slots = int64_t(c->num_sms) * decode_ctas_per_sm(c->cfg.head_dim, 1);
+  int32_t best = 1;
+  double best_cost = 1e30;
+  const int32_t smax = std::max(1, std::min<int32_t>(64, std::max(1, max_entries)));
+  for (int32_t S = 1; S <= smax; ++S) {
+    if (max_chunks / S < 8 && S > 1) break;  // keep >= 8 chunks (128 rows) per split
+    const int64_t ctas = units * S;
+    const double waves = std::ceil(double(ctas) / double(slots));
+    const double cost = waves * (double(max_chunks) / S + 6.0) + (S > 1 ? 2.0 : 0.0);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = S;
+    }
+  }
+  return best;
+}
+
+// Pages needed to append n rows to seq q.
+int32_t pages_for_append(const hpa_cache_t* c, const Seq& q, int32_t n) {
+  if (n <= 0) return 0;
+  const int32_t P = c->cfg.page_size;
+  if (!q.segs.empty() && !q.segs.back().latent) {
+    const Segment& g = q.segs.back();
+    const int32_t room = int32_t(g.pages.size()) * P - g.rows;
+    return n <= room ? 0 : (n - room + P - 1) / P;
+  }
+  return (n + P - 1) / P;
+}
+
+bool valid_dims(const hpa_config_t* g) {
+  auto p2 = [](int x) { return x == 16 || x == 32 || x == 64 || x == 128 || x == 256; };
+  return (g->head_dim == 64 || g->head_dim == 128) && p2(g->page_size);
+}
+
+}  // namespace
+
+// ========================================================================= C ABI
+extern "C" {
+
+const char* hpa_last_error(void) { return g_last_error.c_str(); }
+
+const char* hpa_status_string(hpa_status_t s) {
+  switch (s) {
+    case HPA_OK: return "HPA_OK";
+    case HPA_ERR_INVALID_ARG: return "HPA_ERR_INVALID_ARG";
+    case HPA_ERR_OUT_OF_PAGES: return "HPA_ERR_OUT_OF_PAGES";
+    case HPA_ERR_SEQ_CAPACITY: return "HPA_ERR_SEQ_CAPACITY";
+    case HPA_ERR_UNKNOWN_SEQ: return "HPA_ERR_UNKNOWN_SEQ";
+    case HPA_ERR_UNKNOWN_SET: return "HPA_ERR_UNKNOWN_SET";
+    case HPA_ERR_CUDA: return "HPA_ERR_CUDA";
+    case HPA_ERR_UNSUPPORTED: return "HPA_ERR_UNSUPPORTED";
+  }
+  return "HPA_ERR_?";
+}
+
+uint64_t hpa_kv_bytes(int64_t num_layers, int64_t num_kv_heads, int64_t head_dim, int64_t seq_len,
+                      int64_t elem_bytes) {
+  return 2ull * uint64_t(num_layers) * uint64_t(num_kv_heads) * uint64_t(head_dim) * uint64_t(seq_len) *
+         uint64_t(elem_bytes);
+}
+
+hpa_status_t hpa_cache_create(const hpa_config_t* cfg, hpa_cache_t** out) {
+  if (!cfg || !out) return fail(HPA_ERR_INVALID_ARG, "null argument");
+  *out = nullptr;
+  const hpa_config_t& g = *cfg;
+  if (g.num_layers <= 0 || g.num_q_heads <= 0 || g.num_kv_heads <= 0 || g.num_pages <= 0 ||
+      g.max_seqs <= 0 || g.max_pages_per_seq <= 0)
+    return fail(HPA_ERR_INVALID_ARG, "all config counts must be positive");
+  if (g.num_q_heads % g.num_kv_heads != 0)
+    return fail(HPA_ERR_INVALID_ARG, "num_q_heads %% num_kv_heads != 0 (S:L25)");
+  if (!valid_dims(cfg))
+    return fail(HPA_ERR_UNSUPPORTED, "head_dim must be 64/128 and page_size 16..256 (power of 2)");
+  if (g.num_q_heads / g.num_kv_heads > 16) return fail(HPA_ERR_UNSUPPORTED, "GQA group > 16");
+  const int64_t rows = int64_t(g.num_layers) * g.num_pages * g.num_kv_heads * g.page_size;
+  if (rows >= (int64_t(1) << 31)) return fail(HPA_ERR_UNSUPPORTED, "pool too large for 32-bit TMA row index");
+  if (int64_t(g.max_seqs) * g.max_pages_per_seq * 3 + 2 * g.max_seqs >= (int64_t(1) << 31))
+    return fail(HPA_ERR_UNSUPPORTED, "table too large");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || g.device < 0 || g.device >= ndev)
+    return fail(HPA_ERR_INVALID_ARG, "CUDA device %d not available", g.device);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, g.device) != cudaSuccess)
+    return fail(HPA_ERR_CUDA, "cudaGetDeviceProperties failed");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(HPA_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a", g.device,
+                prop.major, prop.minor);
+  DeviceGuard dg(g.device);
+  std::unique_ptr<hpa_cache> c(new hpa_cache());
+  c->cfg = g;
+  c->num_sms = prop.multiProcessorCount;
+  c->alloc.init(g.num_pages, g.placement_seed);
+  c->seqs.resize(g.max_seqs);
+  c->pool_bytes = uint64_t(rows) * g.head_dim * 2;
+  auto cleanup = [&]() {
+    if (c->k_pool) cudaFree(c->k_pool);
+    if (c->v_pool) cudaFree(c->v_pool);
+    if (c->arena) cudaFree(c->arena);
+    c->ring.destroy();
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&c->k_pool, c->pool_bytes)) != cudaSuccess ||
+      (e = cudaMalloc(&c->v_pool, c->pool_bytes)) != cudaSuccess ||
+      (e = cudaMemset(c->k_pool, 0, c->pool_bytes)) != cudaSuccess ||
+      (e = cudaMemset(c->v_pool, 0, c->pool_bytes)) != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "pool allocation");
+  }
+  const int64_t arena_words = c->off_nent() + g.max_seqs;
+  if ((e = cudaMalloc(&c->arena, size_t(arena_words) * 4)) != cudaSuccess ||
+      (e = cudaMemset(c->arena, 0, size_t(arena_words) * 4)) != cudaSuccess ||
+      (e = c->ring.init(size_t(64) << 20)) != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "table allocation");
+  }
+  c->dt = DevTables{c->arena, c->arena + c->off_pos0(), c->arena + c->off_meta(), c->arena + c->off_len(),
+                    c->arena + c->off_nent(), g.max_pages_per_seq};
+  if (!make_map_2d(&c->tm_k_dec, c->k_pool, uint64_t(rows), uint64_t(g.head_dim), 16) ||
+      !make_map_2d(&c->tm_v_dec, c->v_pool, uint64_t(rows), uint64_t(g.head_dim), 16) ||
+      !make_map_2d(&c->tm_k_pre, c->k_pool, uint64_t(rows), uint64_t(g.head_dim), uint32_t(std::min(g.page_size, 128))) ||
+      !make_map_2d(&c->tm_v_pre, c->v_pool, uint64_t(rows), uint64_t(g.head_dim), uint32_t(std::min(g.page_size, 128)))) {
+    cleanup();
+    return fail(HPA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the KV pools");
+  }
+  if ((e = decode_init_attributes()) != cudaSuccess || (e = prefill_init_attributes()) != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "kernel attribute setup");
+  }
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "cache init");
+  }
+  *out = c.release();
+  return HPA_OK;
+}
+
+hpa_status_t hpa_cache_destroy(hpa_cache_t* c) {
+  if (!c) return HPA_OK;
+  DeviceGuard dg(c->cfg.device);
+  cudaDeviceSynchronize();
+  cudaFree(c->k_pool);
+  cudaFree(c->v_pool);
+  cudaFree(c->arena);
+  if (c->batch_dev) cudaFree(c->batch_dev);
+  if (c->o_part) cudaFree(c->o_part);
+  if (c->lse_part) cudaFree(c->lse_part);
+  c->ring.destroy();
+  delete c;
+  return HPA_OK;
+}
+
+hpa_status_t hpa_cache_pools(hpa_cache_t* c, void** k_pool, void** v_pool, uint64_t* pool_bytes) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (k_pool) *k_pool = c->k_pool;
+  if (v_pool) *v_pool = c->v_pool;
+  if (pool_bytes) *pool_bytes = c->pool_bytes;
+  return HPA_OK;
+}
+
+hpa_status_t hpa_cache_stats(hpa_cache_t* c, int32_t* free_pages, int32_t* used_pages, int32_t* live_seqs) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  int32_t used = 0;
+  for (int32_t p = 0; p < c->alloc.num_pages(); ++p) used += c->alloc.refcount(p) > 0;
+  if (free_pages) *free_pages = c->alloc.num_free();
+  if (used_pages) *used_pages = used;
+  if (live_seqs) *live_seqs = c->live;
+  return HPA_OK;
+}
+
+hpa_status_t hpa_seq_create(hpa_cache_t* c, int32_t* seq_id) {
+  if (!c || !seq_id) return fail(HPA_ERR_INVALID_ARG, "null argument");
+  for (int32_t s = 0; s < c->cfg.max_seqs; ++s) {
+    if (!c->seqs[s].live) {
+      c->seqs[s] = Seq();
+      c->seqs[s].live = true;
+      c->pending.push_back({int32_t(c->off_len() + s), 0});
+      c->pending.push_back({int32_t(c->off_nent() + s), 0});
+      ++c->live;
+      *seq_id = s;
+      return HPA_OK;
+    }
+  }
+  return fail(HPA_ERR_SEQ_CAPACITY, "all %d sequence slots are in use", c->cfg.max_seqs);
+}
+
+hpa_status_t hpa_seq_release(hpa_cache_t* c, int32_t seq_id) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (hpa_status_t st = check_seq(c, seq_id)) return st;
+  Seq& q = c->seqs[seq_id];
+  for (const Segment& g : q.segs)
+    for (int32_t p : g.pages) c->alloc.release(p);
+  q = Seq();
+  c->pending.push_back({int32_t(c->off_len() + seq_id), 0});
+  c->pending.push_back({int32_t(c->off_nent() + seq_id), 0});
+  --c->live;
+  return HPA_OK;
+}
+
+hpa_status_t hpa_append_kv(hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, const int32_t* n_new,
+                           const void* k, const void* v, hpa_stream_t stream) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (n_seqs < 0) return fail(HPA_ERR_INVALID_ARG, "n_seqs < 0");
+  if (n_seqs == 0) return HPA_OK;
+  if (!seq_ids || !n_new) return fail(HPA_ERR_INVALID_ARG, "null seq_ids / n_new");
+  // ---- check (no mutation)
+  int64_t total_rows = 0;
+  int32_t need = 0;
+  std::vector<char> seen(c->cfg.max_seqs, 0);
+  for (int32_t i = 0; i < n_seqs; ++i) {
+    if (hpa_status_t st = check_seq(c, seq_ids[i])) return st;
+    if (seen[seq_ids[i]]) return fail(HPA_ERR_INVALID_ARG, "sequence %d listed twice", seq_ids[i]);
+    seen[seq_ids[i]] = 1;
+    if (n_new[i] < 0) return fail(HPA_ERR_INVALID_ARG, "n_new[%d] < 0", i);
+    const Seq& q = c->seqs[seq_ids[i]];
+    const int32_t np = pages_for_append(c, q, n_new[i]);
+    if (seq_entries(q) + np > c->cfg.max_pages_per_seq)
+      return fail(HPA_ERR_SEQ_CAPACITY, "sequence %d would exceed %d pages", seq_ids[i], c->cfg.max_pages_per_seq);
+    need += np;
+    total_rows += n_new[i];
+  }
+  if (total_rows == 0) return HPA_OK;
+  if (!k || !v) return fail(HPA_ERR_INVALID_ARG, "null k / v");
+  if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15)
+    return fail(HPA_ERR_INVALID_ARG, "k / v must be 16-byte aligned");
+  if (need > c->alloc.num_free())
+    return fail(HPA_ERR_OUT_OF_PAGES, "append needs %d pages, %d free", need, c->alloc.num_free());
+  // ---- apply
+  DeviceGuard dg(c->cfg.device);
+  const int32_t P = c->cfg.page_size;
+  std::vector<int32_t> slots;
+  slots.reserve(size_t(total_rows));
+  for (int32_t i = 0; i < n_seqs; ++i) {
+    Seq& q = c->seqs[seq_ids[i]];
+    int32_t n = n_new[i];
+    if (n == 0) continue;
+    const int32_t first_entry = std::max(0, seq_entries(q) - 1);
+    if (q.segs.empty() || q.segs.back().latent) q.segs.push_back(Segment{false, -1, 0, {}});
+    Segment& g = q.segs.back();
+    const int32_t np = pages_for_append(c, q, n);
+    c->alloc.alloc(np, g.pages);
+    for (int32_t r = 0; r < n; ++r) {
+      const int32_t row = g.rows + r;
+      slots.push_back(g.pages[row / P] * P + row % P);
+    }
+    g.rows += n;
+    c->rebuild(seq_ids[i], first_entry);
+  }
+  const int64_t Hd = int64_t(c->cfg.num_kv_heads) * c->cfg.head_dim;
+  std::vector<ScatterRecord> recs{ScatterRecord{k, v, total_rows * Hd, Hd, int32_t(total_rows), 0}};
+  return ship(c, static_cast<cudaStream_t>(stream), recs, slots, total_rows);
+}
+
+namespace {
+
+struct InstallPlan {
+  int32_t seq, set_id, m;
+  const void* kv;
+  bool is_new;
+  int32_t seg_index;  // existing segment (replace)
+  int32_t new_pages;  // pages to allocate
+  int32_t old_pages;
+};
+
+hpa_status_t plan_install(hpa_cache_t* c, int32_t seq, int32_t set_id, int32_t m, const void* kv,
+                          InstallPlan* p) {
+  if (hpa_status_t st = check_seq(c, seq)) return st;
+  if (m <= 0) return fail(HPA_ERR_INVALID_ARG, "m_rows must be positive");
+  if (!kv || (reinterpret_cast<uintptr_t>(kv) & 15)) return fail(HPA_ERR_INVALID_ARG, "kv must be a 16-byte aligned device pointer");
+  const Seq& q = c->seqs[seq];
+  const int32_t P = c->cfg.page_size;
+  const int32_t np = (m + P - 1) / P;
+  *p = InstallPlan{seq, set_id, m, kv, set_id < 0, -1, np, 0};
+  if (set_id >= 0) {
+    for (int32_t i = 0; i < int32_t(q.segs.size()); ++i)
+      if (q.segs[i].latent && q.segs[i].set_id == set_id) p->seg_index = i;
+    if (p->seg_index < 0) return fail(HPA_ERR_UNKNOWN_SET, "sequence %d has no latent set %d", seq, set_id);
+    p->old_pages = int32_t(q.segs[p->seg_index].pages.size());
+    if (p->old_pages == np) p->new_pages = 0;  // rewrite in place
+  }
+  const int32_t delta = p->new_pages - (p->new_pages ? p->old_pages : 0);
+  if (seq_entries(q) + delta > c->cfg.max_pages_per_seq)
+    return fail(HPA_ERR_SEQ_CAPACITY, "sequence %d would exceed %d pages", seq, c->cfg.max_pages_per_seq);
+  return HPA_OK;
+}
+
+// Applies a checked plan; appends the set's slots; returns the set id.
+int32_t apply_install(hpa_cache_t* c, const InstallPlan& p, std::vector<int32_t>& slots) {
+  Seq& q = c->seqs[p.seq];
+  const int32_t P = c->cfg.page_size;
+  int32_t seg_i, first_entry = 0;
+  if (p.is_new) {
+    first_entry = seq_entries(q);
+    q.segs.push_back(Segment{true, q.next_set++, 0, {}});
+    seg_i = int32_t(q.segs.size()) - 1;
+    c->alloc.alloc(p.new_pages, q.segs[seg_i].pages);
+  } else {
+    seg_i = p.seg_index;
+    for (int32_t i = 0; i < seg_i; ++i) first_entry += int32_t(q.segs[i].pages.size());
+    Segment& g = q.segs[seg_i];
+    if (p.new_pages > 0) {  // different page count: free + allocate + splice
+      for (int32_t pg : g.pages) c->alloc.release(pg);
+      g.pages.clear();
+      c->alloc.alloc(p.new_pages, g.pages);
+    }
+  }
+  Segment& g = q.segs[seg_i];
+  g.rows = p.m;
+  for (int32_t r = 0; r < p.m; ++r) slots.push_back(g.pages[r / P] * P + r % P);
+  c->rebuild(p.seq, first_entry);
+  return g.set_id;
+}
+
+}  // namespace
+
+hpa_status_t hpa_latent_set_install_batch(hpa_cache_t* c, int32_t n, const int32_t* seq_ids,
+                                          const int32_t* set_ids, const int32_t* m_rows,
+                                          const void* const* kv_ptrs, hpa_stream_t stream,
+                                          int32_t* set_ids_out) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (n < 0) return fail(HPA_ERR_INVALID_ARG, "n < 0");
+  if (n == 0) return HPA_OK;
+  if (!seq_ids || !set_ids || !m_rows || !kv_ptrs) return fail(HPA_ERR_INVALID_ARG, "null argument");
+  std::vector<InstallPlan> plans(n);
+  std::vector<char> seen(c->cfg.max_seqs, 0);
+  int32_t need = 0, freed = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    if (hpa_status_t st = plan_install(c, seq_ids[i], set_ids[i], m_rows[i], kv_ptrs[i], &plans[i])) return st;
+    if (seen[seq_ids[i]]) return fail(HPA_ERR_INVALID_ARG, "sequence %d listed twice", seq_ids[i]);
+    seen[seq_ids[i]] = 1;
+    need += plans[i].new_pages;
+    if (plans[i].new_pages && !plans[i].is_new) freed += plans[i].old_pages;
+  }
+  // replaced sets free their pages before allocating (all-or-nothing budget)
+  if (need > c->alloc.num_free() + freed)
+    return fail(HPA_ERR_OUT_OF_PAGES, "install needs %d pages, %d free", need, c->alloc.num_free() + freed);
+  DeviceGuard dg(c->cfg.device);
+  // release replaced pages first so their pages are reusable within this call
+  std::vector<int32_t> slots;
+  std::vector<ScatterRecord> recs;
+  const int64_t Hd = int64_t(c->cfg.num_kv_heads) * c->cfg.head_dim;
+  int64_t max_rows = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const InstallPlan& p = plans[i];
+    if (p.new_pages && !p.is_new) {
+      Segment& g = c->seqs[p.seq].segs[p.seg_index];
+      for (int32_t pg : g.pages) c->alloc.release(pg);
+      g.pages.clear();
+    }
+  }
+  for (int32_t i = 0; i < n; ++i) {
+    InstallPlan p = plans[i];
+    const int32_t slot_off = int32_t(slots.size());
+    if (p.new_pages && !p.is_new) {
+      // pages already released above: allocate + splice
+      Seq& q = c->seqs[p.seq];
+      int32_t first_entry = 0;
+      for (int32_t s = 0; s < p.seg_index; ++s) first_entry += int32_t(q.segs[s].pages.size());
+      Segment& g = q.segs[p.seg_index];
+      c->alloc.alloc(p.new_pages, g.pages);
+      g.rows = p.m;
+      for (int32_t r = 0; r < p.m; ++r) slots.push_back(g.pages[r / c->cfg.page_size] * c->cfg.page_size + r % c->cfg.page_size);
+      c->rebuild(p.seq, first_entry);
+      if (set_ids_out) set_ids_out[i] = g.set_id;
+    } else {
+      const int32_t id = apply_install(c, p, slots);
+      if (set_ids_out) set_ids_out[i] = id;
+    }
+    const char* kv = static_cast<const char*>(p.kv);
+    recs.push_back(ScatterRecord{kv, kv + size_t(p.m) * Hd * 2, 2 * int64_t(p.m) * Hd, Hd, p.m, slot_off});
+    max_rows = std::max<int64_t>(max_rows, p.m);
+  }
+  return ship(c, static_cast<cudaStream_t>(stream), recs, slots, max_rows);
+}
+
+hpa_status_t hpa_latent_set_install(hpa_cache_t* c, int32_t seq_id, int32_t set_id, int32_t m_rows,
+                                    const void* kv, hpa_stream_t stream, int32_t* set_id_out) {
+  int32_t out = -1;
+  hpa_status_t st = hpa_latent_set_install_batch(c, 1, &seq_id, &set_id, &m_rows, &kv, stream, &out);
+  if (st == HPA_OK && set_id_out) *set_id_out = out;
+  return st;
+}
+
+hpa_status_t hpa_latent_set_remove(hpa_cache_t* c, int32_t seq_id, int32_t set_id) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (hpa_status_t st = check_seq(c, seq_id)) return st;
+  Seq& q = c->seqs[seq_id];
+  int32_t first_entry = 0;
+  for (int32_t i = 0; i < int32_t(q.segs.size()); ++i) {
+    if (q.segs[i].latent && q.segs[i].set_id == set_id) {
+      for (int32_t pg : q.segs[i].pages) c->alloc.release(pg);
+      q.segs.erase(q.segs.begin() + i);
+      c->rebuild(seq_id, first_entry);
+      return HPA_OK;
+    }
+    first_entry += int32_t(q.segs[i].pages.size());
+  }
+  return fail(HPA_ERR_UNKNOWN_SET, "sequence %d has no latent set %d", seq_id, set_id);
+}
+
+hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids, const void* q,
+                        void* out, float softmax_scale, hpa_stream_t stream) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (layer < 0 || layer >= c->cfg.num_layers) return fail(HPA_ERR_INVALID_ARG, "layer %d out of range", layer);
+  if (n_seqs < 0) return fail(HPA_ERR_INVALID_ARG, "n_seqs < 0");
+  if (n_seqs == 0) return HPA_OK;
+  if (!seq_ids || !q || !out) return fail(HPA_ERR_INVALID_ARG, "null argument");
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(HPA_ERR_INVALID_ARG, "q / out must be 16-byte aligned");
+  int32_t max_entries = 0, max_chunks = 0;
+  for (int32_t i = 0; i < n_seqs; ++i) {
+    if (hpa_status_t st = check_seq(c, seq_ids[i])) return st;
+    const Seq& s = c->seqs[seq_ids[i]];
+    if (s.len == 0) return fail(HPA_ERR_INVALID_ARG, "sequence %d is empty (reading A11)", seq_ids[i]);
+    max_entries = std::max(max_entries, seq_entries(s));
+    max_chunks = std::max(max_chunks, s.chunks);
+  }
+  DeviceGuard dg(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (hpa_status_t st = ship(c, s, {}, {}, 0)) return st;
+  if (hpa_status_t st = upload_batch(c, n_seqs, seq_ids, s)) return st;
+  const int32_t S = plan_splits(c, n_seqs, max_entries, max_chunks);
+  const int32_t D = c->cfg.head_dim, Hq = c->cfg.num_q_heads;
+  if (S > 1) {
+    const size_t need = size_t(n_seqs) * Hq * S;
+    if (need > c->part_elems) {
+      if (c->o_part) cudaFree(c->o_part);
+      if (c->lse_part) cudaFree(c->lse_part);
+      c->o_part = nullptr;
+      c->lse_part = nullptr;
+      HPA_CUDA(cudaMalloc(&c->o_part, need * D * 4));
+      HPA_CUDA(cudaMalloc(&c->lse_part, need * 4));
+      c->part_elems = need;
+    }
+  }
+  const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt(float(D));
+  DecodeArgs a{c->dt, c->batch_dev, q, out, c->o_part, c->lse_part, n_seqs, Hq, c->cfg.num_kv_heads,
+               Hq / c->cfg.num_kv_heads, c->cfg.page_size, c->cfg.num_pages, layer, S,
+               scale * 1.4426950408889634f};
+  int launched = 0;
+  cudaError_t e = launch_decode(c->tm_k_dec, c->tm_v_dec, a, D, s, &launched);
+  c->launches += launched;
+  if (e != cudaSuccess) return cuda_fail(e, "decode launch");
+  return HPA_OK;
+}
+
+hpa_status_t hpa_prefill(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
+                         const int32_t* q_lens, const void* q, void* out, float softmax_scale,
+                         hpa_stream_t stream) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (layer < 0 || layer >= c->cfg.num_layers) return fail(HPA_ERR_INVALID_ARG, "layer %d out of range", layer);
+  if (n_seqs < 0) return fail(HPA_ERR_INVALID_ARG, "n_seqs < 0");
+  if (n_seqs == 0) return HPA_OK;
+  if (!seq_ids || !q_lens || !q || !out) return fail(HPA_ERR_INVALID_ARG, "null argument");
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(HPA_ERR_INVALID_ARG, "q / out must be 16-byte aligned");
+  std::vector<int32_t> meta(size_t(3) * n_seqs);  // rows | q_len | q_off
+  int64_t total_q = 0;
+  int32_t max_q = 0;
+  for (int32_t i = 0; i < n_seqs; ++i) {
+    if (hpa_status_t st = check_seq(c, seq_ids[i])) return st;
+    const Seq& s = c->seqs[seq_ids[i]];
+    if (q_lens[i] < 1 || q_lens[i] > s.len)
+      return fail(HPA_ERR_INVALID_ARG, "q_lens[%d]=%d must be in [1, seq_len=%d]", i, q_lens[i], s.len);
+    meta[i] = seq_ids[i];
+    meta[n_seqs + i] = q_lens[i];
+    meta[2 * n_seqs + i] = int32_t(total_q);
+    total_q += q_lens[i];
+    max_q = std::max(max_q, q_lens[i]);
+  }
+  if (total_q >= (int64_t(1) << 31)) return fail(HPA_ERR_INVALID_ARG, "too many query rows");
+  DeviceGuard dg(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (hpa_status_t st = ship(c, s, {}, {}, 0)) return st;
+  const size_t bytes = meta.size() * 4;
+  const size_t off = c->ring.reserve(bytes);
+  std::memcpy(c->ring.host(off), meta.data(), bytes);
+  HPA_CUDA(c->ring.upload(off, bytes, s));
+  const int32_t* dmeta = reinterpret_cast<const int32_t*>(c->ring.dev(off));
+  const int32_t D = c->cfg.head_dim, Hq = c->cfg.num_q_heads;
+  CUtensorMap tm_q;
+  if (!make_map_q(&tm_q, q, uint64_t(total_q), uint64_t(Hq), uint64_t(D), 128))
+    return fail(HPA_ERR_CUDA, "cuTensorMapEncodeTiled failed for q");
+  const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt(float(D));
+  PrefillArgs a{c->dt, dmeta, dmeta + n_seqs, dmeta + 2 * n_seqs, out, n_seqs, Hq, c->cfg.num_kv_heads,
+                Hq / c->cfg.num_kv_heads, c->cfg.page_size, c->cfg.num_pages, layer, max_q,
+                scale * 1.4426950408889634f};
+  int launched = 0;
+  cudaError_t e = launch_prefill(tm_q, c->tm_k_pre, c->tm_v_pre, a, D, s, &launched);
+  c->launches += launched;
+  if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
+  HPA_CUDA(c->ring.commit(off, bytes, s));
+  return HPA_OK;
+}
+
+hpa_status_t hpa_seq_info(hpa_cache_t* c, int32_t seq_id, int32_t* len, int32_t* n_pages, int32_t* n_latent_rows) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (hpa_status_t st = check_seq(c, seq_id)) return st;
+  const Seq& q = c->seqs[seq_id];
+  int32_t lat = 0;
+  for (const Segment& g : q.segs) lat += g.latent ? g.rows : 0;
+  if (len) *len = q.len;
+  if (n_pages) *n_pages = seq_entries(q);
+  if (n_latent_rows) *n_latent_rows = lat;
+  return HPA_OK;
+}
+
+hpa_status_t hpa_export_logical_kv(hpa_cache_t* c, int32_t layer, int32_t seq_id, void* k_out, void* v_out,
+                                   hpa_stream_t stream) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (layer < 0 || layer >= c->cfg.num_layers) return fail(HPA_ERR_INVALID_ARG, "layer %d out of range", layer);
+  if (hpa_status_t st = check_seq(c, seq_id)) return st;
+  if (!k_out || !v_out || ((reinterpret_cast<uintptr_t>(k_out) | reinterpret_cast<uintptr_t>(v_out)) & 15))
+    return fail(HPA_ERR_INVALID_ARG, "k_out / v_out must be 16-byte aligned device pointers");
+  DeviceGuard dg(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (hpa_status_t st = ship(c, s, {}, {}, 0)) return st;
+  HPA_CUDA(launch_export(c->geom(), c->dt, layer, seq_id, seq_entries(c->seqs[seq_id]), k_out, v_out, s));
+  c->launches += seq_entries(c->seqs[seq_id]) > 0;
+  return HPA_OK;
+}
+
+hpa_status_t hpa_export_table(hpa_cache_t* c, int32_t seq_id, int32_t* pages, int32_t* pos0, uint16_t* meta,
+                              int32_t cap, int32_t* n_out) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (hpa_status_t st = check_seq(c, seq_id)) return st;
+  const Seq& q = c->seqs[seq_id];
+  const int32_t n = seq_entries(q);
+  if (n_out) *n_out = n;
+  if (cap < n) return fail(HPA_ERR_INVALID_ARG, "cap %d < %d entries", cap, n);
+  for (int32_t e = 0; e < n; ++e) {
+    if (pages) pages[e] = q.pages[e];
+    if (pos0) pos0[e] = q.pos0[e];
+    if (meta)
+      meta[e] = uint16_t((q.meta[e] & kMetaRowsMask) | ((q.meta[e] & kMetaLatent) ? 0x8000 : 0));
+  }
+  return HPA_OK;
+}
+
+hpa_status_t hpa_set_decode_splits(hpa_cache_t* c, int32_t splits) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (splits < 0) return fail(HPA_ERR_INVALID_ARG, "splits < 0");
+  c->forced_splits = splits;
+  return HPA_OK;
+}
+
+hpa_status_t hpa_launch_count(hpa_cache_t* c, uint64_t* n) {
+  if (!c || !n) return fail(HPA_ERR_INVALID_ARG, "null argument");
+  *n = c->launches;
+  return HPA_OK;
+}
+
+}  // extern "C"

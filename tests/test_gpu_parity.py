@@ -1,0 +1,384 @@
+"""GPU parity: CUDA path (through the C ABI) vs the fp64 oracle, element by element.
+
+Tolerance (BASELINE.json north_star): max abs <= 1e-2, relative L2 <= 5e-3.
+Gathers / tables: bit-exact.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import attend, expected_table, gather_physical
+from oracle.hpa_oracle import META_LATENT_BIT
+from tests.hpa_testutil import Pair, check_close, f64
+from workloads import Draw, Shape, tiny_decode
+
+pytestmark = pytest.mark.gpu
+
+
+def oracle_decode(pair, seqs, q, layer=0):
+    out = []
+    for i, s in enumerate(seqs):
+        k, v = pair.orc.logical_kv(s, layer)
+        out.append(attend(f64(q[i:i + 1]), k, v, pair.shape.scale)[0])
+    return np.stack(out)
+
+
+def oracle_prefill(pair, seqs, q_lens, q, layer=0):
+    out, off = [], 0
+    for s, n in zip(seqs, q_lens):
+        k, v = pair.orc.logical_kv(s, layer)
+        out.append(attend(f64(q[off:off + n]), k, v, pair.shape.scale))
+        off += n
+    return np.concatenate(out)
+
+
+# ----------------------------------------------------------------------------- tiny config
+@pytest.mark.parametrize("variant", ["a", "b", "c"])
+def test_tiny_config(variant):
+    """BASELINE.json configs[0]: 1 latent page + 3 token pages (b: m=8, c: prefill 16)."""
+    w = tiny_decode(variant)
+    p = Pair(w.shape, num_pages=8, max_seqs=1, max_pages_per_seq=8)
+    s = p.build(w.seqs[0].segments)
+    q = p.queries(w.seqs[0].q_len)
+    if w.mode == "decode":
+        got = p.cache.decode(0, [s], q.cuda())
+        ref = oracle_decode(p, [s], q)
+    else:
+        got = p.cache.prefill(0, [s], [w.seqs[0].q_len], q.cuda())
+        ref = oracle_prefill(p, [s], [w.seqs[0].q_len], q)
+    torch.cuda.synchronize()
+    check_close(got, ref, w.name)
+
+
+# ----------------------------------------------------------------------------- gathers
+def test_gather_and_table_bit_exact():
+    """Route 1 (oracle model) == hpa_export_logical_kv == route 2 (pool dump +
+    exported table), bitwise; table == expected_table (kinds, valid rows, pos0)."""
+    shape = Shape(2, 4, 2, 128, 16)
+    p = Pair(shape, num_pages=256, max_seqs=4, max_pages_per_seq=64)
+    scripts = [[("latent", 128), ("latent", 8), ("tokens", 37), ("latent", 20), ("tokens", 5)],
+               [("tokens", 1)], [("latent", 128), ("tokens", 300)]]
+    seqs = [p.build(sc) for sc in scripts]
+    p.tokens(seqs, [3, 17, 16])  # cross-boundary / exact-multiple appends in one call
+    torch.cuda.synchronize()
+    kpool, vpool = (f64(t) for t in p.cache.pools())
+    for s in seqs:
+        pages, pos0, meta = p.cache.export_table(s)
+        exp = p.orc.expected_table(s)
+        assert [(("latent" if m & META_LATENT_BIT else "token"), int(m & 0x7fff), int(p0))
+                for m, p0 in zip(meta, pos0)] == exp
+        assert p.cache.seq_info(s)[0] == p.orc.seq_len(s)
+        for layer in range(2):
+            k1, v1 = p.orc.logical_kv(s, layer)
+            k2, v2 = p.cache.export_logical_kv(layer, s)
+            assert np.array_equal(k1, f64(k2)) and np.array_equal(v1, f64(v2))
+            k3, v3 = gather_physical(kpool, vpool, pages.tolist(), meta.tolist(), layer)
+            assert np.array_equal(k1, k3) and np.array_equal(v1, v3)
+
+
+# ----------------------------------------------------------------------------- decode grid
+DECODE_GRID = [
+    # (Hq, Hkv, d, P)
+    (32, 8, 128, 16),
+    (32, 8, 128, 64),
+    (8, 1, 128, 16),    # G = 8
+    (16, 1, 64, 32),    # G = 16, d = 64
+    (2, 1, 64, 16),     # tiny shape
+    (4, 4, 128, 256),   # G = 1, P = 256
+]
+
+
+@pytest.mark.parametrize("hq,hkv,d,P", DECODE_GRID)
+@pytest.mark.parametrize("splits", [0, 1, 3])
+def test_decode_parity_grid(hq, hkv, d, P, splits):
+    shape = Shape(2, hq, hkv, d, P)
+    p = Pair(shape, num_pages=2048, max_seqs=8, max_pages_per_seq=512)
+    scripts = [
+        [("latent", 128)] * 3 + [("tokens", 700)],
+        [("tokens", 1)],
+        [("latent", 8), ("tokens", 33), ("latent", 128), ("tokens", 250)],  # partial pages mid-table
+        [("latent", 128), ("latent", 100)],
+        [("tokens", 2000)],
+    ]
+    seqs = [p.build(sc) for sc in scripts]
+    p.cache.set_decode_splits(splits)
+    q = p.queries(len(seqs))
+    got = p.cache.decode(1, seqs, q.cuda())
+    torch.cuda.synchronize()
+    check_close(got, oracle_decode(p, seqs, q, layer=1), f"decode {hq}/{hkv}/{d}/P{P}/S{splits}")
+
+
+def test_decode_peaked_softmax():
+    """K x 3 stress: peaked softmax, V x 0.5 keeps |o| < 4."""
+    shape = Shape(1, 32, 8, 128, 16)
+    p = Pair(shape, num_pages=4096, max_seqs=4, max_pages_per_seq=1024, v_scale=0.5)
+    seqs = []
+    for _ in range(3):
+        s = p.new_seq()
+        kv = p.draw.latent(shape, 128)
+        kv[:, 0] *= 3
+        kv[:, 1] *= 0.5
+        p.cache.latent_install(s, -1, kv.cuda())
+        p.orc.install(s, -1, f64(kv))
+        k, v = p.draw.tokens(shape, 3000, 0.5)
+        k = (k.float() * 3).to(torch.bfloat16)
+        p.cache.append_kv([s], [3000], k.cuda(), v.cuda())
+        p.orc.append(s, f64(k), f64(v))
+        seqs.append(s)
+    q = p.queries(3)
+    got = p.cache.decode(0, seqs, q.cuda())
+    torch.cuda.synchronize()
+    check_close(got, oracle_decode(p, seqs, q), "peaked")
+
+
+# ----------------------------------------------------------------------------- invariants
+def _decode_once(placement_seed, as_latent, splits=0):
+    shape = Shape(1, 32, 8, 128, 16)
+    p = Pair(shape, num_pages=1024, max_seqs=2, max_pages_per_seq=512, placement_seed=placement_seed)
+    s = p.new_seq()
+    kv = p.draw.latent(shape, 128)
+    if as_latent:
+        p.cache.latent_install(s, -1, kv.cuda())
+    else:  # the same rows appended as token KV (kind flip)
+        p.cache.append_kv([s], [128], kv[:, 0].contiguous().cuda(), kv[:, 1].contiguous().cuda())
+    s2 = p.new_seq()  # keeps the token segment of `s` a separate segment either way
+    p.cache.latent_install(s2, -1, kv.cuda())
+    if not as_latent:
+        p.cache.latent_install(s, -1, p.draw.latent(shape, 128).cuda())
+    else:
+        p.cache.latent_install(s, -1, p.draw.latent(shape, 128).cuda())
+    k, v = p.draw.tokens(shape, 1000)
+    p.cache.append_kv([s], [1000], k.cuda(), v.cuda())
+    p.cache.set_decode_splits(splits)
+    q = p.queries(1).cuda()
+    out = p.cache.decode(0, [s], q)
+    torch.cuda.synchronize()
+    return out.cpu()
+
+
+def test_physical_placement_invariance_bitwise():
+    a = _decode_once(1, True)
+    for seed in (2, 77, 0):
+        assert torch.equal(a, _decode_once(seed, True))
+
+
+def test_kind_flip_bitwise():
+    """Latent page = just KV: the same rows stored as a latent set or as tokens."""
+    assert torch.equal(_decode_once(5, True), _decode_once(5, False))
+
+
+def test_split_invariance():
+    a = _decode_once(3, True, splits=1).float()
+    for s in (2, 5, 16):
+        b = _decode_once(3, True, splits=s).float()
+        assert torch.max(torch.abs(a - b)) <= 2 ** -7 * (1 + torch.max(torch.abs(a)))
+
+
+def test_rows_beyond_valid_are_masked():
+    """Junk written into pool rows >= valid_rows (partial pages) changes nothing."""
+    shape = Shape(1, 8, 2, 128, 16)
+    p = Pair(shape, num_pages=256, max_seqs=2, max_pages_per_seq=64)
+    s = p.build([("latent", 8), ("tokens", 21), ("latent", 100), ("tokens", 3)])
+    q = p.queries(3)
+    out1 = p.cache.decode(0, [s], q[:1].cuda()).clone()
+    pre1 = p.cache.prefill(0, [s], [3], q.cuda()).clone()
+    pages, pos0, meta = p.cache.export_table(s)
+    kp, vp = p.cache.pools()
+    for pg, m in zip(pages, meta):
+        valid = int(m & 0x7fff)
+        kp[0, pg, :, valid:] = 1000.0
+        vp[0, pg, :, valid:] = -777.0
+    out2 = p.cache.decode(0, [s], q[:1].cuda())
+    pre2 = p.cache.prefill(0, [s], [3], q.cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(out1, out2)
+    assert torch.equal(pre1, pre2)
+
+
+def test_gqa_mapping_constant_v():
+    """kv-head h holds V == h+1 everywhere -> q-head hq returns floor(hq/G)+1."""
+    shape = Shape(1, 32, 8, 128, 16)
+    p = Pair(shape, num_pages=256, max_seqs=1, max_pages_per_seq=64)
+    s = p.new_seq()
+    k, _ = p.draw.tokens(shape, 300)
+    v = torch.arange(1, 9, dtype=torch.bfloat16)[None, None, :, None].expand(1, 300, 8, 128).contiguous()
+    p.cache.append_kv([s], [300], k.cuda(), v.cuda())
+    out = p.cache.decode(0, [s], p.queries(1).cuda()).float().cpu()
+    exp = (torch.arange(32) // 4 + 1).float()[:, None].expand(32, 128)
+    assert torch.equal(out[0], exp)
+
+
+# ----------------------------------------------------------------------------- prefill
+PREFILL_GRID = [(32, 8, 128, 16), (32, 8, 128, 64), (8, 2, 64, 16), (4, 4, 128, 256), (16, 1, 128, 32)]
+
+
+@pytest.mark.parametrize("hq,hkv,d,P", PREFILL_GRID)
+def test_prefill_parity_grid(hq, hkv, d, P):
+    shape = Shape(1, hq, hkv, d, P)
+    p = Pair(shape, num_pages=4096, max_seqs=4, max_pages_per_seq=1024)
+    scripts = [[("latent", 128), ("latent", 8), ("tokens", 300)],
+               [("tokens", 77)],
+               [("latent", 128)] * 2 + [("tokens", 900)]]
+    seqs = [p.build(sc) for sc in scripts]
+    q_lens = [300, 1, 385]          # several 128-row tiles + ragged tails; q_len 1
+    q = p.queries(sum(q_lens))
+    got = p.cache.prefill(0, seqs, q_lens, q.cuda())
+    torch.cuda.synchronize()
+    check_close(got, oracle_prefill(p, seqs, q_lens, q), f"prefill {hq}/{hkv}/{d}/P{P}")
+
+
+def test_prefill_queries_spanning_latent_rows():
+    """q_len = seq_len: queries cover latent rows too (latent<->latent causal, A3)."""
+    shape = Shape(1, 8, 2, 128, 16)
+    p = Pair(shape, num_pages=512, max_seqs=2, max_pages_per_seq=128)
+    s = p.build([("latent", 128), ("tokens", 100), ("latent", 8)])
+    q = p.queries(236)
+    got = p.cache.prefill(0, [s], [236], q.cuda())
+    torch.cuda.synchronize()
+    check_close(got, oracle_prefill(p, [s], [236], q), "prefill full")
+
+
+def test_chunk_equals_decodes():
+    """Causal consistency: row t of a prefill == decode of the prefix ending at t."""
+    shape = Shape(1, 32, 8, 128, 16)
+    p = Pair(shape, num_pages=1024, max_seqs=8, max_pages_per_seq=256)
+    s = p.build([("latent", 128), ("tokens", 500)])
+    q = p.queries(4)
+    pre = p.cache.prefill(0, [s], [4], q.cuda()).float()
+    dec = p.cache.decode(0, [s], q[3:4].cuda()).float()
+    torch.cuda.synchronize()
+    assert torch.max(torch.abs(pre[3] - dec[0])) <= 2e-2
+    check_close(pre, oracle_prefill(p, [s], [4], q), "chunk")
+
+
+# ----------------------------------------------------------------------------- O(1) latent update
+def _page_hash(cache, pages):
+    kp, vp = cache.pools()
+    h = hashlib.sha256()
+    for pg in pages:
+        h.update(kp[:, pg].contiguous().view(torch.int16).cpu().numpy().tobytes())
+        h.update(vp[:, pg].contiguous().view(torch.int16).cpu().numpy().tobytes())
+    return h.hexdigest()
+
+
+def test_latent_replace_same_size_and_splice():
+    shape = Shape(1, 32, 8, 128, 16)
+    p = Pair(shape, num_pages=2048, max_seqs=4, max_pages_per_seq=512)
+    seqs = [p.build([("latent", 128)] * 4 + [("tokens", 600)]) for _ in range(3)]
+    pages, _, meta = p.cache.export_table(seqs[0])
+    tok_pages = [int(pg) for pg, m in zip(pages, meta) if not m & META_LATENT_BIT]
+    lat_pages = [int(pg) for pg, m in zip(pages, meta) if m & META_LATENT_BIT]
+    h0 = _page_hash(p.cache, tok_pages)
+    # same size: batched in-place rewrite of set `1` for every sequence
+    kvs = [p.draw.latent(shape, 128) for _ in seqs]
+    p.cache.latent_install_batch(seqs, [1] * 3, [kv.cuda() for kv in kvs])
+    for s, kv in zip(seqs, kvs):
+        p.orc.install(s, 1, f64(kv))
+    pages2, _, meta2 = p.cache.export_table(seqs[0])
+    assert list(pages2) == list(pages) and list(meta2) == list(meta)  # same pages, no splice
+    assert _page_hash(p.cache, tok_pages) == h0                      # token pages untouched
+    q = p.queries(3)
+    got = p.cache.decode(0, seqs, q.cuda())
+    torch.cuda.synchronize()
+    check_close(got, oracle_decode(p, seqs, q), "replace same size")
+    # different size: splice (set 2 of seq 1 -> 40 rows; set 0 of seq 2 -> 300 rows)
+    for s, sid, m in ((seqs[1], 2, 40), (seqs[2], 0, 300)):
+        p.latent(s, m, set_id=sid)
+    p.cache.latent_remove(seqs[0], 3)
+    p.orc.remove(seqs[0], 3)
+    for s in seqs:
+        pages, pos0, meta = p.cache.export_table(s)
+        assert [(("latent" if m & META_LATENT_BIT else "token"), int(m & 0x7fff), int(p0))
+                for m, p0 in zip(meta, pos0)] == p.orc.expected_table(s)
+    q = p.queries(3)
+    got = p.cache.decode(0, seqs, q.cuda())
+    torch.cuda.synchronize()
+    check_close(got, oracle_decode(p, seqs, q), "replace splice")
+    assert len(lat_pages) == 32
+
+
+# ----------------------------------------------------------------------------- errors
+def test_errors_leave_cache_unchanged():
+    from paper_2605_09100_b200 import HPAError
+    shape = Shape(1, 4, 2, 64, 16)
+    p = Pair(shape, num_pages=10, max_seqs=2, max_pages_per_seq=8)
+    s = p.build([("latent", 16), ("tokens", 40)])  # 1 + 3 pages
+    before = (p.cache.stats(), p.cache.export_table(s)[0].tolist())
+    k, v = p.draw.tokens(shape, 200)
+    with pytest.raises(HPAError) as e:
+        p.cache.append_kv([s], [200], k.cuda(), v.cuda())
+    assert e.value.name in ("HPA_ERR_OUT_OF_PAGES", "HPA_ERR_SEQ_CAPACITY")
+    s2 = p.cache.seq_create()
+    k, v = p.draw.tokens(shape, 120)
+    with pytest.raises(HPAError) as e:
+        p.cache.append_kv([s2], [120], k.cuda(), v.cuda())  # 8 pages needed, 6 free
+    assert e.value.name == "HPA_ERR_OUT_OF_PAGES"
+    assert (p.cache.stats()[0], p.cache.export_table(s)[0].tolist()) == (6, before[1])
+    with pytest.raises(HPAError) as e:
+        p.cache.decode(0, [s2], torch.zeros(1, 4, 64, dtype=torch.bfloat16, device="cuda"))
+    assert e.value.name == "HPA_ERR_INVALID_ARG"  # empty sequence
+    with pytest.raises(HPAError) as e:
+        p.cache.prefill(0, [s], [57], torch.zeros(57, 4, 64, dtype=torch.bfloat16, device="cuda"))
+    assert e.value.name == "HPA_ERR_INVALID_ARG"  # q_len > seq_len
+    with pytest.raises(HPAError) as e:
+        p.cache.latent_remove(s, 9)
+    assert e.value.name == "HPA_ERR_UNKNOWN_SET"
+    with pytest.raises(HPAError) as e:
+        p.cache.decode(0, [1 - s + 5], torch.zeros(1, 4, 64, dtype=torch.bfloat16, device="cuda"))
+    assert e.value.name == "HPA_ERR_UNKNOWN_SEQ"
+    p.cache.seq_release(s)
+    assert p.cache.stats() == (10, 0, 1)
+
+
+def test_allocator_fuzz_against_model():
+    """1000 random append / install / replace / remove / release ops keep
+    free + used == NP, used == pages referenced by live tables, and every
+    table equal to the model's expected table."""
+    import random
+    from paper_2605_09100_b200 import HPAError
+    rng = random.Random(0)
+    shape = Shape(1, 2, 1, 64, 16)
+    p = Pair(shape, num_pages=300, max_seqs=6, max_pages_per_seq=64)
+    live = []
+    for step in range(1000):
+        op = rng.random()
+        try:
+            if op < 0.15 and len(live) < 6:
+                live.append(p.new_seq())
+            elif op < 0.45 and live:
+                s = rng.choice(live)
+                p.tokens([s], [rng.randint(0, 40)])
+            elif op < 0.65 and live:
+                s = rng.choice(live)
+                ids = [sg.set_id for sg in p.orc.seqs[s] if sg.kind == "latent"]
+                sid = rng.choice(ids) if ids and rng.random() < 0.5 else -1
+                p.latent(s, rng.randint(1, 70), set_id=sid)
+            elif op < 0.75 and live:
+                s = rng.choice(live)
+                ids = [sg.set_id for sg in p.orc.seqs[s] if sg.kind == "latent"]
+                if ids:
+                    sid = rng.choice(ids)
+                    p.cache.latent_remove(s, sid)
+                    p.orc.remove(s, sid)
+            elif op < 0.85 and live:
+                s = live.pop(rng.randrange(len(live)))
+                p.cache.seq_release(s)
+                p.orc.release(s)
+        except HPAError as e:
+            assert e.name in ("HPA_ERR_OUT_OF_PAGES", "HPA_ERR_SEQ_CAPACITY")
+            # the oracle op was not applied either (the GPU call raised first)
+        free, used, nlive = p.cache.stats()
+        assert free + used == 300 and nlive == len(live)
+        assert used == sum(p.cache.seq_info(s)[1] for s in live)
+        if step % 50 == 0:
+            for s in live:
+                _, pos0, meta = p.cache.export_table(s)
+                assert [(("latent" if m & META_LATENT_BIT else "token"), int(m & 0x7fff), int(x))
+                        for m, x in zip(meta, pos0)] == p.orc.expected_table(s)
+    torch.cuda.synchronize()
+    for s in live:
+        k1, v1 = p.orc.logical_kv(s, 0)
+        k2, v2 = p.cache.export_logical_kv(0, s)
+        assert np.array_equal(k1, f64(k2)) and np.array_equal(v1, f64(v2))
