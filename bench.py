@@ -1,0 +1,467 @@
+#!/usr/bin/env python
+"""bench.py -- hybrid paged attention (HPA) on B200: the BASELINE.json metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Step (N=1 workload = BASELINE.json configs[1], "Qwen3-8B-shaped decode"):
+  B=64 requests per GPU, Hq=32 / H_kv=8 / d=128, page 16; each request holds
+  8 retrieved documents compressed to m=128-row latent sets + 4K reasoning
+  tokens. One step = append the current token's KV for every request (a2,
+  with the a1 table update) + split-KV decode + combine (a4, a5) for one layer.
+  value = decode tokens/s over all ranks (weak scaling: 64 requests per GPU).
+The same run also measures chunked prefill (configs[2], a6, TFLOP/s) and the
+LMAG step with per-request latent replacement (configs[3], a3), reported as
+sub-objects. Inputs are resident in HBM before timing; the KV working set
+(1.4 GB) is >10x L2, so no L2 flush is needed between steps.
+
+--impl reference times the fp64 CPU oracle (oracle/, test infrastructure) on
+a bounded sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode attn tokens/s + achieved HBM GB/s vs 8 TB/s; prefill TFLOP/s, 1/2/4/8 B200"
+NOMINAL_HBM_GBS = 8000.0
+NOMINAL_BF16_TFLOPS = 2250.0
+FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--page-size", type=int, default=16)
+    ap.add_argument("--batch", type=int, default=64, help="requests per GPU (configs[1]: 64)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the prefill / LMAG sub-benchmarks")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--splits", type=int, default=0, help="force decode split count (0 = planner)")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return dict(FALLBACK), "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Polls NVML SM clock + throttle reasons in a thread during the timed region."""
+
+    def __init__(self, device: int, period_s: float = 0.002):
+        self.samples, self.reasons, self.period, self.stop_ev = [], set(), period_s, threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - depends on the box
+            self.nv = None
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self.stop_ev.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- workload build
+def build_decode_cache(torch, Cache, shape, n_req, docs, tokens, extra_rows, device, seed, placement_seed=99):
+    """Creates a cache holding n_req requests of `docs` latent sets (m=128) followed by
+    `tokens` token rows; returns (cache, seq ids). Inputs drawn on the GPU (seeded)."""
+    from workloads import LATENT_ROWS
+    P = shape.page_size
+    rows_max = docs * LATENT_ROWS + tokens + extra_rows
+    pages_per_seq = docs * math.ceil(LATENT_ROWS / P) + math.ceil((tokens + extra_rows) / P) + 1
+    cache = Cache(shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim, P,
+                  n_req * pages_per_seq + 64, n_req, pages_per_seq, device, placement_seed)
+    g = torch.Generator(device=f"cuda:{device}").manual_seed(seed)
+    seqs = [cache.seq_create() for _ in range(n_req)]
+    for _ in range(docs):
+        kv = torch.randn((n_req, shape.num_layers, 2, LATENT_ROWS, shape.num_kv_heads, shape.head_dim),
+                         generator=g, device=f"cuda:{device}").to(torch.bfloat16)
+        cache.latent_install_batch(seqs, [-1] * n_req, [kv[i] for i in range(n_req)])
+        del kv
+    if tokens:
+        chunk = max(1, (1 << 28) // (tokens * shape.num_kv_heads * shape.head_dim * 2))  # <= 256 MB per draw
+        for lo in range(0, n_req, chunk):
+            ids = seqs[lo:lo + chunk]
+            s = (shape.num_layers, len(ids) * tokens, shape.num_kv_heads, shape.head_dim)
+            k = torch.randn(s, generator=g, device=f"cuda:{device}").to(torch.bfloat16)
+            v = torch.randn(s, generator=g, device=f"cuda:{device}").to(torch.bfloat16)
+            cache.append_kv(ids, [tokens] * len(ids), k, v)
+            del k, v
+    torch.cuda.synchronize(device)
+    return cache, seqs, rows_max
+
+
+def decode_bytes(lens, shape):
+    """Algorithmic bytes of one decode call: K+V rows + q + out + table."""
+    hkv, d, hq, P = shape.num_kv_heads, shape.head_dim, shape.num_q_heads, shape.page_size
+    return sum(L * hkv * d * 2 * 2 + 2 * hq * d * 2 + 4 * math.ceil(L / P) for L in lens)
+
+
+def prefill_flops(prior, c, shape):
+    """4 Hq d (C L_prior + C(C+1)/2) per request."""
+    return 4 * shape.num_q_heads * shape.head_dim * (c * prior + c * (c + 1) // 2)
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2605_09100_b200 import Cache
+    from paper_2605_09100_b200.dist import max_over_ranks
+    from workloads import qwen3_8b_shape
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = local
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    pk, pk_kind = peaks()
+    shape = qwen3_8b_shape(args.page_size)
+    B, docs, tokens = args.batch, 8, 4095  # + the current token appended each step -> Lb = 5120
+    K, W = args.steps, args.warmup
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[dev])
+
+    # ------------------------------------------------------------------ configs[1] decode step
+    cache, seqs, _ = build_decode_cache(torch, Cache, shape, B, docs, tokens, 2 * K + W + 16, dev,
+                                        seed=1234 + rank)
+    if args.splits:
+        cache.set_decode_splits(args.splits)
+    g = torch.Generator(device=f"cuda:{dev}").manual_seed(4321 + rank)
+    nsteps = K + W
+    knew = torch.randn((nsteps, 1, B, 8, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+    vnew = torch.randn((nsteps, 1, B, 8, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+    qs = torch.randn((nsteps, B, 32, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+    out = torch.empty((B, 32, 128), dtype=torch.bfloat16, device=f"cuda:{dev}")
+    ones = [1] * B
+    import numpy as np
+    ids = np.asarray(seqs, dtype=np.int32)
+    for i in range(W):
+        cache.append_kv(seqs, ones, knew[i], vnew[i])
+        cache.decode(0, ids, qs[i], out)
+    torch.cuda.synchronize(dev)
+    lens0 = [cache.seq_info(s)[0] for s in seqs]
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = cache.launch_count()
+    barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev) as clk:
+        t0.record(stream)
+        for i in range(K):
+            cache.append_kv(seqs, ones, knew[W + i], vnew[W + i])
+            evs[i][0].record(stream)
+            cache.decode(0, ids, qs[W + i], out)
+            evs[i][1].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    launches = cache.launch_count() - launches0
+    step_ms = t0.elapsed_time(t1) / K
+    dec_ms = [a.elapsed_time(b) for a, b in evs]
+    dec_mean = sum(dec_ms) / K
+    step_ms_max = max_over_ranks(step_ms, device=f"cuda:{dev}")
+    dec_mean_max = max_over_ranks(dec_mean, device=f"cuda:{dev}")
+    total_tokens = B * world
+    value = total_tokens / (step_ms_max / 1e3)
+    # bytes per decode call, averaged over the timed steps (lengths grow by one per step)
+    bytes_per_call = sum(decode_bytes([L + 1 + i for L in lens0], shape) for i in range(K)) / K
+    achieved = bytes_per_call / (dec_mean / 1e3) / 1e9
+    clocks = clk.summary()
+
+    # ------------------------------------------------------------------ e2e through the public API
+    pin_k = knew.cpu().pin_memory()
+    pin_v = vnew.cpu().pin_memory()
+    pin_q = qs.cpu().pin_memory()
+    pin_o = torch.empty((K, B, 32, 128), dtype=torch.bfloat16).pin_memory()
+    dk = torch.empty_like(knew[0])
+    dv = torch.empty_like(vnew[0])
+    dq = torch.empty_like(qs[0])
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for i in range(K):
+        dk.copy_(pin_k[i], non_blocking=True)
+        dv.copy_(pin_v[i], non_blocking=True)
+        dq.copy_(pin_q[i], non_blocking=True)
+        cache.append_kv(seqs, ones, dk, dv)
+        cache.decode(0, ids, dq, out)
+        pin_o[i].copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / K, device=f"cuda:{dev}")
+    h2d = dk.numel() * 2 + dv.numel() * 2 + dq.numel() * 2
+    d2h = out.numel() * 2
+    cache.close()
+    del knew, vnew, qs, pin_k, pin_v, pin_q, pin_o
+    torch.cuda.empty_cache()
+
+    res = {
+        "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(step_ms_max, 5), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "configs[1] Qwen3-8B-shaped HPA decode step (append 1 token + decode), one layer",
+                   "requests_per_gpu": B, "global_batch": B * world, "num_q_heads": 32, "num_kv_heads": 8,
+                   "head_dim": 128, "page_size": args.page_size, "latent_sets": docs, "latent_rows": 128,
+                   "reasoning_tokens": tokens + 1, "seq_len": docs * 128 + tokens + 1,
+                   "parallelism": f"request-shard x{world}" if world > 1 else "single GPU",
+                   "l2": "working set 1.4 GB/GPU >> 126 MB L2 (no flush needed)",
+                   "placement": "seeded random physical page permutation"},
+        "clocks": clocks,
+        "e2e": {"value": round(total_tokens / (e2e_ms / 1e3), 1), "unit": "tokens/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": round(e2e_ms, 5)},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": "hpa decode split (+combine) per call",
+                     "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": round(achieved / pk["hbm_gbs"], 4), "peak_kind": pk_kind,
+                     "frac_vs_nominal_8tbs": round(achieved / NOMINAL_HBM_GBS, 4),
+                     "algorithmic_bytes_per_launch": int(bytes_per_call),
+                     "launch_ms": round(dec_mean, 5), "traffic": traffic_from_profiles("decode")},
+        "decode_kernel_ms": {"mean": round(dec_mean, 5), "min": round(min(dec_ms), 5),
+                             "max_over_ranks_mean": round(dec_mean_max, 5)},
+    }
+
+    # ------------------------------------------------------------------ sub-benchmarks
+    if not args.no_extra:
+        res["prefill"] = bench_prefill(torch, Cache, shape, dev, stream, pk, pk_kind, max_over_ranks)
+        res["lmag"] = bench_lmag(torch, Cache, shape, dev, stream, max(3, min(W, 5)), min(K, 20),
+                                 world, max_over_ranks, barrier)
+    if rank == 0 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(budget_s=15.0)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def traffic_from_profiles(kernel: str):
+    """dram bytes (read + write) per launch from the committed ncu summary, if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+def bench_prefill(torch, Cache, shape, dev, stream, pk, pk_kind, max_over_ranks, reps=5):
+    """configs[2]: C = 2048 new rows over 8 latent sets (1024 rows) + 16384 cached token rows."""
+    out = {}
+    for bp in (1, 4):
+        c_rows, prior_tok = 2048, 16384
+        cache, seqs, _ = build_decode_cache(torch, Cache, shape, bp, 8, prior_tok + c_rows, 0, dev, seed=777)
+        g = torch.Generator(device=f"cuda:{dev}").manual_seed(99)
+        q = torch.randn((bp * c_rows, 32, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+        o = torch.empty_like(q)
+        for _ in range(2):
+            cache.prefill(0, seqs, [c_rows] * bp, q, o)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            cache.prefill(0, seqs, [c_rows] * bp, q, o)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = max_over_ranks(e0.elapsed_time(e1) / reps, device=f"cuda:{dev}")
+        flops = bp * prefill_flops(8 * 128 + prior_tok, c_rows, shape)
+        tf = flops / (ms / 1e3) / 1e12
+        out[f"B{bp}"] = {"ms": round(ms, 4), "tflops": round(tf, 1),
+                         "frac": round(tf / pk["bf16_tflops"], 4), "peak": pk["bf16_tflops"],
+                         "peak_kind": f"{pk_kind} bf16 dense (burst)",
+                         "frac_vs_nominal_2250": round(tf / NOMINAL_BF16_TFLOPS, 4),
+                         "flops": flops}
+        cache.close()
+        del q, o
+    out["workload"] = "configs[2] chunked prefill C=2048 over 1024 latent + 16384 cached token rows"
+    out["roofline"] = {"bound": "tensor", "unit": "TFLOP/s", "traffic": traffic_from_profiles("prefill")}
+    return out
+
+
+def bench_lmag(torch, Cache, shape, dev, stream, W, K, world, max_over_ranks, barrier):
+    """configs[3]: B=256 decode; each step replaces latent set (step mod 8) of every
+    request from a device staging buffer (one batched install), appends 1 token, decodes."""
+    import numpy as np
+    B = 256
+    cache, seqs, _ = build_decode_cache(torch, Cache, shape, B, 8, 4095, K + W + 8, dev, seed=555)
+    g = torch.Generator(device=f"cuda:{dev}").manual_seed(1)
+    stage = torch.randn((2, B, 1, 2, 128, 8, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+    kvs = [[stage[j, i] for i in range(B)] for j in range(2)]
+    kn = torch.randn((1, B, 8, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+    vn = torch.randn((1, B, 8, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+    q = torch.randn((B, 32, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+    o = torch.empty_like(q)
+    ids = np.asarray(seqs, dtype=np.int32)
+    ones = [1] * B
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    for i in range(W + K):
+        e = ev[i - W] if i >= W else None
+        if e:
+            e[0].record(stream)
+        cache.latent_install_batch(seqs, [i % 8] * B, kvs[i % 2])
+        if e:
+            e[1].record(stream)
+        cache.append_kv(seqs, ones, kn, vn)
+        if e:
+            e[2].record(stream)
+        cache.decode(0, ids, q, o)
+        if e:
+            e[3].record(stream)
+    torch.cuda.synchronize(dev)
+    inst = max_over_ranks(sum(a[0].elapsed_time(a[1]) for a in ev) / K, device=f"cuda:{dev}")
+    step = max_over_ranks(sum(a[0].elapsed_time(a[3]) for a in ev) / K, device=f"cuda:{dev}")
+    dec = max_over_ranks(sum(a[2].elapsed_time(a[3]) for a in ev) / K, device=f"cuda:{dev}")
+    lens = [cache.seq_info(s)[0] for s in seqs]
+    inst_bytes = 2 * B * 128 * 8 * 128 * 2 * 2  # K+V, read + write
+    dbytes = decode_bytes(lens, shape)
+    cache.close()
+    return {"workload": "configs[3] LMAG: B=256 decode + per-request latent set replacement each step",
+            "tokens_per_s": round(B * world / (step / 1e3), 1),
+            "tokens_per_s_without_install": round(B * world / ((step - inst) / 1e3), 1),
+            "step_ms": round(step, 4), "install_ms": round(inst, 4), "decode_ms": round(dec, 4),
+            "install_gbs": round(inst_bytes / (inst / 1e3) / 1e9, 1),
+            "decode_gbs": round(dbytes / (dec / 1e3) / 1e9, 1)}
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def _oracle_requests(n, seed=11):
+    """n requests of configs[1] shape built in the oracle's own cache model (CPU)."""
+    import torch
+    from oracle import OracleCache
+    from workloads import Draw, rag_decode
+    w = rag_decode(1)
+    sh = w.shape
+    c = OracleCache(1, 32, 8, 128, 16)
+    d = Draw(seed)
+    for s in range(n):
+        c.create_seq(s)
+        for kind, m in w.seqs[0].segments:
+            if kind == "latent":
+                c.install(s, -1, d.latent(sh, m).to(torch.float64).numpy())
+            else:
+                k, v = d.tokens(sh, m)
+                c.append(s, k.to(torch.float64).numpy(), v.to(torch.float64).numpy())
+    qs = d.queries(sh, n).to(torch.float64).numpy()
+    return c, qs, sh
+
+
+def cpu_baseline(budget_s: float = 15.0):
+    """The fp64 oracle as it stands, BLAS pinned to one thread, on a bounded sample."""
+    from threadpoolctl import threadpool_limits
+    from oracle.hpa_oracle import decode_reference
+    n_req = 4
+    c, qs, sh = _oracle_requests(n_req)
+    done, t_work = 0, 0.0
+    with threadpool_limits(1):
+        while t_work < budget_s:
+            s = done % n_req
+            t = time.perf_counter()
+            decode_reference(c, s, 0, qs[s], sh.scale)
+            t_work += time.perf_counter() - t
+            done += 1
+    return {"value": round(done / t_work, 3), "unit": "tokens/s", "cores": 1, "kind": "oracle",
+            "sample": f"{done} decode queries over {n_req} configs[1] requests (Lb=5120, 32 q-heads), "
+                      f"{t_work:.1f} s of fp64 numpy work on 1 host core"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from threadpoolctl import threadpool_limits
+    from oracle.hpa_oracle import decode_reference
+    n_req = 2
+    c, qs, sh = _oracle_requests(n_req, seed=21)
+    K, W = args.steps, args.warmup
+    with threadpool_limits(1):
+        for i in range(W):
+            decode_reference(c, i % n_req, 0, qs[i % n_req], sh.scale)
+        t = time.perf_counter()
+        for i in range(K):
+            decode_reference(c, i % n_req, 0, qs[i % n_req], sh.scale)
+        el = time.perf_counter() - t
+    value = K / el
+    res = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "tokens/s",
+           "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(el / K * 1e3, 3),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic",
+           "config": {"workload": "configs[1] Qwen3-8B-shaped HPA decode (one query per step, sample)",
+                      "num_q_heads": 32, "num_kv_heads": 8, "head_dim": 128, "page_size": 16,
+                      "seq_len": 5120},
+           "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": 1, "kind": "oracle",
+                            "sample": f"{K} timed decode queries over {n_req} requests, fp64 numpy, 1 core"},
+           "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

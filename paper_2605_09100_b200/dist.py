@@ -1,0 +1,57 @@
+"""Multi-GPU partitioning of the HPA path.
+
+The paper serves on one GPU (tensor_parallel_size 1). Every
+request's attention depends only on its own pages, so the
+default partition is by request: rank r owns a contiguous block of requests,
+one cache per GPU, and there is NO collective on the data path (weak scaling).
+
+Optional KV-head shard: rank r holds kv-heads [r*H_kv/n, (r+1)*H_kv/n) of every
+request (and their G q-heads each); outputs are gathered with one NCCL
+all-gather over NVLink. It exists for latency / capacity, not throughput.
+"""
+from __future__ import annotations
+
+from typing import List, Tuple
+
+import torch
+import torch.distributed as dist
+
+
+def shard_requests(n_requests: int, rank: int, world: int) -> List[int]:
+    """Contiguous block of request indices owned by `rank` (sizes differ by <= 1)."""
+    if world <= 0 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, extra = divmod(n_requests, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return list(range(lo, hi))
+
+
+def head_shard(num_q_heads: int, num_kv_heads: int, rank: int, world: int) -> Tuple[int, int, int, int]:
+    """(kv_lo, kv_hi, q_lo, q_hi) of the heads owned by `rank` in KV-head-shard mode.
+    The GQA mapping hq -> floor(hq / G) (reading A6) keeps q-heads with their kv-head."""
+    if num_kv_heads % world != 0:
+        raise ValueError("num_kv_heads must be divisible by the world size")
+    g = num_q_heads // num_kv_heads
+    per = num_kv_heads // world
+    kv_lo, kv_hi = rank * per, (rank + 1) * per
+    return kv_lo, kv_hi, kv_lo * g, kv_hi * g
+
+
+def gather_head_shards(out_local: torch.Tensor, group=None) -> torch.Tensor:
+    """out_local [B][Hq/n][d] on every rank -> full [B][Hq][d] (rank-major head order)
+    with one all_gather_into_tensor (NCCL over NVLink on GPUs, gloo on CPU)."""
+    world = dist.get_world_size(group)
+    b, hl, d = out_local.shape
+    buf = torch.empty((world * b, hl, d), dtype=out_local.dtype, device=out_local.device)
+    dist.all_gather_into_tensor(buf, out_local.contiguous(), group=group)
+    return buf.view(world, b, hl, d).permute(1, 0, 2, 3).reshape(b, world * hl, d)
+
+
+def max_over_ranks(x: float, device=None) -> float:
+    """Timing reduction for reporting (max over ranks); not on the data path."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
