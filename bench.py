@@ -25,7 +25,6 @@ import math
 import os
 import statistics
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -61,59 +60,82 @@ def peaks():
 
 
 # ----------------------------------------------------------------------------- clocks
+_SAMPLER = r"""
+import sys, time, pynvml as nv
+nv.nvmlInit()
+bus = sys.argv[1]
+try:
+    h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+except Exception:
+    h = nv.nvmlDeviceGetHandleByIndex(0)
+out = open(sys.argv[2], "w")
+out.write(f"max {nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)}\n"); out.flush()
+while True:
+    t = time.time()
+    try:
+        c = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        out.write(f"{t:.6f} {c} {r}\n"); out.flush()
+    except Exception:
+        pass
+    time.sleep(0.0005)
+"""
+
+_REASONS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80}
+
+
 class ClockSampler:
-    """Polls NVML SM clock + throttle reasons in a thread during the timed region."""
+    """NVML SM clock + throttle reasons polled every ~0.5 ms by a separate process;
+    summary() keeps the samples that fall inside [start(), stop()]."""
 
-    def __init__(self, device: int, period_s: float = 0.002):
-        self.samples, self.reasons, self.period, self.stop_ev = [], set(), period_s, threading.Event()
-        self.max_mhz = None
-        try:
-            import pynvml as nv
-            nv.nvmlInit()
-            self.nv = nv
-            self.h = nv.nvmlDeviceGetHandleByIndex(device)
-            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
-        except Exception as e:  # pragma: no cover - depends on the box
-            self.nv = None
-            self.err = str(e)
-
-    def _run(self):
-        nv = self.nv
-        names = {
-            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
-            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
-            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
-            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
-            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
-        }
-        while not self.stop_ev.is_set():
+    def __init__(self, device: int):
+        import subprocess
+        import tempfile
+        import torch
+        self.path = tempfile.mktemp(prefix="hpa_clk_")
+        p = torch.cuda.get_device_properties(device)
+        bus = f"{getattr(p, 'pci_domain_id', 0):08x}:{getattr(p, 'pci_bus_id', 0):02x}:{getattr(p, 'pci_device_id', 0):02x}.0"
+        self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, bus, self.path],
+                                     stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        self.t0 = self.t1 = None
+        deadline = time.time() + 20
+        while time.time() < deadline:  # wait until the sampler produces data
             try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for k, bit in names.items():
-                    if r & bit:
-                        self.reasons.add(k)
-            except Exception:
+                with open(self.path) as f:
+                    if len(f.read().splitlines()) >= 3:
+                        break
+            except FileNotFoundError:
                 pass
-            time.sleep(self.period)
+            time.sleep(0.05)
 
-    def __enter__(self):
-        if self.nv:
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
-        return self
+    def start(self):
+        self.t0 = time.time()
 
-    def __exit__(self, *exc):
-        self.stop_ev.set()
-        if self.nv:
-            self.t.join()
+    def stop(self):
+        self.t1 = time.time()
+        time.sleep(0.01)
+        self.proc.terminate()
+        self.proc.wait()
 
     def summary(self):
-        if not self.nv:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples)}
+        try:
+            lines = open(self.path).read().splitlines()
+            os.unlink(self.path)
+        except Exception as e:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": str(e)}
+        mx, clk, reasons = None, [], set()
+        for ln in lines:
+            parts = ln.split()
+            if parts[0] == "max":
+                mx = int(parts[1])
+                continue
+            t, c, r = float(parts[0]), int(parts[1]), int(parts[2])
+            if self.t0 is not None and self.t0 <= t <= self.t1:
+                clk.append(c)
+                reasons |= {k for k, b in _REASONS.items() if r & b}
+        return {"sm_mhz": statistics.median(clk) if clk else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(clk)}
 
 
 # ----------------------------------------------------------------------------- workload build
@@ -205,17 +227,19 @@ def run_ours(args):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = cache.launch_count()
+    clk = ClockSampler(dev)
     barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(dev) as clk:
-        t0.record(stream)
-        for i in range(K):
-            cache.append_kv(seqs, ones, knew[W + i], vnew[W + i])
-            evs[i][0].record(stream)
-            cache.decode(0, ids, qs[W + i], out)
-            evs[i][1].record(stream)
-        t1.record(stream)
-        torch.cuda.synchronize(dev)
+    clk.start()
+    t0.record(stream)
+    for i in range(K):
+        cache.append_kv(seqs, ones, knew[W + i], vnew[W + i])
+        evs[i][0].record(stream)
+        cache.decode(0, ids, qs[W + i], out)
+        evs[i][1].record(stream)
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk.stop()
     barrier()
     launches = cache.launch_count() - launches0
     step_ms = t0.elapsed_time(t1) / K

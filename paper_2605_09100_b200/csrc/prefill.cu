@@ -9,22 +9,26 @@
 //   P rounded to bf16 before the PV product, bf16 output.
 //
 // Design (sm_100a; roofline: bf16 tensor pipe):
-//  * CTA = one 128-row query tile of one q-head (grid: M tiles x Hq x seqs),
-//    192 threads: warp 0 = TMA producer, warp 1 = tcgen05 MMA issuer (+ TMEM
-//    owner), warps 2..5 = softmax / correction / epilogue (one TMEM lane = one
-//    query row per thread).
-//  * Key tiles are 128 page *slots*: 128/P whole pages (P <= 128) or a
-//    128-row slice of a page (P = 256), each page box loaded by 2-D TMA with
-//    128-B swizzle straight from the pool; slots past the table are TMA
-//    out-of-bounds (zero-filled). The producer also publishes each slot's
-//    logical index (INT_MAX for rows >= valid_rows) for the mask.
-//  * S = Q K^T: tcgen05.mma kind::f16, M=128, N=128, K=16 steps, SS operands
-//    (K-major SW128 descriptors), fp32 accumulator in TMEM (double-buffered:
-//    S_{j+1} is computed while softmax j runs).
-//  * softmax: tcgen05.ld of the row, log2-domain online softmax with lazy
-//    rescaling (O in TMEM is corrected only when the row max grows by > 2^8),
-//    P -> bf16 -> shared memory (K-major SW128) for O += P V (V is the
-//    MN-major B operand), O accumulated in TMEM.
+//  * CTA = two 128-row query tiles ("slots") that share every K/V tile: two
+//    q-heads of the same GQA group over the same token rows (G even), or two
+//    consecutive row tiles of one head (G odd). 320 threads:
+//      warps 0-3  softmax warpgroup for slot 0 (one TMEM lane = one row)
+//      warps 4-7  softmax warpgroup for slot 1
+//      warp  8    TMA producer (all lanes build the mask indices; the page
+//                 boxes are issued in parallel by several lanes)
+//      warp  9    tcgen05 MMA issuer; owns the 512 TMEM columns.
+//  * TMEM: S_s / P_s at columns [128 s, 128 s + 128), O_s at [256 + 128 s, ...).
+//    S = Q K^T (SS: Q and K K-major, 128-B swizzle); the softmax writes P as
+//    packed bf16 over S and O += P V runs in TS form (A = P from TMEM, B = V
+//    MN-major from shared memory). The two slots ping-pong so the tensor pipe
+//    computes one slot's QK^T / PV while the other slot's softmax runs.
+//  * Key tiles are 128 page *slots*: 128/P whole pages (P <= 128) or a 128-row
+//    slice of one page (P = 256); each page box is a 2-D TMA load straight from
+//    the pool; slots past the table are out-of-bounds boxes (zero fill). The
+//    producer publishes each key slot's logical index (INT_MAX when the row is
+//    >= valid_rows) for the causal / partial-page mask.
+//  * Online softmax in the log2 domain with lazy rescaling: O_s in TMEM is
+//    corrected only when a row max grows by more than 2^8.
 #include "hpa_kernels.h"
 #include "ptx.cuh"
 #include <cuda_bf16.h>
@@ -34,30 +38,31 @@
 namespace hpa {
 namespace {
 
-constexpr int kBM = 128;      // query rows per CTA
-constexpr int kBN = 128;      // key slots per tile
-constexpr int kNK = 2;        // K ring depth
-constexpr int kNV = 2;        // V ring depth
-constexpr int kNC = 4;        // column-index ring depth
+constexpr int kBM = 128;   // query rows per slot
+constexpr int kBN = 128;   // key slots per tile
+constexpr int kNK = 2;     // K ring depth
+constexpr int kNV = 2;     // V ring depth
+constexpr int kNC = 4;     // mask-index ring depth
+constexpr int kThreads = 320;
+constexpr int kProducerWarp = 8;
+constexpr int kMmaWarp = 9;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units (factor 256)
 
 template <int D>
 struct PSmem {
-  static constexpr int kQ = kBM * D * 2;
+  static constexpr int kQ = kBM * D * 2;   // one slot's Q tile
   static constexpr int kKV = kBN * D * 2;
-  static constexpr int kP = kBM * kBN * 2;
   static constexpr int oQ = 0;
-  static constexpr int oK = oQ + kQ;
+  static constexpr int oK = oQ + 2 * kQ;
   static constexpr int oV = oK + kNK * kKV;
-  static constexpr int oP = oV + kNV * kKV;
-  static constexpr int oC = oP + kP;                     // int32 [kNC][kBN + 1] (last = flags)
-  static constexpr int oBar = oC + kNC * (kBN + 4) * 4;  // mbarriers
-  // barriers: q_full, k_full[NK], k_empty[NK], v_full[NV], v_empty[NV], s_full[2], s_empty[2],
-  //           p_full, p_empty, o_full, c_full[NC], c_empty[NC]
-  static constexpr int kNBar = 1 + 2 * kNK + 2 * kNV + 4 + 3 + 2 * kNC;
-  static constexpr int oTmem = oBar + kNBar * 8;
-  // >= 116 KB so that exactly one CTA is resident per SM (it owns all 512 TMEM columns)
-  static constexpr int kRaw = oTmem + 16 + 1024;
+  static constexpr int oC = oV + kNV * kKV;              // int32 [kNC][kBN + 4] (kBN = all-visible flag)
+  static constexpr int oBar = oC + kNC * (kBN + 4) * 4;
+  // q_full, k_full[NK], k_empty[NK], v_full[NV], v_empty[NV], s_full[2], p_full[2], o_full,
+  // c_full[NC], c_empty[NC]
+  static constexpr int kNBar = 1 + 2 * kNK + 2 * kNV + 2 + 2 + 1 + 2 * kNC;
+  static constexpr int oMisc = oBar + kNBar * 8;
+  static constexpr int kRaw = oMisc + 16 + 1024;
+  // >= 116 KB so exactly one CTA is resident per SM (it owns all 512 TMEM columns)
   static constexpr int kBytes = kRaw > 116 * 1024 ? kRaw : 116 * 1024;
 };
 
@@ -68,7 +73,9 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+// D[tmem] (+)= A[smem desc] * B[smem desc]
+__device__ __forceinline__ void tc_mma_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
@@ -76,34 +83,47 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
+// D[tmem] (+)= A[tmem] * B[smem desc]
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+#define HPA_R32(r)                                                                                       \
+  "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),       \
+      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),          \
+      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),        \
+      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),        \
+      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+#define HPA_W32(r)                                                                                       \
+  "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),    \
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),    \
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),   \
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
 __device__ __forceinline__ void tc_ld32(uint32_t taddr, float* v) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
       "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : HPA_R32(r)
       : "r"(taddr));
 }
-__device__ __forceinline__ void tc_st32(uint32_t taddr, const float* v) {
-  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+__device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
       "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
-      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
-      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      HPA_W32(r)
       : "memory");
 }
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// Shared-memory matrix descriptor (tcgen05 "smem descriptor"): start >> 4 in
-// bits 0-13, LBO >> 4 in 16-29, SBO >> 4 in 32-45, version 1 in 46-47,
-// layout SWIZZLE_128B (2) in 61-63.
+// Shared-memory matrix descriptor: start >> 4 (bits 0-13), LBO >> 4 (16-29),
+// SBO >> 4 (32-45), version 1 (46-47), layout SWIZZLE_128B = 2 (61-63).
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
   d |= uint64_t((saddr >> 4) & 0x3fff);
@@ -113,28 +133,41 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   d |= uint64_t(2) << 61;
   return d;
 }
-// Instruction descriptor kind::f16: bf16 A/B, fp32 D, M, N, A/B major.
+// Instruction descriptor kind::f16: bf16 A/B, fp32 D, M, N, A/B major (0 = K, 1 = MN).
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, int b_mn_major) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(a_mn_major) << 15) | (uint32_t(b_mn_major) << 16) |
          (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
 template <int D>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, const PrefillArgs a) {
   using L = PSmem<D>;
   constexpr int kHalves = D / 64;
-  const int mt = blockIdx.x, hq = blockIdx.y, b = blockIdx.z;
+  const int b = blockIdx.z;
   const int q_len = a.q_len[b];
-  if (mt * kBM >= q_len) return;  // ragged: this sequence has fewer query tiles
+  // slot -> (q-head, row tile)
+  int hq_s[2], mt_s[2];
+  if ((a.G & 1) == 0) {
+    const int h = blockIdx.y / (a.G >> 1), pair = blockIdx.y % (a.G >> 1);
+    hq_s[0] = h * a.G + 2 * pair;
+    hq_s[1] = hq_s[0] + 1;
+    mt_s[0] = mt_s[1] = blockIdx.x;
+  } else {
+    hq_s[0] = hq_s[1] = blockIdx.y;
+    mt_s[0] = 2 * blockIdx.x;
+    mt_s[1] = 2 * blockIdx.x + 1;
+  }
+  if (mt_s[0] * kBM >= q_len) return;  // ragged: this sequence has fewer query tiles
+  const bool slot1_live = mt_s[1] * kBM < q_len;
+  const int h = hq_s[0] / a.G;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = sm + L::oQ;
   uint8_t* sK = sm + L::oK;
   uint8_t* sV = sm + L::oV;
-  uint8_t* sP = sm + L::oP;
   int32_t* sC = reinterpret_cast<int32_t*>(sm + L::oC);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::oBar);
   uint64_t* q_full = bars;
@@ -143,47 +176,45 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   uint64_t* v_full = k_empty + kNK;
   uint64_t* v_empty = v_full + kNV;
   uint64_t* s_full = v_empty + kNV;
-  uint64_t* s_empty = s_full + 2;
-  uint64_t* p_full = s_empty + 2;
-  uint64_t* p_empty = p_full + 1;
-  uint64_t* o_full = p_empty + 1;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_full = p_full + 2;
   uint64_t* c_full = o_full + 1;
   uint64_t* c_empty = c_full + kNC;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::oTmem);
-  int32_t* ntiles_slot = reinterpret_cast<int32_t*>(sm + L::oTmem + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::oMisc);
+  int32_t* ntiles_slot = reinterpret_cast<int32_t*>(sm + L::oMisc + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int seq = a.seq_rows[b];
-  const int h = hq / a.G;
   const int seq_len = a.t.seq_len[seq];
   const int n_ent = a.t.n_entries[seq];
   const int32_t* bt = a.t.block_table + int64_t(seq) * a.t.max_pages;
   const int32_t* p0 = a.t.pos0 + int64_t(seq) * a.t.max_pages;
   const int32_t* mt_ = a.t.meta + int64_t(seq) * a.t.max_pages;
   const int P = a.P;
-  const int i_min = seq_len - q_len + mt * kBM;                       // logical index of row 0
-  const int i_max = seq_len - q_len + min(q_len, (mt + 1) * kBM) - 1;  // of the last real row
+  const int lp = a.log2P;
+  const int q_base = seq_len - q_len;                         // logical index of query row 0
+  const int i_min = q_base + mt_s[0] * kBM;                     // smallest row index in the CTA
+  const int last_mt = slot1_live ? mt_s[1] : mt_s[0];
+  const int i_max = q_base + min(q_len, (last_mt + 1) * kBM) - 1;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     for (int i = 0; i < kNK; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
     for (int i = 0; i < kNV; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 128); }
-    mbar_init(p_full, 128);
-    mbar_init(p_empty, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 128); }
     mbar_init(o_full, 1);
-    for (int i = 0; i < kNC; ++i) { mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], 128); }
+    for (int i = 0; i < kNC; ++i) { mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], 256); }
     fence_barrier_init();
-    // number of key tiles: the tile holding the slot of logical index i_max
+    // key tiles needed: the tile holding the slot of logical index i_max
     int lo = 0, hi = n_ent - 1;  // last entry with pos0 <= i_max
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
       if (p0[mid] <= i_max) lo = mid; else hi = mid - 1;
     }
-    const int64_t slot = int64_t(lo) * P + (i_max - p0[lo]);
-    *ntiles_slot = int(slot / kBN) + 1;
+    const int slot = (lo << lp) + (i_max - p0[lo]);
+    *ntiles_slot = slot / kBN + 1;
   }
-  if (warp == 1) {  // TMEM: S0 [0,128), S1 [128,256), O [256, 256+D)
+  if (warp == kMmaWarp) {  // TMEM: S/P 0 [0,128), S/P 1 [128,256), O0 [256,..), O1 [384,..)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -194,21 +225,24 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   const uint32_t tmem = *tmem_slot;
   const int n_tiles = *ntiles_slot;
 
-  if (warp == 0) {
+  if (warp == kProducerWarp) {
     // ================================================================ producer
-    // lane 0 issues every TMA; all 32 lanes build the tile's mask indices.
     if (lane == 0) {
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
-      const int q_tok = a.q_off[b] + mt * kBM;
-      mbar_arrive_expect_tx(q_full, L::kQ);
+      mbar_arrive_expect_tx(q_full, slot1_live ? 2 * L::kQ : L::kQ);
+      for (int s = 0; s < (slot1_live ? 2 : 1); ++s) {
+        const int q_tok = a.q_off[b] + mt_s[s] * kBM;
 #pragma unroll
-      for (int hf = 0; hf < kHalves; ++hf) tma_load_3d(sQ + hf * kBM * 128, &tm_q, q_full, hf * 64, hq, q_tok);
+        for (int hf = 0; hf < kHalves; ++hf)
+          tma_load_3d(sQ + s * L::kQ + hf * kBM * 128, &tm_q, q_full, hf * 64, hq_s[s], q_tok);
+      }
     }
     const int pbox = P < kBN ? P : kBN;
     const int nbox = kBN / pbox;
     constexpr int kOobRow = INT_MAX / 2;  // fully out-of-bounds box -> TMA zero fill
+    const int head_row = a.layer * a.NP;
     for (int j = 0; j < n_tiles; ++j) {
       // logical index of every key slot (INT_MAX: row >= valid_rows or past the table)
       const int cs = j % kNC;
@@ -218,8 +252,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #pragma unroll
       for (int x = 0; x < kBN / 32; ++x) {
         const int c = x * 32 + lane;
-        const int64_t slot = int64_t(j) * kBN + c;
-        const int e = int(slot / P), r = int(slot % P);
+        const int slot = j * kBN + c;
+        const int e = slot >> lp, r = slot & (P - 1);
         int v = INT_MAX;
         if (e < n_ent && r < (mt_[e] & kMetaRowsMask)) v = p0[e] + r;
         col[c] = v;
@@ -228,181 +262,186 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       vis = __all_sync(0xffffffffu, vis);
       if (lane == 0) col[kBN] = vis ? 1 : 0;
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&c_full[cs]);
-        const int ks = j % kNK;
-        if (j >= kNK) mbar_wait(&k_empty[ks], ((j / kNK) - 1) & 1);
-        mbar_arrive_expect_tx(&k_full[ks], L::kKV);
-        for (int bx = 0; bx < nbox; ++bx) {
-          const int64_t slot = int64_t(j) * kBN + bx * pbox;
-          const int e = int(slot / P), r = int(slot % P);
-          const int row = e < n_ent ? ((a.layer * a.NP + bt[e]) * a.Hkv + h) * P + r : kOobRow;
+      // page box coordinates (lane bx < nbox owns box bx)
+      int row = kOobRow;
+      if (lane < nbox) {
+        const int slot = j * kBN + lane * pbox;
+        const int e = slot >> lp;
+        if (e < n_ent) row = ((head_row + bt[e]) * a.Hkv + h) * P + (slot & (P - 1));
+      }
+      if (lane == 0) mbar_arrive(&c_full[cs]);
+      const int ks = j % kNK;
+      if (j >= kNK) mbar_wait(&k_empty[ks], ((j / kNK) - 1) & 1);
+      if (lane == 0) mbar_arrive_expect_tx(&k_full[ks], L::kKV);
+      __syncwarp();
+      if (lane < nbox) {
 #pragma unroll
-          for (int hf = 0; hf < kHalves; ++hf)
-            tma_load_2d(sK + ks * L::kKV + hf * kBN * 128 + bx * pbox * 128, &tm_k, &k_full[ks], hf * 64, row);
-        }
-        const int vs = j % kNV;
-        if (j >= kNV) mbar_wait(&v_empty[vs], ((j / kNV) - 1) & 1);
-        mbar_arrive_expect_tx(&v_full[vs], L::kKV);
-        for (int bx = 0; bx < nbox; ++bx) {
-          const int64_t slot = int64_t(j) * kBN + bx * pbox;
-          const int e = int(slot / P), r = int(slot % P);
-          const int row = e < n_ent ? ((a.layer * a.NP + bt[e]) * a.Hkv + h) * P + r : kOobRow;
+        for (int hf = 0; hf < kHalves; ++hf)
+          tma_load_2d(sK + ks * L::kKV + hf * kBN * 128 + lane * pbox * 128, &tm_k, &k_full[ks], hf * 64, row);
+      }
+      const int vs = j % kNV;
+      if (j >= kNV) mbar_wait(&v_empty[vs], ((j / kNV) - 1) & 1);
+      if (lane == 0) mbar_arrive_expect_tx(&v_full[vs], L::kKV);
+      __syncwarp();
+      if (lane < nbox) {
 #pragma unroll
-          for (int hf = 0; hf < kHalves; ++hf)
-            tma_load_2d(sV + vs * L::kKV + hf * kBN * 128 + bx * pbox * 128, &tm_v, &v_full[vs], hf * 64, row);
-        }
+        for (int hf = 0; hf < kHalves; ++hf)
+          tma_load_2d(sV + vs * L::kKV + hf * kBN * 128 + lane * pbox * 128, &tm_v, &v_full[vs], hf * 64, row);
       }
       __syncwarp();
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ================================================================ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idS = idesc_bf16(kBM, kBN, 0, 0);
       constexpr uint32_t idO = idesc_bf16(kBM, D, 0, 1);
-      const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV), aP = smem_u32(sP);
-      const uint32_t tO = tmem + 256;
+      const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV);
+      const int nslot = slot1_live ? 2 : 1;
       mbar_wait(q_full, 0);
-      auto issue_pv = [&](int jj) {
-        mbar_wait(p_full, jj & 1);
-        const int vs = jj % kNV;
-        mbar_wait(&v_full[vs], (jj / kNV) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < kBN / 16; ++k) {
-          // A = P [128 x 128 keys], K-major, 64-key blocks of 16 KB; B = V [keys x D], MN-major
-          const uint64_t ad = sdesc(aP + (k >> 2) * (kBM * 128) + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = sdesc(aV + vs * L::kKV + k * 2048, kBN * 128, 1024);
-          tc_mma(tO, ad, bd, idO, (jj > 0 || k > 0) ? 1u : 0u);
-        }
-        tc_commit(&v_empty[vs]);
-        tc_commit(p_empty);
-      };
-      for (int j = 0; j < n_tiles; ++j) {
-        const int ks = j % kNK, sb = j & 1;
-        mbar_wait(&k_full[ks], (j / kNK) & 1);
-        if (j >= 2) mbar_wait(&s_empty[sb], ((j >> 1) - 1) & 1);
-        tc_fence_after();
+      auto issue_s = [&](int s, int jj) {
+        const int ks = jj % kNK;
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
-          const uint64_t ad = sdesc(aQ + (k >> 2) * (kBM * 128) + (k & 3) * 32, 16, 1024);
+          const uint64_t ad = sdesc(aQ + s * L::kQ + (k >> 2) * (kBM * 128) + (k & 3) * 32, 16, 1024);
           const uint64_t bd = sdesc(aK + ks * L::kKV + (k >> 2) * (kBN * 128) + (k & 3) * 32, 16, 1024);
-          tc_mma(tmem + sb * 128, ad, bd, idS, k > 0 ? 1u : 0u);
+          tc_mma_ss(tmem + s * 128, ad, bd, idS, k > 0 ? 1u : 0u);
         }
-        tc_commit(&k_empty[ks]);
-        tc_commit(&s_full[sb]);
-        if (j >= 1) issue_pv(j - 1);
+        tc_commit(&s_full[s]);
+      };
+      auto issue_pv = [&](int s, int jj) {
+        const int vs = jj % kNV;
+#pragma unroll
+        for (int k = 0; k < kBN / 16; ++k) {
+          const uint64_t bd = sdesc(aV + vs * L::kKV + k * 2048, kBN * 128, 1024);
+          tc_mma_ts(tmem + 256 + s * 128, tmem + s * 128 + k * 8, bd, idO, (jj > 0 || k > 0) ? 1u : 0u);
+        }
+      };
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      for (int s = 0; s < nslot; ++s) issue_s(s, 0);
+      tc_commit(&k_empty[0]);
+      for (int j = 0; j < n_tiles; ++j) {
+        const bool more = j + 1 < n_tiles;
+        if (more) mbar_wait(&k_full[(j + 1) % kNK], ((j + 1) / kNK) & 1);
+        mbar_wait(&v_full[j % kNV], (j / kNV) & 1);
+        for (int s = 0; s < nslot; ++s) {
+          mbar_wait(&p_full[s], j & 1);
+          tc_fence_after();
+          issue_pv(s, j);
+          if (s == nslot - 1) tc_commit(&v_empty[j % kNV]);
+          if (more) issue_s(s, j + 1);  // overwrites S/P s after PV s has read P (in-order pipe)
+        }
+        if (more) tc_commit(&k_empty[(j + 1) % kNK]);
       }
-      issue_pv(n_tiles - 1);
       tc_commit(o_full);
     }
   } else {
-    // ================================================================ softmax
+    // ================================================================ softmax (slot = warp / 4)
+    const int s = warp >> 2;
     const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
-    const int row = quarter * 32 + lane;          // query row within the tile == TMEM lane
-    const int t = mt * kBM + row;
-    const int my_i = seq_len - q_len + t;         // logical index of this query row
+    const int row = quarter * 32 + lane;          // query row within the slot tile == TMEM lane
+    const int t = mt_s[s] * kBM + row;
+    const int my_i = q_base + t;                  // logical index of this query row
     const uint32_t lane_base = uint32_t(quarter * 32) << 16;
+    const uint32_t tS = tmem + lane_base + s * 128;
+    const uint32_t tO = tmem + lane_base + 256 + s * 128;
     const float sl2 = a.scale_log2;
+    const bool live = s == 0 || slot1_live;
     float m_run = -CUDART_INF_F, l_run = 0.f;
-    float s[kBN];
     for (int j = 0; j < n_tiles; ++j) {
-      const int sb = j & 1, cs = j % kNC;
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
+      const int cs = j % kNC;
+      if (!live) {  // dead slot: still release the mask slot
+        mbar_wait(&c_full[cs], (j / kNC) & 1);
+        mbar_arrive(&c_empty[cs]);
+        continue;
+      }
+      float x[kBN];
+      mbar_wait(&s_full[s], j & 1);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < kBN / 32; ++c) tc_ld32(tmem + lane_base + sb * 128 + c * 32, s + c * 32);
-      tc_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&s_empty[sb]);
+      for (int c = 0; c < kBN / 32; ++c) tc_ld32(tS + c * 32, x + c * 32);
       mbar_wait(&c_full[cs], (j / kNC) & 1);
       const int32_t* col = sC + cs * (kBN + 4);
+      const bool all_vis = col[kBN] != 0;
+      tc_wait_ld();
       float mx = -CUDART_INF_F;
-      if (col[kBN]) {
+      if (all_vis) {
 #pragma unroll
-        for (int c = 0; c < kBN; ++c) {
-          s[c] *= sl2;
-          mx = fmaxf(mx, s[c]);
-        }
+        for (int c = 0; c < kBN; c += 2) mx = fmaxf(mx, fmaxf(x[c], x[c + 1]));
       } else {
 #pragma unroll
         for (int c = 0; c < kBN; c += 4) {
           const int4 ci = *reinterpret_cast<const int4*>(col + c);
-          s[c + 0] = ci.x <= my_i ? s[c + 0] * sl2 : -CUDART_INF_F;
-          s[c + 1] = ci.y <= my_i ? s[c + 1] * sl2 : -CUDART_INF_F;
-          s[c + 2] = ci.z <= my_i ? s[c + 2] * sl2 : -CUDART_INF_F;
-          s[c + 3] = ci.w <= my_i ? s[c + 3] * sl2 : -CUDART_INF_F;
-          mx = fmaxf(mx, fmaxf(fmaxf(s[c], s[c + 1]), fmaxf(s[c + 2], s[c + 3])));
+          x[c + 0] = ci.x <= my_i ? x[c + 0] : -CUDART_INF_F;
+          x[c + 1] = ci.y <= my_i ? x[c + 1] : -CUDART_INF_F;
+          x[c + 2] = ci.z <= my_i ? x[c + 2] : -CUDART_INF_F;
+          x[c + 3] = ci.w <= my_i ? x[c + 3] : -CUDART_INF_F;
+          mx = fmaxf(mx, fmaxf(fmaxf(x[c], x[c + 1]), fmaxf(x[c + 2], x[c + 3])));
         }
       }
       mbar_arrive(&c_empty[cs]);
+      mx *= sl2;
       // lazy rescale: move the running max only when it grows by > 2^8
       const bool grow = mx > m_run + kRescaleThreshold;
       const float m_new = grow ? mx : m_run;
       const float alpha = grow ? fast_exp2(m_run - m_new) : 1.f;
-      float rs = 0.f;
-#pragma unroll
-      for (int c = 0; c < kBN; ++c) {
-        s[c] = fast_exp2(s[c] - m_new);
-        rs += s[c];
-      }
-      l_run = l_run * alpha + rs;
       m_run = m_new;
-      // wait until PV_{j-1} has finished with P and O
-      if (j >= 1) mbar_wait(p_empty, (j - 1) & 1);
-      tc_fence_after();
-      if (j >= 1 && __any_sync(0xffffffffu, grow)) {
+      if (j > 0 && __any_sync(0xffffffffu, grow)) {  // O_s is settled: PV_s(j-1) completed before S_s(j)
         float o[32];
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
-          tc_ld32(tmem + lane_base + 256 + c * 32, o);
+          tc_ld32(tO + c * 32, o);
           tc_wait_ld();
 #pragma unroll
-          for (int x = 0; x < 32; ++x) o[x] *= alpha;
-          tc_st32(tmem + lane_base + 256 + c * 32, o);
+          for (int y = 0; y < 32; ++y) o[y] *= alpha;
+          tc_st32(tO + c * 32, reinterpret_cast<const uint32_t*>(o));
         }
-        tc_wait_st();
       }
-      // P (bf16) -> smem, K-major SW128: 64-key blocks, row = query row
+      float rs = 0.f;
+      uint32_t pk[kBN / 2];
 #pragma unroll
-      for (int c8 = 0; c8 < kBN / 8; ++c8) {
-        uint4 pk;
-        pk.x = pack_bf16(s[c8 * 8 + 0], s[c8 * 8 + 1]);
-        pk.y = pack_bf16(s[c8 * 8 + 2], s[c8 * 8 + 3]);
-        pk.z = pack_bf16(s[c8 * 8 + 4], s[c8 * 8 + 5]);
-        pk.w = pack_bf16(s[c8 * 8 + 6], s[c8 * 8 + 7]);
-        *reinterpret_cast<uint4*>(sP + (c8 >> 3) * (kBM * 128) + sw128(row, c8 & 7)) = pk;
+      for (int c = 0; c < kBN; c += 2) {
+        const float e0 = fast_exp2(fmaf(x[c], sl2, -m_new));
+        const float e1 = fast_exp2(fmaf(x[c + 1], sl2, -m_new));
+        rs += e0 + e1;
+        pk[c >> 1] = pack_bf16(e0, e1);
       }
-      fence_proxy_async_smem();
+      l_run = l_run * alpha + rs;
+      // P (bf16 pairs) over S: columns [128 s, 128 s + 64)
+      tc_st32(tS, pk);
+      tc_st32(tS + 32, pk + 32);
+      tc_wait_st();
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[s]);
     }
-    // epilogue: O / l -> bf16 -> global
-    mbar_wait(o_full, 0);
-    tc_fence_after();
-    const float inv = 1.f / l_run;
-    __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + (int64_t(a.q_off[b] + t) * a.Hq + hq) * D;
+    if (live) {
+      // epilogue: O / l -> bf16 -> global
+      mbar_wait(o_full, 0);
+      tc_fence_after();
+      const float inv = 1.f / l_run;
+      __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + (int64_t(a.q_off[b] + t) * a.Hq + hq_s[s]) * D;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      float o[32];
-      tc_ld32(tmem + lane_base + 256 + c * 32, o);
-      tc_wait_ld();
-      if (t < q_len) {
+      for (int c = 0; c < D / 32; ++c) {
+        float o[32];
+        tc_ld32(tO + c * 32, o);
+        tc_wait_ld();
+        if (t < q_len) {
 #pragma unroll
-        for (int x = 0; x < 32; x += 8) {
-          uint4 pk;
-          pk.x = pack_bf16(o[x + 0] * inv, o[x + 1] * inv);
-          pk.y = pack_bf16(o[x + 2] * inv, o[x + 3] * inv);
-          pk.z = pack_bf16(o[x + 4] * inv, o[x + 5] * inv);
-          pk.w = pack_bf16(o[x + 6] * inv, o[x + 7] * inv);
-          *reinterpret_cast<uint4*>(orow + c * 32 + x) = pk;
+          for (int y = 0; y < 32; y += 8) {
+            uint4 v;
+            v.x = pack_bf16(o[y + 0] * inv, o[y + 1] * inv);
+            v.y = pack_bf16(o[y + 2] * inv, o[y + 3] * inv);
+            v.z = pack_bf16(o[y + 4] * inv, o[y + 5] * inv);
+            v.w = pack_bf16(o[y + 6] * inv, o[y + 7] * inv);
+            *reinterpret_cast<uint4*>(orow + c * 32 + y) = v;
+          }
         }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
@@ -411,8 +450,11 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 template <int D>
 cudaError_t launch_prefill_d(const CUtensorMap& tm_q, const CUtensorMap& tm_k, const CUtensorMap& tm_v,
                              const PrefillArgs& a, cudaStream_t s, int* launches) {
-  dim3 grid((a.max_q_len + kBM - 1) / kBM, a.Hq, a.n_seqs);
-  prefill_kernel<D><<<grid, 192, PSmem<D>::kBytes, s>>>(tm_q, tm_k, tm_v, a);
+  const int mtiles = (a.max_q_len + kBM - 1) / kBM;
+  dim3 grid;
+  if ((a.G & 1) == 0) grid = dim3(mtiles, a.Hkv * (a.G / 2), a.n_seqs);
+  else grid = dim3((mtiles + 1) / 2, a.Hq, a.n_seqs);
+  prefill_kernel<D><<<grid, kThreads, PSmem<D>::kBytes, s>>>(tm_q, tm_k, tm_v, a);
   ++*launches;
   return cudaGetLastError();
 }

@@ -896,7 +896,7 @@ hpa_status_t hpa_prefill(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
   const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt(float(D));
   PrefillArgs a{c->dt, dmeta, dmeta + n_seqs, dmeta + 2 * n_seqs, out, n_seqs, Hq, c->cfg.num_kv_heads,
                 Hq / c->cfg.num_kv_heads, c->cfg.page_size, c->cfg.num_pages, layer, max_q,
-                scale * 1.4426950408889634f};
+                scale * 1.4426950408889634f, __builtin_ctz(uint32_t(c->cfg.page_size))};
   int launched = 0;
   cudaError_t e = launch_prefill(tm_q, c->tm_k_pre, c->tm_v_pre, a, D, s, &launched);
   c->launches += launched;
