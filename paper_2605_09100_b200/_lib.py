@@ -5,7 +5,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "libhpa.so")
+# HPA_LIB_PATH overrides the library (A/B experiments with variant builds)
+_LIB_PATH = os.environ.get("HPA_LIB_PATH") or os.path.join(_PKG, "libhpa.so")
 
 c_i32 = ctypes.c_int32
 c_i32p = ctypes.POINTER(ctypes.c_int32)

@@ -43,28 +43,34 @@ def _run(cmd, verbose):
     return r
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest_dep():
-        return LIB
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB) -> str:
+    """defines: extra -D flags (variant builds for A/B experiments go to `out`)."""
+    if not force and not defines and os.path.exists(out) and os.path.getmtime(out) >= _newest_dep():
+        return out
+    build_dir = BUILD if not defines else BUILD + "_" + "_".join(d.replace("=", "") for d in defines)
+    os.makedirs(build_dir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    common += [f"-D{d}" for d in defines]
     jobs = []
     for f in CU_SOURCES:
-        obj = os.path.join(BUILD, f + ".o")
+        obj = os.path.join(build_dir, f + ".o")
         jobs.append(([NVCC, *ARCH, *common, "-lineinfo", "-Xptxas", "-v", "--expt-relaxed-constexpr",
                       "-c", os.path.join(CSRC, f), "-o", obj], obj))
     for f in CPP_SOURCES:
-        obj = os.path.join(BUILD, f + ".o")
+        obj = os.path.join(build_dir, f + ".o")
         jobs.append(([NVCC, *common, "-x", "c++", "-c", os.path.join(CSRC, f), "-o", obj], obj))
     with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
         results = list(ex.map(lambda j: _run(j[0], verbose), jobs))
-    with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
+    with open(os.path.join(build_dir, "ptxas.log"), "w") as f:
         for (cmd, _), r in zip(jobs, results):
             f.write(f"## {cmd[-3]}\n{r.stderr}\n")
-    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB + ".tmp", *[o for _, o in jobs]], verbose)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out + ".tmp", *[o for _, o in jobs]], verbose)
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs,
+                out=outs[0] if outs else LIB))

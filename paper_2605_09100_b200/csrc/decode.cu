@@ -16,8 +16,9 @@
 //    packed into the M dimension (rows 0..G-1 valid), an online softmax in the
 //    log2 domain (ex2.approx), and P rounded to bf16 for the PV product.
 //  * consumers merge their (m, l, O) through shared memory; with one split the
-//    CTA writes bf16 output directly, otherwise fp32 partials + LSE for the
-//    combine kernel (a5).
+//    CTA writes bf16 output directly, otherwise fp32 partials + LSE, and the
+//    last split CTA of each (request, kv-head) to finish (atomic counter)
+//    performs the LSE-weighted combine (a5) in the same launch.
 //  * rows >= valid_rows of a partial page are masked to -inf; the pool is
 //    zero-initialised so those rows are always finite (0 * finite = 0).
 #include "hpa_kernels.h"
@@ -31,6 +32,12 @@ namespace {
 constexpr int kChunk = 16;  // rows per pipeline chunk (one m16n8k16 K-step of keys)
 constexpr int kNCons = 4;   // consumer warps per CTA
 constexpr int kNSt = 8;     // ring depth
+#ifndef HPA_FENCE_MODE
+#define HPA_FENCE_MODE 2  // 0: fence.sc (threadfence), 1: fence.acq_rel, 2: atom.acq_rel
+#endif
+#ifndef HPA_FUSED_COMBINE
+#define HPA_FUSED_COMBINE 0  // 1: a5 by the last split CTA (atomic + GPU fence: measured slower)
+#endif
 
 template <int D>
 struct DecodeSmem {
@@ -56,7 +63,6 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_const
 
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int seq = a.seq_rows[b];
   const int G = a.G;
 
   if (threadIdx.x == 0) {
@@ -68,6 +74,8 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_const
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
   }
+  grid_dependency_wait();  // PDL: everything above overlapped the previous kernel
+  const int seq = a.seq_rows[b];
   // q rows of this kv-head's group -> swizzled smem tile [16][D]; rows >= G are 0.
   {
     const __nv_bfloat16* qg = static_cast<const __nv_bfloat16*>(a.q) + (int64_t(b) * a.Hq + int64_t(h) * G) * D;
@@ -269,13 +277,73 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_const
       if (dcol == 0) a.lse_part[pi] = Ls > 0.f ? M + __log2f(Ls) : -CUDART_INF_F;
     }
   }
+  if (a.splits == 1 || !HPA_FUSED_COMBINE) return;
+  // ------------------------------------------------ a5: the last split of (b, h) combines
+  //   O = sum_s 2^(lse_s - LSE) O_s / sum_s 2^(lse_s - LSE)   (fp32, log2 domain)
+  named_bar_sync(1, kNT);  // every consumer's partial writes precede thread 0's release
+  if (tid == 0) {
+    // release our partials / acquire everyone else's (the last arrival reads them)
+    int prev;
+#if HPA_FENCE_MODE == 0
+    __threadfence();
+    prev = atomicAdd(&a.counters[b * a.Hkv + h], 1);
+    __threadfence();
+#elif HPA_FENCE_MODE == 1
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    prev = atomicAdd(&a.counters[b * a.Hkv + h], 1);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#else
+    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(prev) : "l"(&a.counters[b * a.Hkv + h]) : "memory");
+#endif
+    cmeta[0] = prev == a.splits - 1 ? 1 : 0;
+  }
+  named_bar_sync(1, kNT);
+  if (cmeta[0] == 0) return;
+  const int S = a.splits;
+  float* wts = mo;  // [G][S] normalised split weights (ring memory is free now)
+  const int64_t pbase = (int64_t(b) * a.Hq + h * G) * S;
+  for (int i = tid; i < G * S; i += kNT) wts[i] = __ldcg(a.lse_part + pbase + i);
+  named_bar_sync(1, kNT);
+  if (tid < G) {
+    float M = -CUDART_INF_F, W = 0.f;
+    for (int sp = 0; sp < S; ++sp) M = fmaxf(M, wts[tid * S + sp]);
+    for (int sp = 0; sp < S; ++sp) {
+      const float ls = wts[tid * S + sp];
+      const float w = ls == -CUDART_INF_F ? 0.f : fast_exp2(ls - M);
+      wts[tid * S + sp] = w;
+      W += w;
+    }
+    const float inv = 1.f / W;
+    for (int sp = 0; sp < S; ++sp) wts[tid * S + sp] *= inv;
+  }
+  named_bar_sync(1, kNT);
+  for (int idx = tid; idx < G * (D / 4); idx += kNT) {
+    const int g = idx / (D / 4), d4 = idx % (D / 4);
+    const float4* src = reinterpret_cast<const float4*>(a.o_part + (pbase + int64_t(g) * S) * D) + d4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int sp = 0; sp < S; ++sp) {
+      const float w = wts[g * S + sp];
+      const float4 o = __ldcg(src + int64_t(sp) * (D / 4));
+      acc.x += w * o.x;
+      acc.y += w * o.y;
+      acc.z += w * o.z;
+      acc.w += w * o.w;
+    }
+    uint2 pk;
+    pk.x = pack_bf16(acc.x, acc.y);
+    pk.y = pack_bf16(acc.z, acc.w);
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + (int64_t(b) * a.Hq + h * G + g) * D + d4 * 4) = pk;
+  }
+  if (tid == 0) a.counters[b * a.Hkv + h] = 0;  // ready for the next call (stream order)
 }
 
-// a5: O = sum_s 2^(lse_s - LSE) O_s, LSE = log2 sum_s 2^lse_s  (fp32).
+// a5 as a separate kernel (HPA_FUSED_COMBINE=0): one CTA per (request, q-head).
 template <int D>
 __global__ void __launch_bounds__(D) combine_kernel(const float* __restrict__ o_part,
                                                     const float* __restrict__ lse, __nv_bfloat16* out,
                                                     int S) {
+  grid_dependency_wait();
   const int64_t bh = blockIdx.x;
   const float* ls = lse + bh * S;
   float M = -CUDART_INF_F;
@@ -293,15 +361,14 @@ template <int D>
 cudaError_t launch_decode_d(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,
                             cudaStream_t s, int* launches) {
   const int smem = DecodeSmem<D>::kBytes;
-  dim3 grid(a.splits, a.Hkv, a.n_seqs);
-  decode_split_kernel<D><<<grid, (kNCons + 1) * 32, smem, s>>>(tm_k, tm_v, a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(decode_split_kernel<D>, dim3(a.splits, a.Hkv, a.n_seqs), dim3((kNCons + 1) * 32),
+                             smem, s, tm_k, tm_v, a);
   if (e != cudaSuccess) return e;
   ++*launches;
-  if (a.splits > 1) {
-    combine_kernel<D><<<a.n_seqs * a.Hq, D, 0, s>>>(a.o_part, a.lse_part,
-                                                    static_cast<__nv_bfloat16*>(a.out), a.splits);
-    e = cudaGetLastError();
+  if (a.splits > 1 && !HPA_FUSED_COMBINE) {
+    e = launch_pdl(combine_kernel<D>, dim3(a.n_seqs * a.Hq), dim3(D), 0, s,
+                   static_cast<const float*>(a.o_part), static_cast<const float*>(a.lse_part),
+                   static_cast<__nv_bfloat16*>(a.out), a.splits);
     ++*launches;
   }
   return e;

@@ -54,6 +54,21 @@ cudaError_t launch_scatter(const PoolGeom& g, int32_t* arena, const WordWrite* w
                            int32_t n_words, const ScatterRecord* recs, int32_t n_recs,
                            const int32_t* slots, int64_t max_rows_per_rec, cudaStream_t s);
 
+// Small metadata shipped as kernel parameters instead of an H2D copy (the
+// common decode-step append): table words (2 ints each) then slots (1 int
+// each), at most kInlineInts ints, and at most one record.
+constexpr int kInlineInts = 1536;
+struct InlineMeta {
+  int32_t n_words;
+  int32_t n_slots;
+  int32_t has_rec;
+  int32_t pad;
+  ScatterRecord rec;
+  int32_t data[kInlineInts];
+};
+cudaError_t launch_scatter_inline(const PoolGeom& g, int32_t* arena, const InlineMeta& m, int64_t max_rows,
+                                  cudaStream_t s);
+
 // Logical K/V export of one (layer, seq): out bf16 [H_kv][len][d].
 cudaError_t launch_export(const PoolGeom& g, DevTables t, int32_t layer, int32_t seq,
                           int32_t n_entries_host, void* k_out, void* v_out, cudaStream_t s);
@@ -65,6 +80,7 @@ struct DecodeArgs {
   void* out;                // bf16 [n][Hq][d]
   float* o_part;            // fp32 [n][Hq][S][d]   (S > 1)
   float* lse_part;          // fp32 [n][Hq][S]      (log2 domain)
+  int32_t* counters;        // [n][Hkv] zero; split-arrival counters for the fused combine
   int32_t n_seqs, Hq, Hkv, G, P, NP, layer, splits;
   float scale_log2;         // softmax_scale * log2(e)
 };

@@ -11,12 +11,14 @@
 // Design (sm_100a; roofline: bf16 tensor pipe):
 //  * CTA = two 128-row query tiles ("slots") that share every K/V tile: two
 //    q-heads of the same GQA group over the same token rows (G even), or two
-//    consecutive row tiles of one head (G odd). 320 threads:
+//    consecutive row tiles of one head (G odd). 384 threads = 3 warpgroups:
 //      warps 0-3  softmax warpgroup for slot 0 (one TMEM lane = one row)
 //      warps 4-7  softmax warpgroup for slot 1
 //      warp  8    TMA producer (all lanes build the mask indices; the page
 //                 boxes are issued in parallel by several lanes)
-//      warp  9    tcgen05 MMA issuer; owns the 512 TMEM columns.
+//      warp  9    tcgen05 MMA issuer; owns the 512 TMEM columns
+//      warps 10-11 spare. setmaxnreg moves registers from warpgroup 2 (64)
+//                 to the softmax warpgroups (224).
 //  * TMEM: S_s / P_s at columns [128 s, 128 s + 128), O_s at [256 + 128 s, ...).
 //    S = Q K^T (SS: Q and K K-major, 128-B swizzle); the softmax writes P as
 //    packed bf16 over S and O += P V runs in TS form (A = P from TMEM, B = V
@@ -43,10 +45,27 @@ constexpr int kBN = 128;   // key slots per tile
 constexpr int kNK = 2;     // K ring depth
 constexpr int kNV = 2;     // V ring depth
 constexpr int kNC = 4;     // mask-index ring depth
-constexpr int kThreads = 320;
+constexpr int kThreads = 384;      // 3 warpgroups: softmax 0, softmax 1, producer / MMA / 2 spare
 constexpr int kProducerWarp = 8;
 constexpr int kMmaWarp = 9;
+#ifndef HPA_SOFTMAX_REGS
+#define HPA_SOFTMAX_REGS 216
+#endif
+#ifndef HPA_OTHER_REGS
+#define HPA_OTHER_REGS 72
+#endif
+// setmaxnreg: the launch allocates 168 regs/thread (384 threads), so the two
+// softmax warpgroups may grow only by what warpgroup 2 gives up: 2 S + O <= 3 x 168.
+constexpr int kSoftmaxRegs = HPA_SOFTMAX_REGS;
+constexpr int kOtherRegs = HPA_OTHER_REGS;
+static_assert(2 * kSoftmaxRegs + kOtherRegs <= 3 * 168, "setmaxnreg budget");
 constexpr float kRescaleThreshold = 8.0f;  // log2 units (factor 256)
+#ifndef HPA_POLY_EVERY
+#define HPA_POLY_EVERY 0  // 1 of every N exp2 pairs on the FMA pipe (0 = all on MUFU; measured best)
+#endif
+#ifndef HPA_PV_SPLIT
+#define HPA_PV_SPLIT 1    // publish P in two 64-key halves (PV starts on the first half)
+#endif
 
 template <int D>
 struct PSmem {
@@ -57,9 +76,9 @@ struct PSmem {
   static constexpr int oV = oK + kNK * kKV;
   static constexpr int oC = oV + kNV * kKV;              // int32 [kNC][kBN + 4] (kBN = all-visible flag)
   static constexpr int oBar = oC + kNC * (kBN + 4) * 4;
-  // q_full, k_full[NK], k_empty[NK], v_full[NV], v_empty[NV], s_full[2], p_full[2], o_full,
-  // c_full[NC], c_empty[NC]
-  static constexpr int kNBar = 1 + 2 * kNK + 2 * kNV + 2 + 2 + 1 + 2 * kNC;
+  // q_full, k_full[NK], k_empty[NK], v_full[NV], v_empty[NV], s_full[2], p_full[2 slots][2 halves],
+  // o_full, c_full[NC], c_empty[NC]
+  static constexpr int kNBar = 1 + 2 * kNK + 2 * kNV + 2 + 4 + 1 + 2 * kNC;
   static constexpr int oMisc = oBar + kNBar * 8;
   static constexpr int kRaw = oMisc + 16 + 1024;
   // >= 116 KB so exactly one CTA is resident per SM (it owns all 512 TMEM columns)
@@ -122,6 +141,47 @@ __device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t* r) {
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// ---- packed fp32x2 arithmetic (FFMA2 / FADD2) and a polynomial exp2
+__device__ __forceinline__ uint64_t f2_as_u64(float2 v) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+__device__ __forceinline__ float2 u64_as_f2(uint64_t r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)), "l"(f2_as_u64(c)));
+  return u64_as_f2(d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  uint64_t d;
+  asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)));
+  return u64_as_f2(d);
+}
+// 2^x for x <= 0 on the FMA pipe: x = j + f, j = round(x), f in [-0.5, 0.5];
+// 2^f by a degree-3 minimax polynomial (max rel. error 1.0e-4 < bf16's 2^-9),
+// 2^j by adding j to the exponent field. x < -126 flushes towards 0.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  const float2 lo = make_float2(-126.f, -126.f);
+  x.x = fmaxf(x.x, lo.x);
+  x.y = fmaxf(x.y, lo.y);
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23: round to integer
+  const float2 t = fadd2(x, magic);
+  const float2 j = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = fadd2(x, make_float2(-j.x, -j.y));
+  float2 p = ffma2(f, make_float2(0.05499337f, 0.05499337f), make_float2(0.242211f, 0.242211f));
+  p = ffma2(f, p, make_float2(0.6932861f, 0.6932861f));
+  p = ffma2(f, p, make_float2(1.f, 1.f));
+  float2 r;
+  r.x = __int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23));
+  r.y = __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23));
+  return r;
+}
+
 // Shared-memory matrix descriptor: start >> 4 (bits 0-13), LBO >> 4 (16-29),
 // SBO >> 4 (32-45), version 1 (46-47), layout SWIZZLE_128B = 2 (61-63).
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -146,6 +206,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   using L = PSmem<D>;
   constexpr int kHalves = D / 64;
   const int b = blockIdx.z;
+  grid_dependency_wait();  // PDL
   const int q_len = a.q_len[b];
   // slot -> (q-head, row tile)
   int hq_s[2], mt_s[2];
@@ -177,7 +238,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   uint64_t* v_empty = v_full + kNV;
   uint64_t* s_full = v_empty + kNV;
   uint64_t* p_full = s_full + 2;
-  uint64_t* o_full = p_full + 2;
+  uint64_t* o_full = p_full + 4;
   uint64_t* c_full = o_full + 1;
   uint64_t* c_empty = c_full + kNC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::oMisc);
@@ -201,7 +262,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     mbar_init(q_full, 1);
     for (int i = 0; i < kNK; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
     for (int i = 0; i < kNV; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 128); }
+    for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&p_full[i], 128);
     mbar_init(o_full, 1);
     for (int i = 0; i < kNC; ++i) { mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], 256); }
     fence_barrier_init();
@@ -225,6 +287,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   const uint32_t tmem = *tmem_slot;
   const int n_tiles = *ntiles_slot;
 
+  if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kOtherRegs));
   if (warp == kProducerWarp) {
     // ================================================================ producer
     if (lane == 0) {
@@ -308,10 +371,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         }
         tc_commit(&s_full[s]);
       };
-      auto issue_pv = [&](int s, int jj) {
+      auto issue_pv_half = [&](int s, int jj, int half) {
         const int vs = jj % kNV;
 #pragma unroll
-        for (int k = 0; k < kBN / 16; ++k) {
+        for (int k = half * 4; k < half * 4 + 4; ++k) {
           const uint64_t bd = sdesc(aV + vs * L::kKV + k * 2048, kBN * 128, 1024);
           tc_mma_ts(tmem + 256 + s * 128, tmem + s * 128 + k * 8, bd, idO, (jj > 0 || k > 0) ? 1u : 0u);
         }
@@ -325,9 +388,13 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         if (more) mbar_wait(&k_full[(j + 1) % kNK], ((j + 1) / kNK) & 1);
         mbar_wait(&v_full[j % kNV], (j / kNV) & 1);
         for (int s = 0; s < nslot; ++s) {
-          mbar_wait(&p_full[s], j & 1);
+          // PV over keys 0..63 as soon as the first half of P is in TMEM, then 64..127
+          mbar_wait(&p_full[2 * s], j & 1);
           tc_fence_after();
-          issue_pv(s, j);
+          issue_pv_half(s, j, 0);
+          mbar_wait(&p_full[2 * s + 1], j & 1);
+          tc_fence_after();
+          issue_pv_half(s, j, 1);
           if (s == nslot - 1) tc_commit(&v_empty[j % kNV]);
           if (more) issue_s(s, j + 1);  // overwrites S/P s after PV s has read P (in-order pipe)
         }
@@ -335,8 +402,9 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
       tc_commit(o_full);
     }
-  } else {
+  } else if (warp < 8) {
     // ================================================================ softmax (slot = warp / 4)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
     const int s = warp >> 2;
     const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;          // query row within the slot tile == TMEM lane
@@ -397,22 +465,36 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           tc_st32(tO + c * 32, reinterpret_cast<const uint32_t*>(o));
         }
       }
-      float rs = 0.f;
-      uint32_t pk[kBN / 2];
+      // p = 2^(x*sl2 - m): f32x2 FFMA for the argument; 3 of every 4 pairs on the
+      // MUFU ex2 unit, 1 pair on the FMA pipe (degree-3 polynomial, rel. err 1e-4)
+      const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_new, -m_new);
+      float2 rs2 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int c = 0; c < kBN; c += 2) {
-        const float e0 = fast_exp2(fmaf(x[c], sl2, -m_new));
-        const float e1 = fast_exp2(fmaf(x[c + 1], sl2, -m_new));
-        rs += e0 + e1;
-        pk[c >> 1] = pack_bf16(e0, e1);
+      for (int half = 0; half < 2; ++half) {
+        uint32_t pk[kBN / 4];
+#pragma unroll
+        for (int c = half * 64; c < half * 64 + 64; c += 2) {
+          const float2 arg = ffma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
+          float2 e;
+          if (HPA_POLY_EVERY > 0 && ((c >> 1) % (HPA_POLY_EVERY > 0 ? HPA_POLY_EVERY : 1)) == HPA_POLY_EVERY - 1) {
+            e = exp2_poly2(arg);
+          } else {
+            e.x = fast_exp2(arg.x);
+            e.y = fast_exp2(arg.y);
+          }
+          rs2 = fadd2(rs2, e);
+          pk[(c - half * 64) >> 1] = pack_bf16(e.x, e.y);
+        }
+        // P (bf16 pairs) over S: keys [64 half, 64 half + 64) -> columns [128 s + 32 half, +32)
+        tc_st32(tS + half * 32, pk);
+        if (HPA_PV_SPLIT || half == 1) {
+          tc_wait_st();
+          tc_fence_before();
+          if (!HPA_PV_SPLIT) mbar_arrive(&p_full[2 * s]);
+          mbar_arrive(&p_full[2 * s + half]);
+        }
       }
-      l_run = l_run * alpha + rs;
-      // P (bf16 pairs) over S: columns [128 s, 128 s + 64)
-      tc_st32(tS, pk);
-      tc_st32(tS + 32, pk + 32);
-      tc_wait_st();
-      tc_fence_before();
-      mbar_arrive(&p_full[s]);
+      l_run = l_run * alpha + (rs2.x + rs2.y);
     }
     if (live) {
       // epilogue: O / l -> bf16 -> global
@@ -454,9 +536,8 @@ cudaError_t launch_prefill_d(const CUtensorMap& tm_q, const CUtensorMap& tm_k, c
   dim3 grid;
   if ((a.G & 1) == 0) grid = dim3(mtiles, a.Hkv * (a.G / 2), a.n_seqs);
   else grid = dim3((mtiles + 1) / 2, a.Hq, a.n_seqs);
-  prefill_kernel<D><<<grid, kThreads, PSmem<D>::kBytes, s>>>(tm_q, tm_k, tm_v, a);
   ++*launches;
-  return cudaGetLastError();
+  return launch_pdl(prefill_kernel<D>, grid, dim3(kThreads), PSmem<D>::kBytes, s, tm_q, tm_k, tm_v, a);
 }
 
 }  // namespace

@@ -283,6 +283,7 @@ struct hpa_cache {
   // decode partials
   float* o_part = nullptr;
   float* lse_part = nullptr;
+  int32_t* counters = nullptr;  // [max_seqs][H_kv], zero between calls
   size_t part_elems = 0;
   int32_t forced_splits = 0;
   int num_sms = 148;
@@ -325,15 +326,15 @@ struct hpa_cache {
     while (first < n && first < int32_t(q.pages.size()) && q.pages[first] == pages[first] &&
            q.pos0[first] == pos0[first] && q.meta[first] == meta[first])
       ++first;
-    for (int32_t e = first; e < n; ++e) {
-      pending.push_back({int32_t(idx(s, e)), pages[e]});
-      pending.push_back({int32_t(off_pos0() + idx(s, e)), pos0[e]});
-      pending.push_back({int32_t(off_meta() + idx(s, e)), meta[e]});
+    const int32_t old_n = int32_t(q.pages.size());
+    for (int32_t e = first; e < n; ++e) {  // only the fields that changed
+      const bool fresh = e >= old_n;
+      if (fresh || q.pages[e] != pages[e]) pending.push_back({int32_t(idx(s, e)), pages[e]});
+      if (fresh || q.pos0[e] != pos0[e]) pending.push_back({int32_t(off_pos0() + idx(s, e)), pos0[e]});
+      if (fresh || q.meta[e] != meta[e]) pending.push_back({int32_t(off_meta() + idx(s, e)), meta[e]});
     }
-    if (q.len != pos || int32_t(q.pages.size()) != n) {
-      pending.push_back({int32_t(off_len() + s), pos});
-      pending.push_back({int32_t(off_nent() + s), n});
-    }
+    if (q.len != pos) pending.push_back({int32_t(off_len() + s), pos});
+    if (int32_t(q.pages.size()) != n) pending.push_back({int32_t(off_nent() + s), n});
     q.pages.swap(pages);
     q.pos0.swap(pos0);
     q.meta.swap(meta);
@@ -368,6 +369,23 @@ hpa_status_t ship(hpa_cache_t* c, cudaStream_t s, const std::vector<ScatterRecor
       else c->pending[w++] = c->pending[r];
     }
     c->pending.resize(w);
+  }
+  if (recs.size() <= 1 && 2 * c->pending.size() + slots.size() <= size_t(kInlineInts)) {
+    InlineMeta m;
+    m.n_words = int32_t(c->pending.size());
+    m.n_slots = int32_t(slots.size());
+    m.has_rec = recs.empty() ? 0 : 1;
+    m.pad = 0;
+    if (!recs.empty()) m.rec = recs[0];
+    for (size_t i = 0; i < c->pending.size(); ++i) {
+      m.data[2 * i] = c->pending[i].idx;
+      m.data[2 * i + 1] = c->pending[i].val;
+    }
+    if (!slots.empty()) std::memcpy(m.data + 2 * c->pending.size(), slots.data(), slots.size() * 4);
+    HPA_CUDA(launch_scatter_inline(c->geom(), c->arena, m, max_rows, s));
+    c->launches += 1;
+    c->pending.clear();
+    return HPA_OK;
   }
   Blob b;
   const size_t o_words = b.add(c->pending.data(), c->pending.size());
@@ -509,6 +527,7 @@ hpa_status_t hpa_cache_create(const hpa_config_t* cfg, hpa_cache_t** out) {
     if (c->k_pool) cudaFree(c->k_pool);
     if (c->v_pool) cudaFree(c->v_pool);
     if (c->arena) cudaFree(c->arena);
+    if (c->counters) cudaFree(c->counters);
     c->ring.destroy();
   };
   cudaError_t e;
@@ -525,6 +544,11 @@ hpa_status_t hpa_cache_create(const hpa_config_t* cfg, hpa_cache_t** out) {
       (e = c->ring.init(size_t(64) << 20)) != cudaSuccess) {
     cleanup();
     return cuda_fail(e, "table allocation");
+  }
+  if ((e = cudaMalloc(&c->counters, size_t(g.max_seqs) * g.num_kv_heads * 4)) != cudaSuccess ||
+      (e = cudaMemset(c->counters, 0, size_t(g.max_seqs) * g.num_kv_heads * 4)) != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "counter allocation");
   }
   c->dt = DevTables{c->arena, c->arena + c->off_pos0(), c->arena + c->off_meta(), c->arena + c->off_len(),
                     c->arena + c->off_nent(), g.max_pages_per_seq};
@@ -557,6 +581,7 @@ hpa_status_t hpa_cache_destroy(hpa_cache_t* c) {
   if (c->batch_dev) cudaFree(c->batch_dev);
   if (c->o_part) cudaFree(c->o_part);
   if (c->lse_part) cudaFree(c->lse_part);
+  if (c->counters) cudaFree(c->counters);
   c->ring.destroy();
   delete c;
   return HPA_OK;
@@ -816,6 +841,7 @@ hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int
   if (layer < 0 || layer >= c->cfg.num_layers) return fail(HPA_ERR_INVALID_ARG, "layer %d out of range", layer);
   if (n_seqs < 0) return fail(HPA_ERR_INVALID_ARG, "n_seqs < 0");
   if (n_seqs == 0) return HPA_OK;
+  if (n_seqs > c->cfg.max_seqs) return fail(HPA_ERR_INVALID_ARG, "n_seqs > max_seqs");
   if (!seq_ids || !q || !out) return fail(HPA_ERR_INVALID_ARG, "null argument");
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15)
     return fail(HPA_ERR_INVALID_ARG, "q / out must be 16-byte aligned");
@@ -846,7 +872,7 @@ hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int
     }
   }
   const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt(float(D));
-  DecodeArgs a{c->dt, c->batch_dev, q, out, c->o_part, c->lse_part, n_seqs, Hq, c->cfg.num_kv_heads,
+  DecodeArgs a{c->dt, c->batch_dev, q, out, c->o_part, c->lse_part, c->counters, n_seqs, Hq, c->cfg.num_kv_heads,
                Hq / c->cfg.num_kv_heads, c->cfg.page_size, c->cfg.num_pages, layer, S,
                scale * 1.4426950408889634f};
   int launched = 0;
