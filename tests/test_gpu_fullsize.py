@@ -1,0 +1,127 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times, on sampled outputs the oracle computes one by one.
+
+configs[1]: B=64 decode, 8 x 128 latent rows + 4096 token rows (Lb = 5120),
+            split planner as in the bench; 4 sampled requests, all 32 heads.
+configs[2]: chunked prefill C=2048 over 1024 latent + 16384 cached token rows;
+            48 sampled query rows (first/last/ragged positions), all 32 heads.
+configs[3]: B=256 LMAG step (batched latent replacement + append + decode);
+            4 sampled requests.
+Sampled requests are drawn on the CPU (workloads.Draw); the rest of the batch
+is filled with GPU-drawn data of the same distribution (it only shapes the
+launch; its outputs are checked for finiteness)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import OracleCache, attend
+from tests.hpa_testutil import check_close, f64
+from workloads import LATENT_ROWS, Draw, qwen3_8b_shape
+
+pytestmark = pytest.mark.gpu
+
+
+def _build(cache, orc, shape, n_req, sampled, docs, tokens, seed):
+    """Builds n_req requests; the `sampled` ones with CPU draws mirrored in the oracle."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    seqs = [cache.seq_create() for _ in range(n_req)]
+    draws = {}
+    for s in sampled:
+        orc.create_seq(seqs[s])
+        draws[s] = Draw(seed + 100 + s)
+    for _ in range(docs):
+        kvs = []
+        for s in range(n_req):
+            if s in draws:
+                kv = draws[s].latent(shape, LATENT_ROWS)
+                orc.install(seqs[s], -1, f64(kv))
+                kvs.append(kv.cuda())
+            else:
+                kvs.append(torch.randn((1, 2, LATENT_ROWS, 8, 128), generator=g, device="cuda").to(torch.bfloat16))
+        cache.latent_install_batch(seqs, [-1] * n_req, kvs)
+    ks, vs = [], []
+    for s in range(n_req):
+        if s in draws:
+            k, v = draws[s].tokens(shape, tokens)
+            orc.append(seqs[s], f64(k), f64(v))
+            ks.append(k.cuda())
+            vs.append(v.cuda())
+        else:
+            ks.append(torch.randn((1, tokens, 8, 128), generator=g, device="cuda").to(torch.bfloat16))
+            vs.append(torch.randn((1, tokens, 8, 128), generator=g, device="cuda").to(torch.bfloat16))
+    cache.append_kv(seqs, [tokens] * n_req, torch.cat(ks, 1), torch.cat(vs, 1))
+    return seqs, draws
+
+
+def test_decode_config1_full_size_sampled():
+    from paper_2605_09100_b200 import Cache
+    shape = qwen3_8b_shape(16)
+    B, sampled = 64, [0, 17, 42, 63]
+    cache = Cache(1, 32, 8, 128, 16, B * 330, B, 330, 0, 99)
+    orc = OracleCache(1, 32, 8, 128, 16)
+    seqs, draws = _build(cache, orc, shape, B, sampled, 8, 4096, 2024)
+    q = torch.randn((B, 32, 128), device="cuda").to(torch.bfloat16)
+    qs = Draw(7).queries(shape, len(sampled))
+    for i, s in enumerate(sampled):
+        q[s] = qs[i].cuda()
+    out = cache.decode(0, seqs, q)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    ref = np.stack([attend(f64(qs[i:i + 1]), *orc.logical_kv(seqs[s], 0), shape.scale)[0]
+                    for i, s in enumerate(sampled)])
+    check_close(out[sampled], ref, "configs[1] decode sampled")
+    cache.close()
+
+
+def test_prefill_config2_full_size_sampled():
+    from paper_2605_09100_b200 import Cache
+    shape = qwen3_8b_shape(16)
+    C, prior = 2048, 16384
+    cache = Cache(1, 32, 8, 128, 16, 1300, 1, 1300, 0, 99)
+    orc = OracleCache(1, 32, 8, 128, 16)
+    seqs, draws = _build(cache, orc, shape, 1, [0], 8, prior + C, 77)
+    q = Draw(8).queries(shape, C)
+    out = cache.prefill(0, seqs, [C], q.cuda())
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    k, v = orc.logical_kv(seqs[0], 0)
+    lb = k.shape[1]
+    rows = sorted(set([0, 1, 127, 128, 255, 1000, 1023, 1024, 2046, 2047] +
+                      list(np.random.default_rng(3).integers(0, C, 38))))
+    ref = np.stack([attend(f64(q[t:t + 1]), k[:, :lb - C + t + 1], v[:, :lb - C + t + 1], shape.scale)[0]
+                    for t in rows])
+    check_close(out[rows], ref, "configs[2] prefill sampled rows")
+    cache.close()
+
+
+def test_lmag_config3_full_size_sampled():
+    from paper_2605_09100_b200 import Cache
+    shape = qwen3_8b_shape(16)
+    B, sampled = 256, [0, 100, 200, 255]
+    cache = Cache(1, 32, 8, 128, 16, B * 330, B, 330, 0, 99)
+    orc = OracleCache(1, 32, 8, 128, 16)
+    seqs, draws = _build(cache, orc, shape, B, sampled, 8, 4095, 555)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    for step in range(2):
+        sid = step % 8
+        kvs = []
+        for s in range(B):
+            if s in draws:
+                kv = draws[s].latent(shape, LATENT_ROWS)
+                orc.install(seqs[s], sid, f64(kv))
+                kvs.append(kv.cuda())
+            else:
+                kvs.append(torch.randn((1, 2, LATENT_ROWS, 8, 128), generator=g, device="cuda").to(torch.bfloat16))
+        cache.latent_install_batch(seqs, [sid] * B, kvs)
+        step_draw = Draw(900 + step)                   # CPU draws for everything the oracle sees
+        kn, vn = step_draw.tokens(shape, B)            # [1][B][8][128]: one new row per request
+        cache.append_kv(seqs, [1] * B, kn.cuda(), vn.cuda())
+        for s in sampled:
+            orc.append(seqs[s], f64(kn[:, s:s + 1]), f64(vn[:, s:s + 1]))
+        q = step_draw.queries(shape, B)
+        out = cache.decode(0, seqs, q.cuda())
+        torch.cuda.synchronize()
+        assert torch.isfinite(out.float()).all()
+        ref = np.stack([attend(f64(q[s:s + 1]), *orc.logical_kv(seqs[s], 0), shape.scale)[0] for s in sampled])
+        check_close(out[sampled], ref, f"configs[3] LMAG step {step}")
+    cache.close()
