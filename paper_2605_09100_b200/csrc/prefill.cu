@@ -263,9 +263,9 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     for (int i = 0; i < kNK; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
     for (int i = 0; i < kNV; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
     for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
-    for (int i = 0; i < 4; ++i) mbar_init(&p_full[i], 128);
+    for (int i = 0; i < 4; ++i) mbar_init(&p_full[i], 4);  // one arrive per softmax warp
     mbar_init(o_full, 1);
-    for (int i = 0; i < kNC; ++i) { mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], 256); }
+    for (int i = 0; i < kNC; ++i) { mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], 8); }
     fence_barrier_init();
     // key tiles needed: the tile holding the slot of logical index i_max
     int lo = 0, hi = n_ent - 1;  // last entry with pos0 <= i_max
@@ -420,7 +420,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const int cs = j % kNC;
       if (!live) {  // dead slot: still release the mask slot
         mbar_wait(&c_full[cs], (j / kNC) & 1);
-        mbar_arrive(&c_empty[cs]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&c_empty[cs]);
         continue;
       }
       float x[kBN];
@@ -447,7 +448,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           mx = fmaxf(mx, fmaxf(fmaxf(x[c], x[c + 1]), fmaxf(x[c + 2], x[c + 3])));
         }
       }
-      mbar_arrive(&c_empty[cs]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&c_empty[cs]);
       mx *= sl2;
       // lazy rescale: move the running max only when it grows by > 2^8
       const bool grow = mx > m_run + kRescaleThreshold;
@@ -490,8 +492,11 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         if (HPA_PV_SPLIT || half == 1) {
           tc_wait_st();
           tc_fence_before();
-          if (!HPA_PV_SPLIT) mbar_arrive(&p_full[2 * s]);
-          mbar_arrive(&p_full[2 * s + half]);
+          __syncwarp();
+          if (lane == 0) {
+            if (!HPA_PV_SPLIT) mbar_arrive(&p_full[2 * s]);
+            mbar_arrive(&p_full[2 * s + half]);
+          }
         }
       }
       l_run = l_run * alpha + (rs2.x + rs2.y);
