@@ -130,6 +130,23 @@ class Cache:
                                                _stream(self.device, stream), _p32(out)))
         return out.tolist()
 
+    def latent_install_packed(self, seq_ids, set_ids, kv: torch.Tensor, stream=None) -> np.ndarray:
+        """Batched install from one packed payload kv bf16 [n][L][2][m][H_kv][d] (payload i
+        installs into seq_ids[i]); one launch, pointer arithmetic done vectorised."""
+        ids, sids = _i32(seq_ids), _i32(set_ids)
+        n = ids.size
+        if kv.dim() != 6 or kv.shape[0] != n:
+            raise ValueError("kv must be [n][L][2][m][H_kv][d]")
+        m = kv.shape[3]
+        self._dev_tensor(kv, "kv", (n, self.L, 2, m, self.Hkv, self.d))
+        ptrs = (kv.data_ptr() + np.arange(n, dtype=np.uint64) * np.uint64(kv[0].numel() * 2)).astype(np.uint64)
+        ms = np.full(n, m, dtype=np.int32)
+        out = np.zeros(n, dtype=np.int32)
+        check(LIB.hpa_latent_set_install_batch(self._h, n, _p32(ids), _p32(sids), _p32(ms),
+                                               ptrs.ctypes.data_as(ctypes.POINTER(c_vp)),
+                                               _stream(self.device, stream), _p32(out)))
+        return out
+
     def latent_remove(self, seq: int, set_id: int) -> None:
         check(LIB.hpa_latent_set_remove(self._h, seq, set_id))
 

@@ -300,46 +300,59 @@ struct hpa_cache {
                     cfg.head_dim};
   }
 
-  // Rebuilds the host mirror of seq `s` from its segments and queues device
-  // writes for entries [from_entry, n) plus seq_len / n_entries.
+  // Recomputes the host mirror of seq `s` from entry `from_entry` on (entries
+  // before it are unchanged by the caller's mutation; only a segment's last page
+  // may be partial, so the pages before `from_entry` inside its segment are full)
+  // and queues device writes for the fields that changed. O(changed entries).
   void rebuild(int32_t s, int32_t from_entry) {
     Seq& q = seqs[s];
     const int32_t P = cfg.page_size;
-    std::vector<int32_t> pages, pos0, meta;
-    int32_t pos = 0, chunks = 0;
-    for (const Segment& g : q.segs) {
-      int32_t left = g.rows;
-      for (int32_t pg : g.pages) {
-        int32_t take = std::min(P, left);
-        pages.push_back(pg);
-        pos0.push_back(pos);
-        meta.push_back(take | (g.latent ? kMetaLatent : 0));
-        chunks += (take + 15) / 16;
+    const int32_t old_n = int32_t(q.pages.size());
+    from_entry = std::max(0, std::min(from_entry, old_n));
+    int32_t e = 0;
+    size_t gi = 0;
+    for (; gi < q.segs.size(); ++gi) {  // segment holding from_entry (O(#segments))
+      const int32_t np = int32_t(q.segs[gi].pages.size());
+      if (e + np > from_entry) break;
+      e += np;
+    }
+    int32_t pos = from_entry < old_n ? q.pos0[from_entry] : q.len;
+    int32_t old_tail_chunks = 0;
+    for (int32_t k = from_entry; k < old_n; ++k) old_tail_chunks += ((q.meta[k] & kMetaRowsMask) + 15) / 16;
+    std::vector<int32_t> tp, tpos, tmeta;
+    int32_t new_tail_chunks = 0;
+    int32_t pi = from_entry - e;  // page index inside segment gi
+    for (; gi < q.segs.size(); ++gi, pi = 0) {
+      const Segment& g = q.segs[gi];
+      int32_t left = g.rows - pi * P;
+      for (size_t k = size_t(pi); k < g.pages.size(); ++k) {
+        const int32_t take = std::min(P, left);
+        tp.push_back(g.pages[k]);
+        tpos.push_back(pos);
+        tmeta.push_back(take | (g.latent ? kMetaLatent : 0));
+        new_tail_chunks += (take + 15) / 16;
         pos += take;
         left -= take;
       }
     }
-    const int32_t n = int32_t(pages.size());
-    from_entry = std::max(0, std::min(from_entry, n));
-    // first entry that differs from the previous mirror (cheap diff)
-    int32_t first = from_entry;
-    while (first < n && first < int32_t(q.pages.size()) && q.pages[first] == pages[first] &&
-           q.pos0[first] == pos0[first] && q.meta[first] == meta[first])
-      ++first;
-    const int32_t old_n = int32_t(q.pages.size());
-    for (int32_t e = first; e < n; ++e) {  // only the fields that changed
-      const bool fresh = e >= old_n;
-      if (fresh || q.pages[e] != pages[e]) pending.push_back({int32_t(idx(s, e)), pages[e]});
-      if (fresh || q.pos0[e] != pos0[e]) pending.push_back({int32_t(off_pos0() + idx(s, e)), pos0[e]});
-      if (fresh || q.meta[e] != meta[e]) pending.push_back({int32_t(off_meta() + idx(s, e)), meta[e]});
+    const int32_t n = from_entry + int32_t(tp.size());
+    for (int32_t k = from_entry; k < n; ++k) {  // only the fields that changed
+      const int32_t t = k - from_entry;
+      const bool fresh = k >= old_n;
+      if (fresh || q.pages[k] != tp[t]) pending.push_back({int32_t(idx(s, k)), tp[t]});
+      if (fresh || q.pos0[k] != tpos[t]) pending.push_back({int32_t(off_pos0() + idx(s, k)), tpos[t]});
+      if (fresh || q.meta[k] != tmeta[t]) pending.push_back({int32_t(off_meta() + idx(s, k)), tmeta[t]});
     }
     if (q.len != pos) pending.push_back({int32_t(off_len() + s), pos});
-    if (int32_t(q.pages.size()) != n) pending.push_back({int32_t(off_nent() + s), n});
-    q.pages.swap(pages);
-    q.pos0.swap(pos0);
-    q.meta.swap(meta);
+    if (old_n != n) pending.push_back({int32_t(off_nent() + s), n});
+    q.pages.resize(from_entry);
+    q.pos0.resize(from_entry);
+    q.meta.resize(from_entry);
+    q.pages.insert(q.pages.end(), tp.begin(), tp.end());
+    q.pos0.insert(q.pos0.end(), tpos.begin(), tpos.end());
+    q.meta.insert(q.meta.end(), tmeta.begin(), tmeta.end());
     q.len = pos;
-    q.chunks = chunks;
+    q.chunks += new_tail_chunks - old_tail_chunks;
   }
 };
 
@@ -742,9 +755,10 @@ int32_t apply_install(hpa_cache_t* c, const InstallPlan& p, std::vector<int32_t>
     }
   }
   Segment& g = q.segs[seg_i];
+  const bool same_rows = !p.is_new && g.rows == p.m;
   g.rows = p.m;
   for (int32_t r = 0; r < p.m; ++r) slots.push_back(g.pages[r / P] * P + r % P);
-  c->rebuild(p.seq, first_entry);
+  if (!same_rows) c->rebuild(p.seq, first_entry);  // same rows in the same pages: table unchanged
   return g.set_id;
 }
 
