@@ -13,34 +13,44 @@ namespace hpa {
 namespace {
 
 // Copies record r's rows (all layers, heads, 16-B vectors) into their pool slots,
-// grid-stride over this record's CTAs.
-__device__ __forceinline__ void copy_rows(const PoolGeom& g, const ScatterRecord& r, const int32_t* slots) {
-  const int32_t vec_per_row = g.D / 8;  // 16-byte vectors per (row, head)
-  const int64_t per_layer = int64_t(r.n_rows) * g.Hkv * vec_per_row;
-  const int64_t total = per_layer * g.L;
-  const int64_t page_elems = int64_t(g.P) * g.D;
-  constexpr int kU = 4;  // vectors in flight per thread
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t base = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; base < total; base += stride * kU) {
+// grid-stride over this record's CTAs. A unit is one (layer, row, head) = D/8
+// 16-byte vectors handled by D/8 consecutive threads (coalesced 256-B rows);
+// each thread keeps kU units in flight. 32-bit index math, P a power of two.
+template <int D>
+__device__ __forceinline__ void copy_rows(const PoolGeom& g, const ScatterRecord& r, const int32_t* idx) {
+  constexpr int kVPR = D / 8;
+  constexpr int kU = 4;
+  const uint32_t units = uint32_t(r.n_rows) * uint32_t(g.Hkv) * uint32_t(g.L);
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t ustride = gridDim.x * blockDim.x / kVPR;
+  const uint32_t c = tid % kVPR;
+  const int64_t page_elems = int64_t(g.P) * D;
+  const __nv_bfloat16* ksrc = static_cast<const __nv_bfloat16*>(r.k);
+  const __nv_bfloat16* vsrc = static_cast<const __nv_bfloat16*>(r.v);
+  for (uint32_t u0 = tid / kVPR; u0 < units; u0 += kU * ustride) {
     int4 kv[kU], vv[kU];
     int64_t dst[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int64_t i = base + u * stride;
+      const uint32_t unit = u0 + u * ustride;
       dst[u] = -1;
-      if (i < total) {
-        const int32_t c = int32_t(i % vec_per_row);
-        int64_t rest = i / vec_per_row;
-        const int32_t h = int32_t(rest % g.Hkv);
-        rest /= g.Hkv;
-        const int32_t row = int32_t(rest % r.n_rows);
-        const int32_t l = int32_t(rest / r.n_rows);
-        const int64_t src = int64_t(l) * r.stride_l + int64_t(row) * r.stride_r + int64_t(h) * g.D + c * 8;
-        const int32_t slot = slots[r.slot_off + row];
-        const int32_t page = slot / g.P, prow = slot % g.P;
-        dst[u] = ((int64_t(l) * g.NP + page) * g.Hkv + h) * page_elems + int64_t(prow) * g.D + c * 8;
-        kv[u] = __ldg(reinterpret_cast<const int4*>(static_cast<const __nv_bfloat16*>(r.k) + src));
-        vv[u] = __ldg(reinterpret_cast<const int4*>(static_cast<const __nv_bfloat16*>(r.v) + src));
+      if (unit < units) {
+        const uint32_t h = unit % uint32_t(g.Hkv);
+        const uint32_t rest = unit / uint32_t(g.Hkv);
+        const uint32_t row = rest % uint32_t(r.n_rows);
+        const uint32_t l = rest / uint32_t(r.n_rows);
+        int32_t slot;
+        if (r.page_mode) {
+          const int32_t gr = r.row0 + int32_t(row);
+          slot = (idx[r.idx_off + (gr >> g.log2P)] << g.log2P) + (gr & (g.P - 1));
+        } else {
+          slot = idx[r.idx_off + row];
+        }
+        const int64_t src = int64_t(l) * r.stride_l + int64_t(row) * r.stride_r + int64_t(h) * D + c * 8;
+        dst[u] = ((int64_t(l) * g.NP + (slot >> g.log2P)) * g.Hkv + h) * page_elems +
+                 int64_t(slot & (g.P - 1)) * D + c * 8;
+        kv[u] = __ldg(reinterpret_cast<const int4*>(ksrc + src));
+        vv[u] = __ldg(reinterpret_cast<const int4*>(vsrc + src));
       }
     }
 #pragma unroll
@@ -56,20 +66,22 @@ __device__ __forceinline__ void copy_rows(const PoolGeom& g, const ScatterRecord
 // Grid: x = CTAs per record (grid-stride), y = record. All CTAs also apply the
 // metadata word writes (grid-stride over words) -- the table update rides the
 // same launch as the row copy.
+template <int D>
 __global__ void __launch_bounds__(256) scatter_kernel(PoolGeom g, int32_t* __restrict__ arena,
                                                       const WordWrite* __restrict__ words,
                                                       int32_t n_words,
                                                       const ScatterRecord* __restrict__ recs,
-                                                      const int32_t* __restrict__ slots) {
+                                                      const int32_t* __restrict__ idx) {
   grid_dependency_wait();
   const int64_t nthreads = int64_t(gridDim.x) * gridDim.y * blockDim.x;
   const int64_t gtid = (int64_t(blockIdx.y) * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
   for (int64_t i = gtid; i < n_words; i += nthreads) arena[words[i].idx] = words[i].val;
   if (recs == nullptr) return;
-  copy_rows(g, recs[blockIdx.y], slots);
+  copy_rows<D>(g, recs[blockIdx.y], idx);
 }
 
 // Same, with the metadata in the kernel parameters (no H2D copy).
+template <int D>
 __global__ void __launch_bounds__(256) scatter_inline_kernel(PoolGeom g, int32_t* __restrict__ arena,
                                                              const __grid_constant__ InlineMeta m) {
   grid_dependency_wait();
@@ -77,7 +89,7 @@ __global__ void __launch_bounds__(256) scatter_inline_kernel(PoolGeom g, int32_t
   const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   for (int64_t i = gtid; i < m.n_words; i += nthreads) arena[m.data[2 * i]] = m.data[2 * i + 1];
   if (!m.has_rec) return;
-  copy_rows(g, m.rec, m.data + 2 * m.n_words);
+  copy_rows<D>(g, m.rec, m.data + 2 * m.n_words);
 }
 
 // Grid: x = table entry, y = kv head. Copies rows 0..valid-1 of the page tile
@@ -106,26 +118,27 @@ __global__ void __launch_bounds__(128) export_kernel(PoolGeom g, DevTables t, in
 
 cudaError_t launch_scatter(const PoolGeom& g, int32_t* arena, const WordWrite* words,
                            int32_t n_words, const ScatterRecord* recs, int32_t n_recs,
-                           const int32_t* slots, int64_t max_rows_per_rec, cudaStream_t s) {
+                           const int32_t* idx, int64_t max_rows_per_rec, cudaStream_t s) {
   if (n_words == 0 && n_recs == 0) return cudaSuccess;
-  const int64_t work = max_rows_per_rec * g.Hkv * (g.D / 8) * g.L / 4;  // 4 vectors per thread
-  int64_t bx = (work + 255) / 256;
-  if (n_recs == 0) bx = (n_words + 255) / 256;
+  const int64_t threads = max_rows_per_rec * g.Hkv * g.L * (g.D / 8) / 4;  // 4 units per thread
+  int64_t bx = n_recs == 0 ? (n_words + 255) / 256 : (threads + 255) / 256;
   // Enough CTAs to fill 148 SMs several times over; each loops grid-stride.
   const int64_t cap = n_recs > 0 ? (148 * 16 + n_recs - 1) / n_recs : 148 * 4;
   if (bx > cap) bx = cap;
   if (bx < 1) bx = 1;
-  dim3 grid(unsigned(bx), unsigned(n_recs > 0 ? n_recs : 1));
-  return launch_pdl(scatter_kernel, grid, dim3(256), 0, s, g, arena, words, n_words,
-                    n_recs > 0 ? recs : static_cast<const ScatterRecord*>(nullptr), slots);
+  const dim3 grid(unsigned(bx), unsigned(n_recs > 0 ? n_recs : 1));
+  const ScatterRecord* r = n_recs > 0 ? recs : static_cast<const ScatterRecord*>(nullptr);
+  if (g.D == 128) return launch_pdl(scatter_kernel<128>, grid, dim3(256), 0, s, g, arena, words, n_words, r, idx);
+  return launch_pdl(scatter_kernel<64>, grid, dim3(256), 0, s, g, arena, words, n_words, r, idx);
 }
 
 cudaError_t launch_scatter_inline(const PoolGeom& g, int32_t* arena, const InlineMeta& m, int64_t max_rows,
                                   cudaStream_t s) {
-  int64_t bx = m.has_rec ? (max_rows * g.Hkv * (g.D / 8) * g.L / 4 + 255) / 256 : (m.n_words + 255) / 256;
+  int64_t bx = m.has_rec ? (max_rows * g.Hkv * g.L * (g.D / 8) / 4 + 255) / 256 : (m.n_words + 255) / 256;
   if (bx > 148 * 16) bx = 148 * 16;
   if (bx < 1) bx = 1;
-  return launch_pdl(scatter_inline_kernel, dim3(unsigned(bx)), dim3(256), 0, s, g, arena, m);
+  if (g.D == 128) return launch_pdl(scatter_inline_kernel<128>, dim3(unsigned(bx)), dim3(256), 0, s, g, arena, m);
+  return launch_pdl(scatter_inline_kernel<64>, dim3(unsigned(bx)), dim3(256), 0, s, g, arena, m);
 }
 
 cudaError_t launch_export(const PoolGeom& g, DevTables t, int32_t layer, int32_t seq,

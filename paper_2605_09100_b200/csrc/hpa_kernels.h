@@ -34,25 +34,29 @@ struct WordWrite {
 
 // One scatter record: n_rows rows of K and V, copied for every layer into the
 // pool slots slots[slot_off .. slot_off + n_rows) (slot = page * P + row).
+// Row r's destination: slot mode (append): slot = idx[off + r], slot = page * P + row;
+// page mode (latent install): g = row0 + r, slot = idx[off + g / P] * P + g % P.
 struct ScatterRecord {
   const void* k;      // bf16, element (l, r, h, x) at k + l*stride_l + r*stride_r + h*d + x
   const void* v;
   int64_t stride_l;   // elements
   int64_t stride_r;   // elements
   int32_t n_rows;
-  int32_t slot_off;
+  int32_t idx_off;    // offset into the index array (slots or pages)
+  int32_t row0;       // page mode: row offset inside the first page
+  int32_t page_mode;
 };
 
 struct PoolGeom {
   void* k_pool;  // bf16 [L][NP][H_kv][P][d]
   void* v_pool;
-  int32_t L, NP, Hkv, P, D;
+  int32_t L, NP, Hkv, P, D, log2P;
 };
 
 // Metadata writes + row scatter in one launch (append / install / apply).
 cudaError_t launch_scatter(const PoolGeom& g, int32_t* arena, const WordWrite* words,
                            int32_t n_words, const ScatterRecord* recs, int32_t n_recs,
-                           const int32_t* slots, int64_t max_rows_per_rec, cudaStream_t s);
+                           const int32_t* idx, int64_t max_rows_per_rec, cudaStream_t s);
 
 // Small metadata shipped as kernel parameters instead of an H2D copy (the
 // common decode-step append): table words (2 ints each) then slots (1 int

@@ -297,7 +297,7 @@ struct hpa_cache {
 
   PoolGeom geom() const {
     return PoolGeom{k_pool, v_pool, cfg.num_layers, cfg.num_pages, cfg.num_kv_heads, cfg.page_size,
-                    cfg.head_dim};
+                    cfg.head_dim, __builtin_ctz(uint32_t(cfg.page_size))};
   }
 
   // Recomputes the host mirror of seq `s` from entry `from_entry` on (entries
@@ -697,7 +697,7 @@ hpa_status_t hpa_append_kv(hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_id
     c->rebuild(seq_ids[i], first_entry);
   }
   const int64_t Hd = int64_t(c->cfg.num_kv_heads) * c->cfg.head_dim;
-  std::vector<ScatterRecord> recs{ScatterRecord{k, v, total_rows * Hd, Hd, int32_t(total_rows), 0}};
+  std::vector<ScatterRecord> recs{ScatterRecord{k, v, total_rows * Hd, Hd, int32_t(total_rows), 0, 0, 0}};
   return ship(c, static_cast<cudaStream_t>(stream), recs, slots, total_rows);
 }
 
@@ -757,7 +757,8 @@ int32_t apply_install(hpa_cache_t* c, const InstallPlan& p, std::vector<int32_t>
   Segment& g = q.segs[seg_i];
   const bool same_rows = !p.is_new && g.rows == p.m;
   g.rows = p.m;
-  for (int32_t r = 0; r < p.m; ++r) slots.push_back(g.pages[r / P] * P + r % P);
+  slots.insert(slots.end(), g.pages.begin(), g.pages.end());  // page mode: one index per page
+  (void)P;
   if (!same_rows) c->rebuild(p.seq, first_entry);  // same rows in the same pages: table unchanged
   return g.set_id;
 }
@@ -810,7 +811,7 @@ hpa_status_t hpa_latent_set_install_batch(hpa_cache_t* c, int32_t n, const int32
       Segment& g = q.segs[p.seg_index];
       c->alloc.alloc(p.new_pages, g.pages);
       g.rows = p.m;
-      for (int32_t r = 0; r < p.m; ++r) slots.push_back(g.pages[r / c->cfg.page_size] * c->cfg.page_size + r % c->cfg.page_size);
+      slots.insert(slots.end(), g.pages.begin(), g.pages.end());  // page mode
       c->rebuild(p.seq, first_entry);
       if (set_ids_out) set_ids_out[i] = g.set_id;
     } else {
@@ -818,7 +819,7 @@ hpa_status_t hpa_latent_set_install_batch(hpa_cache_t* c, int32_t n, const int32
       if (set_ids_out) set_ids_out[i] = id;
     }
     const char* kv = static_cast<const char*>(p.kv);
-    recs.push_back(ScatterRecord{kv, kv + size_t(p.m) * Hd * 2, 2 * int64_t(p.m) * Hd, Hd, p.m, slot_off});
+    recs.push_back(ScatterRecord{kv, kv + size_t(p.m) * Hd * 2, 2 * int64_t(p.m) * Hd, Hd, p.m, slot_off, 0, 1});
     max_rows = std::max<int64_t>(max_rows, p.m);
   }
   return ship(c, static_cast<cudaStream_t>(stream), recs, slots, max_rows);
