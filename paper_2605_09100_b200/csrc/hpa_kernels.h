@@ -106,6 +106,7 @@ struct PrefillArgs {
   int32_t n_seqs, Hq, Hkv, G, P, NP, layer, max_q_len;
   float scale_log2;
   int32_t log2P;
+  long long* trace;         // HPA_TRACE builds only: per-phase clock64 stamps of CTA (0,0,0)
 };
 // tm_q: 3-D map over q [sum q][Hq][d] with box {64, 1, 128};
 // tm_k / tm_v: 2-D maps over the pools with box {64, min(P,128)}.

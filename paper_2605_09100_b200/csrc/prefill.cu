@@ -17,7 +17,7 @@
 //      warp  8    TMA producer (all lanes build the mask indices; the page
 //                 boxes are issued in parallel by several lanes)
 //      warp  9    tcgen05 MMA issuer; owns the 512 TMEM columns
-//      warps 10-11 spare. setmaxnreg moves registers from warpgroup 2 (64)
+//      warp  10   V producer (decoupled from K); warp 11 spare. setmaxnreg moves registers from warpgroup 2 (64)
 //                 to the softmax warpgroups (224).
 //  * TMEM: S_s / P_s at columns [128 s, 128 s + 128), O_s at [256 + 128 s, ...).
 //    S = Q K^T (SS: Q and K K-major, 128-B swizzle); the softmax writes P as
@@ -42,12 +42,13 @@ namespace {
 
 constexpr int kBM = 128;   // query rows per slot
 constexpr int kBN = 128;   // key slots per tile
-constexpr int kNK = 2;     // K ring depth
+constexpr int kNK = 3;     // K ring depth
 constexpr int kNV = 2;     // V ring depth
-constexpr int kNC = 4;     // mask-index ring depth
+constexpr int kNC = 3;     // mask-index ring depth
 constexpr int kThreads = 384;      // 3 warpgroups: softmax 0, softmax 1, producer / MMA / 2 spare
 constexpr int kProducerWarp = 8;
 constexpr int kMmaWarp = 9;
+constexpr int kVProducerWarp = 10;
 #ifndef HPA_SOFTMAX_REGS
 #define HPA_SOFTMAX_REGS 216
 #endif
@@ -62,6 +63,16 @@ static_assert(2 * kSoftmaxRegs + kOtherRegs <= 3 * 168, "setmaxnreg budget");
 constexpr float kRescaleThreshold = 8.0f;  // log2 units (factor 256)
 #ifndef HPA_POLY_EVERY
 #define HPA_POLY_EVERY 0  // 1 of every N exp2 pairs on the FMA pipe (0 = all on MUFU; measured best)
+#endif
+// Phase trace (HPA_TRACE builds): stamp[event][tile] for CTA (0,0,0), tiles < 64.
+#ifdef HPA_TRACE
+#define TRACE(ev, j)                                                                         \
+  do {                                                                                       \
+    if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64)        \
+      a.trace[(ev) * 64 + (j)] = clock64();                                                  \
+  } while (0)
+#else
+#define TRACE(ev, j) do { } while (0)
 #endif
 #ifndef HPA_PV_SPLIT
 #define HPA_PV_SPLIT 1    // publish P in two 64-key halves (PV starts on the first half)
@@ -335,12 +346,28 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       if (lane == 0) mbar_arrive(&c_full[cs]);
       const int ks = j % kNK;
       if (j >= kNK) mbar_wait(&k_empty[ks], ((j / kNK) - 1) & 1);
-      if (lane == 0) mbar_arrive_expect_tx(&k_full[ks], L::kKV);
+      if (lane == 0) { TRACE(0, j); mbar_arrive_expect_tx(&k_full[ks], L::kKV); }
       __syncwarp();
       if (lane < nbox) {
 #pragma unroll
         for (int hf = 0; hf < kHalves; ++hf)
           tma_load_2d(sK + ks * L::kKV + hf * kBN * 128 + lane * pbox * 128, &tm_k, &k_full[ks], hf * 64, row);
+      }
+      __syncwarp();
+    }
+  } else if (warp == kVProducerWarp) {
+    // ================================================================ V producer
+    // (decoupled from K so K(j+1) never waits behind V(j)'s ring slot)
+    const int pbox = P < kBN ? P : kBN;
+    const int nbox = kBN / pbox;
+    constexpr int kOobRow = INT_MAX / 2;
+    const int head_row = a.layer * a.NP;
+    for (int j = 0; j < n_tiles; ++j) {
+      int row = kOobRow;
+      if (lane < nbox) {
+        const int slot = j * kBN + lane * pbox;
+        const int e = slot >> lp;
+        if (e < n_ent) row = ((head_row + bt[e]) * a.Hkv + h) * P + (slot & (P - 1));
       }
       const int vs = j % kNV;
       if (j >= kNV) mbar_wait(&v_empty[vs], ((j / kNV) - 1) & 1);
@@ -385,18 +412,29 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       tc_commit(&k_empty[0]);
       for (int j = 0; j < n_tiles; ++j) {
         const bool more = j + 1 < n_tiles;
-        if (more) mbar_wait(&k_full[(j + 1) % kNK], ((j + 1) / kNK) & 1);
         mbar_wait(&v_full[j % kNV], (j / kNV) & 1);
+        TRACE(2, j);
+        bool k_ready = false;
         for (int s = 0; s < nslot; ++s) {
           // PV over keys 0..63 as soon as the first half of P is in TMEM, then 64..127
           mbar_wait(&p_full[2 * s], j & 1);
+          TRACE(3 + s, j);
           tc_fence_after();
           issue_pv_half(s, j, 0);
           mbar_wait(&p_full[2 * s + 1], j & 1);
+          TRACE(5 + s, j);
           tc_fence_after();
           issue_pv_half(s, j, 1);
           if (s == nslot - 1) tc_commit(&v_empty[j % kNV]);
-          if (more) issue_s(s, j + 1);  // overwrites S/P s after PV s has read P (in-order pipe)
+          if (more) {
+            if (!k_ready) {  // K(j+1) is only needed here, not by PV(j)
+              mbar_wait(&k_full[(j + 1) % kNK], ((j + 1) / kNK) & 1);
+              TRACE(1, j);
+              tc_fence_after();
+              k_ready = true;
+            }
+            issue_s(s, j + 1);  // overwrites S/P s after PV s has read P (in-order pipe)
+          }
         }
         if (more) tc_commit(&k_empty[(j + 1) % kNK]);
       }
@@ -426,6 +464,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
       float x[kBN];
       mbar_wait(&s_full[s], j & 1);
+      if (row == 0) TRACE(7 + s, j);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < kBN / 32; ++c) tc_ld32(tS + c * 32, x + c * 32);
@@ -433,11 +472,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const int32_t* col = sC + cs * (kBN + 4);
       const bool all_vis = col[kBN] != 0;
       tc_wait_ld();
-      float mx = -CUDART_INF_F;
-      if (all_vis) {
-#pragma unroll
-        for (int c = 0; c < kBN; c += 2) mx = fmaxf(mx, fmaxf(x[c], x[c + 1]));
-      } else {
+      if (row == 0) TRACE(9 + s, j);
+      if (!all_vis) {
 #pragma unroll
         for (int c = 0; c < kBN; c += 4) {
           const int4 ci = *reinterpret_cast<const int4*>(col + c);
@@ -445,9 +481,18 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           x[c + 1] = ci.y <= my_i ? x[c + 1] : -CUDART_INF_F;
           x[c + 2] = ci.z <= my_i ? x[c + 2] : -CUDART_INF_F;
           x[c + 3] = ci.w <= my_i ? x[c + 3] : -CUDART_INF_F;
-          mx = fmaxf(mx, fmaxf(fmaxf(x[c], x[c + 1]), fmaxf(x[c + 2], x[c + 3])));
         }
       }
+      // row max as a tree (8 independent partial maxima), not a 64-deep chain
+      float pm[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pm[k] = fmaxf(x[k], x[k + 8]);
+#pragma unroll
+      for (int c = 16; c < kBN; c += 16) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pm[k] = fmaxf(pm[k], fmaxf(x[c + k], x[c + k + 8]));
+      }
+      float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
       __syncwarp();
       if (lane == 0) mbar_arrive(&c_empty[cs]);
       mx *= sl2;
@@ -470,7 +515,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       // p = 2^(x*sl2 - m): f32x2 FFMA for the argument; 3 of every 4 pairs on the
       // MUFU ex2 unit, 1 pair on the FMA pipe (degree-3 polynomial, rel. err 1e-4)
       const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_new, -m_new);
-      float2 rs2 = make_float2(0.f, 0.f);
+      float2 rs4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         uint32_t pk[kBN / 4];
@@ -484,7 +529,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             e.x = fast_exp2(arg.x);
             e.y = fast_exp2(arg.y);
           }
-          rs2 = fadd2(rs2, e);
+            rs4[(c >> 1) & 3] = fadd2(rs4[(c >> 1) & 3], e);  // 4 independent partial sums
           pk[(c - half * 64) >> 1] = pack_bf16(e.x, e.y);
         }
         // P (bf16 pairs) over S: keys [64 half, 64 half + 64) -> columns [128 s + 32 half, +32)
@@ -497,9 +542,11 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             if (!HPA_PV_SPLIT) mbar_arrive(&p_full[2 * s]);
             mbar_arrive(&p_full[2 * s + half]);
           }
+          if (row == 0) TRACE(11 + 2 * s + half, j);
         }
       }
-      l_run = l_run * alpha + (rs2.x + rs2.y);
+      const float2 rsa = fadd2(rs4[0], rs4[1]), rsb = fadd2(rs4[2], rs4[3]);
+      l_run = l_run * alpha + ((rsa.x + rsb.x) + (rsa.y + rsb.y));
     }
     if (live) {
       // epilogue: O / l -> bf16 -> global

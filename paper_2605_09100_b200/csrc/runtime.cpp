@@ -286,6 +286,7 @@ struct hpa_cache {
   int32_t* counters = nullptr;  // [max_seqs][H_kv], zero between calls
   size_t part_elems = 0;
   int32_t forced_splits = 0;
+  long long* trace = nullptr;  // prefill phase trace (HPA_TRACE builds; set via hpa_debug_trace)
   int num_sms = 148;
   uint64_t launches = 0;
 
@@ -937,7 +938,7 @@ hpa_status_t hpa_prefill(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
   const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt(float(D));
   PrefillArgs a{c->dt, dmeta, dmeta + n_seqs, dmeta + 2 * n_seqs, out, n_seqs, Hq, c->cfg.num_kv_heads,
                 Hq / c->cfg.num_kv_heads, c->cfg.page_size, c->cfg.num_pages, layer, max_q,
-                scale * 1.4426950408889634f, __builtin_ctz(uint32_t(c->cfg.page_size))};
+                scale * 1.4426950408889634f, __builtin_ctz(uint32_t(c->cfg.page_size)), c->trace};
   int launched = 0;
   cudaError_t e = launch_prefill(tm_q, c->tm_k_pre, c->tm_v_pre, a, D, s, &launched);
   c->launches += launched;
@@ -994,6 +995,14 @@ hpa_status_t hpa_set_decode_splits(hpa_cache_t* c, int32_t splits) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
   if (splits < 0) return fail(HPA_ERR_INVALID_ARG, "splits < 0");
   c->forced_splits = splits;
+  return HPA_OK;
+}
+
+// Internal / experiments only (not in include/hpa.h): device buffer for the
+// HPA_TRACE prefill phase stamps.
+hpa_status_t hpa_debug_trace(hpa_cache_t* c, void* device_buf) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  c->trace = static_cast<long long*>(device_buf);
   return HPA_OK;
 }
 
