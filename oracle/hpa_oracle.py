@@ -106,6 +106,29 @@ class OracleCache:
                 return set_id
         raise KeyError(f"unknown latent set {set_id}")
 
+    def compress(self, seq_id: int, n_doc_rows: int, m_rows: int) -> int:
+        """In-cache compression (P:L251 / P:L973: the meta latent
+        tokens' KV, computed in the same forward pass as the document, becomes the
+        document's compressed memory). Both ranges lie at the end of the trailing
+        TOKEN segment: [.., doc (n_doc_rows), latents (m_rows)] ->
+        [.., LATENT set (the same m rows)]. Returns the new set id."""
+        segs = self.seqs[seq_id]
+        if not segs or segs[-1].kind != "token" or segs[-1].rows < n_doc_rows + m_rows or m_rows <= 0:
+            raise ValueError("compress needs doc + latent rows at the end of a token segment")
+        last = segs[-1]
+        keep = last.rows - n_doc_rows - m_rows
+        lat_k = last.k[:, keep + n_doc_rows:].copy()
+        lat_v = last.v[:, keep + n_doc_rows:].copy()
+        if keep > 0:
+            last.k = last.k[:, :keep].copy()
+            last.v = last.v[:, :keep].copy()
+        else:
+            segs.pop()
+        set_id = self.next_set[seq_id]
+        self.next_set[seq_id] += 1
+        segs.append(_Segment("latent", set_id, lat_k, lat_v))
+        return set_id
+
     def remove(self, seq_id: int, set_id: int) -> None:
         segs = self.seqs[seq_id]
         for i, s in enumerate(segs):

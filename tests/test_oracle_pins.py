@@ -280,3 +280,30 @@ def test_set_ids_and_remove():
         c.remove(0, 7)
     with pytest.raises(ValueError):
         attend(np.zeros((3, 1, 4)), np.zeros((1, 2, 4)), np.zeros((1, 2, 4)), 1.0)
+
+
+def test_compress_keeps_latent_rows_and_drops_document():
+    """NEXT-1 (in-cache compression): [prefix | doc | latents] -> [prefix | LATENT(latents)];
+    logical KV equals the explicit concatenation, attention equals SDPA over it, and the
+    stored rows are m regardless of the document length (O(1) memory)."""
+    shape = Shape(1, 4, 2, 32, 16)
+    for n_doc in (0, 7, 300):
+        c, d = build_cache(shape, [("latent", 128), ("tokens", 21 + n_doc + 64)])
+        k_before, v_before = c.logical_kv(0, 0)
+        sid = c.compress(0, n_doc, 64)
+        assert sid == 1 and [(s.kind, s.rows) for s in c.seqs[0]] == [("latent", 128), ("token", 21), ("latent", 64)]
+        k, v = c.logical_kv(0, 0)
+        keep = 128 + 21
+        exp_k = np.concatenate([k_before[:, :keep], k_before[:, keep + n_doc:]], axis=1)
+        exp_v = np.concatenate([v_before[:, :keep], v_before[:, keep + n_doc:]], axis=1)
+        assert np.array_equal(k, exp_k) and np.array_equal(v, exp_v)
+        assert c.latent_rows(0) == 128 + 64
+        q = f64(d.queries(shape, 2))
+        mask = torch.arange(k.shape[1])[None, :] <= (torch.arange(2)[:, None] + k.shape[1] - 2)
+        ref = torch.nn.functional.scaled_dot_product_attention(
+            torch.from_numpy(q).transpose(0, 1), torch.from_numpy(exp_k).repeat_interleave(2, 0),
+            torch.from_numpy(exp_v).repeat_interleave(2, 0), attn_mask=mask, scale=shape.scale).transpose(0, 1)
+        assert np.max(np.abs(attend(q, k, v, shape.scale) - ref.numpy())) <= 1e-12
+    c, _ = build_cache(shape, [("tokens", 10)])
+    with pytest.raises(ValueError):
+        c.compress(0, 5, 6)
