@@ -133,6 +133,21 @@ hpa_status_t hpa_latent_set_install_batch(hpa_cache_t* c, int32_t n, const int32
 /* Removes a latent set (frees its pages, splices the table). */
 hpa_status_t hpa_latent_set_remove(hpa_cache_t* c, int32_t seq_id, int32_t set_id);
 
+/* In-cache compression: how a latent page set is born.
+ * GRC computes a document's compression in the same forward pass that reads it
+ * ("three tasks in one forward pass"; the meta latent tokens' KV is the
+ * compressed cache): the caller appends the document's token KV, then the
+ * m meta latent tokens' KV (as tokens; their queries can be prefetched with
+ * hpa_prefill), then calls this. The last m_rows rows of the sequence become a new
+ * LATENT set (copied into fresh latent pages, one kernel launch) and the
+ * n_doc_rows rows just before them are dropped; their token pages are freed.
+ * Both ranges must lie in the sequence's trailing TOKEN segment (else
+ * HPA_ERR_INVALID_ARG). Needs ceil(m_rows/P) free pages (else
+ * HPA_ERR_OUT_OF_PAGES, cache unchanged). *set_id_out (may be NULL) receives the
+ * new set id. Memory for the document goes from O(n_doc) to O(m) rows. */
+hpa_status_t hpa_seq_compress(hpa_cache_t* c, int32_t seq_id, int32_t n_doc_rows, int32_t m_rows,
+                              hpa_stream_t stream, int32_t* set_id_out);
+
 /* ---------------------------------------------------------------- attention (a4-a6)
  * Decode (a4 + a5): for each listed sequence the query is its LAST logical row
  * (its KV must already be appended; reading A8), so every stored row is visible.

@@ -1,7 +1,7 @@
 """paper_2605_09100_b200 -- B200-native hybrid paged attention (HPA).
 
 Thin Python binding over the C ABI in include/hpa.h (libhpa.so, built in-tree
-by `paper_2605_09100_b200.build`). Argument marshalling only: every step of the
+by `python paper_2605_09100_b200/build.py`). Argument marshalling only: every step of the
 path runs in the library's CUDA kernels. There is no CPU fallback -- importing
 the binding raises if the library is missing, and cache creation fails on a
 host without an sm_100 GPU.

@@ -46,6 +46,7 @@ SIGNATURES = {
     "hpa_latent_set_install_batch": (c_st, [c_vp, c_i32, c_i32p, c_i32p, c_i32p,
                                             ctypes.POINTER(c_vp), c_vp, c_i32p]),
     "hpa_latent_set_remove": (c_st, [c_vp, c_i32, c_i32]),
+    "hpa_seq_compress": (c_st, [c_vp, c_i32, c_i32, c_i32, c_vp, c_i32p]),
     "hpa_decode": (c_st, [c_vp, c_i32, c_i32, c_i32p, c_vp, c_vp, ctypes.c_float, c_vp]),
     "hpa_prefill": (c_st, [c_vp, c_i32, c_i32, c_i32p, c_i32p, c_vp, c_vp, ctypes.c_float, c_vp]),
     "hpa_seq_info": (c_st, [c_vp, c_i32, c_i32p, c_i32p, c_i32p]),
@@ -70,7 +71,7 @@ def lib_path() -> str:
 def _load():
     if not os.path.exists(_LIB_PATH):
         raise ImportError(
-            f"{_LIB_PATH} is missing: build it with `python -m paper_2605_09100_b200.build` "
+            f"{_LIB_PATH} is missing: build it with `python paper_2605_09100_b200/build.py` "
             "(there is no CPU fallback)")
     lib = ctypes.CDLL(_LIB_PATH)
     for name, (res, args) in SIGNATURES.items():

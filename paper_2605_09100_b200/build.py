@@ -1,6 +1,8 @@
 """Builds libhpa.so in-tree for sm_100a (nvcc cross-compiles; no GPU needed).
 
-    python -m paper_2605_09100_b200.build [--force] [-v]
+    python paper_2605_09100_b200/build.py [--force] [-v] [-DNAME=VAL ... --out=path]
+
+(run by path: importing the package would load the library it is building)
 
 Flags: -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo; the CUDA runtime
 is linked statically and the driver is reached through

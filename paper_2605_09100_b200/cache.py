@@ -147,6 +147,14 @@ class Cache:
                                                _stream(self.device, stream), _p32(out)))
         return out
 
+    def compress(self, seq: int, n_doc_rows: int, m_rows: int, stream=None) -> int:
+        """In-cache compression (hpa_seq_compress): the last m_rows rows become a LATENT set,
+        the n_doc_rows rows before them are dropped. Returns the new set id."""
+        out = c_i32()
+        check(LIB.hpa_seq_compress(self._h, seq, n_doc_rows, m_rows, _stream(self.device, stream),
+                                   ctypes.byref(out)))
+        return out.value
+
     def latent_remove(self, seq: int, set_id: int) -> None:
         check(LIB.hpa_latent_set_remove(self._h, seq, set_id))
 

@@ -46,11 +46,19 @@ __device__ __forceinline__ void copy_rows(const PoolGeom& g, const ScatterRecord
         } else {
           slot = idx[r.idx_off + row];
         }
-        const int64_t src = int64_t(l) * r.stride_l + int64_t(row) * r.stride_r + int64_t(h) * D + c * 8;
         dst[u] = ((int64_t(l) * g.NP + (slot >> g.log2P)) * g.Hkv + h) * page_elems +
                  int64_t(slot & (g.P - 1)) * D + c * 8;
-        kv[u] = __ldg(reinterpret_cast<const int4*>(ksrc + src));
-        vv[u] = __ldg(reinterpret_cast<const int4*>(vsrc + src));
+        if (r.src_from_pool) {  // in-cache move: source is another pool slot
+          const int32_t ss = idx[r.src_off + row];
+          const int64_t src = ((int64_t(l) * g.NP + (ss >> g.log2P)) * g.Hkv + h) * page_elems +
+                              int64_t(ss & (g.P - 1)) * D + c * 8;
+          kv[u] = *reinterpret_cast<const int4*>(static_cast<const __nv_bfloat16*>(g.k_pool) + src);
+          vv[u] = *reinterpret_cast<const int4*>(static_cast<const __nv_bfloat16*>(g.v_pool) + src);
+        } else {
+          const int64_t src = int64_t(l) * r.stride_l + int64_t(row) * r.stride_r + int64_t(h) * D + c * 8;
+          kv[u] = __ldg(reinterpret_cast<const int4*>(ksrc + src));
+          vv[u] = __ldg(reinterpret_cast<const int4*>(vsrc + src));
+        }
       }
     }
 #pragma unroll

@@ -36,6 +36,8 @@ struct WordWrite {
 // pool slots slots[slot_off .. slot_off + n_rows) (slot = page * P + row).
 // Row r's destination: slot mode (append): slot = idx[off + r], slot = page * P + row;
 // page mode (latent install): g = row0 + r, slot = idx[off + g / P] * P + g % P.
+// Source: the k / v pointers, or (src_from_pool) the pool itself at slot
+// idx[src_off + r] (in-cache moves, e.g. hpa_seq_compress).
 struct ScatterRecord {
   const void* k;      // bf16, element (l, r, h, x) at k + l*stride_l + r*stride_r + h*d + x
   const void* v;
@@ -45,6 +47,8 @@ struct ScatterRecord {
   int32_t idx_off;    // offset into the index array (slots or pages)
   int32_t row0;       // page mode: row offset inside the first page
   int32_t page_mode;
+  int32_t src_from_pool;
+  int32_t src_off;    // src_from_pool: offset of the source slots in the index array
 };
 
 struct PoolGeom {

@@ -698,7 +698,7 @@ hpa_status_t hpa_append_kv(hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_id
     c->rebuild(seq_ids[i], first_entry);
   }
   const int64_t Hd = int64_t(c->cfg.num_kv_heads) * c->cfg.head_dim;
-  std::vector<ScatterRecord> recs{ScatterRecord{k, v, total_rows * Hd, Hd, int32_t(total_rows), 0, 0, 0}};
+  std::vector<ScatterRecord> recs{ScatterRecord{k, v, total_rows * Hd, Hd, int32_t(total_rows), 0, 0, 0, 0, 0}};
   return ship(c, static_cast<cudaStream_t>(stream), recs, slots, total_rows);
 }
 
@@ -820,7 +820,7 @@ hpa_status_t hpa_latent_set_install_batch(hpa_cache_t* c, int32_t n, const int32
       if (set_ids_out) set_ids_out[i] = id;
     }
     const char* kv = static_cast<const char*>(p.kv);
-    recs.push_back(ScatterRecord{kv, kv + size_t(p.m) * Hd * 2, 2 * int64_t(p.m) * Hd, Hd, p.m, slot_off, 0, 1});
+    recs.push_back(ScatterRecord{kv, kv + size_t(p.m) * Hd * 2, 2 * int64_t(p.m) * Hd, Hd, p.m, slot_off, 0, 1, 0, 0});
     max_rows = std::max<int64_t>(max_rows, p.m);
   }
   return ship(c, static_cast<cudaStream_t>(stream), recs, slots, max_rows);
@@ -849,6 +849,46 @@ hpa_status_t hpa_latent_set_remove(hpa_cache_t* c, int32_t seq_id, int32_t set_i
     first_entry += int32_t(q.segs[i].pages.size());
   }
   return fail(HPA_ERR_UNKNOWN_SET, "sequence %d has no latent set %d", seq_id, set_id);
+}
+
+hpa_status_t hpa_seq_compress(hpa_cache_t* c, int32_t seq_id, int32_t n_doc_rows, int32_t m_rows,
+                              hpa_stream_t stream, int32_t* set_id_out) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (hpa_status_t st = check_seq(c, seq_id)) return st;
+  Seq& q = c->seqs[seq_id];
+  if (n_doc_rows < 0 || m_rows <= 0) return fail(HPA_ERR_INVALID_ARG, "need n_doc_rows >= 0 and m_rows > 0");
+  if (q.segs.empty() || q.segs.back().latent || q.segs.back().rows < n_doc_rows + m_rows)
+    return fail(HPA_ERR_INVALID_ARG, "document + latent rows must lie in the trailing token segment");
+  const int32_t P = c->cfg.page_size;
+  const int32_t np = (m_rows + P - 1) / P;
+  Segment& T = q.segs.back();
+  const int32_t keep = T.rows - n_doc_rows - m_rows;
+  const int32_t keep_pages = (keep + P - 1) / P;
+  const int32_t n_before = seq_entries(q) - int32_t(T.pages.size());
+  if (n_before + keep_pages + np > c->cfg.max_pages_per_seq)
+    return fail(HPA_ERR_SEQ_CAPACITY, "sequence %d would exceed %d pages", seq_id, c->cfg.max_pages_per_seq);
+  if (np > c->alloc.num_free())
+    return fail(HPA_ERR_OUT_OF_PAGES, "compress needs %d pages, %d free", np, c->alloc.num_free());
+  DeviceGuard dg(c->cfg.device);
+  // destination pages first (never overlapping the sources), then the move record
+  Segment L{true, q.next_set++, m_rows, {}};
+  c->alloc.alloc(np, L.pages);
+  std::vector<int32_t> idx(L.pages.begin(), L.pages.end());  // page-mode destination
+  const int32_t src_off = int32_t(idx.size());
+  for (int32_t r = 0; r < m_rows; ++r) {
+    const int32_t row = keep + n_doc_rows + r;
+    idx.push_back(T.pages[row / P] * P + row % P);
+  }
+  // free the document's (and the latents' token) pages; keep the prefix rows
+  for (size_t k = size_t(keep_pages); k < T.pages.size(); ++k) c->alloc.release(T.pages[k]);
+  T.pages.resize(size_t(keep_pages));
+  T.rows = keep;
+  if (keep == 0) q.segs.pop_back();
+  q.segs.push_back(std::move(L));
+  c->rebuild(seq_id, n_before + std::max(0, keep_pages - 1));
+  if (set_id_out) *set_id_out = q.segs.back().set_id;
+  std::vector<ScatterRecord> recs{ScatterRecord{nullptr, nullptr, 0, 0, m_rows, 0, 0, 1, 1, src_off}};
+  return ship(c, static_cast<cudaStream_t>(stream), recs, idx, m_rows);
 }
 
 hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids, const void* q,

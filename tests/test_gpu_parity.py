@@ -382,3 +382,56 @@ def test_allocator_fuzz_against_model():
         k1, v1 = p.orc.logical_kv(s, 0)
         k2, v2 = p.cache.export_logical_kv(0, s)
         assert np.array_equal(k1, f64(k2)) and np.array_equal(v1, f64(v2))
+
+
+# ----------------------------------------------------------------------------- NEXT-1: compression
+@pytest.mark.parametrize("P", [16, 64])
+def test_compress_in_cache(P):
+    """In-cache compression (hpa_seq_compress): [latents 128 | tokens 21 | doc n | meta-latent m]
+    -> [latents 128 | tokens 21 | LATENT m]; bit-exact table/gather vs the oracle model, decode and
+    prefill parity after compression, document pages returned to the pool."""
+    shape = Shape(1, 8, 2, 128, P)
+    p = Pair(shape, num_pages=2048, max_seqs=4, max_pages_per_seq=256)
+    seqs = []
+    for n_doc, m in ((300, 128), (5, 40), (0, 16)):
+        s = p.build([("latent", 128), ("tokens", 21 + n_doc + m)])
+        seqs.append(s)
+        free0 = p.cache.stats()[0]
+        got = p.cache.compress(s, n_doc, m)
+        assert got == p.orc.compress(s, n_doc, m)
+        pages_before = -(-(21 + n_doc + m) // P)
+        pages_after = -(-21 // P) + -(-m // P)
+        assert p.cache.stats()[0] == free0 + pages_before - pages_after
+    p.tokens(seqs, [3, 17, 1])          # appending after a compressed set opens a token segment
+    torch.cuda.synchronize()
+    for s in seqs:
+        pages, pos0, meta = p.cache.export_table(s)
+        assert [(("latent" if m & META_LATENT_BIT else "token"), int(m & 0x7fff), int(x))
+                for m, x in zip(meta, pos0)] == p.orc.expected_table(s)
+        k1, v1 = p.orc.logical_kv(s, 0)
+        k2, v2 = p.cache.export_logical_kv(0, s)
+        assert np.array_equal(k1, f64(k2)) and np.array_equal(v1, f64(v2))
+    q = p.queries(3)
+    got = p.cache.decode(0, seqs, q.cuda())
+    torch.cuda.synchronize()
+    check_close(got, oracle_decode(p, seqs, q), "decode after compress")
+    q = p.queries(20)
+    got = p.cache.prefill(0, [seqs[0]], [20], q.cuda())
+    torch.cuda.synchronize()
+    check_close(got, oracle_prefill(p, [seqs[0]], [20], q), "prefill after compress")
+
+
+def test_compress_errors_leave_cache_unchanged():
+    from paper_2605_09100_b200 import HPAError
+    shape = Shape(1, 4, 2, 64, 16)
+    p = Pair(shape, num_pages=64, max_seqs=2, max_pages_per_seq=32)
+    s = p.build([("tokens", 40), ("latent", 16)])
+    before = (p.cache.stats(), p.cache.export_table(s)[0].tolist())
+    with pytest.raises(HPAError) as e:
+        p.cache.compress(s, 4, 8)              # trailing segment is LATENT
+    assert e.value.name == "HPA_ERR_INVALID_ARG"
+    p.tokens([s], [10])
+    with pytest.raises(HPAError) as e:
+        p.cache.compress(s, 5, 6)              # 11 > 10 rows in the trailing token segment
+    assert e.value.name == "HPA_ERR_INVALID_ARG"
+    assert p.cache.stats()[0] == before[0][0] - 1
