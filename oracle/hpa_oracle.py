@@ -129,6 +129,19 @@ class OracleCache:
         segs.append(_Segment("latent", set_id, lat_k, lat_v))
         return set_id
 
+    def share(self, dst_seq: int, src_seq: int, src_set_id: int) -> int:
+        """Shared document memory ("KV cache server for storing
+        and retrieving compressed document memories"): dst_seq gets a new LATENT set whose
+        rows are those of src_seq's set src_set_id (the logical model copies the values;
+        physical sharing is the cache's business). Returns dst's new set id."""
+        for sg in self.seqs[src_seq]:
+            if sg.kind == "latent" and sg.set_id == src_set_id:
+                set_id = self.next_set[dst_seq]
+                self.next_set[dst_seq] += 1
+                self.seqs[dst_seq].append(_Segment("latent", set_id, sg.k.copy(), sg.v.copy()))
+                return set_id
+        raise KeyError(f"unknown latent set {src_set_id}")
+
     def remove(self, seq_id: int, set_id: int) -> None:
         segs = self.seqs[seq_id]
         for i, s in enumerate(segs):

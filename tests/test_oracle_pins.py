@@ -307,3 +307,24 @@ def test_compress_keeps_latent_rows_and_drops_document():
     c, _ = build_cache(shape, [("tokens", 10)])
     with pytest.raises(ValueError):
         c.compress(0, 5, 6)
+
+
+def test_share_copies_logical_rows_and_isolates_updates():
+    """NEXT-2 (shared document memories): the shared set reads as the source's rows; a later
+    replacement in either sequence does not change the other (copy-on-write semantics)."""
+    shape = Shape(1, 2, 1, 16, 16)
+    c = OracleCache(1, 2, 1, 16, 16)
+    d = Draw(3)
+    for s in (0, 1):
+        c.create_seq(s)
+    doc = f64(d.latent(shape, 40))
+    c.install(0, -1, doc)
+    k, v = d.tokens(shape, 5)
+    c.append(1, f64(k), f64(v))
+    assert c.share(1, 0, 0) == 0
+    k1, _ = c.logical_kv(1, 0)
+    assert np.array_equal(k1[:, 5:], doc[0, 0].transpose(1, 0, 2))
+    c.install(0, 0, f64(d.latent(shape, 40)))           # replace in the source only
+    assert np.array_equal(c.logical_kv(1, 0)[0], k1)    # destination unchanged
+    with pytest.raises(KeyError):
+        c.share(1, 0, 5)
