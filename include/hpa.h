@@ -130,6 +130,16 @@ hpa_status_t hpa_latent_set_install_batch(hpa_cache_t* c, int32_t n, const int32
                                           const int32_t* set_ids, const int32_t* m_rows,
                                           const void* const* kv_ptrs, hpa_stream_t stream,
                                           int32_t* set_ids_out);
+/* Shared document memory ("KV cache server for storing
+ * and retrieving compressed document memories"): appends to dst_seq a new LATENT
+ * set that references the physical pages of src_seq's set src_set_id (page
+ * refcounts +1; no copy, O(pages) host work, no kernel). A document retrieved by
+ * many requests is stored once. Shared pages are read-only: replacing a shared
+ * set in any sequence writes fresh pages for that sequence only (copy-on-write);
+ * removing / releasing drops that sequence's references. *set_id_out receives
+ * dst's new set id. Errors: HPA_ERR_UNKNOWN_SEQ / _UNKNOWN_SET / _SEQ_CAPACITY. */
+hpa_status_t hpa_latent_set_share(hpa_cache_t* c, int32_t dst_seq, int32_t src_seq, int32_t src_set_id,
+                                  int32_t* set_id_out);
 /* Removes a latent set (frees its pages, splices the table). */
 hpa_status_t hpa_latent_set_remove(hpa_cache_t* c, int32_t seq_id, int32_t set_id);
 

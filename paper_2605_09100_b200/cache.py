@@ -155,6 +155,12 @@ class Cache:
                                    ctypes.byref(out)))
         return out.value
 
+    def latent_share(self, dst_seq: int, src_seq: int, src_set_id: int) -> int:
+        """hpa_latent_set_share: dst gets a new LATENT set referencing src's pages."""
+        out = c_i32()
+        check(LIB.hpa_latent_set_share(self._h, dst_seq, src_seq, src_set_id, ctypes.byref(out)))
+        return out.value
+
     def latent_remove(self, seq: int, set_id: int) -> None:
         check(LIB.hpa_latent_set_remove(self._h, seq, set_id))
 

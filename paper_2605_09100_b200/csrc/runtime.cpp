@@ -150,6 +150,7 @@ class PageAllocator {
   void release(int32_t p) {
     if (--refcnt_[p] == 0) free_.push_back(p);
   }
+  void retain(int32_t p) { ++refcnt_[p]; }
   int32_t refcount(int32_t p) const { return refcnt_[p]; }
 
  private:
@@ -726,8 +727,11 @@ hpa_status_t plan_install(hpa_cache_t* c, int32_t seq, int32_t set_id, int32_t m
     for (int32_t i = 0; i < int32_t(q.segs.size()); ++i)
       if (q.segs[i].latent && q.segs[i].set_id == set_id) p->seg_index = i;
     if (p->seg_index < 0) return fail(HPA_ERR_UNKNOWN_SET, "sequence %d has no latent set %d", seq, set_id);
-    p->old_pages = int32_t(q.segs[p->seg_index].pages.size());
-    if (p->old_pages == np) p->new_pages = 0;  // rewrite in place
+    const Segment& g = q.segs[p->seg_index];
+    p->old_pages = int32_t(g.pages.size());
+    bool shared = false;
+    for (int32_t pg : g.pages) shared |= c->alloc.refcount(pg) > 1;
+    if (p->old_pages == np && !shared) p->new_pages = 0;  // rewrite in place (never into shared pages)
   }
   const int32_t delta = p->new_pages - (p->new_pages ? p->old_pages : 0);
   if (seq_entries(q) + delta > c->cfg.max_pages_per_seq)
@@ -782,7 +786,9 @@ hpa_status_t hpa_latent_set_install_batch(hpa_cache_t* c, int32_t n, const int32
     if (seen[seq_ids[i]]) return fail(HPA_ERR_INVALID_ARG, "sequence %d listed twice", seq_ids[i]);
     seen[seq_ids[i]] = 1;
     need += plans[i].new_pages;
-    if (plans[i].new_pages && !plans[i].is_new) freed += plans[i].old_pages;
+    if (plans[i].new_pages && !plans[i].is_new) {  // only sole references return pages to the pool
+      for (int32_t pg : c->seqs[seq_ids[i]].segs[plans[i].seg_index].pages) freed += c->alloc.refcount(pg) == 1;
+    }
   }
   // replaced sets free their pages before allocating (all-or-nothing budget)
   if (need > c->alloc.num_free() + freed)
@@ -832,6 +838,27 @@ hpa_status_t hpa_latent_set_install(hpa_cache_t* c, int32_t seq_id, int32_t set_
   hpa_status_t st = hpa_latent_set_install_batch(c, 1, &seq_id, &set_id, &m_rows, &kv, stream, &out);
   if (st == HPA_OK && set_id_out) *set_id_out = out;
   return st;
+}
+
+hpa_status_t hpa_latent_set_share(hpa_cache_t* c, int32_t dst_seq, int32_t src_seq, int32_t src_set_id,
+                                  int32_t* set_id_out) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (hpa_status_t st = check_seq(c, dst_seq)) return st;
+  if (hpa_status_t st = check_seq(c, src_seq)) return st;
+  const Segment* src = nullptr;
+  for (const Segment& g : c->seqs[src_seq].segs)
+    if (g.latent && g.set_id == src_set_id) src = &g;
+  if (!src) return fail(HPA_ERR_UNKNOWN_SET, "sequence %d has no latent set %d", src_seq, src_set_id);
+  Seq& d = c->seqs[dst_seq];
+  if (seq_entries(d) + int32_t(src->pages.size()) > c->cfg.max_pages_per_seq)
+    return fail(HPA_ERR_SEQ_CAPACITY, "sequence %d would exceed %d pages", dst_seq, c->cfg.max_pages_per_seq);
+  Segment g{true, d.next_set++, src->rows, src->pages};  // copy first: src may live in d.segs
+  for (int32_t pg : g.pages) c->alloc.retain(pg);
+  const int32_t first_entry = seq_entries(d);
+  d.segs.push_back(std::move(g));
+  c->rebuild(dst_seq, first_entry);
+  if (set_id_out) *set_id_out = d.segs.back().set_id;
+  return HPA_OK;
 }
 
 hpa_status_t hpa_latent_set_remove(hpa_cache_t* c, int32_t seq_id, int32_t set_id) {

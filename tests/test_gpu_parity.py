@@ -435,3 +435,44 @@ def test_compress_errors_leave_cache_unchanged():
         p.cache.compress(s, 5, 6)              # 11 > 10 rows in the trailing token segment
     assert e.value.name == "HPA_ERR_INVALID_ARG"
     assert p.cache.stats()[0] == before[0][0] - 1
+
+
+# ----------------------------------------------------------------------------- NEXT-2: sharing
+def test_shared_latent_sets_refcount_and_copy_on_write():
+    """A document's latent set installed once and shared by 3 other requests: pages are
+    stored once (stats), decode parity for all, replacement in one request copies on
+    write (others unchanged, bitwise), removal/release drop only references."""
+    shape = Shape(1, 32, 8, 128, 16)
+    p = Pair(shape, num_pages=1024, max_seqs=8, max_pages_per_seq=256)
+    owner = p.build([("latent", 128), ("latent", 40)])     # 8 + 3 pages
+    readers = [p.build([("tokens", 30 + 7 * i)]) for i in range(3)]
+    used0 = p.cache.stats()[1]
+    for r in readers:
+        assert p.cache.latent_share(r, owner, 0) == p.orc.share(r, owner, 0)
+        p.tokens([r], [5])
+    assert p.cache.stats()[1] == used0 + 3                 # only the 3 new token pages
+    seqs = [owner] + readers
+    q = p.queries(4)
+    got = p.cache.decode(0, seqs, q.cuda())
+    torch.cuda.synchronize()
+    check_close(got, oracle_decode(p, seqs, q), "decode with shared sets")
+    before = [p.cache.export_logical_kv(0, s) for s in readers]
+    p.latent(readers[0], 128, set_id=0)                    # copy-on-write replacement
+    assert p.cache.stats()[1] == used0 + 3 + 8
+    p.latent(owner, 128, set_id=0)                         # owner also replaces: shared still by 2
+    torch.cuda.synchronize()
+    for r, (k0, v0) in zip(readers[1:], before[1:]):
+        k1, v1 = p.cache.export_logical_kv(0, r)
+        assert torch.equal(k0, k1) and torch.equal(v0, v1)
+    for s in seqs:
+        k1, v1 = p.orc.logical_kv(s, 0)
+        k2, v2 = p.cache.export_logical_kv(0, s)
+        assert np.array_equal(k1, f64(k2)) and np.array_equal(v1, f64(v2))
+    q = p.queries(4)
+    got = p.cache.decode(0, seqs, q.cuda())
+    torch.cuda.synchronize()
+    check_close(got, oracle_decode(p, seqs, q), "decode after copy-on-write")
+    for r in readers:
+        p.cache.seq_release(r)
+    p.cache.seq_release(owner)
+    assert p.cache.stats() == (1024, 0, 0)
