@@ -140,6 +140,18 @@ hpa_status_t hpa_latent_set_install_batch(hpa_cache_t* c, int32_t n, const int32
  * dst's new set id. Errors: HPA_ERR_UNKNOWN_SEQ / _UNKNOWN_SET / _SEQ_CAPACITY. */
 hpa_status_t hpa_latent_set_share(hpa_cache_t* c, int32_t dst_seq, int32_t src_seq, int32_t src_set_id,
                                   int32_t* set_id_out);
+/* Memory-server staging ("KV cache server for storing
+ * and retrieving compressed document memories"): as hpa_latent_set_install_batch,
+ * but payload i is in HOST memory (host_ptrs[i], [L][2][m_rows[i]][H_kv][d] bf16;
+ * pinned memory gives asynchronous copies). The library copies the payloads to
+ * its device staging buffer on an internal copy stream -- so the transfer overlaps
+ * work already queued on `stream` (e.g. the previous step's decode) -- makes
+ * `stream` wait for the copies, and installs them with one scatter launch. The
+ * host buffers may be reused once `stream` has passed the call. */
+hpa_status_t hpa_latent_set_install_host(hpa_cache_t* c, int32_t n, const int32_t* seq_ids,
+                                         const int32_t* set_ids, const int32_t* m_rows,
+                                         const void* const* host_ptrs, hpa_stream_t stream,
+                                         int32_t* set_ids_out);
 /* Removes a latent set (frees its pages, splices the table). */
 hpa_status_t hpa_latent_set_remove(hpa_cache_t* c, int32_t seq_id, int32_t set_id);
 

@@ -155,6 +155,25 @@ class Cache:
                                    ctypes.byref(out)))
         return out.value
 
+    def latent_install_host(self, seq_ids, set_ids, kv: torch.Tensor, stream=None) -> np.ndarray:
+        """hpa_latent_set_install_host: kv is a (preferably pinned) CPU tensor
+        [n][L][2][m][H_kv][d] bf16; copied on the cache's copy stream, then installed."""
+        ids, sids = _i32(seq_ids), _i32(set_ids)
+        n = ids.size
+        if kv.device.type != "cpu" or kv.dtype != torch.bfloat16 or not kv.is_contiguous():
+            raise ValueError("kv must be a contiguous bf16 CPU tensor")
+        if kv.dim() != 6 or kv.shape[0] != n or tuple(kv.shape[1:3]) != (self.L, 2) \
+                or tuple(kv.shape[4:]) != (self.Hkv, self.d):
+            raise ValueError("kv must be [n][L][2][m][H_kv][d]")
+        m = kv.shape[3]
+        ptrs = (kv.data_ptr() + np.arange(n, dtype=np.uint64) * np.uint64(kv[0].numel() * 2)).astype(np.uint64)
+        ms = np.full(n, m, dtype=np.int32)
+        out = np.zeros(n, dtype=np.int32)
+        check(LIB.hpa_latent_set_install_host(self._h, n, _p32(ids), _p32(sids), _p32(ms),
+                                              ptrs.ctypes.data_as(ctypes.POINTER(c_vp)),
+                                              _stream(self.device, stream), _p32(out)))
+        return out
+
     def latent_share(self, dst_seq: int, src_seq: int, src_set_id: int) -> int:
         """hpa_latent_set_share: dst gets a new LATENT set referencing src's pages."""
         out = c_i32()

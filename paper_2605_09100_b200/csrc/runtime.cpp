@@ -287,6 +287,11 @@ struct hpa_cache {
   int32_t* counters = nullptr;  // [max_seqs][H_kv], zero between calls
   size_t part_elems = 0;
   int32_t forced_splits = 0;
+  // host-staged installs (NEXT-3): device payload buffer filled on copy_stream
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_done = nullptr, payload_free = nullptr;
+  char* payload_dev = nullptr;
+  size_t payload_cap = 0;
   long long* trace = nullptr;  // prefill phase trace (HPA_TRACE builds; set via hpa_debug_trace)
   int num_sms = 148;
   uint64_t launches = 0;
@@ -574,6 +579,12 @@ hpa_status_t hpa_cache_create(const hpa_config_t* cfg, hpa_cache_t** out) {
     cleanup();
     return fail(HPA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the KV pools");
   }
+  if ((e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&c->copy_done, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&c->payload_free, cudaEventDisableTiming)) != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "copy stream setup");
+  }
   if ((e = decode_init_attributes()) != cudaSuccess || (e = prefill_init_attributes()) != cudaSuccess) {
     cleanup();
     return cuda_fail(e, "kernel attribute setup");
@@ -597,6 +608,10 @@ hpa_status_t hpa_cache_destroy(hpa_cache_t* c) {
   if (c->o_part) cudaFree(c->o_part);
   if (c->lse_part) cudaFree(c->lse_part);
   if (c->counters) cudaFree(c->counters);
+  if (c->payload_dev) cudaFree(c->payload_dev);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->copy_done) cudaEventDestroy(c->copy_done);
+  if (c->payload_free) cudaEventDestroy(c->payload_free);
   c->ring.destroy();
   delete c;
   return HPA_OK;
@@ -830,6 +845,48 @@ hpa_status_t hpa_latent_set_install_batch(hpa_cache_t* c, int32_t n, const int32
     max_rows = std::max<int64_t>(max_rows, p.m);
   }
   return ship(c, static_cast<cudaStream_t>(stream), recs, slots, max_rows);
+}
+
+hpa_status_t hpa_latent_set_install_host(hpa_cache_t* c, int32_t n, const int32_t* seq_ids,
+                                         const int32_t* set_ids, const int32_t* m_rows,
+                                         const void* const* host_ptrs, hpa_stream_t stream,
+                                         int32_t* set_ids_out) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (n < 0) return fail(HPA_ERR_INVALID_ARG, "n < 0");
+  if (n == 0) return HPA_OK;
+  if (!seq_ids || !set_ids || !m_rows || !host_ptrs) return fail(HPA_ERR_INVALID_ARG, "null argument");
+  const size_t row_bytes = size_t(c->cfg.num_kv_heads) * c->cfg.head_dim * 2;
+  std::vector<size_t> off(n);
+  size_t total = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    if (m_rows[i] <= 0 || !host_ptrs[i]) return fail(HPA_ERR_INVALID_ARG, "bad payload %d", i);
+    off[i] = total;
+    total += (size_t(c->cfg.num_layers) * 2 * m_rows[i] * row_bytes + 255) & ~size_t(255);
+  }
+  DeviceGuard dg(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (total > c->payload_cap) {  // grow (rare): wait for the previous user of the buffer
+    HPA_CUDA(cudaStreamSynchronize(c->copy_stream));
+    HPA_CUDA(cudaEventSynchronize(c->payload_free));
+    if (c->payload_dev) cudaFree(c->payload_dev);
+    c->payload_dev = nullptr;
+    HPA_CUDA(cudaMalloc(&c->payload_dev, total));
+    c->payload_cap = total;
+  }
+  // copies wait (on the GPU) until the previous host install's scatter has read the buffer
+  HPA_CUDA(cudaStreamWaitEvent(c->copy_stream, c->payload_free, 0));
+  std::vector<const void*> dev_ptrs(n);
+  for (int32_t i = 0; i < n; ++i) {
+    const size_t bytes = size_t(c->cfg.num_layers) * 2 * m_rows[i] * row_bytes;
+    HPA_CUDA(cudaMemcpyAsync(c->payload_dev + off[i], host_ptrs[i], bytes, cudaMemcpyHostToDevice, c->copy_stream));
+    dev_ptrs[i] = c->payload_dev + off[i];
+  }
+  HPA_CUDA(cudaEventRecord(c->copy_done, c->copy_stream));
+  HPA_CUDA(cudaStreamWaitEvent(s, c->copy_done, 0));
+  hpa_status_t st = hpa_latent_set_install_batch(c, n, seq_ids, set_ids, m_rows, dev_ptrs.data(), stream,
+                                                 set_ids_out);
+  HPA_CUDA(cudaEventRecord(c->payload_free, s));
+  return st;
 }
 
 hpa_status_t hpa_latent_set_install(hpa_cache_t* c, int32_t seq_id, int32_t set_id, int32_t m_rows,

@@ -476,3 +476,27 @@ def test_shared_latent_sets_refcount_and_copy_on_write():
         p.cache.seq_release(r)
     p.cache.seq_release(owner)
     assert p.cache.stats() == (1024, 0, 0)
+
+
+# ----------------------------------------------------------------------------- NEXT-3: host staging
+def test_install_from_host_payloads():
+    """hpa_latent_set_install_host (pinned host payloads, internal copy stream) installs the
+    same bits as the device-payload path; repeated calls reuse the staging buffer while
+    decodes are queued in between."""
+    shape = Shape(1, 32, 8, 128, 16)
+    p = Pair(shape, num_pages=2048, max_seqs=8, max_pages_per_seq=256)
+    seqs = [p.build([("latent", 128), ("tokens", 200 + 50 * i)]) for i in range(4)]
+    for step in range(3):
+        kv = torch.stack([p.draw.latent(shape, 128) for _ in seqs]).pin_memory()   # [n][L][2][m][Hkv][d]
+        sid = [0] * 4 if step else [-1] * 4
+        got = p.cache.latent_install_host(seqs, sid, kv)
+        for i, s in enumerate(seqs):
+            assert got[i] == p.orc.install(s, sid[i], f64(kv[i]))
+        q = p.queries(4)
+        out = p.cache.decode(0, seqs, q.cuda())
+        torch.cuda.synchronize()
+        check_close(out, oracle_decode(p, seqs, q), f"decode after host install {step}")
+    for s in seqs:
+        k1, v1 = p.orc.logical_kv(s, 0)
+        k2, v2 = p.cache.export_logical_kv(0, s)
+        assert np.array_equal(k1, f64(k2)) and np.array_equal(v1, f64(v2))
