@@ -27,6 +27,7 @@ model would write into latent pages is unpinned (no weights; synthetic data).
 from .hpa_oracle import (  # noqa: F401
     OracleCache,
     attend,
+    attend_span,
     gather_physical,
     kv_cache_bytes,
     expected_table,

@@ -244,6 +244,32 @@ def attend(q: np.ndarray, k_log: np.ndarray, v_log: np.ndarray, scale: float) ->
     return out
 
 
+def attend_span(q: np.ndarray, k_log: np.ndarray, v_log: np.ndarray, scale: float,
+                span_lo: int, span_hi: int, q_from: int) -> np.ndarray:
+    """attend() with the GRC mask-out span (SURVEY §8(f) NEXT-4a; §2, P:L177-183:
+    "we mask out the k vectors in the first segment when computing attention scores from
+    the segment ❸ so that q vectors in segment ❸ only attend to the k vectors of meta
+    latent tokens ... while q vectors of meta latent tokens can attend to the k vectors
+    in segment ❶"). A query at logical index i >= q_from does not see keys j with
+    span_lo <= j < span_hi; other queries follow the plain causal rule (reading A1)."""
+    q = np.asarray(q, dtype=np.float64)
+    k_log = np.asarray(k_log, dtype=np.float64)
+    v_log = np.asarray(v_log, dtype=np.float64)
+    tq, hq_n, d = q.shape
+    hkv, lb, _ = k_log.shape
+    group = hq_n // hkv
+    out = np.zeros((tq, hq_n, d), dtype=np.float64)
+    for hq in range(hq_n):
+        h = hq // group
+        for t in range(tq):
+            i = lb - tq + t
+            keys = [j for j in range(i + 1) if not (i >= q_from and span_lo <= j < span_hi)]
+            s = scale * (k_log[h, keys] @ q[t, hq])
+            p = np.exp(s - s.max())
+            out[t, hq] = (p @ v_log[h, keys]) / p.sum()
+    return out
+
+
 def decode_reference(cache: OracleCache, seq_id: int, layer: int, q: np.ndarray,
                      scale: float) -> np.ndarray:
     """Decode: the query is the last logical row (reading A8). q: [Hq][d]."""

@@ -328,3 +328,28 @@ def test_share_copies_logical_rows_and_isolates_updates():
     assert np.array_equal(c.logical_kv(1, 0)[0], k1)    # destination unchanged
     with pytest.raises(KeyError):
         c.share(1, 0, 5)
+
+
+def test_attend_span_vs_sdpa_and_absent_segment():
+    """NEXT-4a: the GRC mask-out span (P:L177-183). (i) equals SDPA with the explicit mask;
+    (ii) for segment-3 queries it equals plain causal attention over the cache with segment 1
+    removed (reading A4: at inference the segment-1 pages are simply absent); (iii) the
+    latent-token queries (i < q_from) still see segment 1."""
+    from oracle import attend_span
+    rng = np.random.default_rng(11)
+    n1, m, n3, hq, hkv, d = 40, 8, 12, 4, 2, 16
+    lb = n1 + m + n3
+    k = rng.standard_normal((hkv, lb, d))
+    v = rng.standard_normal((hkv, lb, d))
+    q = rng.standard_normal((m + n3, hq, d))
+    got = attend_span(q, k, v, 0.25, 0, n1, n1 + m)
+    i = torch.arange(m + n3)[:, None] + n1
+    j = torch.arange(lb)[None, :]
+    mask = (j <= i) & ~((i >= n1 + m) & (j < n1))
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        torch.from_numpy(q).transpose(0, 1), torch.from_numpy(k).repeat_interleave(2, 0),
+        torch.from_numpy(v).repeat_interleave(2, 0), attn_mask=mask, scale=0.25).transpose(0, 1)
+    assert np.max(np.abs(got - ref.numpy())) <= 1e-12
+    absent = attend(q[m:], k[:, n1:], v[:, n1:], 0.25)
+    assert np.max(np.abs(got[m:] - absent)) <= 1e-12
+    assert np.max(np.abs(got[:m] - attend(q, k, v, 0.25)[:m])) <= 1e-12
