@@ -189,6 +189,15 @@ hpa_status_t hpa_prefill(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
                          const int32_t* q_lens /*host*/, const void* q, void* out,
                          float softmax_scale, hpa_stream_t stream);
 
+/* Chunked prefill with the GRC mask-out span (SURVEY §8(f) NEXT-4a; §2,
+ * queries of segment ❸ must not see segment ❶ while the meta latent
+ * tokens do). As hpa_prefill, plus span (host int32 [n_seqs][3] = lo, hi, q_from):
+ * a query at logical index i >= q_from does not attend keys lo <= j < hi. Requires
+ * 0 <= lo <= hi <= q_from (so every query still sees itself). */
+hpa_status_t hpa_prefill_span(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
+                              const int32_t* q_lens /*host*/, const int32_t* span /*host*/,
+                              const void* q, void* out, float softmax_scale, hpa_stream_t stream);
+
 /* ---------------------------------------------------------------- introspection / tests
  * Host-side sequence summary. */
 hpa_status_t hpa_seq_info(hpa_cache_t* c, int32_t seq_id, int32_t* len, int32_t* n_pages,

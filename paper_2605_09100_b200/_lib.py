@@ -52,6 +52,7 @@ SIGNATURES = {
                                            c_i32p]),
     "hpa_decode": (c_st, [c_vp, c_i32, c_i32, c_i32p, c_vp, c_vp, ctypes.c_float, c_vp]),
     "hpa_prefill": (c_st, [c_vp, c_i32, c_i32, c_i32p, c_i32p, c_vp, c_vp, ctypes.c_float, c_vp]),
+    "hpa_prefill_span": (c_st, [c_vp, c_i32, c_i32, c_i32p, c_i32p, c_i32p, c_vp, c_vp, ctypes.c_float, c_vp]),
     "hpa_seq_info": (c_st, [c_vp, c_i32, c_i32p, c_i32p, c_i32p]),
     "hpa_export_logical_kv": (c_st, [c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "hpa_export_table": (c_st, [c_vp, c_i32, c_i32p, c_i32p, c_u16p, c_i32, c_i32p]),

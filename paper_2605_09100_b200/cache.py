@@ -210,6 +210,23 @@ class Cache:
                               float(scale), _stream(self.device, stream)))
         return out
 
+    def prefill_span(self, layer: int, seq_ids: Sequence[int], q_lens: Sequence[int], spans,
+                     q: torch.Tensor, out: Optional[torch.Tensor] = None, scale: float = 0.0,
+                     stream=None) -> torch.Tensor:
+        """hpa_prefill_span: spans[i] = (lo, hi, q_from) -- GRC mask-out span per sequence."""
+        ids, ql = _i32(seq_ids), _i32(q_lens)
+        sp = _i32(spans)
+        if sp.size != 3 * ids.size:
+            raise ValueError("spans must be [n][3]")
+        shape = (int(ql.sum()), self.Hq, self.d)
+        qp = self._dev_tensor(q, "q", shape)
+        if out is None:
+            out = torch.empty(shape, dtype=torch.bfloat16, device=q.device)
+        op = self._dev_tensor(out, "out", shape)
+        check(LIB.hpa_prefill_span(self._h, layer, ids.size, _p32(ids), _p32(ql), _p32(sp), c_vp(qp),
+                                   c_vp(op), float(scale), _stream(self.device, stream)))
+        return out
+
     # ------------------------------------------------------------------ introspection
     def seq_info(self, seq: int) -> Tuple[int, int, int]:
         a, b, c = c_i32(), c_i32(), c_i32()

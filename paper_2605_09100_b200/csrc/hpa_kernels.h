@@ -110,6 +110,7 @@ struct PrefillArgs {
   int32_t n_seqs, Hq, Hkv, G, P, NP, layer, max_q_len;
   float scale_log2;
   int32_t log2P;
+  const int32_t* span;      // [n][3] device (lo, hi, q_from) or nullptr: GRC mask-out span
   long long* trace;         // HPA_TRACE builds only: per-phase clock64 stamps of CTA (0,0,0)
 };
 // tm_q: 3-D map over q [sum q][Hq][d] with box {64, 1, 128};

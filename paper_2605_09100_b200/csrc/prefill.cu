@@ -61,6 +61,7 @@ constexpr int kSoftmaxRegs = HPA_SOFTMAX_REGS;
 constexpr int kOtherRegs = HPA_OTHER_REGS;
 static_assert(2 * kSoftmaxRegs + kOtherRegs <= 3 * 168, "setmaxnreg budget");
 constexpr float kRescaleThreshold = 8.0f;  // log2 units (factor 256)
+constexpr int kSpanBit = 1 << 30;          // tags span columns in the mask indices (seq_len < 2^30)
 #ifndef HPA_POLY_EVERY
 #define HPA_POLY_EVERY 0  // 1 of every N exp2 pairs on the FMA pipe (0 = all on MUFU; measured best)
 #endif
@@ -268,6 +269,11 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   const int i_min = q_base + mt_s[0] * kBM;                     // smallest row index in the CTA
   const int last_mt = slot1_live ? mt_s[1] : mt_s[0];
   const int i_max = q_base + min(q_len, (last_mt + 1) * kBM) - 1;
+  // GRC mask-out span (NEXT-4a): queries with logical index >= q_from do not see keys in
+  // [span_lo, span_hi). The producer tags span columns with kSpanBit in their logical
+  // index; a row with i >= q_from compares the tagged index (always > i), other rows
+  // compare the index with the tag masked off.
+  const int span_from = a.span ? a.span[3 * b + 2] : INT_MAX;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -330,6 +336,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         const int e = slot >> lp, r = slot & (P - 1);
         int v = INT_MAX;
         if (e < n_ent && r < (mt_[e] & kMetaRowsMask)) v = p0[e] + r;
+        if (a.span && v >= a.span[3 * b] && v < a.span[3 * b + 1]) v |= kSpanBit;
         col[c] = v;
         vis &= (v <= i_min);
       }
@@ -474,13 +481,14 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       tc_wait_ld();
       if (row == 0) TRACE(9 + s, j);
       if (!all_vis) {
+        const int cmask = my_i >= span_from ? -1 : ~kSpanBit;  // span tag visible only to span rows
 #pragma unroll
         for (int c = 0; c < kBN; c += 4) {
           const int4 ci = *reinterpret_cast<const int4*>(col + c);
-          x[c + 0] = ci.x <= my_i ? x[c + 0] : -CUDART_INF_F;
-          x[c + 1] = ci.y <= my_i ? x[c + 1] : -CUDART_INF_F;
-          x[c + 2] = ci.z <= my_i ? x[c + 2] : -CUDART_INF_F;
-          x[c + 3] = ci.w <= my_i ? x[c + 3] : -CUDART_INF_F;
+          x[c + 0] = (ci.x & cmask) <= my_i ? x[c + 0] : -CUDART_INF_F;
+          x[c + 1] = (ci.y & cmask) <= my_i ? x[c + 1] : -CUDART_INF_F;
+          x[c + 2] = (ci.z & cmask) <= my_i ? x[c + 2] : -CUDART_INF_F;
+          x[c + 3] = (ci.w & cmask) <= my_i ? x[c + 3] : -CUDART_INF_F;
         }
       }
       // row max as a tree (8 independent partial maxima), not a 64-deep chain
@@ -514,7 +522,9 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
       // p = 2^(x*sl2 - m): f32x2 FFMA for the argument; 3 of every 4 pairs on the
       // MUFU ex2 unit, 1 pair on the FMA pipe (degree-3 polynomial, rel. err 1e-4)
-      const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_new, -m_new);
+      // a row with nothing visible yet (span-masked leading tiles) keeps p = 0, not NaN
+      const float m_use = m_new == -CUDART_INF_F ? 0.f : m_new;
+      const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_use, -m_use);
       float2 rs4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
       for (int half = 0; half < 2; ++half) {

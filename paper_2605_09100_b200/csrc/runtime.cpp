@@ -527,6 +527,8 @@ hpa_status_t hpa_cache_create(const hpa_config_t* cfg, hpa_cache_t** out) {
   if (rows >= (int64_t(1) << 31)) return fail(HPA_ERR_UNSUPPORTED, "pool too large for 32-bit TMA row index");
   if (int64_t(g.max_seqs) * g.max_pages_per_seq * 3 + 2 * g.max_seqs >= (int64_t(1) << 31))
     return fail(HPA_ERR_UNSUPPORTED, "table too large");
+  if (int64_t(g.max_pages_per_seq) * g.page_size >= (int64_t(1) << 30))
+    return fail(HPA_ERR_UNSUPPORTED, "sequences must stay below 2^30 rows");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || g.device < 0 || g.device >= ndev)
     return fail(HPA_ERR_INVALID_ARG, "CUDA device %d not available", g.device);
@@ -1022,9 +1024,29 @@ hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int
   return HPA_OK;
 }
 
+namespace {
+hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
+                          const int32_t* q_lens, const int32_t* span, const void* q, void* out,
+                          float softmax_scale, hpa_stream_t stream);
+}
+
 hpa_status_t hpa_prefill(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
                          const int32_t* q_lens, const void* q, void* out, float softmax_scale,
                          hpa_stream_t stream) {
+  return prefill_impl(c, layer, n_seqs, seq_ids, q_lens, nullptr, q, out, softmax_scale, stream);
+}
+
+hpa_status_t hpa_prefill_span(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
+                              const int32_t* q_lens, const int32_t* span, const void* q, void* out,
+                              float softmax_scale, hpa_stream_t stream) {
+  if (!span) return fail(HPA_ERR_INVALID_ARG, "null span");
+  return prefill_impl(c, layer, n_seqs, seq_ids, q_lens, span, q, out, softmax_scale, stream);
+}
+
+namespace {
+hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
+                          const int32_t* q_lens, const int32_t* span, const void* q, void* out,
+                          float softmax_scale, hpa_stream_t stream) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
   if (layer < 0 || layer >= c->cfg.num_layers) return fail(HPA_ERR_INVALID_ARG, "layer %d out of range", layer);
   if (n_seqs < 0) return fail(HPA_ERR_INVALID_ARG, "n_seqs < 0");
@@ -1032,7 +1054,7 @@ hpa_status_t hpa_prefill(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
   if (!seq_ids || !q_lens || !q || !out) return fail(HPA_ERR_INVALID_ARG, "null argument");
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15)
     return fail(HPA_ERR_INVALID_ARG, "q / out must be 16-byte aligned");
-  std::vector<int32_t> meta(size_t(3) * n_seqs);  // rows | q_len | q_off
+  std::vector<int32_t> meta(size_t(span ? 6 : 3) * n_seqs);  // rows | q_len | q_off [| span lo,hi,from]
   int64_t total_q = 0;
   int32_t max_q = 0;
   for (int32_t i = 0; i < n_seqs; ++i) {
@@ -1043,6 +1065,14 @@ hpa_status_t hpa_prefill(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
     meta[i] = seq_ids[i];
     meta[n_seqs + i] = q_lens[i];
     meta[2 * n_seqs + i] = int32_t(total_q);
+    if (span) {
+      const int32_t lo = span[3 * i], hi = span[3 * i + 1], from = span[3 * i + 2];
+      if (lo < 0 || hi < lo || from < hi)
+        return fail(HPA_ERR_INVALID_ARG, "span %d must satisfy 0 <= lo <= hi <= q_from", i);
+      meta[3 * n_seqs + 3 * i] = lo;
+      meta[3 * n_seqs + 3 * i + 1] = hi;
+      meta[3 * n_seqs + 3 * i + 2] = from;
+    }
     total_q += q_lens[i];
     max_q = std::max(max_q, q_lens[i]);
   }
@@ -1062,7 +1092,8 @@ hpa_status_t hpa_prefill(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
   const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt(float(D));
   PrefillArgs a{c->dt, dmeta, dmeta + n_seqs, dmeta + 2 * n_seqs, out, n_seqs, Hq, c->cfg.num_kv_heads,
                 Hq / c->cfg.num_kv_heads, c->cfg.page_size, c->cfg.num_pages, layer, max_q,
-                scale * 1.4426950408889634f, __builtin_ctz(uint32_t(c->cfg.page_size)), c->trace};
+                scale * 1.4426950408889634f, __builtin_ctz(uint32_t(c->cfg.page_size)),
+                span ? dmeta + 3 * n_seqs : nullptr, c->trace};
   int launched = 0;
   cudaError_t e = launch_prefill(tm_q, c->tm_k_pre, c->tm_v_pre, a, D, s, &launched);
   c->launches += launched;
@@ -1070,6 +1101,7 @@ hpa_status_t hpa_prefill(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
   HPA_CUDA(c->ring.commit(off, bytes, s));
   return HPA_OK;
 }
+}  // namespace
 
 hpa_status_t hpa_seq_info(hpa_cache_t* c, int32_t seq_id, int32_t* len, int32_t* n_pages, int32_t* n_latent_rows) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");

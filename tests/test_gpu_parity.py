@@ -500,3 +500,45 @@ def test_install_from_host_payloads():
         k1, v1 = p.orc.logical_kv(s, 0)
         k2, v2 = p.cache.export_logical_kv(0, s)
         assert np.array_equal(k1, f64(k2)) and np.array_equal(v1, f64(v2))
+
+
+# ----------------------------------------------------------------------------- NEXT-4a: mask-out span
+@pytest.mark.parametrize("hq,hkv,P", [(32, 8, 16), (8, 8, 64), (6, 2, 32)])
+def test_prefill_span_grc_mask(hq, hkv, P):
+    """Eq. (1) layout [segment 1 (n1) | latents (m) | segment 3 (n3)]: the m + n3 queries run
+    with span (0, n1, n1 + m); parity with oracle.attend_span; rows of segment 3 equal plain
+    prefill over a cache without segment 1."""
+    from oracle import attend_span
+    shape = Shape(1, hq, hkv, 128, P)
+    p = Pair(shape, num_pages=2048, max_seqs=8, max_pages_per_seq=256)
+    cases = [(300, 16, 150), (40, 128, 200), (0, 8, 50), (257, 64, 1)]
+    seqs, q_lens, spans = [], [], []
+    for n1, m, n3 in cases:
+        s = p.new_seq()
+        p.tokens([s], [n1]) if n1 else None
+        p.latent(s, m)
+        p.tokens([s], [n3])
+        seqs.append(s)
+        q_lens.append(m + n3)
+        spans.append((0, n1, n1 + m))
+    q = p.queries(sum(q_lens))
+    got = p.cache.prefill_span(0, seqs, q_lens, spans, q.cuda())
+    torch.cuda.synchronize()
+    ref, off = [], 0
+    for s, ql, (lo, hi, qf) in zip(seqs, q_lens, spans):
+        k, v = p.orc.logical_kv(s, 0)
+        ref.append(attend_span(f64(q[off:off + ql]), k, v, shape.scale, lo, hi, qf))
+        off += ql
+    ref = np.concatenate(ref)
+    check_close(got, ref, "prefill span")
+    # segment-3 rows == a cache whose segment-1 pages are absent (reading A4)
+    p2 = Pair(shape, num_pages=2048, max_seqs=8, max_pages_per_seq=256)
+    n1, m, n3 = cases[0]
+    s2 = p2.new_seq()
+    k, v = p.orc.logical_kv(seqs[0], 0)
+    kk = torch.from_numpy(k[:, n1:]).to(torch.bfloat16).permute(1, 0, 2).unsqueeze(0).contiguous()
+    vv = torch.from_numpy(v[:, n1:]).to(torch.bfloat16).permute(1, 0, 2).unsqueeze(0).contiguous()
+    p2.cache.append_kv([s2], [m + n3], kk.cuda(), vv.cuda())
+    plain = p2.cache.prefill(0, [s2], [m + n3], q[:m + n3].cuda())
+    torch.cuda.synchronize()
+    assert torch.max(torch.abs(plain[m:].float() - got[m:m + n3].float())) <= 2e-2
