@@ -338,6 +338,7 @@ def run_ours(args):
         res["prefill"] = bench_prefill(torch, Cache, shape, dev, stream, pk, pk_kind, max_over_ranks)
         res["lmag"] = bench_lmag(torch, Cache, shape, dev, stream, max(3, min(W, 5)), min(K, 20),
                                  world, max_over_ranks, barrier)
+        res["next"] = bench_next(torch, Cache, shape, dev, stream, pk, max_over_ranks)
     if rank == 0 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(budget_s=15.0)
     if rank == 0:
@@ -432,6 +433,117 @@ def bench_lmag(torch, Cache, shape, dev, stream, W, K, world, max_over_ranks, ba
             "step_ms": round(step, 4), "install_ms": round(inst, 4), "decode_ms": round(dec, 4),
             "install_gbs": round(inst_bytes / (inst / 1e3) / 1e9, 1),
             "decode_gbs": round(dbytes / (dec / 1e3) / 1e9, 1)}
+
+
+def bench_next(torch, Cache, shape, dev, stream, pk, max_over_ranks):
+    """Measurements for the SURVEY §8(f) NEXT rows (one layer each)."""
+    import numpy as np
+    from workloads import LATENT_ROWS
+    out = {}
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    g = torch.Generator(device=f"cuda:{dev}").manual_seed(31)
+    # NEXT-1: in-cache compression of a 4096-token document into m = 128 latent rows, B = 64
+    B, n_doc, m = 64, 4096, LATENT_ROWS
+    cache, seqs, _ = build_decode_cache(torch, Cache, shape, B, 8, n_doc + m, 0, dev, seed=41)
+    free0 = cache.stats()[0]
+    torch.cuda.synchronize(dev)
+    e0, e1 = ev(), ev()
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for s in seqs:
+        cache.compress(s, n_doc, m)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    host_s = time.perf_counter() - t0
+    ms = e0.elapsed_time(e1)
+    moved = B * m * shape.num_kv_heads * shape.head_dim * 2 * 2 * 2  # K+V rows read + written
+    out["compress"] = {"workload": f"B={B}: 4096-token document + 128 meta-latent rows -> 128-row latent set",
+                       "ms_total": round(ms, 4), "us_per_document": round(ms * 1e3 / B, 2),
+                       "host_us_per_document": round(host_s * 1e6 / B, 1),
+                       "pages_freed": cache.stats()[0] - free0, "moved_gbs": round(moved / (ms / 1e3) / 1e9, 1)}
+    cache.close()
+    # NEXT-2: decode with 8 document sets shared by all 64 requests vs private copies
+    B, tokens = 64, 4095
+    P = shape.page_size
+    pages = 8 * (LATENT_ROWS // P) + B * (-(-(tokens + 64) // P) + 1) + 64
+    cache = Cache(1, 32, 8, 128, P, pages, B + 1, 8 * (LATENT_ROWS // P) + (tokens + 64) // P + 2, dev, 99)
+    owner = cache.seq_create()
+    kv = torch.randn((8, 1, 2, LATENT_ROWS, 8, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+    for i in range(8):
+        cache.latent_install(owner, -1, kv[i])
+    seqs = [cache.seq_create() for _ in range(B)]
+    for s in seqs:
+        for i in range(8):
+            cache.latent_share(s, owner, i)
+    k = torch.randn((1, B * tokens, 8, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+    cache.append_kv(seqs, [tokens] * B, k, k)
+    q = torch.randn((B, 32, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+    o = torch.empty_like(q)
+    ids = np.asarray(seqs, dtype=np.int32)
+    for _ in range(3):
+        cache.decode(0, ids, q, o)
+    torch.cuda.synchronize(dev)
+    e0, e1 = ev(), ev()
+    e0.record(stream)
+    for _ in range(20):
+        cache.decode(0, ids, q, o)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / 20
+    lens = [cache.seq_info(s)[0] for s in seqs]
+    out["shared_sets"] = {"workload": "B=64 decode, the same 8 latent sets shared by every request (stored once)",
+                          "decode_ms": round(ms, 4), "tokens_per_s": round(B / (ms / 1e3), 1),
+                          "logical_gbs": round(decode_bytes(lens, shape) / (ms / 1e3) / 1e9, 1),
+                          "latent_pages_stored": 8 * (LATENT_ROWS // P),
+                          "latent_pages_if_private": B * 8 * (LATENT_ROWS // P)}
+    cache.close()
+    # NEXT-3: LMAG-style replacement from pinned host payloads (copy stream) overlapped with decode
+    B = 256
+    cache, seqs, _ = build_decode_cache(torch, Cache, shape, B, 8, 4095, 16, dev, seed=43)
+    ids = np.asarray(seqs, dtype=np.int32)
+    host = torch.randn((2, B, 1, 2, LATENT_ROWS, 8, 128), generator=g, device=f"cuda:{dev}").to(
+        torch.bfloat16).cpu().pin_memory()
+    q = torch.randn((B, 32, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+    o = torch.empty_like(q)
+    sets = [np.full(B, k, dtype=np.int32) for k in range(8)]
+    for i in range(2):
+        cache.latent_install_host(ids, sets[i], host[i % 2])
+        cache.decode(0, ids, q, o)
+    torch.cuda.synchronize(dev)
+    e0, e1 = ev(), ev()
+    e0.record(stream)
+    steps = 6
+    for i in range(steps):
+        cache.latent_install_host(ids, sets[i % 8], host[i % 2])
+        cache.decode(0, ids, q, o)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    payload = B * LATENT_ROWS * 8 * 128 * 2 * 2
+    out["host_staged_install"] = {"workload": "B=256: replace one 128-row set per request from pinned host + decode",
+                                  "step_ms": round(ms, 4), "h2d_bytes_per_step": payload,
+                                  "h2d_gbs": round(payload / (ms / 1e3) / 1e9, 1)}
+    cache.close()
+    # NEXT-4a: GRC mask-out-span prefill: C = 2048 queries, segment 1 = the first 8192 token rows
+    n1, c_rows = 8192, 2048
+    cache, seqs, _ = build_decode_cache(torch, Cache, shape, 1, 8, 16384 + c_rows, 0, dev, seed=45)
+    q = torch.randn((c_rows, 32, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+    span = [(1024, 1024 + n1, 1024 + 16384)]  # all C queries are in segment 3; segment 1 follows the latents
+    for _ in range(2):
+        cache.prefill_span(0, seqs, [c_rows], span, q)
+    torch.cuda.synchronize(dev)
+    e0, e1 = ev(), ev()
+    e0.record(stream)
+    for _ in range(5):
+        cache.prefill_span(0, seqs, [c_rows], span, q)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / 5
+    flops = prefill_flops(8 * 128 + 16384 - n1, c_rows, shape)  # visible pairs only
+    out["span_prefill"] = {"workload": "configs[2] with a masked 8192-row segment 1 (GRC Eq. 1 mask)",
+                           "ms": round(ms, 4), "tflops_visible": round(flops / (ms / 1e3) / 1e12, 1)}
+    cache.close()
+    return out
 
 
 # ----------------------------------------------------------------------------- CPU baseline

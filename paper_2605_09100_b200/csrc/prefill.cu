@@ -92,7 +92,7 @@ struct PSmem {
   // o_full, c_full[NC], c_empty[NC]
   static constexpr int kNBar = 1 + 2 * kNK + 2 * kNV + 2 + 4 + 1 + 2 * kNC;
   static constexpr int oMisc = oBar + kNBar * 8;
-  static constexpr int kRaw = oMisc + 16 + 1024;
+  static constexpr int kRaw = oMisc + 16 + 1024;  // tmem addr + 3 tile words
   // >= 116 KB so exactly one CTA is resident per SM (it owns all 512 TMEM columns)
   static constexpr int kBytes = kRaw > 116 * 1024 ? kRaw : 116 * 1024;
 };
@@ -254,7 +254,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   uint64_t* c_full = o_full + 1;
   uint64_t* c_empty = c_full + kNC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::oMisc);
-  int32_t* ntiles_slot = reinterpret_cast<int32_t*>(sm + L::oMisc + 4);
+  int32_t* ntiles_slot = reinterpret_cast<int32_t*>(sm + L::oMisc + 4);  // [n_tiles, skip_a, n_skip]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int seq = a.seq_rows[b];
@@ -284,14 +284,27 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     mbar_init(o_full, 1);
     for (int i = 0; i < kNC; ++i) { mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], 8); }
     fence_barrier_init();
-    // key tiles needed: the tile holding the slot of logical index i_max
-    int lo = 0, hi = n_ent - 1;  // last entry with pos0 <= i_max
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (p0[mid] <= i_max) lo = mid; else hi = mid - 1;
+    // key slot of a logical index x: the last entry with pos0 <= x, plus the row offset
+    auto slot_of = [&](int x) {
+      int lo = 0, hi = n_ent - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (p0[mid] <= x) lo = mid; else hi = mid - 1;
+      }
+      return (lo << lp) + (x - p0[lo]);
+    };
+    // key tiles needed: up to the tile holding the slot of logical index i_max
+    ntiles_slot[0] = slot_of(i_max) / kBN + 1;
+    // tiles entirely inside the GRC span are skipped when every query row of the CTA
+    // is a span row (their keys are all masked): iteration jj -> tile jj (+ skip)
+    int skip_a = 0, skip_b = 0;
+    if (a.span && i_min >= span_from && a.span[3 * b + 1] > a.span[3 * b]) {
+      skip_a = (slot_of(a.span[3 * b]) + kBN - 1) / kBN;
+      skip_b = (slot_of(a.span[3 * b + 1] - 1) + 1) / kBN;
+      if (skip_b < skip_a) skip_b = skip_a;
     }
-    const int slot = (lo << lp) + (i_max - p0[lo]);
-    *ntiles_slot = slot / kBN + 1;
+    ntiles_slot[1] = skip_a;
+    ntiles_slot[2] = skip_b - skip_a;
   }
   if (warp == kMmaWarp) {  // TMEM: S/P 0 [0,128), S/P 1 [128,256), O0 [256,..), O1 [384,..)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -302,7 +315,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int n_tiles = *ntiles_slot;
+  const int skip_a = ntiles_slot[1], n_skip = ntiles_slot[2];
+  const int n_tiles = ntiles_slot[0] - n_skip;  // iterations; tile(jj) = jj < skip_a ? jj : jj + n_skip
 
   if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kOtherRegs));
   if (warp == kProducerWarp) {
@@ -324,6 +338,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     constexpr int kOobRow = INT_MAX / 2;  // fully out-of-bounds box -> TMA zero fill
     const int head_row = a.layer * a.NP;
     for (int j = 0; j < n_tiles; ++j) {
+      const int tile = j < skip_a ? j : j + n_skip;
       // logical index of every key slot (INT_MAX: row >= valid_rows or past the table)
       const int cs = j % kNC;
       if (j >= kNC) mbar_wait(&c_empty[cs], ((j / kNC) - 1) & 1);
@@ -332,7 +347,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #pragma unroll
       for (int x = 0; x < kBN / 32; ++x) {
         const int c = x * 32 + lane;
-        const int slot = j * kBN + c;
+        const int slot = tile * kBN + c;
         const int e = slot >> lp, r = slot & (P - 1);
         int v = INT_MAX;
         if (e < n_ent && r < (mt_[e] & kMetaRowsMask)) v = p0[e] + r;
@@ -346,7 +361,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       // page box coordinates (lane bx < nbox owns box bx)
       int row = kOobRow;
       if (lane < nbox) {
-        const int slot = j * kBN + lane * pbox;
+        const int slot = tile * kBN + lane * pbox;
         const int e = slot >> lp;
         if (e < n_ent) row = ((head_row + bt[e]) * a.Hkv + h) * P + (slot & (P - 1));
       }
@@ -370,9 +385,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     constexpr int kOobRow = INT_MAX / 2;
     const int head_row = a.layer * a.NP;
     for (int j = 0; j < n_tiles; ++j) {
+      const int tile = j < skip_a ? j : j + n_skip;
       int row = kOobRow;
       if (lane < nbox) {
-        const int slot = j * kBN + lane * pbox;
+        const int slot = tile * kBN + lane * pbox;
         const int e = slot >> lp;
         if (e < n_ent) row = ((head_row + bt[e]) * a.Hkv + h) * P + (slot & (P - 1));
       }
