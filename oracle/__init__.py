@@ -28,6 +28,8 @@ from .hpa_oracle import (  # noqa: F401
     OracleCache,
     attend,
     attend_span,
+    merge_partials,
+    partial_attend,
     gather_physical,
     kv_cache_bytes,
     expected_table,

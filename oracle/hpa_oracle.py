@@ -270,6 +270,34 @@ def attend_span(q: np.ndarray, k_log: np.ndarray, v_log: np.ndarray, scale: floa
     return out
 
 
+def partial_attend(q: np.ndarray, k_part: np.ndarray, v_part: np.ndarray, scale: float):
+    """Context-parallel decode, one shard (SURVEY §8(f) NEXT-4b): attention of one query
+    row per head over a shard of the logical keys (all visible: the query is the
+    sequence's last row). Returns (o [Hq][d] normalised over the shard,
+    lse2 [Hq] = log2 sum_j exp(s_j))."""
+    q = np.asarray(q, dtype=np.float64)
+    hq_n, d = q.shape
+    hkv = k_part.shape[0]
+    group = hq_n // hkv
+    o = np.zeros((hq_n, d))
+    lse2 = np.zeros(hq_n)
+    for hq in range(hq_n):
+        s = scale * (k_part[hq // group] @ q[hq])
+        mx = s.max()
+        p = np.exp(s - mx)
+        o[hq] = (p @ v_part[hq // group]) / p.sum()
+        lse2[hq] = (mx + math.log(p.sum())) / math.log(2.0)
+    return o, lse2
+
+
+def merge_partials(o_parts: np.ndarray, lse2_parts: np.ndarray) -> np.ndarray:
+    """o = sum_r 2^(lse_r - LSE) o_r / sum_r 2^(lse_r - LSE): exact recombination of
+    shard softmaxes (the same identity as the split combine, a5)."""
+    m = lse2_parts.max(axis=0)
+    w = np.exp2(lse2_parts - m)                       # [R][Hq]
+    return (w[..., None] * o_parts).sum(axis=0) / w.sum(axis=0)[..., None]
+
+
 def decode_reference(cache: OracleCache, seq_id: int, layer: int, q: np.ndarray,
                      scale: float) -> np.ndarray:
     """Decode: the query is the last logical row (reading A8). q: [Hq][d]."""

@@ -353,3 +353,23 @@ def test_attend_span_vs_sdpa_and_absent_segment():
     absent = attend(q[m:], k[:, n1:], v[:, n1:], 0.25)
     assert np.max(np.abs(got[m:] - absent)) <= 1e-12
     assert np.max(np.abs(got[:m] - attend(q, k, v, 0.25)[:m])) <= 1e-12
+
+
+def test_partial_attend_and_merge_equal_full_attention():
+    """NEXT-4b: shard softmaxes recombined by LSE equal attention over all keys (SDPA)."""
+    from oracle import merge_partials, partial_attend
+    rng = np.random.default_rng(12)
+    hq, hkv, d, lb = 8, 2, 16, 97
+    k = rng.standard_normal((hkv, lb, d))
+    v = rng.standard_normal((hkv, lb, d))
+    q = rng.standard_normal((hq, d))
+    cuts = [0, 30, 31, 80, lb]
+    parts = [partial_attend(q, k[:, a:b], v[:, a:b], 0.3) for a, b in zip(cuts[:-1], cuts[1:])]
+    got = merge_partials(np.stack([p[0] for p in parts]), np.stack([p[1] for p in parts]))
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        torch.from_numpy(q)[:, None], torch.from_numpy(k).repeat_interleave(4, 0),
+        torch.from_numpy(v).repeat_interleave(4, 0), scale=0.3)[:, 0]
+    assert np.max(np.abs(got - ref.numpy())) <= 1e-12
+    o1, l1 = partial_attend(q, k, v, 0.3)           # one shard: lse is log2 sum exp(s)
+    s0 = 0.3 * (k[0] @ q[0])
+    assert abs(l1[0] - np.log2(np.exp(s0).sum())) <= 1e-12
