@@ -180,6 +180,22 @@ hpa_status_t hpa_seq_compress(hpa_cache_t* c, int32_t seq_id, int32_t n_doc_rows
 hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
                         const void* q, void* out, float softmax_scale, hpa_stream_t stream);
 
+/* Context-parallel decode (SURVEY §8(f) NEXT-4b: contexts beyond one GPU's pool,
+ * pages sharded by row range across GPUs). As hpa_decode, but over the rows this
+ * cache holds for each sequence (a shard of the logical sequence; the query is the
+ * LAST row of the full sequence, so every stored row is visible) and the result is
+ * a mergeable partial: o_part fp32 [n_seqs][Hq][d] (normalised over the shard) and
+ * lse_part fp32 [n_seqs][Hq] = log2 sum_j exp(s_j) over the shard (device). */
+hpa_status_t hpa_decode_partial(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
+                                const void* q, float* o_part, float* lse_part, float softmax_scale,
+                                hpa_stream_t stream);
+/* Merges n_parts partials (device, laid out [n_parts][n_rows][head_dim] and
+ * [n_parts][n_rows], e.g. after an all-gather over NVLink) into bf16
+ * out [n_rows][head_dim]: out = sum_p 2^(lse_p - LSE) o_p / sum_p 2^(lse_p - LSE).
+ * Stateless; runs on the current CUDA device. n_rows = n_seqs * Hq. */
+hpa_status_t hpa_merge_partials(int32_t n_parts, int32_t n_rows, int32_t head_dim, const float* o_parts,
+                                const float* lse_parts, void* out, hpa_stream_t stream);
+
 /* Chunked prefill (a6): queries of sequence i are its LAST q_lens[i] logical
  * rows (1 <= q_lens[i] <= seq_len; their KV appended first). Query row t sits at
  * logical index i = seq_len - q_len + t and attends keys j <= i (bottom-right

@@ -9,6 +9,6 @@ host without an sm_100 GPU.
 PAPER.md §3 "Hybrid paged attention for LLM serving".
 """
 from ._lib import HPAError, kv_bytes, lib_path  # noqa: F401
-from .cache import Cache  # noqa: F401
+from .cache import Cache, merge_partials  # noqa: F401
 
-__all__ = ["Cache", "HPAError", "kv_bytes", "lib_path"]
+__all__ = ["Cache", "HPAError", "kv_bytes", "lib_path", "merge_partials"]

@@ -32,6 +32,21 @@ class _CAI:
                                          "data": (ptr, False), "version": 2, "strides": None}
 
 
+def merge_partials(o_parts: torch.Tensor, lse_parts: torch.Tensor, stream=None) -> torch.Tensor:
+    """hpa_merge_partials: o_parts fp32 [P][n][Hq][d], lse_parts fp32 [P][n][Hq] (CUDA) ->
+    bf16 [n][Hq][d]."""
+    if o_parts.dtype != torch.float32 or lse_parts.dtype != torch.float32 or o_parts.device.type != "cuda":
+        raise ValueError("partials must be fp32 CUDA tensors")
+    o_parts = o_parts.contiguous()
+    lse_parts = lse_parts.contiguous()
+    n_parts, d = o_parts.shape[0], o_parts.shape[-1]
+    rows = lse_parts[0].numel()
+    out = torch.empty(o_parts.shape[1:], dtype=torch.bfloat16, device=o_parts.device)
+    check(LIB.hpa_merge_partials(n_parts, rows, d, c_vp(o_parts.data_ptr()), c_vp(lse_parts.data_ptr()),
+                                 c_vp(out.data_ptr()), _stream(o_parts.device.index, stream)))
+    return out
+
+
 class Cache:
     """Hybrid paged KV cache on one B200 (include/hpa.h, hpa_cache_create).
 
@@ -196,6 +211,17 @@ class Cache:
         check(LIB.hpa_decode(self._h, layer, ids.size, _p32(ids), c_vp(qp), c_vp(op), float(scale),
                              _stream(self.device, stream)))
         return out
+
+    def decode_partial(self, layer: int, seq_ids: Sequence[int], q: torch.Tensor, scale: float = 0.0,
+                       stream=None) -> Tuple[torch.Tensor, torch.Tensor]:
+        """hpa_decode_partial: (o fp32 [n][Hq][d], lse2 fp32 [n][Hq]) over this cache's shard."""
+        ids = _i32(seq_ids)
+        qp = self._dev_tensor(q, "q", (ids.size, self.Hq, self.d))
+        o = torch.empty((ids.size, self.Hq, self.d), dtype=torch.float32, device=q.device)
+        lse = torch.empty((ids.size, self.Hq), dtype=torch.float32, device=q.device)
+        check(LIB.hpa_decode_partial(self._h, layer, ids.size, _p32(ids), c_vp(qp), c_vp(o.data_ptr()),
+                                     c_vp(lse.data_ptr()), float(scale), _stream(self.device, stream)))
+        return o, lse
 
     def prefill(self, layer: int, seq_ids: Sequence[int], q_lens: Sequence[int], q: torch.Tensor,
                 out: Optional[torch.Tensor] = None, scale: float = 0.0, stream=None) -> torch.Tensor:

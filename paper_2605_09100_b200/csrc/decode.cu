@@ -269,7 +269,7 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_const
       }
     }
     const int hq = h * G + g;
-    if (a.splits == 1) {
+    if (a.splits == 1 && !a.part_o) {
       static_cast<__nv_bfloat16*>(a.out)[(int64_t(b) * a.Hq + hq) * D + dcol] = __float2bfloat16_rn(Os / Ls);
     } else {
       const int64_t pi = (int64_t(b) * a.Hq + hq) * a.splits + split;
@@ -277,7 +277,7 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_const
       if (dcol == 0) a.lse_part[pi] = Ls > 0.f ? M + __log2f(Ls) : -CUDART_INF_F;
     }
   }
-  if (a.splits == 1 || !HPA_FUSED_COMBINE) return;
+  if (a.splits == 1 || !HPA_FUSED_COMBINE || a.part_o) return;
   // ------------------------------------------------ a5: the last split of (b, h) combines
   //   O = sum_s 2^(lse_s - LSE) O_s / sum_s 2^(lse_s - LSE)   (fp32, log2 domain)
   named_bar_sync(1, kNT);  // every consumer's partial writes precede thread 0's release
@@ -339,10 +339,12 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_const
 }
 
 // a5 as a separate kernel (HPA_FUSED_COMBINE=0): one CTA per (request, q-head).
+// With part_o set (context-parallel shard) it writes fp32 O and the merged LSE instead.
+// The same kernel merges context-parallel shards (lse/o_part laid out [rows][S]).
 template <int D>
 __global__ void __launch_bounds__(D) combine_kernel(const float* __restrict__ o_part,
                                                     const float* __restrict__ lse, __nv_bfloat16* out,
-                                                    int S) {
+                                                    int S, float* part_o, float* part_lse) {
   grid_dependency_wait();
   const int64_t bh = blockIdx.x;
   const float* ls = lse + bh * S;
@@ -354,7 +356,31 @@ __global__ void __launch_bounds__(D) combine_kernel(const float* __restrict__ o_
     W += w;
     acc += w * o_part[(bh * S + s) * D + threadIdx.x];
   }
-  out[bh * D + threadIdx.x] = __float2bfloat16_rn(acc / W);
+  if (part_o) {
+    part_o[bh * D + threadIdx.x] = acc / W;
+    if (threadIdx.x == 0) part_lse[bh] = M + __log2f(W);
+  } else {
+    out[bh * D + threadIdx.x] = __float2bfloat16_rn(acc / W);
+  }
+}
+
+// Context-parallel merge: parts laid out [P][rows] (as all-gathered); one CTA per row.
+template <int D>
+__global__ void __launch_bounds__(D) merge_kernel(const float* __restrict__ o_parts,
+                                                  const float* __restrict__ lse_parts, __nv_bfloat16* out,
+                                                  int n_parts, int64_t n_rows) {
+  grid_dependency_wait();
+  const int64_t r = blockIdx.x;
+  float M = -CUDART_INF_F;
+  for (int p = 0; p < n_parts; ++p) M = fmaxf(M, lse_parts[p * n_rows + r]);
+  float W = 0.f, acc = 0.f;
+  for (int p = 0; p < n_parts; ++p) {
+    const float l = lse_parts[p * n_rows + r];
+    const float w = l == -CUDART_INF_F ? 0.f : fast_exp2(l - M);
+    W += w;
+    acc += w * o_parts[(p * n_rows + r) * D + threadIdx.x];
+  }
+  out[r * D + threadIdx.x] = __float2bfloat16_rn(acc / W);
 }
 
 template <int D>
@@ -365,16 +391,28 @@ cudaError_t launch_decode_d(const CUtensorMap& tm_k, const CUtensorMap& tm_v, co
                              smem, s, tm_k, tm_v, a);
   if (e != cudaSuccess) return e;
   ++*launches;
-  if (a.splits > 1 && !HPA_FUSED_COMBINE) {
+  if ((a.splits > 1 && !HPA_FUSED_COMBINE) || a.part_o) {
     e = launch_pdl(combine_kernel<D>, dim3(a.n_seqs * a.Hq), dim3(D), 0, s,
                    static_cast<const float*>(a.o_part), static_cast<const float*>(a.lse_part),
-                   static_cast<__nv_bfloat16*>(a.out), a.splits);
+                   static_cast<__nv_bfloat16*>(a.out), a.splits, a.part_o, a.part_lse);
     ++*launches;
   }
   return e;
 }
 
 }  // namespace
+
+cudaError_t launch_merge(int32_t n_parts, int32_t n_rows, int32_t D, const float* o_parts,
+                         const float* lse_parts, void* out, cudaStream_t s) {
+  if (n_rows == 0) return cudaSuccess;
+  if (D == 128)
+    return launch_pdl(merge_kernel<128>, dim3(n_rows), dim3(128), 0, s, o_parts, lse_parts,
+                      static_cast<__nv_bfloat16*>(out), n_parts, int64_t(n_rows));
+  if (D == 64)
+    return launch_pdl(merge_kernel<64>, dim3(n_rows), dim3(64), 0, s, o_parts, lse_parts,
+                      static_cast<__nv_bfloat16*>(out), n_parts, int64_t(n_rows));
+  return cudaErrorInvalidValue;
+}
 
 cudaError_t decode_init_attributes() {
   cudaError_t e = cudaFuncSetAttribute(decode_split_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -89,9 +89,14 @@ struct DecodeArgs {
   float* o_part;            // fp32 [n][Hq][S][d]   (S > 1)
   float* lse_part;          // fp32 [n][Hq][S]      (log2 domain)
   int32_t* counters;        // [n][Hkv] zero; split-arrival counters for the fused combine
+  float* part_o;            // context-parallel partial output (or nullptr): fp32 [n][Hq][d]
+  float* part_lse;          //   and log2-sum-exp [n][Hq]
   int32_t n_seqs, Hq, Hkv, G, P, NP, layer, splits;
   float scale_log2;         // softmax_scale * log2(e)
 };
+// Merge of context-parallel partials: out[r][:] = sum_p 2^(lse_p - LSE) o_p / sum_p 2^(lse_p - LSE).
+cudaError_t launch_merge(int32_t n_parts, int32_t n_rows, int32_t D, const float* o_parts,
+                         const float* lse_parts, void* out, cudaStream_t s);
 // tm_k / tm_v: 2-D tensor maps over the pools viewed as [L*NP*H_kv*P][d],
 // box {64, 16}, 128-B swizzle.
 cudaError_t launch_decode(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,

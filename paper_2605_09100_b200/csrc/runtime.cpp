@@ -977,14 +977,45 @@ hpa_status_t hpa_seq_compress(hpa_cache_t* c, int32_t seq_id, int32_t n_doc_rows
   return ship(c, static_cast<cudaStream_t>(stream), recs, idx, m_rows);
 }
 
+namespace {
+hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids, const void* q,
+                         void* out, float* part_o, float* part_lse, float softmax_scale, hpa_stream_t stream);
+}
+
 hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids, const void* q,
                         void* out, float softmax_scale, hpa_stream_t stream) {
+  if (!out) return fail(HPA_ERR_INVALID_ARG, "null out");
+  return decode_impl(c, layer, n_seqs, seq_ids, q, out, nullptr, nullptr, softmax_scale, stream);
+}
+
+hpa_status_t hpa_decode_partial(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
+                                const void* q, float* o_part, float* lse_part, float softmax_scale,
+                                hpa_stream_t stream) {
+  if (!o_part || !lse_part || (reinterpret_cast<uintptr_t>(o_part) & 15))
+    return fail(HPA_ERR_INVALID_ARG, "o_part / lse_part must be device pointers (o_part 16-byte aligned)");
+  return decode_impl(c, layer, n_seqs, seq_ids, q, nullptr, o_part, lse_part, softmax_scale, stream);
+}
+
+hpa_status_t hpa_merge_partials(int32_t n_parts, int32_t n_rows, int32_t head_dim, const float* o_parts,
+                                const float* lse_parts, void* out, hpa_stream_t stream) {
+  if (n_parts <= 0 || n_rows < 0 || !o_parts || !lse_parts || !out)
+    return fail(HPA_ERR_INVALID_ARG, "bad merge arguments");
+  if (head_dim != 64 && head_dim != 128) return fail(HPA_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+  cudaError_t e = launch_merge(n_parts, n_rows, head_dim, o_parts, lse_parts, out,
+                               static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "merge launch");
+  return HPA_OK;
+}
+
+namespace {
+hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids, const void* q,
+                         void* out, float* part_o, float* part_lse, float softmax_scale, hpa_stream_t stream) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
   if (layer < 0 || layer >= c->cfg.num_layers) return fail(HPA_ERR_INVALID_ARG, "layer %d out of range", layer);
   if (n_seqs < 0) return fail(HPA_ERR_INVALID_ARG, "n_seqs < 0");
   if (n_seqs == 0) return HPA_OK;
   if (n_seqs > c->cfg.max_seqs) return fail(HPA_ERR_INVALID_ARG, "n_seqs > max_seqs");
-  if (!seq_ids || !q || !out) return fail(HPA_ERR_INVALID_ARG, "null argument");
+  if (!seq_ids || !q) return fail(HPA_ERR_INVALID_ARG, "null argument");
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15)
     return fail(HPA_ERR_INVALID_ARG, "q / out must be 16-byte aligned");
   int32_t max_entries = 0, max_chunks = 0;
@@ -1001,7 +1032,7 @@ hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int
   if (hpa_status_t st = upload_batch(c, n_seqs, seq_ids, s)) return st;
   const int32_t S = plan_splits(c, n_seqs, max_entries, max_chunks);
   const int32_t D = c->cfg.head_dim, Hq = c->cfg.num_q_heads;
-  if (S > 1) {
+  if (S > 1 || part_o) {
     const size_t need = size_t(n_seqs) * Hq * S;
     if (need > c->part_elems) {
       if (c->o_part) cudaFree(c->o_part);
@@ -1014,7 +1045,8 @@ hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int
     }
   }
   const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt(float(D));
-  DecodeArgs a{c->dt, c->batch_dev, q, out, c->o_part, c->lse_part, c->counters, n_seqs, Hq, c->cfg.num_kv_heads,
+  DecodeArgs a{c->dt, c->batch_dev, q, out, c->o_part, c->lse_part, c->counters, part_o, part_lse, n_seqs, Hq,
+               c->cfg.num_kv_heads,
                Hq / c->cfg.num_kv_heads, c->cfg.page_size, c->cfg.num_pages, layer, S,
                scale * 1.4426950408889634f};
   int launched = 0;
@@ -1023,6 +1055,7 @@ hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int
   if (e != cudaSuccess) return cuda_fail(e, "decode launch");
   return HPA_OK;
 }
+}  // namespace
 
 namespace {
 hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,

@@ -55,3 +55,25 @@ def max_over_ranks(x: float, device=None) -> float:
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def context_parallel_decode(cache, layer: int, seq_ids, q: torch.Tensor, group=None) -> torch.Tensor:
+    """Context-parallel decode (SURVEY §8(f) NEXT-4b): this rank's cache holds a row-range
+    shard of every listed sequence. Partial attention per rank (hpa_decode_partial), one
+    NCCL all-gather of the fp32 partials over NVLink, LSE merge (hpa_merge_partials).
+    Returns bf16 [n][Hq][d] on every rank."""
+    from .cache import merge_partials
+    o, lse = cache.decode_partial(layer, seq_ids, q)
+    o_all, l_all = gather_partials(o, lse, group)
+    return merge_partials(o_all, l_all)
+
+
+def gather_partials(o: torch.Tensor, lse: torch.Tensor, group=None):
+    """All-gathers every rank's partial (o [n][Hq][d], lse [n][Hq]) into rank-major
+    [world][n][Hq][d] / [world][n][Hq] (two all_gather_into_tensor calls)."""
+    world = dist.get_world_size(group)
+    o_all = torch.empty((world,) + tuple(o.shape), dtype=o.dtype, device=o.device)
+    l_all = torch.empty((world,) + tuple(lse.shape), dtype=lse.dtype, device=lse.device)
+    dist.all_gather_into_tensor(o_all.view(world * o.shape[0], *o.shape[1:]), o.contiguous(), group=group)
+    dist.all_gather_into_tensor(l_all.view(world * lse.shape[0], *lse.shape[1:]), lse.contiguous(), group=group)
+    return o_all, l_all

@@ -42,6 +42,15 @@ def _worker(rank, world, port, ret):
                           for i in range(b)])
         got = gather_head_shards(torch.from_numpy(local))
         ok = bool(np.max(np.abs(got.numpy() - full)) <= 1e-12)
+        # context-parallel decode plumbing: each rank holds a row-range shard of every request
+        from oracle import merge_partials, partial_attend
+        from paper_2605_09100_b200.dist import gather_partials
+        cut = [0, 23, lb][rank:rank + 2]
+        parts = [partial_attend(q[i], k[i][:, cut[0]:cut[1]], v[i][:, cut[0]:cut[1]], 0.25) for i in range(b)]
+        o_all, l_all = gather_partials(torch.from_numpy(np.stack([p[0] for p in parts])),
+                                       torch.from_numpy(np.stack([p[1] for p in parts])))
+        merged = merge_partials(o_all.numpy(), l_all.numpy())
+        ok = ok and bool(np.max(np.abs(merged - full)) <= 1e-12)
         mx = max_over_ranks(float(rank + 1))
         ret[rank] = (ok, mx)
     finally:

@@ -542,3 +542,63 @@ def test_prefill_span_grc_mask(hq, hkv, P):
     plain = p2.cache.prefill(0, [s2], [m + n3], q[:m + n3].cuda())
     torch.cuda.synchronize()
     assert torch.max(torch.abs(plain[m:].float() - got[m:m + n3].float())) <= 2e-2
+
+
+# ----------------------------------------------------------------------------- NEXT-4b: context parallel
+@pytest.mark.parametrize("n_shards", [1, 2, 3])
+def test_context_parallel_decode_shards_merge(n_shards):
+    """A long sequence split by row ranges over n shards (one 'rank' per shard, emulated as
+    sequences of one cache): hpa_decode_partial per shard + hpa_merge_partials == the oracle
+    over the full sequence; the fp32 partials match oracle.partial_attend per shard."""
+    from oracle import partial_attend
+    from paper_2605_09100_b200 import merge_partials
+    shape = Shape(1, 32, 8, 128, 16)
+    p = Pair(shape, num_pages=4096, max_seqs=16, max_pages_per_seq=1024)
+    full = [("latent", 128)] * 4 + [("tokens", 3001)]
+    n_req = 3
+    d = Draw(77)
+    # draw each request's rows once (CPU), then split them over the shards
+    req_rows = []
+    for _ in range(n_req):
+        rows = []
+        for kind, n in full:
+            if kind == "latent":
+                kv = d.latent(shape, n)
+                rows.append((kind, kv[:, 0], kv[:, 1]))
+            else:
+                k, v = d.tokens(shape, n)
+                rows.append((kind, k, v))
+        req_rows.append(rows)
+    shard_seqs = [[None] * n_req for _ in range(n_shards)]
+    for r, rows in enumerate(req_rows):
+        k_all = torch.cat([k for _, k, _ in rows], 1)
+        v_all = torch.cat([v for _, _, v in rows], 1)
+        lb = k_all.shape[1]
+        cuts = [lb * i // n_shards for i in range(n_shards + 1)]
+        for sh in range(n_shards):
+            s = p.new_seq()
+            a, b = cuts[sh], cuts[sh + 1]
+            p.cache.append_kv([s], [b - a], k_all[:, a:b].contiguous().cuda(), v_all[:, a:b].contiguous().cuda())
+            p.orc.append(s, f64(k_all[:, a:b]), f64(v_all[:, a:b]))
+            shard_seqs[sh][r] = s
+    q = p.queries(n_req)
+    parts = [p.cache.decode_partial(0, shard_seqs[sh], q.cuda()) for sh in range(n_shards)]
+    out = merge_partials(torch.stack([o for o, _ in parts]), torch.stack([l for _, l in parts]))
+    torch.cuda.synchronize()
+    ref_parts = []
+    for sh in range(n_shards):
+        o_sh, l_sh = [], []
+        for r in range(n_req):
+            k, v = p.orc.logical_kv(shard_seqs[sh][r], 0)
+            o1, l1 = partial_attend(f64(q[r]), k, v, shape.scale)
+            o_sh.append(o1)
+            l_sh.append(l1)
+        ref_parts.append((np.stack(o_sh), np.stack(l_sh)))
+        assert np.max(np.abs(f64(parts[sh][1]) - ref_parts[-1][1])) <= 1e-3       # LSE (log2)
+        assert np.max(np.abs(f64(parts[sh][0]) - ref_parts[-1][0])) <= 1e-2
+    ref = []
+    for r in range(n_req):
+        k = np.concatenate([p.orc.logical_kv(shard_seqs[sh][r], 0)[0] for sh in range(n_shards)], 1)
+        v = np.concatenate([p.orc.logical_kv(shard_seqs[sh][r], 0)[1] for sh in range(n_shards)], 1)
+        ref.append(attend(f64(q[r:r + 1]), k, v, shape.scale)[0])
+    check_close(out, np.stack(ref), f"context-parallel decode over {n_shards} shards")
