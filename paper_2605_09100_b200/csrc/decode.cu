@@ -25,6 +25,7 @@
 #include "ptx.cuh"
 #include <cuda_bf16.h>
 #include <math_constants.h>
+#include <algorithm>
 
 namespace hpa {
 namespace {
@@ -34,6 +35,12 @@ constexpr int kNCons = 4;   // consumer warps per CTA
 constexpr int kNSt = 8;     // ring depth
 #ifndef HPA_FENCE_MODE
 #define HPA_FENCE_MODE 2  // 0: fence.sc (threadfence), 1: fence.acq_rel, 2: atom.acq_rel
+#endif
+#ifndef HPA_DECODE_PERSISTENT
+#define HPA_DECODE_PERSISTENT 1  // persistent CTAs streaming consecutive work units through one ring
+#endif
+#ifndef HPA_DECODE_CTAS_PER_SM
+#define HPA_DECODE_CTAS_PER_SM 3
 #endif
 #ifndef HPA_FUSED_COMBINE
 #define HPA_FUSED_COMBINE 0  // 1: a5 by the last split CTA (atomic + GPU fence: measured slower)
@@ -338,6 +345,312 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_const
   if (tid == 0) a.counters[b * a.Hkv + h] = 0;  // ready for the next call (stream order)
 }
 
+
+// ---------------------------------------------------------------------------
+// Persistent variant: grid = (#SMs x CTAs/SM); CTA c processes work units
+// u = c, c + grid, ... (unit = (request, kv-head, split)). The producer streams
+// the chunks of consecutive units through the same ring, so the pipeline never
+// drains between units: while the consumers merge unit u the next unit's pages
+// are already in flight. Per unit: a 1-D bulk copy of the G q rows into a
+// 2-deep Q buffer, the unit's chunks, then one end-of-unit sentinel per consumer
+// (cmeta 0); after the last unit one end-of-kernel sentinel per consumer (-1).
+template <int D>
+struct PDecodeSmem {
+  static constexpr int kHalves = D / 64;
+  static constexpr int kTileBytes = kChunk * D * 2;
+  static constexpr int kStageBytes = 2 * kTileBytes;
+  static constexpr int oRing = 0;
+  static constexpr int oBar = kNSt * kStageBytes;     // full[NST], empty[NST], q_full[2], q_empty[2]
+  static constexpr int oMeta = oBar + (2 * kNSt + 4) * 8;
+  static constexpr int oZero = (oMeta + kNSt * 4 + 15) & ~15;  // 16 zero bytes: A-operand rows >= G
+  static constexpr int oQ = oZero + 16;                        // 2 x [G][D] q rows (unswizzled)
+  static __host__ __device__ int qbuf(int G) { return G * D * 2; }
+  static __host__ __device__ int oMerge(int G) { return oQ + 2 * qbuf(G); }
+  // no alignment slack: the dynamic smem base is 1024-B aligned (checked in the kernel)
+  static int bytes(int G) { return oMerge(G) + kNCons * G * (D + 2) * 4; }
+};
+
+template <int D>
+__global__ void __launch_bounds__((kNCons + 1) * 32, 3)
+decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                         const DecodeArgs a, int n_units) {
+  using L = PDecodeSmem<D>;
+  extern __shared__ __align__(1024) uint8_t smem_pd[];
+  uint8_t* smem = smem_pd;
+  if (smem_u32(smem) & 1023) __trap();  // TMA 128-B swizzle needs 1024-B aligned stage buffers
+  const int G = a.G;
+  uint8_t* stages = smem + L::oRing;
+  uint8_t* qbuf = smem + L::oQ;
+  const int qbytes = L::qbuf(G);
+  uint8_t* zero = smem + L::oZero;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::oBar);
+  uint64_t* empty = full + kNSt;
+  uint64_t* q_full = empty + kNSt;
+  uint64_t* q_empty = q_full + 2;
+  volatile int32_t* cmeta = reinterpret_cast<int32_t*>(smem + L::oMeta);
+  float* mo = reinterpret_cast<float*>(smem + L::oMerge(G));  // [NCONS][G][D]
+  float* mm = mo + kNCons * G * D;                          // [NCONS][G]
+  float* ml = mm + kNCons * G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int units_per = a.Hkv * a.splits;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kNSt; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], kNCons);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+  }
+  if (threadIdx.x < 4) reinterpret_cast<uint32_t*>(zero)[threadIdx.x] = 0u;
+  __syncthreads();
+  grid_dependency_wait();  // PDL: everything above overlapped the previous kernel
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      uint32_t i = 0;
+      int ul = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ul) {
+        const int b = u / units_per, h = (u / a.splits) % a.Hkv, split = u % a.splits;
+        const int seq = a.seq_rows[b];
+        const int qb = ul & 1;
+        if (ul >= 2) mbar_wait(&q_empty[qb], ((ul >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&q_full[qb], uint32_t(G * D * 2));
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(qbuf + qb * qbytes)),
+            "l"(static_cast<const __nv_bfloat16*>(a.q) + (int64_t(b) * a.Hq + int64_t(h) * G) * D),
+            "r"(uint32_t(G * D * 2)), "r"(smem_u32(&q_full[qb]))
+            : "memory");
+        const int ne = a.t.n_entries[seq];
+        const int e0 = int(int64_t(split) * ne / a.splits);
+        const int e1 = int(int64_t(split + 1) * ne / a.splits);
+        const int32_t* bt = a.t.block_table + int64_t(seq) * a.t.max_pages;
+        const int32_t* mt = a.t.meta + int64_t(seq) * a.t.max_pages;
+        // Table entries are fetched kPf at a time, one batch ahead of the TMA issue, so the
+        // dependent L2 load of block_table/meta is not paid per chunk (P=16: one chunk per page).
+        constexpr int kPf = 8;
+        int pg_n[kPf], mv_n[kPf];
+#pragma unroll
+        for (int j = 0; j < kPf; ++j) {
+          pg_n[j] = e0 + j < e1 ? __ldg(bt + e0 + j) : 0;
+          mv_n[j] = e0 + j < e1 ? __ldg(mt + e0 + j) : 0;
+        }
+        for (int eb = e0; eb < e1; eb += kPf) {
+          int pg[kPf], mv[kPf];
+#pragma unroll
+          for (int j = 0; j < kPf; ++j) {
+            pg[j] = pg_n[j];
+            mv[j] = mv_n[j];
+            const int en = eb + kPf + j;
+            pg_n[j] = en < e1 ? __ldg(bt + en) : 0;
+            mv_n[j] = en < e1 ? __ldg(mt + en) : 0;
+          }
+#pragma unroll
+          for (int j = 0; j < kPf; ++j) {
+            if (eb + j < e1) {
+              const int valid = mv[j] & kMetaRowsMask;
+              const int rowbase = ((a.layer * a.NP + pg[j]) * a.Hkv + h) * a.P;
+              for (int sub = 0; sub * kChunk < valid; ++sub, ++i) {
+                const int slot = i % kNSt;
+                if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
+                cmeta[slot] = min(kChunk, valid - sub * kChunk);
+                mbar_arrive_expect_tx(&full[slot], L::kStageBytes);
+                uint8_t* kd = stages + slot * L::kStageBytes;
+                uint8_t* vd = kd + L::kTileBytes;
+#pragma unroll
+                for (int hf = 0; hf < L::kHalves; ++hf) {
+                  tma_load_2d(kd + hf * 2048, &tm_k, &full[slot], hf * 64, rowbase + sub * kChunk);
+                  tma_load_2d(vd + hf * 2048, &tm_v, &full[slot], hf * 64, rowbase + sub * kChunk);
+                }
+              }
+            }
+          }
+        }
+        for (int c = 0; c < kNCons; ++c, ++i) {  // end of unit: one sentinel per consumer
+          const int slot = i % kNSt;
+          if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
+          cmeta[slot] = 0;
+          mbar_arrive(&full[slot]);
+        }
+      }
+      for (int c = 0; c < kNCons; ++c, ++i) {  // end of kernel
+        const int slot = i % kNSt;
+        if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
+        cmeta[slot] = -1;
+        mbar_arrive(&full[slot]);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int cw = warp - 1;
+  const int tid = threadIdx.x - 32;
+  constexpr int kNT = kNCons * 32;
+  const float sl2 = a.scale_log2;
+  uint32_t i = cw;
+  int ul = 0;
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ul) {
+    const int b = u / units_per, h = (u / a.splits) % a.Hkv, split = u % a.splits;
+    // Q fragments of this unit (rows >= G read the zero chunk)
+    const int qb = ul & 1;
+    mbar_wait(&q_full[qb], (ul >> 1) & 1);
+    uint32_t qa[D / 16][4];
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks) {
+      const int mi = lane >> 3;
+      const int row = (lane & 7) + (mi & 1) * 8;
+      const int kc = ks * 2 + (mi >> 1);
+      const uint8_t* src = row < G ? qbuf + qb * qbytes + row * D * 2 + kc * 16 : zero;
+      ldsm_x4(smem_u32(src), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&q_empty[qb]);
+    float o[D / 8][4];
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m_r[2] = {-CUDART_INF_F, -CUDART_INF_F};
+    float l_r[2] = {0.f, 0.f};
+    for (;; i += kNCons) {
+      const int slot = i % kNSt;
+      mbar_wait(&full[slot], (i / kNSt) & 1);
+      const int nvalid = cmeta[slot];
+      if (nvalid <= 0) {  // sentinel: release the slot and finish the unit
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        i += kNCons;
+        break;
+      }
+      const uint8_t* kt = stages + slot * L::kStageBytes;
+      const uint8_t* vt = kt + L::kTileBytes;
+      float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks) {
+        const int mi = lane >> 3;
+        const int n = (mi >> 1) * 8 + (lane & 7);
+        const int kc = ks * 2 + (mi & 1);
+        uint32_t b00, b01, b10, b11;
+        ldsm_x4(smem_u32(kt + (kc >> 3) * 2048 + sw128(n, kc & 7)), b00, b01, b10, b11);
+        mma_bf16_16816(s[0], qa[ks], b00, b01);
+        mma_bf16_16816(s[1], qa[ks], b10, b11);
+      }
+      float x[2][4];
+      float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int col = j * 8 + 2 * (lane & 3) + (e & 1);
+          x[j][e] = col < nvalid ? s[j][e] * sl2 : -CUDART_INF_F;
+        }
+        mx0 = fmaxf(mx0, fmaxf(x[j][0], x[j][1]));
+        mx1 = fmaxf(mx1, fmaxf(x[j][2], x[j][3]));
+      }
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float mn0 = fmaxf(m_r[0], mx0), mn1 = fmaxf(m_r[1], mx1);
+      const float al0 = fast_exp2(m_r[0] - mn0), al1 = fast_exp2(m_r[1] - mn1);
+      m_r[0] = mn0;
+      m_r[1] = mn1;
+      float p[2][4];
+      float ps0 = 0.f, ps1 = 0.f;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        p[j][0] = fast_exp2(x[j][0] - mn0);
+        p[j][1] = fast_exp2(x[j][1] - mn0);
+        p[j][2] = fast_exp2(x[j][2] - mn1);
+        p[j][3] = fast_exp2(x[j][3] - mn1);
+        ps0 += p[j][0] + p[j][1];
+        ps1 += p[j][2] + p[j][3];
+      }
+      l_r[0] = l_r[0] * al0 + ps0;
+      l_r[1] = l_r[1] * al1 + ps1;
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        o[n][0] *= al0;
+        o[n][1] *= al0;
+        o[n][2] *= al1;
+        o[n][3] *= al1;
+      }
+      uint32_t pa[4];
+      pa[0] = pack_bf16(p[0][0], p[0][1]);
+      pa[1] = pack_bf16(p[0][2], p[0][3]);
+      pa[2] = pack_bf16(p[1][0], p[1][1]);
+      pa[3] = pack_bf16(p[1][2], p[1][3]);
+#pragma unroll
+      for (int dp = 0; dp < D / 16; ++dp) {
+        const int mi = lane >> 3;
+        const int key = (mi & 1) * 8 + (lane & 7);
+        const int dc = dp * 2 + (mi >> 1);
+        uint32_t v0, v1, v2, v3;
+        ldsm_x4_t(smem_u32(vt + (dc >> 3) * 2048 + sw128(key, dc & 7)), v0, v1, v2, v3);
+        mma_bf16_16816(o[2 * dp], pa, v0, v1);
+        mma_bf16_16816(o[2 * dp + 1], pa, v2, v3);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    // ---------------------------------------------- merge the consumers' states
+    l_r[0] += __shfl_xor_sync(0xffffffffu, l_r[0], 1);
+    l_r[0] += __shfl_xor_sync(0xffffffffu, l_r[0], 2);
+    l_r[1] += __shfl_xor_sync(0xffffffffu, l_r[1], 1);
+    l_r[1] += __shfl_xor_sync(0xffffffffu, l_r[1], 2);
+    {
+      const int g0 = lane >> 2, g1 = g0 + 8;
+#pragma unroll
+      for (int n = 0; n < D / 8; ++n) {
+        const int dcol = n * 8 + 2 * (lane & 3);
+        if (g0 < G) {
+          mo[(cw * G + g0) * D + dcol] = o[n][0];
+          mo[(cw * G + g0) * D + dcol + 1] = o[n][1];
+        }
+        if (g1 < G) {
+          mo[(cw * G + g1) * D + dcol] = o[n][2];
+          mo[(cw * G + g1) * D + dcol + 1] = o[n][3];
+        }
+      }
+      if ((lane & 3) == 0) {
+        if (g0 < G) { mm[cw * G + g0] = m_r[0]; ml[cw * G + g0] = l_r[0]; }
+        if (g1 < G) { mm[cw * G + g1] = m_r[1]; ml[cw * G + g1] = l_r[1]; }
+      }
+    }
+    named_bar_sync(1, kNT);
+    for (int idx = tid; idx < G * D; idx += kNT) {
+      const int g = idx / D, dcol = idx % D;
+      float M = -CUDART_INF_F;
+#pragma unroll
+      for (int c = 0; c < kNCons; ++c) M = fmaxf(M, mm[c * G + g]);
+      float Ls = 0.f, Os = 0.f;
+      if (M != -CUDART_INF_F) {
+#pragma unroll
+        for (int c = 0; c < kNCons; ++c) {
+          const float w = fast_exp2(mm[c * G + g] - M);
+          Ls += w * ml[c * G + g];
+          Os += w * mo[(c * G + g) * D + dcol];
+        }
+      }
+      const int hq = h * G + g;
+      if (a.splits == 1 && !a.part_o) {
+        static_cast<__nv_bfloat16*>(a.out)[(int64_t(b) * a.Hq + hq) * D + dcol] = __float2bfloat16_rn(Os / Ls);
+      } else {
+        const int64_t pi = (int64_t(b) * a.Hq + hq) * a.splits + split;
+        a.o_part[pi * D + dcol] = Ls > 0.f ? Os / Ls : 0.f;
+        if (dcol == 0) a.lse_part[pi] = Ls > 0.f ? M + __log2f(Ls) : -CUDART_INF_F;
+      }
+    }
+    named_bar_sync(1, kNT);  // merge area free for the next unit
+  }
+}
+
 // a5 as a separate kernel (HPA_FUSED_COMBINE=0): one CTA per (request, q-head).
 // With part_o set (context-parallel shard) it writes fp32 O and the merged LSE instead.
 // The same kernel merges context-parallel shards (lse/o_part laid out [rows][S]).
@@ -386,9 +699,25 @@ __global__ void __launch_bounds__(D) merge_kernel(const float* __restrict__ o_pa
 template <int D>
 cudaError_t launch_decode_d(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,
                             cudaStream_t s, int* launches) {
-  const int smem = DecodeSmem<D>::kBytes;
-  cudaError_t e = launch_pdl(decode_split_kernel<D>, dim3(a.splits, a.Hkv, a.n_seqs), dim3((kNCons + 1) * 32),
-                             smem, s, tm_k, tm_v, a);
+  cudaError_t e;
+  if (HPA_DECODE_PERSISTENT) {
+    const int smem = PDecodeSmem<D>::bytes(a.G);
+    static int num_sms = 0;
+    if (num_sms == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int per_sm = std::min(HPA_DECODE_CTAS_PER_SM, (227 * 1024) / (smem + 1024));
+    const int n_units = a.n_seqs * a.Hkv * a.splits;
+    const int grid = std::max(1, std::min(n_units, num_sms * per_sm));
+    e = launch_pdl(decode_persistent_kernel<D>, dim3(grid), dim3((kNCons + 1) * 32), smem, s, tm_k, tm_v, a,
+                   n_units);
+  } else {
+    const int smem = DecodeSmem<D>::kBytes;
+    e = launch_pdl(decode_split_kernel<D>, dim3(a.splits, a.Hkv, a.n_seqs), dim3((kNCons + 1) * 32), smem, s,
+                   tm_k, tm_v, a);
+  }
   if (e != cudaSuccess) return e;
   ++*launches;
   if ((a.splits > 1 && !HPA_FUSED_COMBINE) || a.part_o) {
@@ -418,6 +747,12 @@ cudaError_t decode_init_attributes() {
   cudaError_t e = cudaFuncSetAttribute(decode_split_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        DecodeSmem<128>::kBytes);
   if (e != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(decode_persistent_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                PDecodeSmem<128>::bytes(16))) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(decode_persistent_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                PDecodeSmem<64>::bytes(16))) != cudaSuccess)
+    return e;
   return cudaFuncSetAttribute(decode_split_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               DecodeSmem<64>::kBytes);
 }

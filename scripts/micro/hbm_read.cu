@@ -1,0 +1,68 @@
+// Read-only HBM ceiling: (a) streaming int4 reads, (b) random 4 KB tiles via 1-D TMA-free loads
+// (the decode's access granularity: one (page, head) tile = 4 KB contiguous).
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+__global__ void stream_read(const int4* __restrict__ p, size_t n, int* out) {
+  int acc = 0;
+  size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += 4 * stride) {
+    int4 a = __ldg(p + i), b = i + stride < n ? __ldg(p + i + stride) : int4{0,0,0,0};
+    int4 c = i + 2 * stride < n ? __ldg(p + i + 2 * stride) : int4{0,0,0,0};
+    int4 d = i + 3 * stride < n ? __ldg(p + i + 3 * stride) : int4{0,0,0,0};
+    acc ^= a.x ^ b.y ^ c.z ^ d.w;
+  }
+  if (acc == 0x12345678) out[0] = acc;
+}
+// each warp reads whole 4 KB tiles at random tile indices (perm), 8 tiles in flight per warp
+__global__ void tile_read(const int4* __restrict__ p, const uint32_t* __restrict__ perm, int ntiles, int* out) {
+  int acc = 0;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t0 = warp * 8; t0 < ntiles; t0 += nwarps * 8) {
+    int4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      int t = t0 + u < ntiles ? perm[t0 + u] : perm[0];
+      const int4* base = p + size_t(t) * 256;  // 4 KB tile = 256 int4
+      v[u] = __ldg(base + lane);                // 512 B per u; unroll 8 sub-blocks below
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc ^= v[u].x;
+#pragma unroll
+    for (int s = 1; s < 8; ++s) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        int t = t0 + u < ntiles ? perm[t0 + u] : perm[0];
+        acc ^= __ldg(p + size_t(t) * 256 + s * 32 + lane).y;
+      }
+    }
+  }
+  if (acc == 0x12345678) out[0] = acc;
+}
+int main() {
+  size_t bytes = size_t(8) << 30;  // 8 GB
+  int4* p; int* out; cudaMalloc(&p, bytes); cudaMalloc(&out, 4); cudaMemset(p, 1, bytes);
+  size_t n = bytes / 16;
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int grid : {148 * 4, 148 * 8, 148 * 16}) for (int blk : {256, 512}) {
+    stream_read<<<grid, blk>>>(p, n, out); cudaDeviceSynchronize();
+    cudaEventRecord(a); for (int r = 0; r < 5; ++r) stream_read<<<grid, blk>>>(p, n, out); cudaEventRecord(b);
+    cudaEventSynchronize(b); float ms; cudaEventElapsedTime(&ms, a, b);
+    printf("stream read grid %d x %d: %.1f GB/s\n", grid, blk, 5.0 * bytes / (ms / 1e3) / 1e9);
+  }
+  int ntiles = int(bytes / 4096);
+  uint32_t* perm_h = new uint32_t[ntiles];
+  for (int i = 0; i < ntiles; ++i) perm_h[i] = i;
+  unsigned long long s = 88172645463325252ull;
+  for (int i = ntiles - 1; i > 0; --i) { s ^= s << 13; s ^= s >> 7; s ^= s << 17; int j = s % (i + 1); uint32_t t = perm_h[i]; perm_h[i] = perm_h[j]; perm_h[j] = t; }
+  uint32_t* perm; cudaMalloc(&perm, ntiles * 4); cudaMemcpy(perm, perm_h, ntiles * 4, cudaMemcpyHostToDevice);
+  for (int grid : {148 * 4, 148 * 8, 148 * 16}) {
+    tile_read<<<grid, 256>>>(p, perm, ntiles, out); cudaDeviceSynchronize();
+    cudaEventRecord(a); for (int r = 0; r < 5; ++r) tile_read<<<grid, 256>>>(p, perm, ntiles, out); cudaEventRecord(b);
+    cudaEventSynchronize(b); float ms; cudaEventElapsedTime(&ms, a, b);
+    printf("random 4KB tiles grid %d x 256: %.1f GB/s\n", grid, 5.0 * bytes / (ms / 1e3) / 1e9);
+  }
+  printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
