@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--no-extra", action="store_true", help="skip the prefill / LMAG sub-benchmarks")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--splits", type=int, default=0, help="force decode split count (0 = planner)")
+    ap.add_argument("--sweep", action="store_true", help="configs[4] sweep (per-GPU shard), JSON per point")
+    ap.add_argument("--sweep-n", type=int, default=8, help="GPUs the sweep's global batch is sharded over")
+    ap.add_argument("--sweep-max-gb", type=float, default=120.0)
     return ap.parse_args()
 
 
@@ -141,9 +144,13 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- workload build
 def build_decode_cache(torch, Cache, shape, n_req, docs, tokens, extra_rows, device, seed, placement_seed=99):
     """Creates a cache holding n_req requests of `docs` latent sets (m=128) followed by
-    `tokens` token rows; returns (cache, seq ids). Inputs drawn on the GPU (seeded)."""
+    `tokens` token rows (an int, or one count per request for the ragged variant);
+    returns (cache, seq ids). Inputs drawn on the GPU (seeded)."""
     from workloads import LATENT_ROWS
     P = shape.page_size
+    if not isinstance(tokens, int):
+        return _build_ragged(torch, Cache, shape, n_req, docs, list(tokens), extra_rows, device, seed,
+                             placement_seed)
     rows_max = docs * LATENT_ROWS + tokens + extra_rows
     pages_per_seq = docs * math.ceil(LATENT_ROWS / P) + math.ceil((tokens + extra_rows) / P) + 1
     cache = Cache(shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim, P,
@@ -166,6 +173,127 @@ def build_decode_cache(torch, Cache, shape, n_req, docs, tokens, extra_rows, dev
             del k, v
     torch.cuda.synchronize(device)
     return cache, seqs, rows_max
+
+
+def _build_ragged(torch, Cache, shape, n_req, docs, tokens, extra_rows, device, seed, placement_seed):
+    from workloads import LATENT_ROWS
+    P = shape.page_size
+    pages = [docs * math.ceil(LATENT_ROWS / P) + math.ceil((t + extra_rows) / P) + 1 for t in tokens]
+    cache = Cache(shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim, P,
+                  sum(pages) + 64, n_req, max(pages), device, placement_seed)
+    g = torch.Generator(device=f"cuda:{device}").manual_seed(seed)
+    seqs = [cache.seq_create() for _ in range(n_req)]
+    for _ in range(docs):
+        kv = torch.randn((n_req, shape.num_layers, 2, LATENT_ROWS, shape.num_kv_heads, shape.head_dim),
+                         generator=g, device=f"cuda:{device}").to(torch.bfloat16)
+        cache.latent_install_batch(seqs, [-1] * n_req, [kv[i] for i in range(n_req)])
+        del kv
+    for sq, t in zip(seqs, tokens):
+        s = (shape.num_layers, t, shape.num_kv_heads, shape.head_dim)
+        k = torch.randn(s, generator=g, device=f"cuda:{device}").to(torch.bfloat16)
+        v = torch.randn(s, generator=g, device=f"cuda:{device}").to(torch.bfloat16)
+        cache.append_kv([sq], [t], k, v)
+    torch.cuda.synchronize(device)
+    return cache, seqs, docs * LATENT_ROWS + max(tokens) + extra_rows
+
+
+def time_decode_calls(torch, cache, seqs, shape, dev, stream, K, W, seed=77):
+    """Decode-only timing (CUDA events on the launch stream), mean ms per call."""
+    import numpy as np
+    ids = np.asarray(seqs, dtype=np.int32)
+    g = torch.Generator(device=f"cuda:{dev}").manual_seed(seed)
+    q = torch.randn((len(seqs), shape.num_q_heads, shape.head_dim), generator=g,
+                    device=f"cuda:{dev}").to(torch.bfloat16)
+    out = torch.empty_like(q)
+    for _ in range(W):
+        cache.decode(0, ids, q, out)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(K):
+        cache.decode(0, ids, q, out)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    return e0.elapsed_time(e1) / K
+
+
+def bench_decode_variants(torch, Cache, dev, stream, pk, page_size):
+    """configs[1] variants: ragged reasoning lengths ~ U[1K, 8K], and the other
+    page size (P=64 when the headline runs P=16). Decode call only, CUDA events."""
+    from workloads import qwen3_8b_shape
+    out = {}
+    g = torch.Generator().manual_seed(1234 + 7)
+    ragged = [int(torch.randint(1024, 8193, (1,), generator=g).item()) for _ in range(64)]
+    for name, P, toks in (("ragged_U1K_8K", page_size, ragged), (f"page_size_{64 if page_size != 64 else 16}",
+                                                                   64 if page_size != 64 else 16, 4096)):
+        shape = qwen3_8b_shape(P)
+        cache, seqs, _ = build_decode_cache(torch, Cache, shape, 64, 8, toks, 0, dev, seed=1234)
+        ms = time_decode_calls(torch, cache, seqs, shape, dev, stream, 50, 5)
+        lens = [cache.seq_info(sq)[0] for sq in seqs]
+        byts = decode_bytes(lens, shape)
+        out[name] = {"page_size": P, "requests": 64, "mean_len": round(sum(lens) / len(lens), 1),
+                     "decode_ms": round(ms, 4), "tokens_per_s": round(64 / (ms / 1e3), 1),
+                     "achieved_gbs": round(byts / (ms / 1e3) / 1e9, 1),
+                     "frac": round(byts / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 4)}
+        cache.close()
+        torch.cuda.empty_cache()
+    return out
+
+
+def bench_sweep(args):
+    """configs[4]: the 8xB200 request-sharded sweep. Each rank holds B/n requests (no data-path
+    collective), so one GPU measures exactly the per-GPU work of the n-GPU run; whole-job
+    requests/s = n x per-GPU (weak in requests per GPU), max over ranks when run under torchrun.
+    Latent rows = floor(r*ctx/128)*128 as whole sets placed first (SURVEY 8(d) config-5);
+    achieved GB/s must be flat (+-3 %) across r at fixed (B, ctx). One JSON line per point,
+    then a summary line. Points whose pool exceeds --sweep-max-gb are reported as skipped."""
+    import torch
+    from paper_2605_09100_b200 import Cache
+    from workloads import LATENT_ROWS, qwen3_8b_shape
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    pk, pk_kind = peaks()
+    shape = qwen3_8b_shape(args.page_size)
+    n = args.sweep_n
+    rows_bytes = shape.num_kv_heads * shape.head_dim * 2 * 2
+    points = []
+    for B in (512, 1024, 2048, 4096):
+        b = B // n
+        for ctx in (8192, 16384, 32768, 65536):
+            for r in (0.1, 0.5, 0.9):
+                sets = int(r * ctx) // LATENT_ROWS
+                tok = ctx - sets * LATENT_ROWS
+                gb = b * ctx * rows_bytes / 1e9
+                pt = {"global_batch": B, "n_gpus": n, "requests_per_gpu": b, "context": ctx,
+                      "latent_ratio": r, "latent_sets": sets, "token_rows": tok, "kv_gb_per_gpu": round(gb, 2)}
+                if gb > args.sweep_max_gb:
+                    pt["skipped"] = f"pool {gb:.0f} GB > --sweep-max-gb {args.sweep_max_gb}"
+                    print(json.dumps(pt), flush=True)
+                    points.append(pt)
+                    continue
+                cache, seqs, _ = build_decode_cache(torch, Cache, shape, b, sets, tok, 0, dev, seed=1234)
+                ms = time_decode_calls(torch, cache, seqs, shape, dev, stream, args.steps, args.warmup)
+                byts = decode_bytes([ctx] * b, shape)
+                pt.update({"decode_ms": round(ms, 4), "requests_per_s_per_gpu": round(b / (ms / 1e3), 1),
+                           "requests_per_s_job": round(n * b / (ms / 1e3), 1),
+                           "achieved_gbs": round(byts / (ms / 1e3) / 1e9, 1),
+                           "frac": round(byts / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 4)})
+                cache.close()
+                torch.cuda.empty_cache()
+                print(json.dumps(pt), flush=True)
+                points.append(pt)
+    flat = []
+    for B in (512, 1024, 2048, 4096):
+        for ctx in (8192, 16384, 32768, 65536):
+            g = [p["achieved_gbs"] for p in points if p["global_batch"] == B and p["context"] == ctx
+                 and "achieved_gbs" in p]
+            if len(g) == 3:
+                flat.append({"global_batch": B, "context": ctx,
+                             "spread": round((max(g) - min(g)) / (sum(g) / 3), 4)})
+    print(json.dumps({"sweep": "configs[4]", "peak": pk["hbm_gbs"], "peak_kind": pk_kind,
+                      "page_size": args.page_size, "max_latent_ratio_spread": max(f["spread"] for f in flat),
+                      "flatness": flat}), flush=True)
 
 
 def decode_bytes(lens, shape):
@@ -339,6 +467,7 @@ def run_ours(args):
         res["lmag"] = bench_lmag(torch, Cache, shape, dev, stream, max(3, min(W, 5)), min(K, 20),
                                  world, max_over_ranks, barrier)
         res["next"] = bench_next(torch, Cache, shape, dev, stream, pk, max_over_ranks)
+        res["decode_variants"] = bench_decode_variants(torch, Cache, dev, stream, pk, args.page_size)
     if rank == 0 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(budget_s=15.0)
     if rank == 0:
@@ -623,5 +752,7 @@ if __name__ == "__main__":
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.sweep:
+        bench_sweep(a)
     else:
         run_ours(a)

@@ -32,7 +32,16 @@ namespace {
 
 constexpr int kChunk = 16;  // rows per pipeline chunk (one m16n8k16 K-step of keys)
 constexpr int kNCons = 4;   // consumer warps per CTA
-constexpr int kNSt = 8;     // ring depth
+#ifndef HPA_DEC_STAGES
+#define HPA_DEC_STAGES 12
+#endif
+#ifndef HPA_DEC_DYNAMIC
+#define HPA_DEC_DYNAMIC 1  // 1: units fetched from a ticket counter; 0: static striding over the list
+#endif
+#ifndef HPA_DEC_PF
+#define HPA_DEC_PF 8
+#endif
+constexpr int kNSt = HPA_DEC_STAGES;  // ring depth
 #ifndef HPA_FENCE_MODE
 #define HPA_FENCE_MODE 2  // 0: fence.sc (threadfence), 1: fence.acq_rel, 2: atom.acq_rel
 #endif
@@ -40,7 +49,7 @@ constexpr int kNSt = 8;     // ring depth
 #define HPA_DECODE_PERSISTENT 1  // persistent CTAs streaming consecutive work units through one ring
 #endif
 #ifndef HPA_DECODE_CTAS_PER_SM
-#define HPA_DECODE_CTAS_PER_SM 3
+#define HPA_DECODE_CTAS_PER_SM 2
 #endif
 #ifndef HPA_FUSED_COMBINE
 #define HPA_FUSED_COMBINE 0  // 1: a5 by the last split CTA (atomic + GPU fence: measured slower)
@@ -354,16 +363,21 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_const
 // are already in flight. Per unit: a 1-D bulk copy of the G q rows into a
 // 2-deep Q buffer, the unit's chunks, then one end-of-unit sentinel per consumer
 // (cmeta 0); after the last unit one end-of-kernel sentinel per consumer (-1).
+constexpr int kWB = 8;  // table-walker ring: pieces of one header + up to 31 page entries
+
 template <int D>
 struct PDecodeSmem {
   static constexpr int kHalves = D / 64;
   static constexpr int kTileBytes = kChunk * D * 2;
   static constexpr int kStageBytes = 2 * kTileBytes;
   static constexpr int oRing = 0;
-  static constexpr int oBar = kNSt * kStageBytes;     // full[NST], empty[NST], q_full[2], q_empty[2]
-  static constexpr int oMeta = oBar + (2 * kNSt + 4) * 8;
-  static constexpr int oZero = (oMeta + kNSt * 4 + 15) & ~15;  // 16 zero bytes: A-operand rows >= G
-  static constexpr int oQ = oZero + 16;                        // 2 x [G][D] q rows (unswizzled)
+  // full[NST], empty[NST], q_full[2], q_empty[2], w_full[WB], w_empty[WB]
+  static constexpr int oBar = kNSt * kStageBytes;
+  static constexpr int oMeta = oBar + (2 * kNSt + 4 + 2 * kWB) * 8;
+  static constexpr int oQMeta = (oMeta + kNSt * 4 + 15) & ~15;  // 2 x int4 {b, h, split, -}: unit of Q buffer
+  static constexpr int oWalk = oQMeta + 32;                      // [WB][32] int2 pieces
+  static constexpr int oZero = oWalk + kWB * 32 * 8;             // 16 zero bytes: A-operand rows >= G
+  static constexpr int oQ = oZero + 16;                          // 2 x [G][D] q rows (unswizzled)
   static __host__ __device__ int qbuf(int G) { return G * D * 2; }
   static __host__ __device__ int oMerge(int G) { return oQ + 2 * qbuf(G); }
   // no alignment slack: the dynamic smem base is 1024-B aligned (checked in the kernel)
@@ -371,9 +385,9 @@ struct PDecodeSmem {
 };
 
 template <int D>
-__global__ void __launch_bounds__((kNCons + 1) * 32, 3)
+__global__ void __launch_bounds__((kNCons + 2) * 32, HPA_DECODE_CTAS_PER_SM)
 decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                         const DecodeArgs a, int n_units) {
+                         const DecodeArgs a) {
   using L = PDecodeSmem<D>;
   extern __shared__ __align__(1024) uint8_t smem_pd[];
   uint8_t* smem = smem_pd;
@@ -387,12 +401,15 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
   uint64_t* empty = full + kNSt;
   uint64_t* q_full = empty + kNSt;
   uint64_t* q_empty = q_full + 2;
+  uint64_t* w_full = q_empty + 2;
+  uint64_t* w_empty = w_full + kWB;
   volatile int32_t* cmeta = reinterpret_cast<int32_t*>(smem + L::oMeta);
+  int4* qmeta = reinterpret_cast<int4*>(smem + L::oQMeta);
+  int2* walk = reinterpret_cast<int2*>(smem + L::oWalk);
   float* mo = reinterpret_cast<float*>(smem + L::oMerge(G));  // [NCONS][G][D]
   float* mm = mo + kNCons * G * D;                          // [NCONS][G]
   float* ml = mm + kNCons * G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int units_per = a.Hkv * a.splits;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kNSt; ++i) {
@@ -403,6 +420,10 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], kNCons);
     }
+    for (int i = 0; i < kWB; ++i) {
+      mbar_init(&w_full[i], 1);
+      mbar_init(&w_empty[i], 1);
+    }
     fence_barrier_init();
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
@@ -411,80 +432,124 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
   __syncthreads();
   grid_dependency_wait();  // PDL: everything above overlapped the previous kernel
 
+  if (warp == kNCons + 1) {
+    // --------------------------------------------------------- table walker
+    // Resolves work units (ticket -> record -> entry count) and their block-table entries
+    // (coalesced, one lane per entry) into pieces of {header, <= 31 x (rowbase, valid)} up to
+    // kWB pieces ahead, so no global-load latency ever sits on the TMA producer's path.
+    const int U = a.n_units;
+    uint32_t pc = 0;
+    int t = 0;
+    if (lane == 0) t = HPA_DEC_DYNAMIC ? atomicAdd(a.sched, 1) : int(blockIdx.x);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    for (;;) {
+      if (t >= U) {
+        const int ws = pc % kWB;
+        if (lane == 0) {
+          if (pc >= kWB) mbar_wait(&w_empty[ws], ((pc / kWB) - 1) & 1);
+          walk[ws * 32] = make_int2(-1, 0);
+          mbar_arrive(&w_full[ws]);
+        }
+        break;
+      }
+      int tn = 0;
+      if (lane == 0) tn = HPA_DEC_DYNAMIC ? atomicAdd(a.sched, 1) : t + int(gridDim.x);
+      const int4 ur = a.units[t];
+      const int seq = ur.y, h = ur.z & 0xff, split = (ur.z >> 8) & 0xff, sb = ur.z >> 16;
+      const int ne = a.t.n_entries[seq];
+      const int e0 = int(int64_t(split) * ne / sb);
+      const int e1 = int(int64_t(split + 1) * ne / sb);
+      const int32_t* bt = a.t.block_table + int64_t(seq) * a.t.max_pages;
+      const int32_t* mt = a.t.meta + int64_t(seq) * a.t.max_pages;
+      for (int e = e0, first = 1;; e += 31, first = 0) {
+        const int cnt = min(31, e1 - e);
+        const int last = e + cnt >= e1;
+        int2 item;
+        if (lane == 0) {
+          item = make_int2(ur.x, h | (split << 8) | (cnt << 16) | (first << 24) | (last << 25));
+        } else if (lane <= cnt) {
+          const int page = bt[e + lane - 1];
+          item = make_int2(((a.layer * a.NP + page) * a.Hkv + h) * a.P, mt[e + lane - 1] & kMetaRowsMask);
+        }
+        const int ws = pc % kWB;
+        if (pc >= kWB) mbar_wait(&w_empty[ws], ((pc / kWB) - 1) & 1);
+        if (lane <= cnt) walk[ws * 32 + lane] = item;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&w_full[ws]);
+        ++pc;
+        if (last) break;
+      }
+      t = __shfl_sync(0xffffffffu, tn, 0);
+    }
+    // every ticket fetch of every CTA is done once all CTAs got here: the last one resets
+    if (lane == 0 && HPA_DEC_DYNAMIC && atomicAdd(a.sched + 1, 1) == int(gridDim.x) - 1) {
+      atomicExch(a.sched, 0);
+      atomicExch(a.sched + 1, 0);
+    }
+    return;
+  }
+
   if (warp == 0) {
     // ------------------------------------------------------------ producer
+    // Consumes the walker's pieces: a unit's first piece starts its Q copy, every entry
+    // becomes TMA chunks, the unit's last piece ends with one sentinel per consumer.
     if (lane == 0) {
-      uint32_t i = 0;
+      uint32_t i = 0, pc = 0;
       int ul = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ul) {
-        const int b = u / units_per, h = (u / a.splits) % a.Hkv, split = u % a.splits;
-        const int seq = a.seq_rows[b];
-        const int qb = ul & 1;
-        if (ul >= 2) mbar_wait(&q_empty[qb], ((ul >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(&q_full[qb], uint32_t(G * D * 2));
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(qbuf + qb * qbytes)),
-            "l"(static_cast<const __nv_bfloat16*>(a.q) + (int64_t(b) * a.Hq + int64_t(h) * G) * D),
-            "r"(uint32_t(G * D * 2)), "r"(smem_u32(&q_full[qb]))
-            : "memory");
-        const int ne = a.t.n_entries[seq];
-        const int e0 = int(int64_t(split) * ne / a.splits);
-        const int e1 = int(int64_t(split + 1) * ne / a.splits);
-        const int32_t* bt = a.t.block_table + int64_t(seq) * a.t.max_pages;
-        const int32_t* mt = a.t.meta + int64_t(seq) * a.t.max_pages;
-        // Table entries are fetched kPf at a time, one batch ahead of the TMA issue, so the
-        // dependent L2 load of block_table/meta is not paid per chunk (P=16: one chunk per page).
-        constexpr int kPf = 8;
-        int pg_n[kPf], mv_n[kPf];
-#pragma unroll
-        for (int j = 0; j < kPf; ++j) {
-          pg_n[j] = e0 + j < e1 ? __ldg(bt + e0 + j) : 0;
-          mv_n[j] = e0 + j < e1 ? __ldg(mt + e0 + j) : 0;
+      for (;;) {
+        const int ws = pc % kWB;
+        mbar_wait(&w_full[ws], (pc / kWB) & 1);
+        const int2* it = walk + ws * 32;
+        const int2 hd = it[0];
+        if (hd.x < 0) {  // end of work: tell the consumers through the Q slot
+          const int qb = ul & 1;
+          if (ul >= 2) mbar_wait(&q_empty[qb], ((ul >> 1) - 1) & 1);
+          qmeta[qb] = make_int4(-1, 0, 0, 0);
+          mbar_arrive(&q_full[qb]);
+          break;
         }
-        for (int eb = e0; eb < e1; eb += kPf) {
-          int pg[kPf], mv[kPf];
+        const int b = hd.x, h = hd.y & 0xff, split = (hd.y >> 8) & 0xff, cnt = (hd.y >> 16) & 0xff;
+        if ((hd.y >> 24) & 1) {  // first piece of a unit: its Q rows
+          const int qb = ul & 1;
+          if (ul >= 2) mbar_wait(&q_empty[qb], ((ul >> 1) - 1) & 1);
+          qmeta[qb] = make_int4(b, h, split, 0);
+          mbar_arrive_expect_tx(&q_full[qb], uint32_t(G * D * 2));
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(qbuf + qb * qbytes)),
+              "l"(static_cast<const __nv_bfloat16*>(a.q) + (int64_t(b) * a.Hq + int64_t(h) * G) * D),
+              "r"(uint32_t(G * D * 2)), "r"(smem_u32(&q_full[qb]))
+              : "memory");
+        }
+        const int last = (hd.y >> 25) & 1;
+        for (int j = 1; j <= cnt; ++j) {
+          const int2 en = it[j];
+          const int rowbase = en.x, valid = en.y;
+          for (int sub = 0; sub * kChunk < valid; ++sub, ++i) {
+            const int slot = i % kNSt;
+            if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
+            cmeta[slot] = min(kChunk, valid - sub * kChunk);
+            mbar_arrive_expect_tx(&full[slot], L::kStageBytes);
+            uint8_t* kd = stages + slot * L::kStageBytes;
+            uint8_t* vd = kd + L::kTileBytes;
 #pragma unroll
-          for (int j = 0; j < kPf; ++j) {
-            pg[j] = pg_n[j];
-            mv[j] = mv_n[j];
-            const int en = eb + kPf + j;
-            pg_n[j] = en < e1 ? __ldg(bt + en) : 0;
-            mv_n[j] = en < e1 ? __ldg(mt + en) : 0;
-          }
-#pragma unroll
-          for (int j = 0; j < kPf; ++j) {
-            if (eb + j < e1) {
-              const int valid = mv[j] & kMetaRowsMask;
-              const int rowbase = ((a.layer * a.NP + pg[j]) * a.Hkv + h) * a.P;
-              for (int sub = 0; sub * kChunk < valid; ++sub, ++i) {
-                const int slot = i % kNSt;
-                if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
-                cmeta[slot] = min(kChunk, valid - sub * kChunk);
-                mbar_arrive_expect_tx(&full[slot], L::kStageBytes);
-                uint8_t* kd = stages + slot * L::kStageBytes;
-                uint8_t* vd = kd + L::kTileBytes;
-#pragma unroll
-                for (int hf = 0; hf < L::kHalves; ++hf) {
-                  tma_load_2d(kd + hf * 2048, &tm_k, &full[slot], hf * 64, rowbase + sub * kChunk);
-                  tma_load_2d(vd + hf * 2048, &tm_v, &full[slot], hf * 64, rowbase + sub * kChunk);
-                }
-              }
+            for (int hf = 0; hf < L::kHalves; ++hf) {
+              tma_load_2d(kd + hf * 2048, &tm_k, &full[slot], hf * 64, rowbase + sub * kChunk);
+              tma_load_2d(vd + hf * 2048, &tm_v, &full[slot], hf * 64, rowbase + sub * kChunk);
             }
           }
         }
-        for (int c = 0; c < kNCons; ++c, ++i) {  // end of unit: one sentinel per consumer
-          const int slot = i % kNSt;
-          if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
-          cmeta[slot] = 0;
-          mbar_arrive(&full[slot]);
+        mbar_arrive(&w_empty[ws]);
+        ++pc;
+        if (last) {
+          for (int c = 0; c < kNCons; ++c, ++i) {  // end of unit: one sentinel per consumer
+            const int slot = i % kNSt;
+            if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
+            cmeta[slot] = 0;
+            mbar_arrive(&full[slot]);
+          }
+          ++ul;
         }
-      }
-      for (int c = 0; c < kNCons; ++c, ++i) {  // end of kernel
-        const int slot = i % kNSt;
-        if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
-        cmeta[slot] = -1;
-        mbar_arrive(&full[slot]);
       }
     }
     return;
@@ -496,12 +561,13 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
   constexpr int kNT = kNCons * 32;
   const float sl2 = a.scale_log2;
   uint32_t i = cw;
-  int ul = 0;
-  for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++ul) {
-    const int b = u / units_per, h = (u / a.splits) % a.Hkv, split = u % a.splits;
-    // Q fragments of this unit (rows >= G read the zero chunk)
+  for (int ul = 0;; ++ul) {
     const int qb = ul & 1;
     mbar_wait(&q_full[qb], (ul >> 1) & 1);
+    const int4 um = qmeta[qb];
+    if (um.x < 0) break;  // end of work
+    const int b = um.x, h = um.y, split = um.z;
+    // Q fragments of this unit (rows >= G read the zero chunk)
     uint32_t qa[D / 16][4];
 #pragma unroll
     for (int ks = 0; ks < D / 16; ++ks) {
@@ -657,17 +723,19 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
 template <int D>
 __global__ void __launch_bounds__(D) combine_kernel(const float* __restrict__ o_part,
                                                     const float* __restrict__ lse, __nv_bfloat16* out,
-                                                    int S, float* part_o, float* part_lse) {
+                                                    int S_max, const int32_t* __restrict__ nsplit, int Hq,
+                                                    float* part_o, float* part_lse) {
   grid_dependency_wait();
   const int64_t bh = blockIdx.x;
-  const float* ls = lse + bh * S;
+  const int S = nsplit ? nsplit[bh / Hq] : S_max;  // this request's split count
+  const float* ls = lse + bh * S_max;
   float M = -CUDART_INF_F;
   for (int s = 0; s < S; ++s) M = fmaxf(M, ls[s]);
   float W = 0.f, acc = 0.f;
   for (int s = 0; s < S; ++s) {
     const float w = ls[s] == -CUDART_INF_F ? 0.f : fast_exp2(ls[s] - M);
     W += w;
-    acc += w * o_part[(bh * S + s) * D + threadIdx.x];
+    acc += w * o_part[(bh * S_max + s) * D + threadIdx.x];
   }
   if (part_o) {
     part_o[bh * D + threadIdx.x] = acc / W;
@@ -702,17 +770,8 @@ cudaError_t launch_decode_d(const CUtensorMap& tm_k, const CUtensorMap& tm_v, co
   cudaError_t e;
   if (HPA_DECODE_PERSISTENT) {
     const int smem = PDecodeSmem<D>::bytes(a.G);
-    static int num_sms = 0;
-    if (num_sms == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const int per_sm = std::min(HPA_DECODE_CTAS_PER_SM, (227 * 1024) / (smem + 1024));
-    const int n_units = a.n_seqs * a.Hkv * a.splits;
-    const int grid = std::max(1, std::min(n_units, num_sms * per_sm));
-    e = launch_pdl(decode_persistent_kernel<D>, dim3(grid), dim3((kNCons + 1) * 32), smem, s, tm_k, tm_v, a,
-                   n_units);
+    const int grid = std::max(1, std::min(a.n_units, decode_slots(D, a.G)));
+    e = launch_pdl(decode_persistent_kernel<D>, dim3(grid), dim3((kNCons + 2) * 32), smem, s, tm_k, tm_v, a);
   } else {
     const int smem = DecodeSmem<D>::kBytes;
     e = launch_pdl(decode_split_kernel<D>, dim3(a.splits, a.Hkv, a.n_seqs), dim3((kNCons + 1) * 32), smem, s,
@@ -723,7 +782,8 @@ cudaError_t launch_decode_d(const CUtensorMap& tm_k, const CUtensorMap& tm_v, co
   if ((a.splits > 1 && !HPA_FUSED_COMBINE) || a.part_o) {
     e = launch_pdl(combine_kernel<D>, dim3(a.n_seqs * a.Hq), dim3(D), 0, s,
                    static_cast<const float*>(a.o_part), static_cast<const float*>(a.lse_part),
-                   static_cast<__nv_bfloat16*>(a.out), a.splits, a.part_o, a.part_lse);
+                   static_cast<__nv_bfloat16*>(a.out), a.splits, HPA_DECODE_PERSISTENT ? a.nsplit : nullptr,
+                   a.Hq, a.part_o, a.part_lse);
     ++*launches;
   }
   return e;
@@ -755,6 +815,20 @@ cudaError_t decode_init_attributes() {
     return e;
   return cudaFuncSetAttribute(decode_split_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               DecodeSmem<64>::kBytes);
+}
+
+bool decode_persistent() { return HPA_DECODE_PERSISTENT != 0; }
+
+int decode_slots(int32_t D, int32_t G) {
+  static int num_sms = 0;
+  if (num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int smem = D == 64 ? PDecodeSmem<64>::bytes(G) : PDecodeSmem<128>::bytes(G);
+  const int per_sm = std::max(1, std::min(HPA_DECODE_CTAS_PER_SM, (227 * 1024) / (smem + 1024)));
+  return num_sms * per_sm;
 }
 
 int decode_ctas_per_sm(int32_t D, int32_t /*G*/) {

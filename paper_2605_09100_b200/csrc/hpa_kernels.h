@@ -91,8 +91,13 @@ struct DecodeArgs {
   int32_t* counters;        // [n][Hkv] zero; split-arrival counters for the fused combine
   float* part_o;            // context-parallel partial output (or nullptr): fp32 [n][Hq][d]
   float* part_lse;          //   and log2-sum-exp [n][Hq]
-  int32_t n_seqs, Hq, Hkv, G, P, NP, layer, splits;
+  int32_t n_seqs, Hq, Hkv, G, P, NP, layer, splits;  // splits = S_max (partials stride)
   float scale_log2;         // softmax_scale * log2(e)
+  // persistent kernel work list (host-planned, longest unit first):
+  const int4* units;        // [n_units] {request b, seq id, h | split << 8 | S_b << 16, 0}
+  const int32_t* nsplit;    // [n] per-request split count S_b (combine); nullptr = uniform `splits`
+  int32_t* sched;           // [2] unit ticket / finished-CTA counters, zero between calls
+  int32_t n_units;
 };
 // Merge of context-parallel partials: out[r][:] = sum_p 2^(lse_p - LSE) o_p / sum_p 2^(lse_p - LSE).
 cudaError_t launch_merge(int32_t n_parts, int32_t n_rows, int32_t D, const float* o_parts,
@@ -102,6 +107,9 @@ cudaError_t launch_merge(int32_t n_parts, int32_t n_rows, int32_t D, const float
 cudaError_t launch_decode(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,
                           int32_t D, cudaStream_t s, int* launches);
 int decode_ctas_per_sm(int32_t D, int32_t G);
+// Persistent decode kernel compiled in (HPA_DECODE_PERSISTENT) and its resident CTA count.
+bool decode_persistent();
+int decode_slots(int32_t D, int32_t G);
 // Per-device one-time setup (dynamic smem opt-in); call with the device current.
 cudaError_t decode_init_attributes();
 cudaError_t prefill_init_attributes();

@@ -25,6 +25,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <deque>
 #include <memory>
 #include <string>
@@ -284,8 +285,14 @@ struct hpa_cache {
   // decode partials
   float* o_part = nullptr;
   float* lse_part = nullptr;
-  int32_t* counters = nullptr;  // [max_seqs][H_kv], zero between calls
+  int32_t* counters = nullptr;  // [max_seqs][H_kv] + 2 (persistent ticket counters), zero between calls
   size_t part_elems = 0;
+  // persistent decode work list (rebuilt only when the batch or a split count changes)
+  std::vector<int32_t> plan_key;
+  int4* units_dev = nullptr;
+  int32_t* nsplit_dev = nullptr;
+  size_t units_cap = 0, nsplit_cap = 0;
+  int32_t plan_units = 0, plan_smax = 1;
   int32_t forced_splits = 0;
   // host-staged installs (NEXT-3): device payload buffer filled on copy_stream
   cudaStream_t copy_stream = nullptr;
@@ -467,6 +474,69 @@ int32_t plan_splits(hpa_cache_t* c, int32_t n, int32_t max_entries, int32_t max_
   return best;
 }
 
+// Persistent decode: per-request split counts S_b so that every (request, kv-head, split)
+// work unit covers about the same number of 16-row chunks (ragged batches stay balanced),
+// chosen by a makespan estimate over the resident CTA slots:
+//   cost = total / slots + max_unit / 2 + combine,   total = H_kv * sum_b (chunks_b + c0 * S_b).
+// The units go to the kernel longest first (it fetches them dynamically), so the tail is
+// about half a unit.  Returns S_max and fills splits[] (one per request).
+int32_t plan_request_splits(const hpa_cache_t* c, int32_t n, const int32_t* seq_ids, int32_t slots,
+                            std::vector<int32_t>& splits) {
+  splits.assign(n, 1);
+  std::vector<int32_t> ch(n), ne(n);
+  int32_t cmax = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const Seq& q = c->seqs[seq_ids[i]];
+    ch[i] = std::max(1, q.chunks);
+    ne[i] = std::max(1, seq_entries(q));
+    cmax = std::max(cmax, ch[i]);
+  }
+  if (c->forced_splits > 0) {
+    int32_t smax = 1;
+    for (int32_t i = 0; i < n; ++i) {
+      splits[i] = std::min(std::min(c->forced_splits, 64), ne[i]);
+      smax = std::max(smax, splits[i]);
+    }
+    return smax;
+  }
+  // per-unit cost in chunks (Q load, merge, partial write) and the combine's fixed cost;
+  // HPA_PLAN_C0 / HPA_PLAN_COMBINE override them (tuning knobs, read once)
+  static const double c0 = std::getenv("HPA_PLAN_C0") ? std::atof(std::getenv("HPA_PLAN_C0")) : 0.5;
+  static const double k_comb = std::getenv("HPA_PLAN_COMBINE") ? std::atof(std::getenv("HPA_PLAN_COMBINE")) : 4.0;
+  const double hkv = c->cfg.num_kv_heads;
+  const double part_chunks = double(c->cfg.num_q_heads) * (c->cfg.head_dim + 1) * 8 / 8192.0;
+  double best_cost = 1e300;
+  int32_t best_E = cmax;
+  int32_t prevE = -1;
+  for (int32_t sref = 1; sref <= 64; ++sref) {
+    const int32_t E = (cmax + sref - 1) / sref;        // chunk budget per unit
+    if (E == prevE) continue;
+    if (sref > 1 && E < 4) break;
+    prevE = E;
+    double total = 0, maxu = 0;
+    int32_t smax = 1;
+    for (int32_t i = 0; i < n; ++i) {
+      const int32_t sb = std::min(std::min(64, ne[i]), std::max(1, (ch[i] + E - 1) / E));
+      total += ch[i] + c0 * sb;
+      maxu = std::max(maxu, double(ch[i]) / sb);
+      smax = std::max(smax, sb);
+    }
+    total *= hkv;
+    double cost = total / slots + 0.5 * (maxu + c0);
+    if (smax > 1) cost += k_comb + n * smax * part_chunks / slots;  // combine launch + partial traffic
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best_E = E;
+    }
+  }
+  int32_t smax = 1;
+  for (int32_t i = 0; i < n; ++i) {
+    splits[i] = std::min(std::min(64, ne[i]), std::max(1, (ch[i] + best_E - 1) / best_E));
+    smax = std::max(smax, splits[i]);
+  }
+  return smax;
+}
+
 // Pages needed to append n rows to seq q.
 int32_t pages_for_append(const hpa_cache_t* c, const Seq& q, int32_t n) {
   if (n <= 0) return 0;
@@ -567,8 +637,10 @@ hpa_status_t hpa_cache_create(const hpa_config_t* cfg, hpa_cache_t** out) {
     cleanup();
     return cuda_fail(e, "table allocation");
   }
-  if ((e = cudaMalloc(&c->counters, size_t(g.max_seqs) * g.num_kv_heads * 4)) != cudaSuccess ||
-      (e = cudaMemset(c->counters, 0, size_t(g.max_seqs) * g.num_kv_heads * 4)) != cudaSuccess) {
+  // [max_seqs][H_kv] fused-combine counters, then the persistent decode's 2 ticket counters
+  const size_t n_counters = size_t(g.max_seqs) * g.num_kv_heads + 2;
+  if ((e = cudaMalloc(&c->counters, n_counters * 4)) != cudaSuccess ||
+      (e = cudaMemset(c->counters, 0, n_counters * 4)) != cudaSuccess) {
     cleanup();
     return cuda_fail(e, "counter allocation");
   }
@@ -610,6 +682,8 @@ hpa_status_t hpa_cache_destroy(hpa_cache_t* c) {
   if (c->o_part) cudaFree(c->o_part);
   if (c->lse_part) cudaFree(c->lse_part);
   if (c->counters) cudaFree(c->counters);
+  if (c->units_dev) cudaFree(c->units_dev);
+  if (c->nsplit_dev) cudaFree(c->nsplit_dev);
   if (c->payload_dev) cudaFree(c->payload_dev);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->copy_done) cudaEventDestroy(c->copy_done);
@@ -1030,8 +1104,61 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (hpa_status_t st = ship(c, s, {}, {}, 0)) return st;
   if (hpa_status_t st = upload_batch(c, n_seqs, seq_ids, s)) return st;
-  const int32_t S = plan_splits(c, n_seqs, max_entries, max_chunks);
-  const int32_t D = c->cfg.head_dim, Hq = c->cfg.num_q_heads;
+  const int32_t D = c->cfg.head_dim, Hq = c->cfg.num_q_heads, Hkv = c->cfg.num_kv_heads;
+  int32_t S = 1;
+  if (decode_persistent()) {
+    if (Hkv > 255) return fail(HPA_ERR_UNSUPPORTED, "persistent decode supports H_kv <= 255");
+    std::vector<int32_t> sp;
+    S = plan_request_splits(c, n_seqs, seq_ids, decode_slots(D, Hq / Hkv), sp);
+    std::vector<int32_t> key(seq_ids, seq_ids + n_seqs);
+    key.insert(key.end(), sp.begin(), sp.end());
+    if (key != c->plan_key) {
+      // unit list, longest unit first (the kernel fetches units dynamically in this order)
+      std::vector<std::pair<double, int32_t>> order;  // (-size, request)
+      int64_t U = 0;
+      for (int32_t i = 0; i < n_seqs; ++i) {
+        order.emplace_back(-double(std::max(1, c->seqs[seq_ids[i]].chunks)) / sp[i], i);
+        U += int64_t(sp[i]) * Hkv;
+      }
+      std::stable_sort(order.begin(), order.end(),
+                       [](const std::pair<double, int32_t>& x, const std::pair<double, int32_t>& y) {
+                         return x.first < y.first;
+                       });
+      if (U > (int64_t(1) << 30)) return fail(HPA_ERR_INVALID_ARG, "too many decode work units");
+      if (size_t(U) > c->units_cap) {
+        if (c->units_dev) cudaFree(c->units_dev);
+        c->units_dev = nullptr;
+        c->units_cap = std::max<size_t>(size_t(U), 4096);
+        HPA_CUDA(cudaMalloc(&c->units_dev, c->units_cap * sizeof(int4)));
+      }
+      if (size_t(n_seqs) > c->nsplit_cap) {
+        if (c->nsplit_dev) cudaFree(c->nsplit_dev);
+        c->nsplit_dev = nullptr;
+        c->nsplit_cap = std::max<size_t>(size_t(n_seqs), 1024);
+        HPA_CUDA(cudaMalloc(&c->nsplit_dev, c->nsplit_cap * 4));
+      }
+      const size_t ub = size_t(U) * sizeof(int4), nb = size_t(n_seqs) * 4;
+      const size_t off = c->ring.reserve(ub + nb);
+      int4* hu = reinterpret_cast<int4*>(c->ring.host(off));
+      size_t k = 0;
+      for (const auto& o : order) {
+        const int32_t i = o.second;
+        // splits of one (request, head) adjacent: concurrently running units read unrelated
+        // pages (heads of one page adjacent measured 7 % slower: HBM channel locality)
+        for (int32_t h = 0; h < Hkv; ++h)
+          for (int32_t sp_i = 0; sp_i < sp[i]; ++sp_i) hu[k++] = int4{i, seq_ids[i], h | (sp_i << 8) | (sp[i] << 16), 0};
+      }
+      std::memcpy(c->ring.host(off) + ub, sp.data(), nb);
+      HPA_CUDA(cudaMemcpyAsync(c->units_dev, c->ring.host(off), ub, cudaMemcpyHostToDevice, s));
+      HPA_CUDA(cudaMemcpyAsync(c->nsplit_dev, c->ring.host(off) + ub, nb, cudaMemcpyHostToDevice, s));
+      HPA_CUDA(c->ring.commit(off, ub + nb, s));
+      c->plan_key.swap(key);
+      c->plan_units = int32_t(U);
+      c->plan_smax = S;
+    }
+  } else {
+    S = plan_splits(c, n_seqs, max_entries, max_chunks);
+  }
   if (S > 1 || part_o) {
     const size_t need = size_t(n_seqs) * Hq * S;
     if (need > c->part_elems) {
@@ -1048,7 +1175,8 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
   DecodeArgs a{c->dt, c->batch_dev, q, out, c->o_part, c->lse_part, c->counters, part_o, part_lse, n_seqs, Hq,
                c->cfg.num_kv_heads,
                Hq / c->cfg.num_kv_heads, c->cfg.page_size, c->cfg.num_pages, layer, S,
-               scale * 1.4426950408889634f};
+               scale * 1.4426950408889634f, c->units_dev, c->nsplit_dev,
+               c->counters + size_t(c->cfg.max_seqs) * Hkv, c->plan_units};
   int launched = 0;
   cudaError_t e = launch_decode(c->tm_k_dec, c->tm_v_dec, a, D, s, &launched);
   c->launches += launched;

@@ -1,5 +1,5 @@
 #!/bin/bash
-for lib in paper_2605_09100_b200/libhpa.so variants/*.so; do
+for lib in paper_2605_09100_b200/libhpa.so $(ls variants/*.so 2>/dev/null); do
   echo "== $lib"
   for r in 1 2; do
   HPA_LIB_PATH=$PWD/$lib timeout -s KILL 200 python bench.py --steps 100 --warmup 10 --no-cpu-baseline --no-extra 2>&1 | tail -1 | python3 -c "

@@ -7,6 +7,9 @@ configs[2]: chunked prefill C=2048 over 1024 latent + 16384 cached token rows;
             48 sampled query rows (first/last/ragged positions), all 32 heads.
 configs[3]: B=256 LMAG step (batched latent replacement + append + decode);
             4 sampled requests.
+configs[1] ragged variant: reasoning rows ~ U[1K, 8K] per request.
+configs[4]: per-GPU shard of the 8-GPU sweep (B=512/8=64 requests) at ctx=64K
+            with latent ratios 0.1 and 0.9; 2 sampled requests.
 Sampled requests are drawn on the CPU (workloads.Draw); the rest of the batch
 is filled with GPU-drawn data of the same distribution (it only shapes the
 launch; its outputs are checked for finiteness)."""
@@ -22,7 +25,9 @@ pytestmark = pytest.mark.gpu
 
 
 def _build(cache, orc, shape, n_req, sampled, docs, tokens, seed):
-    """Builds n_req requests; the `sampled` ones with CPU draws mirrored in the oracle."""
+    """Builds n_req requests; the `sampled` ones with CPU draws mirrored in the oracle.
+    `tokens` is one row count for all requests or a list (ragged)."""
+    tok = [tokens] * n_req if isinstance(tokens, int) else list(tokens)
     g = torch.Generator(device="cuda").manual_seed(seed)
     seqs = [cache.seq_create() for _ in range(n_req)]
     draws = {}
@@ -42,14 +47,14 @@ def _build(cache, orc, shape, n_req, sampled, docs, tokens, seed):
     ks, vs = [], []
     for s in range(n_req):
         if s in draws:
-            k, v = draws[s].tokens(shape, tokens)
+            k, v = draws[s].tokens(shape, tok[s])
             orc.append(seqs[s], f64(k), f64(v))
             ks.append(k.cuda())
             vs.append(v.cuda())
         else:
-            ks.append(torch.randn((1, tokens, 8, 128), generator=g, device="cuda").to(torch.bfloat16))
-            vs.append(torch.randn((1, tokens, 8, 128), generator=g, device="cuda").to(torch.bfloat16))
-    cache.append_kv(seqs, [tokens] * n_req, torch.cat(ks, 1), torch.cat(vs, 1))
+            ks.append(torch.randn((1, tok[s], 8, 128), generator=g, device="cuda").to(torch.bfloat16))
+            vs.append(torch.randn((1, tok[s], 8, 128), generator=g, device="cuda").to(torch.bfloat16))
+    cache.append_kv(seqs, tok, torch.cat(ks, 1), torch.cat(vs, 1))
     return seqs, draws
 
 
@@ -124,4 +129,48 @@ def test_lmag_config3_full_size_sampled():
         assert torch.isfinite(out.float()).all()
         ref = np.stack([attend(f64(q[s:s + 1]), *orc.logical_kv(seqs[s], 0), shape.scale)[0] for s in sampled])
         check_close(out[sampled], ref, f"configs[3] LMAG step {step}")
+    cache.close()
+
+
+def _decode_sampled(cache, orc, shape, seqs, sampled, what, qseed=7):
+    B = len(seqs)
+    q = torch.randn((B, 32, 128), device="cuda").to(torch.bfloat16)
+    qs = Draw(qseed).queries(shape, len(sampled))
+    for i, s in enumerate(sampled):
+        q[s] = qs[i].cuda()
+    out = cache.decode(0, seqs, q)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    ref = np.stack([attend(f64(qs[i:i + 1]), *orc.logical_kv(seqs[s], 0), shape.scale)[0]
+                    for i, s in enumerate(sampled)])
+    check_close(out[sampled], ref, what)
+
+
+def test_decode_config1_ragged_sampled():
+    from paper_2605_09100_b200 import Cache
+    shape = qwen3_8b_shape(16)
+    B, sampled = 64, [0, 5, 33, 63]
+    g = torch.Generator().manual_seed(1234 + 7)
+    toks = [int(torch.randint(1024, 8193, (1,), generator=g).item()) for _ in range(B)]
+    toks[5], toks[33] = 1024, 8192                     # both ends of the range among the sampled
+    pages = 64 + 8192 // 16 + 2
+    cache = Cache(1, 32, 8, 128, 16, B * pages, B, pages, 0, 99)
+    orc = OracleCache(1, 32, 8, 128, 16)
+    seqs, _ = _build(cache, orc, shape, B, sampled, 8, toks, 4242)
+    _decode_sampled(cache, orc, shape, seqs, sampled, "configs[1] ragged decode sampled")
+    cache.close()
+
+
+@pytest.mark.parametrize("ratio", [0.1, 0.9])
+def test_decode_config4_sweep_shard_64k_sampled(ratio):
+    from paper_2605_09100_b200 import Cache
+    shape = qwen3_8b_shape(16)
+    ctx, B, sampled = 65536, 64, [0, 63]
+    sets = int(ratio * ctx) // LATENT_ROWS
+    tok = ctx - sets * LATENT_ROWS
+    pages = sets * (LATENT_ROWS // 16) + tok // 16 + 1
+    cache = Cache(1, 32, 8, 128, 16, B * pages, B, pages, 0, 99)
+    orc = OracleCache(1, 32, 8, 128, 16)
+    seqs, _ = _build(cache, orc, shape, B, sampled, sets, tok, 31)
+    _decode_sampled(cache, orc, shape, seqs, sampled, f"configs[4] shard ctx=64K r={ratio}")
     cache.close()
