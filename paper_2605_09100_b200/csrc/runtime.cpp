@@ -101,6 +101,38 @@ bool make_map_2d(CUtensorMap* m, void* base, uint64_t rows, uint64_t cols, uint3
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+#ifndef HPA_DEC_MAP3
+#define HPA_DEC_MAP3 1  // decode: one 3-D TMA per 16-row K or V tile (else two 2-D boxes)
+#endif
+#ifndef HPA_DEC_L2PROMO
+#define HPA_DEC_L2PROMO 2  // 0 none, 1 128 B, 2 256 B
+#endif
+
+// Decode map over a pool [rows][d]: dims {64, rows, d/64} with the d/64 column halves as the
+// outer dim (stride 128 B), box {64, 16, d/64}: one TMA fills the same [half][16][64] smem
+// layout the two 2-D boxes did.
+bool make_map_dec(CUtensorMap* m, void* base, uint64_t rows, uint64_t cols) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const CUtensorMapL2promotion promo = HPA_DEC_L2PROMO == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                       : HPA_DEC_L2PROMO == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                              : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  if (!HPA_DEC_MAP3) {
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {64, 16};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  cuuint64_t dims[3] = {64, rows, cols / 64};
+  cuuint64_t strides[2] = {cols * 2, 128};
+  cuuint32_t box[3] = {64, 16, cuuint32_t(cols / 64)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // 3-D bf16 map over q [tokens][Hq][d]: box {64, 1, box_tok}, 128-B swizzle.
 bool make_map_q(CUtensorMap* m, const void* base, uint64_t tokens, uint64_t heads, uint64_t d,
                 uint32_t box_tok) {
@@ -646,8 +678,8 @@ hpa_status_t hpa_cache_create(const hpa_config_t* cfg, hpa_cache_t** out) {
   }
   c->dt = DevTables{c->arena, c->arena + c->off_pos0(), c->arena + c->off_meta(), c->arena + c->off_len(),
                     c->arena + c->off_nent(), g.max_pages_per_seq};
-  if (!make_map_2d(&c->tm_k_dec, c->k_pool, uint64_t(rows), uint64_t(g.head_dim), 16) ||
-      !make_map_2d(&c->tm_v_dec, c->v_pool, uint64_t(rows), uint64_t(g.head_dim), 16) ||
+  if (!make_map_dec(&c->tm_k_dec, c->k_pool, uint64_t(rows), uint64_t(g.head_dim)) ||
+      !make_map_dec(&c->tm_v_dec, c->v_pool, uint64_t(rows), uint64_t(g.head_dim)) ||
       !make_map_2d(&c->tm_k_pre, c->k_pool, uint64_t(rows), uint64_t(g.head_dim), uint32_t(std::min(g.page_size, 128))) ||
       !make_map_2d(&c->tm_v_pre, c->v_pool, uint64_t(rows), uint64_t(g.head_dim), uint32_t(std::min(g.page_size, 128)))) {
     cleanup();
