@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(PoolGeom g, int32_t* __res
                                                       const ScatterRecord* __restrict__ recs,
                                                       const int32_t* __restrict__ idx) {
   grid_dependency_wait();
+  grid_launch_dependents();
   const int64_t nthreads = int64_t(gridDim.x) * gridDim.y * blockDim.x;
   const int64_t gtid = (int64_t(blockIdx.y) * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
   for (int64_t i = gtid; i < n_words; i += nthreads) arena[words[i].idx] = words[i].val;
@@ -93,6 +94,7 @@ template <int D>
 __global__ void __launch_bounds__(256) scatter_inline_kernel(PoolGeom g, int32_t* __restrict__ arena,
                                                              const __grid_constant__ InlineMeta m) {
   grid_dependency_wait();
+  grid_launch_dependents();
   const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
   const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   for (int64_t i = gtid; i < m.n_words; i += nthreads) arena[m.data[2 * i]] = m.data[2 * i + 1];

@@ -101,6 +101,7 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_const
     tma_prefetch_desc(&tm_v);
   }
   grid_dependency_wait();  // PDL: everything above overlapped the previous kernel
+  grid_launch_dependents();
   const int seq = a.seq_rows[b];
   // q rows of this kv-head's group -> swizzled smem tile [16][D]; rows >= G are 0.
   {
@@ -449,6 +450,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
   if (threadIdx.x < 4) reinterpret_cast<uint32_t*>(zero)[threadIdx.x] = 0u;
   __syncthreads();
   grid_dependency_wait();  // PDL: everything above overlapped the previous kernel
+  grid_launch_dependents();
 
   if (warp == kNCons + 1) {
     // --------------------------------------------------------- table walker
@@ -753,6 +755,7 @@ __global__ void __launch_bounds__(D) combine_kernel(const float* __restrict__ o_
                                                     int S_max, const int32_t* __restrict__ nsplit, int Hq,
                                                     float* part_o, float* part_lse) {
   grid_dependency_wait();
+  grid_launch_dependents();
   const int64_t bh = blockIdx.x;
   const int S = nsplit ? nsplit[bh / Hq] : S_max;  // this request's split count
   const float* ls = lse + bh * S_max;
@@ -778,6 +781,7 @@ __global__ void __launch_bounds__(D) merge_kernel(const float* __restrict__ o_pa
                                                   const float* __restrict__ lse_parts, __nv_bfloat16* out,
                                                   int n_parts, int64_t n_rows) {
   grid_dependency_wait();
+  grid_launch_dependents();
   const int64_t r = blockIdx.x;
   float M = -CUDART_INF_F;
   for (int p = 0; p < n_parts; ++p) M = fmaxf(M, lse_parts[p * n_rows + r]);

@@ -219,6 +219,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   constexpr int kHalves = D / 64;
   const int b = blockIdx.z;
   grid_dependency_wait();  // PDL
+  grid_launch_dependents();
   const int q_len = a.q_len[b];
   // slot -> (q-head, row tile)
   int hq_s[2], mt_s[2];

@@ -142,6 +142,12 @@ __device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t chunk) {
 __device__ __forceinline__ void grid_dependency_wait() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+// PDL: let the next kernel in the stream start its prologue now. Safe because every kernel
+// this library launches with PDL calls grid_dependency_wait() (full completion + memory
+// visibility of the predecessor) before touching memory another kernel uses.
+__device__ __forceinline__ void grid_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 #ifdef __CUDACC__
 template <typename... KArgs, typename... Args>
