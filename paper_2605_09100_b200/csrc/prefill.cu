@@ -104,6 +104,13 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+// One lane of a converged warp (the lowest): the MMA issuer runs its loop warp-uniformly so the
+// descriptor arithmetic stays in uniform registers, and only the elected lane issues.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
 // D[tmem] (+)= A[smem desc] * B[smem desc]
 __device__ __forceinline__ void tc_mma_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                           uint32_t acc) {
@@ -406,7 +413,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     }
   } else if (warp == kMmaWarp) {
     // ================================================================ MMA issuer
-    if (lane == 0) {
+    // All 32 lanes run the loop (warp-uniform waits keep the descriptor math in uniform
+    // registers); the elected lane issues every tcgen05.mma and commit (commit tracks the
+    // MMAs of the issuing thread, and elect.sync picks the same lowest lane each time).
+    {
       constexpr uint32_t idS = idesc_bf16(kBM, kBN, 0, 0);
       constexpr uint32_t idO = idesc_bf16(kBM, D, 0, 1);
       const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV);
@@ -414,55 +424,65 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       mbar_wait(q_full, 0);
       auto issue_s = [&](int s, int jj) {
         const int ks = jj % kNK;
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint64_t ad = sdesc(aQ + s * L::kQ + (k >> 2) * (kBM * 128) + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = sdesc(aK + ks * L::kKV + (k >> 2) * (kBN * 128) + (k & 3) * 32, 16, 1024);
-          tc_mma_ss(tmem + s * 128, ad, bd, idS, k > 0 ? 1u : 0u);
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t ad = sdesc(aQ + s * L::kQ + (k >> 2) * (kBM * 128) + (k & 3) * 32, 16, 1024);
+            const uint64_t bd = sdesc(aK + ks * L::kKV + (k >> 2) * (kBN * 128) + (k & 3) * 32, 16, 1024);
+            tc_mma_ss(tmem + s * 128, ad, bd, idS, k > 0 ? 1u : 0u);
+          }
+          tc_commit(&s_full[s]);
         }
-        tc_commit(&s_full[s]);
+        __syncwarp();
       };
       auto issue_pv_half = [&](int s, int jj, int half) {
         const int vs = jj % kNV;
+        if (elect_one()) {
 #pragma unroll
-        for (int k = half * 4; k < half * 4 + 4; ++k) {
-          const uint64_t bd = sdesc(aV + vs * L::kKV + k * 2048, kBN * 128, 1024);
-          tc_mma_ts(tmem + 256 + s * 128, tmem + s * 128 + k * 8, bd, idO, (jj > 0 || k > 0) ? 1u : 0u);
+          for (int k = half * 4; k < half * 4 + 4; ++k) {
+            const uint64_t bd = sdesc(aV + vs * L::kKV + k * 2048, kBN * 128, 1024);
+            tc_mma_ts(tmem + 256 + s * 128, tmem + s * 128 + k * 8, bd, idO, (jj > 0 || k > 0) ? 1u : 0u);
+          }
         }
+        __syncwarp();
+      };
+      auto commit = [&](uint64_t* bar) {
+        if (elect_one()) tc_commit(bar);
+        __syncwarp();
       };
       mbar_wait(&k_full[0], 0);
       tc_fence_after();
       for (int s = 0; s < nslot; ++s) issue_s(s, 0);
-      tc_commit(&k_empty[0]);
+      commit(&k_empty[0]);
       for (int j = 0; j < n_tiles; ++j) {
         const bool more = j + 1 < n_tiles;
         mbar_wait(&v_full[j % kNV], (j / kNV) & 1);
-        TRACE(2, j);
+        if (lane == 0) TRACE(2, j);
         bool k_ready = false;
         for (int s = 0; s < nslot; ++s) {
           // PV over keys 0..63 as soon as the first half of P is in TMEM, then 64..127
           mbar_wait(&p_full[2 * s], j & 1);
-          TRACE(3 + s, j);
+          if (lane == 0) TRACE(3 + s, j);
           tc_fence_after();
           issue_pv_half(s, j, 0);
           mbar_wait(&p_full[2 * s + 1], j & 1);
-          TRACE(5 + s, j);
+          if (lane == 0) TRACE(5 + s, j);
           tc_fence_after();
           issue_pv_half(s, j, 1);
-          if (s == nslot - 1) tc_commit(&v_empty[j % kNV]);
+          if (s == nslot - 1) commit(&v_empty[j % kNV]);
           if (more) {
             if (!k_ready) {  // K(j+1) is only needed here, not by PV(j)
               mbar_wait(&k_full[(j + 1) % kNK], ((j + 1) / kNK) & 1);
-              TRACE(1, j);
+              if (lane == 0) TRACE(1, j);
               tc_fence_after();
               k_ready = true;
             }
             issue_s(s, j + 1);  // overwrites S/P s after PV s has read P (in-order pipe)
           }
         }
-        if (more) tc_commit(&k_empty[(j + 1) % kNK]);
+        if (more) commit(&k_empty[(j + 1) % kNK]);
       }
-      tc_commit(o_full);
+      commit(o_full);
     }
   } else if (warp < 8) {
     // ================================================================ softmax (slot = warp / 4)
@@ -570,6 +590,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             mbar_arrive(&p_full[2 * s + half]);
           }
           if (row == 0) TRACE(11 + 2 * s + half, j);
+          if (lane == 0 && half == 1) TRACE(15 + 4 * s + quarter, j);  // per-warp P completion
+          if (lane == 0 && half == 0) TRACE(23 + 4 * s + quarter, j);  // per-warp P half0
         }
       }
       const float2 rsa = fadd2(rs4[0], rs4[1]), rsb = fadd2(rs4[2], rs4[3]);
