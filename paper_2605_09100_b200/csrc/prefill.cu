@@ -40,26 +40,36 @@
 namespace hpa {
 namespace {
 
+// HPA_SM16 = 1: 16 softmax warps -- two per SMSP per slot, each owning 64 of a row's 128
+// key columns (and half of O's columns); the row max is exchanged through shared memory.
+// A slot's exps are then spread over twice the warps, shortening the QK -> softmax -> PV
+// chain. HPA_SM16 = 0: 8 softmax warps, one per row.
+#ifndef HPA_SM16
+#define HPA_SM16 0  // 1 measured slower (1101 vs 1236 TFLOP/s): a slot's exps share the same SMSP MUFUs
+#endif
 constexpr int kBM = 128;   // query rows per slot
 constexpr int kBN = 128;   // key slots per tile
-constexpr int kNK = 3;     // K ring depth
+constexpr int kNK = HPA_SM16 ? 2 : 3;  // K ring depth (2 leaves room for the max exchange)
 constexpr int kNV = 2;     // V ring depth
 constexpr int kNC = 3;     // mask-index ring depth
-constexpr int kThreads = 384;      // 3 warpgroups: softmax 0, softmax 1, producer / MMA / 2 spare
-constexpr int kProducerWarp = 8;
-constexpr int kMmaWarp = 9;
-constexpr int kVProducerWarp = 10;
+constexpr int kSoftWarps = HPA_SM16 ? 16 : 8;
+constexpr int kThreads = (kSoftWarps + 4) * 32;  // softmax warpgroups + producer / MMA / V producer / spare
+constexpr int kProducerWarp = kSoftWarps;
+constexpr int kMmaWarp = kSoftWarps + 1;
+constexpr int kVProducerWarp = kSoftWarps + 2;
 #ifndef HPA_SOFTMAX_REGS
-#define HPA_SOFTMAX_REGS 216
+#define HPA_SOFTMAX_REGS (HPA_SM16 ? 104 : 216)
 #endif
 #ifndef HPA_OTHER_REGS
-#define HPA_OTHER_REGS 72
+#define HPA_OTHER_REGS (HPA_SM16 ? 64 : 72)
 #endif
-// setmaxnreg: the launch allocates 168 regs/thread (384 threads), so the two
-// softmax warpgroups may grow only by what warpgroup 2 gives up: 2 S + O <= 3 x 168.
+// setmaxnreg: the launch allocates R0 = floor(65536 / kThreads / 8) * 8 regs per thread;
+// the softmax warpgroups may grow only by what the role warpgroup gives up.
+constexpr int kLaunchRegs = (65536 / kThreads) / 8 * 8 > 168 ? 168 : (65536 / kThreads) / 8 * 8;
 constexpr int kSoftmaxRegs = HPA_SOFTMAX_REGS;
 constexpr int kOtherRegs = HPA_OTHER_REGS;
-static_assert(2 * kSoftmaxRegs + kOtherRegs <= 3 * 168, "setmaxnreg budget");
+static_assert((kSoftWarps / 4) * kSoftmaxRegs + kOtherRegs <= (kSoftWarps / 4 + 1) * kLaunchRegs,
+              "setmaxnreg budget");
 constexpr float kRescaleThreshold = 8.0f;  // log2 units (factor 256)
 constexpr int kSpanBit = 1 << 30;          // tags span columns in the mask indices (seq_len < 2^30)
 #ifndef HPA_POLY_EVERY
@@ -74,6 +84,15 @@ constexpr int kSpanBit = 1 << 30;          // tags span columns in the mask indi
   } while (0)
 #else
 #define TRACE(ev, j) do { } while (0)
+#endif
+#ifndef HPA_P_PACK_ALU
+#define HPA_P_PACK_ALU 0  // 1: P -> bf16 on the ALU pipe instead of F2FP (measured slower)
+#endif
+#ifndef HPA_EXP_INPLACE
+#define HPA_EXP_INPLACE 0  // 1: all ex2 of a half first (in place), then sums and packs (measured no faster)
+#endif
+#ifndef HPA_OPT_EXP  // softmax: first-half exps against the running max with the tile max reduced
+#define HPA_OPT_EXP (!HPA_EXP_INPLACE)  // alongside (needs the raw scores, so not with in-place exps)
 #endif
 #ifndef HPA_PV_SPLIT
 #define HPA_PV_SPLIT 1    // publish P in two 64-key halves (PV starts on the first half)
@@ -91,7 +110,9 @@ struct PSmem {
   // q_full, k_full[NK], k_empty[NK], v_full[NV], v_empty[NV], s_full[2], p_full[2 slots][2 halves],
   // o_full, c_full[NC], c_empty[NC]
   static constexpr int kNBar = 1 + 2 * kNK + 2 * kNV + 2 + 4 + 1 + 2 * kNC;
-  static constexpr int oMisc = oBar + kNBar * 8;
+  static constexpr int oX = oBar + kNBar * 8;      // HPA_SM16: row max [2 buf][2 slot][2 half][128], row sum [2][2][128]
+  static constexpr int kXBytes = HPA_SM16 ? (8 + 4) * kBM * 4 : 0;
+  static constexpr int oMisc = oX + kXBytes;
   static constexpr int kRaw = oMisc + 16 + 1024;  // tmem addr + 3 tile words
   // >= 116 KB so exactly one CTA is resident per SM (it owns all 512 TMEM columns)
   static constexpr int kBytes = kRaw > 116 * 1024 ? kRaw : 116 * 1024;
@@ -156,6 +177,22 @@ __device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t* r) {
       "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
       HPA_W32(r)
       : "memory");
+}
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
 }
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -290,7 +327,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
     for (int i = 0; i < 4; ++i) mbar_init(&p_full[i], 4);  // one arrive per softmax warp
     mbar_init(o_full, 1);
-    for (int i = 0; i < kNC; ++i) { mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], 8); }
+    for (int i = 0; i < kNC; ++i) { mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], kSoftWarps); }
     fence_barrier_init();
     // key slot of a logical index x: the last entry with pos0 <= x, plus the row offset
     auto slot_of = [&](int x) {
@@ -326,7 +363,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   const int skip_a = ntiles_slot[1], n_skip = ntiles_slot[2];
   const int n_tiles = ntiles_slot[0] - n_skip;  // iterations; tile(jj) = jj < skip_a ? jj : jj + n_skip
 
-  if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kOtherRegs));
+  if (warp >= kSoftWarps) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kOtherRegs));
   if (warp == kProducerWarp) {
     // ================================================================ producer
     if (lane == 0) {
@@ -484,6 +521,145 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
       commit(o_full);
     }
+#if HPA_SM16
+  } else if (warp < kSoftWarps) {
+    // ================================================================ softmax, 16 warps
+    // warp = 8 slot + 4 half + quarter: rows quarter*32 + lane of slot `s`, key columns
+    // [64 hc, 64 hc + 64) of S, P columns [32 hc, +32) (bf16 pairs), O columns [D/2 hc, +D/2).
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
+    constexpr int kCols = kBN / 2, kOCols = D / 2;
+    const int s = warp >> 3, hc = (warp >> 2) & 1, quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int t = mt_s[s] * kBM + row;
+    const int my_i = q_base + t;
+    const uint32_t lane_base = uint32_t(quarter * 32) << 16;
+    const uint32_t tS = tmem + lane_base + s * 128 + hc * kCols;
+    const uint32_t tP = tmem + lane_base + s * 128 + hc * (kCols / 2);
+    const uint32_t tO = tmem + lane_base + 256 + s * 128 + hc * kOCols;
+    float* xmax = reinterpret_cast<float*>(sm + L::oX);             // [2 buf][2 slot][2 half][128]
+    float* xsum = xmax + 8 * kBM;                                     // [2 slot][2 half][128]
+    const float sl2 = a.scale_log2;
+    const bool live = s == 0 || slot1_live;
+    float m_run = -CUDART_INF_F, l_run = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int cs = j % kNC;
+      if (!live) {  // dead slot: still release the mask slot
+        mbar_wait(&c_full[cs], (j / kNC) & 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&c_empty[cs]);
+        continue;
+      }
+      float x[kCols];
+      mbar_wait(&s_full[s], j & 1);
+      if (row == 0 && hc == 0) TRACE(7 + s, j);
+      tc_fence_after();
+      tc_ld32(tS, x);
+      tc_ld32(tS + 32, x + 32);
+      mbar_wait(&c_full[cs], (j / kNC) & 1);
+      const int32_t* col = sC + cs * (kBN + 4) + hc * kCols;
+      const bool all_vis = sC[cs * (kBN + 4) + kBN] != 0;
+      tc_wait_ld();
+      if (row == 0 && hc == 0) TRACE(9 + s, j);
+      if (!all_vis) {
+        const int cmask = my_i >= span_from ? -1 : ~kSpanBit;
+#pragma unroll
+        for (int c = 0; c < kCols; c += 4) {
+          const int4 ci = *reinterpret_cast<const int4*>(col + c);
+          x[c + 0] = (ci.x & cmask) <= my_i ? x[c + 0] : -CUDART_INF_F;
+          x[c + 1] = (ci.y & cmask) <= my_i ? x[c + 1] : -CUDART_INF_F;
+          x[c + 2] = (ci.z & cmask) <= my_i ? x[c + 2] : -CUDART_INF_F;
+          x[c + 3] = (ci.w & cmask) <= my_i ? x[c + 3] : -CUDART_INF_F;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&c_empty[cs]);
+      float pm[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pm[k] = fmaxf(x[k], x[k + 8]);
+#pragma unroll
+      for (int c = 16; c < kCols; c += 16) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pm[k] = fmaxf(pm[k], fmaxf(x[c + k], x[c + k + 8]));
+      }
+      float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+      // row max over both column halves: exchange with the partner warp (same rows, other half)
+      float* xb = xmax + ((j & 1) * 2 + s) * 2 * kBM;
+      xb[hc * kBM + row] = mx;
+      named_bar_sync(1 + s, 8 * 32);
+      mx = fmaxf(mx, xb[(hc ^ 1) * kBM + row]);
+      mx *= sl2;
+      const bool grow = mx > m_run + kRescaleThreshold;  // lazy rescale (both halves agree)
+      const float m_new = grow ? mx : m_run;
+      const float alpha = grow ? fast_exp2(m_run - m_new) : 1.f;
+      m_run = m_new;
+      if (j > 0 && __any_sync(0xffffffffu, grow)) {  // this half of O_s (PV_s(j-1) completed)
+#pragma unroll
+        for (int c = 0; c < kOCols; c += 16) {
+          float o[16];
+          tc_ld16(tO + c, o);
+          tc_wait_ld();
+#pragma unroll
+          for (int y = 0; y < 16; ++y) o[y] *= alpha;
+          tc_st16(tO + c, reinterpret_cast<const uint32_t*>(o));
+        }
+      }
+      const float m_use = m_new == -CUDART_INF_F ? 0.f : m_new;
+      const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_use, -m_use);
+#pragma unroll
+      for (int c = 0; c < kCols; c += 2) {  // all ex2 first, in place
+        const float2 arg = ffma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
+        x[c] = fast_exp2(arg.x);
+        x[c + 1] = fast_exp2(arg.y);
+      }
+      float2 rs4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+      for (int ch = 0; ch < kCols / 32; ++ch) {  // sums + bf16 pairs, stored 16 columns at a time
+        uint32_t pk[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const float2 e = make_float2(x[ch * 32 + 2 * q], x[ch * 32 + 2 * q + 1]);
+          rs4[q & 3] = fadd2(rs4[q & 3], e);
+          pk[q] = pack_bf16(e.x, e.y);
+        }
+        tc_st16(tP + ch * 16, pk);
+      }
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[2 * s + hc]);
+      if (row == 0) TRACE(11 + 2 * s + hc, j);
+      const float2 rsa = fadd2(rs4[0], rs4[1]), rsb = fadd2(rs4[2], rs4[3]);
+      l_run = l_run * alpha + ((rsa.x + rsb.x) + (rsa.y + rsb.y));
+    }
+    if (live) {
+      // epilogue: l = both halves' sums; this warp's half of O / l -> bf16 -> global
+      xsum[(s * 2 + hc) * kBM + row] = l_run;
+      named_bar_sync(1 + s, 8 * 32);
+      const float inv = 1.f / (l_run + xsum[(s * 2 + (hc ^ 1)) * kBM + row]);
+      mbar_wait(o_full, 0);
+      tc_fence_after();
+      __nv_bfloat16* orow =
+          static_cast<__nv_bfloat16*>(a.out) + (int64_t(a.q_off[b] + t) * a.Hq + hq_s[s]) * D + hc * kOCols;
+#pragma unroll
+      for (int c = 0; c < kOCols; c += 16) {
+        float o[16];
+        tc_ld16(tO + c, o);
+        tc_wait_ld();
+        if (t < q_len) {
+#pragma unroll
+          for (int y = 0; y < 16; y += 8) {
+            uint4 v;
+            v.x = pack_bf16(o[y + 0] * inv, o[y + 1] * inv);
+            v.y = pack_bf16(o[y + 2] * inv, o[y + 3] * inv);
+            v.z = pack_bf16(o[y + 4] * inv, o[y + 5] * inv);
+            v.w = pack_bf16(o[y + 6] * inv, o[y + 7] * inv);
+            *reinterpret_cast<uint4*>(orow + c + y) = v;
+          }
+        }
+      }
+    }
+  }
+#else
   } else if (warp < 8) {
     // ================================================================ softmax (slot = warp / 4)
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
@@ -528,44 +704,31 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           x[c + 3] = (ci.w & cmask) <= my_i ? x[c + 3] : -CUDART_INF_F;
         }
       }
-      // row max as a tree (8 independent partial maxima), not a 64-deep chain
-      float pm[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) pm[k] = fmaxf(x[k], x[k + 8]);
-#pragma unroll
-      for (int c = 16; c < kBN; c += 16) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) pm[k] = fmaxf(pm[k], fmaxf(x[c + k], x[c + k + 8]));
-      }
-      float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
       __syncwarp();
-      if (lane == 0) mbar_arrive(&c_empty[cs]);
-      mx *= sl2;
-      // lazy rescale: move the running max only when it grows by > 2^8
-      const bool grow = mx > m_run + kRescaleThreshold;
-      const float m_new = grow ? mx : m_run;
-      const float alpha = grow ? fast_exp2(m_run - m_new) : 1.f;
-      m_run = m_new;
-      if (j > 0 && __any_sync(0xffffffffu, grow)) {  // O_s is settled: PV_s(j-1) completed before S_s(j)
-        float o[32];
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          tc_ld32(tO + c * 32, o);
-          tc_wait_ld();
-#pragma unroll
-          for (int y = 0; y < 32; ++y) o[y] *= alpha;
-          tc_st32(tO + c * 32, reinterpret_cast<const uint32_t*>(o));
-        }
-      }
-      // p = 2^(x*sl2 - m): f32x2 FFMA for the argument; 3 of every 4 pairs on the
-      // MUFU ex2 unit, 1 pair on the FMA pipe (degree-3 polynomial, rel. err 1e-4)
-      // a row with nothing visible yet (span-masked leading tiles) keeps p = 0, not NaN
-      const float m_use = m_new == -CUDART_INF_F ? 0.f : m_new;
-      const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_use, -m_use);
+      if (lane == 0) mbar_arrive(&c_empty[cs]);  // col[] consumed (masking done)
+      // p = 2^(x*sl2 - m): f32x2 FFMA for the argument, MUFU ex2 (optionally 1 pair in
+      // HPA_POLY_EVERY on the FMA pipe); 4 independent partial row sums
+      const float2 sl2x2 = make_float2(sl2, sl2);
       float2 rs4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      auto exps_half = [&](int half, float m_use, uint32_t* pk) {
+        const float2 negm = make_float2(-m_use, -m_use);
+        if (HPA_EXP_INPLACE) {
+          // all ex2 first (in place: x of this half is dead once its max is known), then the sums
+          // and bf16 packs, so no MUFU result is consumed right behind its producer
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t pk[kBN / 4];
+          for (int c = half * 64; c < half * 64 + 64; c += 2) {
+            const float2 arg = ffma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
+            x[c] = fast_exp2(arg.x);
+            x[c + 1] = fast_exp2(arg.y);
+          }
+#pragma unroll
+          for (int c = half * 64; c < half * 64 + 64; c += 2) {
+            const float2 e = make_float2(x[c], x[c + 1]);
+            rs4[(c >> 1) & 3] = fadd2(rs4[(c >> 1) & 3], e);
+            pk[(c - half * 64) >> 1] = HPA_P_PACK_ALU ? pack_bf16_alu(e.x, e.y) : pack_bf16(e.x, e.y);
+          }
+          return;
+        }
 #pragma unroll
         for (int c = half * 64; c < half * 64 + 64; c += 2) {
           const float2 arg = ffma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
@@ -576,23 +739,81 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             e.x = fast_exp2(arg.x);
             e.y = fast_exp2(arg.y);
           }
-            rs4[(c >> 1) & 3] = fadd2(rs4[(c >> 1) & 3], e);  // 4 independent partial sums
-          pk[(c - half * 64) >> 1] = pack_bf16(e.x, e.y);
+          rs4[(c >> 1) & 3] = fadd2(rs4[(c >> 1) & 3], e);
+          pk[(c - half * 64) >> 1] = HPA_P_PACK_ALU ? pack_bf16_alu(e.x, e.y) : pack_bf16(e.x, e.y);
         }
-        // P (bf16 pairs) over S: keys [64 half, 64 half + 64) -> columns [128 s + 32 half, +32)
-        tc_st32(tS + half * 32, pk);
-        if (HPA_PV_SPLIT || half == 1) {
-          tc_wait_st();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            if (!HPA_PV_SPLIT) mbar_arrive(&p_full[2 * s]);
-            mbar_arrive(&p_full[2 * s + half]);
+      };
+      // Optimistic first half: once every row of the warp has a finite running max, the
+      // first half's exps are computed against it while the tile max is reduced alongside
+      // (ALU work next to MUFU work). Lazy rescaling keeps the running max unless the tile max
+      // exceeds it by > 2^8, so the result is exact whenever no row grew; otherwise the warp
+      // redoes half 0 on the exact path below.
+      uint32_t pk0[kBN / 4];
+      const bool opt = HPA_OPT_EXP && __all_sync(0xffffffffu, m_run != -CUDART_INF_F);
+      if (opt) exps_half(0, m_run, pk0);
+      if (row == 0) TRACE(31 + s, j);
+      // row max as a tree (8 independent partial maxima), not a 64-deep chain
+      float pm[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pm[k] = fmaxf(x[k], x[k + 8]);
+#pragma unroll
+      for (int c = 16; c < kBN; c += 16) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pm[k] = fmaxf(pm[k], fmaxf(x[c + k], x[c + k + 8]));
+      }
+      float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+      mx *= sl2;
+      // lazy rescale: move the running max only when it grows by > 2^8
+      const bool grow = mx > m_run + kRescaleThreshold;
+      float alpha = 1.f;
+      float m_use = m_run;
+      if (row == 0) TRACE(33 + s, j);
+      if (!opt || __any_sync(0xffffffffu, grow)) {
+        if (row == 0) TRACE(37 + s, j);  // exact path taken
+        const float m_new = grow ? mx : m_run;
+        alpha = grow ? fast_exp2(m_run - m_new) : 1.f;
+        m_run = m_new;
+        if (j > 0 && __any_sync(0xffffffffu, grow)) {  // O_s is settled: PV_s(j-1) completed before S_s(j)
+          float o[32];
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            tc_ld32(tO + c * 32, o);
+            tc_wait_ld();
+#pragma unroll
+            for (int y = 0; y < 32; ++y) o[y] *= alpha;
+            tc_st32(tO + c * 32, reinterpret_cast<const uint32_t*>(o));
           }
-          if (row == 0) TRACE(11 + 2 * s + half, j);
-          if (lane == 0 && half == 1) TRACE(15 + 4 * s + quarter, j);  // per-warp P completion
-          if (lane == 0 && half == 0) TRACE(23 + 4 * s + quarter, j);  // per-warp P half0
         }
+        // a row with nothing visible yet (span-masked leading tiles) keeps p = 0, not NaN
+        m_use = m_new == -CUDART_INF_F ? 0.f : m_new;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rs4[k] = make_float2(0.f, 0.f);
+        exps_half(0, m_use, pk0);
+      }
+      // P (bf16 pairs) over S: keys [64 half, 64 half + 64) -> columns [128 s + 32 half, +32)
+      if (row == 0) TRACE(35 + s, j);
+      tc_st32(tS, pk0);
+      if (HPA_PV_SPLIT) {
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[2 * s]);
+        if (row == 0) TRACE(11 + 2 * s, j);
+        if (lane == 0) TRACE(23 + 4 * s + quarter, j);  // per-warp P half0
+      }
+      {
+        uint32_t pk1[kBN / 4];
+        exps_half(1, m_use, pk1);
+        tc_st32(tS + 32, pk1);
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (!HPA_PV_SPLIT) mbar_arrive(&p_full[2 * s]);
+          mbar_arrive(&p_full[2 * s + 1]);
+        }
+        if (row == 0) TRACE(12 + 2 * s, j);
+        if (lane == 0) TRACE(15 + 4 * s + quarter, j);  // per-warp P completion
       }
       const float2 rsa = fadd2(rs4[0], rs4[1]), rsb = fadd2(rs4[2], rs4[3]);
       l_run = l_run * alpha + ((rsa.x + rsb.x) + (rsa.y + rsb.y));
@@ -622,6 +843,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
     }
   }
+#endif  // HPA_SM16
   tc_fence_before();
   __syncthreads();
   if (warp == kMmaWarp) {

@@ -124,6 +124,12 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo (low 16 bits)
   return *reinterpret_cast<uint32_t*>(&v);
 }
+// Same packing on the integer ALU pipe (F2FP issues on the XU pipe that MUFU.EX2 also uses):
+// round to nearest with ties away from zero (add half an ulp of bf16, keep the upper halves).
+// Differs from RNE only on exact ties. For finite non-negative inputs (softmax P).
+__device__ __forceinline__ uint32_t pack_bf16_alu(float lo, float hi) {
+  return __byte_perm(__float_as_uint(lo) + 0x8000u, __float_as_uint(hi) + 0x8000u, 0x7632);
+}
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

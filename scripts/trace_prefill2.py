@@ -35,3 +35,10 @@ for s in (0, 1):
     print(f"slot{s} per-warp P half0 rel s_full{s}:", [[int(t[23 + 4 * s + w, j] - t[7 + s, j]) for w in range(4)] for j in range(20, 24)])
     print(f"slot{s} per-warp P done rel s_full{s}:", [[int(t[15 + 4 * s + w, j] - t[7 + s, j]) for w in range(4)] for j in range(20, 24)])
     print(f"slot{s} mma got half0 / half1 rel s_full{s}:", [(int(t[3 + s, j] - t[7 + s, j]), int(t[5 + s, j] - t[7 + s, j])) for j in range(20, 24)])
+
+for s in (0, 1):
+    print(f"slot{s} (warp q0): ld->opt exps done, ->max done, ->before st, exact path?:",
+          [(int(t[31 + s, j] - t[9 + s, j]), int(t[33 + s, j] - t[31 + s, j]), int(t[35 + s, j] - t[33 + s, j]), int(t[37 + s, j] != 0)) for j in range(20, 26)])
+
+for s in (0, 1):
+    print(f"slot{s} (warp q0): ld -> before P st (exact path: max + exps):", [int(t[35 + s, j] - t[9 + s, j]) for j in range(20, 28)])
