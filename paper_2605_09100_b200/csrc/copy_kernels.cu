@@ -90,9 +90,9 @@ __global__ void __launch_bounds__(256) scatter_kernel(PoolGeom g, int32_t* __res
 }
 
 // Same, with the metadata in the kernel parameters (no H2D copy).
-template <int D>
+template <int D, int N>
 __global__ void __launch_bounds__(256) scatter_inline_kernel(PoolGeom g, int32_t* __restrict__ arena,
-                                                             const __grid_constant__ InlineMeta m) {
+                                                             const __grid_constant__ InlineMetaT<N> m) {
   grid_dependency_wait();
   grid_launch_dependents();
   const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
@@ -142,13 +142,23 @@ cudaError_t launch_scatter(const PoolGeom& g, int32_t* arena, const WordWrite* w
   return launch_pdl(scatter_kernel<64>, grid, dim3(256), 0, s, g, arena, words, n_words, r, idx);
 }
 
-cudaError_t launch_scatter_inline(const PoolGeom& g, int32_t* arena, const InlineMeta& m, int64_t max_rows,
-                                  cudaStream_t s) {
+template <int N>
+cudaError_t launch_scatter_inline_n(const PoolGeom& g, int32_t* arena, const InlineMetaT<N>& m, int64_t max_rows,
+                                    cudaStream_t s) {
   int64_t bx = m.has_rec ? (max_rows * g.Hkv * g.L * (g.D / 8) / 4 + 255) / 256 : (m.n_words + 255) / 256;
   if (bx > 148 * 16) bx = 148 * 16;
   if (bx < 1) bx = 1;
-  if (g.D == 128) return launch_pdl(scatter_inline_kernel<128>, dim3(unsigned(bx)), dim3(256), 0, s, g, arena, m);
-  return launch_pdl(scatter_inline_kernel<64>, dim3(unsigned(bx)), dim3(256), 0, s, g, arena, m);
+  if (g.D == 128) return launch_pdl(scatter_inline_kernel<128, N>, dim3(unsigned(bx)), dim3(256), 0, s, g, arena, m);
+  return launch_pdl(scatter_inline_kernel<64, N>, dim3(unsigned(bx)), dim3(256), 0, s, g, arena, m);
+}
+
+cudaError_t launch_scatter_inline(const PoolGeom& g, int32_t* arena, const InlineMeta& m, int64_t max_rows,
+                                  cudaStream_t s) {
+  return launch_scatter_inline_n(g, arena, m, max_rows, s);
+}
+cudaError_t launch_scatter_inline(const PoolGeom& g, int32_t* arena, const InlineMetaSmall& m, int64_t max_rows,
+                                  cudaStream_t s) {
+  return launch_scatter_inline_n(g, arena, m, max_rows, s);
 }
 
 cudaError_t launch_export(const PoolGeom& g, DevTables t, int32_t layer, int32_t seq,

@@ -66,14 +66,20 @@ cudaError_t launch_scatter(const PoolGeom& g, int32_t* arena, const WordWrite* w
 // common decode-step append): table words (2 ints each) then slots (1 int
 // each), at most kInlineInts ints, and at most one record.
 constexpr int kInlineInts = 1536;
-struct InlineMeta {
+constexpr int kInlineIntsSmall = 224;  // the common case (a decode-step append, a compress) in < 1 KB
+template <int N>
+struct InlineMetaT {
   int32_t n_words;
   int32_t n_slots;
   int32_t has_rec;
   int32_t pad;
   ScatterRecord rec;
-  int32_t data[kInlineInts];
+  int32_t data[N];
 };
+using InlineMeta = InlineMetaT<kInlineInts>;
+using InlineMetaSmall = InlineMetaT<kInlineIntsSmall>;  // the launch copies the whole parameter block
+cudaError_t launch_scatter_inline(const PoolGeom& g, int32_t* arena, const InlineMetaSmall& m, int64_t max_rows,
+                                  cudaStream_t s);
 cudaError_t launch_scatter_inline(const PoolGeom& g, int32_t* arena, const InlineMeta& m, int64_t max_rows,
                                   cudaStream_t s);
 

@@ -429,19 +429,30 @@ hpa_status_t ship(hpa_cache_t* c, cudaStream_t s, const std::vector<ScatterRecor
     }
     c->pending.resize(w);
   }
-  if (recs.size() <= 1 && 2 * c->pending.size() + slots.size() <= size_t(kInlineInts)) {
-    InlineMeta m;
-    m.n_words = int32_t(c->pending.size());
-    m.n_slots = int32_t(slots.size());
-    m.has_rec = recs.empty() ? 0 : 1;
-    m.pad = 0;
-    if (!recs.empty()) m.rec = recs[0];
-    for (size_t i = 0; i < c->pending.size(); ++i) {
-      m.data[2 * i] = c->pending[i].idx;
-      m.data[2 * i + 1] = c->pending[i].val;
+  const size_t n_ints = 2 * c->pending.size() + slots.size();
+  if (recs.size() <= 1 && n_ints <= size_t(kInlineInts)) {
+    // metadata as kernel parameters (no H2D copy); the launch copies the whole parameter
+    // block, so the common small case uses the small variant
+    auto fill_launch = [&](auto& m) -> cudaError_t {
+      m.n_words = int32_t(c->pending.size());
+      m.n_slots = int32_t(slots.size());
+      m.has_rec = recs.empty() ? 0 : 1;
+      m.pad = 0;
+      if (!recs.empty()) m.rec = recs[0];
+      for (size_t i = 0; i < c->pending.size(); ++i) {
+        m.data[2 * i] = c->pending[i].idx;
+        m.data[2 * i + 1] = c->pending[i].val;
+      }
+      if (!slots.empty()) std::memcpy(m.data + 2 * c->pending.size(), slots.data(), slots.size() * 4);
+      return launch_scatter_inline(c->geom(), c->arena, m, max_rows, s);
+    };
+    if (n_ints <= size_t(kInlineIntsSmall)) {
+      InlineMetaSmall m;
+      HPA_CUDA(fill_launch(m));
+    } else {
+      InlineMeta m;
+      HPA_CUDA(fill_launch(m));
     }
-    if (!slots.empty()) std::memcpy(m.data + 2 * c->pending.size(), slots.data(), slots.size() * 4);
-    HPA_CUDA(launch_scatter_inline(c->geom(), c->arena, m, max_rows, s));
     c->launches += 1;
     c->pending.clear();
     return HPA_OK;
