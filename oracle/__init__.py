@@ -34,4 +34,10 @@ from .hpa_oracle import (  # noqa: F401
     kv_cache_bytes,
     expected_table,
     META_LATENT_BIT,
+    E4M3_MAX,
+    e4m3_values,
+    e4m3_encode,
+    quantize_rows_e4m3,
+    dequantize_rows_e4m3,
+    bf16_round,
 )

@@ -23,6 +23,64 @@ def kv_cache_bytes(num_layers: int, num_kv_heads: int, head_dim: int, seq_len: i
     return 2 * num_layers * num_kv_heads * head_dim * seq_len * elem_bytes
 
 
+# --------------------------------------------------------------------------- fp8 token pages
+# SURVEY §8(f) NEXT-4c ("fp8 token pages with bf16 latent pages"); the paper fixes no fp8
+# scheme (it stores bf16), so the scheme is DESIGN.md reading A20:
+#   per (layer, token row, kv-head) and per tensor (K, V): amax = max_d |x|,
+#   s = fp32(amax / 448) (1 if amax = 0), code = e4m3 RNE-satfinite of fp32(x * fp32(448 / amax));
+#   the stored row means code * s. Latent pages stay bf16.
+E4M3_MAX = 448.0
+
+
+def e4m3_values() -> np.ndarray:
+    """Value of every e4m3 ("e4m3fn": 1-4-3, bias 7, no inf, S.1111.111 = NaN) code, by the
+    format's definition; index = code byte."""
+    out = np.zeros(256)
+    for c in range(256):
+        sign = -1.0 if c & 0x80 else 1.0
+        e, m = (c >> 3) & 0xF, c & 0x7
+        if e == 0xF and m == 0x7:
+            out[c] = np.nan
+        elif e == 0:
+            out[c] = sign * (m / 8.0) * 2.0 ** -6
+        else:
+            out[c] = sign * (1.0 + m / 8.0) * 2.0 ** (e - 7)
+    return out
+
+
+def e4m3_encode(y: np.ndarray) -> np.ndarray:
+    """float32 -> e4m3 code bytes, round to nearest even, saturating to +-448 (the
+    library cast; pinned against a brute-force nearest-value search in the tests)."""
+    import torch
+    t = torch.from_numpy(np.clip(np.asarray(y, dtype=np.float32), -E4M3_MAX, E4M3_MAX))
+    return t.to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+
+
+def quantize_rows_e4m3(x: np.ndarray):
+    """x: [..., d] holding bf16 values. Returns (codes uint8 [..., d], scales float32 [...])
+    following reading A20 in fp32, the precision the kernel uses."""
+    x32 = np.asarray(x, dtype=np.float32)
+    amax = np.max(np.abs(x32), axis=-1)
+    pos = amax > 0
+    safe = np.where(pos, amax, np.float32(1.0)).astype(np.float32)
+    scale = np.where(pos, safe / np.float32(E4M3_MAX), np.float32(1.0)).astype(np.float32)
+    inv = np.where(pos, np.float32(E4M3_MAX) / safe, np.float32(1.0)).astype(np.float32)
+    y = (x32 * inv[..., None]).astype(np.float32)
+    return e4m3_encode(y), scale
+
+
+def dequantize_rows_e4m3(codes: np.ndarray, scales: np.ndarray) -> np.ndarray:
+    """code value * scale, exact in fp64 (4-bit x 24-bit significands)."""
+    return e4m3_values()[codes] * np.asarray(scales, dtype=np.float64)[..., None]
+
+
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """fp32 -> bf16, round to nearest even (torch's cast), returned as fp64 values."""
+    import torch
+    t = torch.from_numpy(np.asarray(x, dtype=np.float32)).to(torch.bfloat16)
+    return t.to(torch.float64).numpy()
+
+
 class _Segment:
     """One segment of a sequence: a run of TOKEN rows or one LATENT set.
 
@@ -31,11 +89,13 @@ class _Segment:
     K, V: fp64 arrays [L][n][H_kv][d] holding the exact bf16 values.
     """
 
-    def __init__(self, kind: str, set_id: int, k: np.ndarray, v: np.ndarray):
+    def __init__(self, kind: str, set_id: int, k: np.ndarray, v: np.ndarray, q8=None):
         self.kind = kind
         self.set_id = set_id
         self.k = k
         self.v = v
+        # fp8 token rows (A20): (k codes, k scales, v codes, v scales), [L][n][H_kv][d] / [L][n][H_kv]
+        self.q8 = q8
 
     @property
     def rows(self) -> int:
@@ -57,7 +117,7 @@ class OracleCache:
     """
 
     def __init__(self, num_layers: int, num_q_heads: int, num_kv_heads: int, head_dim: int,
-                 page_size: int):
+                 page_size: int, token_fp8: bool = False):
         if num_q_heads % num_kv_heads != 0:
             raise ValueError("num_q_heads must be a multiple of num_kv_heads (S:L25)")
         self.L = num_layers
@@ -67,6 +127,7 @@ class OracleCache:
         self.P = page_size
         self.seqs: Dict[int, List[_Segment]] = {}
         self.next_set: Dict[int, int] = {}
+        self.token_fp8 = token_fp8  # NEXT-4c: token rows stored as e4m3 + per-row scales (A20)
 
     # -- op log ---------------------------------------------------------------
     def create_seq(self, seq_id: int) -> None:
@@ -78,16 +139,26 @@ class OracleCache:
         del self.next_set[seq_id]
 
     def append(self, seq_id: int, k: np.ndarray, v: np.ndarray) -> None:
-        """k, v: [L][n][H_kv][d] (values of the bf16 inputs)."""
+        """k, v: [L][n][H_kv][d] (values of the bf16 inputs). With token_fp8 the rows are
+        quantized (A20) and the segment holds their dequantized values."""
         k = np.asarray(k, dtype=np.float64)
         v = np.asarray(v, dtype=np.float64)
+        q8 = None
+        if self.token_fp8:
+            kc, ks = quantize_rows_e4m3(k)
+            vc, vs = quantize_rows_e4m3(v)
+            q8 = (kc, ks, vc, vs)
+            k = dequantize_rows_e4m3(kc, ks)
+            v = dequantize_rows_e4m3(vc, vs)
         segs = self.seqs[seq_id]
         if segs and segs[-1].kind == "token":
             last = segs[-1]
             last.k = np.concatenate([last.k, k], axis=1)
             last.v = np.concatenate([last.v, v], axis=1)
+            if q8 is not None:
+                last.q8 = tuple(np.concatenate([a, b], axis=1) for a, b in zip(last.q8, q8))
         else:
-            segs.append(_Segment("token", -1, k.copy(), v.copy()))
+            segs.append(_Segment("token", -1, k.copy(), v.copy(), q8))
 
     def install(self, seq_id: int, set_id: int, kv: np.ndarray) -> int:
         """kv: [L][2][m][H_kv][d] (SPEC CompressedMemory payload)."""
@@ -119,9 +190,15 @@ class OracleCache:
         keep = last.rows - n_doc_rows - m_rows
         lat_k = last.k[:, keep + n_doc_rows:].copy()
         lat_v = last.v[:, keep + n_doc_rows:].copy()
+        if self.token_fp8:  # latent pages are bf16: the moved rows become bf16(fp32(code) * scale)
+            kc, ks, vc, vs = (a[:, keep + n_doc_rows:] for a in last.q8)
+            lat_k = bf16_round(e4m3_values()[kc].astype(np.float32) * ks[..., None])
+            lat_v = bf16_round(e4m3_values()[vc].astype(np.float32) * vs[..., None])
         if keep > 0:
             last.k = last.k[:, :keep].copy()
             last.v = last.v[:, :keep].copy()
+            if last.q8 is not None:
+                last.q8 = tuple(a[:, :keep].copy() for a in last.q8)
         else:
             segs.pop()
         set_id = self.next_set[seq_id]
@@ -166,6 +243,11 @@ class OracleCache:
         k = np.concatenate([s.k[layer] for s in segs], axis=0)  # [Lb][H_kv][d]
         v = np.concatenate([s.v[layer] for s in segs], axis=0)
         return k.transpose(1, 0, 2).copy(), v.transpose(1, 0, 2).copy()
+
+    def token_codes(self, seq_id: int, layer: int):
+        """fp8 mode: per TOKEN segment in order, (k codes, k scales, v codes, v scales) of
+        one layer, [n][H_kv][d] / [n][H_kv] -- for bit-exact checks of the token pools."""
+        return [tuple(a[layer] for a in sg.q8) for sg in self.seqs[seq_id] if sg.kind == "token"]
 
     def expected_table(self, seq_id: int) -> List[Tuple[str, int, int]]:
         """Expected block-table entries (kind, valid_rows, pos0) for this sequence."""

@@ -373,3 +373,99 @@ def test_partial_attend_and_merge_equal_full_attention():
     o1, l1 = partial_attend(q, k, v, 0.3)           # one shard: lse is log2 sum exp(s)
     s0 = 0.3 * (k[0] @ q[0])
     assert abs(l1[0] - np.log2(np.exp(s0).sum())) <= 1e-12
+
+
+# ----------------------------------------------------------------------------- NEXT-4c fp8 token pages
+def _nearest_e4m3_bruteforce(y):
+    """Independent e4m3 rounding: nearest finite code value, ties to the even mantissa,
+    saturating at +-448 -- by search over the 254 finite codes."""
+    from oracle import e4m3_values
+    vals = e4m3_values()
+    codes = [c for c in range(256) if np.isfinite(vals[c])]
+    out = []
+    for t in np.asarray(y, dtype=np.float64).ravel():
+        t = min(max(t, -448.0), 448.0)
+        best = None
+        for c in codes:
+            dist = abs(vals[c] - t)
+            key = (dist, c & 1)  # ties: even mantissa (lowest code bit) first
+            if best is None or key < best[0]:
+                best = (key, c)
+        c = best[1]
+        if vals[c] == 0.0:  # +0 / -0 both encode the value 0: keep the sign of t
+            c = 0x80 if np.signbit(t) else 0x00
+        out.append(c)
+    return np.array(out, dtype=np.uint8).reshape(np.shape(y))
+
+
+def test_e4m3_format_values():
+    from oracle import e4m3_values
+    v = e4m3_values()
+    assert v[0x7E] == 448.0 and v[0xFE] == -448.0           # largest finite
+    assert v[0x01] == 2.0 ** -9 and v[0x08] == 2.0 ** -6     # smallest subnormal / normal
+    assert np.isnan(v[0x7F]) and np.isnan(v[0xFF])
+    assert np.all(v[:0x7F] == -v[0x80:0xFF])
+    assert np.all(np.diff(v[:0x7F]) > 0)                     # codes 0..126 increase strictly
+
+
+def test_e4m3_encode_matches_bruteforce_including_ties():
+    from oracle import e4m3_encode, e4m3_values
+    rng = np.random.default_rng(5)
+    v = e4m3_values()
+    pos = v[:0x7F]
+    mids = (pos[:-1] + pos[1:]) / 2                           # exact ties between neighbours
+    y = np.concatenate([rng.uniform(-460, 460, 2000), rng.standard_normal(2000) * 0.01,
+                        mids, -mids, [0.0, 448.0, 449.0, 463.9, -500.0]]).astype(np.float32)
+    got = e4m3_encode(y)
+    ref = _nearest_e4m3_bruteforce(y.astype(np.float64))
+    same_value = v[got] == v[ref]
+    assert np.all(same_value), y[~same_value][:10]
+
+
+def test_row_quantization_scheme_a20():
+    from oracle import dequantize_rows_e4m3, e4m3_values, quantize_rows_e4m3
+    rng = np.random.default_rng(6)
+    x = (rng.standard_normal((2, 7, 4, 128)) * rng.uniform(0.01, 5, (2, 7, 4, 1))).astype(np.float32)
+    x[0, 3, 2] = 0.0                                          # an all-zero row
+    codes, s = quantize_rows_e4m3(x)
+    v = e4m3_values()
+    assert s[0, 3, 2] == 1.0 and np.all(codes[0, 3, 2] == 0)
+    amax = np.abs(x).max(-1)
+    nz = amax > 0
+    # the row's largest magnitude lands on +-448 and the scale is amax / 448 (fp32)
+    assert np.all(np.abs(v[codes]).max(-1)[nz] == 448.0)
+    assert np.all(s[nz] == (amax[nz] / np.float32(448)).astype(np.float32))
+    # dequantized error: at most half a code spacing, i.e. <= 2^-4 relative in the normal
+    # range and <= 2^-10 * s below it
+    d = dequantize_rows_e4m3(codes, s)
+    y = np.abs(x / s[..., None])
+    bound = np.where(y >= 2.0 ** -6, 2.0 ** -4 * np.abs(x), 2.0 ** -10 * s[..., None]) * (1 + 1e-6)
+    assert np.all(np.abs(d - x) <= bound)
+
+
+def _bf16(a):
+    return torch.from_numpy(np.asarray(a, dtype=np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
+
+
+def test_oracle_cache_fp8_tokens_and_bf16_latents():
+    from oracle import OracleCache, bf16_round, dequantize_rows_e4m3, e4m3_values, quantize_rows_e4m3
+    rng = np.random.default_rng(8)
+    c = OracleCache(1, 2, 1, 64, 16, token_fp8=True)
+    c.create_seq(0)
+    lat = _bf16(rng.standard_normal((1, 2, 16, 1, 64)))
+    c.install(0, -1, lat)
+    k, v = _bf16(rng.standard_normal((1, 40, 1, 64))), _bf16(rng.standard_normal((1, 40, 1, 64)))
+    c.append(0, k, v)
+    kl, vl = c.logical_kv(0, 0)
+    assert np.array_equal(kl[0, :16], lat[0, 0, :, 0])         # latent rows untouched (bf16)
+    kc, ks = quantize_rows_e4m3(k)
+    assert np.array_equal(kl[0, 16:], dequantize_rows_e4m3(kc, ks)[0, :, 0])
+    assert not np.array_equal(kl[0, 16:], k[0, :, 0])          # tokens really are quantized
+    codes = c.token_codes(0, 0)
+    assert len(codes) == 1 and np.array_equal(codes[0][0], kc[0])
+    # compress moves the trailing m token rows into a bf16 latent set: bf16(fp32(code) * scale)
+    c.compress(0, 24, 16)
+    kl2, _ = c.logical_kv(0, 0)
+    assert kl2.shape[1] == 32
+    exp = bf16_round(e4m3_values()[kc[0, 24:, 0]].astype(np.float32) * ks[0, 24:, 0][:, None])
+    assert np.array_equal(kl2[0, 16:], exp)
