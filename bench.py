@@ -142,7 +142,8 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- workload build
-def build_decode_cache(torch, Cache, shape, n_req, docs, tokens, extra_rows, device, seed, placement_seed=99):
+def build_decode_cache(torch, Cache, shape, n_req, docs, tokens, extra_rows, device, seed, placement_seed=99,
+                       token_kv_dtype="bf16"):
     """Creates a cache holding n_req requests of `docs` latent sets (m=128) followed by
     `tokens` token rows (an int, or one count per request for the ragged variant);
     returns (cache, seq ids). Inputs drawn on the GPU (seeded)."""
@@ -153,8 +154,14 @@ def build_decode_cache(torch, Cache, shape, n_req, docs, tokens, extra_rows, dev
                              placement_seed)
     rows_max = docs * LATENT_ROWS + tokens + extra_rows
     pages_per_seq = docs * math.ceil(LATENT_ROWS / P) + math.ceil((tokens + extra_rows) / P) + 1
-    cache = Cache(shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim, P,
-                  n_req * pages_per_seq + 64, n_req, pages_per_seq, device, placement_seed)
+    if token_kv_dtype == "fp8":  # NEXT-4c: token pages in their own fp8 pool
+        lat_pages = docs * math.ceil(LATENT_ROWS / P)
+        cache = Cache(shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim, P,
+                      n_req * lat_pages + 64, n_req, pages_per_seq, device, placement_seed, "fp8",
+                      n_req * (pages_per_seq - lat_pages) + 64)
+    else:
+        cache = Cache(shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim, P,
+                      n_req * pages_per_seq + 64, n_req, pages_per_seq, device, placement_seed)
     g = torch.Generator(device=f"cuda:{device}").manual_seed(seed)
     seqs = [cache.seq_create() for _ in range(n_req)]
     for _ in range(docs):
@@ -237,6 +244,23 @@ def bench_decode_variants(torch, Cache, dev, stream, pk, page_size):
                      "frac": round(byts / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 4)}
         cache.close()
         torch.cuda.empty_cache()
+    # NEXT-4c: the same configs[1] batch with fp8 token pages (latent pages stay bf16)
+    shape = qwen3_8b_shape(page_size)
+    cache, seqs, _ = build_decode_cache(torch, Cache, shape, 64, 8, 4096, 0, dev, seed=1234, token_kv_dtype="fp8")
+    ms = time_decode_calls(torch, cache, seqs, shape, dev, stream, 50, 5)
+    hkv, d = shape.num_kv_heads, shape.head_dim
+    lat_rows, tok_rows = 8 * 128, 4096
+    per_req = (lat_rows * hkv * d * 2 * 2 + tok_rows * hkv * (d + 4) * 2 + 2 * shape.num_q_heads * d * 2
+               + 4 * math.ceil((lat_rows + tok_rows) / shape.page_size))
+    byts = 64 * per_req
+    bf16_ms = out.get(f"page_size_{64 if page_size != 64 else 16}", {}).get("decode_ms")
+    out["fp8_token_pages"] = {"page_size": page_size, "requests": 64, "latent_rows": lat_rows, "token_rows": tok_rows,
+                              "decode_ms": round(ms, 4), "tokens_per_s": round(64 / (ms / 1e3), 1),
+                              "bytes_per_call": byts, "achieved_gbs": round(byts / (ms / 1e3) / 1e9, 1),
+                              "frac": round(byts / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 4),
+                              "note": "token rows: e4m3 codes + fp32 K/V row scales (reading A20); bytes are those read"}
+    cache.close()
+    torch.cuda.empty_cache()
     return out
 
 

@@ -67,6 +67,12 @@ typedef struct {
   uint64_t placement_seed;   /* 0: free list in page order; else a seeded shuffle of the
                                 free list (physical placement is then a random permutation,
                                 SURVEY §8(d) "Physical pages") */
+  int32_t token_kv_dtype;    /* SURVEY §8(f) NEXT-4c: 0 = token pages bf16 (default, the paper's
+                                storage); 1 = token pages fp8 e4m3 with one fp32 scale
+                                per (layer, row, kv-head) for K and for V (reading A20),
+                                held in a separate token pool; latent pages stay bf16. With 1,
+                                decode reads both kinds; prefill returns HPA_ERR_UNSUPPORTED. */
+  int32_t num_token_pages;   /* token_kv_dtype = 1: pages of the fp8 token pool (> 0) */
 } hpa_config_t;
 
 /* Thread-local message of the last failing call ("" if none). */
@@ -90,6 +96,15 @@ hpa_status_t hpa_cache_destroy(hpa_cache_t* c);
 hpa_status_t hpa_cache_pools(hpa_cache_t* c, void** k_pool, void** v_pool, uint64_t* pool_bytes);
 
 /* Allocator state: free pages, pages referenced by at least one table, live sequences. */
+/* NEXT-4c fp8 token pool (token_kv_dtype = 1): device pointers to the e4m3 codes
+ * K8, V8 uint8 [L][num_token_pages][H_kv][P][d] and the fp32 scales KS, VS
+ * [L][num_token_pages][H_kv][P] (row r of a page means code * scale, reading A20), and the
+ * free token pages. The cache owns them; read-only for callers (tests compare them
+ * bit-exactly with the oracle's quantizer). HPA_ERR_INVALID_ARG if the cache stores bf16
+ * token pages. */
+hpa_status_t hpa_cache_token_pool(hpa_cache_t* c, void** k8, void** v8, void** ks, void** vs,
+                                  int32_t* free_token_pages);
+
 hpa_status_t hpa_cache_stats(hpa_cache_t* c, int32_t* free_pages, int32_t* used_pages,
                              int32_t* live_seqs);
 
@@ -219,7 +234,8 @@ hpa_status_t hpa_prefill_span(hpa_cache_t* c, int32_t layer, int32_t n_seqs, con
 hpa_status_t hpa_seq_info(hpa_cache_t* c, int32_t seq_id, int32_t* len, int32_t* n_pages,
                           int32_t* n_latent_rows);
 /* Gathers the logical K and V of (layer, seq) into device bf16 [H_kv][len][d]
- * (one kernel; bit-exact copy of the stored rows in block-table order). */
+ * (one kernel; bit-exact copy of the stored rows in block-table order; fp8 token rows are
+ * written as bf16(fp32(code) * scale), reading A20). */
 hpa_status_t hpa_export_logical_kv(hpa_cache_t* c, int32_t layer, int32_t seq_id, void* k_out,
                                    void* v_out, hpa_stream_t stream);
 /* Host copy of a sequence's block table: pages[i], pos0[i] (logical index of the

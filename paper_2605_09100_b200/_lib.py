@@ -21,6 +21,7 @@ class HPAConfig(ctypes.Structure):
         ("head_dim", c_i32), ("page_size", c_i32), ("num_pages", c_i32),
         ("max_seqs", c_i32), ("max_pages_per_seq", c_i32), ("device", c_i32),
         ("placement_seed", ctypes.c_uint64),
+        ("token_kv_dtype", c_i32), ("num_token_pages", c_i32),
     ]
 
 
@@ -39,6 +40,8 @@ SIGNATURES = {
     "hpa_cache_pools": (c_st, [c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
                                ctypes.POINTER(ctypes.c_uint64)]),
     "hpa_cache_stats": (c_st, [c_vp, c_i32p, c_i32p, c_i32p]),
+    "hpa_cache_token_pool": (c_st, [c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
+                                    ctypes.POINTER(c_vp), c_i32p]),
     "hpa_seq_create": (c_st, [c_vp, c_i32p]),
     "hpa_seq_release": (c_st, [c_vp, c_i32]),
     "hpa_append_kv": (c_st, [c_vp, c_i32, c_i32p, c_i32p, c_vp, c_vp, c_vp]),

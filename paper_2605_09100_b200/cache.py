@@ -56,9 +56,17 @@ class Cache:
 
     def __init__(self, num_layers: int, num_q_heads: int, num_kv_heads: int, head_dim: int,
                  page_size: int, num_pages: int, max_seqs: int, max_pages_per_seq: int,
-                 device: int = 0, placement_seed: int = 0):
+                 device: int = 0, placement_seed: int = 0, token_kv_dtype: str = "bf16",
+                 num_token_pages: int = 0):
+        """token_kv_dtype "fp8" (NEXT-4c): token pages are e4m3 + per-row scales in a separate
+        pool of num_token_pages pages; latent pages stay bf16 (reading A20)."""
+        if token_kv_dtype not in ("bf16", "fp8"):
+            raise ValueError("token_kv_dtype must be 'bf16' or 'fp8'")
+        self.token_fp8 = token_kv_dtype == "fp8"
+        self.num_token_pages = num_token_pages
         self.cfg = HPAConfig(num_layers, num_q_heads, num_kv_heads, head_dim, page_size, num_pages,
-                             max_seqs, max_pages_per_seq, device, placement_seed)
+                             max_seqs, max_pages_per_seq, device, placement_seed,
+                             1 if self.token_fp8 else 0, num_token_pages)
         self.device = device
         self.L, self.Hq, self.Hkv, self.d, self.P = (num_layers, num_q_heads, num_kv_heads,
                                                       head_dim, page_size)
@@ -288,6 +296,18 @@ class Cache:
         k = torch.as_tensor(_CAI(kp.value, shape), device=dev).view(torch.bfloat16)
         v = torch.as_tensor(_CAI(vp.value, shape), device=dev).view(torch.bfloat16)
         return k, v
+
+    def token_pool(self):
+        """NEXT-4c fp8 token pool views: (k codes, v codes) uint8 [L][NPt][H_kv][P][d],
+        (k scales, v scales) fp32 [L][NPt][H_kv][P], free token pages."""
+        k8, v8, ks, vs, free = c_vp(), c_vp(), c_vp(), c_vp(), c_i32()
+        check(LIB.hpa_cache_token_pool(self._h, ctypes.byref(k8), ctypes.byref(v8), ctypes.byref(ks),
+                                       ctypes.byref(vs), ctypes.byref(free)))
+        dev = torch.device(f"cuda:{self.device}")
+        shp = (self.L, self.num_token_pages, self.Hkv, self.P)
+        codes = lambda p: torch.as_tensor(_CAI(p, shp + (self.d,), "|u1"), device=dev)
+        scales = lambda p: torch.as_tensor(_CAI(p, shp, "<f4"), device=dev)
+        return codes(k8.value), codes(v8.value), scales(ks.value), scales(vs.value), free.value
 
     def set_decode_splits(self, splits: int) -> None:
         check(LIB.hpa_set_decode_splits(self._h, splits))

@@ -7,10 +7,81 @@
 #include "hpa_kernels.h"
 #include "ptx.cuh"
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 namespace hpa {
 
 namespace {
+
+// ---- NEXT-4c fp8 token rows (reading A20) --------------------------------------
+// 8 e4m3 codes <- 8 fp32 values, round to nearest even, saturating (element i in byte i).
+__device__ __forceinline__ uint2 e4m3x8_from_f32(const float* x) {
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint16_t h;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(h) : "f"(x[2 * i + 1]), "f"(x[2 * i]));
+    w[i] = h;
+  }
+  return make_uint2(w[0] | (w[1] << 16), w[2] | (w[3] << 16));
+}
+// Appends record r's rows into the fp8 token pool: one (layer, row, head) unit per group of
+// D/8 consecutive lanes (8 elements each); the group reduces the row's amax, then
+// s = amax / 448, codes = e4m3(x * (448 / amax)) (s = 1, codes 0 for an all-zero row).
+template <int D>
+__device__ __forceinline__ void quant_rows(const PoolGeom& g, const ScatterRecord& r, const int32_t* idx) {
+  constexpr int kVPR = D / 8;
+  const uint32_t units = uint32_t(r.n_rows) * uint32_t(g.Hkv) * uint32_t(g.L);
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t ustride = gridDim.x * blockDim.x / kVPR;
+  const uint32_t c = tid % kVPR;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t gmask = ((kVPR == 32 ? 0xffffffffu : ((1u << kVPR) - 1u))) << (lane & ~uint32_t(kVPR - 1));
+  const __nv_bfloat16* ksrc = static_cast<const __nv_bfloat16*>(r.k);
+  const __nv_bfloat16* vsrc = static_cast<const __nv_bfloat16*>(r.v);
+  for (uint32_t unit = tid / kVPR; unit < units; unit += ustride) {
+    const uint32_t h = unit % uint32_t(g.Hkv);
+    const uint32_t rest = unit / uint32_t(g.Hkv);
+    const uint32_t row = rest % uint32_t(r.n_rows);
+    const uint32_t l = rest / uint32_t(r.n_rows);
+    const int32_t slot = r.page_mode ? (idx[r.idx_off + ((r.row0 + int32_t(row)) >> g.log2P)] << g.log2P) +
+                                           ((r.row0 + int32_t(row)) & (g.P - 1))
+                                     : idx[r.idx_off + row];
+    const int64_t prow = ((int64_t(l) * g.NPt + (slot >> g.log2P)) * g.Hkv + h) * g.P + (slot & (g.P - 1));
+    const int64_t src = int64_t(l) * r.stride_l + int64_t(row) * r.stride_r + int64_t(h) * D + c * 8;
+    const int4 kraw = __ldg(reinterpret_cast<const int4*>(ksrc + src));
+    const int4 vraw = __ldg(reinterpret_cast<const int4*>(vsrc + src));
+    float kx[8], vx[8];
+    const __nv_bfloat162* kb = reinterpret_cast<const __nv_bfloat162*>(&kraw);
+    const __nv_bfloat162* vb = reinterpret_cast<const __nv_bfloat162*>(&vraw);
+    float ka = 0.f, va = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 kf = __bfloat1622float2(kb[i]), vf = __bfloat1622float2(vb[i]);
+      kx[2 * i] = kf.x; kx[2 * i + 1] = kf.y;
+      vx[2 * i] = vf.x; vx[2 * i + 1] = vf.y;
+      ka = fmaxf(ka, fmaxf(fabsf(kf.x), fabsf(kf.y)));
+      va = fmaxf(va, fmaxf(fabsf(vf.x), fabsf(vf.y)));
+    }
+#pragma unroll
+    for (int o = kVPR / 2; o > 0; o >>= 1) {
+      ka = fmaxf(ka, __shfl_xor_sync(gmask, ka, o));
+      va = fmaxf(va, __shfl_xor_sync(gmask, va, o));
+    }
+    const float kinv = ka > 0.f ? __fdiv_rn(448.f, ka) : 1.f, vinv = va > 0.f ? __fdiv_rn(448.f, va) : 1.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      kx[i] = __fmul_rn(kx[i], kinv);
+      vx[i] = __fmul_rn(vx[i], vinv);
+    }
+    *reinterpret_cast<uint2*>(g.k8 + prow * D + c * 8) = e4m3x8_from_f32(kx);
+    *reinterpret_cast<uint2*>(g.v8 + prow * D + c * 8) = e4m3x8_from_f32(vx);
+    if (c == 0) {
+      g.ks[prow] = ka > 0.f ? __fdiv_rn(ka, 448.f) : 1.f;
+      g.vs[prow] = va > 0.f ? __fdiv_rn(va, 448.f) : 1.f;
+    }
+  }
+}
 
 // Copies record r's rows (all layers, heads, 16-B vectors) into their pool slots,
 // grid-stride over this record's CTAs. A unit is one (layer, row, head) = D/8
@@ -48,7 +119,12 @@ __device__ __forceinline__ void copy_rows(const PoolGeom& g, const ScatterRecord
         }
         dst[u] = ((int64_t(l) * g.NP + (slot >> g.log2P)) * g.Hkv + h) * page_elems +
                  int64_t(slot & (g.P - 1)) * D + c * 8;
-        if (r.src_from_pool) {  // in-cache move: source is another pool slot
+        if (r.src_from_pool && r.src_fp8) {  // move out of the fp8 token pool: dequantize
+          const int32_t ss = idx[r.src_off + row];
+          const int64_t prow = ((int64_t(l) * g.NPt + (ss >> g.log2P)) * g.Hkv + h) * g.P + (ss & (g.P - 1));
+          kv[u] = bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(g.k8 + prow * D + c * 8), g.ks[prow]);
+          vv[u] = bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(g.v8 + prow * D + c * 8), g.vs[prow]);
+        } else if (r.src_from_pool) {  // in-cache move: source is another pool slot
           const int32_t ss = idx[r.src_off + row];
           const int64_t src = ((int64_t(l) * g.NP + (ss >> g.log2P)) * g.Hkv + h) * page_elems +
                               int64_t(ss & (g.P - 1)) * D + c * 8;
@@ -86,7 +162,8 @@ __global__ void __launch_bounds__(256) scatter_kernel(PoolGeom g, int32_t* __res
   const int64_t gtid = (int64_t(blockIdx.y) * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
   for (int64_t i = gtid; i < n_words; i += nthreads) arena[words[i].idx] = words[i].val;
   if (recs == nullptr) return;
-  copy_rows<D>(g, recs[blockIdx.y], idx);
+  if (recs[blockIdx.y].quant8) quant_rows<D>(g, recs[blockIdx.y], idx);
+  else copy_rows<D>(g, recs[blockIdx.y], idx);
 }
 
 // Same, with the metadata in the kernel parameters (no H2D copy).
@@ -99,7 +176,8 @@ __global__ void __launch_bounds__(256) scatter_inline_kernel(PoolGeom g, int32_t
   const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   for (int64_t i = gtid; i < m.n_words; i += nthreads) arena[m.data[2 * i]] = m.data[2 * i + 1];
   if (!m.has_rec) return;
-  copy_rows<D>(g, m.rec, m.data + 2 * m.n_words);
+  if (m.rec.quant8) quant_rows<D>(g, m.rec, m.data + 2 * m.n_words);
+  else copy_rows<D>(g, m.rec, m.data + 2 * m.n_words);
 }
 
 // Grid: x = table entry, y = kv head. Copies rows 0..valid-1 of the page tile
@@ -113,6 +191,19 @@ __global__ void __launch_bounds__(128) export_kernel(PoolGeom g, DevTables t, in
   const int32_t valid = t.meta[idx] & kMetaRowsMask;
   const int32_t len = t.seq_len[seq];
   const int32_t vec_per_row = g.D / 8;
+  if (g.k8 && !(t.meta[idx] & kMetaLatent)) {  // fp8 token page: dequantized to bf16
+    const int64_t row0 = ((int64_t(layer) * g.NPt + page) * g.Hkv + h) * g.P;
+    const int64_t dst0 = (int64_t(h) * len + pos0) * g.D;
+    for (int32_t i = threadIdx.x; i < valid * vec_per_row; i += blockDim.x) {
+      const int64_t prow = row0 + i / vec_per_row;
+      const int64_t off = int64_t(i % vec_per_row) * 8;
+      reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(k_out) + dst0)[i] =
+          bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(g.k8 + prow * g.D + off), g.ks[prow]);
+      reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(v_out) + dst0)[i] =
+          bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(g.v8 + prow * g.D + off), g.vs[prow]);
+    }
+    return;
+  }
   const int64_t src0 = ((int64_t(layer) * g.NP + page) * g.Hkv + h) * int64_t(g.P) * g.D;
   const int64_t dst0 = (int64_t(h) * len + pos0) * g.D;
   for (int32_t i = threadIdx.x; i < valid * vec_per_row; i += blockDim.x) {

@@ -44,6 +44,12 @@ constexpr int kNCons = 4;   // consumer warps per CTA
 #ifndef HPA_DEC_DYNAMIC
 #define HPA_DEC_DYNAMIC 1  // 1: units fetched from a ticket counter; 0: static striding over the list
 #endif
+#ifndef HPA_DEC_LAZY
+#define HPA_DEC_LAZY 1  // decode consumers: lazy running-max rescale (threshold 2^8)
+#endif
+#ifndef HPA_FP8_DIAG
+#define HPA_FP8_DIAG 0  // timing diagnostics only (wrong numerics): 1 skip scale loads, 2 skip conversion
+#endif
 #ifndef HPA_DEC_PF
 #define HPA_DEC_PF 8
 #endif
@@ -379,6 +385,32 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_const
 // are already in flight. Per unit: a 1-D bulk copy of the G q rows into a
 // 2-deep Q buffer, the unit's chunks, then one end-of-unit sentinel per consumer
 // (cmeta 0); after the last unit one end-of-kernel sentinel per consumer (-1).
+// NEXT-4c: one 16-row fp8 tile (codes, row stride D bytes) -> the bf16 [D/64][16][128 B]
+// 128-B-swizzled layout the ldmatrix code reads; raw code values (exact in bf16), the
+// per-row scales are applied to S and P. Warp-wide: lane -> row lane/2, half the columns.
+// All lanes read before any lane writes, so src may overlap dst (the V tile converts in place).
+template <int D>
+__device__ __forceinline__ void fp8_tile_to_bf16(const uint8_t* src, uint8_t* dst, int lane) {
+  constexpr int kG = D / 16;  // 8-element groups per lane
+  const int r = lane >> 1;
+  const uint2* s2 = reinterpret_cast<const uint2*>(src + r * D + (lane & 1) * (D / 2));
+  uint2 c[kG];
+#pragma unroll
+  for (int g = 0; g < kG; ++g) c[g] = s2[g];
+  __syncwarp();
+#pragma unroll
+  for (int g = 0; g < kG; ++g) {
+    const int cc = ((lane & 1) * (D / 2) + g * 8) >> 3;  // 16-B bf16 chunk index in the row
+    *reinterpret_cast<int4*>(dst + (cc >> 3) * 2048 + sw128(r, cc & 7)) = bf16x8_from_e4m3(c[g], 1.f);
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 constexpr int kWB = 8;  // table-walker ring: pieces of one header + up to 31 page entries
 
 template <int D>
@@ -392,7 +424,8 @@ struct PDecodeSmem {
   static constexpr int oMeta = oBar + (2 * kNSt + 4 + 2 * kWB) * 8;
   static constexpr int oQMeta = (oMeta + kNSt * 4 + 15) & ~15;  // 2 x int4 {b, h, split, -}: unit of Q buffer
   static constexpr int oWalk = oQMeta + 32;                      // [WB][32] int2 pieces
-  static constexpr int oZero = oWalk + kWB * 32 * 8;             // 16 zero bytes: A-operand rows >= G
+  static constexpr int oScl = oWalk + kWB * 32 * 8;              // [NST][32] fp32: K, V scales of fp8 chunks
+  static constexpr int oZero = oScl + kNSt * 32 * 4;             // 16 zero bytes: A-operand rows >= G
   static constexpr int oQ = oZero + 16;                          // 2 x [G][D] q rows (unswizzled)
   static __host__ __device__ int qbuf(int G) { return G * D * 2; }
   static __host__ __device__ int oMerge(int G) { return oQ + 2 * qbuf(G); }
@@ -403,6 +436,7 @@ struct PDecodeSmem {
 template <int D>
 __global__ void __launch_bounds__((kNCons + 2) * 32, HPA_DECODE_CTAS_PER_SM)
 decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                         const __grid_constant__ CUtensorMap tm_k8, const __grid_constant__ CUtensorMap tm_v8,
                          const DecodeArgs a) {
   using L = PDecodeSmem<D>;
   extern __shared__ __align__(1024) uint8_t smem_pd[];
@@ -425,6 +459,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
   volatile int32_t* cmeta = reinterpret_cast<int32_t*>(smem + L::oMeta);
   int4* qmeta = reinterpret_cast<int4*>(smem + L::oQMeta);
   int2* walk = reinterpret_cast<int2*>(smem + L::oWalk);
+  float* scl = reinterpret_cast<float*>(smem + L::oScl);
   float* mo = reinterpret_cast<float*>(smem + L::oMerge(G));  // [NCONS][G][D]
   float* mm = mo + kNCons * G * D;                          // [NCONS][G]
   float* ml = mm + kNCons * G;
@@ -489,7 +524,10 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
           item = make_int2(ur.x, h | (split << 8) | (cnt << 16) | (first << 24) | (last << 25));
         } else if (lane <= cnt) {
           const int page = bt[e + lane - 1];
-          item = make_int2(((a.layer * a.NP + page) * a.Hkv + h) * a.P, mt[e + lane - 1] & kMetaRowsMask);
+          const int mv = mt[e + lane - 1];
+          const int f8 = a.fp8 && !(mv & kMetaLatent);  // fp8 token page (NEXT-4c)
+          item = make_int2(((a.layer * (f8 ? a.NPt : a.NP) + page) * a.Hkv + h) * a.P,
+                           (mv & kMetaRowsMask) | (f8 << 16));
         }
         const int ws = pc % kWB;
         if (pc >= kWB) mbar_wait(&w_empty[ws], ((pc / kWB) - 1) & 1);
@@ -545,14 +583,26 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         const int last = (hd.y >> 25) & 1;
         for (int j = 1; j <= cnt; ++j) {
           const int2 en = it[j];
-          const int rowbase = en.x, valid = en.y;
+          const int rowbase = en.x, valid = en.y & 0xffff, f8 = en.y >> 16;
           for (int sub = 0; sub * kChunk < valid; ++sub, ++i) {
             const int slot = i % kNSt;
             if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
-            cmeta[slot] = min(kChunk, valid - sub * kChunk);
-            mbar_arrive_expect_tx(&full[slot], L::kStageBytes);
+            cmeta[slot] = min(kChunk, valid - sub * kChunk) | (f8 << 16);
             uint8_t* kd = stages + slot * L::kStageBytes;
             uint8_t* vd = kd + L::kTileBytes;
+            if (f8) {
+              // fp8 chunk (NEXT-4c): codes into the stage's upper half, per-row scales aside;
+              // the consumer converts them to the bf16 layout in place
+              mbar_arrive_expect_tx(&full[slot], uint32_t(2 * kChunk * D + (HPA_FP8_DIAG == 1 ? 0 : 2 * kChunk * 4)));
+              tma_load_2d(kd + L::kTileBytes, &tm_k8, &full[slot], 0, rowbase + sub * kChunk);
+              tma_load_2d(kd + L::kTileBytes + kChunk * D, &tm_v8, &full[slot], 0, rowbase + sub * kChunk);
+              if (HPA_FP8_DIAG != 1) {
+                bulk_g2s(scl + slot * 32, a.ks + rowbase + sub * kChunk, kChunk * 4, &full[slot]);
+                bulk_g2s(scl + slot * 32 + 16, a.vs + rowbase + sub * kChunk, kChunk * 4, &full[slot]);
+              }
+              continue;
+            }
+            mbar_arrive_expect_tx(&full[slot], L::kStageBytes);
             if (HPA_DEC_MAP3 && HPA_DEC_EVICT_FIRST) {
               tma_load_3d_hint(kd, &tm_k, &full[slot], 0, rowbase + sub * kChunk, 0, pol);
               tma_load_3d_hint(vd, &tm_v, &full[slot], 0, rowbase + sub * kChunk, 0, pol);
@@ -616,15 +666,33 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     for (;; i += kNCons) {
       const int slot = i % kNSt;
       mbar_wait(&full[slot], (i / kNSt) & 1);
-      const int nvalid = cmeta[slot];
+      int nvalid = cmeta[slot];
       if (nvalid <= 0) {  // sentinel: release the slot and finish the unit
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
         i += kNCons;
         break;
       }
-      const uint8_t* kt = stages + slot * L::kStageBytes;
-      const uint8_t* vt = kt + L::kTileBytes;
+      const bool c8 = nvalid >= 0x10000;  // fp8 chunk (NEXT-4c)
+      nvalid &= 0xffff;
+      uint8_t* kt = stages + slot * L::kStageBytes;
+      uint8_t* vt = kt + L::kTileBytes;
+      // per owned key column (2t, 2t+1, 8+2t, 9+2t): K scale (x softmax scale) and V scale
+      float kmul[4] = {sl2, sl2, sl2, sl2}, vmul[4] = {1.f, 1.f, 1.f, 1.f};
+      if (c8) {
+        if (HPA_FP8_DIAG != 2) {
+          fp8_tile_to_bf16<D>(kt + L::kTileBytes, kt, lane);
+          fp8_tile_to_bf16<D>(kt + L::kTileBytes + kChunk * D, vt, lane);
+        }
+        __syncwarp();
+        const float* sc = scl + slot * 32;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int col = (q >> 1) * 8 + 2 * (lane & 3) + (q & 1);
+          kmul[q] = sc[col] * sl2;
+          vmul[q] = sc[16 + col];
+        }
+      }
       float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks) {
@@ -643,7 +711,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int col = j * 8 + 2 * (lane & 3) + (e & 1);
-          x[j][e] = col < nvalid ? s[j][e] * sl2 : -CUDART_INF_F;
+          x[j][e] = col < nvalid ? s[j][e] * kmul[j * 2 + (e & 1)] : -CUDART_INF_F;
         }
         mx0 = fmaxf(mx0, fmaxf(x[j][0], x[j][1]));
         mx1 = fmaxf(mx1, fmaxf(x[j][2], x[j][3]));
@@ -652,7 +720,17 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
       mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
       mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+#if HPA_DEC_LAZY
+      // lazy rescale (as in prefill): the running max moves only when a row's chunk max exceeds
+      // it by > 2^8, so p <= 2^8 (exact enough in bf16, far from fp32 limits) and the O rescale
+      // below is skipped for most chunks
+      const bool g0 = mx0 > m_r[0] + 8.f, g1 = mx1 > m_r[1] + 8.f;
+      const float mn0 = g0 ? mx0 : m_r[0], mn1 = g1 ? mx1 : m_r[1];
+      const bool any_grow = __any_sync(0xffffffffu, g0 || g1);
+#else
       const float mn0 = fmaxf(m_r[0], mx0), mn1 = fmaxf(m_r[1], mx1);
+      const bool any_grow = true;
+#endif
       const float al0 = fast_exp2(m_r[0] - mn0), al1 = fast_exp2(m_r[1] - mn1);
       m_r[0] = mn0;
       m_r[1] = mn1;
@@ -669,18 +747,20 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       }
       l_r[0] = l_r[0] * al0 + ps0;
       l_r[1] = l_r[1] * al1 + ps1;
+      if (any_grow) {
 #pragma unroll
-      for (int n = 0; n < D / 8; ++n) {
-        o[n][0] *= al0;
-        o[n][1] *= al0;
-        o[n][2] *= al1;
-        o[n][3] *= al1;
+        for (int n = 0; n < D / 8; ++n) {
+          o[n][0] *= al0;
+          o[n][1] *= al0;
+          o[n][2] *= al1;
+          o[n][3] *= al1;
+        }
       }
       uint32_t pa[4];
-      pa[0] = pack_bf16(p[0][0], p[0][1]);
-      pa[1] = pack_bf16(p[0][2], p[0][3]);
-      pa[2] = pack_bf16(p[1][0], p[1][1]);
-      pa[3] = pack_bf16(p[1][2], p[1][3]);
+      pa[0] = pack_bf16(p[0][0] * vmul[0], p[0][1] * vmul[1]);  // V scales fold into P (fp8 chunks)
+      pa[1] = pack_bf16(p[0][2] * vmul[0], p[0][3] * vmul[1]);
+      pa[2] = pack_bf16(p[1][0] * vmul[2], p[1][1] * vmul[3]);
+      pa[3] = pack_bf16(p[1][2] * vmul[2], p[1][3] * vmul[3]);
 #pragma unroll
       for (int dp = 0; dp < D / 16; ++dp) {
         const int mi = lane >> 3;
@@ -796,13 +876,15 @@ __global__ void __launch_bounds__(D) merge_kernel(const float* __restrict__ o_pa
 }
 
 template <int D>
-cudaError_t launch_decode_d(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,
+cudaError_t launch_decode_d(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const CUtensorMap& tm_k8,
+                            const CUtensorMap& tm_v8, const DecodeArgs& a,
                             cudaStream_t s, int* launches) {
   cudaError_t e;
   if (HPA_DECODE_PERSISTENT) {
     const int smem = PDecodeSmem<D>::bytes(a.G);
     const int grid = std::max(1, std::min(a.n_units, decode_slots(D, a.G)));
-    e = launch_pdl(decode_persistent_kernel<D>, dim3(grid), dim3((kNCons + 2) * 32), smem, s, tm_k, tm_v, a);
+    e = launch_pdl(decode_persistent_kernel<D>, dim3(grid), dim3((kNCons + 2) * 32), smem, s, tm_k, tm_v, tm_k8,
+                   tm_v8, a);
   } else {
     const int smem = DecodeSmem<D>::kBytes;
     e = launch_pdl(decode_split_kernel<D>, dim3(a.splits, a.Hkv, a.n_seqs), dim3((kNCons + 1) * 32), smem, s,
@@ -870,11 +952,12 @@ int decode_ctas_per_sm(int32_t D, int32_t /*G*/) {
   return by_smem < 3 ? by_smem : 3;
 }
 
-cudaError_t launch_decode(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,
+cudaError_t launch_decode(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const CUtensorMap& tm_k8,
+                          const CUtensorMap& tm_v8, const DecodeArgs& a,
                           int32_t D, cudaStream_t s, int* launches) {
   if (a.n_seqs == 0) return cudaSuccess;
-  if (D == 128) return launch_decode_d<128>(tm_k, tm_v, a, s, launches);
-  if (D == 64) return launch_decode_d<64>(tm_k, tm_v, a, s, launches);
+  if (D == 128) return launch_decode_d<128>(tm_k, tm_v, tm_k8, tm_v8, a, s, launches);
+  if (D == 64) return launch_decode_d<64>(tm_k, tm_v, tm_k8, tm_v8, a, s, launches);
   return cudaErrorInvalidValue;
 }
 

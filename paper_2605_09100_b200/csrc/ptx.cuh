@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cstdint>
 #include <cstdio>
 #include <utility>
@@ -124,6 +125,21 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo (low 16 bits)
   return *reinterpret_cast<uint32_t*>(&v);
 }
+// 8 codes * scale -> 8 bf16 (fp32 product, bf16 round to nearest even): int4.
+__device__ __forceinline__ int4 bf16x8_from_e4m3(uint2 c, float scale) {
+  uint32_t in[4] = {c.x & 0xffffu, c.x >> 16, c.y & 0xffffu, c.y >> 16};
+  uint32_t out[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t h2;
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(uint16_t(in[i])));
+    const float lo = __half2float(__ushort_as_half(uint16_t(h2 & 0xffffu))) * scale;
+    const float hi = __half2float(__ushort_as_half(uint16_t(h2 >> 16))) * scale;
+    out[i] = pack_bf16(lo, hi);
+  }
+  return make_int4(int(out[0]), int(out[1]), int(out[2]), int(out[3]));
+}
+
 // Same packing on the integer ALU pipe (F2FP issues on the XU pipe that MUFU.EX2 also uses):
 // round to nearest with ties away from zero (add half an ulp of bf16, keep the upper halves).
 // Differs from RNE only on exact ties. For finite non-negative inputs (softmax P).

@@ -133,6 +133,20 @@ bool make_map_dec(CUtensorMap* m, void* base, uint64_t rows, uint64_t cols) {
             CU_TENSOR_MAP_SWIZZLE_128B, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// fp8 token pool map [rows][d] bytes: box {d, 16}, no swizzle (the decode consumers convert
+// the 16 x d tile to the bf16 swizzled layout in shared memory).
+bool make_map_u8(CUtensorMap* m, void* base, uint64_t rows, uint64_t cols) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols};
+  cuuint32_t box[2] = {cuuint32_t(cols), 16};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 // 3-D bf16 map over q [tokens][Hq][d]: box {64, 1, box_tok}, 128-B swizzle.
 bool make_map_q(CUtensorMap* m, const void* base, uint64_t tokens, uint64_t heads, uint64_t d,
                 uint32_t box_tok) {
@@ -305,6 +319,16 @@ struct hpa_cache {
   void* k_pool = nullptr;
   void* v_pool = nullptr;
   uint64_t pool_bytes = 0;
+  // NEXT-4c fp8 token pool (token_kv_dtype = 1): codes + per-row scales, its own allocator
+  bool fp8 = false;
+  PageAllocator alloc8;
+  uint8_t* k8_pool = nullptr;
+  uint8_t* v8_pool = nullptr;
+  float* ks_pool = nullptr;
+  float* vs_pool = nullptr;
+  CUtensorMap tm_k8{}, tm_v8{};
+  // allocator of a segment's pages: token pages live in the fp8 pool when fp8
+  PageAllocator& pages_of(bool latent) { return (fp8 && !latent) ? alloc8 : alloc; }
   int32_t* arena = nullptr;
   DevTables dt{};
   CUtensorMap tm_k_dec{}, tm_v_dec{}, tm_k_pre{}, tm_v_pre{};
@@ -343,7 +367,8 @@ struct hpa_cache {
 
   PoolGeom geom() const {
     return PoolGeom{k_pool, v_pool, cfg.num_layers, cfg.num_pages, cfg.num_kv_heads, cfg.page_size,
-                    cfg.head_dim, __builtin_ctz(uint32_t(cfg.page_size))};
+                    cfg.head_dim, __builtin_ctz(uint32_t(cfg.page_size)), k8_pool, v8_pool, ks_pool, vs_pool,
+                    fp8 ? cfg.num_token_pages : 0};
   }
 
   // Recomputes the host mirror of seq `s` from entry `from_entry` on (entries
@@ -638,6 +663,12 @@ hpa_status_t hpa_cache_create(const hpa_config_t* cfg, hpa_cache_t** out) {
   if (g.num_q_heads / g.num_kv_heads > 16) return fail(HPA_ERR_UNSUPPORTED, "GQA group > 16");
   const int64_t rows = int64_t(g.num_layers) * g.num_pages * g.num_kv_heads * g.page_size;
   if (rows >= (int64_t(1) << 31)) return fail(HPA_ERR_UNSUPPORTED, "pool too large for 32-bit TMA row index");
+  if (g.token_kv_dtype != 0 && g.token_kv_dtype != 1)
+    return fail(HPA_ERR_INVALID_ARG, "token_kv_dtype must be 0 (bf16) or 1 (fp8 e4m3)");
+  const int64_t rows8 = g.token_kv_dtype == 1 ? int64_t(g.num_layers) * g.num_token_pages * g.num_kv_heads * g.page_size : 0;
+  if (g.token_kv_dtype == 1 && g.num_token_pages <= 0)
+    return fail(HPA_ERR_INVALID_ARG, "token_kv_dtype = 1 needs num_token_pages > 0");
+  if (rows8 >= (int64_t(1) << 31)) return fail(HPA_ERR_UNSUPPORTED, "token pool too large for 32-bit TMA row index");
   if (int64_t(g.max_seqs) * g.max_pages_per_seq * 3 + 2 * g.max_seqs >= (int64_t(1) << 31))
     return fail(HPA_ERR_UNSUPPORTED, "table too large");
   if (int64_t(g.max_pages_per_seq) * g.page_size >= (int64_t(1) << 30))
@@ -656,11 +687,17 @@ hpa_status_t hpa_cache_create(const hpa_config_t* cfg, hpa_cache_t** out) {
   c->cfg = g;
   c->num_sms = prop.multiProcessorCount;
   c->alloc.init(g.num_pages, g.placement_seed);
+  c->fp8 = g.token_kv_dtype == 1;
+  if (c->fp8) c->alloc8.init(g.num_token_pages, g.placement_seed ? g.placement_seed ^ 0x5bd1e995ull : 0);
   c->seqs.resize(g.max_seqs);
   c->pool_bytes = uint64_t(rows) * g.head_dim * 2;
   auto cleanup = [&]() {
     if (c->k_pool) cudaFree(c->k_pool);
     if (c->v_pool) cudaFree(c->v_pool);
+    if (c->k8_pool) cudaFree(c->k8_pool);
+    if (c->v8_pool) cudaFree(c->v8_pool);
+    if (c->ks_pool) cudaFree(c->ks_pool);
+    if (c->vs_pool) cudaFree(c->vs_pool);
     if (c->arena) cudaFree(c->arena);
     if (c->counters) cudaFree(c->counters);
     c->ring.destroy();
@@ -672,6 +709,21 @@ hpa_status_t hpa_cache_create(const hpa_config_t* cfg, hpa_cache_t** out) {
       (e = cudaMemset(c->v_pool, 0, c->pool_bytes)) != cudaSuccess) {
     cleanup();
     return cuda_fail(e, "pool allocation");
+  }
+  if (c->fp8) {
+    const size_t b8 = size_t(rows8) * g.head_dim, bs = size_t(rows8) * 4;
+    if ((e = cudaMalloc(&c->k8_pool, b8)) != cudaSuccess || (e = cudaMalloc(&c->v8_pool, b8)) != cudaSuccess ||
+        (e = cudaMalloc(&c->ks_pool, bs)) != cudaSuccess || (e = cudaMalloc(&c->vs_pool, bs)) != cudaSuccess ||
+        (e = cudaMemset(c->k8_pool, 0, b8)) != cudaSuccess || (e = cudaMemset(c->v8_pool, 0, b8)) != cudaSuccess ||
+        (e = cudaMemset(c->ks_pool, 0, bs)) != cudaSuccess || (e = cudaMemset(c->vs_pool, 0, bs)) != cudaSuccess) {
+      cleanup();
+      return cuda_fail(e, "fp8 token pool allocation");
+    }
+    if (!make_map_u8(&c->tm_k8, c->k8_pool, uint64_t(rows8), uint64_t(g.head_dim)) ||
+        !make_map_u8(&c->tm_v8, c->v8_pool, uint64_t(rows8), uint64_t(g.head_dim))) {
+      cleanup();
+      return fail(HPA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the fp8 token pools");
+    }
   }
   const int64_t arena_words = c->off_nent() + g.max_seqs;
   if ((e = cudaMalloc(&c->arena, size_t(arena_words) * 4)) != cudaSuccess ||
@@ -720,6 +772,10 @@ hpa_status_t hpa_cache_destroy(hpa_cache_t* c) {
   cudaDeviceSynchronize();
   cudaFree(c->k_pool);
   cudaFree(c->v_pool);
+  if (c->k8_pool) cudaFree(c->k8_pool);
+  if (c->v8_pool) cudaFree(c->v8_pool);
+  if (c->ks_pool) cudaFree(c->ks_pool);
+  if (c->vs_pool) cudaFree(c->vs_pool);
   cudaFree(c->arena);
   if (c->batch_dev) cudaFree(c->batch_dev);
   if (c->o_part) cudaFree(c->o_part);
@@ -741,6 +797,18 @@ hpa_status_t hpa_cache_pools(hpa_cache_t* c, void** k_pool, void** v_pool, uint6
   if (k_pool) *k_pool = c->k_pool;
   if (v_pool) *v_pool = c->v_pool;
   if (pool_bytes) *pool_bytes = c->pool_bytes;
+  return HPA_OK;
+}
+
+hpa_status_t hpa_cache_token_pool(hpa_cache_t* c, void** k8, void** v8, void** ks, void** vs,
+                                  int32_t* free_token_pages) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (!c->fp8) return fail(HPA_ERR_INVALID_ARG, "this cache stores bf16 token pages (token_kv_dtype = 0)");
+  if (k8) *k8 = c->k8_pool;
+  if (v8) *v8 = c->v8_pool;
+  if (ks) *ks = c->ks_pool;
+  if (vs) *vs = c->vs_pool;
+  if (free_token_pages) *free_token_pages = c->alloc8.num_free();
   return HPA_OK;
 }
 
@@ -775,7 +843,7 @@ hpa_status_t hpa_seq_release(hpa_cache_t* c, int32_t seq_id) {
   if (hpa_status_t st = check_seq(c, seq_id)) return st;
   Seq& q = c->seqs[seq_id];
   for (const Segment& g : q.segs)
-    for (int32_t p : g.pages) c->alloc.release(p);
+    for (int32_t p : g.pages) c->pages_of(g.latent).release(p);
   q = Seq();
   c->pending.push_back({int32_t(c->off_len() + seq_id), 0});
   c->pending.push_back({int32_t(c->off_nent() + seq_id), 0});
@@ -809,8 +877,9 @@ hpa_status_t hpa_append_kv(hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_id
   if (!k || !v) return fail(HPA_ERR_INVALID_ARG, "null k / v");
   if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15)
     return fail(HPA_ERR_INVALID_ARG, "k / v must be 16-byte aligned");
-  if (need > c->alloc.num_free())
-    return fail(HPA_ERR_OUT_OF_PAGES, "append needs %d pages, %d free", need, c->alloc.num_free());
+  PageAllocator& tok = c->pages_of(false);
+  if (need > tok.num_free())
+    return fail(HPA_ERR_OUT_OF_PAGES, "append needs %d pages, %d free", need, tok.num_free());
   // ---- apply
   DeviceGuard dg(c->cfg.device);
   const int32_t P = c->cfg.page_size;
@@ -824,7 +893,7 @@ hpa_status_t hpa_append_kv(hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_id
     if (q.segs.empty() || q.segs.back().latent) q.segs.push_back(Segment{false, -1, 0, {}});
     Segment& g = q.segs.back();
     const int32_t np = pages_for_append(c, q, n);
-    c->alloc.alloc(np, g.pages);
+    tok.alloc(np, g.pages);
     for (int32_t r = 0; r < n; ++r) {
       const int32_t row = g.rows + r;
       slots.push_back(g.pages[row / P] * P + row % P);
@@ -833,7 +902,8 @@ hpa_status_t hpa_append_kv(hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_id
     c->rebuild(seq_ids[i], first_entry);
   }
   const int64_t Hd = int64_t(c->cfg.num_kv_heads) * c->cfg.head_dim;
-  std::vector<ScatterRecord> recs{ScatterRecord{k, v, total_rows * Hd, Hd, int32_t(total_rows), 0, 0, 0, 0, 0}};
+  std::vector<ScatterRecord> recs{
+      ScatterRecord{k, v, total_rows * Hd, Hd, int32_t(total_rows), 0, 0, 0, 0, 0, c->fp8 ? 1 : 0, 0}};
   return ship(c, static_cast<cudaStream_t>(stream), recs, slots, total_rows);
 }
 
@@ -1083,14 +1153,14 @@ hpa_status_t hpa_seq_compress(hpa_cache_t* c, int32_t seq_id, int32_t n_doc_rows
     idx.push_back(T.pages[row / P] * P + row % P);
   }
   // free the document's (and the latents' token) pages; keep the prefix rows
-  for (size_t k = size_t(keep_pages); k < T.pages.size(); ++k) c->alloc.release(T.pages[k]);
+  for (size_t k = size_t(keep_pages); k < T.pages.size(); ++k) c->pages_of(false).release(T.pages[k]);
   T.pages.resize(size_t(keep_pages));
   T.rows = keep;
   if (keep == 0) q.segs.pop_back();
   q.segs.push_back(std::move(L));
   c->rebuild(seq_id, n_before + std::max(0, keep_pages - 1));
   if (set_id_out) *set_id_out = q.segs.back().set_id;
-  std::vector<ScatterRecord> recs{ScatterRecord{nullptr, nullptr, 0, 0, m_rows, 0, 0, 1, 1, src_off}};
+  std::vector<ScatterRecord> recs{ScatterRecord{nullptr, nullptr, 0, 0, m_rows, 0, 0, 1, 1, src_off, 0, c->fp8 ? 1 : 0}};
   return ship(c, static_cast<cudaStream_t>(stream), recs, idx, m_rows);
 }
 
@@ -1218,10 +1288,13 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
   DecodeArgs a{c->dt, c->batch_dev, q, out, c->o_part, c->lse_part, c->counters, part_o, part_lse, n_seqs, Hq,
                c->cfg.num_kv_heads,
                Hq / c->cfg.num_kv_heads, c->cfg.page_size, c->cfg.num_pages, layer, S,
-               scale * 1.4426950408889634f, c->units_dev, c->nsplit_dev,
+               scale * 1.4426950408889634f, c->fp8 ? 1 : 0, c->fp8 ? c->cfg.num_token_pages : 0,
+               c->ks_pool, c->vs_pool, c->units_dev, c->nsplit_dev,
                c->counters + size_t(c->cfg.max_seqs) * Hkv, c->plan_units};
+  if (c->fp8 && !decode_persistent())
+    return fail(HPA_ERR_UNSUPPORTED, "fp8 token pages need the persistent decode kernel");
   int launched = 0;
-  cudaError_t e = launch_decode(c->tm_k_dec, c->tm_v_dec, a, D, s, &launched);
+  cudaError_t e = launch_decode(c->tm_k_dec, c->tm_v_dec, c->tm_k8, c->tm_v8, a, D, s, &launched);
   c->launches += launched;
   if (e != cudaSuccess) return cuda_fail(e, "decode launch");
   return HPA_OK;
@@ -1266,6 +1339,10 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
     const Seq& s = c->seqs[seq_ids[i]];
     if (q_lens[i] < 1 || q_lens[i] > s.len)
       return fail(HPA_ERR_INVALID_ARG, "q_lens[%d]=%d must be in [1, seq_len=%d]", i, q_lens[i], s.len);
+    if (c->fp8)
+      for (const Segment& g : s.segs)
+        if (!g.latent && g.rows > 0)
+          return fail(HPA_ERR_UNSUPPORTED, "prefill over fp8 token pages is not implemented (NEXT-4c is decode-side)");
     meta[i] = seq_ids[i];
     meta[n_seqs + i] = q_lens[i];
     meta[2 * n_seqs + i] = int32_t(total_q);

@@ -31,13 +31,15 @@ class Pair:
     """A CUDA `Cache` and an `OracleCache` fed the same ops."""
 
     def __init__(self, shape: Shape, num_pages: int, max_seqs: int, max_pages_per_seq: int,
-                 placement_seed: int = 99, seed: int = 1234, v_scale: float = 1.0):
+                 placement_seed: int = 99, seed: int = 1234, v_scale: float = 1.0,
+                 token_fp8: bool = False, num_token_pages: int = 0):
         from paper_2605_09100_b200 import Cache
         self.shape = shape
         self.cache = Cache(shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim,
-                           shape.page_size, num_pages, max_seqs, max_pages_per_seq, 0, placement_seed)
+                           shape.page_size, num_pages, max_seqs, max_pages_per_seq, 0, placement_seed,
+                           "fp8" if token_fp8 else "bf16", num_token_pages)
         self.orc = OracleCache(shape.num_layers, shape.num_q_heads, shape.num_kv_heads,
-                               shape.head_dim, shape.page_size)
+                               shape.head_dim, shape.page_size, token_fp8=token_fp8)
         self.draw = Draw(seed)
         self.v_scale = v_scale
 
