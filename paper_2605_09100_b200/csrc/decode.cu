@@ -44,6 +44,12 @@ constexpr int kNCons = 4;   // consumer warps per CTA
 #ifndef HPA_DEC_DYNAMIC
 #define HPA_DEC_DYNAMIC 1  // 1: units fetched from a ticket counter; 0: static striding over the list
 #endif
+#ifndef HPA_FP8_CVT_INT
+#define HPA_FP8_CVT_INT 0  // 1: integer placement + bf16x2 multiply instead of F2FP (exact; measured slower)
+#endif
+#ifndef HPA_DEC_SWAP
+#define HPA_DEC_SWAP 1  // G <= 8: swapped-operand consumers (keys in M, heads in N)
+#endif
 #ifndef HPA_DEC_LAZY
 #define HPA_DEC_LAZY 1  // decode consumers: lazy running-max rescale (threshold 2^8)
 #endif
@@ -391,17 +397,38 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_const
 // All lanes read before any lane writes, so src may overlap dst (the V tile converts in place).
 template <int D>
 __device__ __forceinline__ void fp8_tile_to_bf16(const uint8_t* src, uint8_t* dst, int lane) {
-  constexpr int kG = D / 16;  // 8-element groups per lane
-  const int r = lane >> 1;
-  const uint2* s2 = reinterpret_cast<const uint2*>(src + r * D + (lane & 1) * (D / 2));
+  constexpr int kG = D / 16;  // 8-byte groups per lane (16 x D bytes / 32 lanes / 8)
+  // lane reads bytes [(32 g + lane) * 8, +8): each LDS.64 covers 256 contiguous bytes
+  // (conflict-free; a row-per-lane-pair mapping was a 16-way bank conflict)
   uint2 c[kG];
 #pragma unroll
-  for (int g = 0; g < kG; ++g) c[g] = s2[g];
+  for (int g = 0; g < kG; ++g) c[g] = reinterpret_cast<const uint2*>(src)[32 * g + lane];
   __syncwarp();
 #pragma unroll
   for (int g = 0; g < kG; ++g) {
-    const int cc = ((lane & 1) * (D / 2) + g * 8) >> 3;  // 16-B bf16 chunk index in the row
-    *reinterpret_cast<int4*>(dst + (cc >> 3) * 2048 + sw128(r, cc & 7)) = bf16x8_from_e4m3(c[g], 1.f);
+    const int byte = (32 * g + lane) * 8;
+    const int r = byte / D, cc = (byte % D) >> 3;  // row, 16-B bf16 chunk index in the row
+    int4 out;
+    if (HPA_FP8_CVT_INT) {
+      // e4m3 -> bf16 without the conversion unit: a code's 7 magnitude bits placed at bf16
+      // bits 4..10 (sign at 15) read as bf16 are the value times 2^-120 for every code,
+      // subnormals included (e4m3 bias 7 vs bf16 bias 127); one bf16x2 multiply by 2^120
+      // restores it exactly
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t bytes = q == 0 ? c[g].x : c[g].y;
+        const uint32_t t0 = __byte_perm(bytes, 0u, 0x1404), t1 = __byte_perm(bytes, 0u, 0x3424);
+        const uint32_t u0 = ((t0 >> 4) & 0x07f007f0u) | (t0 & 0x80008000u);
+        const uint32_t u1 = ((t1 >> 4) & 0x07f007f0u) | (t1 & 0x80008000u);
+        asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(w[2 * q]) : "r"(u0), "r"(0x7b807b80u));
+        asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(w[2 * q + 1]) : "r"(u1), "r"(0x7b807b80u));
+      }
+      out = make_int4(int(w[0]), int(w[1]), int(w[2]), int(w[3]));
+    } else {
+      out = bf16x8_from_e4m3(c[g], 1.f);
+    }
+    *reinterpret_cast<int4*>(dst + (cc >> 3) * 2048 + sw128(r, cc & 7)) = out;
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -433,7 +460,7 @@ struct PDecodeSmem {
   static int bytes(int G) { return oMerge(G) + kNCons * G * (D + 2) * 4; }
 };
 
-template <int D>
+template <int D, bool SW>
 __global__ void __launch_bounds__((kNCons + 2) * 32, HPA_DECODE_CTAS_PER_SM)
 decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                          const __grid_constant__ CUtensorMap tm_k8, const __grid_constant__ CUtensorMap tm_v8,
@@ -646,6 +673,135 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     const int4 um = qmeta[qb];
     if (um.x < 0) break;  // end of work
     const int b = um.x, h = um.y, split = um.z;
+    if constexpr (SW) {
+    // ---- swapped operands (G <= 8): S^T = K Q^T with the chunk's 16 keys in M and the
+    // G heads in N = 8; O^T = V^T P^T with 16 head dims per M tile. Half the MMAs of the
+    // Q-in-M form (whose 16-row M tile is 3/4 padding at G = 4) and half the O registers.
+    // Fragment owner: g = lane / 4 (key row / dim row), t = lane % 4 (heads 2t, 2t+1).
+    const int gq = lane >> 2, tq = lane & 3;
+    uint32_t qbf[D / 16][2];  // B operand Q^T: (dims 16 ks + 2t.., head g), (dims + 8.., head g)
+    {
+      const uint32_t* qrow = reinterpret_cast<const uint32_t*>(qbuf + qb * qbytes + gq * D * 2);
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks) {
+        qbf[ks][0] = gq < G ? qrow[8 * ks + tq] : 0u;
+        qbf[ks][1] = gq < G ? qrow[8 * ks + 4 + tq] : 0u;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&q_empty[qb]);
+    float o[D / 16][4];  // O^T tile mt: (dim 16mt+g, head 2t), (.., 2t+1), (dim +8, 2t), (dim +8, 2t+1)
+#pragma unroll
+    for (int n = 0; n < D / 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m_h[2] = {-CUDART_INF_F, -CUDART_INF_F};  // running max of heads 2t, 2t+1 (log2 domain)
+    float l_h[2] = {0.f, 0.f};                       // partial sums over this lane's keys
+    for (;; i += kNCons) {
+      const int slot = i % kNSt;
+      mbar_wait(&full[slot], (i / kNSt) & 1);
+      int nvalid = cmeta[slot];
+      if (nvalid <= 0) {  // sentinel: release the slot and finish the unit
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        i += kNCons;
+        break;
+      }
+      const bool c8 = nvalid >= 0x10000;  // fp8 chunk (NEXT-4c)
+      nvalid &= 0xffff;
+      uint8_t* kt = stages + slot * L::kStageBytes;
+      uint8_t* vt = kt + L::kTileBytes;
+      float kmul0 = sl2, kmul1 = sl2, vmul0 = 1.f, vmul1 = 1.f;  // keys g and g + 8
+      if (c8) {
+        fp8_tile_to_bf16<D>(kt + L::kTileBytes, kt, lane);
+        fp8_tile_to_bf16<D>(kt + L::kTileBytes + kChunk * D, vt, lane);
+        __syncwarp();
+        const float* sc = scl + slot * 32;
+        kmul0 = sc[gq] * sl2;
+        kmul1 = sc[gq + 8] * sl2;
+        vmul0 = sc[16 + gq];
+        vmul1 = sc[16 + gq + 8];
+      }
+      float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks) {  // A = K (16 keys x 16 dims)
+        const int mi = lane >> 3;
+        const int row = (lane & 7) + (mi & 1) * 8;
+        const int kc = ks * 2 + (mi >> 1);
+        uint32_t ka[4];
+        ldsm_x4(smem_u32(kt + (kc >> 3) * 2048 + sw128(row, kc & 7)), ka[0], ka[1], ka[2], ka[3]);
+        mma_bf16_16816(sacc, ka, qbf[ks][0], qbf[ks][1]);
+      }
+      const float x0 = gq < nvalid ? sacc[0] * kmul0 : -CUDART_INF_F;      // key g,   head 2t
+      const float x1 = gq < nvalid ? sacc[1] * kmul0 : -CUDART_INF_F;      // key g,   head 2t+1
+      const float x2 = gq + 8 < nvalid ? sacc[2] * kmul1 : -CUDART_INF_F;  // key g+8, head 2t
+      const float x3 = gq + 8 < nvalid ? sacc[3] * kmul1 : -CUDART_INF_F;  // key g+8, head 2t+1
+      float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {  // over the 8 key-row lanes
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+      }
+      // lazy rescale: the running max moves only when the chunk max exceeds it by > 2^8
+      const bool g0 = mx0 > m_h[0] + 8.f, g1 = mx1 > m_h[1] + 8.f;
+      const float mn0 = g0 ? mx0 : m_h[0], mn1 = g1 ? mx1 : m_h[1];
+      const bool any_grow = __any_sync(0xffffffffu, g0 || g1);
+      const float al0 = fast_exp2(m_h[0] - mn0), al1 = fast_exp2(m_h[1] - mn1);
+      m_h[0] = mn0;
+      m_h[1] = mn1;
+      const float p0 = fast_exp2(x0 - mn0), p1 = fast_exp2(x1 - mn1);
+      const float p2 = fast_exp2(x2 - mn0), p3 = fast_exp2(x3 - mn1);
+      l_h[0] = l_h[0] * al0 + (p0 + p2);
+      l_h[1] = l_h[1] * al1 + (p1 + p3);
+      if (any_grow) {
+#pragma unroll
+        for (int n = 0; n < D / 16; ++n) {
+          o[n][0] *= al0;
+          o[n][1] *= al1;
+          o[n][2] *= al0;
+          o[n][3] *= al1;
+        }
+      }
+      // B operand P^T: (key g: heads 2t, 2t+1) pairs transposed in registers to (head g: keys
+      // 2t, 2t+1); the V scales (fp8 chunks) fold into P per key
+      const uint32_t pb0 = movmatrix_t(pack_bf16(p0 * vmul0, p1 * vmul0));
+      const uint32_t pb1 = movmatrix_t(pack_bf16(p2 * vmul1, p3 * vmul1));
+#pragma unroll
+      for (int mt = 0; mt < D / 16; ++mt) {  // A = V^T (16 dims x 16 keys)
+        const int mi = lane >> 3;
+        const int key = (lane & 7) + (mi >> 1) * 8;
+        const int dc = 2 * mt + (mi & 1);
+        uint32_t va[4];
+        ldsm_x4_t(smem_u32(vt + (dc >> 3) * 2048 + sw128(key, dc & 7)), va[0], va[1], va[2], va[3]);
+        mma_bf16_16816(o[mt], va, pb0, pb1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    // ---------------------------------------------- merge the consumers' states
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      l_h[0] += __shfl_xor_sync(0xffffffffu, l_h[0], off);
+      l_h[1] += __shfl_xor_sync(0xffffffffu, l_h[1], off);
+    }
+    {
+      const int h0 = 2 * tq, h1 = 2 * tq + 1;
+#pragma unroll
+      for (int mt = 0; mt < D / 16; ++mt) {
+        const int d0 = 16 * mt + gq;
+        if (h0 < G) {
+          mo[(cw * G + h0) * D + d0] = o[mt][0];
+          mo[(cw * G + h0) * D + d0 + 8] = o[mt][2];
+        }
+        if (h1 < G) {
+          mo[(cw * G + h1) * D + d0] = o[mt][1];
+          mo[(cw * G + h1) * D + d0 + 8] = o[mt][3];
+        }
+      }
+      if (gq == 0) {
+        if (h0 < G) { mm[cw * G + h0] = m_h[0]; ml[cw * G + h0] = l_h[0]; }
+        if (h1 < G) { mm[cw * G + h1] = m_h[1]; ml[cw * G + h1] = l_h[1]; }
+      }
+    }
+    } else {
     // Q fragments of this unit (rows >= G read the zero chunk)
     uint32_t qa[D / 16][4];
 #pragma unroll
@@ -798,6 +954,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         if (g1 < G) { mm[cw * G + g1] = m_r[1]; ml[cw * G + g1] = l_r[1]; }
       }
     }
+    }
     named_bar_sync(1, kNT);
     for (int idx = tid; idx < G * D; idx += kNT) {
       const int g = idx / D, dcol = idx % D;
@@ -883,8 +1040,12 @@ cudaError_t launch_decode_d(const CUtensorMap& tm_k, const CUtensorMap& tm_v, co
   if (HPA_DECODE_PERSISTENT) {
     const int smem = PDecodeSmem<D>::bytes(a.G);
     const int grid = std::max(1, std::min(a.n_units, decode_slots(D, a.G)));
-    e = launch_pdl(decode_persistent_kernel<D>, dim3(grid), dim3((kNCons + 2) * 32), smem, s, tm_k, tm_v, tm_k8,
-                   tm_v8, a);
+    if (a.G <= 8 && HPA_DEC_SWAP)
+      e = launch_pdl(decode_persistent_kernel<D, true>, dim3(grid), dim3((kNCons + 2) * 32), smem, s, tm_k, tm_v,
+                     tm_k8, tm_v8, a);
+    else
+      e = launch_pdl(decode_persistent_kernel<D, false>, dim3(grid), dim3((kNCons + 2) * 32), smem, s, tm_k, tm_v,
+                     tm_k8, tm_v8, a);
   } else {
     const int smem = DecodeSmem<D>::kBytes;
     e = launch_pdl(decode_split_kernel<D>, dim3(a.splits, a.Hkv, a.n_seqs), dim3((kNCons + 1) * 32), smem, s,
@@ -924,10 +1085,14 @@ cudaError_t decode_init_attributes() {
                                 cap(DecodeSmem<128>::kBytes))) != cudaSuccess ||
       (e = cudaFuncSetAttribute(decode_split_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 cap(DecodeSmem<64>::kBytes))) != cudaSuccess ||
-      (e = cudaFuncSetAttribute(decode_persistent_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      (e = cudaFuncSetAttribute(decode_persistent_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 cap(PDecodeSmem<128>::bytes(16)))) != cudaSuccess ||
-      (e = cudaFuncSetAttribute(decode_persistent_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                cap(PDecodeSmem<64>::bytes(16)))) != cudaSuccess)
+      (e = cudaFuncSetAttribute(decode_persistent_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cap(PDecodeSmem<64>::bytes(16)))) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(decode_persistent_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cap(PDecodeSmem<128>::bytes(8)))) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(decode_persistent_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cap(PDecodeSmem<64>::bytes(8)))) != cudaSuccess)
     return e;
   return cudaSuccess;
 }
