@@ -143,7 +143,7 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- workload build
 def build_decode_cache(torch, Cache, shape, n_req, docs, tokens, extra_rows, device, seed, placement_seed=99,
-                       token_kv_dtype="bf16"):
+                       token_kv_dtype="bf16", bf16_headroom_pages=0):
     """Creates a cache holding n_req requests of `docs` latent sets (m=128) followed by
     `tokens` token rows (an int, or one count per request for the ragged variant);
     returns (cache, seq ids). Inputs drawn on the GPU (seeded)."""
@@ -157,8 +157,8 @@ def build_decode_cache(torch, Cache, shape, n_req, docs, tokens, extra_rows, dev
     if token_kv_dtype == "fp8":  # NEXT-4c: token pages in their own fp8 pool
         lat_pages = docs * math.ceil(LATENT_ROWS / P)
         cache = Cache(shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim, P,
-                      n_req * lat_pages + 64, n_req, pages_per_seq, device, placement_seed, "fp8",
-                      n_req * (pages_per_seq - lat_pages) + 64)
+                      n_req * lat_pages + 64 + bf16_headroom_pages, n_req, pages_per_seq, device, placement_seed,
+                      "fp8", n_req * (pages_per_seq - lat_pages) + 64)
     else:
         cache = Cache(shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim, P,
                       n_req * pages_per_seq + 64, n_req, pages_per_seq, device, placement_seed)
@@ -492,6 +492,8 @@ def run_ours(args):
                                  world, max_over_ranks, barrier)
         res["next"] = bench_next(torch, Cache, shape, dev, stream, pk, max_over_ranks)
         res["decode_variants"] = bench_decode_variants(torch, Cache, dev, stream, pk, args.page_size)
+        res["next"]["fp8_prefill"] = bench_prefill(torch, Cache, shape, dev, stream, pk, pk_kind, max_over_ranks,
+                                                   token_kv_dtype="fp8", batches=(4,))
     if rank == 0 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(budget_s=15.0)
     if rank == 0:
@@ -510,12 +512,18 @@ def traffic_from_profiles(kernel: str):
         return None
 
 
-def bench_prefill(torch, Cache, shape, dev, stream, pk, pk_kind, max_over_ranks, reps=5):
-    """configs[2]: C = 2048 new rows over 8 latent sets (1024 rows) + 16384 cached token rows."""
+def bench_prefill(torch, Cache, shape, dev, stream, pk, pk_kind, max_over_ranks, reps=5, token_kv_dtype="bf16",
+                  batches=(1, 4)):
+    """configs[2]: C = 2048 new rows over 8 latent sets (1024 rows) + 16384 cached token rows.
+    token_kv_dtype "fp8" (NEXT-4c): the token pages are fp8; each call first dequantizes
+    them into temporary bf16 pages (included in the time)."""
     out = {}
-    for bp in (1, 4):
+    for bp in batches:
         c_rows, prior_tok = 2048, 16384
-        cache, seqs, _ = build_decode_cache(torch, Cache, shape, bp, 8, prior_tok + c_rows, 0, dev, seed=777)
+        tok_pages = bp * (math.ceil((prior_tok + c_rows) / shape.page_size) + 1)  # fp8: temporaries of a call
+        cache, seqs, _ = build_decode_cache(torch, Cache, shape, bp, 8, prior_tok + c_rows, 0, dev, seed=777,
+                                            token_kv_dtype=token_kv_dtype,
+                                            bf16_headroom_pages=tok_pages if token_kv_dtype == "fp8" else 0)
         g = torch.Generator(device=f"cuda:{dev}").manual_seed(99)
         q = torch.randn((bp * c_rows, 32, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
         o = torch.empty_like(q)
@@ -539,7 +547,8 @@ def bench_prefill(torch, Cache, shape, dev, stream, pk, pk_kind, max_over_ranks,
         cache.close()
         del q, o
     out["workload"] = "configs[2] chunked prefill C=2048 over 1024 latent + 16384 cached token rows"
-    out["roofline"] = {"bound": "tensor", "unit": "TFLOP/s", "traffic": traffic_from_profiles("prefill")}
+    if token_kv_dtype == "bf16":
+        out["roofline"] = {"bound": "tensor", "unit": "TFLOP/s", "traffic": traffic_from_profiles("prefill")}
     return out
 
 

@@ -71,7 +71,9 @@ typedef struct {
                                 storage); 1 = token pages fp8 e4m3 with one fp32 scale
                                 per (layer, row, kv-head) for K and for V (reading A20),
                                 held in a separate token pool; latent pages stay bf16. With 1,
-                                decode reads both kinds; prefill returns HPA_ERR_UNSUPPORTED. */
+                                decode reads both kinds; prefill dequantizes the batch's token pages
+                                into temporary bf16 pages of the main pool for the call (needs
+                                free pages; HPA_ERR_OUT_OF_PAGES otherwise). */
   int32_t num_token_pages;   /* token_kv_dtype = 1: pages of the fp8 token pool (> 0) */
 } hpa_config_t;
 

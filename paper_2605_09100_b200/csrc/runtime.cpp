@@ -19,6 +19,7 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 
 #include <algorithm>
 #include <cmath>
@@ -440,7 +441,8 @@ int32_t seq_entries(const Seq& q) { return int32_t(q.pages.size()); }
 // Ships pending word writes (+ optional scatter records/slots) in one upload and
 // one scatter launch on `s`.
 hpa_status_t ship(hpa_cache_t* c, cudaStream_t s, const std::vector<ScatterRecord>& recs,
-                  const std::vector<int32_t>& slots, int64_t max_rows) {
+                  const std::vector<int32_t>& slots, int64_t max_rows, const PoolGeom* geom = nullptr) {
+  const PoolGeom gm = geom ? *geom : c->geom();
   if (c->pending.empty() && recs.empty()) return HPA_OK;
   // The scatter kernel applies words in parallel, so each index may appear at
   // most once: keep the LAST queued write per index (program order).
@@ -469,7 +471,7 @@ hpa_status_t ship(hpa_cache_t* c, cudaStream_t s, const std::vector<ScatterRecor
         m.data[2 * i + 1] = c->pending[i].val;
       }
       if (!slots.empty()) std::memcpy(m.data + 2 * c->pending.size(), slots.data(), slots.size() * 4);
-      return launch_scatter_inline(c->geom(), c->arena, m, max_rows, s);
+      return launch_scatter_inline(gm, c->arena, m, max_rows, s);
     };
     if (n_ints <= size_t(kInlineIntsSmall)) {
       InlineMetaSmall m;
@@ -493,7 +495,7 @@ hpa_status_t ship(hpa_cache_t* c, cudaStream_t s, const std::vector<ScatterRecor
   std::memcpy(c->ring.host(off), b.bytes.data(), b.bytes.size());
   HPA_CUDA(c->ring.upload(off, b.bytes.size(), s));
   char* d = c->ring.dev(off);
-  HPA_CUDA(launch_scatter(c->geom(), c->arena, reinterpret_cast<const WordWrite*>(d + o_words),
+  HPA_CUDA(launch_scatter(gm, c->arena, reinterpret_cast<const WordWrite*>(d + o_words),
                           int32_t(c->pending.size()), reinterpret_cast<const ScatterRecord*>(d + o_recs),
                           int32_t(recs.size()), reinterpret_cast<const int32_t*>(d + o_slots), max_rows, s));
   c->launches += 1;
@@ -1339,10 +1341,6 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
     const Seq& s = c->seqs[seq_ids[i]];
     if (q_lens[i] < 1 || q_lens[i] > s.len)
       return fail(HPA_ERR_INVALID_ARG, "q_lens[%d]=%d must be in [1, seq_len=%d]", i, q_lens[i], s.len);
-    if (c->fp8)
-      for (const Segment& g : s.segs)
-        if (!g.latent && g.rows > 0)
-          return fail(HPA_ERR_UNSUPPORTED, "prefill over fp8 token pages is not implemented (NEXT-4c is decode-side)");
     meta[i] = seq_ids[i];
     meta[n_seqs + i] = q_lens[i];
     meta[2 * n_seqs + i] = int32_t(total_q);
@@ -1361,6 +1359,63 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
   DeviceGuard dg(c->cfg.device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (hpa_status_t st = ship(c, s, {}, {}, 0)) return st;
+  // NEXT-4c: the tcgen05 prefill reads bf16 tiles, so a cache with fp8 token pages first
+  // dequantizes this layer's token pages of the batch into temporary bf16 pages of the main
+  // pool (the pool-to-pool scatter, rows bf16(fp32(code) * scale) as in reading A20) and
+  // points the device table entries at them; after the launch the entries are restored and
+  // the pages returned (stream order: the host mirror never changes). Same-stream semantics.
+  std::vector<int32_t> tmp_pages;
+  std::vector<WordWrite> restore;
+  if (c->fp8) {
+    const int32_t P = c->cfg.page_size;
+    std::vector<char> seen(c->cfg.max_seqs, 0);
+    int32_t need = 0;
+    for (int32_t i = 0; i < n_seqs; ++i) {
+      if (seen[seq_ids[i]]) continue;
+      seen[seq_ids[i]] = 1;
+      for (const Segment& g : c->seqs[seq_ids[i]].segs)
+        if (!g.latent) need += int32_t(g.pages.size());
+    }
+    if (need > c->alloc.num_free())
+      return fail(HPA_ERR_OUT_OF_PAGES, "prefill over fp8 token pages needs %d temporary pages, %d free", need,
+                  c->alloc.num_free());
+    if (need > 0) {
+      c->alloc.alloc(need, tmp_pages);
+      std::vector<int32_t> dst, src;
+      int32_t k = 0;
+      std::fill(seen.begin(), seen.end(), 0);
+      for (int32_t i = 0; i < n_seqs; ++i) {
+        const int32_t sq = seq_ids[i];
+        if (seen[sq]) continue;
+        seen[sq] = 1;
+        const Seq& q = c->seqs[sq];
+        for (size_t e = 0; e < q.pages.size(); ++e) {
+          if (q.meta[e] & kMetaLatent) continue;
+          const int32_t t = tmp_pages[size_t(k++)], valid = q.meta[e] & kMetaRowsMask;
+          for (int32_t r = 0; r < valid; ++r) {
+            dst.push_back(t * P + r);
+            src.push_back(q.pages[e] * P + r);
+          }
+          c->pending.push_back({int32_t(c->idx(sq, int32_t(e))), t});
+          restore.push_back({int32_t(c->idx(sq, int32_t(e))), q.pages[e]});
+        }
+      }
+      const int32_t nrows = int32_t(dst.size());
+      dst.insert(dst.end(), src.begin(), src.end());
+      PoolGeom gl = c->geom();  // this layer only
+      const int64_t bf_off = int64_t(layer) * c->cfg.num_pages * c->cfg.num_kv_heads * P * c->cfg.head_dim;
+      const int64_t f8_rows = int64_t(layer) * c->cfg.num_token_pages * c->cfg.num_kv_heads * P;
+      gl.k_pool = static_cast<__nv_bfloat16_raw*>(c->k_pool) + bf_off;
+      gl.v_pool = static_cast<__nv_bfloat16_raw*>(c->v_pool) + bf_off;
+      gl.k8 = c->k8_pool + f8_rows * c->cfg.head_dim;
+      gl.v8 = c->v8_pool + f8_rows * c->cfg.head_dim;
+      gl.ks = c->ks_pool + f8_rows;
+      gl.vs = c->vs_pool + f8_rows;
+      gl.L = 1;
+      std::vector<ScatterRecord> recs{ScatterRecord{nullptr, nullptr, 0, 0, nrows, 0, 0, 0, 1, nrows, 0, 1}};
+      if (hpa_status_t st = ship(c, s, recs, dst, nrows, &gl)) return st;
+    }
+  }
   const size_t bytes = meta.size() * 4;
   const size_t off = c->ring.reserve(bytes);
   std::memcpy(c->ring.host(off), meta.data(), bytes);
@@ -1380,6 +1435,11 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
   c->launches += launched;
   if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
   HPA_CUDA(c->ring.commit(off, bytes, s));
+  if (!tmp_pages.empty()) {  // NEXT-4c: table entries back to the fp8 pages, temporaries freed
+    c->pending.insert(c->pending.end(), restore.begin(), restore.end());
+    if (hpa_status_t st = ship(c, s, {}, {}, 0)) return st;
+    for (int32_t p : tmp_pages) c->alloc.release(p);
+  }
   return HPA_OK;
 }
 }  // namespace

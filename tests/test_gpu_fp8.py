@@ -5,7 +5,8 @@ and for V). The oracle quantizes the same bf16 inputs with its own quantizer
 (oracle.quantize_rows_e4m3, pinned in test_oracle_pins.py) and attends over the
 dequantized rows in fp64. Checks: the stored codes and scales are bit-exact; decode over
 mixed latent (bf16) + token (fp8) pages is within the north-star tolerance; export and
-compression dequantize exactly as the oracle; prefill is refused (UNSUPPORTED)."""
+compression dequantize exactly as the oracle; prefill dequantizes the batch's token pages
+into temporary bf16 pages and leaves the cache unchanged."""
 import numpy as np
 import pytest
 import torch
@@ -88,10 +89,45 @@ def test_fp8_latent_only_and_token_only_sequences_and_errors():
     out = pr.cache.decode(0, [a, b], q.cuda())
     ref = np.stack([attend(f64(q[i:i + 1]), *pr.orc.logical_kv(s, 0), shape.scale)[0] for i, s in enumerate([a, b])])
     check_close(out, ref, "fp8 latent-only / token-only")
-    with pytest.raises(HPAError):                         # prefill over fp8 token pages: UNSUPPORTED
-        pr.cache.prefill(0, [b], [16], pr.queries(16).cuda())
-    out2 = pr.cache.prefill(0, [a], [10], pr.queries(10).cuda())   # latent-only rows still prefill
+    with pytest.raises(HPAError):
+        pr.cache.prefill(0, [b], [251], pr.queries(251).cuda())   # q_len > seq_len
+    out2 = pr.cache.prefill(0, [a], [10], pr.queries(10).cuda())   # latent-only rows
     assert torch.isfinite(out2.float()).all()
+
+
+@pytest.mark.parametrize("hq,hkv,d,P", [(32, 8, 128, 16), (8, 1, 128, 64), (16, 2, 64, 32)])
+def test_fp8_prefill_parity_and_cache_unchanged(hq, hkv, d, P):
+    """Prefill over fp8 token pages (dequantized into temporary bf16 pages for the call):
+    parity with the oracle over the dequantized rows; afterwards the table, the token pool,
+    the free-page counts and decode are unchanged."""
+    shape = _shape(hq, hkv, d, P, L=2)
+    pr = _fp8_pair(shape, pages=1024, tpages=1024, seqs=4, per_seq=200)
+    seqs = [pr.build([("latent", 128), ("tokens", 500)]), pr.build([("tokens", 300), ("latent", 64), ("tokens", 77)])]
+    qd = pr.queries(1)
+    before = pr.cache.decode(1, [seqs[0]], qd.cuda()).clone()
+    tables = [pr.cache.export_table(s) for s in seqs]
+    free0, tfree0 = pr.cache.stats()[0], pr.cache.token_pool()[4]
+    k8a = pr.cache.token_pool()[0].clone()
+    q_lens = [200, 77]
+    q = pr.queries(sum(q_lens))
+    for layer in (0, 1):
+        out = pr.cache.prefill(layer, seqs, q_lens, q.cuda())
+        torch.cuda.synchronize()
+        off = 0
+        for s, n in zip(seqs, q_lens):
+            k, v = pr.orc.logical_kv(s, layer)
+            lb = k.shape[1]
+            ref = np.stack([attend(f64(q[off + t:off + t + 1]), k[:, :lb - n + t + 1], v[:, :lb - n + t + 1],
+                                   shape.scale)[0] for t in range(n)])
+            check_close(out[off:off + n], ref, f"fp8 prefill layer {layer} seq {s}")
+            off += n
+    assert pr.cache.stats()[0] == free0 and pr.cache.token_pool()[4] == tfree0
+    for s, t in zip(seqs, tables):
+        t2 = pr.cache.export_table(s)
+        assert all(np.array_equal(x, y) for x, y in zip(t, t2))
+    assert torch.equal(pr.cache.token_pool()[0], k8a)
+    after = pr.cache.decode(1, [seqs[0]], qd.cuda())
+    assert torch.equal(before, after)
 
 
 def test_fp8_export_and_compress_dequantize_like_the_oracle():
