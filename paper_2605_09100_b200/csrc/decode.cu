@@ -38,6 +38,12 @@ constexpr int kNCons = 4;   // consumer warps per CTA
 #ifndef HPA_DEC_EVICT_FIRST
 #define HPA_DEC_EVICT_FIRST 1  // L2 evict-first hint on the streamed K/V tiles (+4 %)
 #endif
+#ifndef HPA_DEC_DEBUG_RING
+#define HPA_DEC_DEBUG_RING 0  // debug builds: stage tags checked by the consumers (printf + trap)
+#endif
+#ifndef HPA_DEC_ALLOW_ANY_DEPTH
+#define HPA_DEC_ALLOW_ANY_DEPTH 0
+#endif
 #ifndef HPA_DEC_STAGES
 #define HPA_DEC_STAGES 12
 #endif
@@ -60,10 +66,13 @@ constexpr int kNCons = 4;   // consumer warps per CTA
 #define HPA_DEC_PF 8
 #endif
 constexpr int kNSt = HPA_DEC_STAGES;  // ring depth
-// Depths with gcd(kNSt, kNCons) < kNCons (slots alternating between two consumers, e.g. 6 or 10)
-// faulted in the configs[1] bench although small parity cases passed; cause not yet found, so
-// only depths where every slot belongs to one consumer are allowed (8, 12, 16, 24 verified).
-static_assert(HPA_DEC_STAGES % 4 == 0, "decode ring depth must be a multiple of the consumer count");
+// Ring depth must be a multiple of the consumer count, so that every slot is consumed by one
+// consumer, which then waits the slot's mbarrier phases in order. Otherwise (e.g. 10 stages,
+// 4 consumers) consumer 3 takes items 3 and 23 of slot 3 while consumer 1 takes item 13; TMA
+// completions land out of order, so consumer 3 can wait for item 23 (phase 2) while phase 1
+// is still open, and try_wait.parity(phase 2) matches the completed phase 0 (same parity):
+// an ABA that reads a stale stage (found with HPA_DEC_DEBUG_RING stage tags).
+static_assert(HPA_DEC_STAGES % 4 == 0 || HPA_DEC_ALLOW_ANY_DEPTH, "decode ring depth must be a multiple of the consumer count");
 #ifndef HPA_FENCE_MODE
 #define HPA_FENCE_MODE 2  // 0: fence.sc (threadfence), 1: fence.acq_rel, 2: atom.acq_rel
 #endif
@@ -487,6 +496,9 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
   int4* qmeta = reinterpret_cast<int4*>(smem + L::oQMeta);
   int2* walk = reinterpret_cast<int2*>(smem + L::oWalk);
   float* scl = reinterpret_cast<float*>(smem + L::oScl);
+#if HPA_DEC_DEBUG_RING
+  __shared__ volatile uint32_t dbg_tag[kNSt];
+#endif
   float* mo = reinterpret_cast<float*>(smem + L::oMerge(G));  // [NCONS][G][D]
   float* mm = mo + kNCons * G * D;                          // [NCONS][G]
   float* ml = mm + kNCons * G;
@@ -615,6 +627,9 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
             const int slot = i % kNSt;
             if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
             cmeta[slot] = min(kChunk, valid - sub * kChunk) | (f8 << 16);
+#if HPA_DEC_DEBUG_RING
+            dbg_tag[slot] = i;
+#endif
             uint8_t* kd = stages + slot * L::kStageBytes;
             uint8_t* vd = kd + L::kTileBytes;
             if (f8) {
@@ -652,6 +667,9 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
             const int slot = i % kNSt;
             if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
             cmeta[slot] = 0;
+#if HPA_DEC_DEBUG_RING
+            dbg_tag[slot] = i;
+#endif
             mbar_arrive(&full[slot]);
           }
           ++ul;
@@ -698,6 +716,14 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     for (;; i += kNCons) {
       const int slot = i % kNSt;
       mbar_wait(&full[slot], (i / kNSt) & 1);
+#if HPA_DEC_DEBUG_RING
+      if (dbg_tag[slot] != i) {
+        if (lane == 0)
+          printf("hpa decode ring: block %d consumer %d slot %d expected item %u, stage holds %u\n", blockIdx.x, cw,
+                 slot, i, dbg_tag[slot]);
+        __trap();
+      }
+#endif
       int nvalid = cmeta[slot];
       if (nvalid <= 0) {  // sentinel: release the slot and finish the unit
         __syncwarp();
@@ -822,6 +848,14 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     for (;; i += kNCons) {
       const int slot = i % kNSt;
       mbar_wait(&full[slot], (i / kNSt) & 1);
+#if HPA_DEC_DEBUG_RING
+      if (dbg_tag[slot] != i) {
+        if (lane == 0)
+          printf("hpa decode ring: block %d consumer %d slot %d expected item %u, stage holds %u\n", blockIdx.x, cw,
+                 slot, i, dbg_tag[slot]);
+        __trap();
+      }
+#endif
       int nvalid = cmeta[slot];
       if (nvalid <= 0) {  // sentinel: release the slot and finish the unit
         __syncwarp();
