@@ -94,6 +94,9 @@ constexpr int kSpanBit = 1 << 30;          // tags span columns in the mask indi
 #ifndef HPA_OPT_EXP  // softmax: first-half exps against the running max with the tile max reduced
 #define HPA_OPT_EXP (!HPA_EXP_INPLACE)  // alongside (needs the raw scores, so not with in-place exps)
 #endif
+#ifndef HPA_SPLIT_LD
+#define HPA_SPLIT_LD 0  // 1: S loaded in two halves, P half 0 stored before the max check (measured 1 % slower)
+#endif
 #ifndef HPA_PV_SPLIT
 #define HPA_PV_SPLIT 1    // publish P in two 64-key halves (PV starts on the first half)
 #endif
@@ -686,26 +689,34 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       mbar_wait(&s_full[s], j & 1);
       if (row == 0) TRACE(7 + s, j);
       tc_fence_after();
+      constexpr int kLd0 = HPA_SPLIT_LD ? kBN / 2 : kBN;  // columns loaded before the first wait
 #pragma unroll
-      for (int c = 0; c < kBN / 32; ++c) tc_ld32(tS + c * 32, x + c * 32);
+      for (int c = 0; c < kLd0 / 32; ++c) tc_ld32(tS + c * 32, x + c * 32);
       mbar_wait(&c_full[cs], (j / kNC) & 1);
       const int32_t* col = sC + cs * (kBN + 4);
       const bool all_vis = col[kBN] != 0;
-      tc_wait_ld();
-      if (row == 0) TRACE(9 + s, j);
-      if (!all_vis) {
-        const int cmask = my_i >= span_from ? -1 : ~kSpanBit;  // span tag visible only to span rows
+      const int cmask = my_i >= span_from ? -1 : ~kSpanBit;  // span tag visible only to span rows
+      auto mask_cols = [&](int c0, int c1) {
 #pragma unroll
-        for (int c = 0; c < kBN; c += 4) {
+        for (int c = c0; c < c1; c += 4) {
           const int4 ci = *reinterpret_cast<const int4*>(col + c);
           x[c + 0] = (ci.x & cmask) <= my_i ? x[c + 0] : -CUDART_INF_F;
           x[c + 1] = (ci.y & cmask) <= my_i ? x[c + 1] : -CUDART_INF_F;
           x[c + 2] = (ci.z & cmask) <= my_i ? x[c + 2] : -CUDART_INF_F;
           x[c + 3] = (ci.w & cmask) <= my_i ? x[c + 3] : -CUDART_INF_F;
         }
+      };
+      tc_wait_ld();
+      if (HPA_SPLIT_LD) {  // second half in flight while the first is masked (and exp'd, below)
+#pragma unroll
+        for (int c = kLd0 / 32; c < kBN / 32; ++c) tc_ld32(tS + c * 32, x + c * 32);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&c_empty[cs]);  // col[] consumed (masking done)
+      if (row == 0) TRACE(9 + s, j);
+      if (!all_vis) mask_cols(0, kLd0);
+      if (!HPA_SPLIT_LD) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&c_empty[cs]);  // col[] consumed (masking done)
+      }
       // p = 2^(x*sl2 - m): f32x2 FFMA for the argument, MUFU ex2 (optionally 1 pair in
       // HPA_POLY_EVERY on the FMA pipe); 4 independent partial row sums
       const float2 sl2x2 = make_float2(sl2, sl2);
@@ -750,7 +761,20 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       // redoes half 0 on the exact path below.
       uint32_t pk0[kBN / 4];
       const bool opt = HPA_OPT_EXP && __all_sync(0xffffffffu, m_run != -CUDART_INF_F);
-      if (opt) exps_half(0, m_run, pk0);
+      bool p0_stored = false;  // P half 0 already in TMEM (not yet published)
+      if (opt) {
+        exps_half(0, m_run, pk0);
+        if (HPA_SPLIT_LD) {  // async store overlapping the second half's load and the max
+          tc_st32(tS, pk0);
+          p0_stored = true;
+        }
+      }
+      if (HPA_SPLIT_LD) {
+        tc_wait_ld();
+        if (!all_vis) mask_cols(kLd0, kBN);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&c_empty[cs]);  // col[] consumed (masking done)
+      }
       if (row == 0) TRACE(31 + s, j);
       // row max as a tree (8 independent partial maxima), not a 64-deep chain
       float pm[8];
@@ -789,10 +813,12 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #pragma unroll
         for (int k = 0; k < 4; ++k) rs4[k] = make_float2(0.f, 0.f);
         exps_half(0, m_use, pk0);
+        if (p0_stored) tc_wait_st();  // the optimistic store lands before it is overwritten
+        p0_stored = false;
       }
       // P (bf16 pairs) over S: keys [64 half, 64 half + 64) -> columns [128 s + 32 half, +32)
       if (row == 0) TRACE(35 + s, j);
-      tc_st32(tS, pk0);
+      if (!p0_stored) tc_st32(tS, pk0);
       if (HPA_PV_SPLIT) {
         tc_wait_st();
         tc_fence_before();
