@@ -98,14 +98,14 @@ hpa_status_t hpa_cache_destroy(hpa_cache_t* c);
 hpa_status_t hpa_cache_pools(hpa_cache_t* c, void** k_pool, void** v_pool, uint64_t* pool_bytes);
 
 /* Allocator state: free pages, pages referenced by at least one table, live sequences. */
-/* NEXT-4c fp8 token pool (token_kv_dtype = 1): device pointers to the e4m3 codes
- * K8, V8 uint8 [L][num_token_pages][H_kv][P][d] and the fp32 scales KS, VS
- * [L][num_token_pages][H_kv][P] (row r of a page means code * scale, reading A20), and the
- * free token pages. The cache owns them; read-only for callers (tests compare them
- * bit-exactly with the oracle's quantizer). HPA_ERR_INVALID_ARG if the cache stores bf16
- * token pages. */
-hpa_status_t hpa_cache_token_pool(hpa_cache_t* c, void** k8, void** v8, void** ks, void** vs,
-                                  int32_t* free_token_pages);
+/* NEXT-4c fp8 token pool (token_kv_dtype = 1): device pointers to the K and V token pools
+ * and the free token pages. Layout (reading A20): pool row prow = ((layer * num_token_pages +
+ * page) * H_kv + h) * P + r; rows are grouped 16 at a time into contiguous blocks of
+ * [16 x d e4m3 codes | 16 fp32 scales] (16 d + 64 bytes), block index prow / 16; row r of
+ * a block means code * scale. The cache owns the pools; read-only for callers (tests
+ * compare them bit-exactly with the oracle's quantizer). HPA_ERR_INVALID_ARG if the cache
+ * stores bf16 token pages. */
+hpa_status_t hpa_cache_token_pool(hpa_cache_t* c, void** k8, void** v8, int32_t* free_token_pages);
 
 hpa_status_t hpa_cache_stats(hpa_cache_t* c, int32_t* free_pages, int32_t* used_pages,
                              int32_t* live_seqs);

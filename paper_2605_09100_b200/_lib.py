@@ -40,8 +40,7 @@ SIGNATURES = {
     "hpa_cache_pools": (c_st, [c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
                                ctypes.POINTER(ctypes.c_uint64)]),
     "hpa_cache_stats": (c_st, [c_vp, c_i32p, c_i32p, c_i32p]),
-    "hpa_cache_token_pool": (c_st, [c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
-                                    ctypes.POINTER(c_vp), c_i32p]),
+    "hpa_cache_token_pool": (c_st, [c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_i32p]),
     "hpa_seq_create": (c_st, [c_vp, c_i32p]),
     "hpa_seq_release": (c_st, [c_vp, c_i32]),
     "hpa_append_kv": (c_st, [c_vp, c_i32, c_i32p, c_i32p, c_vp, c_vp, c_vp]),

@@ -298,16 +298,22 @@ class Cache:
         return k, v
 
     def token_pool(self):
-        """NEXT-4c fp8 token pool views: (k codes, v codes) uint8 [L][NPt][H_kv][P][d],
-        (k scales, v scales) fp32 [L][NPt][H_kv][P], free token pages."""
-        k8, v8, ks, vs, free = c_vp(), c_vp(), c_vp(), c_vp(), c_i32()
-        check(LIB.hpa_cache_token_pool(self._h, ctypes.byref(k8), ctypes.byref(v8), ctypes.byref(ks),
-                                       ctypes.byref(vs), ctypes.byref(free)))
+        """NEXT-4c fp8 token pool views (include/hpa.h hpa_cache_token_pool): (k codes, v codes)
+        uint8 [L][NPt][H_kv][P][d], (k scales, v scales) fp32 [L][NPt][H_kv][P], free token pages.
+        Codes and scales are strided views of the 16-row [codes | scales] blocks."""
+        k8, v8, free = c_vp(), c_vp(), c_i32()
+        check(LIB.hpa_cache_token_pool(self._h, ctypes.byref(k8), ctypes.byref(v8), ctypes.byref(free)))
         dev = torch.device(f"cuda:{self.device}")
-        shp = (self.L, self.num_token_pages, self.Hkv, self.P)
-        codes = lambda p: torch.as_tensor(_CAI(p, shp + (self.d,), "|u1"), device=dev)
-        scales = lambda p: torch.as_tensor(_CAI(p, shp, "<f4"), device=dev)
-        return codes(k8.value), codes(v8.value), scales(ks.value), scales(vs.value), free.value
+        nblk = self.L * self.num_token_pages * self.Hkv * self.P // 16
+        blk = 16 * self.d + 64
+        views = []
+        for ptr in (k8.value, v8.value):
+            raw = torch.as_tensor(_CAI(ptr, (nblk, blk), "|u1"), device=dev)
+            codes = raw[:, :16 * self.d].reshape(self.L, self.num_token_pages, self.Hkv, self.P, self.d)
+            scales = raw[:, 16 * self.d:].contiguous().view(torch.float32).reshape(
+                self.L, self.num_token_pages, self.Hkv, self.P)
+            views.append((codes, scales))
+        return views[0][0], views[1][0], views[0][1], views[1][1], free.value
 
     def set_decode_splits(self, splits: int) -> None:
         check(LIB.hpa_set_decode_splits(self._h, splits))

@@ -74,11 +74,11 @@ __device__ __forceinline__ void quant_rows(const PoolGeom& g, const ScatterRecor
       kx[i] = __fmul_rn(kx[i], kinv);
       vx[i] = __fmul_rn(vx[i], vinv);
     }
-    *reinterpret_cast<uint2*>(g.k8 + prow * D + c * 8) = e4m3x8_from_f32(kx);
-    *reinterpret_cast<uint2*>(g.v8 + prow * D + c * 8) = e4m3x8_from_f32(vx);
+    *reinterpret_cast<uint2*>(fp8_code_ptr(g.k8, prow, D) + c * 8) = e4m3x8_from_f32(kx);
+    *reinterpret_cast<uint2*>(fp8_code_ptr(g.v8, prow, D) + c * 8) = e4m3x8_from_f32(vx);
     if (c == 0) {
-      g.ks[prow] = ka > 0.f ? __fdiv_rn(ka, 448.f) : 1.f;
-      g.vs[prow] = va > 0.f ? __fdiv_rn(va, 448.f) : 1.f;
+      *fp8_scale_ptr(g.k8, prow, D) = ka > 0.f ? __fdiv_rn(ka, 448.f) : 1.f;
+      *fp8_scale_ptr(g.v8, prow, D) = va > 0.f ? __fdiv_rn(va, 448.f) : 1.f;
     }
   }
 }
@@ -122,8 +122,10 @@ __device__ __forceinline__ void copy_rows(const PoolGeom& g, const ScatterRecord
         if (r.src_from_pool && r.src_fp8) {  // move out of the fp8 token pool: dequantize
           const int32_t ss = idx[r.src_off + row];
           const int64_t prow = ((int64_t(l) * g.NPt + (ss >> g.log2P)) * g.Hkv + h) * g.P + (ss & (g.P - 1));
-          kv[u] = bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(g.k8 + prow * D + c * 8), g.ks[prow]);
-          vv[u] = bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(g.v8 + prow * D + c * 8), g.vs[prow]);
+          kv[u] = bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(fp8_code_ptr(g.k8, prow, D) + c * 8),
+                                   *fp8_scale_ptr(g.k8, prow, D));
+          vv[u] = bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(fp8_code_ptr(g.v8, prow, D) + c * 8),
+                                   *fp8_scale_ptr(g.v8, prow, D));
         } else if (r.src_from_pool) {  // in-cache move: source is another pool slot
           const int32_t ss = idx[r.src_off + row];
           const int64_t src = ((int64_t(l) * g.NP + (ss >> g.log2P)) * g.Hkv + h) * page_elems +
@@ -198,9 +200,11 @@ __global__ void __launch_bounds__(128) export_kernel(PoolGeom g, DevTables t, in
       const int64_t prow = row0 + i / vec_per_row;
       const int64_t off = int64_t(i % vec_per_row) * 8;
       reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(k_out) + dst0)[i] =
-          bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(g.k8 + prow * g.D + off), g.ks[prow]);
+          bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(fp8_code_ptr(g.k8, prow, g.D) + off),
+                           *fp8_scale_ptr(g.k8, prow, g.D));
       reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(v_out) + dst0)[i] =
-          bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(g.v8 + prow * g.D + off), g.vs[prow]);
+          bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(fp8_code_ptr(g.v8, prow, g.D) + off),
+                           *fp8_scale_ptr(g.v8, prow, g.D));
     }
     return;
   }

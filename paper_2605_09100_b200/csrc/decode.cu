@@ -59,9 +59,6 @@ constexpr int kNCons = 4;   // consumer warps per CTA
 #ifndef HPA_DEC_LAZY
 #define HPA_DEC_LAZY 1  // decode consumers: lazy running-max rescale (threshold 2^8)
 #endif
-#ifndef HPA_FP8_DIAG
-#define HPA_FP8_DIAG 0  // timing diagnostics only (wrong numerics): 1 skip scale loads, 2 skip conversion
-#endif
 #ifndef HPA_DEC_PF
 #define HPA_DEC_PF 8
 #endif
@@ -460,8 +457,12 @@ struct PDecodeSmem {
   static constexpr int oMeta = oBar + (2 * kNSt + 4 + 2 * kWB) * 8;
   static constexpr int oQMeta = (oMeta + kNSt * 4 + 15) & ~15;  // 2 x int4 {b, h, split, -}: unit of Q buffer
   static constexpr int oWalk = oQMeta + 32;                      // [WB][32] int2 pieces
-  static constexpr int oScl = oWalk + kWB * 32 * 8;              // [NST][32] fp32: K, V scales of fp8 chunks
-  static constexpr int oZero = oScl + kNSt * 32 * 4;             // 16 zero bytes: A-operand rows >= G
+  static constexpr int oZero = oWalk + kWB * 32 * 8;             // 16 zero bytes: A-operand rows >= G
+  // fp8 chunk (NEXT-4c): the K and V blocks [16 x D codes | 16 scales] sit at the top of the
+  // stage; the consumer reads the scales, then converts K to [0, kTile), V to [kTile, 2 kTile)
+  static constexpr int kBlk8 = 16 * D + 64;
+  static constexpr int oK8 = kStageBytes - 2 * kBlk8;
+  static constexpr int oV8 = kStageBytes - kBlk8;
   static constexpr int oQ = oZero + 16;                          // 2 x [G][D] q rows (unswizzled)
   static __host__ __device__ int qbuf(int G) { return G * D * 2; }
   static __host__ __device__ int oMerge(int G) { return oQ + 2 * qbuf(G); }
@@ -472,7 +473,6 @@ struct PDecodeSmem {
 template <int D, bool SW>
 __global__ void __launch_bounds__((kNCons + 2) * 32, HPA_DECODE_CTAS_PER_SM)
 decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                         const __grid_constant__ CUtensorMap tm_k8, const __grid_constant__ CUtensorMap tm_v8,
                          const DecodeArgs a) {
   using L = PDecodeSmem<D>;
   extern __shared__ __align__(1024) uint8_t smem_pd[];
@@ -495,7 +495,6 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
   volatile int32_t* cmeta = reinterpret_cast<int32_t*>(smem + L::oMeta);
   int4* qmeta = reinterpret_cast<int4*>(smem + L::oQMeta);
   int2* walk = reinterpret_cast<int2*>(smem + L::oWalk);
-  float* scl = reinterpret_cast<float*>(smem + L::oScl);
 #if HPA_DEC_DEBUG_RING
   __shared__ volatile uint32_t dbg_tag[kNSt];
 #endif
@@ -633,15 +632,12 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
             uint8_t* kd = stages + slot * L::kStageBytes;
             uint8_t* vd = kd + L::kTileBytes;
             if (f8) {
-              // fp8 chunk (NEXT-4c): codes into the stage's upper half, per-row scales aside;
-              // the consumer converts them to the bf16 layout in place
-              mbar_arrive_expect_tx(&full[slot], uint32_t(2 * kChunk * D + (HPA_FP8_DIAG == 1 ? 0 : 2 * kChunk * 4)));
-              tma_load_2d(kd + L::kTileBytes, &tm_k8, &full[slot], 0, rowbase + sub * kChunk);
-              tma_load_2d(kd + L::kTileBytes + kChunk * D, &tm_v8, &full[slot], 0, rowbase + sub * kChunk);
-              if (HPA_FP8_DIAG != 1) {
-                bulk_g2s(scl + slot * 32, a.ks + rowbase + sub * kChunk, kChunk * 4, &full[slot]);
-                bulk_g2s(scl + slot * 32 + 16, a.vs + rowbase + sub * kChunk, kChunk * 4, &full[slot]);
-              }
+              // fp8 chunk (NEXT-4c): one bulk copy per K / V block (codes + row scales) into the
+              // top of the stage; the consumer converts them to the bf16 layout in place
+              const int64_t blk = (int64_t(rowbase) + sub * kChunk) >> 4;
+              mbar_arrive_expect_tx(&full[slot], uint32_t(2 * L::kBlk8));
+              bulk_g2s(kd + L::oK8, a.k8 + blk * L::kBlk8, L::kBlk8, &full[slot]);
+              bulk_g2s(kd + L::oV8, a.v8 + blk * L::kBlk8, L::kBlk8, &full[slot]);
               continue;
             }
             mbar_arrive_expect_tx(&full[slot], L::kStageBytes);
@@ -737,14 +733,16 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       uint8_t* vt = kt + L::kTileBytes;
       float kmul0 = sl2, kmul1 = sl2, vmul0 = 1.f, vmul1 = 1.f;  // keys g and g + 8
       if (c8) {
-        fp8_tile_to_bf16<D>(kt + L::kTileBytes, kt, lane);
-        fp8_tile_to_bf16<D>(kt + L::kTileBytes + kChunk * D, vt, lane);
+        const float* ksc = reinterpret_cast<const float*>(kt + L::oK8 + 16 * D);
+        const float* vsc = reinterpret_cast<const float*>(kt + L::oV8 + 16 * D);
+        kmul0 = ksc[gq] * sl2;  // scales first: the conversion overwrites them
+        kmul1 = ksc[gq + 8] * sl2;
+        vmul0 = vsc[gq];
+        vmul1 = vsc[gq + 8];
         __syncwarp();
-        const float* sc = scl + slot * 32;
-        kmul0 = sc[gq] * sl2;
-        kmul1 = sc[gq + 8] * sl2;
-        vmul0 = sc[16 + gq];
-        vmul1 = sc[16 + gq + 8];
+        fp8_tile_to_bf16<D>(kt + L::oK8, kt, lane);
+        fp8_tile_to_bf16<D>(kt + L::oV8, vt, lane);
+        __syncwarp();
       }
       float sacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -870,18 +868,18 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       // per owned key column (2t, 2t+1, 8+2t, 9+2t): K scale (x softmax scale) and V scale
       float kmul[4] = {sl2, sl2, sl2, sl2}, vmul[4] = {1.f, 1.f, 1.f, 1.f};
       if (c8) {
-        if (HPA_FP8_DIAG != 2) {
-          fp8_tile_to_bf16<D>(kt + L::kTileBytes, kt, lane);
-          fp8_tile_to_bf16<D>(kt + L::kTileBytes + kChunk * D, vt, lane);
+        const float* ksc = reinterpret_cast<const float*>(kt + L::oK8 + 16 * D);
+        const float* vsc = reinterpret_cast<const float*>(kt + L::oV8 + 16 * D);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // scales first: the conversion overwrites them
+          const int col = (q >> 1) * 8 + 2 * (lane & 3) + (q & 1);
+          kmul[q] = ksc[col] * sl2;
+          vmul[q] = vsc[col];
         }
         __syncwarp();
-        const float* sc = scl + slot * 32;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int col = (q >> 1) * 8 + 2 * (lane & 3) + (q & 1);
-          kmul[q] = sc[col] * sl2;
-          vmul[q] = sc[16 + col];
-        }
+        fp8_tile_to_bf16<D>(kt + L::oK8, kt, lane);
+        fp8_tile_to_bf16<D>(kt + L::oV8, vt, lane);
+        __syncwarp();
       }
       float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
@@ -1067,8 +1065,7 @@ __global__ void __launch_bounds__(D) merge_kernel(const float* __restrict__ o_pa
 }
 
 template <int D>
-cudaError_t launch_decode_d(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const CUtensorMap& tm_k8,
-                            const CUtensorMap& tm_v8, const DecodeArgs& a,
+cudaError_t launch_decode_d(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,
                             cudaStream_t s, int* launches) {
   cudaError_t e;
   if (HPA_DECODE_PERSISTENT) {
@@ -1076,10 +1073,10 @@ cudaError_t launch_decode_d(const CUtensorMap& tm_k, const CUtensorMap& tm_v, co
     const int grid = std::max(1, std::min(a.n_units, decode_slots(D, a.G)));
     if (a.G <= 8 && HPA_DEC_SWAP)
       e = launch_pdl(decode_persistent_kernel<D, true>, dim3(grid), dim3((kNCons + 2) * 32), smem, s, tm_k, tm_v,
-                     tm_k8, tm_v8, a);
+                     a);
     else
       e = launch_pdl(decode_persistent_kernel<D, false>, dim3(grid), dim3((kNCons + 2) * 32), smem, s, tm_k, tm_v,
-                     tm_k8, tm_v8, a);
+                     a);
   } else {
     const int smem = DecodeSmem<D>::kBytes;
     e = launch_pdl(decode_split_kernel<D>, dim3(a.splits, a.Hkv, a.n_seqs), dim3((kNCons + 1) * 32), smem, s,
@@ -1151,12 +1148,11 @@ int decode_ctas_per_sm(int32_t D, int32_t /*G*/) {
   return by_smem < 3 ? by_smem : 3;
 }
 
-cudaError_t launch_decode(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const CUtensorMap& tm_k8,
-                          const CUtensorMap& tm_v8, const DecodeArgs& a,
+cudaError_t launch_decode(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,
                           int32_t D, cudaStream_t s, int* launches) {
   if (a.n_seqs == 0) return cudaSuccess;
-  if (D == 128) return launch_decode_d<128>(tm_k, tm_v, tm_k8, tm_v8, a, s, launches);
-  if (D == 64) return launch_decode_d<64>(tm_k, tm_v, tm_k8, tm_v8, a, s, launches);
+  if (D == 128) return launch_decode_d<128>(tm_k, tm_v, a, s, launches);
+  if (D == 64) return launch_decode_d<64>(tm_k, tm_v, a, s, launches);
   return cudaErrorInvalidValue;
 }
 

@@ -57,12 +57,10 @@ struct PoolGeom {
   void* k_pool;  // bf16 [L][NP][H_kv][P][d]
   void* v_pool;
   int32_t L, NP, Hkv, P, D, log2P;
-  // NEXT-4c fp8 token pool (nullptr when the cache stores bf16 token pages): e4m3 codes
-  // [L][NPt][H_kv][P][d] and fp32 scales [L][NPt][H_kv][P] for K and V (reading A20)
+  // NEXT-4c fp8 token pools (nullptr when the cache stores bf16 token pages), K and V:
+  // blocks of [16 x d e4m3 codes | 16 fp32 row scales] (reading A20; fp8_code_ptr / fp8_scale_ptr)
   uint8_t* k8;
   uint8_t* v8;
-  float* ks;
-  float* vs;
   int32_t NPt;
 };
 
@@ -109,10 +107,10 @@ struct DecodeArgs {
   int32_t n_seqs, Hq, Hkv, G, P, NP, layer, splits;  // splits = S_max (partials stride)
   float scale_log2;         // softmax_scale * log2(e)
   // persistent kernel work list (host-planned, longest unit first):
-  // NEXT-4c: token entries read the fp8 pool ([L][NPt][H_kv][P][d] codes + per-row scales)
+  // NEXT-4c: token entries read the fp8 pools (16-row blocks of codes + row scales)
   int32_t fp8, NPt;
-  const float* ks;
-  const float* vs;
+  const uint8_t* k8;
+  const uint8_t* v8;
   const int4* units;        // [n_units] {request b, seq id, h | split << 8 | S_b << 16, 0}
   const int32_t* nsplit;    // [n] per-request split count S_b (combine); nullptr = uniform `splits`
   int32_t* sched;           // [2] unit ticket / finished-CTA counters, zero between calls
@@ -123,8 +121,7 @@ cudaError_t launch_merge(int32_t n_parts, int32_t n_rows, int32_t D, const float
                          const float* lse_parts, void* out, cudaStream_t s);
 // tm_k / tm_v: 2-D tensor maps over the pools viewed as [L*NP*H_kv*P][d],
 // box {64, 16}, 128-B swizzle.
-cudaError_t launch_decode(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const CUtensorMap& tm_k8,
-                          const CUtensorMap& tm_v8, const DecodeArgs& a,
+cudaError_t launch_decode(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,
                           int32_t D, cudaStream_t s, int* launches);
 int decode_ctas_per_sm(int32_t D, int32_t G);
 // Persistent decode kernel compiled in (HPA_DECODE_PERSISTENT) and its resident CTA count.

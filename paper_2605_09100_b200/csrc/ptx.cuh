@@ -146,6 +146,16 @@ __device__ __forceinline__ int4 bf16x8_from_e4m3(uint2 c, float scale) {
   return make_int4(int(out[0]), int(out[1]), int(out[2]), int(out[3]));
 }
 
+// NEXT-4c fp8 token pool layout: per 16-row group of a (layer, page, head) tile one
+// contiguous block [16 x D e4m3 codes | 16 fp32 row scales] (16 D + 64 bytes), so a decode
+// chunk is one bulk copy. Pool row prow = ((l * NPt + page) * H_kv + h) * P + r -> block prow/16.
+__host__ __device__ __forceinline__ int64_t fp8_block_bytes(int D) { return 16 * int64_t(D) + 64; }
+__host__ __device__ __forceinline__ uint8_t* fp8_code_ptr(uint8_t* base, int64_t prow, int D) {
+  return base + (prow >> 4) * fp8_block_bytes(D) + (prow & 15) * int64_t(D);
+}
+__host__ __device__ __forceinline__ float* fp8_scale_ptr(uint8_t* base, int64_t prow, int D) {
+  return reinterpret_cast<float*>(base + (prow >> 4) * fp8_block_bytes(D) + 16 * int64_t(D) + 4 * (prow & 15));
+}
 // Same packing on the integer ALU pipe (F2FP issues on the XU pipe that MUFU.EX2 also uses):
 // round to nearest with ties away from zero (add half an ulp of bf16, keep the upper halves).
 // Differs from RNE only on exact ties. For finite non-negative inputs (softmax P).

@@ -134,20 +134,6 @@ bool make_map_dec(CUtensorMap* m, void* base, uint64_t rows, uint64_t cols) {
             CU_TENSOR_MAP_SWIZZLE_128B, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// fp8 token pool map [rows][d] bytes: box {d, 16}, no swizzle (the decode consumers convert
-// the 16 x d tile to the bf16 swizzled layout in shared memory).
-bool make_map_u8(CUtensorMap* m, void* base, uint64_t rows, uint64_t cols) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols};
-  cuuint32_t box[2] = {cuuint32_t(cols), 16};
-  cuuint32_t estr[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-         CUDA_SUCCESS;
-}
-
 // 3-D bf16 map over q [tokens][Hq][d]: box {64, 1, box_tok}, 128-B swizzle.
 bool make_map_q(CUtensorMap* m, const void* base, uint64_t tokens, uint64_t heads, uint64_t d,
                 uint32_t box_tok) {
@@ -323,11 +309,8 @@ struct hpa_cache {
   // NEXT-4c fp8 token pool (token_kv_dtype = 1): codes + per-row scales, its own allocator
   bool fp8 = false;
   PageAllocator alloc8;
-  uint8_t* k8_pool = nullptr;
+  uint8_t* k8_pool = nullptr;  // 16-row blocks [16 x d codes | 16 fp32 scales] (fp8_code_ptr)
   uint8_t* v8_pool = nullptr;
-  float* ks_pool = nullptr;
-  float* vs_pool = nullptr;
-  CUtensorMap tm_k8{}, tm_v8{};
   // allocator of a segment's pages: token pages live in the fp8 pool when fp8
   PageAllocator& pages_of(bool latent) { return (fp8 && !latent) ? alloc8 : alloc; }
   int32_t* arena = nullptr;
@@ -368,7 +351,7 @@ struct hpa_cache {
 
   PoolGeom geom() const {
     return PoolGeom{k_pool, v_pool, cfg.num_layers, cfg.num_pages, cfg.num_kv_heads, cfg.page_size,
-                    cfg.head_dim, __builtin_ctz(uint32_t(cfg.page_size)), k8_pool, v8_pool, ks_pool, vs_pool,
+                    cfg.head_dim, __builtin_ctz(uint32_t(cfg.page_size)), k8_pool, v8_pool,
                     fp8 ? cfg.num_token_pages : 0};
   }
 
@@ -698,8 +681,6 @@ hpa_status_t hpa_cache_create(const hpa_config_t* cfg, hpa_cache_t** out) {
     if (c->v_pool) cudaFree(c->v_pool);
     if (c->k8_pool) cudaFree(c->k8_pool);
     if (c->v8_pool) cudaFree(c->v8_pool);
-    if (c->ks_pool) cudaFree(c->ks_pool);
-    if (c->vs_pool) cudaFree(c->vs_pool);
     if (c->arena) cudaFree(c->arena);
     if (c->counters) cudaFree(c->counters);
     c->ring.destroy();
@@ -713,18 +694,11 @@ hpa_status_t hpa_cache_create(const hpa_config_t* cfg, hpa_cache_t** out) {
     return cuda_fail(e, "pool allocation");
   }
   if (c->fp8) {
-    const size_t b8 = size_t(rows8) * g.head_dim, bs = size_t(rows8) * 4;
+    const size_t b8 = size_t(rows8) * (g.head_dim + 4);  // codes + one fp32 scale per row
     if ((e = cudaMalloc(&c->k8_pool, b8)) != cudaSuccess || (e = cudaMalloc(&c->v8_pool, b8)) != cudaSuccess ||
-        (e = cudaMalloc(&c->ks_pool, bs)) != cudaSuccess || (e = cudaMalloc(&c->vs_pool, bs)) != cudaSuccess ||
-        (e = cudaMemset(c->k8_pool, 0, b8)) != cudaSuccess || (e = cudaMemset(c->v8_pool, 0, b8)) != cudaSuccess ||
-        (e = cudaMemset(c->ks_pool, 0, bs)) != cudaSuccess || (e = cudaMemset(c->vs_pool, 0, bs)) != cudaSuccess) {
+        (e = cudaMemset(c->k8_pool, 0, b8)) != cudaSuccess || (e = cudaMemset(c->v8_pool, 0, b8)) != cudaSuccess) {
       cleanup();
       return cuda_fail(e, "fp8 token pool allocation");
-    }
-    if (!make_map_u8(&c->tm_k8, c->k8_pool, uint64_t(rows8), uint64_t(g.head_dim)) ||
-        !make_map_u8(&c->tm_v8, c->v8_pool, uint64_t(rows8), uint64_t(g.head_dim))) {
-      cleanup();
-      return fail(HPA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the fp8 token pools");
     }
   }
   const int64_t arena_words = c->off_nent() + g.max_seqs;
@@ -776,8 +750,6 @@ hpa_status_t hpa_cache_destroy(hpa_cache_t* c) {
   cudaFree(c->v_pool);
   if (c->k8_pool) cudaFree(c->k8_pool);
   if (c->v8_pool) cudaFree(c->v8_pool);
-  if (c->ks_pool) cudaFree(c->ks_pool);
-  if (c->vs_pool) cudaFree(c->vs_pool);
   cudaFree(c->arena);
   if (c->batch_dev) cudaFree(c->batch_dev);
   if (c->o_part) cudaFree(c->o_part);
@@ -802,14 +774,11 @@ hpa_status_t hpa_cache_pools(hpa_cache_t* c, void** k_pool, void** v_pool, uint6
   return HPA_OK;
 }
 
-hpa_status_t hpa_cache_token_pool(hpa_cache_t* c, void** k8, void** v8, void** ks, void** vs,
-                                  int32_t* free_token_pages) {
+hpa_status_t hpa_cache_token_pool(hpa_cache_t* c, void** k8, void** v8, int32_t* free_token_pages) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
   if (!c->fp8) return fail(HPA_ERR_INVALID_ARG, "this cache stores bf16 token pages (token_kv_dtype = 0)");
   if (k8) *k8 = c->k8_pool;
   if (v8) *v8 = c->v8_pool;
-  if (ks) *ks = c->ks_pool;
-  if (vs) *vs = c->vs_pool;
   if (free_token_pages) *free_token_pages = c->alloc8.num_free();
   return HPA_OK;
 }
@@ -1291,12 +1260,12 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
                c->cfg.num_kv_heads,
                Hq / c->cfg.num_kv_heads, c->cfg.page_size, c->cfg.num_pages, layer, S,
                scale * 1.4426950408889634f, c->fp8 ? 1 : 0, c->fp8 ? c->cfg.num_token_pages : 0,
-               c->ks_pool, c->vs_pool, c->units_dev, c->nsplit_dev,
+               c->k8_pool, c->v8_pool, c->units_dev, c->nsplit_dev,
                c->counters + size_t(c->cfg.max_seqs) * Hkv, c->plan_units};
   if (c->fp8 && !decode_persistent())
     return fail(HPA_ERR_UNSUPPORTED, "fp8 token pages need the persistent decode kernel");
   int launched = 0;
-  cudaError_t e = launch_decode(c->tm_k_dec, c->tm_v_dec, c->tm_k8, c->tm_v8, a, D, s, &launched);
+  cudaError_t e = launch_decode(c->tm_k_dec, c->tm_v_dec, a, D, s, &launched);
   c->launches += launched;
   if (e != cudaSuccess) return cuda_fail(e, "decode launch");
   return HPA_OK;
@@ -1407,10 +1376,8 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
       const int64_t f8_rows = int64_t(layer) * c->cfg.num_token_pages * c->cfg.num_kv_heads * P;
       gl.k_pool = static_cast<__nv_bfloat16_raw*>(c->k_pool) + bf_off;
       gl.v_pool = static_cast<__nv_bfloat16_raw*>(c->v_pool) + bf_off;
-      gl.k8 = c->k8_pool + f8_rows * c->cfg.head_dim;
-      gl.v8 = c->v8_pool + f8_rows * c->cfg.head_dim;
-      gl.ks = c->ks_pool + f8_rows;
-      gl.vs = c->vs_pool + f8_rows;
+      gl.k8 = c->k8_pool + f8_rows * (c->cfg.head_dim + 4);  // whole 16-row blocks per layer
+      gl.v8 = c->v8_pool + f8_rows * (c->cfg.head_dim + 4);
       gl.L = 1;
       std::vector<ScatterRecord> recs{ScatterRecord{nullptr, nullptr, 0, 0, nrows, 0, 0, 0, 1, nrows, 0, 1}};
       if (hpa_status_t st = ship(c, s, recs, dst, nrows, &gl)) return st;
