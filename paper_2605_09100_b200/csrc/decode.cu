@@ -53,6 +53,9 @@ constexpr int kNCons = 4;   // consumer warps per CTA
 #ifndef HPA_FP8_CVT_INT
 #define HPA_FP8_CVT_INT 0  // 1: integer placement + bf16x2 multiply instead of F2FP (exact; measured slower)
 #endif
+#ifndef HPA_FP8_F16
+#define HPA_FP8_F16 0  // 1: fp8 chunks converted to f16 and run as f16 MMAs (measured slower: 197 vs 187 us)
+#endif
 #ifndef HPA_DEC_SWAP
 #define HPA_DEC_SWAP 1  // G <= 8: swapped-operand consumers (keys in M, heads in N)
 #endif
@@ -437,6 +440,27 @@ __device__ __forceinline__ void fp8_tile_to_bf16(const uint8_t* src, uint8_t* ds
     *reinterpret_cast<int4*>(dst + (cc >> 3) * 2048 + sw128(r, cc & 7)) = out;
   }
 }
+// Same as fp8_tile_to_bf16 but to f16 (one cvt per code pair; e4m3 values are exact in f16):
+// the swapped-operand consumers run fp8 chunks as f16 MMAs.
+template <int D>
+__device__ __forceinline__ void fp8_tile_to_f16(const uint8_t* src, uint8_t* dst, int lane) {
+  constexpr int kG = D / 16;
+  uint2 c[kG];
+#pragma unroll
+  for (int g = 0; g < kG; ++g) c[g] = reinterpret_cast<const uint2*>(src)[32 * g + lane];
+  __syncwarp();
+#pragma unroll
+  for (int g = 0; g < kG; ++g) {
+    const int byte = (32 * g + lane) * 8;
+    const int r = byte / D, cc = (byte % D) >> 3;
+    const uint32_t in[4] = {c[g].x & 0xffffu, c[g].x >> 16, c[g].y & 0xffffu, c[g].y >> 16};
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(w[q]) : "h"(uint16_t(in[q])));
+    *reinterpret_cast<int4*>(dst + (cc >> 3) * 2048 + sw128(r, cc & 7)) =
+        make_int4(int(w[0]), int(w[1]), int(w[2]), int(w[3]));
+  }
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
@@ -704,6 +728,14 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&q_empty[qb]);
+    uint32_t qbh[D / 16][2];  // the same B operand in f16, for fp8 chunks (f16 MMAs)
+    if (a.fp8) {
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks) {
+        qbh[ks][0] = bf16x2_to_f16x2(qbf[ks][0]);
+        qbh[ks][1] = bf16x2_to_f16x2(qbf[ks][1]);
+      }
+    }
     float o[D / 16][4];  // O^T tile mt: (dim 16mt+g, head 2t), (.., 2t+1), (dim +8, 2t), (dim +8, 2t+1)
 #pragma unroll
     for (int n = 0; n < D / 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
@@ -740,10 +772,16 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         vmul0 = vsc[gq];
         vmul1 = vsc[gq + 8];
         __syncwarp();
-        fp8_tile_to_bf16<D>(kt + L::oK8, kt, lane);
-        fp8_tile_to_bf16<D>(kt + L::oV8, vt, lane);
+        if (HPA_FP8_F16) {
+          fp8_tile_to_f16<D>(kt + L::oK8, kt, lane);
+          fp8_tile_to_f16<D>(kt + L::oV8, vt, lane);
+        } else {
+          fp8_tile_to_bf16<D>(kt + L::oK8, kt, lane);
+          fp8_tile_to_bf16<D>(kt + L::oV8, vt, lane);
+        }
         __syncwarp();
       }
+      const bool h16 = HPA_FP8_F16 && c8;  // this chunk runs as f16 MMAs
       float sacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks) {  // A = K (16 keys x 16 dims)
@@ -752,7 +790,8 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         const int kc = ks * 2 + (mi >> 1);
         uint32_t ka[4];
         ldsm_x4(smem_u32(kt + (kc >> 3) * 2048 + sw128(row, kc & 7)), ka[0], ka[1], ka[2], ka[3]);
-        mma_bf16_16816(sacc, ka, qbf[ks][0], qbf[ks][1]);
+        if (h16) mma_f16_16816(sacc, ka, qbh[ks][0], qbh[ks][1]);
+        else mma_bf16_16816(sacc, ka, qbf[ks][0], qbf[ks][1]);
       }
       const float x0 = gq < nvalid ? sacc[0] * kmul0 : -CUDART_INF_F;      // key g,   head 2t
       const float x1 = gq < nvalid ? sacc[1] * kmul0 : -CUDART_INF_F;      // key g,   head 2t+1
@@ -786,8 +825,8 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       }
       // B operand P^T: (key g: heads 2t, 2t+1) pairs transposed in registers to (head g: keys
       // 2t, 2t+1); the V scales (fp8 chunks) fold into P per key
-      const uint32_t pb0 = movmatrix_t(pack_bf16(p0 * vmul0, p1 * vmul0));
-      const uint32_t pb1 = movmatrix_t(pack_bf16(p2 * vmul1, p3 * vmul1));
+      const uint32_t pb0 = movmatrix_t(h16 ? pack_f16(p0 * vmul0, p1 * vmul0) : pack_bf16(p0 * vmul0, p1 * vmul0));
+      const uint32_t pb1 = movmatrix_t(h16 ? pack_f16(p2 * vmul1, p3 * vmul1) : pack_bf16(p2 * vmul1, p3 * vmul1));
 #pragma unroll
       for (int mt = 0; mt < D / 16; ++mt) {  // A = V^T (16 dims x 16 keys)
         const int mi = lane >> 3;
@@ -795,7 +834,8 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         const int dc = 2 * mt + (mi & 1);
         uint32_t va[4];
         ldsm_x4_t(smem_u32(vt + (dc >> 3) * 2048 + sw128(key, dc & 7)), va[0], va[1], va[2], va[3]);
-        mma_bf16_16816(o[mt], va, pb0, pb1);
+        if (h16) mma_f16_16816(o[mt], va, pb0, pb1);
+        else mma_bf16_16816(o[mt], va, pb0, pb1);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
