@@ -482,6 +482,8 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": int(bytes_per_call),
                      "launch_ms": round(dec_mean, 5), "traffic": traffic_from_profiles("decode")},
         "decode_kernel_ms": {"mean": round(dec_mean, 5), "min": round(min(dec_ms), 5),
+                             "median": round(sorted(dec_ms)[len(dec_ms) // 2], 5),
+                             "p90": round(sorted(dec_ms)[min(len(dec_ms) - 1, int(0.9 * len(dec_ms)))], 5),
                              "max_over_ranks_mean": round(dec_mean_max, 5)},
     }
 
@@ -589,12 +591,30 @@ def bench_lmag(torch, Cache, shape, dev, stream, W, K, world, max_over_ranks, ba
     inst_bytes = 2 * B * 128 * 8 * 128 * 2 * 2  # K+V, read + write
     dbytes = decode_bytes(lens, shape)
     cache.close()
+    # O(1) check (SURVEY 8(d) configs[3]): the install must not depend on the token context
+    o1 = {}
+    for tokens in (1024, 8192, 32768):
+        cache, seqs, _ = build_decode_cache(torch, Cache, shape, B, 8, tokens, 0, dev, seed=556)
+        ids = np.asarray(seqs, dtype=np.int32)
+        for _ in range(3):
+            cache.latent_install_packed(ids, sets[0], stage[0])
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for k in range(10):
+            cache.latent_install_packed(ids, sets[k % 8], stage[k % 2])
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        o1[str(tokens)] = round(e0.elapsed_time(e1) / 10 * 1e3, 1)
+        cache.close()
+        torch.cuda.empty_cache()
     return {"workload": "configs[3] LMAG: B=256 decode + per-request latent set replacement each step",
             "tokens_per_s": round(B * world / (step / 1e3), 1),
             "tokens_per_s_without_install": round(B * world / ((step - inst) / 1e3), 1),
             "step_ms": round(step, 4), "install_ms": round(inst, 4), "decode_ms": round(dec, 4),
             "install_gbs": round(inst_bytes / (inst / 1e3) / 1e9, 1),
-            "decode_gbs": round(dbytes / (dec / 1e3) / 1e9, 1)}
+            "decode_gbs": round(dbytes / (dec / 1e3) / 1e9, 1),
+            "install_us_vs_reasoning_tokens": o1}
 
 
 def bench_next(torch, Cache, shape, dev, stream, pk, max_over_ranks):
@@ -730,23 +750,54 @@ def _oracle_requests(n, seed=11):
     return c, qs, sh
 
 
+def _oracle_worker(args):
+    """One host process: builds its own request(s) and times oracle decodes for budget_s (1 BLAS thread)."""
+    seed, budget_s = args
+    from threadpoolctl import threadpool_limits
+    from oracle.hpa_oracle import decode_reference
+    c, qs, sh = _oracle_requests(1, seed=seed)
+    done, t_work = 0, 0.0
+    with threadpool_limits(1):
+        while t_work < budget_s:
+            t = time.perf_counter()
+            decode_reference(c, 0, 0, qs[0], sh.scale)
+            t_work += time.perf_counter() - t
+            done += 1
+    return done, t_work
+
+
 def cpu_baseline(budget_s: float = 15.0):
-    """The fp64 oracle as it stands, BLAS pinned to one thread, on a bounded sample."""
+    """The fp64 oracle as it stands on a bounded sample of configs[1] requests (SURVEY 8(d)
+    "Oracle timing beside it"): first on 1 host core (BLAS pinned to one thread), then on all
+    host cores (one process per core, each with its own request, BLAS pinned to one thread).
+    `value` / `cores` describe the all-cores run; the 1-core figure is reported beside it."""
+    import multiprocessing as mp
     from threadpoolctl import threadpool_limits
     from oracle.hpa_oracle import decode_reference
     n_req = 4
     c, qs, sh = _oracle_requests(n_req)
     done, t_work = 0, 0.0
+    half = budget_s / 2
     with threadpool_limits(1):
-        while t_work < budget_s:
+        while t_work < half:
             s = done % n_req
             t = time.perf_counter()
             decode_reference(c, s, 0, qs[s], sh.scale)
             t_work += time.perf_counter() - t
             done += 1
-    return {"value": round(done / t_work, 3), "unit": "tokens/s", "cores": 1, "kind": "oracle",
-            "sample": f"{done} decode queries over {n_req} configs[1] requests (Lb=5120, 32 q-heads), "
-                      f"{t_work:.1f} s of fp64 numpy work on 1 host core"}
+    one = done / t_work
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(cores) as pool:
+        res = pool.map(_oracle_worker, [(100 + i, half) for i in range(cores)])
+    wall = time.perf_counter() - t0
+    all_cores = sum(d / t for d, t in res)  # each process's own rate (spawn/setup excluded)
+    kv_gb = 5120 * 8 * 128 * 2 * 2 / 1e9     # bf16-equivalent KV bytes per configs[1] request
+    return {"value": round(all_cores, 3), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "single_core_value": round(one, 3), "kv_gbs_processed": round(all_cores * kv_gb, 3),
+            "sample": f"{done} decode queries over {n_req} configs[1] requests (Lb=5120, 32 q-heads) on 1 core "
+                      f"({t_work:.1f} s of fp64 numpy work), then {sum(d for d, _ in res)} queries on {cores} "
+                      f"processes x {half:.1f} s (1 BLAS thread each; {wall:.1f} s wall incl. spawn)"}
 
 
 def run_reference(args):
