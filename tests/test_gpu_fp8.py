@@ -179,3 +179,21 @@ def test_fp8_full_size_configs1_sampled():
                     for i, s in enumerate(sampled)])
     check_close(out[sampled], ref, "configs[1] fp8 token pages, sampled")
     cache.close()
+
+
+def test_fp8_page256_and_partial_pages():
+    shape = _shape(8, 2, 128, 256)
+    pr = _fp8_pair(shape, pages=64, tpages=64, seqs=3, per_seq=16)
+    s1 = pr.build([("tokens", 300), ("latent", 40), ("tokens", 700)])
+    s2 = pr.build([("latent", 300), ("tokens", 3)])
+    q = pr.queries(2)
+    out = pr.cache.decode(0, [s1, s2], q.cuda())
+    ref = np.stack([attend(f64(q[i:i + 1]), *pr.orc.logical_kv(s, 0), shape.scale)[0] for i, s in enumerate([s1, s2])])
+    check_close(out, ref, "fp8 P=256")
+    qp = pr.queries(64)
+    outp = pr.cache.prefill(0, [s1], [64], qp.cuda())
+    k, v = pr.orc.logical_kv(s1, 0)
+    lb = k.shape[1]
+    refp = np.stack([attend(f64(qp[t:t + 1]), k[:, :lb - 64 + t + 1], v[:, :lb - 64 + t + 1], shape.scale)[0]
+                     for t in range(64)])
+    check_close(outp, refp, "fp8 P=256 prefill")

@@ -602,3 +602,41 @@ def test_context_parallel_decode_shards_merge(n_shards):
         v = np.concatenate([p.orc.logical_kv(shard_seqs[sh][r], 0)[1] for sh in range(n_shards)], 1)
         ref.append(attend(f64(q[r:r + 1]), k, v, shape.scale)[0])
     check_close(out, np.stack(ref), f"context-parallel decode over {n_shards} shards")
+
+
+# ----------------------------------------------------------------------------- planner edge cases
+def test_decode_many_tiny_requests_and_more_ctas_than_units():
+    """4096 one-row requests (units << CTA slots is false: units >> slots, S_b = 1 everywhere)
+    and a 3-request batch (fewer units than resident CTAs): both through the persistent kernel."""
+    from tests.hpa_testutil import Pair
+    shape = Shape(num_layers=1, num_q_heads=8, num_kv_heads=2, head_dim=128, page_size=16)
+    pr = Pair(shape, num_pages=4200, max_seqs=4100, max_pages_per_seq=4)
+    seqs = [pr.new_seq() for _ in range(4096)]
+    pr.tokens(seqs, [1] * 4096)
+    q = pr.queries(4096)
+    out = pr.cache.decode(0, seqs, q.cuda())
+    torch.cuda.synchronize()
+    for i in (0, 1, 777, 2048, 4095):
+        ref = attend(f64(q[i:i + 1]), *pr.orc.logical_kv(seqs[i], 0), shape.scale)
+        check_close(out[i:i + 1], ref, f"tiny request {i}")
+    few = seqs[:3]
+    out3 = pr.cache.decode(0, few, q[:3].cuda())
+    assert torch.equal(out3, out[:3])              # same per-request result, different grid / plan
+
+
+def test_decode_one_long_request_many_splits():
+    """A single 40K-row request (1 request x H_kv units: the planner splits it up to 64 ways)
+    next to a short one: parity and equality with a forced single split."""
+    from tests.hpa_testutil import Pair
+    shape = Shape(num_layers=1, num_q_heads=16, num_kv_heads=2, head_dim=64, page_size=64)
+    pr = Pair(shape, num_pages=800, max_seqs=4, max_pages_per_seq=700)
+    a = pr.build([("latent", 128), ("tokens", 40000)])
+    b = pr.build([("tokens", 50)])
+    q = pr.queries(2)
+    out = pr.cache.decode(0, [a, b], q.cuda())
+    for i, s in enumerate([a, b]):
+        check_close(out[i:i + 1], attend(f64(q[i:i + 1]), *pr.orc.logical_kv(s, 0), shape.scale), f"long req {i}")
+    pr.cache.set_decode_splits(1)
+    out1 = pr.cache.decode(0, [a, b], q.cuda())
+    rel = float((out1.float() - out.float()).norm() / out.float().norm())
+    assert rel < 1e-2
