@@ -62,9 +62,6 @@ constexpr int kNCons = 4;   // consumer warps per CTA
 #ifndef HPA_DEC_LAZY
 #define HPA_DEC_LAZY 1  // decode consumers: lazy running-max rescale (threshold 2^8)
 #endif
-#ifndef HPA_DEC_PF
-#define HPA_DEC_PF 8
-#endif
 constexpr int kNSt = HPA_DEC_STAGES;  // ring depth
 // Ring depth must be a multiple of the consumer count, so that every slot is consumed by one
 // consumer, which then waits the slot's mbarrier phases in order. Otherwise (e.g. 10 stages,
