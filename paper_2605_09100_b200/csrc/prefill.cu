@@ -44,6 +44,13 @@ namespace {
 // key columns (and half of O's columns); the row max is exchanged through shared memory.
 // A slot's exps are then spread over twice the warps, shortening the QK -> softmax -> PV
 // chain. HPA_SM16 = 0: 8 softmax warps, one per row.
+// HPA_PF1 = 1: one 128-row query tile per CTA with TWO S buffers in TMEM, so Q K^T of tile
+// j+2 runs while the softmax of tile j+1 runs (the QK -> softmax -> PV chain of one tile no
+// longer serialises the tensor pipe); the 8 softmax warps split each row's 128 key columns
+// in two halves (row max exchanged through shared memory).
+#ifndef HPA_PF1
+#define HPA_PF1 0
+#endif
 #ifndef HPA_SM16
 #define HPA_SM16 0  // 1 measured slower (1101 vs 1236 TFLOP/s): a slot's exps share the same SMSP MUFUs
 #endif
@@ -106,15 +113,15 @@ struct PSmem {
   static constexpr int kQ = kBM * D * 2;   // one slot's Q tile
   static constexpr int kKV = kBN * D * 2;
   static constexpr int oQ = 0;
-  static constexpr int oK = oQ + 2 * kQ;
+  static constexpr int oK = oQ + (HPA_PF1 ? 1 : 2) * kQ;
   static constexpr int oV = oK + kNK * kKV;
   static constexpr int oC = oV + kNV * kKV;              // int32 [kNC][kBN + 4] (kBN = all-visible flag)
   static constexpr int oBar = oC + kNC * (kBN + 4) * 4;
   // q_full, k_full[NK], k_empty[NK], v_full[NV], v_empty[NV], s_full[2], p_full[2 slots][2 halves],
   // o_full, c_full[NC], c_empty[NC]
-  static constexpr int kNBar = 1 + 2 * kNK + 2 * kNV + 2 + 4 + 1 + 2 * kNC;
+  static constexpr int kNBar = 1 + 2 * kNK + 2 * kNV + 2 + 4 + 1 + 2 * kNC + 1;  // + o_ready (HPA_PF1)
   static constexpr int oX = oBar + kNBar * 8;      // HPA_SM16: row max [2 buf][2 slot][2 half][128], row sum [2][2][128]
-  static constexpr int kXBytes = HPA_SM16 ? (8 + 4) * kBM * 4 : 0;
+  static constexpr int kXBytes = (HPA_SM16 || HPA_PF1) ? (8 + 4) * kBM * 4 : 0;
   static constexpr int oMisc = oX + kXBytes;
   static constexpr int kRaw = oMisc + 16 + 1024;  // tmem addr + 3 tile words
   // >= 116 KB so exactly one CTA is resident per SM (it owns all 512 TMEM columns)
@@ -270,7 +277,11 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   const int q_len = a.q_len[b];
   // slot -> (q-head, row tile)
   int hq_s[2], mt_s[2];
-  if ((a.G & 1) == 0) {
+  if (HPA_PF1) {  // one query tile per CTA: (row tile, q-head)
+    hq_s[0] = hq_s[1] = blockIdx.y;
+    mt_s[0] = blockIdx.x;
+    mt_s[1] = INT_MAX / kBM;  // never live
+  } else if ((a.G & 1) == 0) {
     const int h = blockIdx.y / (a.G >> 1), pair = blockIdx.y % (a.G >> 1);
     hq_s[0] = h * a.G + 2 * pair;
     hq_s[1] = hq_s[0] + 1;
@@ -301,6 +312,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   uint64_t* o_full = p_full + 4;
   uint64_t* c_full = o_full + 1;
   uint64_t* c_empty = c_full + kNC;
+  uint64_t* o_ready = c_empty + kNC;  // HPA_PF1: one phase per PV(j) completion
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::oMisc);
   int32_t* ntiles_slot = reinterpret_cast<int32_t*>(sm + L::oMisc + 4);  // [n_tiles, skip_a, n_skip]
 
@@ -330,6 +342,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
     for (int i = 0; i < 4; ++i) mbar_init(&p_full[i], 4);  // one arrive per softmax warp
     mbar_init(o_full, 1);
+    mbar_init(o_ready, 1);
     for (int i = 0; i < kNC; ++i) { mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], kSoftWarps); }
     fence_barrier_init();
     // key slot of a logical index x: the last entry with pos0 <= x, plus the row offset
@@ -385,8 +398,36 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const int nbox = kBN / pbox;
     constexpr int kOobRow = INT_MAX / 2;  // fully out-of-bounds box -> TMA zero fill
     const int head_row = a.layer * a.NP;
+    // The block-table values of tile j+1 are fetched while tile j is processed: their L2
+    // latency would otherwise pace this loop (and with it the whole pipeline).
+    int nmv[kBN / 32], np0[kBN / 32], nrow = kOobRow;
+    auto fetch = [&](int jj, int* mv, int* pv, int& rw) {
+      const int tile = jj < skip_a ? jj : jj + n_skip;
+      const bool ok = jj < n_tiles;
+#pragma unroll
+      for (int x = 0; x < kBN / 32; ++x) {
+        const int e = (tile * kBN + x * 32 + lane) >> lp;
+        mv[x] = ok && e < n_ent ? __ldg(mt_ + e) : 0;
+        pv[x] = ok && e < n_ent ? __ldg(p0 + e) : 0;
+      }
+      rw = kOobRow;
+      if (ok && lane < nbox) {
+        const int slot = tile * kBN + lane * pbox;
+        const int e = slot >> lp;
+        if (e < n_ent) rw = ((head_row + __ldg(bt + e)) * a.Hkv + h) * P + (slot & (P - 1));
+      }
+    };
+    fetch(0, nmv, np0, nrow);
     for (int j = 0; j < n_tiles; ++j) {
       const int tile = j < skip_a ? j : j + n_skip;
+      int cmv[kBN / 32], cp0[kBN / 32];
+#pragma unroll
+      for (int x = 0; x < kBN / 32; ++x) {
+        cmv[x] = nmv[x];
+        cp0[x] = np0[x];
+      }
+      const int row = nrow;
+      fetch(j + 1, nmv, np0, nrow);
       // logical index of every key slot (INT_MAX: row >= valid_rows or past the table)
       const int cs = j % kNC;
       if (j >= kNC) mbar_wait(&c_empty[cs], ((j / kNC) - 1) & 1);
@@ -398,7 +439,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         const int slot = tile * kBN + c;
         const int e = slot >> lp, r = slot & (P - 1);
         int v = INT_MAX;
-        if (e < n_ent && r < (mt_[e] & kMetaRowsMask)) v = p0[e] + r;
+        if (e < n_ent && r < (cmv[x] & kMetaRowsMask)) v = cp0[x] + r;
         if (a.span && v >= a.span[3 * b] && v < a.span[3 * b + 1]) v |= kSpanBit;
         col[c] = v;
         vis &= (v <= i_min);
@@ -406,13 +447,6 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       vis = __all_sync(0xffffffffu, vis);
       if (lane == 0) col[kBN] = vis ? 1 : 0;
       __syncwarp();
-      // page box coordinates (lane bx < nbox owns box bx)
-      int row = kOobRow;
-      if (lane < nbox) {
-        const int slot = tile * kBN + lane * pbox;
-        const int e = slot >> lp;
-        if (e < n_ent) row = ((head_row + bt[e]) * a.Hkv + h) * P + (slot & (P - 1));
-      }
       if (lane == 0) mbar_arrive(&c_full[cs]);
       const int ks = j % kNK;
       if (j >= kNK) mbar_wait(&k_empty[ks], ((j / kNK) - 1) & 1);
@@ -432,14 +466,20 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const int nbox = kBN / pbox;
     constexpr int kOobRow = INT_MAX / 2;
     const int head_row = a.layer * a.NP;
-    for (int j = 0; j < n_tiles; ++j) {
-      const int tile = j < skip_a ? j : j + n_skip;
-      int row = kOobRow;
-      if (lane < nbox) {
+    auto vrow = [&](int jj) {  // fetched one tile ahead (see the K producer)
+      int rw = kOobRow;
+      if (jj < n_tiles && lane < nbox) {
+        const int tile = jj < skip_a ? jj : jj + n_skip;
         const int slot = tile * kBN + lane * pbox;
         const int e = slot >> lp;
-        if (e < n_ent) row = ((head_row + bt[e]) * a.Hkv + h) * P + (slot & (P - 1));
+        if (e < n_ent) rw = ((head_row + __ldg(bt + e)) * a.Hkv + h) * P + (slot & (P - 1));
       }
+      return rw;
+    };
+    int next_row = vrow(0);
+    for (int j = 0; j < n_tiles; ++j) {
+      const int row = next_row;
+      next_row = vrow(j + 1);
       const int vs = j % kNV;
       if (j >= kNV) mbar_wait(&v_empty[vs], ((j / kNV) - 1) & 1);
       if (lane == 0) mbar_arrive_expect_tx(&v_full[vs], L::kKV);
@@ -451,6 +491,62 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
       __syncwarp();
     }
+  } else if (warp == kMmaWarp && HPA_PF1) {
+    // ================================================================ MMA issuer (HPA_PF1)
+    // One query tile, S double-buffered in TMEM: QK(0), QK(1); then per tile j: PV(j) (two
+    // 64-key halves, A = P(j) from buffer j%2) and QK(j+2) into the same buffer (the pipe is
+    // in order, so PV(j) has read P(j) before QK(j+2) overwrites it).
+    constexpr uint32_t idS = idesc_bf16(kBM, kBN, 0, 0);
+    constexpr uint32_t idO = idesc_bf16(kBM, D, 0, 1);
+    const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV);
+    mbar_wait(q_full, 0);
+    auto commit = [&](uint64_t* bar) {
+      if (elect_one()) tc_commit(bar);
+      __syncwarp();
+    };
+    auto issue_s = [&](int jj) {  // S buffer jj % 2
+      mbar_wait(&k_full[jj % kNK], (jj / kNK) & 1);
+      if (lane == 0) TRACE(1, jj);
+      tc_fence_after();
+      const int ks = jj % kNK;
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint64_t ad = sdesc(aQ + (k >> 2) * (kBM * 128) + (k & 3) * 32, 16, 1024);
+          const uint64_t bd = sdesc(aK + ks * L::kKV + (k >> 2) * (kBN * 128) + (k & 3) * 32, 16, 1024);
+          tc_mma_ss(tmem + (jj & 1) * 128, ad, bd, idS, k > 0 ? 1u : 0u);
+        }
+        tc_commit(&s_full[jj & 1]);
+        tc_commit(&k_empty[ks]);
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    if (n_tiles > 1) issue_s(1);
+    for (int j = 0; j < n_tiles; ++j) {
+      const int buf = j & 1, vs = j % kNV;
+      if (lane == 0) TRACE(5, j);
+      mbar_wait(&v_full[vs], (j / kNV) & 1);
+      if (lane == 0) TRACE(2, j);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        mbar_wait(&p_full[2 * buf + half], (j >> 1) & 1);
+        if (lane == 0) TRACE(3 + half, j);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int k = half * 4; k < half * 4 + 4; ++k) {
+            const uint64_t bd = sdesc(aV + vs * L::kKV + k * 2048, kBN * 128, 1024);
+            tc_mma_ts(tmem + 256, tmem + buf * 128 + k * 8, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
+          }
+        }
+        __syncwarp();
+      }
+      commit(&v_empty[vs]);
+      commit(o_ready);  // PV(j) done -> the softmax of tile j+1 may rescale O
+      if (j + 2 < n_tiles) issue_s(j + 2);
+    }
+    commit(o_full);
   } else if (warp == kMmaWarp) {
     // ================================================================ MMA issuer
     // All 32 lanes run the loop (warp-uniform waits keep the descriptor math in uniform
@@ -524,7 +620,132 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
       commit(o_full);
     }
-#if HPA_SM16
+#if HPA_PF1
+  } else if (warp < kSoftWarps) {
+    // ================================================================ softmax (HPA_PF1)
+    // warp = 4 half + quarter: rows quarter*32 + lane, key columns [64 hc, 64 hc + 64) of the
+    // tile's S buffer, P columns [32 hc, +32) of it, O columns [D/2 hc, +D/2).
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
+    constexpr int kCols = kBN / 2, kOCols = D / 2;
+    const int hc = (warp >> 2) & 1, quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int t = mt_s[0] * kBM + row;
+    const int my_i = q_base + t;
+    const uint32_t lane_base = uint32_t(quarter * 32) << 16;
+    const uint32_t tO = tmem + lane_base + 256 + hc * kOCols;
+    float* xmax = reinterpret_cast<float*>(sm + L::oX);  // [2 buf][2 half][128]
+    float* xsum = xmax + 8 * kBM;                        // [2 half][128]
+    const float sl2 = a.scale_log2;
+    float m_run = -CUDART_INF_F, l_run = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int cs = j % kNC, buf = j & 1;
+      const uint32_t tS = tmem + lane_base + buf * 128 + hc * kCols;
+      const uint32_t tP = tmem + lane_base + buf * 128 + hc * (kCols / 2);
+      float x[kCols];
+      mbar_wait(&s_full[buf], (j >> 1) & 1);
+      if (row == 0) TRACE(7 + hc, j);
+      tc_fence_after();
+      tc_ld32(tS, x);
+      tc_ld32(tS + 32, x + 32);
+      mbar_wait(&c_full[cs], (j / kNC) & 1);
+      const int32_t* col = sC + cs * (kBN + 4) + hc * kCols;
+      const bool all_vis = sC[cs * (kBN + 4) + kBN] != 0;
+      tc_wait_ld();
+      if (!all_vis) {
+        const int cmask = my_i >= span_from ? -1 : ~kSpanBit;
+#pragma unroll
+        for (int c = 0; c < kCols; c += 4) {
+          const int4 ci = *reinterpret_cast<const int4*>(col + c);
+          x[c + 0] = (ci.x & cmask) <= my_i ? x[c + 0] : -CUDART_INF_F;
+          x[c + 1] = (ci.y & cmask) <= my_i ? x[c + 1] : -CUDART_INF_F;
+          x[c + 2] = (ci.z & cmask) <= my_i ? x[c + 2] : -CUDART_INF_F;
+          x[c + 3] = (ci.w & cmask) <= my_i ? x[c + 3] : -CUDART_INF_F;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&c_empty[cs]);
+      float pm[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pm[k] = fmaxf(x[k], x[k + 8]);
+#pragma unroll
+      for (int c = 16; c < kCols; c += 16) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pm[k] = fmaxf(pm[k], fmaxf(x[c + k], x[c + k + 8]));
+      }
+      float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+      float* xb = xmax + buf * 2 * kBM;
+      xb[hc * kBM + row] = mx;
+      named_bar_sync(1, 8 * 32);
+      mx = fmaxf(mx, xb[(hc ^ 1) * kBM + row]);
+      mx *= sl2;
+      const bool grow = mx > m_run + kRescaleThreshold;  // lazy rescale (both halves agree)
+      const float m_new = grow ? mx : m_run;
+      const float alpha = grow ? fast_exp2(m_run - m_new) : 1.f;
+      m_run = m_new;
+      if (j > 0 && __any_sync(0xffffffffu, grow)) {
+        // S(j) ready only implies PV(j-2) done: wait for PV(j-1) before touching O (phases up
+        // to j-2 are complete, so the parity wait for phase j-1 cannot alias)
+        mbar_wait(o_ready, (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < kOCols; c += 16) {
+          float o[16];
+          tc_ld16(tO + c, o);
+          tc_wait_ld();
+#pragma unroll
+          for (int y = 0; y < 16; ++y) o[y] *= alpha;
+          tc_st16(tO + c, reinterpret_cast<const uint32_t*>(o));
+        }
+      }
+      const float m_use = m_new == -CUDART_INF_F ? 0.f : m_new;
+      const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_use, -m_use);
+      float2 rs4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      uint32_t pk[kCols / 2];
+#pragma unroll
+      for (int c = 0; c < kCols; c += 2) {
+        const float2 arg = ffma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
+        float2 e;
+        e.x = fast_exp2(arg.x);
+        e.y = fast_exp2(arg.y);
+        rs4[(c >> 1) & 3] = fadd2(rs4[(c >> 1) & 3], e);
+        pk[c >> 1] = pack_bf16(e.x, e.y);
+      }
+      tc_st32(tP, pk);
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[2 * buf + hc]);
+      if (row == 0) TRACE(11 + hc, j);
+      const float2 rsa = fadd2(rs4[0], rs4[1]), rsb = fadd2(rs4[2], rs4[3]);
+      l_run = l_run * alpha + ((rsa.x + rsb.x) + (rsa.y + rsb.y));
+    }
+    // epilogue: l = both halves' sums; this warp's half of O / l -> bf16 -> global
+    xsum[hc * kBM + row] = l_run;
+    named_bar_sync(1, 8 * 32);
+    const float inv = 1.f / (l_run + xsum[(hc ^ 1) * kBM + row]);
+    mbar_wait(o_full, 0);
+    tc_fence_after();
+    __nv_bfloat16* orow =
+        static_cast<__nv_bfloat16*>(a.out) + (int64_t(a.q_off[b] + t) * a.Hq + hq_s[0]) * D + hc * kOCols;
+#pragma unroll
+    for (int c = 0; c < kOCols; c += 16) {
+      float o[16];
+      tc_ld16(tO + c, o);
+      tc_wait_ld();
+      if (t < q_len) {
+#pragma unroll
+        for (int y = 0; y < 16; y += 8) {
+          uint4 v;
+          v.x = pack_bf16(o[y + 0] * inv, o[y + 1] * inv);
+          v.y = pack_bf16(o[y + 2] * inv, o[y + 3] * inv);
+          v.z = pack_bf16(o[y + 4] * inv, o[y + 5] * inv);
+          v.w = pack_bf16(o[y + 6] * inv, o[y + 7] * inv);
+          *reinterpret_cast<uint4*>(orow + c + y) = v;
+        }
+      }
+    }
+  }
+#elif HPA_SM16
   } else if (warp < kSoftWarps) {
     // ================================================================ softmax, 16 warps
     // warp = 8 slot + 4 half + quarter: rows quarter*32 + lane of slot `s`, key columns
@@ -869,7 +1090,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
     }
   }
-#endif  // HPA_SM16
+#endif  // HPA_PF1 / HPA_SM16
   tc_fence_before();
   __syncthreads();
   if (warp == kMmaWarp) {
@@ -883,7 +1104,8 @@ cudaError_t launch_prefill_d(const CUtensorMap& tm_q, const CUtensorMap& tm_k, c
                              const PrefillArgs& a, cudaStream_t s, int* launches) {
   const int mtiles = (a.max_q_len + kBM - 1) / kBM;
   dim3 grid;
-  if ((a.G & 1) == 0) grid = dim3(mtiles, a.Hkv * (a.G / 2), a.n_seqs);
+  if (HPA_PF1) grid = dim3(mtiles, a.Hq, a.n_seqs);
+  else if ((a.G & 1) == 0) grid = dim3(mtiles, a.Hkv * (a.G / 2), a.n_seqs);
   else grid = dim3((mtiles + 1) / 2, a.Hq, a.n_seqs);
   ++*launches;
   return launch_pdl(prefill_kernel<D>, grid, dim3(kThreads), PSmem<D>::kBytes, s, tm_q, tm_k, tm_v, a);
