@@ -430,7 +430,9 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       fetch(j + 1, nmv, np0, nrow);
       // logical index of every key slot (INT_MAX: row >= valid_rows or past the table)
       const int cs = j % kNC;
+      if (lane == 0) TRACE(13, j);
       if (j >= kNC) mbar_wait(&c_empty[cs], ((j / kNC) - 1) & 1);
+      if (lane == 0) TRACE(14, j);
       int32_t* col = sC + cs * (kBN + 4);
       bool vis = true;
 #pragma unroll
@@ -449,6 +451,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       __syncwarp();
       if (lane == 0) mbar_arrive(&c_full[cs]);
       const int ks = j % kNK;
+      if (lane == 0) TRACE(15, j);
       if (j >= kNK) mbar_wait(&k_empty[ks], ((j / kNK) - 1) & 1);
       if (lane == 0) { TRACE(0, j); mbar_arrive_expect_tx(&k_full[ks], L::kKV); }
       __syncwarp();

@@ -28,3 +28,7 @@ print("mma: v_full wait duration:", [int(t[2, j] - t[5, j]) for j in J])
 print("mma: got P0 rel v done:", [int(t[3, j] - t[2, j]) for j in J])
 print("mma: k_full(j+2) got rel P1 got (j):", [int(t[1, j + 2] - t[4, j]) for j in J])
 print("K producer issue (ev0) j+2 rel mma wants (P1 got j):", [int(t[0, j + 2] - t[4, j]) for j in J])
+print("K prod: c_empty wait:", [int(t[14, j] - t[13, j]) for j in J])
+print("K prod: mask work (after c wait -> before k wait):", [int(t[15, j] - t[14, j]) for j in J])
+print("K prod: k_empty wait:", [int(t[0, j] - t[15, j]) for j in J])
+print("K prod: loop (issue j -> top j+1):", [int(t[13, j + 1] - t[0, j]) for j in J])
