@@ -51,6 +51,9 @@ namespace {
 #ifndef HPA_PF1
 #define HPA_PF1 0
 #endif
+#ifndef HPA_PF1_CLUSTER
+#define HPA_PF1_CLUSTER 1  // HPA_PF1, G even: 2-CTA clusters share K/V boxes by TMA multicast
+#endif
 #ifndef HPA_SM16
 #define HPA_SM16 0  // 1 measured slower (1101 vs 1236 TFLOP/s): a slot's exps share the same SMSP MUFUs
 #endif
@@ -248,6 +251,31 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   return r;
 }
 
+// ---- HPA_PF1 clusters: TMA multicast to both CTAs of a pair, multicast MMA commit, cluster barrier
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0,
+                                               int32_t c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 // Shared-memory matrix descriptor: start >> 4 (bits 0-13), LBO >> 4 (16-29),
 // SBO >> 4 (32-45), version 1 (46-47), layout SWIZZLE_128B = 2 (61-63).
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -265,19 +293,27 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, 
          (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
-template <int D>
+// kCl (HPA_PF1 with G even): the two q-heads of a KV-head pair run as a 2-CTA cluster over
+// the same row tile; each CTA issues half of the K/V page boxes and multicasts them to both.
+template <int D, bool kCl>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, const PrefillArgs a) {
   using L = PSmem<D>;
   constexpr int kHalves = D / 64;
-  const int b = blockIdx.z;
+  constexpr uint16_t kPair = 0x3;
+  const int b = kCl ? int(blockIdx.z) / (a.Hq / 2) : int(blockIdx.z);
+  const uint32_t crank = kCl ? cluster_rank() : 0u;
   grid_dependency_wait();  // PDL
   grid_launch_dependents();
   const int q_len = a.q_len[b];
   // slot -> (q-head, row tile)
   int hq_s[2], mt_s[2];
-  if (HPA_PF1) {  // one query tile per CTA: (row tile, q-head)
+  if (kCl) {  // cluster (x = member, y = row tile, z = head pair + Hq/2 * sequence)
+    hq_s[0] = hq_s[1] = 2 * (int(blockIdx.z) % (a.Hq / 2)) + int(blockIdx.x);
+    mt_s[0] = blockIdx.y;
+    mt_s[1] = INT_MAX / kBM;
+  } else if (HPA_PF1) {  // one query tile per CTA: (row tile, q-head)
     hq_s[0] = hq_s[1] = blockIdx.y;
     mt_s[0] = blockIdx.x;
     mt_s[1] = INT_MAX / kBM;  // never live
@@ -337,8 +373,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < kNK; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
-    for (int i = 0; i < kNV; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
+    for (int i = 0; i < kNK; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], kCl ? 2 : 1); }
+    for (int i = 0; i < kNV; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], kCl ? 2 : 1); }
     for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
     for (int i = 0; i < 4; ++i) mbar_init(&p_full[i], 4);  // one arrive per softmax warp
     mbar_init(o_full, 1);
@@ -374,6 +410,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kCl) cluster_sync();  // the peer's barriers are initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int skip_a = ntiles_slot[1], n_skip = ntiles_slot[2];
@@ -457,8 +494,11 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       __syncwarp();
       if (lane < nbox) {
 #pragma unroll
-        for (int hf = 0; hf < kHalves; ++hf)
-          tma_load_2d(sK + ks * L::kKV + hf * kBN * 128 + lane * pbox * 128, &tm_k, &k_full[ks], hf * 64, row);
+        for (int hf = 0; hf < kHalves; ++hf) {
+          uint8_t* dst = sK + ks * L::kKV + hf * kBN * 128 + lane * pbox * 128;
+          if (!kCl) tma_load_2d(dst, &tm_k, &k_full[ks], hf * 64, row);
+          else if (((lane * kHalves + hf) & 1) == int(crank)) tma_load_2d_mc(dst, &tm_k, &k_full[ks], hf * 64, row, kPair);
+        }
       }
       __syncwarp();
     }
@@ -489,8 +529,11 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       __syncwarp();
       if (lane < nbox) {
 #pragma unroll
-        for (int hf = 0; hf < kHalves; ++hf)
-          tma_load_2d(sV + vs * L::kKV + hf * kBN * 128 + lane * pbox * 128, &tm_v, &v_full[vs], hf * 64, row);
+        for (int hf = 0; hf < kHalves; ++hf) {
+          uint8_t* dst = sV + vs * L::kKV + hf * kBN * 128 + lane * pbox * 128;
+          if (!kCl) tma_load_2d(dst, &tm_v, &v_full[vs], hf * 64, row);
+          else if (((lane * kHalves + hf) & 1) == int(crank)) tma_load_2d_mc(dst, &tm_v, &v_full[vs], hf * 64, row, kPair);
+        }
       }
       __syncwarp();
     }
@@ -520,7 +563,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           tc_mma_ss(tmem + (jj & 1) * 128, ad, bd, idS, k > 0 ? 1u : 0u);
         }
         tc_commit(&s_full[jj & 1]);
-        tc_commit(&k_empty[ks]);
+        if (kCl) tc_commit_mc(&k_empty[ks], kPair);  // both CTAs' producers may reuse the stage
+        else tc_commit(&k_empty[ks]);
       }
       __syncwarp();
     };
@@ -545,7 +589,12 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         }
         __syncwarp();
       }
-      commit(&v_empty[vs]);
+      if (kCl) {
+        if (elect_one()) tc_commit_mc(&v_empty[vs], kPair);
+        __syncwarp();
+      } else {
+        commit(&v_empty[vs]);
+      }
       commit(o_ready);  // PV(j) done -> the softmax of tile j+1 may rescale O
       if (j + 2 < n_tiles) issue_s(j + 2);
     }
@@ -1096,6 +1145,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #endif  // HPA_PF1 / HPA_SM16
   tc_fence_before();
   __syncthreads();
+  if constexpr (kCl) cluster_sync();  // the peer may still multicast into / signal this CTA until here
   if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
@@ -1106,21 +1156,48 @@ template <int D>
 cudaError_t launch_prefill_d(const CUtensorMap& tm_q, const CUtensorMap& tm_k, const CUtensorMap& tm_v,
                              const PrefillArgs& a, cudaStream_t s, int* launches) {
   const int mtiles = (a.max_q_len + kBM - 1) / kBM;
+  ++*launches;
+  if (HPA_PF1 && HPA_PF1_CLUSTER && (a.G & 1) == 0) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2, mtiles, (a.Hq / 2) * a.n_seqs);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = PSmem<D>::kBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, prefill_kernel<D, true>, tm_q, tm_k, tm_v, a);
+  }
   dim3 grid;
   if (HPA_PF1) grid = dim3(mtiles, a.Hq, a.n_seqs);
   else if ((a.G & 1) == 0) grid = dim3(mtiles, a.Hkv * (a.G / 2), a.n_seqs);
   else grid = dim3((mtiles + 1) / 2, a.Hq, a.n_seqs);
-  ++*launches;
-  return launch_pdl(prefill_kernel<D>, grid, dim3(kThreads), PSmem<D>::kBytes, s, tm_q, tm_k, tm_v, a);
+  return launch_pdl(prefill_kernel<D, false>, grid, dim3(kThreads), PSmem<D>::kBytes, s, tm_q, tm_k, tm_v, a);
 }
 
 }  // namespace
 
 cudaError_t prefill_init_attributes() {
-  cudaError_t e = cudaFuncSetAttribute(prefill_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       PSmem<128>::kBytes);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(prefill_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, PSmem<64>::kBytes);
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(prefill_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                PSmem<128>::kBytes)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(prefill_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                PSmem<64>::kBytes)) != cudaSuccess)
+    return e;
+  if (HPA_PF1 && HPA_PF1_CLUSTER) {
+    if ((e = cudaFuncSetAttribute(prefill_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  PSmem<128>::kBytes)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(prefill_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  PSmem<64>::kBytes)) != cudaSuccess)
+      return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_prefill(const CUtensorMap& tm_q, const CUtensorMap& tm_k, const CUtensorMap& tm_v,
