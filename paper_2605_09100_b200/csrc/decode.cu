@@ -53,6 +53,9 @@ constexpr int kNCons = 4;   // consumer warps per CTA
 #ifndef HPA_FP8_CVT_INT
 #define HPA_FP8_CVT_INT 0  // 1: integer placement + bf16x2 multiply instead of F2FP (exact; measured slower)
 #endif
+#ifndef HPA_COMBINE_WARP
+#define HPA_COMBINE_WARP 1  // a5: one warp per (request, q-head) instead of one CTA of D threads
+#endif
 #ifndef HPA_FP8_F16
 #define HPA_FP8_F16 0  // 1: fp8 chunks converted to f16 and run as f16 MMAs (measured slower: 197 vs 187 us)
 #endif
@@ -1081,6 +1084,78 @@ __global__ void __launch_bounds__(D) combine_kernel(const float* __restrict__ o_
   }
 }
 
+// a5 with one warp per (request, q-head): the lanes read the S_b split LSEs at once (S <= 64),
+// reduce max and weight sum with shuffles, then each lane accumulates D/32 contiguous dims
+// over the splits (independent float4 / float2 loads). 4 rows per 128-thread CTA.
+template <int D>
+__global__ void __launch_bounds__(128) combine_warp_kernel(const float* __restrict__ o_part,
+                                                           const float* __restrict__ lse, __nv_bfloat16* out,
+                                                           int S_max, const int32_t* __restrict__ nsplit, int Hq,
+                                                           int64_t rows, float* part_o, float* part_lse) {
+  grid_dependency_wait();
+  grid_launch_dependents();
+  constexpr int kV = D / 32;  // dims per lane
+  const int lane = threadIdx.x & 31;
+  const int64_t bh = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  if (bh >= rows) return;
+  const int S = nsplit ? nsplit[bh / Hq] : S_max;
+  const float* ls = lse + bh * S_max;
+  const float l0 = lane < S ? ls[lane] : -CUDART_INF_F;
+  const float l1 = lane + 32 < S ? ls[lane + 32] : -CUDART_INF_F;
+  float M = fmaxf(l0, l1);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  const float w0 = l0 == -CUDART_INF_F ? 0.f : fast_exp2(l0 - M);
+  const float w1 = l1 == -CUDART_INF_F ? 0.f : fast_exp2(l1 - M);
+  float W = w0 + w1;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) W += __shfl_xor_sync(0xffffffffu, W, o);
+  float acc[kV];
+#pragma unroll
+  for (int v = 0; v < kV; ++v) acc[v] = 0.f;
+  const float* op = o_part + bh * S_max * D + lane * kV;
+  for (int s0 = 0; s0 < S; s0 += 4) {
+    float vals[4][kV];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // up to 4 splits' loads in flight
+      if (s0 + u < S) {
+        if (kV == 4) {
+          const float4 t = *reinterpret_cast<const float4*>(op + (s0 + u) * D);
+          vals[u][0] = t.x; vals[u][1] = t.y; vals[u][2 % kV] = t.z; vals[u][3 % kV] = t.w;
+        } else {
+          const float2 t = *reinterpret_cast<const float2*>(op + (s0 + u) * D);
+          vals[u][0] = t.x; vals[u][1 % kV] = t.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int sidx = s0 + u;
+      const float w = __shfl_sync(0xffffffffu, sidx < 32 ? w0 : w1, sidx & 31);
+      if (sidx < S) {
+#pragma unroll
+        for (int v = 0; v < kV; ++v) acc[v] += w * vals[u][v];
+      }
+    }
+  }
+  const float inv = 1.f / W;
+  if (part_o) {
+#pragma unroll
+    for (int v = 0; v < kV; ++v) part_o[bh * D + lane * kV + v] = acc[v] * inv;
+    if (lane == 0) part_lse[bh] = M + __log2f(W);
+  } else {
+    __nv_bfloat16* orow = out + bh * D + lane * kV;
+    if (kV == 4) {
+      uint2 w;
+      w.x = pack_bf16(acc[0] * inv, acc[1] * inv);
+      w.y = pack_bf16(acc[2 % kV] * inv, acc[3 % kV] * inv);
+      *reinterpret_cast<uint2*>(orow) = w;
+    } else {
+      *reinterpret_cast<uint32_t*>(orow) = pack_bf16(acc[0] * inv, acc[1 % kV] * inv);
+    }
+  }
+}
+
 // Context-parallel merge: parts laid out [P][rows] (as all-gathered); one CTA per row.
 template <int D>
 __global__ void __launch_bounds__(D) merge_kernel(const float* __restrict__ o_parts,
@@ -1122,10 +1197,17 @@ cudaError_t launch_decode_d(const CUtensorMap& tm_k, const CUtensorMap& tm_v, co
   if (e != cudaSuccess) return e;
   ++*launches;
   if ((a.splits > 1 && !HPA_FUSED_COMBINE) || a.part_o) {
-    e = launch_pdl(combine_kernel<D>, dim3(a.n_seqs * a.Hq), dim3(D), 0, s,
-                   static_cast<const float*>(a.o_part), static_cast<const float*>(a.lse_part),
-                   static_cast<__nv_bfloat16*>(a.out), a.splits, HPA_DECODE_PERSISTENT ? a.nsplit : nullptr,
-                   a.Hq, a.part_o, a.part_lse);
+    const int64_t rows = int64_t(a.n_seqs) * a.Hq;
+    if (HPA_COMBINE_WARP && a.splits <= 64)
+      e = launch_pdl(combine_warp_kernel<D>, dim3(unsigned((rows + 3) / 4)), dim3(128), 0, s,
+                     static_cast<const float*>(a.o_part), static_cast<const float*>(a.lse_part),
+                     static_cast<__nv_bfloat16*>(a.out), a.splits, HPA_DECODE_PERSISTENT ? a.nsplit : nullptr,
+                     a.Hq, rows, a.part_o, a.part_lse);
+    else
+      e = launch_pdl(combine_kernel<D>, dim3(unsigned(rows)), dim3(D), 0, s,
+                     static_cast<const float*>(a.o_part), static_cast<const float*>(a.lse_part),
+                     static_cast<__nv_bfloat16*>(a.out), a.splits, HPA_DECODE_PERSISTENT ? a.nsplit : nullptr,
+                     a.Hq, a.part_o, a.part_lse);
     ++*launches;
   }
   return e;
