@@ -247,6 +247,10 @@ hpa_status_t hpa_export_table(hpa_cache_t* c, int32_t seq_id, int32_t* pages, in
                               uint16_t* meta, int32_t cap, int32_t* n_out);
 /* Testing / tuning hook: force the decode split count (0 = planner). */
 hpa_status_t hpa_set_decode_splits(hpa_cache_t* c, int32_t splits);
+/* Testing / tuning hook for hpa_prefill / hpa_prefill_span: 0 = planner (split-KV only for
+ * the units of an under-filled last wave), 1 = never split, 2..15 = split every unit's key
+ * tiles into that many pieces (merged by LSE). INVALID_ARG outside [0, 15]. */
+hpa_status_t hpa_set_prefill_splits(hpa_cache_t* c, int32_t splits);
 /* Number of kernels this cache has launched so far (bench "gpu_launches"). */
 hpa_status_t hpa_launch_count(hpa_cache_t* c, uint64_t* n);
 

@@ -318,6 +318,10 @@ class Cache:
     def set_decode_splits(self, splits: int) -> None:
         check(LIB.hpa_set_decode_splits(self._h, splits))
 
+    def set_prefill_splits(self, splits: int) -> None:
+        """0 = planner, 1 = never split, 2..15 = every unit split into that many key ranges."""
+        check(LIB.hpa_set_prefill_splits(self._h, splits))
+
     def launch_count(self) -> int:
         n = ctypes.c_uint64()
         check(LIB.hpa_launch_count(self._h, ctypes.byref(n)))

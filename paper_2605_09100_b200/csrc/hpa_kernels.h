@@ -142,11 +142,28 @@ struct PrefillArgs {
   int32_t log2P;
   const int32_t* span;      // [n][3] device (lo, hi, q_from) or nullptr: GRC mask-out span
   long long* trace;         // HPA_TRACE builds only: per-phase clock64 stamps of CTA (0,0,0)
+  // Work list (plan_prefill; nullptr: one CTA per (row tile, head pair, sequence) of a grid,
+  // each searching the table for its key-tile count). CTA i reads work[4i .. 4i+3] =
+  // {seq b, head index y, row-tile index x, piece | nsplit << 4 | part << 8},
+  // {first iteration jb, iterations n, skip_a, n_skip} (iteration j loads key tile
+  // j < skip_a ? j : j + n_skip), {seq id, q_len, q_off, seq_len}, {n_entries, 0, 0, 0}.
+  // nsplit == 1 writes bf16 output directly; nsplit > 1 writes O / l (fp32) and the
+  // log2-domain LSE of piece `piece` of split unit `part` to o_part / lse_part, merged by
+  // prefill_combine_kernel over parts[2j], parts[2j+1] = {b, y, x, nsplit}, {q_len, q_off, 0, 0}.
+  const int4* work;
+  int32_t n_work;
+  const int4* parts;
+  int32_t n_parts, split_max;
+  float* o_part;            // [n_parts][split_max][2 slots][128 rows][D]
+  float* lse_part;          // [n_parts][split_max][2][128]
 };
-// tm_q: 3-D map over q [sum q][Hq][d] with box {64, 1, 128};
-// tm_k / tm_v: 2-D maps over the pools with box {64, min(P,128)}.
+// Split-KV prefill (work lists) is built in the default kernel configuration only.
+bool prefill_split_supported();
+// tm_q / tm_o: 3-D maps over q / out [sum q][Hq][d] with box {64, 1, 128};
+// tm_k / tm_v: 2-D maps over the pools with box {64, min(P,128)};
+// tm_op: 2-D fp32 map over o_part [rows][d] with box {32, 128} (work lists with splits).
 cudaError_t launch_prefill(const CUtensorMap& tm_q, const CUtensorMap& tm_k,
-                           const CUtensorMap& tm_v, const PrefillArgs& a, int32_t D,
-                           cudaStream_t s, int* launches);
+                           const CUtensorMap& tm_v, const CUtensorMap& tm_o, const CUtensorMap& tm_op,
+                           const PrefillArgs& a, int32_t D, cudaStream_t s, int* launches);
 
 }  // namespace hpa

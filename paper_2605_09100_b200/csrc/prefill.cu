@@ -92,8 +92,20 @@ constexpr int kSpanBit = 1 << 30;          // tags span columns in the mask indi
     if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64)        \
       a.trace[(ev) * 64 + (j)] = clock64();                                                  \
   } while (0)
+// CTA timeline (HPA_TRACE builds): trace[4096 + 8 i ...] = {entry ns, setup done, first S,
+// o_full passed, exit ns, smid, n_tiles, 1} of CTA i (globaltimer).
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CTA_STAMP(k, v)                                                                      \
+  do {                                                                                       \
+    if (a.trace) a.trace[4096 + 8 * int64_t(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) + (k)] = (v); \
+  } while (0)
 #else
 #define TRACE(ev, j) do { } while (0)
+#define CTA_STAMP(k, v) do { } while (0)
 #endif
 #ifndef HPA_P_PACK_ALU
 #define HPA_P_PACK_ALU 0  // 1: P -> bf16 on the ALU pipe instead of F2FP (measured slower)
@@ -293,20 +305,56 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, 
          (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
+// Unit (y, x) -> the two slots' (q-head, row tile): G even pairs two q-heads of one GQA group
+// over row tile x (y = kv-head * G/2 + pair); G odd pairs row tiles 2x, 2x+1 of q-head y.
+__device__ __forceinline__ void unit_slots(int G, int y, int x, int* hq_s, int* mt_s) {
+  if ((G & 1) == 0) {
+    const int h = y / (G >> 1), pair = y % (G >> 1);
+    hq_s[0] = h * G + 2 * pair;
+    hq_s[1] = hq_s[0] + 1;
+    mt_s[0] = mt_s[1] = x;
+  } else {
+    hq_s[0] = hq_s[1] = y;
+    mt_s[0] = 2 * x;
+    mt_s[1] = 2 * x + 1;
+  }
+}
+
 // kCl (HPA_PF1 with G even): the two q-heads of a KV-head pair run as a 2-CTA cluster over
 // the same row tile; each CTA issues half of the K/V page boxes and multicasts them to both.
 template <int D, bool kCl>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-               const __grid_constant__ CUtensorMap tm_v, const PrefillArgs a) {
+               const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+               const __grid_constant__ CUtensorMap tm_op, const PrefillArgs a) {
   using L = PSmem<D>;
   constexpr int kHalves = D / 64;
   constexpr uint16_t kPair = 0x3;
-  const int b = kCl ? int(blockIdx.z) / (a.Hq / 2) : int(blockIdx.z);
   const uint32_t crank = kCl ? cluster_rank() : 0u;
   grid_dependency_wait();  // PDL
   grid_launch_dependents();
-  const int q_len = a.q_len[b];
+#ifdef HPA_TRACE
+  if (threadIdx.x == 0) CTA_STAMP(0, gtimer());
+#endif
+  // unit (b, y, x) and key-range piece: from the work list (plan_prefill) or the grid
+  int ux = blockIdx.x, uy = blockIdx.y, piece = 0, part = -1;
+  int b = kCl ? int(blockIdx.z) / (a.Hq / 2) : int(blockIdx.z);
+  const bool listed = !kCl && !HPA_PF1 && a.work != nullptr;
+  // listed: wr = {jb, n_tiles, skip_a, n_skip}, wq = {seq, q_len, q_off, seq_len}, wn = {n_ent}
+  // (four independent 16-B loads instead of a chain of dependent metadata loads)
+  int4 wr = make_int4(0, 0, 0, 0), wq = make_int4(0, 0, 0, 0), wn = make_int4(0, 0, 0, 0);
+  if (listed) {
+    const int4 w = a.work[4 * blockIdx.x];
+    wr = a.work[4 * blockIdx.x + 1];
+    wq = a.work[4 * blockIdx.x + 2];
+    wn = a.work[4 * blockIdx.x + 3];
+    b = w.x;
+    uy = w.y;
+    ux = w.z;
+    piece = w.w & 15;
+    part = ((w.w >> 4) & 15) > 1 ? (w.w >> 8) : -1;
+  }
+  const int q_len = listed ? wq.y : a.q_len[b];
   // slot -> (q-head, row tile)
   int hq_s[2], mt_s[2];
   if (kCl) {  // cluster (x = member, y = row tile, z = head pair + Hq/2 * sequence)
@@ -317,15 +365,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     hq_s[0] = hq_s[1] = blockIdx.y;
     mt_s[0] = blockIdx.x;
     mt_s[1] = INT_MAX / kBM;  // never live
-  } else if ((a.G & 1) == 0) {
-    const int h = blockIdx.y / (a.G >> 1), pair = blockIdx.y % (a.G >> 1);
-    hq_s[0] = h * a.G + 2 * pair;
-    hq_s[1] = hq_s[0] + 1;
-    mt_s[0] = mt_s[1] = blockIdx.x;
   } else {
-    hq_s[0] = hq_s[1] = blockIdx.y;
-    mt_s[0] = 2 * blockIdx.x;
-    mt_s[1] = 2 * blockIdx.x + 1;
+    unit_slots(a.G, uy, ux, hq_s, mt_s);
   }
   if (mt_s[0] * kBM >= q_len) return;  // ragged: this sequence has fewer query tiles
   const bool slot1_live = mt_s[1] * kBM < q_len;
@@ -353,9 +394,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   int32_t* ntiles_slot = reinterpret_cast<int32_t*>(sm + L::oMisc + 4);  // [n_tiles, skip_a, n_skip]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int seq = a.seq_rows[b];
-  const int seq_len = a.t.seq_len[seq];
-  const int n_ent = a.t.n_entries[seq];
+  const int seq = listed ? wq.x : a.seq_rows[b];
+  const int seq_len = listed ? wq.w : a.t.seq_len[seq];
+  const int n_ent = listed ? wn.x : a.t.n_entries[seq];
+  const int q_off = listed ? wq.z : a.q_off[b];
   const int32_t* bt = a.t.block_table + int64_t(seq) * a.t.max_pages;
   const int32_t* p0 = a.t.pos0 + int64_t(seq) * a.t.max_pages;
   const int32_t* mt_ = a.t.meta + int64_t(seq) * a.t.max_pages;
@@ -381,6 +423,15 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     mbar_init(o_ready, 1);
     for (int i = 0; i < kNC; ++i) { mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], kSoftWarps); }
     fence_barrier_init();
+    if (!kCl) {  // Q tiles in flight while the CTA finishes its setup
+      tma_prefetch_desc(&tm_q);
+      mbar_arrive_expect_tx(q_full, slot1_live ? 2 * L::kQ : L::kQ);
+      for (int s = 0; s < (slot1_live ? 2 : 1); ++s) {
+#pragma unroll
+        for (int hf = 0; hf < kHalves; ++hf)
+          tma_load_3d(sQ + s * L::kQ + hf * kBM * 128, &tm_q, q_full, hf * 64, hq_s[s], q_off + mt_s[s] * kBM);
+      }
+    }
     // key slot of a logical index x: the last entry with pos0 <= x, plus the row offset
     auto slot_of = [&](int x) {
       int lo = 0, hi = n_ent - 1;
@@ -390,6 +441,9 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
       return (lo << lp) + (x - p0[lo]);
     };
+    if (listed) {  // the host computed the tile range (plan_prefill): no table search here
+      ntiles_slot[0] = ntiles_slot[1] = ntiles_slot[2] = 0;
+    } else {
     // key tiles needed: up to the tile holding the slot of logical index i_max
     ntiles_slot[0] = slot_of(i_max) / kBN + 1;
     // tiles entirely inside the GRC span are skipped when every query row of the CTA
@@ -402,6 +456,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     }
     ntiles_slot[1] = skip_a;
     ntiles_slot[2] = skip_b - skip_a;
+    }
   }
   if (warp == kMmaWarp) {  // TMEM: S/P 0 [0,128), S/P 1 [128,256), O0 [256,..), O1 [384,..)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -413,22 +468,50 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   if constexpr (kCl) cluster_sync();  // the peer's barriers are initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int skip_a = ntiles_slot[1], n_skip = ntiles_slot[2];
-  const int n_tiles = ntiles_slot[0] - n_skip;  // iterations; tile(jj) = jj < skip_a ? jj : jj + n_skip
+#ifdef HPA_TRACE
+  if (threadIdx.x == 0) CTA_STAMP(1, gtimer());
+#endif
+  // this CTA runs iterations [jb, jb + n_tiles) of its unit; iteration jj loads key tile
+  // tile_of(jj) (past the tiles skipped inside the GRC span)
+  const int skip_a = listed ? wr.z : ntiles_slot[1], n_skip = listed ? wr.w : ntiles_slot[2];
+  const int jb = listed ? wr.x : 0;
+  const int n_tiles = listed ? wr.y : ntiles_slot[0] - n_skip;
+  auto tile_of = [&](int jj) {
+    jj += jb;
+    return jj < skip_a ? jj : jj + n_skip;
+  };
+  if (n_tiles <= 0) {  // an empty split piece (more pieces than key tiles): O = 0, LSE = -inf
+    if (warp < 8 && part >= 0) {
+      const int s = warp >> 2, row = (warp & 3) * 32 + lane;
+      const int pp = (part * a.split_max + piece) * 2 + s;
+      float4* orow = reinterpret_cast<float4*>(a.o_part + (int64_t(pp) * kBM + row) * D);
+      for (int c = 0; c < D / 4; ++c) orow[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      a.lse_part[int64_t(pp) * kBM + row] = -CUDART_INF_F;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+    return;
+  }
 
   if (warp >= kSoftWarps) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kOtherRegs));
   if (warp == kProducerWarp) {
     // ================================================================ producer
     if (lane == 0) {
-      tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
-      mbar_arrive_expect_tx(q_full, slot1_live ? 2 * L::kQ : L::kQ);
-      for (int s = 0; s < (slot1_live ? 2 : 1); ++s) {
-        const int q_tok = a.q_off[b] + mt_s[s] * kBM;
+      if (kCl) {
+        tma_prefetch_desc(&tm_q);
+        mbar_arrive_expect_tx(q_full, slot1_live ? 2 * L::kQ : L::kQ);
+        for (int s = 0; s < (slot1_live ? 2 : 1); ++s) {
+          const int q_tok = q_off + mt_s[s] * kBM;
 #pragma unroll
-        for (int hf = 0; hf < kHalves; ++hf)
-          tma_load_3d(sQ + s * L::kQ + hf * kBM * 128, &tm_q, q_full, hf * 64, hq_s[s], q_tok);
+          for (int hf = 0; hf < kHalves; ++hf)
+            tma_load_3d(sQ + s * L::kQ + hf * kBM * 128, &tm_q, q_full, hf * 64, hq_s[s], q_tok);
+        }
       }
     }
     const int pbox = P < kBN ? P : kBN;
@@ -439,7 +522,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     // latency would otherwise pace this loop (and with it the whole pipeline).
     int nmv[kBN / 32], np0[kBN / 32], nrow = kOobRow;
     auto fetch = [&](int jj, int* mv, int* pv, int& rw) {
-      const int tile = jj < skip_a ? jj : jj + n_skip;
+      const int tile = tile_of(jj);
       const bool ok = jj < n_tiles;
 #pragma unroll
       for (int x = 0; x < kBN / 32; ++x) {
@@ -456,7 +539,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     };
     fetch(0, nmv, np0, nrow);
     for (int j = 0; j < n_tiles; ++j) {
-      const int tile = j < skip_a ? j : j + n_skip;
+      const int tile = tile_of(j);
       int cmv[kBN / 32], cp0[kBN / 32];
 #pragma unroll
       for (int x = 0; x < kBN / 32; ++x) {
@@ -512,7 +595,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     auto vrow = [&](int jj) {  // fetched one tile ahead (see the K producer)
       int rw = kOobRow;
       if (jj < n_tiles && lane < nbox) {
-        const int tile = jj < skip_a ? jj : jj + n_skip;
+        const int tile = tile_of(jj);
         const int slot = tile * kBN + lane * pbox;
         const int e = slot >> lp;
         if (e < n_ent) rw = ((head_row + __ldg(bt + e)) * a.Hkv + h) * P + (slot & (P - 1));
@@ -778,7 +861,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     mbar_wait(o_full, 0);
     tc_fence_after();
     __nv_bfloat16* orow =
-        static_cast<__nv_bfloat16*>(a.out) + (int64_t(a.q_off[b] + t) * a.Hq + hq_s[0]) * D + hc * kOCols;
+        static_cast<__nv_bfloat16*>(a.out) + (int64_t(q_off + t) * a.Hq + hq_s[0]) * D + hc * kOCols;
 #pragma unroll
     for (int c = 0; c < kOCols; c += 16) {
       float o[16];
@@ -915,7 +998,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       mbar_wait(o_full, 0);
       tc_fence_after();
       __nv_bfloat16* orow =
-          static_cast<__nv_bfloat16*>(a.out) + (int64_t(a.q_off[b] + t) * a.Hq + hq_s[s]) * D + hc * kOCols;
+          static_cast<__nv_bfloat16*>(a.out) + (int64_t(q_off + t) * a.Hq + hq_s[s]) * D + hc * kOCols;
 #pragma unroll
       for (int c = 0; c < kOCols; c += 16) {
         float o[16];
@@ -961,6 +1044,9 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       float x[kBN];
       mbar_wait(&s_full[s], j & 1);
       if (row == 0) TRACE(7 + s, j);
+#ifdef HPA_TRACE
+      if (j == 0 && threadIdx.x == 0) CTA_STAMP(2, gtimer());
+#endif
       tc_fence_after();
       constexpr int kLd0 = HPA_SPLIT_LD ? kBN / 2 : kBN;  // columns loaded before the first wait
 #pragma unroll
@@ -1117,26 +1203,82 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const float2 rsa = fadd2(rs4[0], rs4[1]), rsb = fadd2(rs4[2], rs4[3]);
       l_run = l_run * alpha + ((rsa.x + rsb.x) + (rsa.y + rsb.y));
     }
+#ifdef HPA_TRACE
+    if (threadIdx.x == 0) {
+      mbar_wait(o_full, 0);
+      CTA_STAMP(3, gtimer());
+    }
+#endif
     if (live) {
-      // epilogue: O / l -> bf16 -> global
+      // Epilogue. O / l is staged in shared memory (the K and V rings are idle once o_full has
+      // fired: every MMA has completed) in the 128-B-swizzled box layout and written by TMA
+      // stores: bf16 into the output rows, or -- a split piece -- fp32 O / l into the
+      // workspace with LSE = m + log2 l (log2 domain; -inf when no key of the piece was
+      // visible to the row), merged by prefill_combine_kernel. A ragged last row tile (its
+      // box would cover the next sequence's rows) is stored row by row instead.
       mbar_wait(o_full, 0);
       tc_fence_after();
-      const float inv = 1.f / l_run;
-      __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + (int64_t(a.q_off[b] + t) * a.Hq + hq_s[s]) * D;
+      const bool split = part >= 0;
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      if (split || (mt_s[s] + 1) * kBM <= q_len) {
+        uint8_t* stage = s == 0 ? sK : sV;
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        float o[32];
-        tc_ld32(tO + c * 32, o);
-        tc_wait_ld();
-        if (t < q_len) {
+        for (int c = 0; c < D / 32; ++c) {
+          float o[32];
+          tc_ld32(tO + c * 32, o);
+          tc_wait_ld();
+          if (split) {  // fp32 box c: columns [32 c, 32 c + 32) = one 128-B row of 8 chunks
+            uint8_t* box = stage + c * (kBM * 128);
 #pragma unroll
-          for (int y = 0; y < 32; y += 8) {
-            uint4 v;
-            v.x = pack_bf16(o[y + 0] * inv, o[y + 1] * inv);
-            v.y = pack_bf16(o[y + 2] * inv, o[y + 3] * inv);
-            v.z = pack_bf16(o[y + 4] * inv, o[y + 5] * inv);
-            v.w = pack_bf16(o[y + 6] * inv, o[y + 7] * inv);
-            *reinterpret_cast<uint4*>(orow + c * 32 + y) = v;
+            for (int k = 0; k < 8; ++k)
+              *reinterpret_cast<float4*>(box + sw128(row, k)) =
+                  make_float4(o[4 * k] * inv, o[4 * k + 1] * inv, o[4 * k + 2] * inv, o[4 * k + 3] * inv);
+          } else {  // bf16 box c / 2: columns [64 (c / 2), + 64), chunks 4 (c & 1) .. + 3
+            uint8_t* box = stage + (c >> 1) * (kBM * 128);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              uint4 v;
+              v.x = pack_bf16(o[8 * k + 0] * inv, o[8 * k + 1] * inv);
+              v.y = pack_bf16(o[8 * k + 2] * inv, o[8 * k + 3] * inv);
+              v.z = pack_bf16(o[8 * k + 4] * inv, o[8 * k + 5] * inv);
+              v.w = pack_bf16(o[8 * k + 6] * inv, o[8 * k + 7] * inv);
+              *reinterpret_cast<uint4*>(box + sw128(row, (c & 1) * 4 + k)) = v;
+            }
+          }
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1 + s, 128);
+        const int pp = (part * a.split_max + piece) * 2 + s;
+        if (quarter == 0 && lane == 0) {
+          if (split) {
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) tma_store_2d(&tm_op, stage + c * (kBM * 128), c * 32, pp * kBM);
+          } else {
+#pragma unroll
+            for (int hf = 0; hf < kHalves; ++hf)
+              tma_store_3d(&tm_o, stage + hf * (kBM * 128), hf * 64, hq_s[s], q_off + mt_s[s] * kBM);
+          }
+          bulk_commit();
+          bulk_wait_read();  // the smem is released at exit
+        }
+        if (split) a.lse_part[int64_t(pp) * kBM + row] = l_run > 0.f ? m_run + __log2f(l_run) : -CUDART_INF_F;
+      } else {
+        __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + (int64_t(q_off + t) * a.Hq + hq_s[s]) * D;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          float o[32];
+          tc_ld32(tO + c * 32, o);
+          tc_wait_ld();
+          if (t < q_len) {
+#pragma unroll
+            for (int y = 0; y < 32; y += 8) {
+              uint4 v;
+              v.x = pack_bf16(o[y + 0] * inv, o[y + 1] * inv);
+              v.y = pack_bf16(o[y + 2] * inv, o[y + 3] * inv);
+              v.z = pack_bf16(o[y + 4] * inv, o[y + 5] * inv);
+              v.w = pack_bf16(o[y + 6] * inv, o[y + 7] * inv);
+              *reinterpret_cast<uint4*>(orow + c * 32 + y) = v;
+            }
           }
         }
       }
@@ -1145,6 +1287,16 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #endif  // HPA_PF1 / HPA_SM16
   tc_fence_before();
   __syncthreads();
+#ifdef HPA_TRACE
+  if (threadIdx.x == 0) {
+    CTA_STAMP(4, gtimer());
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    CTA_STAMP(5, smid);
+    CTA_STAMP(6, n_tiles);
+    CTA_STAMP(7, 1);
+  }
+#endif
   if constexpr (kCl) cluster_sync();  // the peer may still multicast into / signal this CTA until here
   if (warp == kMmaWarp) {
     tc_fence_after();
@@ -1152,9 +1304,66 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   }
 }
 
+// Split-KV merge (the LSE algebra of the decode combine, a5): one warp per (split unit, slot,
+// query row); lane l holds the LSE of piece l, every lane accumulates D/32 dims over the pieces.
+// out = sum_i 2^(lse_i - M) O_i / sum_i 2^(lse_i - M), bf16, into the caller's output rows.
+template <int D>
+__global__ void __launch_bounds__(128) prefill_combine_kernel(const PrefillArgs a) {
+  grid_dependency_wait();
+  grid_launch_dependents();
+  constexpr int kV = D / 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t rid = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  if (rid >= int64_t(a.n_parts) * 2 * kBM) return;
+  const int part = int(rid / (2 * kBM)), s = int(rid / kBM) & 1, row = int(rid % kBM);
+  const int4 u = a.parts[2 * part], uq = a.parts[2 * part + 1];  // {b, y, x, nsplit}, {q_len, q_off}
+  int hq_s[2], mt_s[2];
+  unit_slots(a.G, u.y, u.z, hq_s, mt_s);
+  const int t = mt_s[s] * kBM + row;
+  if (t >= uq.x) return;
+  const int S = u.w;
+  auto pidx = [&](int i) { return (int64_t(part * a.split_max + i) * 2 + s) * kBM + row; };
+  const float l = lane < S ? a.lse_part[pidx(lane)] : -CUDART_INF_F;
+  float M = l;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  const float w = l == -CUDART_INF_F ? 0.f : fast_exp2(l - M);
+  float W = w;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) W += __shfl_xor_sync(0xffffffffu, W, o);
+  float acc[kV];
+#pragma unroll
+  for (int v = 0; v < kV; ++v) acc[v] = 0.f;
+  for (int i = 0; i < S; ++i) {
+    const float wi = __shfl_sync(0xffffffffu, w, i);
+    const float* op = a.o_part + pidx(i) * D + lane * kV;
+    float vals[kV];
+    if constexpr (kV == 4) {
+      const float4 x = *reinterpret_cast<const float4*>(op);
+      vals[0] = x.x; vals[1] = x.y; vals[2 % kV] = x.z; vals[3 % kV] = x.w;
+    } else {
+      const float2 x = *reinterpret_cast<const float2*>(op);
+      vals[0] = x.x; vals[1 % kV] = x.y;
+    }
+#pragma unroll
+    for (int v = 0; v < kV; ++v) acc[v] += wi * vals[v];
+  }
+  const float inv = W > 0.f ? 1.f / W : 0.f;
+  __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + (int64_t(uq.y + t) * a.Hq + hq_s[s]) * D + lane * kV;
+  if constexpr (kV == 4) {
+    uint2 v;
+    v.x = pack_bf16(acc[0] * inv, acc[1] * inv);
+    v.y = pack_bf16(acc[2 % kV] * inv, acc[3 % kV] * inv);
+    *reinterpret_cast<uint2*>(orow) = v;
+  } else {
+    *reinterpret_cast<uint32_t*>(orow) = pack_bf16(acc[0] * inv, acc[1 % kV] * inv);
+  }
+}
+
 template <int D>
 cudaError_t launch_prefill_d(const CUtensorMap& tm_q, const CUtensorMap& tm_k, const CUtensorMap& tm_v,
-                             const PrefillArgs& a, cudaStream_t s, int* launches) {
+                             const CUtensorMap& tm_o, const CUtensorMap& tm_op, const PrefillArgs& a, cudaStream_t s,
+                             int* launches) {
   const int mtiles = (a.max_q_len + kBM - 1) / kBM;
   ++*launches;
   if (HPA_PF1 && HPA_PF1_CLUSTER && (a.G & 1) == 0) {
@@ -1172,16 +1381,28 @@ cudaError_t launch_prefill_d(const CUtensorMap& tm_q, const CUtensorMap& tm_k, c
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, prefill_kernel<D, true>, tm_q, tm_k, tm_v, a);
+    return cudaLaunchKernelEx(&cfg, prefill_kernel<D, true>, tm_q, tm_k, tm_v, tm_o, tm_op, a);
+  }
+  if (!HPA_PF1 && a.work) {  // split-KV work list: one CTA per (unit, piece), then the merge
+    if (a.n_work == 0) return cudaSuccess;
+    cudaError_t e = launch_pdl(prefill_kernel<D, false>, dim3(unsigned(a.n_work)), dim3(kThreads), PSmem<D>::kBytes,
+                               s, tm_q, tm_k, tm_v, tm_o, tm_op, a);
+    if (e != cudaSuccess || a.n_parts == 0) return e;
+    ++*launches;
+    const int64_t rows = int64_t(a.n_parts) * 2 * kBM;
+    return launch_pdl(prefill_combine_kernel<D>, dim3(unsigned((rows + 3) / 4)), dim3(128), 0, s, a);
   }
   dim3 grid;
   if (HPA_PF1) grid = dim3(mtiles, a.Hq, a.n_seqs);
   else if ((a.G & 1) == 0) grid = dim3(mtiles, a.Hkv * (a.G / 2), a.n_seqs);
   else grid = dim3((mtiles + 1) / 2, a.Hq, a.n_seqs);
-  return launch_pdl(prefill_kernel<D, false>, grid, dim3(kThreads), PSmem<D>::kBytes, s, tm_q, tm_k, tm_v, a);
+  return launch_pdl(prefill_kernel<D, false>, grid, dim3(kThreads), PSmem<D>::kBytes, s, tm_q, tm_k, tm_v, tm_o,
+                    tm_op, a);
 }
 
 }  // namespace
+
+bool prefill_split_supported() { return !HPA_PF1 && !HPA_SM16; }
 
 cudaError_t prefill_init_attributes() {
   cudaError_t e;
@@ -1201,10 +1422,11 @@ cudaError_t prefill_init_attributes() {
 }
 
 cudaError_t launch_prefill(const CUtensorMap& tm_q, const CUtensorMap& tm_k, const CUtensorMap& tm_v,
-                           const PrefillArgs& a, int32_t D, cudaStream_t s, int* launches) {
+                           const CUtensorMap& tm_o, const CUtensorMap& tm_op, const PrefillArgs& a, int32_t D,
+                           cudaStream_t s, int* launches) {
   if (a.n_seqs == 0) return cudaSuccess;
-  if (D == 128) return launch_prefill_d<128>(tm_q, tm_k, tm_v, a, s, launches);
-  if (D == 64) return launch_prefill_d<64>(tm_q, tm_k, tm_v, a, s, launches);
+  if (D == 128) return launch_prefill_d<128>(tm_q, tm_k, tm_v, tm_o, tm_op, a, s, launches);
+  if (D == 64) return launch_prefill_d<64>(tm_q, tm_k, tm_v, tm_o, tm_op, a, s, launches);
   return cudaErrorInvalidValue;
 }
 

@@ -28,6 +28,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <deque>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -132,6 +133,19 @@ bool make_map_dec(CUtensorMap* m, void* base, uint64_t rows, uint64_t cols) {
   cuuint32_t estr[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 2-D fp32 map over a [rows][cols] workspace: box {32, 128} (128-B rows), 128-B swizzle.
+bool make_map_f32(CUtensorMap* m, void* base, uint64_t rows, uint64_t cols) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 4};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
 }
 
 // 3-D bf16 map over q [tokens][Hq][d]: box {64, 1, box_tok}, 128-B swizzle.
@@ -297,6 +311,13 @@ struct Blob {
 
 }  // namespace
 
+// Split-KV prefill work list (plan_prefill).
+struct PfPlan {
+  std::vector<int4> work;   // 4 per CTA (PrefillArgs::work)
+  std::vector<int4> parts;  // 2 per split unit: {b, y, x, nsplit}, {q_len, q_off, 0, 0}
+  int32_t split_max = 1;
+};
+
 struct hpa_cache {
   hpa_config_t cfg{};
   PageAllocator alloc;
@@ -316,6 +337,7 @@ struct hpa_cache {
   int32_t* arena = nullptr;
   DevTables dt{};
   CUtensorMap tm_k_dec{}, tm_v_dec{}, tm_k_pre{}, tm_v_pre{};
+  CUtensorMap tm_opart{};  // fp32 map over pf_o_part (split-KV prefill workspace)
   StagingRing ring;
   std::vector<WordWrite> pending;  // device table writes not yet shipped
   // decode batch cache
@@ -334,6 +356,15 @@ struct hpa_cache {
   size_t units_cap = 0, nsplit_cap = 0;
   int32_t plan_units = 0, plan_smax = 1;
   int32_t forced_splits = 0;
+  // split-KV prefill: forced split count (0 = planner) and the partial workspace
+  int32_t pf_forced_splits = 0;
+  uint64_t table_version = 0;    // bumped by every block-table rebuild
+  std::vector<int32_t> pf_key;   // last prefill plan's inputs (version, forced, batch, q_lens, span)
+  PfPlan pf_plan;
+  bool pf_listed = false;
+  float* pf_o_part = nullptr;
+  float* pf_lse_part = nullptr;
+  size_t pf_part_rows = 0;
   // host-staged installs (NEXT-3): device payload buffer filled on copy_stream
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t copy_done = nullptr, payload_free = nullptr;
@@ -360,6 +391,7 @@ struct hpa_cache {
   // may be partial, so the pages before `from_entry` inside its segment are full)
   // and queues device writes for the fields that changed. O(changed entries).
   void rebuild(int32_t s, int32_t from_entry) {
+    ++table_version;
     Seq& q = seqs[s];
     const int32_t P = cfg.page_size;
     const int32_t old_n = int32_t(q.pages.size());
@@ -590,6 +622,140 @@ int32_t plan_request_splits(const hpa_cache_t* c, int32_t n, const int32_t* seq_
   return smax;
 }
 
+// Split-KV prefill plan. The prefill kernel owns all 512 TMEM columns, so one CTA runs per SM
+// and U units (two 128-row query tiles sharing K/V) take ceil(U / W) waves of about equal
+// length: B = 1 of configs[2] is 256 units on 148 SMs, 1.73 waves of work in 2 waves. The
+// plan puts the units longest first and splits the shortest ones -- those of the under-filled
+// last wave, optionally one more wave's worth -- into s key ranges whose pieces fill the SMs;
+// each split unit's pieces are merged by LSE (prefill_combine_kernel). Chosen by a greedy
+// list-scheduling simulation of the hardware's in-order CTA dispatch, in key tiles:
+//   unit = tiles(i_max) + o,  piece = tiles / s + o,  merge = c_m + partial bytes / bandwidth.
+
+// Greedy in-order dispatch onto W SMs (min-heap of the times the SMs become free): `items`
+// are appended to the state `heap` (W entries); returns the makespan of the state.
+double list_schedule(std::vector<double>& heap, const double* items, size_t n) {
+  auto gt = std::greater<double>();
+  for (size_t k = 0; k < n; ++k) {
+    std::pop_heap(heap.begin(), heap.end(), gt);
+    heap.back() += items[k];
+    std::push_heap(heap.begin(), heap.end(), gt);
+  }
+  return *std::max_element(heap.begin(), heap.end());
+}
+
+// Key-tile iterations of every unit, computed here from the host mirror of the table exactly
+// as the kernel would (so the kernel needs no table search before its pipeline starts):
+// n = slot(i_max) / 128 + 1 tiles, minus the tiles wholly inside the GRC span when every
+// query row of the unit is a span row. Returns false when the legacy grid (no work list) is
+// used (HPA_PF1 / HPA_SM16 builds, or splits forced to 1 with HPA_PF_GRID=1).
+bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, const int32_t* q_lens,
+                  const int32_t* q_off, const int32_t* span, PfPlan& plan) {
+  const int32_t forced = c->pf_forced_splits;
+  static const bool grid_only = std::getenv("HPA_PF_GRID") && std::atoi(std::getenv("HPA_PF_GRID")) != 0;
+  if (grid_only || !prefill_split_supported()) return false;
+  const int32_t Hq = c->cfg.num_q_heads, Hkv = c->cfg.num_kv_heads, G = Hq / Hkv;
+  const int32_t lp = __builtin_ctz(uint32_t(c->cfg.page_size));
+  const int32_t Y = (G & 1) == 0 ? Hkv * (G / 2) : Hq;
+  struct U { int32_t b, x, n, skip_a, n_skip; };
+  std::vector<U> rows;  // one per (sequence, row-tile index); the Y head units share it
+  for (int32_t i = 0; i < n_seqs; ++i) {
+    const Seq& q = c->seqs[seq_ids[i]];
+    const int32_t ql = q_lens[i], mt = (ql + 127) / 128, X = (G & 1) == 0 ? mt : (mt + 1) / 2;
+    const int32_t ne = int32_t(q.pages.size());
+    auto slot_of = [&](int32_t x) {
+      const int32_t e = std::max<int32_t>(
+          0, int32_t(std::upper_bound(q.pos0.begin(), q.pos0.begin() + ne, x) - q.pos0.begin()) - 1);
+      return (int64_t(e) << lp) + (x - q.pos0[size_t(e)]);
+    };
+    const int32_t q_base = q.len - ql;
+    for (int32_t x = 0; x < X; ++x) {
+      const int32_t first_mt = (G & 1) == 0 ? x : 2 * x;
+      const int32_t last_mt = (G & 1) == 0 ? x : std::min(2 * x + 1, mt - 1);
+      const int32_t i_min = q_base + first_mt * 128;
+      const int32_t i_max = q_base + std::min(ql, (last_mt + 1) * 128) - 1;
+      const int32_t total = int32_t(slot_of(i_max) / 128 + 1);
+      int32_t skip_a = 0, skip_b = 0;
+      if (span && i_min >= span[3 * i + 2] && span[3 * i + 1] > span[3 * i]) {
+        skip_a = int32_t((slot_of(span[3 * i]) + 127) / 128);
+        skip_b = int32_t((slot_of(span[3 * i + 1] - 1) + 1) / 128);
+        if (skip_b < skip_a) skip_b = skip_a;
+      }
+      rows.push_back({i, x, total - (skip_b - skip_a), skip_a, skip_b - skip_a});
+    }
+  }
+  const int64_t nU = int64_t(rows.size()) * Y;
+  const int32_t W = c->num_sms;
+  // units longest first (the hardware dispatches CTAs in order); (b, x) rows sorted, heads inner
+  std::stable_sort(rows.begin(), rows.end(), [](const U& a, const U& b) { return a.n > b.n; });
+  auto unit = [&](int64_t k) -> const U& { return rows[size_t(k / Y)]; };
+  int64_t best_tail = 0;
+  int32_t best_s = 1;
+  if (forced > 1) {
+    best_tail = nU;
+    best_s = forced;
+  } else if (forced == 0 && nU < int64_t(16) * W) {  // beyond 16 waves the tail loss is < 1/16
+    // measured per-CTA fixed cost (scripts/trace_prefill_ctas.py: setup, pipeline fill, epilogue,
+    // CTA switch) ~6.6 us = 3.3 key tiles; a split piece's fp32 epilogue adds ~1.4 us
+    static const double o = std::getenv("HPA_PF_OVH") ? std::atof(std::getenv("HPA_PF_OVH")) : 3.3;
+    const double o_piece = o + 0.7;
+    static const double c_m = std::getenv("HPA_PF_MERGE") ? std::atof(std::getenv("HPA_PF_MERGE")) : 2.0;
+    const double tile_us = 1.95 * c->cfg.head_dim / 128.0;
+    const double part_tiles = 2.0 * 128 * c->cfg.head_dim * 4 / 5e6 / tile_us;  // one piece's partial read
+    std::vector<double> items(static_cast<size_t>(nU)), base(static_cast<size_t>(W), 0.0), heap, pieces;
+    for (int64_t k = 0; k < nU; ++k) items[size_t(k)] = unit(k).n + o;
+    heap = base;
+    const double t0 = list_schedule(heap, items.data(), items.size());
+    double best = t0;
+    const int64_t R = nU % W;
+    for (int64_t tail : {R, R + W}) {
+      if (tail <= 0 || tail > nU) continue;
+      std::vector<double> head = base;  // the unsplit units, longest first
+      list_schedule(head, items.data(), size_t(nU - tail));
+      for (int32_t s : {2, 3, 4, 6, 8}) {
+        pieces.clear();
+        for (int64_t k = nU - tail; k < nU; ++k)
+          for (int32_t p = 0; p < s; ++p) pieces.push_back(double(unit(k).n) / s + o_piece);
+        heap = head;
+        const double t = list_schedule(heap, pieces.data(), pieces.size()) + c_m + double(tail) * s * part_tiles / W;
+        if (t < best && t < 0.98 * t0) {
+          best = t;
+          best_tail = tail;
+          best_s = s;
+        }
+      }
+    }
+  }
+  plan.work.clear();
+  plan.parts.clear();
+  plan.split_max = best_s;
+  plan.work.reserve(size_t(4 * (nU + best_tail * (best_s - 1))));
+  for (int64_t k = 0; k < nU; ++k) {
+    const U& u = unit(k);
+    const int32_t y = int32_t(k % Y);
+    const Seq& q = c->seqs[seq_ids[u.b]];
+    const int4 wq = make_int4(seq_ids[u.b], q_lens[u.b], q_off[u.b], q.len);
+    const int4 wn = make_int4(int32_t(q.pages.size()), 0, 0, 0);
+    if (k < nU - best_tail) {
+      plan.work.push_back(make_int4(u.b, y, u.x, 0 | (1 << 4)));
+      plan.work.push_back(make_int4(0, u.n, u.skip_a, u.n_skip));
+      plan.work.push_back(wq);
+      plan.work.push_back(wn);
+      continue;
+    }
+    const int32_t part = int32_t(plan.parts.size() / 2);
+    plan.parts.push_back(make_int4(u.b, y, u.x, best_s));
+    plan.parts.push_back(make_int4(q_lens[u.b], q_off[u.b], 0, 0));
+    for (int32_t p = 0; p < best_s; ++p) {
+      const int32_t jb = int32_t(int64_t(u.n) * p / best_s), je = int32_t(int64_t(u.n) * (p + 1) / best_s);
+      plan.work.push_back(make_int4(u.b, y, u.x, p | (best_s << 4) | (part << 8)));
+      plan.work.push_back(make_int4(jb, je - jb, u.skip_a, u.n_skip));
+      plan.work.push_back(wq);
+      plan.work.push_back(wn);
+    }
+  }
+  return true;
+}
+
 // Pages needed to append n rows to seq q.
 int32_t pages_for_append(const hpa_cache_t* c, const Seq& q, int32_t n) {
   if (n <= 0) return 0;
@@ -754,6 +920,8 @@ hpa_status_t hpa_cache_destroy(hpa_cache_t* c) {
   if (c->batch_dev) cudaFree(c->batch_dev);
   if (c->o_part) cudaFree(c->o_part);
   if (c->lse_part) cudaFree(c->lse_part);
+  if (c->pf_o_part) cudaFree(c->pf_o_part);
+  if (c->pf_lse_part) cudaFree(c->pf_lse_part);
   if (c->counters) cudaFree(c->counters);
   if (c->units_dev) cudaFree(c->units_dev);
   if (c->nsplit_dev) cudaFree(c->nsplit_dev);
@@ -1383,22 +1551,66 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
       if (hpa_status_t st = ship(c, s, recs, dst, nrows, &gl)) return st;
     }
   }
-  const size_t bytes = meta.size() * 4;
-  const size_t off = c->ring.reserve(bytes);
-  std::memcpy(c->ring.host(off), meta.data(), bytes);
-  HPA_CUDA(c->ring.upload(off, bytes, s));
-  const int32_t* dmeta = reinterpret_cast<const int32_t*>(c->ring.dev(off));
   const int32_t D = c->cfg.head_dim, Hq = c->cfg.num_q_heads;
-  CUtensorMap tm_q;
-  if (!make_map_q(&tm_q, q, uint64_t(total_q), uint64_t(Hq), uint64_t(D), 128))
-    return fail(HPA_ERR_CUDA, "cuTensorMapEncodeTiled failed for q");
+  // work list (plan_prefill) + per-sequence metadata in one staged upload
+  // the plan depends only on the tables, the batch and the split setting: reuse it when those
+  // are unchanged since the last call (repeated chunks over a fixed batch skip the simulation)
+  std::vector<int32_t> key{int32_t(c->table_version), int32_t(c->table_version >> 32), c->pf_forced_splits, n_seqs,
+                           span ? 1 : 0};
+  key.insert(key.end(), seq_ids, seq_ids + n_seqs);
+  key.insert(key.end(), q_lens, q_lens + n_seqs);
+  if (span) key.insert(key.end(), span, span + 3 * size_t(n_seqs));
+  if (key != c->pf_key) {
+    c->pf_listed = plan_prefill(c, n_seqs, seq_ids, q_lens, meta.data() + 2 * n_seqs, span, c->pf_plan);
+    c->pf_key.swap(key);
+  }
+  const PfPlan& plan = c->pf_plan;
+  const bool listed = c->pf_listed;
+  const size_t wbytes = listed ? (plan.work.size() + plan.parts.size()) * sizeof(int4) : 0;
+  const size_t bytes = wbytes + meta.size() * 4;
+  const size_t off = c->ring.reserve(bytes);
+  if (listed) {
+    std::memcpy(c->ring.host(off), plan.work.data(), plan.work.size() * sizeof(int4));
+    std::memcpy(c->ring.host(off) + plan.work.size() * sizeof(int4), plan.parts.data(),
+                plan.parts.size() * sizeof(int4));
+  }
+  std::memcpy(c->ring.host(off) + wbytes, meta.data(), meta.size() * 4);
+  HPA_CUDA(c->ring.upload(off, bytes, s));
+  const int32_t* dmeta = reinterpret_cast<const int32_t*>(c->ring.dev(off) + wbytes);
+  CUtensorMap tm_q, tm_o;
+  if (!make_map_q(&tm_q, q, uint64_t(total_q), uint64_t(Hq), uint64_t(D), 128) ||
+      !make_map_q(&tm_o, out, uint64_t(total_q), uint64_t(Hq), uint64_t(D), 128))
+    return fail(HPA_ERR_CUDA, "cuTensorMapEncodeTiled failed for q / out");
   const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt(float(D));
   PrefillArgs a{c->dt, dmeta, dmeta + n_seqs, dmeta + 2 * n_seqs, out, n_seqs, Hq, c->cfg.num_kv_heads,
                 Hq / c->cfg.num_kv_heads, c->cfg.page_size, c->cfg.num_pages, layer, max_q,
                 scale * 1.4426950408889634f, __builtin_ctz(uint32_t(c->cfg.page_size)),
-                span ? dmeta + 3 * n_seqs : nullptr, c->trace};
+                span ? dmeta + 3 * n_seqs : nullptr, c->trace, nullptr, 0, nullptr, 0, 1, nullptr, nullptr};
+  if (listed) {
+    const size_t rows = plan.parts.size() / 2 * size_t(plan.split_max) * 2 * 128;
+    if (rows > c->pf_part_rows) {  // split workspace (grown on demand) and its fp32 TMA map
+      if (c->pf_o_part) cudaFree(c->pf_o_part);
+      if (c->pf_lse_part) cudaFree(c->pf_lse_part);
+      c->pf_o_part = nullptr;
+      c->pf_lse_part = nullptr;
+      c->pf_part_rows = 0;
+      HPA_CUDA(cudaMalloc(&c->pf_o_part, rows * D * 4));
+      HPA_CUDA(cudaMalloc(&c->pf_lse_part, rows * 4));
+      if (!make_map_f32(&c->tm_opart, c->pf_o_part, rows, uint64_t(D)))
+        return fail(HPA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the prefill workspace");
+      c->pf_part_rows = rows;
+    }
+    const int4* dwork = reinterpret_cast<const int4*>(c->ring.dev(off));
+    a.work = dwork;
+    a.n_work = int32_t(plan.work.size() / 4);
+    a.parts = dwork + plan.work.size();
+    a.n_parts = int32_t(plan.parts.size() / 2);
+    a.split_max = plan.split_max;
+    a.o_part = c->pf_o_part;
+    a.lse_part = c->pf_lse_part;
+  }
   int launched = 0;
-  cudaError_t e = launch_prefill(tm_q, c->tm_k_pre, c->tm_v_pre, a, D, s, &launched);
+  cudaError_t e = launch_prefill(tm_q, c->tm_k_pre, c->tm_v_pre, tm_o, c->tm_opart, a, D, s, &launched);
   c->launches += launched;
   if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
   HPA_CUDA(c->ring.commit(off, bytes, s));
@@ -1452,6 +1664,13 @@ hpa_status_t hpa_export_table(hpa_cache_t* c, int32_t seq_id, int32_t* pages, in
     if (meta)
       meta[e] = uint16_t((q.meta[e] & kMetaRowsMask) | ((q.meta[e] & kMetaLatent) ? 0x8000 : 0));
   }
+  return HPA_OK;
+}
+
+hpa_status_t hpa_set_prefill_splits(hpa_cache_t* c, int32_t splits) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (splits < 0 || splits > 15) return fail(HPA_ERR_INVALID_ARG, "prefill splits %d outside [0, 15]", splits);
+  c->pf_forced_splits = splits;
   return HPA_OK;
 }
 

@@ -1,0 +1,103 @@
+"""Split-KV chunked prefill (SURVEY §8(a) a6 with the a5 LSE merge): units of an under-filled
+last wave run as several key ranges whose partial (O / l, LSE) results are merged.
+
+Parity with the fp64 oracle for forced split counts (including more pieces than key tiles,
+i.e. empty pieces), the GRC span mask, ragged query lengths, G odd, D = 64, and the planner's
+own choice at configs[2] B = 1 (the case it exists for)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import attend, attend_span
+from tests.hpa_testutil import Pair, check_close, f64
+from workloads import Shape
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_prefill(pair, seqs, q_lens, q):
+    out, off = [], 0
+    for s, n in zip(seqs, q_lens):
+        k, v = pair.orc.logical_kv(s, 0)
+        out.append(attend(f64(q[off:off + n]), k, v, pair.shape.scale))
+        off += n
+    return np.concatenate(out)
+
+
+@pytest.mark.parametrize("hq,hkv,d,P", [(32, 8, 128, 16), (6, 2, 64, 32), (16, 1, 128, 64), (4, 4, 128, 256)])
+@pytest.mark.parametrize("splits", [2, 3, 8, 15])
+def test_prefill_forced_splits_parity(hq, hkv, d, P, splits):
+    shape = Shape(1, hq, hkv, d, P)
+    p = Pair(shape, num_pages=4096, max_seqs=4, max_pages_per_seq=1024)
+    scripts = [[("latent", 128), ("latent", 8), ("tokens", 700)],
+               [("tokens", 77)],                                   # 1 key tile: pieces >= 1 empty
+               [("latent", 128)] * 2 + [("tokens", 1500)]]
+    seqs = [p.build(sc) for sc in scripts]
+    q_lens = [300, 1, 385]
+    q = p.queries(sum(q_lens))
+    ref = _oracle_prefill(p, seqs, q_lens, q)
+    p.cache.set_prefill_splits(splits)
+    got = p.cache.prefill(0, seqs, q_lens, q.cuda())
+    torch.cuda.synchronize()
+    check_close(got, ref, f"prefill split {splits} {hq}/{hkv}/{d}/P{P}")
+    # the unsplit kernel on the same data agrees to bf16 output rounding
+    p.cache.set_prefill_splits(1)
+    one = p.cache.prefill(0, seqs, q_lens, q.cuda())
+    torch.cuda.synchronize()
+    assert torch.max(torch.abs(one.float() - got.float())).item() <= 1.6e-2
+
+
+@pytest.mark.parametrize("splits", [0, 4])
+def test_prefill_split_with_span(splits):
+    """Pieces that lie entirely inside the GRC mask-out span leave span rows with nothing
+    visible (LSE = -inf); the merge must weight them 0."""
+    shape = Shape(1, 32, 8, 128, 16)
+    p = Pair(shape, num_pages=2048, max_seqs=8, max_pages_per_seq=256)
+    cases = [(900, 16, 150), (40, 128, 200), (257, 64, 1)]
+    seqs, q_lens, spans = [], [], []
+    for n1, m, n3 in cases:
+        s = p.new_seq()
+        p.tokens([s], [n1])
+        p.latent(s, m)
+        p.tokens([s], [n3])
+        seqs.append(s)
+        q_lens.append(m + n3)
+        spans.append((0, n1, n1 + m))
+    q = p.queries(sum(q_lens))
+    p.cache.set_prefill_splits(splits)
+    got = p.cache.prefill_span(0, seqs, q_lens, spans, q.cuda())
+    torch.cuda.synchronize()
+    ref, off = [], 0
+    for s, ql, (lo, hi, qf) in zip(seqs, q_lens, spans):
+        k, v = p.orc.logical_kv(s, 0)
+        ref.append(attend_span(f64(q[off:off + ql]), k, v, shape.scale, lo, hi, qf))
+        off += ql
+    check_close(got, np.concatenate(ref), f"prefill span split {splits}")
+
+
+def test_prefill_planner_small_batch_fills_sms():
+    """Planner (splits = 0) on a batch of fewer units than SMs: every unit is split; parity."""
+    shape = Shape(1, 8, 2, 128, 16)
+    p = Pair(shape, num_pages=4096, max_seqs=2, max_pages_per_seq=1024)
+    s = p.build([("latent", 128), ("tokens", 6000)])
+    q = p.queries(512)
+    p.cache.set_prefill_splits(1)
+    p.cache.prefill(0, [s], [512], q.cuda())          # ships pending table writes
+    before = p.cache.launch_count()
+    p.cache.prefill(0, [s], [512], q.cuda())
+    n_one = p.cache.launch_count() - before
+    p.cache.set_prefill_splits(0)
+    before = p.cache.launch_count()
+    got = p.cache.prefill(0, [s], [512], q.cuda())
+    torch.cuda.synchronize()
+    assert p.cache.launch_count() - before == n_one + 1, "split plan: prefill + merge kernels"
+    check_close(got, _oracle_prefill(p, [s], [512], q), "prefill planner small batch")
+
+
+def test_prefill_split_invalid_count():
+    shape = Shape(1, 8, 2, 128, 16)
+    p = Pair(shape, num_pages=64, max_seqs=2, max_pages_per_seq=16)
+    with pytest.raises(Exception):
+        p.cache.set_prefill_splits(16)
+    with pytest.raises(Exception):
+        p.cache.set_prefill_splits(-1)
