@@ -515,7 +515,7 @@ def traffic_from_profiles(kernel: str):
 
 
 def bench_prefill(torch, Cache, shape, dev, stream, pk, pk_kind, max_over_ranks, reps=5, token_kv_dtype="bf16",
-                  batches=(1, 4)):
+                  batches=(1, 4), windows=5):
     """configs[2]: C = 2048 new rows over 8 latent sets (1024 rows) + 16384 cached token rows.
     token_kv_dtype "fp8" (NEXT-4c): the token pages are fp8; each call first dequantizes
     them into temporary bf16 pages (included in the time)."""
@@ -529,23 +529,33 @@ def bench_prefill(torch, Cache, shape, dev, stream, pk, pk_kind, max_over_ranks,
         g = torch.Generator(device=f"cuda:{dev}").manual_seed(99)
         q = torch.randn((bp * c_rows, 32, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
         o = torch.empty_like(q)
-        for _ in range(2):
+        for _ in range(3):
             cache.prefill(0, seqs, [c_rows] * bp, q, o)
         torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(reps):
-            cache.prefill(0, seqs, [c_rows] * bp, q, o)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        ms = max_over_ranks(e0.elapsed_time(e1) / reps, device=f"cuda:{dev}")
+        # `windows` timed windows of `reps` calls each (the tensor-bound kernel runs into the
+        # board power cap within a few ms, so single windows scatter by ~10 %): median window
+        clk = ClockSampler(dev)
+        clk.start()
+        win = []
+        for _ in range(windows):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                cache.prefill(0, seqs, [c_rows] * bp, q, o)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            win.append(e0.elapsed_time(e1) / reps)
+        clk.stop()
+        ms = max_over_ranks(statistics.median(win), device=f"cuda:{dev}")
         flops = bp * prefill_flops(8 * 128 + prior_tok, c_rows, shape)
         tf = flops / (ms / 1e3) / 1e12
         out[f"B{bp}"] = {"ms": round(ms, 4), "tflops": round(tf, 1),
                          "frac": round(tf / pk["bf16_tflops"], 4), "peak": pk["bf16_tflops"],
                          "peak_kind": f"{pk_kind} bf16 dense (burst)",
                          "frac_vs_nominal_2250": round(tf / NOMINAL_BF16_TFLOPS, 4),
-                         "flops": flops}
+                         "flops": flops, "ms_windows": [round(w, 4) for w in win],
+                         "tflops_best_window": round(flops / (min(win) / 1e3) / 1e12, 1),
+                         "plan": cache.prefill_plan_info(), "clocks": clk.summary()}
         cache.close()
         del q, o
     out["workload"] = "configs[2] chunked prefill C=2048 over 1024 latent + 16384 cached token rows"

@@ -249,8 +249,13 @@ hpa_status_t hpa_export_table(hpa_cache_t* c, int32_t seq_id, int32_t* pages, in
 hpa_status_t hpa_set_decode_splits(hpa_cache_t* c, int32_t splits);
 /* Testing / tuning hook for hpa_prefill / hpa_prefill_span: 0 = planner (split-KV only for
  * the units of an under-filled last wave), 1 = never split, 2..15 = split every unit's key
- * tiles into that many pieces (merged by LSE). INVALID_ARG outside [0, 15]. */
+ * tiles into that many pieces (merged by LSE), 16 = no host work list (one CTA per unit of a
+ * grid; each CTA searches the block table for its key-tile range). INVALID_ARG outside [0, 16]. */
 hpa_status_t hpa_set_prefill_splits(hpa_cache_t* c, int32_t splits);
+/* Introspection of the last hpa_prefill / hpa_prefill_span plan: *n_ctas prefill CTAs
+ * launched, *n_split_units units split into *splits key ranges each (0 / 1 when none), or
+ * *n_ctas = 0 when the grid path ran. Any output pointer may be NULL. */
+hpa_status_t hpa_prefill_plan_info(hpa_cache_t* c, int32_t* n_ctas, int32_t* n_split_units, int32_t* splits);
 /* Number of kernels this cache has launched so far (bench "gpu_launches"). */
 hpa_status_t hpa_launch_count(hpa_cache_t* c, uint64_t* n);
 

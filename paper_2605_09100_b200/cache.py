@@ -319,8 +319,15 @@ class Cache:
         check(LIB.hpa_set_decode_splits(self._h, splits))
 
     def set_prefill_splits(self, splits: int) -> None:
-        """0 = planner, 1 = never split, 2..15 = every unit split into that many key ranges."""
+        """0 = planner, 1 = never split, 2..15 = every unit split into that many key ranges,
+        16 = the grid kernel without a host work list."""
         check(LIB.hpa_set_prefill_splits(self._h, splits))
+
+    def prefill_plan_info(self) -> dict:
+        """The last prefill's plan: CTAs launched, units split, key ranges per split unit."""
+        n, u, s = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        check(LIB.hpa_prefill_plan_info(self._h, ctypes.byref(n), ctypes.byref(u), ctypes.byref(s)))
+        return {"ctas": n.value, "split_units": u.value, "splits": s.value}
 
     def launch_count(self) -> int:
         n = ctypes.c_uint64()

@@ -625,8 +625,9 @@ int32_t plan_request_splits(const hpa_cache_t* c, int32_t n, const int32_t* seq_
 // Split-KV prefill plan. The prefill kernel owns all 512 TMEM columns, so one CTA runs per SM
 // and U units (two 128-row query tiles sharing K/V) take ceil(U / W) waves of about equal
 // length: B = 1 of configs[2] is 256 units on 148 SMs, 1.73 waves of work in 2 waves. The
-// plan puts the units longest first and splits the shortest ones -- those of the under-filled
-// last wave, optionally one more wave's worth -- into s key ranges whose pieces fill the SMs;
+// plan keeps the L2-friendly dispatch order and splits the units dispatched last -- those of
+// the under-filled last wave, optionally one more wave's worth -- into s key ranges whose
+// pieces fill the SMs;
 // each split unit's pieces are merged by LSE (prefill_combine_kernel). Chosen by a greedy
 // list-scheduling simulation of the hardware's in-order CTA dispatch, in key tiles:
 //   unit = tiles(i_max) + o,  piece = tiles / s + o,  merge = c_m + partial bytes / bandwidth.
@@ -647,12 +648,11 @@ double list_schedule(std::vector<double>& heap, const double* items, size_t n) {
 // as the kernel would (so the kernel needs no table search before its pipeline starts):
 // n = slot(i_max) / 128 + 1 tiles, minus the tiles wholly inside the GRC span when every
 // query row of the unit is a span row. Returns false when the legacy grid (no work list) is
-// used (HPA_PF1 / HPA_SM16 builds, or splits forced to 1 with HPA_PF_GRID=1).
+// used (HPA_PF1 / HPA_SM16 builds, or hpa_set_prefill_splits(c, 16)).
 bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, const int32_t* q_lens,
                   const int32_t* q_off, const int32_t* span, PfPlan& plan) {
   const int32_t forced = c->pf_forced_splits;
-  static const bool grid_only = std::getenv("HPA_PF_GRID") && std::atoi(std::getenv("HPA_PF_GRID")) != 0;
-  if (grid_only || !prefill_split_supported()) return false;
+  if (forced == 16 || !prefill_split_supported()) return false;
   const int32_t Hq = c->cfg.num_q_heads, Hkv = c->cfg.num_kv_heads, G = Hq / Hkv;
   const int32_t lp = __builtin_ctz(uint32_t(c->cfg.page_size));
   const int32_t Y = (G & 1) == 0 ? Hkv * (G / 2) : Hq;
@@ -683,11 +683,22 @@ bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, 
       rows.push_back({i, x, total - (skip_b - skip_a), skip_a, skip_b - skip_a});
     }
   }
+  // Dispatch order (the hardware starts CTAs in order): sequence, then head index y, then row
+  // tile x fastest -- the CTAs running at the same time then share K/V tiles in L2 (all row
+  // tiles of one KV head read the same keys). Ordering units by length instead scattered a
+  // wave over every (sequence, KV head) and re-read K/V from HBM (-4 % at configs[2] B = 4).
   const int64_t nU = int64_t(rows.size()) * Y;
   const int32_t W = c->num_sms;
-  // units longest first (the hardware dispatches CTAs in order); (b, x) rows sorted, heads inner
-  std::stable_sort(rows.begin(), rows.end(), [](const U& a, const U& b) { return a.n > b.n; });
-  auto unit = [&](int64_t k) -> const U& { return rows[size_t(k / Y)]; };
+  std::vector<std::pair<int32_t, int32_t>> order;  // (row index, y)
+  order.reserve(size_t(nU));
+  for (size_t r0 = 0; r0 < rows.size();) {
+    size_t r1 = r0;
+    while (r1 < rows.size() && rows[r1].b == rows[r0].b) ++r1;
+    for (int32_t y = 0; y < Y; ++y)
+      for (size_t r = r0; r < r1; ++r) order.push_back({int32_t(r), y});
+    r0 = r1;
+  }
+  auto unit = [&](int64_t k) -> const U& { return rows[size_t(order[size_t(k)].first)]; };
   int64_t best_tail = 0;
   int32_t best_s = 1;
   if (forced > 1) {
@@ -709,7 +720,7 @@ bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, 
     const int64_t R = nU % W;
     for (int64_t tail : {R, R + W}) {
       if (tail <= 0 || tail > nU) continue;
-      std::vector<double> head = base;  // the unsplit units, longest first
+      std::vector<double> head = base;  // the unsplit units
       list_schedule(head, items.data(), size_t(nU - tail));
       for (int32_t s : {2, 3, 4, 6, 8}) {
         pieces.clear();
@@ -731,7 +742,7 @@ bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, 
   plan.work.reserve(size_t(4 * (nU + best_tail * (best_s - 1))));
   for (int64_t k = 0; k < nU; ++k) {
     const U& u = unit(k);
-    const int32_t y = int32_t(k % Y);
+    const int32_t y = order[size_t(k)].second;
     const Seq& q = c->seqs[seq_ids[u.b]];
     const int4 wq = make_int4(seq_ids[u.b], q_lens[u.b], q_off[u.b], q.len);
     const int4 wn = make_int4(int32_t(q.pages.size()), 0, 0, 0);
@@ -1667,9 +1678,18 @@ hpa_status_t hpa_export_table(hpa_cache_t* c, int32_t seq_id, int32_t* pages, in
   return HPA_OK;
 }
 
+hpa_status_t hpa_prefill_plan_info(hpa_cache_t* c, int32_t* n_ctas, int32_t* n_split_units, int32_t* splits) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  const bool l = c->pf_listed;
+  if (n_ctas) *n_ctas = l ? int32_t(c->pf_plan.work.size() / 4) : 0;
+  if (n_split_units) *n_split_units = l ? int32_t(c->pf_plan.parts.size() / 2) : 0;
+  if (splits) *splits = l ? c->pf_plan.split_max : 1;
+  return HPA_OK;
+}
+
 hpa_status_t hpa_set_prefill_splits(hpa_cache_t* c, int32_t splits) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
-  if (splits < 0 || splits > 15) return fail(HPA_ERR_INVALID_ARG, "prefill splits %d outside [0, 15]", splits);
+  if (splits < 0 || splits > 16) return fail(HPA_ERR_INVALID_ARG, "prefill splits %d outside [0, 16]", splits);
   c->pf_forced_splits = splits;
   return HPA_OK;
 }

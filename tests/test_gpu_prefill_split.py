@@ -25,7 +25,7 @@ def _oracle_prefill(pair, seqs, q_lens, q):
 
 
 @pytest.mark.parametrize("hq,hkv,d,P", [(32, 8, 128, 16), (6, 2, 64, 32), (16, 1, 128, 64), (4, 4, 128, 256)])
-@pytest.mark.parametrize("splits", [2, 3, 8, 15])
+@pytest.mark.parametrize("splits", [2, 3, 8, 15, 16])
 def test_prefill_forced_splits_parity(hq, hkv, d, P, splits):
     shape = Shape(1, hq, hkv, d, P)
     p = Pair(shape, num_pages=4096, max_seqs=4, max_pages_per_seq=1024)
@@ -91,6 +91,8 @@ def test_prefill_planner_small_batch_fills_sms():
     got = p.cache.prefill(0, [s], [512], q.cuda())
     torch.cuda.synchronize()
     assert p.cache.launch_count() - before == n_one + 1, "split plan: prefill + merge kernels"
+    info = p.cache.prefill_plan_info()
+    assert info["split_units"] == 16 and info["splits"] >= 2 and info["ctas"] == 16 * info["splits"], info
     check_close(got, _oracle_prefill(p, [s], [512], q), "prefill planner small batch")
 
 
@@ -98,6 +100,6 @@ def test_prefill_split_invalid_count():
     shape = Shape(1, 8, 2, 128, 16)
     p = Pair(shape, num_pages=64, max_seqs=2, max_pages_per_seq=16)
     with pytest.raises(Exception):
-        p.cache.set_prefill_splits(16)
+        p.cache.set_prefill_splits(17)
     with pytest.raises(Exception):
         p.cache.set_prefill_splits(-1)
