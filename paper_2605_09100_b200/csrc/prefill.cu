@@ -1307,11 +1307,14 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 // Split-KV merge (the LSE algebra of the decode combine, a5): one warp per (split unit, slot,
 // query row); lane l holds the LSE of piece l, every lane accumulates D/32 dims over the pieces.
 // out = sum_i 2^(lse_i - M) O_i / sum_i 2^(lse_i - M), bf16, into the caller's output rows.
-template <int D>
+// kS > 0: compiled for exactly kS pieces (the planner's counts), so every piece's loads are
+// issued before the first use; kS = 0: any count <= 15.
+template <int D, int kS>
 __global__ void __launch_bounds__(128) prefill_combine_kernel(const PrefillArgs a) {
   grid_dependency_wait();
   grid_launch_dependents();
   constexpr int kV = D / 32;
+  constexpr int kU = kS > 0 ? kS : 1;  // pieces held in registers at once
   const int lane = threadIdx.x & 31;
   const int64_t rid = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
   if (rid >= int64_t(a.n_parts) * 2 * kBM) return;
@@ -1321,9 +1324,24 @@ __global__ void __launch_bounds__(128) prefill_combine_kernel(const PrefillArgs 
   unit_slots(a.G, u.y, u.z, hq_s, mt_s);
   const int t = mt_s[s] * kBM + row;
   if (t >= uq.x) return;
-  const int S = u.w;
+  const int S = kS > 0 ? kS : u.w;
   auto pidx = [&](int i) { return (int64_t(part * a.split_max + i) * 2 + s) * kBM + row; };
+  auto load = [&](int i, float* v) {
+    const float* op = a.o_part + pidx(i) * D + lane * kV;
+    if constexpr (kV == 4) {
+      const float4 x = *reinterpret_cast<const float4*>(op);
+      v[0] = x.x; v[1] = x.y; v[2 % kV] = x.z; v[3 % kV] = x.w;
+    } else {
+      const float2 x = *reinterpret_cast<const float2*>(op);
+      v[0] = x.x; v[1 % kV] = x.y;
+    }
+  };
   const float l = lane < S ? a.lse_part[pidx(lane)] : -CUDART_INF_F;
+  float vals[kU][kV];
+  if constexpr (kS > 0) {
+#pragma unroll
+    for (int i = 0; i < kS; ++i) load(i, vals[i]);
+  }
   float M = l;
 #pragma unroll
   for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
@@ -1334,19 +1352,20 @@ __global__ void __launch_bounds__(128) prefill_combine_kernel(const PrefillArgs 
   float acc[kV];
 #pragma unroll
   for (int v = 0; v < kV; ++v) acc[v] = 0.f;
-  for (int i = 0; i < S; ++i) {
-    const float wi = __shfl_sync(0xffffffffu, w, i);
-    const float* op = a.o_part + pidx(i) * D + lane * kV;
-    float vals[kV];
-    if constexpr (kV == 4) {
-      const float4 x = *reinterpret_cast<const float4*>(op);
-      vals[0] = x.x; vals[1] = x.y; vals[2 % kV] = x.z; vals[3 % kV] = x.w;
-    } else {
-      const float2 x = *reinterpret_cast<const float2*>(op);
-      vals[0] = x.x; vals[1 % kV] = x.y;
-    }
+  if constexpr (kS > 0) {
 #pragma unroll
-    for (int v = 0; v < kV; ++v) acc[v] += wi * vals[v];
+    for (int i = 0; i < kS; ++i) {
+      const float wi = __shfl_sync(0xffffffffu, w, i);
+#pragma unroll
+      for (int v = 0; v < kV; ++v) acc[v] += wi * vals[i][v];
+    }
+  } else {
+    for (int i = 0; i < S; ++i) {
+      const float wi = __shfl_sync(0xffffffffu, w, i);
+      load(i, vals[0]);
+#pragma unroll
+      for (int v = 0; v < kV; ++v) acc[v] += wi * vals[0][v];
+    }
   }
   const float inv = W > 0.f ? 1.f / W : 0.f;
   __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + (int64_t(uq.y + t) * a.Hq + hq_s[s]) * D + lane * kV;
@@ -1357,6 +1376,19 @@ __global__ void __launch_bounds__(128) prefill_combine_kernel(const PrefillArgs 
     *reinterpret_cast<uint2*>(orow) = v;
   } else {
     *reinterpret_cast<uint32_t*>(orow) = pack_bf16(acc[0] * inv, acc[1 % kV] * inv);
+  }
+}
+
+template <int D>
+cudaError_t launch_combine_d(const PrefillArgs& a, cudaStream_t s) {
+  const dim3 grid(unsigned((int64_t(a.n_parts) * 2 * kBM + 3) / 4));
+  switch (a.split_max) {  // every split unit of a plan has split_max pieces
+    case 2: return launch_pdl(prefill_combine_kernel<D, 2>, grid, dim3(128), 0, s, a);
+    case 3: return launch_pdl(prefill_combine_kernel<D, 3>, grid, dim3(128), 0, s, a);
+    case 4: return launch_pdl(prefill_combine_kernel<D, 4>, grid, dim3(128), 0, s, a);
+    case 6: return launch_pdl(prefill_combine_kernel<D, 6>, grid, dim3(128), 0, s, a);
+    case 8: return launch_pdl(prefill_combine_kernel<D, 8>, grid, dim3(128), 0, s, a);
+    default: return launch_pdl(prefill_combine_kernel<D, 0>, grid, dim3(128), 0, s, a);
   }
 }
 
@@ -1389,8 +1421,7 @@ cudaError_t launch_prefill_d(const CUtensorMap& tm_q, const CUtensorMap& tm_k, c
                                s, tm_q, tm_k, tm_v, tm_o, tm_op, a);
     if (e != cudaSuccess || a.n_parts == 0) return e;
     ++*launches;
-    const int64_t rows = int64_t(a.n_parts) * 2 * kBM;
-    return launch_pdl(prefill_combine_kernel<D>, dim3(unsigned((rows + 3) / 4)), dim3(128), 0, s, a);
+    return launch_combine_d<D>(a, s);
   }
   dim3 grid;
   if (HPA_PF1) grid = dim3(mtiles, a.Hq, a.n_seqs);
