@@ -323,6 +323,10 @@ class Cache:
         16 = the grid kernel without a host work list."""
         check(LIB.hpa_set_prefill_splits(self._h, splits))
 
+    def set_prefill_ctas(self, n: int) -> None:
+        """-1 = one CTA per item (default), 0 = persistent prefill on every SM, n > 0 = at most n CTAs."""
+        check(LIB.hpa_set_prefill_ctas(self._h, n))
+
     def prefill_plan_info(self) -> dict:
         """The last prefill's plan: CTAs launched, units split, key ranges per split unit."""
         n, u, s = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()

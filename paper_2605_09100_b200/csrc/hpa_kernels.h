@@ -156,6 +156,10 @@ struct PrefillArgs {
   int32_t n_parts, split_max;
   float* o_part;            // [n_parts][split_max][2 slots][128 rows][D]
   float* lse_part;          // [n_parts][split_max][2][128]
+  // Persistent launch (nullptr: one CTA per work item): CTA c runs items
+  // [cta_off[c], cta_off[c + 1]) of `work`, in order; n_ctas <= #SMs.
+  const int32_t* cta_off;
+  int32_t n_ctas;
 };
 // Split-KV prefill (work lists) is built in the default kernel configuration only.
 bool prefill_split_supported();

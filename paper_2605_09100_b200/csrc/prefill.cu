@@ -134,7 +134,7 @@ struct PSmem {
   static constexpr int oBar = oC + kNC * (kBN + 4) * 4;
   // q_full, k_full[NK], k_empty[NK], v_full[NV], v_empty[NV], s_full[2], p_full[2 slots][2 halves],
   // o_full, c_full[NC], c_empty[NC]
-  static constexpr int kNBar = 1 + 2 * kNK + 2 * kNV + 2 + 4 + 1 + 2 * kNC + 1;  // + o_ready (HPA_PF1)
+  static constexpr int kNBar = 1 + 2 * kNK + 2 * kNV + 2 + 4 + 1 + 2 * kNC + 2;  // + o_ready (HPA_PF1) / q_empty, o_full1 (persistent)
   static constexpr int oX = oBar + kNBar * 8;      // HPA_SM16: row max [2 buf][2 slot][2 half][128], row sum [2][2][128]
   static constexpr int kXBytes = (HPA_SM16 || HPA_PF1) ? (8 + 4) * kBM * 4 : 0;
   static constexpr int oMisc = oX + kXBytes;
@@ -318,6 +318,172 @@ __device__ __forceinline__ void unit_slots(int G, int y, int x, int* hq_s, int* 
     mt_s[0] = 2 * x;
     mt_s[1] = 2 * x + 1;
   }
+}
+
+// One 128-key tile of a slot's online softmax (default kernel configuration): S_s from TMEM,
+// the causal / span / partial-page mask from the producer's key indices `col` (ring stage
+// released on `cempty`), lazy-rescaled running max, exps (optimistic first half), P as bf16
+// pairs over S_s in two published halves (pf[0], pf[1]), running row sum. The caller has
+// waited for S_s(j). `j` = the tile's index within its unit (O_s is rescaled only for j > 0).
+template <int D>
+__device__ __forceinline__ void softmax_tile(const PrefillArgs& a, int s, int quarter, int row, int lane, int j,
+                                             uint32_t tS, uint32_t tO, const int32_t* col, uint64_t* cfull,
+                                             uint32_t cpar, uint64_t* cempty, uint64_t* pf, int my_i,
+                                             int span_from, float sl2, float& m_run, float& l_run) {
+  float x[kBN];
+  constexpr int kLd0 = HPA_SPLIT_LD ? kBN / 2 : kBN;  // columns loaded before the first wait
+#pragma unroll
+  for (int c = 0; c < kLd0 / 32; ++c) tc_ld32(tS + c * 32, x + c * 32);
+  mbar_wait(cfull, cpar);
+  const bool all_vis = col[kBN] != 0;
+  const int cmask = my_i >= span_from ? -1 : ~kSpanBit;  // span tag visible only to span rows
+  auto mask_cols = [&](int c0, int c1) {
+#pragma unroll
+    for (int c = c0; c < c1; c += 4) {
+      const int4 ci = *reinterpret_cast<const int4*>(col + c);
+      x[c + 0] = (ci.x & cmask) <= my_i ? x[c + 0] : -CUDART_INF_F;
+      x[c + 1] = (ci.y & cmask) <= my_i ? x[c + 1] : -CUDART_INF_F;
+      x[c + 2] = (ci.z & cmask) <= my_i ? x[c + 2] : -CUDART_INF_F;
+      x[c + 3] = (ci.w & cmask) <= my_i ? x[c + 3] : -CUDART_INF_F;
+    }
+  };
+  tc_wait_ld();
+  if (HPA_SPLIT_LD) {  // second half in flight while the first is masked (and exp'd, below)
+#pragma unroll
+    for (int c = kLd0 / 32; c < kBN / 32; ++c) tc_ld32(tS + c * 32, x + c * 32);
+  }
+  if (row == 0) TRACE(9 + s, j);
+  if (!all_vis) mask_cols(0, kLd0);
+  if (!HPA_SPLIT_LD) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(cempty);  // col[] consumed (masking done)
+  }
+  // p = 2^(x*sl2 - m): f32x2 FFMA for the argument, MUFU ex2 (optionally 1 pair in
+  // HPA_POLY_EVERY on the FMA pipe); 4 independent partial row sums
+  const float2 sl2x2 = make_float2(sl2, sl2);
+  float2 rs4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  auto exps_half = [&](int half, float m_use, uint32_t* pk) {
+    const float2 negm = make_float2(-m_use, -m_use);
+    if (HPA_EXP_INPLACE) {
+      // all ex2 first (in place: x of this half is dead once its max is known), then the sums
+      // and bf16 packs, so no MUFU result is consumed right behind its producer
+#pragma unroll
+      for (int c = half * 64; c < half * 64 + 64; c += 2) {
+        const float2 arg = ffma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
+        x[c] = fast_exp2(arg.x);
+        x[c + 1] = fast_exp2(arg.y);
+      }
+#pragma unroll
+      for (int c = half * 64; c < half * 64 + 64; c += 2) {
+        const float2 e = make_float2(x[c], x[c + 1]);
+        rs4[(c >> 1) & 3] = fadd2(rs4[(c >> 1) & 3], e);
+        pk[(c - half * 64) >> 1] = HPA_P_PACK_ALU ? pack_bf16_alu(e.x, e.y) : pack_bf16(e.x, e.y);
+      }
+      return;
+    }
+#pragma unroll
+    for (int c = half * 64; c < half * 64 + 64; c += 2) {
+      const float2 arg = ffma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
+      float2 e;
+      if (HPA_POLY_EVERY > 0 && ((c >> 1) % (HPA_POLY_EVERY > 0 ? HPA_POLY_EVERY : 1)) == HPA_POLY_EVERY - 1) {
+        e = exp2_poly2(arg);
+      } else {
+        e.x = fast_exp2(arg.x);
+        e.y = fast_exp2(arg.y);
+      }
+      rs4[(c >> 1) & 3] = fadd2(rs4[(c >> 1) & 3], e);
+      pk[(c - half * 64) >> 1] = HPA_P_PACK_ALU ? pack_bf16_alu(e.x, e.y) : pack_bf16(e.x, e.y);
+    }
+  };
+  // Optimistic first half: once every row of the warp has a finite running max, the
+  // first half's exps are computed against it while the tile max is reduced alongside
+  // (ALU work next to MUFU work). Lazy rescaling keeps the running max unless the tile max
+  // exceeds it by > 2^8, so the result is exact whenever no row grew; otherwise the warp
+  // redoes half 0 on the exact path below.
+  uint32_t pk0[kBN / 4];
+  const bool opt = HPA_OPT_EXP && __all_sync(0xffffffffu, m_run != -CUDART_INF_F);
+  bool p0_stored = false;  // P half 0 already in TMEM (not yet published)
+  if (opt) {
+    exps_half(0, m_run, pk0);
+    if (HPA_SPLIT_LD) {  // async store overlapping the second half's load and the max
+      tc_st32(tS, pk0);
+      p0_stored = true;
+    }
+  }
+  if (HPA_SPLIT_LD) {
+    tc_wait_ld();
+    if (!all_vis) mask_cols(kLd0, kBN);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(cempty);  // col[] consumed (masking done)
+  }
+  if (row == 0) TRACE(31 + s, j);
+  // row max as a tree (8 independent partial maxima), not a 64-deep chain
+  float pm[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) pm[k] = fmaxf(x[k], x[k + 8]);
+#pragma unroll
+  for (int c = 16; c < kBN; c += 16) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) pm[k] = fmaxf(pm[k], fmaxf(x[c + k], x[c + k + 8]));
+  }
+  float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+  mx *= sl2;
+  // lazy rescale: move the running max only when it grows by > 2^8
+  const bool grow = mx > m_run + kRescaleThreshold;
+  float alpha = 1.f;
+  float m_use = m_run;
+  if (row == 0) TRACE(33 + s, j);
+  if (!opt || __any_sync(0xffffffffu, grow)) {
+    if (row == 0) TRACE(37 + s, j);  // exact path taken
+    const float m_new = grow ? mx : m_run;
+    alpha = grow ? fast_exp2(m_run - m_new) : 1.f;
+    m_run = m_new;
+    if (j > 0 && __any_sync(0xffffffffu, grow)) {  // O_s is settled: PV_s(j-1) completed before S_s(j)
+      float o[32];
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        tc_ld32(tO + c * 32, o);
+        tc_wait_ld();
+#pragma unroll
+        for (int y = 0; y < 32; ++y) o[y] *= alpha;
+        tc_st32(tO + c * 32, reinterpret_cast<const uint32_t*>(o));
+      }
+    }
+    // a row with nothing visible yet (span-masked leading tiles) keeps p = 0, not NaN
+    m_use = m_new == -CUDART_INF_F ? 0.f : m_new;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rs4[k] = make_float2(0.f, 0.f);
+    exps_half(0, m_use, pk0);
+    if (p0_stored) tc_wait_st();  // the optimistic store lands before it is overwritten
+    p0_stored = false;
+  }
+  // P (bf16 pairs) over S: keys [64 half, 64 half + 64) -> columns [128 s + 32 half, +32)
+  if (row == 0) TRACE(35 + s, j);
+  if (!p0_stored) tc_st32(tS, pk0);
+  if (HPA_PV_SPLIT) {
+    tc_wait_st();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&pf[0]);
+    if (row == 0) TRACE(11 + 2 * s, j);
+    if (lane == 0) TRACE(23 + 4 * s + quarter, j);  // per-warp P half0
+  }
+  {
+    uint32_t pk1[kBN / 4];
+    exps_half(1, m_use, pk1);
+    tc_st32(tS + 32, pk1);
+    tc_wait_st();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      if (!HPA_PV_SPLIT) mbar_arrive(&pf[0]);
+      mbar_arrive(&pf[1]);
+    }
+    if (row == 0) TRACE(12 + 2 * s, j);
+    if (lane == 0) TRACE(15 + 4 * s + quarter, j);  // per-warp P completion
+  }
+  const float2 rsa = fadd2(rs4[0], rs4[1]), rsb = fadd2(rs4[2], rs4[3]);
+  l_run = l_run * alpha + ((rsa.x + rsb.x) + (rsa.y + rsb.y));
 }
 
 // kCl (HPA_PF1 with G even): the two q-heads of a KV-head pair run as a 2-CTA cluster over
@@ -1041,167 +1207,14 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         if (lane == 0) mbar_arrive(&c_empty[cs]);
         continue;
       }
-      float x[kBN];
       mbar_wait(&s_full[s], j & 1);
       if (row == 0) TRACE(7 + s, j);
 #ifdef HPA_TRACE
       if (j == 0 && threadIdx.x == 0) CTA_STAMP(2, gtimer());
 #endif
       tc_fence_after();
-      constexpr int kLd0 = HPA_SPLIT_LD ? kBN / 2 : kBN;  // columns loaded before the first wait
-#pragma unroll
-      for (int c = 0; c < kLd0 / 32; ++c) tc_ld32(tS + c * 32, x + c * 32);
-      mbar_wait(&c_full[cs], (j / kNC) & 1);
-      const int32_t* col = sC + cs * (kBN + 4);
-      const bool all_vis = col[kBN] != 0;
-      const int cmask = my_i >= span_from ? -1 : ~kSpanBit;  // span tag visible only to span rows
-      auto mask_cols = [&](int c0, int c1) {
-#pragma unroll
-        for (int c = c0; c < c1; c += 4) {
-          const int4 ci = *reinterpret_cast<const int4*>(col + c);
-          x[c + 0] = (ci.x & cmask) <= my_i ? x[c + 0] : -CUDART_INF_F;
-          x[c + 1] = (ci.y & cmask) <= my_i ? x[c + 1] : -CUDART_INF_F;
-          x[c + 2] = (ci.z & cmask) <= my_i ? x[c + 2] : -CUDART_INF_F;
-          x[c + 3] = (ci.w & cmask) <= my_i ? x[c + 3] : -CUDART_INF_F;
-        }
-      };
-      tc_wait_ld();
-      if (HPA_SPLIT_LD) {  // second half in flight while the first is masked (and exp'd, below)
-#pragma unroll
-        for (int c = kLd0 / 32; c < kBN / 32; ++c) tc_ld32(tS + c * 32, x + c * 32);
-      }
-      if (row == 0) TRACE(9 + s, j);
-      if (!all_vis) mask_cols(0, kLd0);
-      if (!HPA_SPLIT_LD) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&c_empty[cs]);  // col[] consumed (masking done)
-      }
-      // p = 2^(x*sl2 - m): f32x2 FFMA for the argument, MUFU ex2 (optionally 1 pair in
-      // HPA_POLY_EVERY on the FMA pipe); 4 independent partial row sums
-      const float2 sl2x2 = make_float2(sl2, sl2);
-      float2 rs4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      auto exps_half = [&](int half, float m_use, uint32_t* pk) {
-        const float2 negm = make_float2(-m_use, -m_use);
-        if (HPA_EXP_INPLACE) {
-          // all ex2 first (in place: x of this half is dead once its max is known), then the sums
-          // and bf16 packs, so no MUFU result is consumed right behind its producer
-#pragma unroll
-          for (int c = half * 64; c < half * 64 + 64; c += 2) {
-            const float2 arg = ffma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
-            x[c] = fast_exp2(arg.x);
-            x[c + 1] = fast_exp2(arg.y);
-          }
-#pragma unroll
-          for (int c = half * 64; c < half * 64 + 64; c += 2) {
-            const float2 e = make_float2(x[c], x[c + 1]);
-            rs4[(c >> 1) & 3] = fadd2(rs4[(c >> 1) & 3], e);
-            pk[(c - half * 64) >> 1] = HPA_P_PACK_ALU ? pack_bf16_alu(e.x, e.y) : pack_bf16(e.x, e.y);
-          }
-          return;
-        }
-#pragma unroll
-        for (int c = half * 64; c < half * 64 + 64; c += 2) {
-          const float2 arg = ffma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
-          float2 e;
-          if (HPA_POLY_EVERY > 0 && ((c >> 1) % (HPA_POLY_EVERY > 0 ? HPA_POLY_EVERY : 1)) == HPA_POLY_EVERY - 1) {
-            e = exp2_poly2(arg);
-          } else {
-            e.x = fast_exp2(arg.x);
-            e.y = fast_exp2(arg.y);
-          }
-          rs4[(c >> 1) & 3] = fadd2(rs4[(c >> 1) & 3], e);
-          pk[(c - half * 64) >> 1] = HPA_P_PACK_ALU ? pack_bf16_alu(e.x, e.y) : pack_bf16(e.x, e.y);
-        }
-      };
-      // Optimistic first half: once every row of the warp has a finite running max, the
-      // first half's exps are computed against it while the tile max is reduced alongside
-      // (ALU work next to MUFU work). Lazy rescaling keeps the running max unless the tile max
-      // exceeds it by > 2^8, so the result is exact whenever no row grew; otherwise the warp
-      // redoes half 0 on the exact path below.
-      uint32_t pk0[kBN / 4];
-      const bool opt = HPA_OPT_EXP && __all_sync(0xffffffffu, m_run != -CUDART_INF_F);
-      bool p0_stored = false;  // P half 0 already in TMEM (not yet published)
-      if (opt) {
-        exps_half(0, m_run, pk0);
-        if (HPA_SPLIT_LD) {  // async store overlapping the second half's load and the max
-          tc_st32(tS, pk0);
-          p0_stored = true;
-        }
-      }
-      if (HPA_SPLIT_LD) {
-        tc_wait_ld();
-        if (!all_vis) mask_cols(kLd0, kBN);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&c_empty[cs]);  // col[] consumed (masking done)
-      }
-      if (row == 0) TRACE(31 + s, j);
-      // row max as a tree (8 independent partial maxima), not a 64-deep chain
-      float pm[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) pm[k] = fmaxf(x[k], x[k + 8]);
-#pragma unroll
-      for (int c = 16; c < kBN; c += 16) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) pm[k] = fmaxf(pm[k], fmaxf(x[c + k], x[c + k + 8]));
-      }
-      float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
-      mx *= sl2;
-      // lazy rescale: move the running max only when it grows by > 2^8
-      const bool grow = mx > m_run + kRescaleThreshold;
-      float alpha = 1.f;
-      float m_use = m_run;
-      if (row == 0) TRACE(33 + s, j);
-      if (!opt || __any_sync(0xffffffffu, grow)) {
-        if (row == 0) TRACE(37 + s, j);  // exact path taken
-        const float m_new = grow ? mx : m_run;
-        alpha = grow ? fast_exp2(m_run - m_new) : 1.f;
-        m_run = m_new;
-        if (j > 0 && __any_sync(0xffffffffu, grow)) {  // O_s is settled: PV_s(j-1) completed before S_s(j)
-          float o[32];
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            tc_ld32(tO + c * 32, o);
-            tc_wait_ld();
-#pragma unroll
-            for (int y = 0; y < 32; ++y) o[y] *= alpha;
-            tc_st32(tO + c * 32, reinterpret_cast<const uint32_t*>(o));
-          }
-        }
-        // a row with nothing visible yet (span-masked leading tiles) keeps p = 0, not NaN
-        m_use = m_new == -CUDART_INF_F ? 0.f : m_new;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) rs4[k] = make_float2(0.f, 0.f);
-        exps_half(0, m_use, pk0);
-        if (p0_stored) tc_wait_st();  // the optimistic store lands before it is overwritten
-        p0_stored = false;
-      }
-      // P (bf16 pairs) over S: keys [64 half, 64 half + 64) -> columns [128 s + 32 half, +32)
-      if (row == 0) TRACE(35 + s, j);
-      if (!p0_stored) tc_st32(tS, pk0);
-      if (HPA_PV_SPLIT) {
-        tc_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[2 * s]);
-        if (row == 0) TRACE(11 + 2 * s, j);
-        if (lane == 0) TRACE(23 + 4 * s + quarter, j);  // per-warp P half0
-      }
-      {
-        uint32_t pk1[kBN / 4];
-        exps_half(1, m_use, pk1);
-        tc_st32(tS + 32, pk1);
-        tc_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (!HPA_PV_SPLIT) mbar_arrive(&p_full[2 * s]);
-          mbar_arrive(&p_full[2 * s + 1]);
-        }
-        if (row == 0) TRACE(12 + 2 * s, j);
-        if (lane == 0) TRACE(15 + 4 * s + quarter, j);  // per-warp P completion
-      }
-      const float2 rsa = fadd2(rs4[0], rs4[1]), rsb = fadd2(rs4[2], rs4[3]);
-      l_run = l_run * alpha + ((rsa.x + rsb.x) + (rsa.y + rsb.y));
+      softmax_tile<D>(a, s, quarter, row, lane, j, tS, tO, sC + cs * (kBN + 4), &c_full[cs], (j / kNC) & 1,
+                      &c_empty[cs], &p_full[2 * s], my_i, span_from, sl2, m_run, l_run);
     }
 #ifdef HPA_TRACE
     if (threadIdx.x == 0) {
@@ -1304,6 +1317,402 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Persistent prefill (default configuration): one CTA per SM loops over the work items the host
+// assigned to it (PrefillArgs::cta_off, longest-processing-time greedy over estimated tile
+// counts). Setup (barrier init, TMEM allocation) happens once; the K/V/mask rings, the
+// S/P handshakes and the tile counters run on across items, so the next item's K/V tiles
+// stream in while the current item drains, and its Q tiles are loaded (warp 11) as soon as the
+// current item's last Q K^T has completed (q_empty; issued by the V producer warp). Per item the
+// softmax warps finish with the epilogue (row stores: the shared memory rings stay in use) and
+// carry straight on with the next item's first tile. Items never have an empty key range (the host clamps split counts).
+struct PItem {
+  int b, piece, part, jb, n_tiles, skip_a, n_skip, seq, q_len, q_off, seq_len, n_ent;
+  int hq0, hq1, mt0, mt1;
+  bool live1;
+};
+__device__ __forceinline__ PItem load_item(const PrefillArgs& a, int idx) {
+  const int4 w = a.work[4 * idx], wr = a.work[4 * idx + 1], wq = a.work[4 * idx + 2], wn = a.work[4 * idx + 3];
+  PItem u;
+  u.b = w.x;
+  u.piece = w.w & 15;
+  u.part = ((w.w >> 4) & 15) > 1 ? (w.w >> 8) : -1;
+  u.jb = wr.x;
+  u.n_tiles = wr.y;
+  u.skip_a = wr.z;
+  u.n_skip = wr.w;
+  u.seq = wq.x;
+  u.q_len = wq.y;
+  u.q_off = wq.z;
+  u.seq_len = wq.w;
+  u.n_ent = wn.x;
+  int hq[2], mt[2];
+  unit_slots(a.G, w.y, w.z, hq, mt);
+  u.hq0 = hq[0];
+  u.hq1 = hq[1];
+  u.mt0 = mt[0];
+  u.mt1 = mt[1];
+  u.live1 = mt[1] * kBM < u.q_len;
+  return u;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+prefill_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                          const __grid_constant__ CUtensorMap tm_v, const PrefillArgs a) {
+  using L = PSmem<D>;
+  constexpr int kHalves = D / 64;
+  grid_dependency_wait();  // PDL
+  grid_launch_dependents();
+  const int beg = a.cta_off[blockIdx.x], end = a.cta_off[blockIdx.x + 1];
+  if (beg >= end) return;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm + L::oQ;
+  uint8_t* sK = sm + L::oK;
+  uint8_t* sV = sm + L::oV;
+  int32_t* sC = reinterpret_cast<int32_t*>(sm + L::oC);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::oBar);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = q_full + 1;
+  uint64_t* k_empty = k_full + kNK;
+  uint64_t* v_full = k_empty + kNK;
+  uint64_t* v_empty = v_full + kNV;
+  uint64_t* s_full = v_empty + kNV;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_full = p_full + 4;
+  uint64_t* c_full = o_full + 1;
+  uint64_t* c_empty = c_full + kNC;
+  uint64_t* q_empty = c_empty + kNC;  // (the o_ready slot of the single-unit kernel)
+  uint64_t* o_full1 = q_empty + 1;    // o_full: slot 0's O ready; o_full1: slot 1's (items with slot 1 live)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::oMisc);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  auto issue_q = [&](const PItem& u) {  // one thread
+    mbar_arrive_expect_tx(q_full, u.live1 ? 2 * L::kQ : L::kQ);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (s == 1 && !u.live1) break;
+#pragma unroll
+      for (int hf = 0; hf < kHalves; ++hf)
+        tma_load_3d(sQ + s * L::kQ + hf * kBM * 128, &tm_q, q_full, hf * 64, s ? u.hq1 : u.hq0,
+                    u.q_off + (s ? u.mt1 : u.mt0) * kBM);
+    }
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int i = 0; i < kNK; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
+    for (int i = 0; i < kNV; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&p_full[i], 4);  // one arrive per softmax warp
+    mbar_init(o_full, 1);
+    mbar_init(o_full1, 1);
+    for (int i = 0; i < kNC; ++i) { mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], kSoftWarps); }
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_q);
+    issue_q(load_item(a, beg));  // the first item's Q during setup
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int P = a.P, lp = a.log2P;
+
+  if (warp >= kSoftWarps) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kOtherRegs));
+  if (warp == kProducerWarp) {
+    // ================================================================ K producer + mask indices
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+    }
+    const int pbox = P < kBN ? P : kBN;
+    const int nbox = kBN / pbox;
+    constexpr int kOobRow = INT_MAX / 2;
+    const int head_row = a.layer * a.NP;
+    uint32_t g = 0;  // K tiles issued by this CTA (ring position)
+    for (int it = beg; it < end; ++it) {
+      const PItem u = load_item(a, it);
+      const int32_t* bt = a.t.block_table + int64_t(u.seq) * a.t.max_pages;
+      const int32_t* p0 = a.t.pos0 + int64_t(u.seq) * a.t.max_pages;
+      const int32_t* mt_ = a.t.meta + int64_t(u.seq) * a.t.max_pages;
+      const int h = u.hq0 / a.G;
+      const int i_min = u.seq_len - u.q_len + u.mt0 * kBM;
+      const int span_lo = a.span ? a.span[3 * u.b] : 0, span_hi = a.span ? a.span[3 * u.b + 1] : 0;
+      auto tile_of = [&](int jj) {
+        jj += u.jb;
+        return jj < u.skip_a ? jj : jj + u.n_skip;
+      };
+      int nmv[kBN / 32], np0[kBN / 32], nrow = kOobRow;
+      auto fetch = [&](int jj, int* mv, int* pv, int& rw) {
+        const int tile = tile_of(jj);
+        const bool ok = jj < u.n_tiles;
+#pragma unroll
+        for (int x = 0; x < kBN / 32; ++x) {
+          const int e = (tile * kBN + x * 32 + lane) >> lp;
+          mv[x] = ok && e < u.n_ent ? __ldg(mt_ + e) : 0;
+          pv[x] = ok && e < u.n_ent ? __ldg(p0 + e) : 0;
+        }
+        rw = kOobRow;
+        if (ok && lane < nbox) {
+          const int slot = tile * kBN + lane * pbox;
+          const int e = slot >> lp;
+          if (e < u.n_ent) rw = ((head_row + __ldg(bt + e)) * a.Hkv + h) * P + (slot & (P - 1));
+        }
+      };
+      fetch(0, nmv, np0, nrow);
+      for (int j = 0; j < u.n_tiles; ++j, ++g) {
+        const int tile = tile_of(j);
+        int cmv[kBN / 32], cp0[kBN / 32];
+#pragma unroll
+        for (int x = 0; x < kBN / 32; ++x) {
+          cmv[x] = nmv[x];
+          cp0[x] = np0[x];
+        }
+        const int row = nrow;
+        fetch(j + 1, nmv, np0, nrow);
+        const int cs = g % kNC;
+        if (g >= kNC) mbar_wait(&c_empty[cs], ((g / kNC) - 1) & 1);
+        int32_t* col = sC + cs * (kBN + 4);
+        bool vis = true;
+#pragma unroll
+        for (int x = 0; x < kBN / 32; ++x) {
+          const int c = x * 32 + lane;
+          const int slot = tile * kBN + c;
+          const int e = slot >> lp, r = slot & (P - 1);
+          int v = INT_MAX;
+          if (e < u.n_ent && r < (cmv[x] & kMetaRowsMask)) v = cp0[x] + r;
+          if (a.span && v >= span_lo && v < span_hi) v |= kSpanBit;
+          col[c] = v;
+          vis &= (v <= i_min);
+        }
+        vis = __all_sync(0xffffffffu, vis);
+        if (lane == 0) col[kBN] = vis ? 1 : 0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&c_full[cs]);
+        const int ks = g % kNK;
+        if (g >= kNK) mbar_wait(&k_empty[ks], ((g / kNK) - 1) & 1);
+        if (lane == 0) mbar_arrive_expect_tx(&k_full[ks], L::kKV);
+        __syncwarp();
+        if (lane < nbox) {
+#pragma unroll
+          for (int hf = 0; hf < kHalves; ++hf)
+            tma_load_2d(sK + ks * L::kKV + hf * kBN * 128 + lane * pbox * 128, &tm_k, &k_full[ks], hf * 64, row);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == kVProducerWarp) {
+    // ================================================================ V producer
+    const int pbox = P < kBN ? P : kBN;
+    const int nbox = kBN / pbox;
+    constexpr int kOobRow = INT_MAX / 2;
+    const int head_row = a.layer * a.NP;
+    uint32_t g = 0;
+    for (int it = beg; it < end; ++it) {
+      const PItem u = load_item(a, it);
+      if (it > beg && lane == 0) {  // this item's Q once every Q K^T of the previous one completed
+        mbar_wait(q_empty, (it - beg - 1) & 1);
+        issue_q(u);
+      }
+      const int32_t* bt = a.t.block_table + int64_t(u.seq) * a.t.max_pages;
+      const int h = u.hq0 / a.G;
+      auto vrow = [&](int jj) {
+        int rw = kOobRow;
+        if (jj < u.n_tiles && lane < nbox) {
+          int tile = jj + u.jb;
+          tile = tile < u.skip_a ? tile : tile + u.n_skip;
+          const int slot = tile * kBN + lane * pbox;
+          const int e = slot >> lp;
+          if (e < u.n_ent) rw = ((head_row + __ldg(bt + e)) * a.Hkv + h) * P + (slot & (P - 1));
+        }
+        return rw;
+      };
+      int next_row = vrow(0);
+      for (int j = 0; j < u.n_tiles; ++j, ++g) {
+        const int row = next_row;
+        next_row = vrow(j + 1);
+        const int vs = g % kNV;
+        if (g >= kNV) mbar_wait(&v_empty[vs], ((g / kNV) - 1) & 1);
+        if (lane == 0) mbar_arrive_expect_tx(&v_full[vs], L::kKV);
+        __syncwarp();
+        if (lane < nbox) {
+#pragma unroll
+          for (int hf = 0; hf < kHalves; ++hf)
+            tma_load_2d(sV + vs * L::kKV + hf * kBN * 128 + lane * pbox * 128, &tm_v, &v_full[vs], hf * 64, row);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ================================================================ MMA issuer
+    constexpr uint32_t idS = idesc_bf16(kBM, kBN, 0, 0);
+    constexpr uint32_t idO = idesc_bf16(kBM, D, 0, 1);
+    const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV);
+    auto issue_s = [&](int s, uint32_t gg) {
+      const int ks = gg % kNK;
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint64_t ad = sdesc(aQ + s * L::kQ + (k >> 2) * (kBM * 128) + (k & 3) * 32, 16, 1024);
+          const uint64_t bd = sdesc(aK + ks * L::kKV + (k >> 2) * (kBN * 128) + (k & 3) * 32, 16, 1024);
+          tc_mma_ss(tmem + s * 128, ad, bd, idS, k > 0 ? 1u : 0u);
+        }
+        tc_commit(&s_full[s]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv_half = [&](int s, uint32_t gg, int half, bool acc0) {
+      const int vs = gg % kNV;
+      if (elect_one()) {
+#pragma unroll
+        for (int k = half * 4; k < half * 4 + 4; ++k) {
+          const uint64_t bd = sdesc(aV + vs * L::kKV + k * 2048, kBN * 128, 1024);
+          tc_mma_ts(tmem + 256 + s * 128, tmem + s * 128 + k * 8, bd, idO, (acc0 || k > 0) ? 1u : 0u);
+        }
+      }
+      __syncwarp();
+    };
+    auto commit = [&](uint64_t* bar) {
+      if (elect_one()) tc_commit(bar);
+      __syncwarp();
+    };
+    uint32_t g = 0;                // tiles (K and V ring position)
+    uint32_t np[2] = {0u, 0u};     // P publications per slot (p_full phase)
+    for (int it = beg; it < end; ++it) {
+      const PItem u = load_item(a, it);
+      const int nslot = u.live1 ? 2 : 1;
+      mbar_wait(q_full, (it - beg) & 1);
+      mbar_wait(&k_full[g % kNK], (g / kNK) & 1);
+      tc_fence_after();
+      for (int s = 0; s < nslot; ++s) issue_s(s, g);
+      if (u.n_tiles == 1) commit(q_empty);
+      commit(&k_empty[g % kNK]);
+      for (int j = 0; j < u.n_tiles; ++j, ++g) {
+        const bool more = j + 1 < u.n_tiles;
+        mbar_wait(&v_full[g % kNV], (g / kNV) & 1);
+        bool k_ready = false;
+        for (int s = 0; s < nslot; ++s) {
+          mbar_wait(&p_full[2 * s], np[s] & 1);
+          tc_fence_after();
+          issue_pv_half(s, g, 0, j > 0);
+          mbar_wait(&p_full[2 * s + 1], np[s] & 1);
+          tc_fence_after();
+          issue_pv_half(s, g, 1, j > 0);
+          ++np[s];
+          if (s == nslot - 1) commit(&v_empty[g % kNV]);
+          if (more) {
+            if (!k_ready) {
+              mbar_wait(&k_full[(g + 1) % kNK], ((g + 1) / kNK) & 1);
+              tc_fence_after();
+              k_ready = true;
+            }
+            issue_s(s, g + 1);
+          }
+        }
+        if (more) {
+          commit(&k_empty[(g + 1) % kNK]);
+          if (j + 2 == u.n_tiles) commit(q_empty);  // the item's last Q K^T was just issued
+        }
+      }
+      commit(o_full);
+      if (u.live1) commit(o_full1);
+    }
+  } else if (warp < kSoftWarps) {
+    // ================================================================ softmax (slot = warp / 4)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
+    const int s = warp >> 2;
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_base = uint32_t(quarter * 32) << 16;
+    const uint32_t tS = tmem + lane_base + s * 128;
+    const uint32_t tO = tmem + lane_base + 256 + s * 128;
+    const float sl2 = a.scale_log2;
+    uint64_t* my_o_full = s ? o_full1 : o_full;
+    // tiles seen (mask ring), S tiles of this slot (s_full phase), items with this slot live
+    // (o_full phase: a slot waits only for items it takes part in, so it cannot fall two
+    // phases behind -- the next such item needs its P)
+    uint32_t g = 0, ns = 0, no = 0;
+    for (int it = beg; it < end; ++it) {
+      const PItem u = load_item(a, it);
+      const bool live = s == 0 || u.live1;
+      const int mt = s ? u.mt1 : u.mt0;
+      const int t = mt * kBM + row;
+      const int my_i = u.seq_len - u.q_len + t;
+      const int span_from = a.span ? a.span[3 * u.b + 2] : INT_MAX;
+      float m_run = -CUDART_INF_F, l_run = 0.f;
+      for (int j = 0; j < u.n_tiles; ++j, ++g) {
+        const int cs = g % kNC;
+        if (!live) {  // dead slot: still release the mask slot
+          mbar_wait(&c_full[cs], (g / kNC) & 1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&c_empty[cs]);
+          continue;
+        }
+        mbar_wait(&s_full[s], ns & 1);
+        ++ns;
+        tc_fence_after();
+        softmax_tile<D>(a, s, quarter, row, lane, j, tS, tO, sC + cs * (kBN + 4), &c_full[cs], (g / kNC) & 1,
+                        &c_empty[cs], &p_full[2 * s], my_i, span_from, sl2, m_run, l_run);
+      }
+      if (!live) continue;
+      mbar_wait(my_o_full, no & 1);
+      ++no;
+      tc_fence_after();
+      // epilogue (row stores: the K/V rings already hold the next item's tiles)
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      if (u.part >= 0) {
+        const int pp = (u.part * a.split_max + u.piece) * 2 + s;
+        float* orow = a.o_part + (int64_t(pp) * kBM + row) * D;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          float o[32];
+          tc_ld32(tO + c * 32, o);
+          tc_wait_ld();
+#pragma unroll
+          for (int y = 0; y < 32; y += 4)
+            *reinterpret_cast<float4*>(orow + c * 32 + y) =
+                make_float4(o[y] * inv, o[y + 1] * inv, o[y + 2] * inv, o[y + 3] * inv);
+        }
+        a.lse_part[int64_t(pp) * kBM + row] = l_run > 0.f ? m_run + __log2f(l_run) : -CUDART_INF_F;
+      } else {
+        __nv_bfloat16* orow =
+            static_cast<__nv_bfloat16*>(a.out) + (int64_t(u.q_off + t) * a.Hq + (s ? u.hq1 : u.hq0)) * D;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          float o[32];
+          tc_ld32(tO + c * 32, o);
+          tc_wait_ld();
+          if (t < u.q_len) {
+#pragma unroll
+            for (int y = 0; y < 32; y += 8) {
+              uint4 v;
+              v.x = pack_bf16(o[y + 0] * inv, o[y + 1] * inv);
+              v.y = pack_bf16(o[y + 2] * inv, o[y + 3] * inv);
+              v.z = pack_bf16(o[y + 4] * inv, o[y + 5] * inv);
+              v.w = pack_bf16(o[y + 6] * inv, o[y + 7] * inv);
+              *reinterpret_cast<uint4*>(orow + c * 32 + y) = v;
+            }
+          }
+        }
+      }
+      tc_fence_before();  // O_s read before the next item's P(0) publication lets PV overwrite it
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 // Split-KV merge (the LSE algebra of the decode combine, a5): one warp per (split unit, slot,
 // query row); lane l holds the LSE of piece l, every lane accumulates D/32 dims over the pieces.
 // out = sum_i 2^(lse_i - M) O_i / sum_i 2^(lse_i - M), bf16, into the caller's output rows.
@@ -1324,7 +1733,7 @@ __global__ void __launch_bounds__(128) prefill_combine_kernel(const PrefillArgs 
   unit_slots(a.G, u.y, u.z, hq_s, mt_s);
   const int t = mt_s[s] * kBM + row;
   if (t >= uq.x) return;
-  const int S = kS > 0 ? kS : u.w;
+  const int S = u.w;  // <= kS when kS > 0 (kS = the plan's largest piece count)
   auto pidx = [&](int i) { return (int64_t(part * a.split_max + i) * 2 + s) * kBM + row; };
   auto load = [&](int i, float* v) {
     const float* op = a.o_part + pidx(i) * D + lane * kV;
@@ -1340,7 +1749,8 @@ __global__ void __launch_bounds__(128) prefill_combine_kernel(const PrefillArgs 
   float vals[kU][kV];
   if constexpr (kS > 0) {
 #pragma unroll
-    for (int i = 0; i < kS; ++i) load(i, vals[i]);
+    for (int i = 0; i < kS; ++i)
+      if (i < S) load(i, vals[i]);
   }
   float M = l;
 #pragma unroll
@@ -1356,8 +1766,10 @@ __global__ void __launch_bounds__(128) prefill_combine_kernel(const PrefillArgs 
 #pragma unroll
     for (int i = 0; i < kS; ++i) {
       const float wi = __shfl_sync(0xffffffffu, w, i);
+      if (i < S) {
 #pragma unroll
-      for (int v = 0; v < kV; ++v) acc[v] += wi * vals[i][v];
+        for (int v = 0; v < kV; ++v) acc[v] += wi * vals[i][v];
+      }
     }
   } else {
     for (int i = 0; i < S; ++i) {
@@ -1417,7 +1829,10 @@ cudaError_t launch_prefill_d(const CUtensorMap& tm_q, const CUtensorMap& tm_k, c
   }
   if (!HPA_PF1 && a.work) {  // split-KV work list: one CTA per (unit, piece), then the merge
     if (a.n_work == 0) return cudaSuccess;
-    cudaError_t e = launch_pdl(prefill_kernel<D, false>, dim3(unsigned(a.n_work)), dim3(kThreads), PSmem<D>::kBytes,
+    cudaError_t e =
+        a.cta_off ? launch_pdl(prefill_persistent_kernel<D>, dim3(unsigned(a.n_ctas)), dim3(kThreads),
+                               PSmem<D>::kBytes, s, tm_q, tm_k, tm_v, a)
+                  : launch_pdl(prefill_kernel<D, false>, dim3(unsigned(a.n_work)), dim3(kThreads), PSmem<D>::kBytes,
                                s, tm_q, tm_k, tm_v, tm_o, tm_op, a);
     if (e != cudaSuccess || a.n_parts == 0) return e;
     ++*launches;
@@ -1440,6 +1855,10 @@ cudaError_t prefill_init_attributes() {
   if ((e = cudaFuncSetAttribute(prefill_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 PSmem<128>::kBytes)) != cudaSuccess ||
       (e = cudaFuncSetAttribute(prefill_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                PSmem<64>::kBytes)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(prefill_persistent_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                PSmem<128>::kBytes)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(prefill_persistent_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 PSmem<64>::kBytes)) != cudaSuccess)
     return e;
   if (HPA_PF1 && HPA_PF1_CLUSTER) {

@@ -316,6 +316,7 @@ struct PfPlan {
   std::vector<int4> work;   // 4 per CTA (PrefillArgs::work)
   std::vector<int4> parts;  // 2 per split unit: {b, y, x, nsplit}, {q_len, q_off, 0, 0}
   int32_t split_max = 1;
+  std::vector<int32_t> cta_off;  // persistent launch: items of CTA c = [cta_off[c], cta_off[c+1])
 };
 
 struct hpa_cache {
@@ -358,6 +359,7 @@ struct hpa_cache {
   int32_t forced_splits = 0;
   // split-KV prefill: forced split count (0 = planner) and the partial workspace
   int32_t pf_forced_splits = 0;
+  int32_t pf_ctas = -1;          // prefill CTAs: -1 = one per item (default), 0 = persistent on every SM, n > 0 = at most n
   uint64_t table_version = 0;    // bumped by every block-table rebuild
   std::vector<int32_t> pf_key;   // last prefill plan's inputs (version, forced, batch, q_lens, span)
   PfPlan pf_plan;
@@ -653,6 +655,16 @@ bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, 
                   const int32_t* q_off, const int32_t* span, PfPlan& plan) {
   const int32_t forced = c->pf_forced_splits;
   if (forced == 16 || !prefill_split_supported()) return false;
+  // persistent launch (one CTA per SM looping over its items) when selected with
+  // hpa_set_prefill_ctas(c, n >= 0); a positive value caps the CTA count. Not the default: it
+  // measured 2-3 % slower than one CTA per item
+  const bool persistent = c->pf_ctas >= 0;
+  const int32_t max_ctas = c->pf_ctas > 0 ? std::min(c->pf_ctas, c->num_sms) : c->num_sms;
+  // per-item fixed cost in key tiles: a launched CTA (setup, pipeline fill, epilogue, CTA
+  // switch; scripts/trace_prefill_ctas.py) vs a persistent item (Q reload bubble and the
+  // epilogue, partly overlapped by the other slot's work)
+  static const double o_item_p = std::getenv("HPA_PF_OVH_P") ? std::atof(std::getenv("HPA_PF_OVH_P")) : 1.5;
+  static const double o_piece_p = o_item_p + 1.5;
   const int32_t Hq = c->cfg.num_q_heads, Hkv = c->cfg.num_kv_heads, G = Hq / Hkv;
   const int32_t lp = __builtin_ctz(uint32_t(c->cfg.page_size));
   const int32_t Y = (G & 1) == 0 ? Hkv * (G / 2) : Hq;
@@ -688,7 +700,7 @@ bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, 
   // tiles of one KV head read the same keys). Ordering units by length instead scattered a
   // wave over every (sequence, KV head) and re-read K/V from HBM (-4 % at configs[2] B = 4).
   const int64_t nU = int64_t(rows.size()) * Y;
-  const int32_t W = c->num_sms;
+  const int32_t W = persistent ? max_ctas : c->num_sms;
   std::vector<std::pair<int32_t, int32_t>> order;  // (row index, y)
   order.reserve(size_t(nU));
   for (size_t r0 = 0; r0 < rows.size();) {
@@ -707,8 +719,9 @@ bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, 
   } else if (forced == 0 && nU < int64_t(16) * W) {  // beyond 16 waves the tail loss is < 1/16
     // measured per-CTA fixed cost (scripts/trace_prefill_ctas.py: setup, pipeline fill, epilogue,
     // CTA switch) ~6.6 us = 3.3 key tiles; a split piece's fp32 epilogue adds ~1.4 us
-    static const double o = std::getenv("HPA_PF_OVH") ? std::atof(std::getenv("HPA_PF_OVH")) : 3.3;
-    const double o_piece = o + 0.7;
+    static const double o_launch = std::getenv("HPA_PF_OVH") ? std::atof(std::getenv("HPA_PF_OVH")) : 3.3;
+    const double o = persistent ? o_item_p : o_launch;
+    const double o_piece = persistent ? o_piece_p : o_launch + 0.7;
     static const double c_m = std::getenv("HPA_PF_MERGE") ? std::atof(std::getenv("HPA_PF_MERGE")) : 2.0;
     const double tile_us = 1.95 * c->cfg.head_dim / 128.0;
     const double part_tiles = 2.0 * 128 * c->cfg.head_dim * 4 / 5e6 / tile_us;  // one piece's partial read
@@ -753,16 +766,55 @@ bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, 
       plan.work.push_back(wn);
       continue;
     }
+    // persistent items never have an empty key range: a unit gets at most n pieces
+    const int32_t ns = persistent ? std::max(1, std::min(best_s, u.n)) : best_s;
+    if (ns == 1) {
+      plan.work.push_back(make_int4(u.b, y, u.x, 0 | (1 << 4)));
+      plan.work.push_back(make_int4(0, u.n, u.skip_a, u.n_skip));
+      plan.work.push_back(wq);
+      plan.work.push_back(wn);
+      continue;
+    }
     const int32_t part = int32_t(plan.parts.size() / 2);
-    plan.parts.push_back(make_int4(u.b, y, u.x, best_s));
+    plan.parts.push_back(make_int4(u.b, y, u.x, ns));
     plan.parts.push_back(make_int4(q_lens[u.b], q_off[u.b], 0, 0));
-    for (int32_t p = 0; p < best_s; ++p) {
-      const int32_t jb = int32_t(int64_t(u.n) * p / best_s), je = int32_t(int64_t(u.n) * (p + 1) / best_s);
-      plan.work.push_back(make_int4(u.b, y, u.x, p | (best_s << 4) | (part << 8)));
+    for (int32_t p = 0; p < ns; ++p) {
+      const int32_t jb = int32_t(int64_t(u.n) * p / ns), je = int32_t(int64_t(u.n) * (p + 1) / ns);
+      plan.work.push_back(make_int4(u.b, y, u.x, p | (ns << 4) | (part << 8)));
       plan.work.push_back(make_int4(jb, je - jb, u.skip_a, u.n_skip));
       plan.work.push_back(wq);
       plan.work.push_back(wn);
     }
+  }
+  plan.cta_off.clear();
+  if (persistent) {
+    // Items go, in dispatch order, to the CTA that is free first (estimated key tiles + the
+    // per-item cost), as the hardware would dispatch them; each CTA's list keeps that order.
+    const size_t n_items = plan.work.size() / 4;
+    const int32_t n_ctas = int32_t(std::min<size_t>(size_t(max_ctas), n_items));
+    std::vector<std::pair<double, int32_t>> heap;
+    for (int32_t i = 0; i < n_ctas; ++i) heap.push_back({0.0, i});
+    std::vector<int32_t> owner(n_items);
+    std::vector<int32_t> count(size_t(n_ctas), 0);
+    auto gt = std::greater<std::pair<double, int32_t>>();
+    std::make_heap(heap.begin(), heap.end(), gt);
+    for (size_t k = 0; k < n_items; ++k) {
+      std::pop_heap(heap.begin(), heap.end(), gt);
+      const bool piece = ((plan.work[4 * k].w >> 4) & 15) > 1;
+      heap.back().first += plan.work[4 * k + 1].y + (piece ? o_piece_p : o_item_p);
+      owner[k] = heap.back().second;
+      ++count[size_t(owner[k])];
+      std::push_heap(heap.begin(), heap.end(), gt);
+    }
+    plan.cta_off.assign(size_t(n_ctas) + 1, 0);
+    for (int32_t i = 0; i < n_ctas; ++i) plan.cta_off[size_t(i) + 1] = plan.cta_off[size_t(i)] + count[size_t(i)];
+    std::vector<int4> sorted(plan.work.size());
+    std::vector<int32_t> fill(plan.cta_off.begin(), plan.cta_off.end() - 1);
+    for (size_t k = 0; k < n_items; ++k) {
+      const int32_t dst = fill[size_t(owner[k])]++;
+      for (int f = 0; f < 4; ++f) sorted[4 * size_t(dst) + f] = plan.work[4 * k + f];
+    }
+    plan.work.swap(sorted);
   }
   return true;
 }
@@ -1566,8 +1618,8 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
   // work list (plan_prefill) + per-sequence metadata in one staged upload
   // the plan depends only on the tables, the batch and the split setting: reuse it when those
   // are unchanged since the last call (repeated chunks over a fixed batch skip the simulation)
-  std::vector<int32_t> key{int32_t(c->table_version), int32_t(c->table_version >> 32), c->pf_forced_splits, n_seqs,
-                           span ? 1 : 0};
+  std::vector<int32_t> key{int32_t(c->table_version), int32_t(c->table_version >> 32), c->pf_forced_splits,
+                           c->pf_ctas, n_seqs, span ? 1 : 0};
   key.insert(key.end(), seq_ids, seq_ids + n_seqs);
   key.insert(key.end(), q_lens, q_lens + n_seqs);
   if (span) key.insert(key.end(), span, span + 3 * size_t(n_seqs));
@@ -1578,16 +1630,18 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
   const PfPlan& plan = c->pf_plan;
   const bool listed = c->pf_listed;
   const size_t wbytes = listed ? (plan.work.size() + plan.parts.size()) * sizeof(int4) : 0;
-  const size_t bytes = wbytes + meta.size() * 4;
+  const size_t cbytes = listed ? plan.cta_off.size() * 4 : 0;
+  const size_t bytes = wbytes + cbytes + meta.size() * 4;
   const size_t off = c->ring.reserve(bytes);
   if (listed) {
     std::memcpy(c->ring.host(off), plan.work.data(), plan.work.size() * sizeof(int4));
     std::memcpy(c->ring.host(off) + plan.work.size() * sizeof(int4), plan.parts.data(),
                 plan.parts.size() * sizeof(int4));
+    if (cbytes) std::memcpy(c->ring.host(off) + wbytes, plan.cta_off.data(), cbytes);
   }
-  std::memcpy(c->ring.host(off) + wbytes, meta.data(), meta.size() * 4);
+  std::memcpy(c->ring.host(off) + wbytes + cbytes, meta.data(), meta.size() * 4);
   HPA_CUDA(c->ring.upload(off, bytes, s));
-  const int32_t* dmeta = reinterpret_cast<const int32_t*>(c->ring.dev(off) + wbytes);
+  const int32_t* dmeta = reinterpret_cast<const int32_t*>(c->ring.dev(off) + wbytes + cbytes);
   CUtensorMap tm_q, tm_o;
   if (!make_map_q(&tm_q, q, uint64_t(total_q), uint64_t(Hq), uint64_t(D), 128) ||
       !make_map_q(&tm_o, out, uint64_t(total_q), uint64_t(Hq), uint64_t(D), 128))
@@ -1596,7 +1650,7 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
   PrefillArgs a{c->dt, dmeta, dmeta + n_seqs, dmeta + 2 * n_seqs, out, n_seqs, Hq, c->cfg.num_kv_heads,
                 Hq / c->cfg.num_kv_heads, c->cfg.page_size, c->cfg.num_pages, layer, max_q,
                 scale * 1.4426950408889634f, __builtin_ctz(uint32_t(c->cfg.page_size)),
-                span ? dmeta + 3 * n_seqs : nullptr, c->trace, nullptr, 0, nullptr, 0, 1, nullptr, nullptr};
+                span ? dmeta + 3 * n_seqs : nullptr, c->trace, nullptr, 0, nullptr, 0, 1, nullptr, nullptr, nullptr, 0};
   if (listed) {
     const size_t rows = plan.parts.size() / 2 * size_t(plan.split_max) * 2 * 128;
     if (rows > c->pf_part_rows) {  // split workspace (grown on demand) and its fp32 TMA map
@@ -1619,6 +1673,10 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
     a.split_max = plan.split_max;
     a.o_part = c->pf_o_part;
     a.lse_part = c->pf_lse_part;
+    if (cbytes) {
+      a.cta_off = reinterpret_cast<const int32_t*>(c->ring.dev(off) + wbytes);
+      a.n_ctas = int32_t(plan.cta_off.size()) - 1;
+    }
   }
   int launched = 0;
   cudaError_t e = launch_prefill(tm_q, c->tm_k_pre, c->tm_v_pre, tm_o, c->tm_opart, a, D, s, &launched);
@@ -1681,9 +1739,19 @@ hpa_status_t hpa_export_table(hpa_cache_t* c, int32_t seq_id, int32_t* pages, in
 hpa_status_t hpa_prefill_plan_info(hpa_cache_t* c, int32_t* n_ctas, int32_t* n_split_units, int32_t* splits) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
   const bool l = c->pf_listed;
-  if (n_ctas) *n_ctas = l ? int32_t(c->pf_plan.work.size() / 4) : 0;
+  if (n_ctas)
+    *n_ctas = !l ? 0
+              : c->pf_plan.cta_off.empty() ? int32_t(c->pf_plan.work.size() / 4)
+                                           : int32_t(c->pf_plan.cta_off.size()) - 1;
   if (n_split_units) *n_split_units = l ? int32_t(c->pf_plan.parts.size() / 2) : 0;
   if (splits) *splits = l ? c->pf_plan.split_max : 1;
+  return HPA_OK;
+}
+
+hpa_status_t hpa_set_prefill_ctas(hpa_cache_t* c, int32_t n) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (n < -1) return fail(HPA_ERR_INVALID_ARG, "prefill ctas %d < -1", n);
+  c->pf_ctas = n;
   return HPA_OK;
 }
 

@@ -17,9 +17,10 @@ def main():
     torch.cuda.set_device(dev)
     shape = qwen3_8b_shape(16)
     stream = torch.cuda.current_stream()
-    modes = [int(x) for x in os.environ.get("MODES", "1,0,2,3,4,6").split(",")]
+    # a mode is a split setting, suffixed "p" for the persistent kernel (else one CTA per item)
+    modes = os.environ.get("MODES", "1,0,2,3,4,6").split(",")
     for bp in [int(x) for x in os.environ.get("BATCHES", "1,2,3,4").split(",")]:
-        c_rows, prior = 2048, 16384
+        c_rows, prior = int(os.environ.get("C_ROWS", "2048")), 16384
         cache, seqs, _ = bench.build_decode_cache(torch, Cache, shape, bp, 8, prior + c_rows, 0, dev, seed=777)
         g = torch.Generator(device="cuda:0").manual_seed(99)
         q = torch.randn((bp * c_rows, 32, 128), generator=g, device="cuda:0").to(torch.bfloat16)
@@ -28,7 +29,8 @@ def main():
         ref = None
         res = {}
         for mode in modes * int(os.environ.get("ROUNDS", "1")):
-            cache.set_prefill_splits(mode)
+            cache.set_prefill_splits(int(mode.rstrip("p")))
+            cache.set_prefill_ctas(0 if mode.endswith("p") else -1)
             for _ in range(3):
                 cache.prefill(0, seqs, [c_rows] * bp, q, o)
             torch.cuda.synchronize()
@@ -45,10 +47,10 @@ def main():
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 10
             res.setdefault(mode, []).append(ms)
-            print(f"B={bp} splits={mode:2d}: {ms * 1e3:8.1f} us  {flops / ms / 1e9:7.1f} TFLOP/s  "
+            print(f"B={bp} splits={mode:>3}: {ms * 1e3:8.1f} us  {flops / ms / 1e9:7.1f} TFLOP/s  "
                   f"max|diff vs splits=1| {err:.4f}  host {host_us:.0f} us/call", flush=True)
         for mode, v in res.items():
-            print(f"  B={bp} splits={mode:2d}: min {min(v) * 1e3:7.1f} us  median {sorted(v)[len(v) // 2] * 1e3:7.1f} us "
+            print(f"  B={bp} splits={mode:>3}: min {min(v) * 1e3:7.1f} us  median {sorted(v)[len(v) // 2] * 1e3:7.1f} us "
                   f"({flops / min(v) / 1e9:.1f} TFLOP/s at min)", flush=True)
         cache.close()
 

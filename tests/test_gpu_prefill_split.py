@@ -92,7 +92,7 @@ def test_prefill_planner_small_batch_fills_sms():
     torch.cuda.synchronize()
     assert p.cache.launch_count() - before == n_one + 1, "split plan: prefill + merge kernels"
     info = p.cache.prefill_plan_info()
-    assert info["split_units"] == 16 and info["splits"] >= 2 and info["ctas"] == 16 * info["splits"], info
+    assert info["split_units"] == 16 and info["splits"] >= 2 and 1 <= info["ctas"] <= 16 * info["splits"], info
     check_close(got, _oracle_prefill(p, [s], [512], q), "prefill planner small batch")
 
 
@@ -103,3 +103,54 @@ def test_prefill_split_invalid_count():
         p.cache.set_prefill_splits(17)
     with pytest.raises(Exception):
         p.cache.set_prefill_splits(-1)
+
+
+@pytest.mark.parametrize("hq,hkv,d,P", [(32, 8, 128, 16), (6, 2, 64, 32), (3, 1, 128, 64)])
+@pytest.mark.parametrize("ctas,splits", [(1, 1), (3, 1), (5, 3), (2, 0), (-1, 0)])
+def test_prefill_persistent_many_items_per_cta(hq, hkv, d, P, ctas, splits):
+    """The persistent kernel with the CTA count capped so every CTA loops over many items:
+    short items (1 key tile) next to long ones, G odd (a dead second slot in ragged items),
+    split pieces; parity and agreement with the one-CTA-per-item kernel."""
+    shape = Shape(1, hq, hkv, d, P)
+    p = Pair(shape, num_pages=4096, max_seqs=4, max_pages_per_seq=1024)
+    scripts = [[("latent", 128), ("latent", 8), ("tokens", 700)],
+               [("tokens", 77)],
+               [("latent", 128)] * 2 + [("tokens", 1500)]]
+    seqs = [p.build(sc) for sc in scripts]
+    q_lens = [300, 1, 385]
+    q = p.queries(sum(q_lens))
+    ref = _oracle_prefill(p, seqs, q_lens, q)
+    p.cache.set_prefill_splits(splits)
+    p.cache.set_prefill_ctas(ctas)
+    got = p.cache.prefill(0, seqs, q_lens, q.cuda())
+    torch.cuda.synchronize()
+    info = p.cache.prefill_plan_info()
+    if ctas > 0:
+        assert 1 <= info["ctas"] <= ctas, info
+    check_close(got, ref, f"persistent prefill ctas={ctas} splits={splits} {hq}/{hkv}/{d}/P{P}")
+
+
+def test_prefill_persistent_span():
+    shape = Shape(1, 32, 8, 128, 16)
+    p = Pair(shape, num_pages=2048, max_seqs=8, max_pages_per_seq=256)
+    cases = [(900, 16, 150), (40, 128, 200), (257, 64, 1)]
+    seqs, q_lens, spans = [], [], []
+    for n1, m, n3 in cases:
+        s = p.new_seq()
+        p.tokens([s], [n1])
+        p.latent(s, m)
+        p.tokens([s], [n3])
+        seqs.append(s)
+        q_lens.append(m + n3)
+        spans.append((0, n1, n1 + m))
+    q = p.queries(sum(q_lens))
+    p.cache.set_prefill_ctas(2)
+    p.cache.set_prefill_splits(2)
+    got = p.cache.prefill_span(0, seqs, q_lens, spans, q.cuda())
+    torch.cuda.synchronize()
+    ref, off = [], 0
+    for s, ql, (lo, hi, qf) in zip(seqs, q_lens, spans):
+        k, v = p.orc.logical_kv(s, 0)
+        ref.append(attend_span(f64(q[off:off + ql]), k, v, shape.scale, lo, hi, qf))
+        off += ql
+    check_close(got, np.concatenate(ref), "persistent prefill span")
