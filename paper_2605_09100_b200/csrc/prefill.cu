@@ -59,8 +59,14 @@ namespace {
 #endif
 constexpr int kBM = 128;   // query rows per slot
 constexpr int kBN = 128;   // key slots per tile
-constexpr int kNK = HPA_SM16 ? 2 : 3;  // K ring depth (2 leaves room for the max exchange)
-constexpr int kNV = 2;     // V ring depth
+#ifndef HPA_PF_NK
+#define HPA_PF_NK (HPA_SM16 ? 2 : 3)  // K ring depth (2 leaves room for the SM16 max exchange)
+#endif
+#ifndef HPA_PF_NV
+#define HPA_PF_NV 2  // V ring depth (NK 2 / NV 3 measured the same)
+#endif
+constexpr int kNK = HPA_PF_NK;
+constexpr int kNV = HPA_PF_NV;
 constexpr int kNC = 3;     // mask-index ring depth
 constexpr int kSoftWarps = HPA_SM16 ? 16 : 8;
 constexpr int kThreads = (kSoftWarps + 4) * 32;  // softmax warpgroups + producer / MMA / V producer / spare

@@ -9,14 +9,14 @@ from paper_2605_09100_b200._lib import LIB
 from workloads import qwen3_8b_shape
 shape = qwen3_8b_shape(16)
 cache, seqs, _ = build_decode_cache(torch, Cache, shape, 4, 8, 16384 + 2048, 0, 0, seed=777)
-buf = torch.zeros(40 * 64, dtype=torch.int64, device="cuda")
+buf = torch.zeros(4096 + 8 * 8192, dtype=torch.int64, device="cuda")  # events + CTA timeline
 LIB.hpa_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 LIB.hpa_debug_trace(cache._h, ctypes.c_void_p(buf.data_ptr()))
 q = torch.randn((4 * 2048, 32, 128), device="cuda").to(torch.bfloat16)
 for _ in range(3):
     cache.prefill(0, seqs, [2048] * 4, q)
 torch.cuda.synchronize()
-t = buf.view(40, 64).cpu().long()
+t = buf[:40 * 64].view(40, 64).cpu().long()
 J = range(20, 30)
 per = [int(t[7, j + 1] - t[7, j]) for j in J]
 print("period (s_full0 j -> j+1):", per, "mean", sum(per) / len(per))
