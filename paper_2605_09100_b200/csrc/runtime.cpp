@@ -629,10 +629,10 @@ int32_t plan_request_splits(const hpa_cache_t* c, int32_t n, const int32_t* seq_
 // length: B = 1 of configs[2] is 256 units on 148 SMs, 1.73 waves of work in 2 waves. The
 // plan keeps the L2-friendly dispatch order and splits the units dispatched last -- those of
 // the under-filled last wave, optionally one more wave's worth -- into s key ranges whose
-// pieces fill the SMs;
-// each split unit's pieces are merged by LSE (prefill_combine_kernel). Chosen by a greedy
-// list-scheduling simulation of the hardware's in-order CTA dispatch, in key tiles:
-//   unit = tiles(i_max) + o,  piece = tiles / s + o,  merge = c_m + partial bytes / bandwidth.
+// pieces fill the SMs; each split unit's pieces are merged by LSE (prefill_combine_kernel).
+// Chosen by a greedy list-scheduling simulation of the hardware's in-order CTA dispatch, in
+// key tiles: unit = tiles(i_max) + o, piece = tiles / s + o', merge = c_m + partial bytes /
+// bandwidth (o, o' measured per CTA).
 
 // Greedy in-order dispatch onto W SMs (min-heap of the times the SMs become free): `items`
 // are appended to the state `heap` (W entries); returns the makespan of the state.
