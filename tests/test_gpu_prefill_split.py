@@ -154,3 +154,32 @@ def test_prefill_persistent_span():
         ref.append(attend_span(f64(q[off:off + ql]), k, v, shape.scale, lo, hi, qf))
         off += ql
     check_close(got, np.concatenate(ref), "persistent prefill span")
+
+
+@pytest.mark.parametrize("splits", [0, 3])
+def test_prefill_plan_cache_follows_table_changes(splits):
+    """The cached prefill plan (tile ranges computed on the host) must be rebuilt when the
+    table changes under an identical call (same sequence ids and q_lens): after appends, after a
+    latent set is replaced by one of another size, and after a latent set is removed."""
+    shape = Shape(1, 8, 2, 128, 16)
+    p = Pair(shape, num_pages=4096, max_seqs=4, max_pages_per_seq=1024)
+    s = p.new_seq()
+    set_a = p.latent(s, 128)
+    p.tokens([s], [700])
+    p.cache.set_prefill_splits(splits)
+
+    def check(tag):
+        q = p.queries(200)
+        got = p.cache.prefill(0, [s], [200], q.cuda())
+        torch.cuda.synchronize()
+        check_close(got, _oracle_prefill(p, [s], [200], q), f"plan cache {tag} splits={splits}")
+
+    check("initial")
+    check("repeat")                     # plan reused
+    p.tokens([s], [300])
+    check("after append")
+    p.latent(s, 40, set_a)              # replace the 128-row set by a 40-row one (splice)
+    check("after replace")
+    p.cache.latent_remove(s, set_a)
+    p.orc.remove(s, set_a)
+    check("after remove")
