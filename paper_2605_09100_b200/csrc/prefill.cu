@@ -598,7 +598,9 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     if (!kCl) {  // Q tiles in flight while the CTA finishes its setup
       tma_prefetch_desc(&tm_q);
       mbar_arrive_expect_tx(q_full, slot1_live ? 2 * L::kQ : L::kQ);
-      for (int s = 0; s < (slot1_live ? 2 : 1); ++s) {
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        if (s == 1 && !slot1_live) break;
 #pragma unroll
         for (int hf = 0; hf < kHalves; ++hf)
           tma_load_3d(sQ + s * L::kQ + hf * kBM * 128, &tm_q, q_full, hf * 64, hq_s[s], q_off + mt_s[s] * kBM);
@@ -1196,8 +1198,9 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
     const int s = warp >> 2;
     const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
+    const int my_mt = s ? mt_s[1] : mt_s[0], my_hq = s ? hq_s[1] : hq_s[0];  // (no local-memory indexing)
     const int row = quarter * 32 + lane;          // query row within the slot tile == TMEM lane
-    const int t = mt_s[s] * kBM + row;
+    const int t = my_mt * kBM + row;
     const int my_i = q_base + t;                  // logical index of this query row
     const uint32_t lane_base = uint32_t(quarter * 32) << 16;
     const uint32_t tS = tmem + lane_base + s * 128;
@@ -1239,7 +1242,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       tc_fence_after();
       const bool split = part >= 0;
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-      if (split || (mt_s[s] + 1) * kBM <= q_len) {
+      if (split || (my_mt + 1) * kBM <= q_len) {
         uint8_t* stage = s == 0 ? sK : sV;
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
@@ -1275,14 +1278,14 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           } else {
 #pragma unroll
             for (int hf = 0; hf < kHalves; ++hf)
-              tma_store_3d(&tm_o, stage + hf * (kBM * 128), hf * 64, hq_s[s], q_off + mt_s[s] * kBM);
+              tma_store_3d(&tm_o, stage + hf * (kBM * 128), hf * 64, my_hq, q_off + my_mt * kBM);
           }
           bulk_commit();
           bulk_wait_read();  // the smem is released at exit
         }
         if (split) a.lse_part[int64_t(pp) * kBM + row] = l_run > 0.f ? m_run + __log2f(l_run) : -CUDART_INF_F;
       } else {
-        __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + (int64_t(q_off + t) * a.Hq + hq_s[s]) * D;
+        __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + (int64_t(q_off + t) * a.Hq + my_hq) * D;
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           float o[32];

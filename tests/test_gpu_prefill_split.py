@@ -183,3 +183,29 @@ def test_prefill_plan_cache_follows_table_changes(splits):
     p.cache.latent_remove(s, set_a)
     p.orc.remove(s, set_a)
     check("after remove")
+
+
+@pytest.mark.parametrize("token_fp8", [False, True])
+@pytest.mark.parametrize("splits", [1, 3])
+def test_prefill_upper_layer(token_fp8, splits):
+    """Prefill of layer 2 of a 3-layer cache (the K/V rows of layer l live at pool rows
+    l * NP * H_kv * P + ...): parity per layer, and each layer's output differs."""
+    shape = Shape(3, 8, 2, 128, 16)
+    p = Pair(shape, num_pages=2048, max_seqs=4, max_pages_per_seq=512, token_fp8=token_fp8,
+             num_token_pages=1024 if token_fp8 else 0)
+    seqs = [p.build([("latent", 128), ("tokens", 500)]), p.build([("tokens", 260), ("latent", 8), ("tokens", 40)])]
+    q_lens = [300, 140]
+    q = p.queries(sum(q_lens))
+    p.cache.set_prefill_splits(splits)
+    outs = []
+    for layer in (2, 0):
+        got = p.cache.prefill(layer, seqs, q_lens, q.cuda())
+        torch.cuda.synchronize()
+        ref, off = [], 0
+        for s, n in zip(seqs, q_lens):
+            k, v = p.orc.logical_kv(s, layer)
+            ref.append(attend(f64(q[off:off + n]), k, v, shape.scale))
+            off += n
+        check_close(got, np.concatenate(ref), f"prefill layer {layer} fp8={token_fp8} splits={splits}")
+        outs.append(got.float())
+    assert torch.max(torch.abs(outs[0] - outs[1])).item() > 0.05
