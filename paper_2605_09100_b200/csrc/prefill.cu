@@ -149,6 +149,8 @@ struct PSmem {
   static constexpr int kBytes = kRaw > 116 * 1024 ? kRaw : 116 * 1024;
 };
 
+static_assert(PSmem<128>::kBytes <= 227 * 1024 && PSmem<64>::kBytes <= 227 * 1024, "prefill shared memory");
+
 // ---- tcgen05 helpers
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
