@@ -505,6 +505,11 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     if (threadIdx.x == 0) printf("hpa decode: dynamic smem base 0x%x not 1024-B aligned\n", smem_u32(smem));
     __trap();
   }
+#ifdef HPA_TRACE
+  long long t_entry;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
+  if (a.trace && threadIdx.x == 0) a.trace[4 * blockIdx.x] = t_entry;
+#endif
   const int G = a.G;
   uint8_t* stages = smem + L::oRing;
   uint8_t* qbuf = smem + L::oQ;
@@ -709,7 +714,17 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     const int qb = ul & 1;
     mbar_wait(&q_full[qb], (ul >> 1) & 1);
     const int4 um = qmeta[qb];
-    if (um.x < 0) break;  // end of work
+    if (um.x < 0) {  // end of work
+#ifdef HPA_TRACE
+      if (a.trace && lane == 0) {
+        long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(reinterpret_cast<unsigned long long*>(a.trace + 4 * blockIdx.x + 1), (unsigned long long)t);
+        if (cw == 0) a.trace[4 * blockIdx.x + 2] = ul;
+      }
+#endif
+      break;
+    }
     const int b = um.x, h = um.y, split = um.z;
     if constexpr (SW) {
     // ---- swapped operands (G <= 8): S^T = K Q^T with the chunk's 16 keys in M and the

@@ -115,6 +115,7 @@ struct DecodeArgs {
   const int32_t* nsplit;    // [n] per-request split count S_b (combine); nullptr = uniform `splits`
   int32_t* sched;           // [2] unit ticket / finished-CTA counters, zero between calls
   int32_t n_units;
+  long long* trace;         // HPA_TRACE builds only: per-CTA {entry ns, last consumer exit ns, units}
 };
 // Merge of context-parallel partials: out[r][:] = sum_p 2^(lse_p - LSE) o_p / sum_p 2^(lse_p - LSE).
 cudaError_t launch_merge(int32_t n_parts, int32_t n_rows, int32_t D, const float* o_parts,

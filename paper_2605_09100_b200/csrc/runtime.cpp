@@ -1492,7 +1492,7 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
                Hq / c->cfg.num_kv_heads, c->cfg.page_size, c->cfg.num_pages, layer, S,
                scale * 1.4426950408889634f, c->fp8 ? 1 : 0, c->fp8 ? c->cfg.num_token_pages : 0,
                c->k8_pool, c->v8_pool, c->units_dev, c->nsplit_dev,
-               c->counters + size_t(c->cfg.max_seqs) * Hkv, c->plan_units};
+               c->counters + size_t(c->cfg.max_seqs) * Hkv, c->plan_units, c->trace};
   if (c->fp8 && !decode_persistent())
     return fail(HPA_ERR_UNSUPPORTED, "fp8 token pages need the persistent decode kernel");
   int launched = 0;
