@@ -26,6 +26,10 @@
  *     thread-safe. Different caches (e.g. one per GPU) are independent.
  *   - Failure atomicity: a call that returns an error leaves the cache
  *     unchanged (HPA_ERR_OUT_OF_PAGES is the "backpressure" signal of S:L388).
+ *   - Calls are not CUDA-graph capturable: each stages its per-call metadata
+ *     (table writes, scatter records, work lists) through host memory or
+ *     kernel parameters at enqueue time, so a replayed graph would repeat
+ *     stale metadata. Kernels use programmatic dependent launch instead.
  *   - bf16 everywhere (KV bytes = 2); fp32 accumulation.
  */
 #ifndef HPA_H_
