@@ -182,6 +182,29 @@ __global__ void __launch_bounds__(256) scatter_inline_kernel(PoolGeom g, int32_t
   else copy_rows<D>(g, m.rec, m.data + 2 * m.n_words);
 }
 
+// NEXT-4c prefill staging: item i = {fp8 token page, bf16 page, valid rows}; CTA (i, h) writes
+// rows 0..valid-1 of the (page, head) tile as bf16(fp32(code) * scale) (reading A20) into the
+// bf16 page's tile. Page-granular: no per-row index arrays; one 16-B store per thread.
+template <int D>
+__global__ void __launch_bounds__(256) dequant_pages_kernel(PoolGeom g, const int4* __restrict__ items) {
+  grid_dependency_wait();
+  grid_launch_dependents();
+  constexpr int kVPR = D / 8;
+  const int4 it = items[blockIdx.x];
+  const int h = blockIdx.y;
+  const int64_t row0 = (int64_t(it.x) * g.Hkv + h) * g.P;  // fp8 pool row of the tile's row 0
+  const int64_t dst0 = (int64_t(it.y) * g.Hkv + h) * g.P * D;
+  for (int v = threadIdx.x; v < it.z * kVPR; v += blockDim.x) {
+    const int r = v / kVPR, c = v % kVPR;
+    const int64_t prow = row0 + r;
+    const uint2 kc = *reinterpret_cast<const uint2*>(fp8_code_ptr(g.k8, prow, D) + c * 8);
+    const uint2 vc = *reinterpret_cast<const uint2*>(fp8_code_ptr(g.v8, prow, D) + c * 8);
+    const float ks = *fp8_scale_ptr(g.k8, prow, D), vs = *fp8_scale_ptr(g.v8, prow, D);
+    reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(g.k_pool) + dst0 + int64_t(r) * D)[c] = bf16x8_from_e4m3(kc, ks);
+    reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(g.v_pool) + dst0 + int64_t(r) * D)[c] = bf16x8_from_e4m3(vc, vs);
+  }
+}
+
 // Grid: x = table entry, y = kv head. Copies rows 0..valid-1 of the page tile
 // to out[h][pos0 + r][:].
 __global__ void __launch_bounds__(128) export_kernel(PoolGeom g, DevTables t, int32_t layer,
@@ -254,6 +277,13 @@ cudaError_t launch_scatter_inline(const PoolGeom& g, int32_t* arena, const Inlin
 cudaError_t launch_scatter_inline(const PoolGeom& g, int32_t* arena, const InlineMetaSmall& m, int64_t max_rows,
                                   cudaStream_t s) {
   return launch_scatter_inline_n(g, arena, m, max_rows, s);
+}
+
+cudaError_t launch_dequant_pages(const PoolGeom& g, const int4* items, int32_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const dim3 grid(unsigned(n), unsigned(g.Hkv));
+  if (g.D == 128) return launch_pdl(dequant_pages_kernel<128>, grid, dim3(256), 0, s, g, items);
+  return launch_pdl(dequant_pages_kernel<64>, grid, dim3(256), 0, s, g, items);
 }
 
 cudaError_t launch_export(const PoolGeom& g, DevTables t, int32_t layer, int32_t seq,

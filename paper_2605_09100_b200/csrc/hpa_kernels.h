@@ -90,6 +90,10 @@ cudaError_t launch_scatter_inline(const PoolGeom& g, int32_t* arena, const Inlin
 cudaError_t launch_scatter_inline(const PoolGeom& g, int32_t* arena, const InlineMeta& m, int64_t max_rows,
                                   cudaStream_t s);
 
+// NEXT-4c: dequantize whole fp8 token-page tiles into bf16 pages of the main pool;
+// items[n] = {fp8 token page, bf16 page, valid rows, 0} (device), g sliced to one layer.
+cudaError_t launch_dequant_pages(const PoolGeom& g, const int4* items, int32_t n, cudaStream_t s);
+
 // Logical K/V export of one (layer, seq): out bf16 [H_kv][len][d].
 cudaError_t launch_export(const PoolGeom& g, DevTables t, int32_t layer, int32_t seq,
                           int32_t n_entries_host, void* k_out, void* v_out, cudaStream_t s);

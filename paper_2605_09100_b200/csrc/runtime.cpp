@@ -1581,7 +1581,7 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
                   c->alloc.num_free());
     if (need > 0) {
       c->alloc.alloc(need, tmp_pages);
-      std::vector<int32_t> dst, src;
+      std::vector<int4> items;  // {fp8 token page, temporary bf16 page, valid rows, 0}
       int32_t k = 0;
       std::fill(seen.begin(), seen.end(), 0);
       for (int32_t i = 0; i < n_seqs; ++i) {
@@ -1592,16 +1592,14 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
         for (size_t e = 0; e < q.pages.size(); ++e) {
           if (q.meta[e] & kMetaLatent) continue;
           const int32_t t = tmp_pages[size_t(k++)], valid = q.meta[e] & kMetaRowsMask;
-          for (int32_t r = 0; r < valid; ++r) {
-            dst.push_back(t * P + r);
-            src.push_back(q.pages[e] * P + r);
-          }
+          items.push_back(make_int4(q.pages[e], t, valid, 0));
           c->pending.push_back({int32_t(c->idx(sq, int32_t(e))), t});
           restore.push_back({int32_t(c->idx(sq, int32_t(e))), q.pages[e]});
         }
       }
-      const int32_t nrows = int32_t(dst.size());
-      dst.insert(dst.end(), src.begin(), src.end());
+      // table entries -> temporary pages (one scatter launch), then the page-granular
+      // dequantization of this layer's tiles
+      if (hpa_status_t st = ship(c, s, {}, {}, 0)) return st;
       PoolGeom gl = c->geom();  // this layer only
       const int64_t bf_off = int64_t(layer) * c->cfg.num_pages * c->cfg.num_kv_heads * P * c->cfg.head_dim;
       const int64_t f8_rows = int64_t(layer) * c->cfg.num_token_pages * c->cfg.num_kv_heads * P;
@@ -1610,8 +1608,16 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
       gl.k8 = c->k8_pool + f8_rows * (c->cfg.head_dim + 4);  // whole 16-row blocks per layer
       gl.v8 = c->v8_pool + f8_rows * (c->cfg.head_dim + 4);
       gl.L = 1;
-      std::vector<ScatterRecord> recs{ScatterRecord{nullptr, nullptr, 0, 0, nrows, 0, 0, 0, 1, nrows, 0, 1}};
-      if (hpa_status_t st = ship(c, s, recs, dst, nrows, &gl)) return st;
+      const size_t ib = items.size() * sizeof(int4);
+      const size_t ioff = c->ring.reserve(ib);
+      std::memcpy(c->ring.host(ioff), items.data(), ib);
+      HPA_CUDA(c->ring.upload(ioff, ib, s));
+      int launched = 1;
+      cudaError_t ed = launch_dequant_pages(gl, reinterpret_cast<const int4*>(c->ring.dev(ioff)),
+                                            int32_t(items.size()), s);
+      c->launches += launched;
+      if (ed != cudaSuccess) return cuda_fail(ed, "dequant launch");
+      HPA_CUDA(c->ring.commit(ioff, ib, s));
     }
   }
   const int32_t D = c->cfg.head_dim, Hq = c->cfg.num_q_heads;
