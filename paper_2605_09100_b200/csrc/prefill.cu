@@ -17,8 +17,8 @@
 //      warp  8    TMA producer (all lanes build the mask indices; the page
 //                 boxes are issued in parallel by several lanes)
 //      warp  9    tcgen05 MMA issuer; owns the 512 TMEM columns
-//      warp  10   V producer (decoupled from K); warp 11 spare. setmaxnreg moves registers from warpgroup 2 (64)
-//                 to the softmax warpgroups (224).
+//      warp  10   V producer (decoupled from K); warp 11 spare. setmaxnreg moves registers
+//                 from warpgroup 2 (72) to the softmax warpgroups (216).
 //  * TMEM: S_s / P_s at columns [128 s, 128 s + 128), O_s at [256 + 128 s, ...).
 //    S = Q K^T (SS: Q and K K-major, 128-B swizzle); the softmax writes P as
 //    packed bf16 over S and O += P V runs in TS form (A = P from TMEM, B = V
@@ -31,6 +31,11 @@
 //    >= valid_rows) for the causal / partial-page mask.
 //  * Online softmax in the log2 domain with lazy rescaling: O_s in TMEM is
 //    corrected only when a row max grows by more than 2^8.
+//  * Work: a host-planned list (plan_prefill in runtime.cpp) gives each CTA its unit and
+//    key-tile range; units of an under-filled last wave are split into key ranges whose
+//    fp32 O / l + LSE partials prefill_combine_kernel merges. The epilogue stages O in the
+//    idle K/V rings and writes it with TMA stores. prefill_persistent_kernel (opt-in) runs
+//    one CTA per SM over an item list instead.
 #include "hpa_kernels.h"
 #include "ptx.cuh"
 #include <cuda_bf16.h>
