@@ -1,0 +1,92 @@
+"""Randomised parity sweeps (seeded): random head layouts, head dims, page sizes, segment
+scripts (latent sets of various sizes, partial pages, token runs), query lengths, split and
+CTA settings and GRC spans, each checked element by element against the fp64 oracle."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import attend, attend_span
+from tests.hpa_testutil import Pair, check_close, f64
+from workloads import Shape
+
+pytestmark = pytest.mark.gpu
+
+LAYOUTS = [(32, 8), (8, 2), (6, 2), (16, 1), (4, 4), (12, 4), (2, 1)]
+
+
+def _script(rng, max_rows):
+    segs, rows = [], 0
+    for _ in range(int(rng.integers(1, 6))):
+        if rng.random() < 0.4:
+            m = int(rng.choice([8, 16, 40, 128, 130]))
+            segs.append(("latent", m))
+            rows += m
+        else:
+            n = int(rng.integers(1, 600))
+            segs.append(("tokens", n))
+            rows += n
+        if rows > max_rows:
+            break
+    if all(k == "latent" for k, _ in segs):
+        segs.append(("tokens", int(rng.integers(1, 300))))
+    return segs
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_prefill_fuzz(case):
+    rng = np.random.default_rng(1000 + case)
+    hq, hkv = LAYOUTS[int(rng.integers(len(LAYOUTS)))]
+    d = int(rng.choice([64, 128]))
+    P = int(rng.choice([16, 32, 64, 128, 256]))
+    shape = Shape(2, hq, hkv, d, P)
+    p = Pair(shape, num_pages=40000 // P + 256, max_seqs=8, max_pages_per_seq=2048, seed=case)
+    n_seqs = int(rng.integers(1, 4))
+    seqs = [p.build(_script(rng, 2500)) for _ in range(n_seqs)]
+    lens = [p.cache.seq_info(s)[0] for s in seqs]
+    q_lens = [min(int(rng.integers(1, L + 1)) if rng.random() < 0.7 else L, 900) for L in lens]
+    layer = int(rng.integers(2))
+    p.cache.set_prefill_splits(int(rng.choice([0, 0, 1, 2, 3, 5, 16])))
+    p.cache.set_prefill_ctas(int(rng.choice([-1, -1, 0, 1, 3])))
+    q = p.queries(sum(q_lens))
+    use_span = rng.random() < 0.3
+    if use_span:
+        spans = []
+        for L, ql in zip(lens, q_lens):
+            q_from = L - ql
+            lo = int(rng.integers(0, max(1, q_from)))
+            hi = int(rng.integers(lo, q_from + 1))
+            spans.append((lo, hi, q_from))
+        got = p.cache.prefill_span(layer, seqs, q_lens, spans, q.cuda())
+    else:
+        got = p.cache.prefill(layer, seqs, q_lens, q.cuda())
+    torch.cuda.synchronize()
+    ref, off = [], 0
+    for i, (s, n) in enumerate(zip(seqs, q_lens)):
+        k, v = p.orc.logical_kv(s, layer)
+        if use_span:
+            lo, hi, qf = spans[i]
+            ref.append(attend_span(f64(q[off:off + n]), k, v, shape.scale, lo, hi, qf))
+        else:
+            ref.append(attend(f64(q[off:off + n]), k, v, shape.scale))
+        off += n
+    check_close(got, np.concatenate(ref), f"prefill fuzz case {case}: {hq}/{hkv}/{d}/P{P} q_lens={q_lens}")
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_decode_fuzz(case):
+    rng = np.random.default_rng(2000 + case)
+    hq, hkv = LAYOUTS[int(rng.integers(len(LAYOUTS)))]
+    d = int(rng.choice([64, 128]))
+    P = int(rng.choice([16, 32, 64, 128, 256]))
+    shape = Shape(2, hq, hkv, d, P)
+    p = Pair(shape, num_pages=40000 // P + 256, max_seqs=16, max_pages_per_seq=2048, seed=case)
+    n_seqs = int(rng.integers(1, 9))
+    seqs = [p.build(_script(rng, 3000)) for _ in range(n_seqs)]
+    layer = int(rng.integers(2))
+    p.cache.set_decode_splits(int(rng.choice([0, 0, 1, 2, 7])))
+    q = p.queries(n_seqs)
+    got = p.cache.decode(layer, seqs, q.cuda())
+    torch.cuda.synchronize()
+    ref = np.stack([attend(f64(q[i:i + 1]), *p.orc.logical_kv(s, layer), shape.scale)[0]
+                    for i, s in enumerate(seqs)])
+    check_close(got, ref, f"decode fuzz case {case}: {hq}/{hkv}/{d}/P{P} n={n_seqs}")
