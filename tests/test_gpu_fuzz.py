@@ -90,3 +90,38 @@ def test_decode_fuzz(case):
     ref = np.stack([attend(f64(q[i:i + 1]), *p.orc.logical_kv(s, layer), shape.scale)[0]
                     for i, s in enumerate(seqs)])
     check_close(got, ref, f"decode fuzz case {case}: {hq}/{hkv}/{d}/P{P} n={n_seqs}")
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_fp8_token_pages_fuzz(case):
+    """fp8 (e4m3) token pages with bf16 latent pages (reading A20): random shapes and scripts,
+    decode and prefill on a random layer against the oracle's quantized cache."""
+    rng = np.random.default_rng(3000 + case)
+    hq, hkv = LAYOUTS[int(rng.integers(len(LAYOUTS)))]
+    d = int(rng.choice([64, 128]))
+    P = int(rng.choice([16, 32, 64, 128, 256]))
+    shape = Shape(2, hq, hkv, d, P)
+    npg = 40000 // P + 256
+    p = Pair(shape, num_pages=npg, max_seqs=8, max_pages_per_seq=2048, seed=case, token_fp8=True,
+             num_token_pages=npg)
+    n_seqs = int(rng.integers(1, 5))
+    seqs = [p.build(_script(rng, 2500)) for _ in range(n_seqs)]
+    layer = int(rng.integers(2))
+    q = p.queries(n_seqs)
+    got = p.cache.decode(layer, seqs, q.cuda())
+    torch.cuda.synchronize()
+    ref = np.stack([attend(f64(q[i:i + 1]), *p.orc.logical_kv(s, layer), shape.scale)[0]
+                    for i, s in enumerate(seqs)])
+    check_close(got, ref, f"fp8 decode fuzz case {case}")
+    lens = [p.cache.seq_info(s)[0] for s in seqs]
+    q_lens = [min(int(rng.integers(1, L + 1)), 600) for L in lens]
+    p.cache.set_prefill_splits(int(rng.choice([0, 1, 3])))
+    qp = p.queries(sum(q_lens))
+    got = p.cache.prefill(layer, seqs, q_lens, qp.cuda())
+    torch.cuda.synchronize()
+    ref, off = [], 0
+    for s, n in zip(seqs, q_lens):
+        k, v = p.orc.logical_kv(s, layer)
+        ref.append(attend(f64(qp[off:off + n]), k, v, shape.scale))
+        off += n
+    check_close(got, np.concatenate(ref), f"fp8 prefill fuzz case {case}")
