@@ -125,3 +125,83 @@ def test_fp8_token_pages_fuzz(case):
         ref.append(attend(f64(qp[off:off + n]), k, v, shape.scale))
         off += n
     check_close(got, np.concatenate(ref), f"fp8 prefill fuzz case {case}")
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_cache_ops_fuzz_with_attention(seed):
+    """400 random cache operations -- appends, latent installs and replacements of other
+    sizes, removals, in-cache compression, sharing a set from another request, releases --
+    with decode and prefill parity for every live request every 40 operations."""
+    import random
+    from paper_2605_09100_b200 import HPAError
+    rng = random.Random(seed)
+    nrng = np.random.default_rng(seed)
+    shape = Shape(1, 8, 2, 128, int(rng.choice([16, 32])))
+    p = Pair(shape, num_pages=1200, max_seqs=6, max_pages_per_seq=256, seed=seed)
+    live = []
+
+    def latents(s):
+        return [sg.set_id for sg in p.orc.seqs[s] if sg.kind == "latent"]
+
+    def check(tag):
+        alive = [s for s in live if p.cache.seq_info(s)[0] > 0]
+        if not alive:
+            return
+        q = p.queries(len(alive))
+        got = p.cache.decode(0, alive, q.cuda())
+        torch.cuda.synchronize()
+        ref = np.stack([attend(f64(q[i:i + 1]), *p.orc.logical_kv(s, 0), shape.scale)[0]
+                        for i, s in enumerate(alive)])
+        check_close(got, ref, f"ops fuzz decode {tag}")
+        lens = [p.cache.seq_info(s)[0] for s in alive]
+        q_lens = [int(nrng.integers(1, min(L, 300) + 1)) for L in lens]
+        qp = p.queries(sum(q_lens))
+        got = p.cache.prefill(0, alive, q_lens, qp.cuda())
+        torch.cuda.synchronize()
+        ref, off = [], 0
+        for s, n in zip(alive, q_lens):
+            k, v = p.orc.logical_kv(s, 0)
+            ref.append(attend(f64(qp[off:off + n]), k, v, shape.scale))
+            off += n
+        check_close(got, np.concatenate(ref), f"ops fuzz prefill {tag}")
+
+    for step in range(400):
+        op = rng.random()
+        try:
+            if op < 0.12 and len(live) < 6:
+                live.append(p.new_seq())
+            elif op < 0.40 and live:
+                p.tokens([rng.choice(live)], [rng.randint(1, 90)])
+            elif op < 0.58 and live:
+                s = rng.choice(live)
+                ids = latents(s)
+                sid = rng.choice(ids) if ids and rng.random() < 0.5 else -1
+                p.latent(s, rng.choice([8, 16, 40, 64, 128]), set_id=sid)
+            elif op < 0.66 and live:
+                s = rng.choice(live)
+                ids = latents(s)
+                if ids:
+                    sid = rng.choice(ids)
+                    p.cache.latent_remove(s, sid)
+                    p.orc.remove(s, sid)
+            elif op < 0.76 and live:
+                s = rng.choice(live)
+                segs = p.orc.seqs[s]
+                if segs and segs[-1].kind == "token" and segs[-1].rows >= 24:
+                    m = rng.randint(1, 8)
+                    n_doc = rng.randint(0, segs[-1].rows - m)
+                    assert p.cache.compress(s, n_doc, m) == p.orc.compress(s, n_doc, m)
+            elif op < 0.84 and len(live) >= 2:
+                src, dst = rng.sample(live, 2)
+                ids = latents(src)
+                if ids:
+                    sid = rng.choice(ids)
+                    assert p.cache.latent_share(dst, src, sid) == p.orc.share(dst, src, sid)
+            elif op < 0.90 and live:
+                s = live.pop(rng.randrange(len(live)))
+                p.cache.seq_release(s)
+                p.orc.release(s)
+        except HPAError as e:
+            assert e.name in ("HPA_ERR_OUT_OF_PAGES", "HPA_ERR_SEQ_CAPACITY"), e
+        if step % 40 == 39:
+            check(f"seed {seed} step {step}")
