@@ -267,6 +267,15 @@ class StagingRing {
   cudaError_t upload(size_t off, size_t n, cudaStream_t s) {
     return cudaMemcpyAsync(dev_ + off, host_ + off, n, cudaMemcpyHostToDevice, s);
   }
+  // The same copy on a side stream `cs`, with `s` waiting for it: the copy engine can move the
+  // metadata while `s` still runs earlier kernels (reserve() already guaranteed that no earlier
+  // consumer of this region is still reading it).
+  cudaError_t upload_side(size_t off, size_t n, cudaStream_t s, cudaStream_t cs, cudaEvent_t ev) {
+    cudaError_t e = cudaMemcpyAsync(dev_ + off, host_ + off, n, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(ev, cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev, 0);
+    return e;
+  }
   cudaError_t commit(size_t off, size_t n, cudaStream_t s) {
     cudaEvent_t ev;
     if (!pool_.empty()) {
@@ -369,6 +378,7 @@ struct hpa_cache {
   size_t pf_part_rows = 0;
   // host-staged installs (NEXT-3): device payload buffer filled on copy_stream
   cudaStream_t copy_stream = nullptr;
+  cudaEvent_t upload_done = nullptr;  // staging-ring metadata copies issued on copy_stream
   cudaEvent_t copy_done = nullptr, payload_free = nullptr;
   char* payload_dev = nullptr;
   size_t payload_cap = 0;
@@ -510,7 +520,7 @@ hpa_status_t ship(hpa_cache_t* c, cudaStream_t s, const std::vector<ScatterRecor
                 b.bytes.size(), c->ring.cap());
   const size_t off = c->ring.reserve(b.bytes.size());
   std::memcpy(c->ring.host(off), b.bytes.data(), b.bytes.size());
-  HPA_CUDA(c->ring.upload(off, b.bytes.size(), s));
+  HPA_CUDA(c->ring.upload_side(off, b.bytes.size(), s, c->copy_stream, c->upload_done));
   char* d = c->ring.dev(off);
   HPA_CUDA(launch_scatter(gm, c->arena, reinterpret_cast<const WordWrite*>(d + o_words),
                           int32_t(c->pending.size()), reinterpret_cast<const ScatterRecord*>(d + o_recs),
@@ -912,6 +922,12 @@ hpa_status_t hpa_cache_create(const hpa_config_t* cfg, hpa_cache_t** out) {
     if (c->v8_pool) cudaFree(c->v8_pool);
     if (c->arena) cudaFree(c->arena);
     if (c->counters) cudaFree(c->counters);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->upload_done) cudaEventDestroy(c->upload_done);
+    if (c->copy_done) cudaEventDestroy(c->copy_done);
+    if (c->payload_free) cudaEventDestroy(c->payload_free);
+    c->copy_stream = nullptr;
+    c->upload_done = c->copy_done = c->payload_free = nullptr;
     c->ring.destroy();
   };
   cudaError_t e;
@@ -954,6 +970,7 @@ hpa_status_t hpa_cache_create(const hpa_config_t* cfg, hpa_cache_t** out) {
     return fail(HPA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the KV pools");
   }
   if ((e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&c->upload_done, cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&c->copy_done, cudaEventDisableTiming)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&c->payload_free, cudaEventDisableTiming)) != cudaSuccess) {
     cleanup();
@@ -990,6 +1007,7 @@ hpa_status_t hpa_cache_destroy(hpa_cache_t* c) {
   if (c->nsplit_dev) cudaFree(c->nsplit_dev);
   if (c->payload_dev) cudaFree(c->payload_dev);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->upload_done) cudaEventDestroy(c->upload_done);
   if (c->copy_done) cudaEventDestroy(c->copy_done);
   if (c->payload_free) cudaEventDestroy(c->payload_free);
   c->ring.destroy();
@@ -1611,7 +1629,7 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
       const size_t ib = items.size() * sizeof(int4);
       const size_t ioff = c->ring.reserve(ib);
       std::memcpy(c->ring.host(ioff), items.data(), ib);
-      HPA_CUDA(c->ring.upload(ioff, ib, s));
+      HPA_CUDA(c->ring.upload_side(ioff, ib, s, c->copy_stream, c->upload_done));
       int launched = 1;
       cudaError_t ed = launch_dequant_pages(gl, reinterpret_cast<const int4*>(c->ring.dev(ioff)),
                                             int32_t(items.size()), s);
@@ -1646,7 +1664,7 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
     if (cbytes) std::memcpy(c->ring.host(off) + wbytes, plan.cta_off.data(), cbytes);
   }
   std::memcpy(c->ring.host(off) + wbytes + cbytes, meta.data(), meta.size() * 4);
-  HPA_CUDA(c->ring.upload(off, bytes, s));
+  HPA_CUDA(c->ring.upload_side(off, bytes, s, c->copy_stream, c->upload_done));
   const int32_t* dmeta = reinterpret_cast<const int32_t*>(c->ring.dev(off) + wbytes + cbytes);
   CUtensorMap tm_q, tm_o;
   if (!make_map_q(&tm_q, q, uint64_t(total_q), uint64_t(Hq), uint64_t(D), 128) ||
