@@ -1382,6 +1382,9 @@ prefill_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
   grid_launch_dependents();
   const int beg = a.cta_off[blockIdx.x], end = a.cta_off[blockIdx.x + 1];
   if (beg >= end) return;
+#ifdef HPA_TRACE
+  if (threadIdx.x == 0) CTA_STAMP(0, gtimer());
+#endif
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1440,6 +1443,9 @@ prefill_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int P = a.P, lp = a.log2P;
+#ifdef HPA_TRACE
+  if (threadIdx.x == 0) CTA_STAMP(1, gtimer());
+#endif
 
   if (warp >= kSoftWarps) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kOtherRegs));
   if (warp == kProducerWarp) {
@@ -1672,6 +1678,9 @@ prefill_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
           continue;
         }
         mbar_wait(&s_full[s], ns & 1);
+#ifdef HPA_TRACE
+        if (ns == 0 && threadIdx.x == 0) CTA_STAMP(2, gtimer());
+#endif
         ++ns;
         tc_fence_after();
         softmax_tile<D>(a, s, quarter, row, lane, j, tS, tO, sC + cs * (kBN + 4), &c_full[cs], (g / kNC) & 1,
@@ -1679,6 +1688,9 @@ prefill_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
       }
       if (!live) continue;
       mbar_wait(my_o_full, no & 1);
+#ifdef HPA_TRACE
+      if (threadIdx.x == 0 && it == end - 1) CTA_STAMP(3, gtimer());
+#endif
       ++no;
       tc_fence_after();
       // epilogue (row stores: the K/V rings already hold the next item's tiles)
@@ -1723,6 +1735,16 @@ prefill_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
   }
   tc_fence_before();
   __syncthreads();
+#ifdef HPA_TRACE
+  if (threadIdx.x == 0) {
+    CTA_STAMP(4, gtimer());
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    CTA_STAMP(5, smid);
+    CTA_STAMP(6, end - beg);
+    CTA_STAMP(7, 1);
+  }
+#endif
   if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));

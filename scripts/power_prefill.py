@@ -16,6 +16,7 @@ shape = qwen3_8b_shape(16)
 bp = int(os.environ.get("B", "4"))
 cache, seqs, _ = bench.build_decode_cache(torch, Cache, shape, bp, 8, 16384 + 2048, 0, 0, seed=777)
 q = torch.randn((bp * 2048, 32, 128), device="cuda").to(torch.bfloat16)
+cache.set_prefill_ctas(int(os.environ.get("PF_CTAS", "-1")))  # 0: the persistent kernel
 o = torch.empty_like(q)
 for _ in range(3):
     cache.prefill(0, seqs, [2048] * bp, q, o)
@@ -39,4 +40,4 @@ torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / n
 time.sleep(0.3)
 smi.terminate()
-print(f"B={bp}: {n} calls, {ms * 1e3:.1f} us per call, {flops / ms / 1e9:.1f} TFLOP/s sustained")
+print(f"B={bp} ctas={os.environ.get('PF_CTAS', '-1')}: {n} calls, {ms * 1e3:.1f} us per call, {flops / ms / 1e9:.1f} TFLOP/s sustained")

@@ -13,6 +13,7 @@ buf = torch.zeros(4096 + 8 * 8192, dtype=torch.int64, device="cuda")  # events +
 LIB.hpa_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 LIB.hpa_debug_trace(cache._h, ctypes.c_void_p(buf.data_ptr()))
 q = torch.randn((4 * 2048, 32, 128), device="cuda").to(torch.bfloat16)
+cache.set_prefill_ctas(int(os.environ.get("PF_CTAS", "-1")))  # 0: the persistent kernel
 for _ in range(3):
     cache.prefill(0, seqs, [2048] * 4, q)
 torch.cuda.synchronize()

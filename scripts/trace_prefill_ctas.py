@@ -17,18 +17,20 @@ from paper_2605_09100_b200._lib import LIB  # noqa: E402
 from workloads import qwen3_8b_shape  # noqa: E402
 
 B = int(os.environ.get("B", "4"))
+C = int(os.environ.get("C", "2048"))
 for splits in [int(x) for x in os.environ.get("SPLITS", "1,2").split(",")]:
     shape = qwen3_8b_shape(16)
-    cache, seqs, _ = build_decode_cache(torch, Cache, shape, B, 8, 16384 + 2048, 0, 0, seed=777)
+    cache, seqs, _ = build_decode_cache(torch, Cache, shape, B, 8, 16384 + C, 0, 0, seed=777)
     cache.set_prefill_splits(splits)
+    cache.set_prefill_ctas(int(os.environ.get("PF_CTAS", "-1")))  # 0: persistent (n_tiles column = items)
     n_cta_max = B * 16 * 16 * 16
     buf = torch.zeros(4096 + 8 * n_cta_max, dtype=torch.int64, device="cuda")
     LIB.hpa_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
     LIB.hpa_debug_trace(cache._h, ctypes.c_void_p(buf.data_ptr()))
-    q = torch.randn((B * 2048, 32, 128), device="cuda").to(torch.bfloat16)
+    q = torch.randn((B * C, 32, 128), device="cuda").to(torch.bfloat16)
     for _ in range(3):
         buf.zero_()
-        cache.prefill(0, seqs, [2048] * B, q)
+        cache.prefill(0, seqs, [C] * B, q)
         torch.cuda.synchronize()
     t = buf[4096:].view(-1, 8).cpu().numpy()
     t = t[t[:, 7] == 1]
