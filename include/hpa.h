@@ -256,9 +256,11 @@ hpa_status_t hpa_set_decode_splits(hpa_cache_t* c, int32_t splits);
  * tiles into that many pieces (merged by LSE), 16 = no host work list (one CTA per unit of a
  * grid; each CTA searches the block table for its key-tile range). INVALID_ARG outside [0, 16]. */
 hpa_status_t hpa_set_prefill_splits(hpa_cache_t* c, int32_t splits);
-/* Testing / tuning hook: prefill CTAs. -1 = one CTA per planned item (default); 0 = the
- * persistent kernel, one CTA per SM looping over the planned items; n > 0 = persistent with at
- * most n CTAs. INVALID_ARG below -1. */
+/* Testing / tuning hook: prefill CTAs. -1 = one CTA per planned item (default; batches of
+ * >= 4 waves with G % 4 == 0 run the items as 2-CTA clusters sharing K/V by multicast);
+ * -2 = one CTA per item, clusters forced whenever G % 4 == 0; 0 = the persistent kernel, one
+ * CTA per SM looping over the planned items; n > 0 = persistent with at most n CTAs.
+ * INVALID_ARG below -2. */
 hpa_status_t hpa_set_prefill_ctas(hpa_cache_t* c, int32_t n);
 /* Introspection of the last hpa_prefill / hpa_prefill_span plan: *n_ctas prefill CTAs
  * launched, *n_split_units units split into *splits key ranges each (0 / 1 when none), or

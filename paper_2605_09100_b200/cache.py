@@ -324,7 +324,8 @@ class Cache:
         check(LIB.hpa_set_prefill_splits(self._h, splits))
 
     def set_prefill_ctas(self, n: int) -> None:
-        """-1 = one CTA per item (default), 0 = persistent prefill on every SM, n > 0 = at most n CTAs."""
+        """-1 = one CTA per item (default), -2 = one CTA per item as forced 2-CTA clusters (G % 4 == 0),
+        0 = persistent prefill on every SM, n > 0 = at most n CTAs."""
         check(LIB.hpa_set_prefill_ctas(self._h, n))
 
     def prefill_plan_info(self) -> dict:

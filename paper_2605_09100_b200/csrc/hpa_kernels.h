@@ -165,9 +165,11 @@ struct PrefillArgs {
   // [cta_off[c], cta_off[c + 1]) of `work`, in order; n_ctas <= #SMs.
   const int32_t* cta_off;
   int32_t n_ctas;
+  int32_t mc2;              // HPA_PF_MC2 builds: work items 2k, 2k+1 are a 2-CTA cluster sharing K/V
 };
 // Split-KV prefill (work lists) is built in the default kernel configuration only.
 bool prefill_split_supported();
+bool prefill_mc2_supported(int32_t G);
 // tm_q / tm_o: 3-D maps over q / out [sum q][Hq][d] with box {64, 1, 128};
 // tm_k / tm_v: 2-D maps over the pools with box {64, min(P,128)};
 // tm_op: 2-D fp32 map over o_part [rows][d] with box {32, 128} (work lists with splits).

@@ -64,6 +64,13 @@ namespace {
 #endif
 constexpr int kBM = 128;   // query rows per slot
 constexpr int kBN = 128;   // key slots per tile
+#ifndef HPA_PF_MC2
+#define HPA_PF_MC2 1  // default kernel as 2-CTA clusters (the 4 q-heads of a KV head) sharing K/V by TMA multicast
+#endif
+#if HPA_PF1
+#undef HPA_PF_MC2
+#define HPA_PF_MC2 0
+#endif
 #ifndef HPA_PF_NK
 #define HPA_PF_NK (HPA_SM16 ? 2 : 3)  // K ring depth (2 leaves room for the SM16 max exchange)
 #endif
@@ -517,8 +524,11 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #endif
   // unit (b, y, x) and key-range piece: from the work list (plan_prefill) or the grid
   int ux = blockIdx.x, uy = blockIdx.y, piece = 0, part = -1;
-  int b = kCl ? int(blockIdx.z) / (a.Hq / 2) : int(blockIdx.z);
-  const bool listed = !kCl && !HPA_PF1 && a.work != nullptr;
+  // kCl with HPA_PF1: the PF1 cluster mapping below; kCl without it (HPA_PF_MC2): two listed
+  // units of one KV head (consecutive work items) share every K/V box by multicast
+  constexpr bool kPf1Cl = kCl && HPA_PF1;
+  int b = kPf1Cl ? int(blockIdx.z) / (a.Hq / 2) : int(blockIdx.z);
+  const bool listed = !HPA_PF1 && a.work != nullptr;
   // listed: wr = {jb, n_tiles, skip_a, n_skip}, wq = {seq, q_len, q_off, seq_len}, wn = {n_ent}
   // (four independent 16-B loads instead of a chain of dependent metadata loads)
   int4 wr = make_int4(0, 0, 0, 0), wq = make_int4(0, 0, 0, 0), wn = make_int4(0, 0, 0, 0);
@@ -536,7 +546,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   const int q_len = listed ? wq.y : a.q_len[b];
   // slot -> (q-head, row tile)
   int hq_s[2], mt_s[2];
-  if (kCl) {  // cluster (x = member, y = row tile, z = head pair + Hq/2 * sequence)
+  if (kPf1Cl) {  // cluster (x = member, y = row tile, z = head pair + Hq/2 * sequence)
     hq_s[0] = hq_s[1] = 2 * (int(blockIdx.z) % (a.Hq / 2)) + int(blockIdx.x);
     mt_s[0] = blockIdx.y;
     mt_s[1] = INT_MAX / kBM;
@@ -602,7 +612,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     mbar_init(o_ready, 1);
     for (int i = 0; i < kNC; ++i) { mbar_init(&c_full[i], 1); mbar_init(&c_empty[i], kSoftWarps); }
     fence_barrier_init();
-    if (!kCl) {  // Q tiles in flight while the CTA finishes its setup
+    if (!kPf1Cl) {  // Q tiles in flight while the CTA finishes its setup
       tma_prefetch_desc(&tm_q);
       mbar_arrive_expect_tx(q_full, slot1_live ? 2 * L::kQ : L::kQ);
 #pragma unroll
@@ -684,7 +694,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     if (lane == 0) {
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
-      if (kCl) {
+      if (kPf1Cl) {
         tma_prefetch_desc(&tm_q);
         mbar_arrive_expect_tx(q_full, slot1_live ? 2 * L::kQ : L::kQ);
         for (int s = 0; s < (slot1_live ? 2 : 1); ++s) {
@@ -902,10 +912,20 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         if (elect_one()) tc_commit(bar);
         __syncwarp();
       };
+      // a K / V stage is refilled (by multicast into both CTAs) only after both CTAs' MMAs
+      // have read it: with kCl the release arrives on both CTAs' barriers (count 2)
+      auto release = [&](uint64_t* bar) {
+        if (kCl) {
+          if (elect_one()) tc_commit_mc(bar, kPair);
+          __syncwarp();
+        } else {
+          commit(bar);
+        }
+      };
       mbar_wait(&k_full[0], 0);
       tc_fence_after();
       for (int s = 0; s < nslot; ++s) issue_s(s, 0);
-      commit(&k_empty[0]);
+      release(&k_empty[0]);
       for (int j = 0; j < n_tiles; ++j) {
         const bool more = j + 1 < n_tiles;
         mbar_wait(&v_full[j % kNV], (j / kNV) & 1);
@@ -921,7 +941,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           if (lane == 0) TRACE(5 + s, j);
           tc_fence_after();
           issue_pv_half(s, j, 1);
-          if (s == nslot - 1) commit(&v_empty[j % kNV]);
+          if (s == nslot - 1) release(&v_empty[j % kNV]);
           if (more) {
             if (!k_ready) {  // K(j+1) is only needed here, not by PV(j)
               mbar_wait(&k_full[(j + 1) % kNK], ((j + 1) / kNK) & 1);
@@ -932,7 +952,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             issue_s(s, j + 1);  // overwrites S/P s after PV s has read P (in-order pipe)
           }
         }
-        if (more) commit(&k_empty[(j + 1) % kNK]);
+        if (more) release(&k_empty[(j + 1) % kNK]);
       }
       commit(o_full);
     }
@@ -1867,11 +1887,30 @@ cudaError_t launch_prefill_d(const CUtensorMap& tm_q, const CUtensorMap& tm_k, c
   }
   if (!HPA_PF1 && a.work) {  // split-KV work list: one CTA per (unit, piece), then the merge
     if (a.n_work == 0) return cudaSuccess;
-    cudaError_t e =
-        a.cta_off ? launch_pdl(prefill_persistent_kernel<D>, dim3(unsigned(a.n_ctas)), dim3(kThreads),
-                               PSmem<D>::kBytes, s, tm_q, tm_k, tm_v, a)
-                  : launch_pdl(prefill_kernel<D, false>, dim3(unsigned(a.n_work)), dim3(kThreads), PSmem<D>::kBytes,
-                               s, tm_q, tm_k, tm_v, tm_o, tm_op, a);
+    cudaError_t e;
+    if (a.cta_off) {
+      e = launch_pdl(prefill_persistent_kernel<D>, dim3(unsigned(a.n_ctas)), dim3(kThreads), PSmem<D>::kBytes, s,
+                     tm_q, tm_k, tm_v, a);
+    } else if (HPA_PF_MC2 && a.mc2) {  // consecutive work items pair up as 2-CTA clusters
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(unsigned(a.n_work));
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = PSmem<D>::kBytes;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[2];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 2;
+      e = cudaLaunchKernelEx(&cfg, prefill_kernel<D, true>, tm_q, tm_k, tm_v, tm_o, tm_op, a);
+    } else {
+      e = launch_pdl(prefill_kernel<D, false>, dim3(unsigned(a.n_work)), dim3(kThreads), PSmem<D>::kBytes, s, tm_q,
+                     tm_k, tm_v, tm_o, tm_op, a);
+    }
     if (e != cudaSuccess || a.n_parts == 0) return e;
     ++*launches;
     return launch_combine_d<D>(a, s);
@@ -1887,6 +1926,7 @@ cudaError_t launch_prefill_d(const CUtensorMap& tm_q, const CUtensorMap& tm_k, c
 }  // namespace
 
 bool prefill_split_supported() { return !HPA_PF1 && !HPA_SM16; }
+bool prefill_mc2_supported(int32_t G) { return HPA_PF_MC2 && !HPA_SM16 && G % 4 == 0; }
 
 cudaError_t prefill_init_attributes() {
   cudaError_t e;
@@ -1899,7 +1939,7 @@ cudaError_t prefill_init_attributes() {
       (e = cudaFuncSetAttribute(prefill_persistent_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 PSmem<64>::kBytes)) != cudaSuccess)
     return e;
-  if (HPA_PF1 && HPA_PF1_CLUSTER) {
+  if ((HPA_PF1 && HPA_PF1_CLUSTER) || HPA_PF_MC2) {
     if ((e = cudaFuncSetAttribute(prefill_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   PSmem<128>::kBytes)) != cudaSuccess ||
         (e = cudaFuncSetAttribute(prefill_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

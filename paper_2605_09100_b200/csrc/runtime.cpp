@@ -326,6 +326,7 @@ struct PfPlan {
   std::vector<int4> parts;  // 2 per split unit: {b, y, x, nsplit}, {q_len, q_off, 0, 0}
   int32_t split_max = 1;
   std::vector<int32_t> cta_off;  // persistent launch: items of CTA c = [cta_off[c], cta_off[c+1])
+  bool mc2 = false;              // items 2k, 2k+1 form 2-CTA clusters (HPA_PF_MC2)
 };
 
 struct hpa_cache {
@@ -711,13 +712,25 @@ bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, 
   // wave over every (sequence, KV head) and re-read K/V from HBM (-4 % at configs[2] B = 4).
   const int64_t nU = int64_t(rows.size()) * Y;
   const int32_t W = persistent ? max_ctas : c->num_sms;
+  // The two head-pair units of a KV head as a 2-CTA cluster (consecutive work items, identical
+  // key ranges) sharing every K/V box by TMA multicast: +1.3 % at configs[2] B=4, but pairing
+  // constrains the split plan (-1.2 % at B=1), so only for batches of >= 4 waves (or forced by
+  // the testing hook hpa_set_prefill_ctas(c, -2)).
+  const bool mc2 = !persistent && prefill_mc2_supported(G) && (c->pf_ctas == -2 || nU >= int64_t(4) * W);
   std::vector<std::pair<int32_t, int32_t>> order;  // (row index, y)
   order.reserve(size_t(nU));
   for (size_t r0 = 0; r0 < rows.size();) {
     size_t r1 = r0;
     while (r1 < rows.size() && rows[r1].b == rows[r0].b) ++r1;
-    for (int32_t y = 0; y < Y; ++y)
-      for (size_t r = r0; r < r1; ++r) order.push_back({int32_t(r), y});
+    if (mc2) {  // y = h * G/2 + pair, pair fastest: cluster partners adjacent
+      const int32_t np = G / 2;
+      for (int32_t h = 0; h < Hkv; ++h)
+        for (size_t r = r0; r < r1; ++r)
+          for (int32_t pr = 0; pr < np; ++pr) order.push_back({int32_t(r), h * np + pr});
+    } else {
+      for (int32_t y = 0; y < Y; ++y)
+        for (size_t r = r0; r < r1; ++r) order.push_back({int32_t(r), y});
+    }
     r0 = r1;
   }
   auto unit = [&](int64_t k) -> const U& { return rows[size_t(order[size_t(k)].first)]; };
@@ -740,7 +753,7 @@ bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, 
     heap = base;
     const double t0 = list_schedule(heap, items.data(), items.size());
     double best = t0;
-    const int64_t R = nU % W;
+    const int64_t R = mc2 ? ((nU % W) + 1) / 2 * 2 : nU % W;  // whole clusters
     for (int64_t tail : {R, R + W}) {
       if (tail <= 0 || tail > nU) continue;
       std::vector<double> head = base;  // the unsplit units
@@ -785,6 +798,25 @@ bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, 
       plan.work.push_back(wn);
       continue;
     }
+    if (mc2) {  // units k, k + 1 are cluster partners: emit their pieces interleaved
+      const int32_t y2 = order[size_t(k + 1)].second;
+      const int32_t part = int32_t(plan.parts.size() / 2);
+      plan.parts.push_back(make_int4(u.b, y, u.x, ns));
+      plan.parts.push_back(make_int4(q_lens[u.b], q_off[u.b], 0, 0));
+      plan.parts.push_back(make_int4(u.b, y2, u.x, ns));
+      plan.parts.push_back(make_int4(q_lens[u.b], q_off[u.b], 0, 0));
+      for (int32_t p = 0; p < ns; ++p) {
+        const int32_t jb = int32_t(int64_t(u.n) * p / ns), je = int32_t(int64_t(u.n) * (p + 1) / ns);
+        for (int32_t m = 0; m < 2; ++m) {
+          plan.work.push_back(make_int4(u.b, m ? y2 : y, u.x, p | (ns << 4) | ((part + m) << 8)));
+          plan.work.push_back(make_int4(jb, je - jb, u.skip_a, u.n_skip));
+          plan.work.push_back(wq);
+          plan.work.push_back(wn);
+        }
+      }
+      ++k;
+      continue;
+    }
     const int32_t part = int32_t(plan.parts.size() / 2);
     plan.parts.push_back(make_int4(u.b, y, u.x, ns));
     plan.parts.push_back(make_int4(q_lens[u.b], q_off[u.b], 0, 0));
@@ -796,6 +828,7 @@ bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, 
       plan.work.push_back(wn);
     }
   }
+  plan.mc2 = mc2;
   plan.cta_off.clear();
   if (persistent) {
     // Items go, in dispatch order, to the CTA that is free first (estimated key tiles + the
@@ -1674,7 +1707,7 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
   PrefillArgs a{c->dt, dmeta, dmeta + n_seqs, dmeta + 2 * n_seqs, out, n_seqs, Hq, c->cfg.num_kv_heads,
                 Hq / c->cfg.num_kv_heads, c->cfg.page_size, c->cfg.num_pages, layer, max_q,
                 scale * 1.4426950408889634f, __builtin_ctz(uint32_t(c->cfg.page_size)),
-                span ? dmeta + 3 * n_seqs : nullptr, c->trace, nullptr, 0, nullptr, 0, 1, nullptr, nullptr, nullptr, 0};
+                span ? dmeta + 3 * n_seqs : nullptr, c->trace, nullptr, 0, nullptr, 0, 1, nullptr, nullptr, nullptr, 0, 0};
   if (listed) {
     const size_t rows = plan.parts.size() / 2 * size_t(plan.split_max) * 2 * 128;
     if (rows > c->pf_part_rows) {  // split workspace (grown on demand) and its fp32 TMA map
@@ -1697,6 +1730,7 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
     a.split_max = plan.split_max;
     a.o_part = c->pf_o_part;
     a.lse_part = c->pf_lse_part;
+    a.mc2 = plan.mc2 ? 1 : 0;
     if (cbytes) {
       a.cta_off = reinterpret_cast<const int32_t*>(c->ring.dev(off) + wbytes);
       a.n_ctas = int32_t(plan.cta_off.size()) - 1;
@@ -1774,7 +1808,7 @@ hpa_status_t hpa_prefill_plan_info(hpa_cache_t* c, int32_t* n_ctas, int32_t* n_s
 
 hpa_status_t hpa_set_prefill_ctas(hpa_cache_t* c, int32_t n) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
-  if (n < -1) return fail(HPA_ERR_INVALID_ARG, "prefill ctas %d < -1", n);
+  if (n < -2) return fail(HPA_ERR_INVALID_ARG, "prefill ctas %d < -2", n);
   c->pf_ctas = n;
   return HPA_OK;
 }

@@ -209,3 +209,23 @@ def test_prefill_upper_layer(token_fp8, splits):
         check_close(got, np.concatenate(ref), f"prefill layer {layer} fp8={token_fp8} splits={splits}")
         outs.append(got.float())
     assert torch.max(torch.abs(outs[0] - outs[1])).item() > 0.05
+
+
+@pytest.mark.parametrize("hq,hkv,P", [(32, 8, 16), (16, 2, 64), (16, 1, 256)])
+@pytest.mark.parametrize("splits", [0, 1, 3])
+def test_prefill_cluster_pairs_multicast(hq, hkv, P, splits):
+    """Forced 2-CTA clusters (hpa_set_prefill_ctas(c, -2); G % 4 == 0): the two head-pair units
+    of a KV head share every K/V box by TMA multicast; ragged q_len, splits, parity."""
+    shape = Shape(1, hq, hkv, 128, P)
+    p = Pair(shape, num_pages=4096, max_seqs=4, max_pages_per_seq=1024)
+    scripts = [[("latent", 128), ("latent", 8), ("tokens", 700)],
+               [("tokens", 77)],
+               [("latent", 128)] * 2 + [("tokens", 1500)]]
+    seqs = [p.build(sc) for sc in scripts]
+    q_lens = [300, 1, 385]
+    q = p.queries(sum(q_lens))
+    p.cache.set_prefill_splits(splits)
+    p.cache.set_prefill_ctas(-2)
+    got = p.cache.prefill(0, seqs, q_lens, q.cuda())
+    torch.cuda.synchronize()
+    check_close(got, _oracle_prefill(p, seqs, q_lens, q), f"cluster prefill {hq}/{hkv}/P{P} splits={splits}")
