@@ -17,7 +17,8 @@ def main():
     torch.cuda.set_device(dev)
     shape = qwen3_8b_shape(16)
     stream = torch.cuda.current_stream()
-    # a mode is a split setting, suffixed "p" for the persistent kernel (else one CTA per item)
+    # a mode is a split setting, suffixed "p" for the persistent kernel, "c" for forced 2-CTA
+    # clusters (else one CTA per item)
     modes = os.environ.get("MODES", "1,0,2,3,4,6").split(",")
     for bp in [int(x) for x in os.environ.get("BATCHES", "1,2,3,4").split(",")]:
         c_rows, prior = int(os.environ.get("C_ROWS", "2048")), 16384
@@ -29,8 +30,8 @@ def main():
         ref = None
         res = {}
         for mode in modes * int(os.environ.get("ROUNDS", "1")):
-            cache.set_prefill_splits(int(mode.rstrip("p")))
-            cache.set_prefill_ctas(0 if mode.endswith("p") else -1)
+            cache.set_prefill_splits(int(mode.rstrip("pc")))
+            cache.set_prefill_ctas(0 if mode.endswith("p") else -2 if mode.endswith("c") else -1)
             for _ in range(3):
                 cache.prefill(0, seqs, [c_rows] * bp, q, o)
             torch.cuda.synchronize()
