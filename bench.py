@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--sweep", action="store_true", help="configs[4] sweep (per-GPU shard), JSON per point")
     ap.add_argument("--sweep-n", type=int, default=8, help="GPUs the sweep's global batch is sharded over")
     ap.add_argument("--sweep-max-gb", type=float, default=120.0)
+    ap.add_argument("--sweep-min-gb", type=float, default=0.0, help="only points with at least this pool size")
     return ap.parse_args()
 
 
@@ -300,6 +301,8 @@ def bench_sweep(args):
                 gb = b * ctx * rows_bytes / 1e9
                 pt = {"global_batch": B, "n_gpus": n, "requests_per_gpu": b, "context": ctx,
                       "latent_ratio": r, "latent_sets": sets, "token_rows": tok, "kv_gb_per_gpu": round(gb, 2)}
+                if gb < args.sweep_min_gb:
+                    continue
                 if gb > args.sweep_max_gb:
                     pt["skipped"] = f"pool {gb:.0f} GB > --sweep-max-gb {args.sweep_max_gb}"
                     print(json.dumps(pt), flush=True)
@@ -325,7 +328,8 @@ def bench_sweep(args):
                 flat.append({"global_batch": B, "context": ctx,
                              "spread": round((max(g) - min(g)) / (sum(g) / 3), 4)})
     print(json.dumps({"sweep": "configs[4]", "peak": pk["hbm_gbs"], "peak_kind": pk_kind,
-                      "page_size": args.page_size, "max_latent_ratio_spread": max(f["spread"] for f in flat),
+                      "page_size": args.page_size,
+                      "max_latent_ratio_spread": max((f["spread"] for f in flat), default=None),
                       "flatness": flat}), flush=True)
 
 
