@@ -229,3 +229,23 @@ def test_prefill_cluster_pairs_multicast(hq, hkv, P, splits):
     got = p.cache.prefill(0, seqs, q_lens, q.cuda())
     torch.cuda.synchronize()
     check_close(got, _oracle_prefill(p, seqs, q_lens, q), f"cluster prefill {hq}/{hkv}/P{P} splits={splits}")
+
+
+def test_prefill_many_short_sequences_cluster_waves():
+    """200 sequences with q_len 1..5 (one ragged row tile each): enough units for >= 4 waves,
+    so the default plan runs 2-CTA multicast clusters; parity on every row."""
+    shape = Shape(1, 32, 8, 128, 16)
+    p = Pair(shape, num_pages=8192, max_seqs=200, max_pages_per_seq=64)
+    rng = np.random.default_rng(5)
+    seqs = []
+    for i in range(200):
+        s = p.new_seq()
+        if i % 3 == 0:
+            p.latent(s, 128)
+        p.tokens([s], [int(rng.integers(5, 300))])
+        seqs.append(s)
+    q_lens = [int(rng.integers(1, 6)) for _ in seqs]
+    q = p.queries(sum(q_lens))
+    got = p.cache.prefill(0, seqs, q_lens, q.cuda())
+    torch.cuda.synchronize()
+    check_close(got, _oracle_prefill(p, seqs, q_lens, q), "many short sequences")
