@@ -106,7 +106,9 @@ hpa_status_t hpa_cache_pools(hpa_cache_t* c, void** k_pool, void** v_pool, uint6
  * and the free token pages. Layout (reading A20): pool row prow = ((layer * num_token_pages +
  * page) * H_kv + h) * P + r; rows are grouped 16 at a time into contiguous blocks of
  * [16 x d e4m3 codes | 16 fp32 scales] (16 d + 64 bytes), block index prow / 16; row r of
- * a block means code * scale. The cache owns the pools; read-only for callers (tests
+ * a block means code * scale. K rows (not V) store their 16-byte code chunks XOR-swizzled:
+ * logical chunk c of block row r sits at chunk c ^ (r & (d/16 - 1)) (bank-conflict-free
+ * register loads of the K fragments in decode). The cache owns the pools; read-only for callers (tests
  * compare them bit-exactly with the oracle's quantizer). HPA_ERR_INVALID_ARG if the cache
  * stores bf16 token pages. */
 hpa_status_t hpa_cache_token_pool(hpa_cache_t* c, void** k8, void** v8, int32_t* free_token_pages);

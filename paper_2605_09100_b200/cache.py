@@ -300,16 +300,25 @@ class Cache:
     def token_pool(self):
         """NEXT-4c fp8 token pool views (include/hpa.h hpa_cache_token_pool): (k codes, v codes)
         uint8 [L][NPt][H_kv][P][d], (k scales, v scales) fp32 [L][NPt][H_kv][P], free token pages.
-        Codes and scales are strided views of the 16-row [codes | scales] blocks."""
+        V codes and the scales are strided views of the 16-row [codes | scales] blocks; K codes
+        are a copy in logical column order (the pool stores them chunk-swizzled)."""
         k8, v8, free = c_vp(), c_vp(), c_i32()
         check(LIB.hpa_cache_token_pool(self._h, ctypes.byref(k8), ctypes.byref(v8), ctypes.byref(free)))
         dev = torch.device(f"cuda:{self.device}")
         nblk = self.L * self.num_token_pages * self.Hkv * self.P // 16
         blk = 16 * self.d + 64
         views = []
-        for ptr in (k8.value, v8.value):
+        nch = self.d // 16
+        # K rows store their 16-byte chunks XOR-swizzled by the row's index in its 16-row block
+        # (include/hpa.h): physical chunk of logical chunk c in row r is c ^ (r & (d/16 - 1))
+        r = torch.arange(16, device=dev)[:, None]
+        swz = torch.arange(nch, device=dev)[None, :] ^ (r & (nch - 1))
+        for ptr, is_k in ((k8.value, True), (v8.value, False)):
             raw = torch.as_tensor(_CAI(ptr, (nblk, blk), "|u1"), device=dev)
-            codes = raw[:, :16 * self.d].reshape(self.L, self.num_token_pages, self.Hkv, self.P, self.d)
+            codes = raw[:, :16 * self.d]
+            if is_k:  # a logical-order copy
+                codes = codes.reshape(nblk, 16, nch, 16)[:, r, swz, :]
+            codes = codes.reshape(self.L, self.num_token_pages, self.Hkv, self.P, self.d)
             scales = raw[:, 16 * self.d:].contiguous().view(torch.float32).reshape(
                 self.L, self.num_token_pages, self.Hkv, self.P)
             views.append((codes, scales))

@@ -74,7 +74,7 @@ __device__ __forceinline__ void quant_rows(const PoolGeom& g, const ScatterRecor
       kx[i] = __fmul_rn(kx[i], kinv);
       vx[i] = __fmul_rn(vx[i], vinv);
     }
-    *reinterpret_cast<uint2*>(fp8_code_ptr(g.k8, prow, D) + c * 8) = e4m3x8_from_f32(kx);
+    *reinterpret_cast<uint2*>(fp8_kcode_ptr(g.k8, prow, D, int(c) * 8)) = e4m3x8_from_f32(kx);
     *reinterpret_cast<uint2*>(fp8_code_ptr(g.v8, prow, D) + c * 8) = e4m3x8_from_f32(vx);
     if (c == 0) {
       *fp8_scale_ptr(g.k8, prow, D) = ka > 0.f ? __fdiv_rn(ka, 448.f) : 1.f;
@@ -122,7 +122,7 @@ __device__ __forceinline__ void copy_rows(const PoolGeom& g, const ScatterRecord
         if (r.src_from_pool && r.src_fp8) {  // move out of the fp8 token pool: dequantize
           const int32_t ss = idx[r.src_off + row];
           const int64_t prow = ((int64_t(l) * g.NPt + (ss >> g.log2P)) * g.Hkv + h) * g.P + (ss & (g.P - 1));
-          kv[u] = bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(fp8_code_ptr(g.k8, prow, D) + c * 8),
+          kv[u] = bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(fp8_kcode_ptr(g.k8, prow, D, int(c) * 8)),
                                    *fp8_scale_ptr(g.k8, prow, D));
           vv[u] = bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(fp8_code_ptr(g.v8, prow, D) + c * 8),
                                    *fp8_scale_ptr(g.v8, prow, D));
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(256) dequant_pages_kernel(PoolGeom g, const in
   for (int v = threadIdx.x; v < it.z * kVPR; v += blockDim.x) {
     const int r = v / kVPR, c = v % kVPR;
     const int64_t prow = row0 + r;
-    const uint2 kc = *reinterpret_cast<const uint2*>(fp8_code_ptr(g.k8, prow, D) + c * 8);
+    const uint2 kc = *reinterpret_cast<const uint2*>(fp8_kcode_ptr(g.k8, prow, D, c * 8));
     const uint2 vc = *reinterpret_cast<const uint2*>(fp8_code_ptr(g.v8, prow, D) + c * 8);
     const float ks = *fp8_scale_ptr(g.k8, prow, D), vs = *fp8_scale_ptr(g.v8, prow, D);
     reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(g.k_pool) + dst0 + int64_t(r) * D)[c] = bf16x8_from_e4m3(kc, ks);
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(128) export_kernel(PoolGeom g, DevTables t, in
       const int64_t prow = row0 + i / vec_per_row;
       const int64_t off = int64_t(i % vec_per_row) * 8;
       reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(k_out) + dst0)[i] =
-          bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(fp8_code_ptr(g.k8, prow, g.D) + off),
+          bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(fp8_kcode_ptr(g.k8, prow, g.D, int(off))),
                            *fp8_scale_ptr(g.k8, prow, g.D));
       reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(v_out) + dst0)[i] =
           bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(fp8_code_ptr(g.v8, prow, g.D) + off),

@@ -404,7 +404,7 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_const
 // 128-B-swizzled layout the ldmatrix code reads; raw code values (exact in bf16), the
 // per-row scales are applied to S and P. Warp-wide: lane -> row lane/2, half the columns.
 // All lanes read before any lane writes, so src may overlap dst (the V tile converts in place).
-template <int D>
+template <int D, bool KSW = false>
 __device__ __forceinline__ void fp8_tile_to_bf16(const uint8_t* src, uint8_t* dst, int lane) {
   constexpr int kG = D / 16;  // 8-byte groups per lane (16 x D bytes / 32 lanes / 8)
   // lane reads bytes [(32 g + lane) * 8, +8): each LDS.64 covers 256 contiguous bytes
@@ -416,7 +416,9 @@ __device__ __forceinline__ void fp8_tile_to_bf16(const uint8_t* src, uint8_t* ds
 #pragma unroll
   for (int g = 0; g < kG; ++g) {
     const int byte = (32 * g + lane) * 8;
-    const int r = byte / D, cc = (byte % D) >> 3;  // row, 16-B bf16 chunk index in the row
+    const int r = byte / D;
+    int cc = (byte % D) >> 3;  // 8-code group = 16-B bf16 chunk index in the row
+    if (KSW) cc = fp8_kswz(cc * 8, r, D) >> 3;  // swizzled K codes: physical -> logical (an involution)
     int4 out;
     if (HPA_FP8_CVT_INT) {
       // e4m3 -> bf16 without the conversion unit: a code's 7 magnitude bits placed at bf16
@@ -442,7 +444,7 @@ __device__ __forceinline__ void fp8_tile_to_bf16(const uint8_t* src, uint8_t* ds
 }
 // Same as fp8_tile_to_bf16 but to f16 (one cvt per code pair; e4m3 values are exact in f16):
 // the swapped-operand consumers run fp8 chunks as f16 MMAs.
-template <int D>
+template <int D, bool KSW = false>
 __device__ __forceinline__ void fp8_tile_to_f16(const uint8_t* src, uint8_t* dst, int lane) {
   constexpr int kG = D / 16;
   uint2 c[kG];
@@ -452,7 +454,9 @@ __device__ __forceinline__ void fp8_tile_to_f16(const uint8_t* src, uint8_t* dst
 #pragma unroll
   for (int g = 0; g < kG; ++g) {
     const int byte = (32 * g + lane) * 8;
-    const int r = byte / D, cc = (byte % D) >> 3;
+    const int r = byte / D;
+    int cc = (byte % D) >> 3;
+    if (KSW) cc = fp8_kswz(cc * 8, r, D) >> 3;
     const uint32_t in[4] = {c[g].x & 0xffffu, c[g].x >> 16, c[g].y & 0xffffu, c[g].y >> 16};
     uint32_t w[4];
 #pragma unroll
@@ -733,12 +737,19 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     // Fragment owner: g = lane / 4 (key row / dim row), t = lane % 4 (heads 2t, 2t+1).
     const int gq = lane >> 2, tq = lane & 3;
     uint32_t qbf[D / 16][2];  // B operand Q^T: (dims 16 ks + 2t.., head g), (dims + 8.., head g)
+    // HPA_FP8_KSWZ: f16 B operand over the dims in the register-direct order of the fp8 K
+    // path: k (2t, 2t+1) <-> dims 16 ks + 4t, +1 and k (2t+8, 2t+9) <-> dims 16 ks + 4t + 2, +3
+    uint32_t qbk[D / 16][2];
     {
       const uint32_t* qrow = reinterpret_cast<const uint32_t*>(qbuf + qb * qbytes + gq * D * 2);
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks) {
         qbf[ks][0] = gq < G ? qrow[8 * ks + tq] : 0u;
         qbf[ks][1] = gq < G ? qrow[8 * ks + 4 + tq] : 0u;
+        if (HPA_FP8_KSWZ && a.fp8) {
+          qbk[ks][0] = gq < G ? bf16x2_to_f16x2(qrow[8 * ks + 2 * tq]) : 0u;
+          qbk[ks][1] = gq < G ? bf16x2_to_f16x2(qrow[8 * ks + 2 * tq + 1]) : 0u;
+        }
       }
     }
     __syncwarp();
@@ -751,6 +762,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         qbh[ks][1] = bf16x2_to_f16x2(qbf[ks][1]);
       }
     }
+
     float o[D / 16][4];  // O^T tile mt: (dim 16mt+g, head 2t), (.., 2t+1), (dim +8, 2t), (dim +8, 2t+1)
 #pragma unroll
     for (int n = 0; n < D / 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
@@ -786,18 +798,41 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         kmul1 = ksc[gq + 8] * sl2;
         vmul0 = vsc[gq];
         vmul1 = vsc[gq + 8];
+      }
+      float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+      const bool kreg = HPA_FP8_KSWZ && !HPA_FP8_F16 && c8;
+      if (kreg) {
+        // fp8 K straight into registers (no shared-memory conversion): lane (g, t) reads codes
+        // 4t..4t+3 of each 16-column group of keys g and g + 8 (chunk-swizzled rows: no bank
+        // conflict) and converts them to f16 pairs for f16 MMAs against qbk. K is consumed
+        // before the V tile conversion below overwrites the upper part of the K code block.
+        const uint8_t* kb = kt + L::oK8;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + gq * D + fp8_kswz(ks * 16 + 4 * tq, gq, D));
+          const uint32_t w1 =
+              *reinterpret_cast<const uint32_t*>(kb + (gq + 8) * D + fp8_kswz(ks * 16 + 4 * tq, gq + 8, D));
+          uint32_t ka[4];
+          ka[0] = f16x2_from_e4m3x2(w0);
+          ka[1] = f16x2_from_e4m3x2(w1);
+          ka[2] = f16x2_from_e4m3x2(w0 >> 16);
+          ka[3] = f16x2_from_e4m3x2(w1 >> 16);
+          mma_f16_16816(sacc, ka, qbk[ks][0], qbk[ks][1]);
+        }
+      }
+      if (c8) {
         __syncwarp();
         if (HPA_FP8_F16) {
-          fp8_tile_to_f16<D>(kt + L::oK8, kt, lane);
+          fp8_tile_to_f16<D, true>(kt + L::oK8, kt, lane);
           fp8_tile_to_f16<D>(kt + L::oV8, vt, lane);
         } else {
-          fp8_tile_to_bf16<D>(kt + L::oK8, kt, lane);
+          if (!kreg) fp8_tile_to_bf16<D, true>(kt + L::oK8, kt, lane);
           fp8_tile_to_bf16<D>(kt + L::oV8, vt, lane);
         }
         __syncwarp();
       }
       const bool h16 = HPA_FP8_F16 && c8;  // this chunk runs as f16 MMAs
-      float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+      if (!kreg) {
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks) {  // A = K (16 keys x 16 dims)
         const int mi = lane >> 3;
@@ -807,6 +842,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         ldsm_x4(smem_u32(kt + (kc >> 3) * 2048 + sw128(row, kc & 7)), ka[0], ka[1], ka[2], ka[3]);
         if (h16) mma_f16_16816(sacc, ka, qbh[ks][0], qbh[ks][1]);
         else mma_bf16_16816(sacc, ka, qbf[ks][0], qbf[ks][1]);
+      }
       }
       const float x0 = gq < nvalid ? sacc[0] * kmul0 : -CUDART_INF_F;      // key g,   head 2t
       const float x1 = gq < nvalid ? sacc[1] * kmul0 : -CUDART_INF_F;      // key g,   head 2t+1
@@ -932,7 +968,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
           vmul[q] = vsc[col];
         }
         __syncwarp();
-        fp8_tile_to_bf16<D>(kt + L::oK8, kt, lane);
+        fp8_tile_to_bf16<D, true>(kt + L::oK8, kt, lane);
         fp8_tile_to_bf16<D>(kt + L::oV8, vt, lane);
         __syncwarp();
       }

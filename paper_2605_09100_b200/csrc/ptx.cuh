@@ -151,6 +151,11 @@ __device__ __forceinline__ void mma_f16_16816(float* d, const uint32_t* a, uint3
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+__device__ __forceinline__ uint32_t f16x2_from_e4m3x2(uint32_t two_codes) {  // low 16 bits: 2 codes
+  uint32_t h2;
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(uint16_t(two_codes)));
+  return h2;
+}
 __device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));  // lo in the low 16 bits
@@ -185,6 +190,21 @@ __device__ __forceinline__ int4 bf16x8_from_e4m3(uint2 c, float scale) {
 __host__ __device__ __forceinline__ int64_t fp8_block_bytes(int D) { return 16 * int64_t(D) + 64; }
 __host__ __device__ __forceinline__ uint8_t* fp8_code_ptr(uint8_t* base, int64_t prow, int D) {
   return base + (prow >> 4) * fp8_block_bytes(D) + (prow & 15) * int64_t(D);
+}
+// K codes only (HPA_FP8_KSWZ): the 16-byte chunks of a row are XOR-swizzled by the row's
+// position in its 16-row block, chunk' = chunk ^ (r & (D/16 - 1)), so that lanes reading the
+// same chunk column of 8 different rows hit different banks. Address of K code byte `off`
+// (logical column) of pool row prow.
+#ifndef HPA_FP8_KSWZ
+#define HPA_FP8_KSWZ 1
+#endif
+__host__ __device__ __forceinline__ int fp8_kswz(int off, int64_t prow, int D) {
+  if (!HPA_FP8_KSWZ) return off;
+  const int r = int(prow & 15) & (D / 16 - 1);
+  return (((off >> 4) ^ r) << 4) | (off & 15);
+}
+__host__ __device__ __forceinline__ uint8_t* fp8_kcode_ptr(uint8_t* base, int64_t prow, int D, int off) {
+  return fp8_code_ptr(base, prow, D) + fp8_kswz(off, prow, D);
 }
 __host__ __device__ __forceinline__ float* fp8_scale_ptr(uint8_t* base, int64_t prow, int D) {
   return reinterpret_cast<float*>(base + (prow >> 4) * fp8_block_bytes(D) + 16 * int64_t(D) + 4 * (prow & 15));
