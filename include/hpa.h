@@ -108,7 +108,9 @@ hpa_status_t hpa_cache_pools(hpa_cache_t* c, void** k_pool, void** v_pool, uint6
  * [16 x d e4m3 codes | 16 fp32 scales] (16 d + 64 bytes), block index prow / 16; row r of
  * a block means code * scale. K rows (not V) store their 16-byte code chunks XOR-swizzled:
  * logical chunk c of block row r sits at chunk c ^ (r & (d/16 - 1)) (bank-conflict-free
- * register loads of the K fragments in decode). The cache owns the pools; read-only for callers (tests
+ * register loads of the K fragments in decode). V rows pair up: the codes of block rows 2p and
+ * 2p+1 interleave by dim in "pair row" p (2 d bytes: byte 2 j + (row & 1) holds dim j), whose
+ * 16-byte chunks are XOR-swizzled by p & 7 (one 16-bit load = a V^T operand register). The cache owns the pools; read-only for callers (tests
  * compare them bit-exactly with the oracle's quantizer). HPA_ERR_INVALID_ARG if the cache
  * stores bf16 token pages. */
 hpa_status_t hpa_cache_token_pool(hpa_cache_t* c, void** k8, void** v8, int32_t* free_token_pages);

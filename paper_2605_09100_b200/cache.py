@@ -300,8 +300,8 @@ class Cache:
     def token_pool(self):
         """NEXT-4c fp8 token pool views (include/hpa.h hpa_cache_token_pool): (k codes, v codes)
         uint8 [L][NPt][H_kv][P][d], (k scales, v scales) fp32 [L][NPt][H_kv][P], free token pages.
-        V codes and the scales are strided views of the 16-row [codes | scales] blocks; K codes
-        are a copy in logical column order (the pool stores them chunk-swizzled)."""
+        The scales are strided views of the 16-row [codes | scales] blocks; K and V codes are
+        copies in logical order (the pool stores K chunk-swizzled and V as swizzled key pairs)."""
         k8, v8, free = c_vp(), c_vp(), c_i32()
         check(LIB.hpa_cache_token_pool(self._h, ctypes.byref(k8), ctypes.byref(v8), ctypes.byref(free)))
         dev = torch.device(f"cuda:{self.device}")
@@ -318,6 +318,13 @@ class Cache:
             codes = raw[:, :16 * self.d]
             if is_k:  # a logical-order copy
                 codes = codes.reshape(nblk, 16, nch, 16)[:, r, swz, :]
+            else:
+                # V: pair row p holds keys 2p, 2p + 1 interleaved by dim (byte 2 d + key parity)
+                # in 2 d/16 chunks of 16 bytes, chunk c at c ^ (p & 7)
+                pr = torch.arange(8, device=dev)[:, None]
+                vsw = torch.arange(2 * nch, device=dev)[None, :] ^ (pr & 7)
+                lin = codes.reshape(nblk, 8, 2 * nch, 16)[:, pr, vsw, :].reshape(nblk, 8, self.d, 2)
+                codes = lin.permute(0, 1, 3, 2).reshape(nblk, 16, self.d)
             codes = codes.reshape(self.L, self.num_token_pages, self.Hkv, self.P, self.d)
             scales = raw[:, 16 * self.d:].contiguous().view(torch.float32).reshape(
                 self.L, self.num_token_pages, self.Hkv, self.P)

@@ -75,7 +75,7 @@ __device__ __forceinline__ void quant_rows(const PoolGeom& g, const ScatterRecor
       vx[i] = __fmul_rn(vx[i], vinv);
     }
     *reinterpret_cast<uint2*>(fp8_kcode_ptr(g.k8, prow, D, int(c) * 8)) = e4m3x8_from_f32(kx);
-    *reinterpret_cast<uint2*>(fp8_code_ptr(g.v8, prow, D) + c * 8) = e4m3x8_from_f32(vx);
+    fp8_vstore8(fp8_block_codes(g.v8, prow, D), int(prow & 15), int(c) * 8, D, e4m3x8_from_f32(vx));
     if (c == 0) {
       *fp8_scale_ptr(g.k8, prow, D) = ka > 0.f ? __fdiv_rn(ka, 448.f) : 1.f;
       *fp8_scale_ptr(g.v8, prow, D) = va > 0.f ? __fdiv_rn(va, 448.f) : 1.f;
@@ -124,7 +124,7 @@ __device__ __forceinline__ void copy_rows(const PoolGeom& g, const ScatterRecord
           const int64_t prow = ((int64_t(l) * g.NPt + (ss >> g.log2P)) * g.Hkv + h) * g.P + (ss & (g.P - 1));
           kv[u] = bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(fp8_kcode_ptr(g.k8, prow, D, int(c) * 8)),
                                    *fp8_scale_ptr(g.k8, prow, D));
-          vv[u] = bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(fp8_code_ptr(g.v8, prow, D) + c * 8),
+          vv[u] = bf16x8_from_e4m3(fp8_vcodes8(fp8_block_codes(g.v8, prow, D), int(prow & 15), int(c) * 8, D),
                                    *fp8_scale_ptr(g.v8, prow, D));
         } else if (r.src_from_pool) {  // in-cache move: source is another pool slot
           const int32_t ss = idx[r.src_off + row];
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(256) dequant_pages_kernel(PoolGeom g, const in
     const int r = v / kVPR, c = v % kVPR;
     const int64_t prow = row0 + r;
     const uint2 kc = *reinterpret_cast<const uint2*>(fp8_kcode_ptr(g.k8, prow, D, c * 8));
-    const uint2 vc = *reinterpret_cast<const uint2*>(fp8_code_ptr(g.v8, prow, D) + c * 8);
+    const uint2 vc = fp8_vcodes8(fp8_block_codes(g.v8, prow, D), int(prow & 15), c * 8, D);
     const float ks = *fp8_scale_ptr(g.k8, prow, D), vs = *fp8_scale_ptr(g.v8, prow, D);
     reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(g.k_pool) + dst0 + int64_t(r) * D)[c] = bf16x8_from_e4m3(kc, ks);
     reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(g.v_pool) + dst0 + int64_t(r) * D)[c] = bf16x8_from_e4m3(vc, vs);
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(128) export_kernel(PoolGeom g, DevTables t, in
           bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(fp8_kcode_ptr(g.k8, prow, g.D, int(off))),
                            *fp8_scale_ptr(g.k8, prow, g.D));
       reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(v_out) + dst0)[i] =
-          bf16x8_from_e4m3(*reinterpret_cast<const uint2*>(fp8_code_ptr(g.v8, prow, g.D) + off),
+          bf16x8_from_e4m3(fp8_vcodes8(fp8_block_codes(g.v8, prow, g.D), int(prow & 15), int(off), g.D),
                            *fp8_scale_ptr(g.v8, prow, g.D));
     }
     return;

@@ -442,6 +442,32 @@ __device__ __forceinline__ void fp8_tile_to_bf16(const uint8_t* src, uint8_t* ds
     *reinterpret_cast<int4*>(dst + (cc >> 3) * 2048 + sw128(r, cc & 7)) = out;
   }
 }
+// The V tile of an fp8 chunk in the HPA_FP8_VPAIR layout (pair rows of interleaved key codes,
+// swizzled 16-byte chunks) -> the bf16 [D/64][16][128 B] layout: each 16-byte chunk holds 8 dims
+// of two keys; all lanes read before any lane writes (src overlaps dst).
+template <int D>
+__device__ __forceinline__ void fp8_vtile_to_bf16(const uint8_t* src, uint8_t* dst, const float* scale_unused,
+                                                  int lane) {
+  constexpr int kChunks = 16 * D / 16;  // 16-byte chunks in the tile's code area
+  constexpr int kPer = kChunks / 32;
+  constexpr int kCPR = 2 * D / 16;      // chunks per pair row
+  uint4 c[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) c[i] = reinterpret_cast<const uint4*>(src)[32 * i + lane];
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int q = 32 * i + lane, pr = q / kCPR, cl = (q % kCPR) ^ (pr & 7);  // logical chunk
+    const int dg = cl;  // 8-dim group: lin 16 cl .. 16 cl + 15 = dims 8 cl .. 8 cl + 7 of both keys
+#pragma unroll
+    for (int odd = 0; odd < 2; ++odd) {
+      const uint32_t sel = odd ? 0x7531u : 0x6420u;
+      const uint2 codes = make_uint2(__byte_perm(c[i].x, c[i].y, sel), __byte_perm(c[i].z, c[i].w, sel));
+      const int r = 2 * pr + odd;
+      *reinterpret_cast<int4*>(dst + (dg >> 3) * 2048 + sw128(r, dg & 7)) = bf16x8_from_e4m3(codes, 1.f);
+    }
+  }
+}
 // Same as fp8_tile_to_bf16 but to f16 (one cvt per code pair; e4m3 values are exact in f16):
 // the swapped-operand consumers run fp8 chunks as f16 MMAs.
 template <int D, bool KSW = false>
@@ -763,6 +789,9 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       }
     }
 
+    // HPA_FP8_VPAIR: every P^T fragment is pre-scaled by vpre (f16 range for the fp8 chunks;
+    // latent bf16 chunks carry the same factor so O stays consistent); undone at the merge
+    const float vpre = (HPA_FP8_VPAIR && a.fp8) ? 256.f : 1.f;
     float o[D / 16][4];  // O^T tile mt: (dim 16mt+g, head 2t), (.., 2t+1), (dim +8, 2t), (dim +8, 2t+1)
 #pragma unroll
     for (int n = 0; n < D / 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
@@ -790,14 +819,14 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       nvalid &= 0xffff;
       uint8_t* kt = stages + slot * L::kStageBytes;
       uint8_t* vt = kt + L::kTileBytes;
-      float kmul0 = sl2, kmul1 = sl2, vmul0 = 1.f, vmul1 = 1.f;  // keys g and g + 8
+      float kmul0 = sl2, kmul1 = sl2, vmul0 = vpre, vmul1 = vpre;  // keys g and g + 8
       if (c8) {
         const float* ksc = reinterpret_cast<const float*>(kt + L::oK8 + 16 * D);
         const float* vsc = reinterpret_cast<const float*>(kt + L::oV8 + 16 * D);
         kmul0 = ksc[gq] * sl2;  // scales first: the conversion overwrites them
         kmul1 = ksc[gq + 8] * sl2;
-        vmul0 = vsc[gq];
-        vmul1 = vsc[gq + 8];
+        vmul0 = vsc[gq] * vpre;
+        vmul1 = vsc[gq + 8] * vpre;
       }
       float sacc[4] = {0.f, 0.f, 0.f, 0.f};
       const bool kreg = HPA_FP8_KSWZ && !HPA_FP8_F16 && c8;
@@ -827,7 +856,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
           fp8_tile_to_f16<D>(kt + L::oV8, vt, lane);
         } else {
           if (!kreg) fp8_tile_to_bf16<D, true>(kt + L::oK8, kt, lane);
-          fp8_tile_to_bf16<D>(kt + L::oV8, vt, lane);
+          if (!HPA_FP8_VPAIR) fp8_tile_to_bf16<D>(kt + L::oV8, vt, lane);  // (VPAIR: V read below)
         }
         __syncwarp();
       }
@@ -876,6 +905,24 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       }
       // B operand P^T: (key g: heads 2t, 2t+1) pairs transposed in registers to (head g: keys
       // 2t, 2t+1); the V scales (fp8 chunks) fold into P per key
+      if (HPA_FP8_VPAIR && c8) {
+        // fp8 V^T fragments straight from the pair-row codes: one 16-bit load = the (key 2t,
+        // key 2t+1) code pair of one dim = one f16x2 register; P^T in f16 (pre-scaled by vpre
+        // so tiny V scales stay normal in f16; O is divided by vpre at the unit's merge)
+        const uint32_t pb0 = movmatrix_t(pack_f16(p0 * vmul0, p1 * vmul0));
+        const uint32_t pb1 = movmatrix_t(pack_f16(p2 * vmul1, p3 * vmul1));
+        const uint8_t* vb = kt + L::oV8;
+#pragma unroll
+        for (int mt = 0; mt < D / 16; ++mt) {
+          const int d = 16 * mt + gq;
+          uint32_t va[4];
+          va[0] = f16x2_from_e4m3x2(*reinterpret_cast<const uint16_t*>(vb + fp8_voff(2 * tq, d, D)));
+          va[1] = f16x2_from_e4m3x2(*reinterpret_cast<const uint16_t*>(vb + fp8_voff(2 * tq, d + 8, D)));
+          va[2] = f16x2_from_e4m3x2(*reinterpret_cast<const uint16_t*>(vb + fp8_voff(2 * tq + 8, d, D)));
+          va[3] = f16x2_from_e4m3x2(*reinterpret_cast<const uint16_t*>(vb + fp8_voff(2 * tq + 8, d + 8, D)));
+          mma_f16_16816(o[mt], va, pb0, pb1);
+        }
+      } else {
       const uint32_t pb0 = movmatrix_t(h16 ? pack_f16(p0 * vmul0, p1 * vmul0) : pack_bf16(p0 * vmul0, p1 * vmul0));
       const uint32_t pb1 = movmatrix_t(h16 ? pack_f16(p2 * vmul1, p3 * vmul1) : pack_bf16(p2 * vmul1, p3 * vmul1));
 #pragma unroll
@@ -887,6 +934,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         ldsm_x4_t(smem_u32(vt + (dc >> 3) * 2048 + sw128(key, dc & 7)), va[0], va[1], va[2], va[3]);
         if (h16) mma_f16_16816(o[mt], va, pb0, pb1);
         else mma_bf16_16816(o[mt], va, pb0, pb1);
+      }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
@@ -902,13 +950,14 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
 #pragma unroll
       for (int mt = 0; mt < D / 16; ++mt) {
         const int d0 = 16 * mt + gq;
+        const float ivp = 1.f / vpre;
         if (h0 < G) {
-          mo[(cw * G + h0) * D + d0] = o[mt][0];
-          mo[(cw * G + h0) * D + d0 + 8] = o[mt][2];
+          mo[(cw * G + h0) * D + d0] = o[mt][0] * ivp;
+          mo[(cw * G + h0) * D + d0 + 8] = o[mt][2] * ivp;
         }
         if (h1 < G) {
-          mo[(cw * G + h1) * D + d0] = o[mt][1];
-          mo[(cw * G + h1) * D + d0 + 8] = o[mt][3];
+          mo[(cw * G + h1) * D + d0] = o[mt][1] * ivp;
+          mo[(cw * G + h1) * D + d0 + 8] = o[mt][3] * ivp;
         }
       }
       if (gq == 0) {
@@ -969,7 +1018,8 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         }
         __syncwarp();
         fp8_tile_to_bf16<D, true>(kt + L::oK8, kt, lane);
-        fp8_tile_to_bf16<D>(kt + L::oV8, vt, lane);
+        if (HPA_FP8_VPAIR) fp8_vtile_to_bf16<D>(kt + L::oV8, vt, nullptr, lane);
+        else fp8_tile_to_bf16<D>(kt + L::oV8, vt, lane);
         __syncwarp();
       }
       float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};

@@ -206,8 +206,44 @@ __host__ __device__ __forceinline__ int fp8_kswz(int off, int64_t prow, int D) {
 __host__ __device__ __forceinline__ uint8_t* fp8_kcode_ptr(uint8_t* base, int64_t prow, int D, int off) {
   return fp8_code_ptr(base, prow, D) + fp8_kswz(off, prow, D);
 }
+// V rows (HPA_FP8_VPAIR): the codes of keys 2p and 2p+1 of a 16-row block interleave by dim
+// in "pair row" p (byte 2d + (r & 1) of the pair row), and the pair row's 16-byte chunks are
+// XOR-swizzled by p, so one 16-bit load gives the (key 2p, key 2p+1) code pair of a dim --
+// an f16x2 register of the V^T MMA operand -- without bank conflicts.
+#ifndef HPA_FP8_VPAIR
+#define HPA_FP8_VPAIR 1
+#endif
+#if HPA_FP8_F16
+#undef HPA_FP8_VPAIR
+#define HPA_FP8_VPAIR 0
+#endif
+__host__ __device__ __forceinline__ int fp8_voff(int r, int d, int D) {  // byte in the block's code area
+  if (!HPA_FP8_VPAIR) return r * D + d;
+  const int pr = r >> 1, lin = 2 * d + (r & 1);
+  return pr * 2 * D + ((((lin >> 4) ^ (pr & 7))) << 4) + (lin & 15);
+}
+__host__ __device__ __forceinline__ uint8_t* fp8_block_codes(uint8_t* base, int64_t prow, int D) {
+  return base + (prow >> 4) * fp8_block_bytes(D);
+}
 __host__ __device__ __forceinline__ float* fp8_scale_ptr(uint8_t* base, int64_t prow, int D) {
   return reinterpret_cast<float*>(base + (prow >> 4) * fp8_block_bytes(D) + 16 * int64_t(D) + 4 * (prow & 15));
+}
+// The 8 V codes of block row r, dims d0 .. d0+7 (d0 % 8 == 0), as one uint2 (logical order).
+__device__ __forceinline__ uint2 fp8_vcodes8(const uint8_t* blk, int r, int d0, int D) {
+  if (!HPA_FP8_VPAIR) return *reinterpret_cast<const uint2*>(blk + r * D + d0);
+  const uint4 ch = *reinterpret_cast<const uint4*>(blk + fp8_voff(r & ~1, d0, D));  // rows 2p, 2p+1
+  const uint32_t sel = (r & 1) ? 0x7531u : 0x6420u;  // odd / even bytes
+  return make_uint2(__byte_perm(ch.x, ch.y, sel), __byte_perm(ch.z, ch.w, sel));
+}
+// Writes 8 V codes (logical order, element i in byte i) of block row r, dims d0 .. d0+7.
+__device__ __forceinline__ void fp8_vstore8(uint8_t* blk, int r, int d0, int D, uint2 codes) {
+  if (!HPA_FP8_VPAIR) {
+    *reinterpret_cast<uint2*>(blk + r * D + d0) = codes;
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    blk[fp8_voff(r, d0 + i, D)] = uint8_t(((i < 4 ? codes.x : codes.y) >> (8 * (i & 3))) & 0xff);
 }
 // Same packing on the integer ALU pipe (F2FP issues on the XU pipe that MUFU.EX2 also uses):
 // round to nearest with ties away from zero (add half an ulp of bf16, keep the upper halves).
