@@ -446,8 +446,7 @@ __device__ __forceinline__ void fp8_tile_to_bf16(const uint8_t* src, uint8_t* ds
 // swizzled 16-byte chunks) -> the bf16 [D/64][16][128 B] layout: each 16-byte chunk holds 8 dims
 // of two keys; all lanes read before any lane writes (src overlaps dst).
 template <int D>
-__device__ __forceinline__ void fp8_vtile_to_bf16(const uint8_t* src, uint8_t* dst, const float* scale_unused,
-                                                  int lane) {
+__device__ __forceinline__ void fp8_vtile_to_bf16(const uint8_t* src, uint8_t* dst, int lane) {
   constexpr int kChunks = 16 * D / 16;  // 16-byte chunks in the tile's code area
   constexpr int kPer = kChunks / 32;
   constexpr int kCPR = 2 * D / 16;      // chunks per pair row
@@ -1018,7 +1017,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         }
         __syncwarp();
         fp8_tile_to_bf16<D, true>(kt + L::oK8, kt, lane);
-        if (HPA_FP8_VPAIR) fp8_vtile_to_bf16<D>(kt + L::oV8, vt, nullptr, lane);
+        if (HPA_FP8_VPAIR) fp8_vtile_to_bf16<D>(kt + L::oV8, vt, lane);
         else fp8_tile_to_bf16<D>(kt + L::oV8, vt, lane);
         __syncwarp();
       }
