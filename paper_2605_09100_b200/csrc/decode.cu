@@ -848,7 +848,9 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
           mma_f16_16816(sacc, ka, qbk[ks][0], qbk[ks][1]);
         }
       }
-      if (c8) {
+      // shared-memory conversions only for the variant builds (both operands are read from the
+      // codes directly by default)
+      if (c8 && (HPA_FP8_F16 || !kreg || !HPA_FP8_VPAIR)) {
         __syncwarp();
         if (HPA_FP8_F16) {
           fp8_tile_to_f16<D, true>(kt + L::oK8, kt, lane);
