@@ -31,7 +31,10 @@ namespace hpa {
 namespace {
 
 constexpr int kChunk = 16;  // rows per pipeline chunk (one m16n8k16 K-step of keys)
-constexpr int kNCons = 4;   // consumer warps per CTA
+#ifndef HPA_DEC_NCONS
+#define HPA_DEC_NCONS 4
+#endif
+constexpr int kNCons = HPA_DEC_NCONS;  // consumer warps per CTA
 #ifndef HPA_DEC_MAP3
 #define HPA_DEC_MAP3 1  // must match runtime.cpp: decode tensor maps are 3-D (one TMA per tile)
 #endif
@@ -72,7 +75,7 @@ constexpr int kNSt = HPA_DEC_STAGES;  // ring depth
 // completions land out of order, so consumer 3 can wait for item 23 (phase 2) while phase 1
 // is still open, and try_wait.parity(phase 2) matches the completed phase 0 (same parity):
 // an ABA that reads a stale stage (found with HPA_DEC_DEBUG_RING stage tags).
-static_assert(HPA_DEC_STAGES % 4 == 0 || HPA_DEC_ALLOW_ANY_DEPTH, "decode ring depth must be a multiple of the consumer count");
+static_assert(HPA_DEC_STAGES % kNCons == 0 || HPA_DEC_ALLOW_ANY_DEPTH, "decode ring depth must be a multiple of the consumer count");
 #ifndef HPA_FENCE_MODE
 #define HPA_FENCE_MODE 2  // 0: fence.sc (threadfence), 1: fence.acq_rel, 2: atom.acq_rel
 #endif
