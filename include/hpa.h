@@ -109,8 +109,9 @@ hpa_status_t hpa_cache_pools(hpa_cache_t* c, void** k_pool, void** v_pool, uint6
  * a block means code * scale. K rows (not V) store their 16-byte code chunks XOR-swizzled:
  * logical chunk c of block row r sits at chunk c ^ (r & (d/16 - 1)) (bank-conflict-free
  * register loads of the K fragments in decode). V rows pair up: the codes of block rows 2p and
- * 2p+1 interleave by dim in "pair row" p (2 d bytes: byte 2 j + (row & 1) holds dim j), whose
- * 16-byte chunks are XOR-swizzled by p & 7 (one 16-bit load = a V^T operand register). The cache owns the pools; read-only for callers (tests
+ * 2p+1 interleave in "pair row" p (2 d bytes: dim 16 m + 8 h + g, g < 8, of row r at byte
+ * 32 m + 4 g + 2 h + (r & 1)), whose 16-byte chunks are XOR-swizzled by (2p) & 7 (one 32-bit
+ * load = two V^T operand registers). The cache owns the pools; read-only for callers (tests
  * compare them bit-exactly with the oracle's quantizer). HPA_ERR_INVALID_ARG if the cache
  * stores bf16 token pages. */
 hpa_status_t hpa_cache_token_pool(hpa_cache_t* c, void** k8, void** v8, int32_t* free_token_pages);

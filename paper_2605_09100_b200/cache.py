@@ -319,12 +319,13 @@ class Cache:
             if is_k:  # a logical-order copy
                 codes = codes.reshape(nblk, 16, nch, 16)[:, r, swz, :]
             else:
-                # V: pair row p holds keys 2p, 2p + 1 interleaved by dim (byte 2 d + key parity)
-                # in 2 d/16 chunks of 16 bytes, chunk c at c ^ (p & 7)
+                # V: pair row p holds keys 2p, 2p + 1: dim 16 m + 8 h + g of row r at byte
+                # 32 m + 4 g + 2 h + (r & 1), in 2 d/16 chunks of 16 bytes, chunk c at c ^ ((2 p) & 7)
                 pr = torch.arange(8, device=dev)[:, None]
-                vsw = torch.arange(2 * nch, device=dev)[None, :] ^ (pr & 7)
-                lin = codes.reshape(nblk, 8, 2 * nch, 16)[:, pr, vsw, :].reshape(nblk, 8, self.d, 2)
-                codes = lin.permute(0, 1, 3, 2).reshape(nblk, 16, self.d)
+                vsw = torch.arange(2 * nch, device=dev)[None, :] ^ ((2 * pr) & 7)
+                lin = codes.reshape(nblk, 8, 2 * nch, 16)[:, pr, vsw, :].reshape(nblk, 8, nch, 8, 2, 2)
+                # (block, p, m, g, h, parity) -> (block, p, parity, m, h, g)
+                codes = lin.permute(0, 1, 5, 2, 4, 3).reshape(nblk, 16, self.d)
             codes = codes.reshape(self.L, self.num_token_pages, self.Hkv, self.P, self.d)
             scales = raw[:, 16 * self.d:].contiguous().view(torch.float32).reshape(
                 self.L, self.num_token_pages, self.Hkv, self.P)

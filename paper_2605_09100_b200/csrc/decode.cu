@@ -446,26 +446,31 @@ __device__ __forceinline__ void fp8_tile_to_bf16(const uint8_t* src, uint8_t* ds
   }
 }
 // The V tile of an fp8 chunk in the HPA_FP8_VPAIR layout (pair rows of interleaved key codes,
-// swizzled 16-byte chunks) -> the bf16 [D/64][16][128 B] layout: each 16-byte chunk holds 8 dims
-// of two keys; all lanes read before any lane writes (src overlaps dst).
+// swizzled 16-byte chunks; ptx.cuh fp8_voff) -> the bf16 [D/64][16][128 B] layout: the two chunks
+// of a (pair row, 16-dim group) hold 8-dim groups 2m and 2m + 1 of both keys; all lanes read
+// before any lane writes (src overlaps dst).
 template <int D>
 __device__ __forceinline__ void fp8_vtile_to_bf16(const uint8_t* src, uint8_t* dst, int lane) {
-  constexpr int kChunks = 16 * D / 16;  // 16-byte chunks in the tile's code area
-  constexpr int kPer = kChunks / 32;
-  constexpr int kCPR = 2 * D / 16;      // chunks per pair row
-  uint4 c[kPer];
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) c[i] = reinterpret_cast<const uint4*>(src)[32 * i + lane];
-  __syncwarp();
+  constexpr int kGroups = D / 16;           // 16-dim groups per pair row
+  constexpr int kPer = 8 * kGroups / 32;    // (pair row, group) items per lane
+  uint4 ca[kPer], cb[kPer];                 // the group's two chunks: dims g and g + 8, g < 4 / g >= 4
 #pragma unroll
   for (int i = 0; i < kPer; ++i) {
-    const int q = 32 * i + lane, pr = q / kCPR, cl = (q % kCPR) ^ (pr & 7);  // logical chunk
-    const int dg = cl;  // 8-dim group: lin 16 cl .. 16 cl + 15 = dims 8 cl .. 8 cl + 7 of both keys
+    const int q = 32 * i + lane, pr = q / kGroups, m = q % kGroups;
+    ca[i] = *reinterpret_cast<const uint4*>(src + fp8_voff(2 * pr, 16 * m, D));
+    cb[i] = *reinterpret_cast<const uint4*>(src + fp8_voff(2 * pr, 16 * m + 4, D));
+  }
+  __syncwarp();  // the source overlaps the destination tile
 #pragma unroll
-    for (int odd = 0; odd < 2; ++odd) {
-      const uint32_t sel = odd ? 0x7531u : 0x6420u;
-      const uint2 codes = make_uint2(__byte_perm(c[i].x, c[i].y, sel), __byte_perm(c[i].z, c[i].w, sel));
-      const int r = 2 * pr + odd;
+  for (int i = 0; i < kPer; ++i) {
+    const int q = 32 * i + lane, pr = q / kGroups, m = q % kGroups;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {  // byte b = 2 h + key parity of every word
+      const uint32_t sel = uint32_t(b) | (uint32_t(b + 4) << 4);
+      const uint2 codes = make_uint2(
+          __byte_perm(__byte_perm(ca[i].x, ca[i].y, sel), __byte_perm(ca[i].z, ca[i].w, sel), 0x5410),
+          __byte_perm(__byte_perm(cb[i].x, cb[i].y, sel), __byte_perm(cb[i].z, cb[i].w, sel), 0x5410));
+      const int r = 2 * pr + (b & 1), dg = 2 * m + (b >> 1);  // row, 8-dim group
       *reinterpret_cast<int4*>(dst + (dg >> 3) * 2048 + sw128(r, dg & 7)) = bf16x8_from_e4m3(codes, 1.f);
     }
   }
@@ -919,11 +924,14 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
 #pragma unroll
         for (int mt = 0; mt < D / 16; ++mt) {
           const int d = 16 * mt + gq;
+          // one 32-bit load = dims d and d + 8 of keys (2t, 2t+1) (resp. 2t+8, 2t+9)
+          const uint32_t w0 = *reinterpret_cast<const uint32_t*>(vb + fp8_voff(2 * tq, d, D));
+          const uint32_t w1 = *reinterpret_cast<const uint32_t*>(vb + fp8_voff(2 * tq + 8, d, D));
           uint32_t va[4];
-          va[0] = f16x2_from_e4m3x2(*reinterpret_cast<const uint16_t*>(vb + fp8_voff(2 * tq, d, D)));
-          va[1] = f16x2_from_e4m3x2(*reinterpret_cast<const uint16_t*>(vb + fp8_voff(2 * tq, d + 8, D)));
-          va[2] = f16x2_from_e4m3x2(*reinterpret_cast<const uint16_t*>(vb + fp8_voff(2 * tq + 8, d, D)));
-          va[3] = f16x2_from_e4m3x2(*reinterpret_cast<const uint16_t*>(vb + fp8_voff(2 * tq + 8, d + 8, D)));
+          va[0] = f16x2_from_e4m3x2(w0);
+          va[1] = f16x2_from_e4m3x2(w0 >> 16);
+          va[2] = f16x2_from_e4m3x2(w1);
+          va[3] = f16x2_from_e4m3x2(w1 >> 16);
           mma_f16_16816(o[mt], va, pb0, pb1);
         }
       } else {

@@ -206,10 +206,12 @@ __host__ __device__ __forceinline__ int fp8_kswz(int off, int64_t prow, int D) {
 __host__ __device__ __forceinline__ uint8_t* fp8_kcode_ptr(uint8_t* base, int64_t prow, int D, int off) {
   return fp8_code_ptr(base, prow, D) + fp8_kswz(off, prow, D);
 }
-// V rows (HPA_FP8_VPAIR): the codes of keys 2p and 2p+1 of a 16-row block interleave by dim
-// in "pair row" p (byte 2d + (r & 1) of the pair row), and the pair row's 16-byte chunks are
-// XOR-swizzled by p, so one 16-bit load gives the (key 2p, key 2p+1) code pair of a dim --
-// an f16x2 register of the V^T MMA operand -- without bank conflicts.
+// V rows (HPA_FP8_VPAIR): the codes of keys 2p and 2p+1 of a 16-row block interleave in
+// "pair row" p: dim 16m + 8h + g (g < 8) of row r sits at byte 32m + 4g + 2h + (r & 1), so the
+// 4 bytes at 32m + 4g are the (key 2p, key 2p+1) code pairs of dims 16m + g and 16m + g + 8 --
+// two f16x2 registers of the V^T MMA operand (rows g and g + 8 of M tile m) from one 32-bit
+// load. The pair row's 16-byte chunks are XOR-swizzled by (2p) & 7, which makes those loads
+// (lanes (g, t) read pair rows t and t + 4) bank-conflict-free.
 #ifndef HPA_FP8_VPAIR
 #define HPA_FP8_VPAIR 1
 #endif
@@ -219,8 +221,8 @@ __host__ __device__ __forceinline__ uint8_t* fp8_kcode_ptr(uint8_t* base, int64_
 #endif
 __host__ __device__ __forceinline__ int fp8_voff(int r, int d, int D) {  // byte in the block's code area
   if (!HPA_FP8_VPAIR) return r * D + d;
-  const int pr = r >> 1, lin = 2 * d + (r & 1);
-  return pr * 2 * D + ((((lin >> 4) ^ (pr & 7))) << 4) + (lin & 15);
+  const int pr = r >> 1, lin = 32 * (d >> 4) + 4 * (d & 7) + 2 * ((d >> 3) & 1) + (r & 1);
+  return pr * 2 * D + ((((lin >> 4) ^ ((2 * pr) & 7))) << 4) + (lin & 15);
 }
 __host__ __device__ __forceinline__ uint8_t* fp8_block_codes(uint8_t* base, int64_t prow, int D) {
   return base + (prow >> 4) * fp8_block_bytes(D);
@@ -231,9 +233,15 @@ __host__ __device__ __forceinline__ float* fp8_scale_ptr(uint8_t* base, int64_t 
 // The 8 V codes of block row r, dims d0 .. d0+7 (d0 % 8 == 0), as one uint2 (logical order).
 __device__ __forceinline__ uint2 fp8_vcodes8(const uint8_t* blk, int r, int d0, int D) {
   if (!HPA_FP8_VPAIR) return *reinterpret_cast<const uint2*>(blk + r * D + d0);
-  const uint4 ch = *reinterpret_cast<const uint4*>(blk + fp8_voff(r & ~1, d0, D));  // rows 2p, 2p+1
-  const uint32_t sel = (r & 1) ? 0x7531u : 0x6420u;  // odd / even bytes
-  return make_uint2(__byte_perm(ch.x, ch.y, sel), __byte_perm(ch.z, ch.w, sel));
+  // dims d0 + g sit at byte 4 g + b (b = 2 h + (r & 1)) of the 32 bytes of group d0 / 16:
+  // byte b of every word of its two chunks
+  const int m16 = d0 & ~15, b = 2 * ((d0 >> 3) & 1) + (r & 1);
+  const uint4 ca = *reinterpret_cast<const uint4*>(blk + fp8_voff(r & ~1, m16, D));      // dims m16 + 0..3
+  const uint4 cb = *reinterpret_cast<const uint4*>(blk + fp8_voff(r & ~1, m16 + 4, D));  // dims m16 + 4..7
+  const uint32_t sel = uint32_t(b) | (uint32_t(b + 4) << 4);
+  const uint32_t a01 = __byte_perm(ca.x, ca.y, sel), a23 = __byte_perm(ca.z, ca.w, sel);
+  const uint32_t b01 = __byte_perm(cb.x, cb.y, sel), b23 = __byte_perm(cb.z, cb.w, sel);
+  return make_uint2(__byte_perm(a01, a23, 0x5410), __byte_perm(b01, b23, 0x5410));
 }
 // Writes 8 V codes (logical order, element i in byte i) of block row r, dims d0 .. d0+7.
 __device__ __forceinline__ void fp8_vstore8(uint8_t* blk, int r, int d0, int D, uint2 codes) {
