@@ -65,6 +65,12 @@ constexpr int kNCons = HPA_DEC_NCONS;  // consumer warps per CTA
 #ifndef HPA_DEC_SWAP
 #define HPA_DEC_SWAP 1  // G <= 8: swapped-operand consumers (keys in M, heads in N)
 #endif
+#ifndef HPA_DEC_PAIR
+#define HPA_DEC_PAIR 0  // 1: swapped consumers take two chunks per softmax step (needs KSWZ, VPAIR, !F16; measured slower: 178.5 vs 166.1 us fp8, 208 vs 202 us bf16)
+#endif
+#ifndef HPA_DEC_VOTE_MAX
+#define HPA_DEC_VOTE_MAX 1  // swapped consumers: vote before the chunk-max reduction (skipped unless the max grows)
+#endif
 #ifndef HPA_DEC_LAZY
 #define HPA_DEC_LAZY 1  // decode consumers: lazy running-max rescale (threshold 2^8)
 #endif
@@ -804,6 +810,162 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     for (int n = 0; n < D / 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
     float m_h[2] = {-CUDART_INF_F, -CUDART_INF_F};  // running max of heads 2t, 2t+1 (log2 domain)
     float l_h[2] = {0.f, 0.f};                       // partial sums over this lane's keys
+#if HPA_DEC_PAIR
+    static_assert(HPA_FP8_KSWZ && HPA_FP8_VPAIR && !HPA_FP8_F16, "HPA_DEC_PAIR needs the register-direct fp8 paths");
+    // HPA_DEC_PAIR: a consumer takes its next two chunks (items i, i + kNCons) together: two
+    // independent QK^T MMA chains, one softmax step over 32 keys, then both PV halves. The
+    // stages are released together. No deadlock with kNSt >= 3 kNCons: the producer waiting for
+    // item n - kNSt finds its holder waiting at most for item n - kNSt + kNCons < n.
+    static_assert(kNSt >= 3 * kNCons, "paired decode consumers need a ring of >= 3 items per consumer");
+    for (;;) {
+      const int sA = i % kNSt;
+      mbar_wait(&full[sA], (i / kNSt) & 1);
+      int nv[2];
+      nv[0] = cmeta[sA];
+      if (nv[0] <= 0) {  // sentinel: release the slot and finish the unit
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[sA]);
+        i += kNCons;
+        break;
+      }
+      const uint32_t iB = i + kNCons;
+      const int sB = iB % kNSt;
+      mbar_wait(&full[sB], (iB / kNSt) & 1);
+      nv[1] = cmeta[sB];
+      const bool haveB = nv[1] > 0;  // else item iB is the unit's sentinel
+      const int sl[2] = {sA, sB};
+      float x[2][4], vm[2][2];
+      bool c8[2] = {false, false};
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        x[c][0] = x[c][1] = x[c][2] = x[c][3] = -CUDART_INF_F;
+        vm[c][0] = vm[c][1] = 0.f;
+        if (c == 1 && !haveB) continue;
+        c8[c] = nv[c] >= 0x10000;
+        const int nvalid = nv[c] & 0xffff;
+        const uint8_t* kt = stages + sl[c] * L::kStageBytes;
+        float kmul0 = sl2, kmul1 = sl2;
+        vm[c][0] = vm[c][1] = vpre;
+        float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+        if (c8[c]) {
+          const float* ksc = reinterpret_cast<const float*>(kt + L::oK8 + 16 * D);
+          const float* vsc = reinterpret_cast<const float*>(kt + L::oV8 + 16 * D);
+          kmul0 = ksc[gq] * sl2;
+          kmul1 = ksc[gq + 8] * sl2;
+          vm[c][0] = vsc[gq] * vpre;
+          vm[c][1] = vsc[gq + 8] * vpre;
+          const uint8_t* kb = kt + L::oK8;
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks) {
+            const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + gq * D + fp8_kswz(ks * 16 + 4 * tq, gq, D));
+            const uint32_t w1 =
+                *reinterpret_cast<const uint32_t*>(kb + (gq + 8) * D + fp8_kswz(ks * 16 + 4 * tq, gq + 8, D));
+            uint32_t ka[4];
+            ka[0] = f16x2_from_e4m3x2(w0);
+            ka[1] = f16x2_from_e4m3x2(w1);
+            ka[2] = f16x2_from_e4m3x2(w0 >> 16);
+            ka[3] = f16x2_from_e4m3x2(w1 >> 16);
+            mma_f16_16816(sacc, ka, qbk[ks][0], qbk[ks][1]);
+          }
+        } else {
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks) {  // A = K (16 keys x 16 dims)
+            const int mi = lane >> 3;
+            const int row = (lane & 7) + (mi & 1) * 8;
+            const int kc = ks * 2 + (mi >> 1);
+            uint32_t ka[4];
+            ldsm_x4(smem_u32(kt + (kc >> 3) * 2048 + sw128(row, kc & 7)), ka[0], ka[1], ka[2], ka[3]);
+            mma_bf16_16816(sacc, ka, qbf[ks][0], qbf[ks][1]);
+          }
+        }
+        x[c][0] = gq < nvalid ? sacc[0] * kmul0 : -CUDART_INF_F;      // key g,   head 2t
+        x[c][1] = gq < nvalid ? sacc[1] * kmul0 : -CUDART_INF_F;      // key g,   head 2t+1
+        x[c][2] = gq + 8 < nvalid ? sacc[2] * kmul1 : -CUDART_INF_F;  // key g+8, head 2t
+        x[c][3] = gq + 8 < nvalid ? sacc[3] * kmul1 : -CUDART_INF_F;  // key g+8, head 2t+1
+      }
+      float mx0 = fmaxf(fmaxf(x[0][0], x[0][2]), fmaxf(x[1][0], x[1][2]));
+      float mx1 = fmaxf(fmaxf(x[0][1], x[0][3]), fmaxf(x[1][1], x[1][3]));
+      const bool any_grow = __any_sync(0xffffffffu, mx0 > m_h[0] + 8.f || mx1 > m_h[1] + 8.f);
+      if (any_grow) {
+#pragma unroll
+        for (int off = 4; off < 32; off <<= 1) {  // over the 8 key-row lanes
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+        }
+      }
+      const bool g0 = any_grow && mx0 > m_h[0] + 8.f, g1 = any_grow && mx1 > m_h[1] + 8.f;
+      const float mn0 = g0 ? mx0 : m_h[0], mn1 = g1 ? mx1 : m_h[1];
+      float pp[2][4];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        pp[c][0] = fast_exp2(x[c][0] - mn0);
+        pp[c][1] = fast_exp2(x[c][1] - mn1);
+        pp[c][2] = fast_exp2(x[c][2] - mn0);
+        pp[c][3] = fast_exp2(x[c][3] - mn1);
+      }
+      const float s0 = (pp[0][0] + pp[0][2]) + (pp[1][0] + pp[1][2]);
+      const float s1 = (pp[0][1] + pp[0][3]) + (pp[1][1] + pp[1][3]);
+      if (!any_grow) {
+        l_h[0] += s0;
+        l_h[1] += s1;
+      } else {
+        const float al0 = fast_exp2(m_h[0] - mn0), al1 = fast_exp2(m_h[1] - mn1);
+        m_h[0] = mn0;
+        m_h[1] = mn1;
+        l_h[0] = l_h[0] * al0 + s0;
+        l_h[1] = l_h[1] * al1 + s1;
+#pragma unroll
+        for (int n = 0; n < D / 16; ++n) {
+          o[n][0] *= al0;
+          o[n][1] *= al1;
+          o[n][2] *= al0;
+          o[n][3] *= al1;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        if (c == 1 && !haveB) continue;
+        const uint8_t* kt = stages + sl[c] * L::kStageBytes;
+        if (c8[c]) {  // fp8 V^T fragments straight from the pair-row codes (see the unpaired loop)
+          const uint32_t pb0 = movmatrix_t(pack_f16(pp[c][0] * vm[c][0], pp[c][1] * vm[c][0]));
+          const uint32_t pb1 = movmatrix_t(pack_f16(pp[c][2] * vm[c][1], pp[c][3] * vm[c][1]));
+          const uint8_t* vb = kt + L::oV8;
+#pragma unroll
+          for (int mt = 0; mt < D / 16; ++mt) {
+            const int d = 16 * mt + gq;
+            const uint32_t w0 = *reinterpret_cast<const uint32_t*>(vb + fp8_voff(2 * tq, d, D));
+            const uint32_t w1 = *reinterpret_cast<const uint32_t*>(vb + fp8_voff(2 * tq + 8, d, D));
+            uint32_t va[4];
+            va[0] = f16x2_from_e4m3x2(w0);
+            va[1] = f16x2_from_e4m3x2(w0 >> 16);
+            va[2] = f16x2_from_e4m3x2(w1);
+            va[3] = f16x2_from_e4m3x2(w1 >> 16);
+            mma_f16_16816(o[mt], va, pb0, pb1);
+          }
+        } else {
+          const uint32_t pb0 = movmatrix_t(pack_bf16(pp[c][0] * vm[c][0], pp[c][1] * vm[c][0]));
+          const uint32_t pb1 = movmatrix_t(pack_bf16(pp[c][2] * vm[c][1], pp[c][3] * vm[c][1]));
+          const uint8_t* vt = kt + L::kTileBytes;
+#pragma unroll
+          for (int mt = 0; mt < D / 16; ++mt) {  // A = V^T (16 dims x 16 keys)
+            const int mi = lane >> 3;
+            const int key = (lane & 7) + (mi >> 1) * 8;
+            const int dc = 2 * mt + (mi & 1);
+            uint32_t va[4];
+            ldsm_x4_t(smem_u32(vt + (dc >> 3) * 2048 + sw128(key, dc & 7)), va[0], va[1], va[2], va[3]);
+            mma_bf16_16816(o[mt], va, pb0, pb1);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&empty[sA]);
+        mbar_arrive(&empty[sB]);
+      }
+      i = iB + kNCons;
+      if (!haveB) break;
+    }
+#else
     for (;; i += kNCons) {
       const int slot = i % kNSt;
       mbar_wait(&full[slot], (i / kNSt) & 1);
@@ -887,29 +1049,40 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       const float x2 = gq + 8 < nvalid ? sacc[2] * kmul1 : -CUDART_INF_F;  // key g+8, head 2t
       const float x3 = gq + 8 < nvalid ? sacc[3] * kmul1 : -CUDART_INF_F;  // key g+8, head 2t+1
       float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
-#pragma unroll
-      for (int off = 4; off < 32; off <<= 1) {  // over the 8 key-row lanes
-        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
-      }
-      // lazy rescale: the running max moves only when the chunk max exceeds it by > 2^8
-      const bool g0 = mx0 > m_h[0] + 8.f, g1 = mx1 > m_h[1] + 8.f;
-      const float mn0 = g0 ? mx0 : m_h[0], mn1 = g1 ? mx1 : m_h[1];
-      const bool any_grow = __any_sync(0xffffffffu, g0 || g1);
-      const float al0 = fast_exp2(m_h[0] - mn0), al1 = fast_exp2(m_h[1] - mn1);
-      m_h[0] = mn0;
-      m_h[1] = mn1;
-      const float p0 = fast_exp2(x0 - mn0), p1 = fast_exp2(x1 - mn1);
-      const float p2 = fast_exp2(x2 - mn0), p3 = fast_exp2(x3 - mn1);
-      l_h[0] = l_h[0] * al0 + (p0 + p2);
-      l_h[1] = l_h[1] * al1 + (p1 + p3);
+      // lazy rescale: the running max moves only when the chunk max exceeds it by > 2^8.
+      // HPA_DEC_VOTE_MAX: one vote on the lanes' own keys first; the 8-lane max reduction
+      // runs only when some key grows the max (same result: no lane grows <=> the max doesn't)
+      bool any_grow = true;
+      if (HPA_DEC_VOTE_MAX) any_grow = __any_sync(0xffffffffu, mx0 > m_h[0] + 8.f || mx1 > m_h[1] + 8.f);
       if (any_grow) {
 #pragma unroll
-        for (int n = 0; n < D / 16; ++n) {
-          o[n][0] *= al0;
-          o[n][1] *= al1;
-          o[n][2] *= al0;
-          o[n][3] *= al1;
+        for (int off = 4; off < 32; off <<= 1) {  // over the 8 key-row lanes
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+        }
+      }
+      const bool g0 = any_grow && mx0 > m_h[0] + 8.f, g1 = any_grow && mx1 > m_h[1] + 8.f;
+      const float mn0 = g0 ? mx0 : m_h[0], mn1 = g1 ? mx1 : m_h[1];
+      if (!HPA_DEC_VOTE_MAX) any_grow = __any_sync(0xffffffffu, g0 || g1);
+      const float p0 = fast_exp2(x0 - mn0), p1 = fast_exp2(x1 - mn1);
+      const float p2 = fast_exp2(x2 - mn0), p3 = fast_exp2(x3 - mn1);
+      if (HPA_DEC_VOTE_MAX && !any_grow) {  // max unchanged: the factors are 1 (l * 1 + s == l + s)
+        l_h[0] += p0 + p2;
+        l_h[1] += p1 + p3;
+      } else {
+        const float al0 = fast_exp2(m_h[0] - mn0), al1 = fast_exp2(m_h[1] - mn1);
+        m_h[0] = mn0;
+        m_h[1] = mn1;
+        l_h[0] = l_h[0] * al0 + (p0 + p2);
+        l_h[1] = l_h[1] * al1 + (p1 + p3);
+        if (any_grow) {
+#pragma unroll
+          for (int n = 0; n < D / 16; ++n) {
+            o[n][0] *= al0;
+            o[n][1] *= al1;
+            o[n][2] *= al0;
+            o[n][3] *= al1;
+          }
         }
       }
       // B operand P^T: (key g: heads 2t, 2t+1) pairs transposed in registers to (head g: keys
@@ -951,6 +1124,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
     }
+#endif  // HPA_DEC_PAIR
     // ---------------------------------------------- merge the consumers' states
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
