@@ -469,3 +469,57 @@ def test_oracle_cache_fp8_tokens_and_bf16_latents():
     assert kl2.shape[1] == 32
     exp = bf16_round(e4m3_values()[kc[0, 24:, 0]].astype(np.float32) * ks[0, 24:, 0][:, None])
     assert np.array_equal(kl2[0, 16:], exp)
+
+
+# --------------------------------------------------------------------------- bf16 rounding
+def _bf16_rne_bits(x32: float) -> float:
+    """Independent fp32 -> bf16 round-to-nearest-even on the bit pattern (pure Python):
+    keep the upper 16 bits after adding 0x7FFF + (bit 16), the textbook RNE carry trick;
+    NaN stays NaN (quieted), +-inf stay +-inf, overflow past the largest bf16 gives inf."""
+    import struct
+    u = struct.unpack("<I", struct.pack("<f", x32))[0]
+    if (u & 0x7F800000) == 0x7F800000 and (u & 0x007FFFFF):       # NaN
+        return float("nan")
+    lsb = (u >> 16) & 1
+    u = ((u + 0x7FFF + lsb) >> 16) << 16
+    return struct.unpack("<f", struct.pack("<I", u & 0xFFFFFFFF))[0]
+
+
+def test_bf16_round_matches_bit_level_rne():
+    """Pins oracle.bf16_round (used by the fp8 -> bf16 latent conversion of compress,
+    reading A20) against the bit-level RNE definition: ties to even in both directions,
+    subnormals, the overflow edge, +-inf, NaN, signed zero, and random fp32 values.
+    A truncating or ties-away rounding fails the tie rows."""
+    import struct
+    from oracle import bf16_round
+
+    def f32(bits):
+        return struct.unpack("<f", struct.pack("<I", bits))[0]
+
+    ulp = 2.0 ** -7
+    hand = [  # (input, expected) fixed by the format: 7 stored mantissa bits
+        (1.0 + ulp / 2, 1.0),                      # tie, lower neighbour even
+        (1.0 + 3 * ulp / 2, 1.0 + 2 * ulp),        # tie, upper neighbour even
+        (-(1.0 + 3 * ulp / 2), -(1.0 + 2 * ulp)),
+        (1.0 + ulp / 2 + 2.0 ** -20, 1.0 + ulp),   # just above a tie
+        (1.0 + ulp / 2 - 2.0 ** -20, 1.0),         # just below a tie
+    ]
+    for x, want in hand:
+        assert bf16_round(np.array([x]))[0] == want, (x, want)
+    edge_bits = [0x00000000, 0x80000000, 0x00000001, 0x00008000, 0x00018000, 0x00008001,
+                 0x007FFFFF, 0x00800000, 0x3F808000, 0x3F818000, 0x7F7F7FFF, 0x7F7F8000,
+                 0x7F7FFFFF, 0xFF7FFFFF, 0x7F800000, 0xFF800000, 0x3F800000, 0xC0490FDB]
+    rng = np.random.default_rng(11)
+    rand_bits = [int(b) for b in rng.integers(0, 2 ** 32, 4000, dtype=np.uint64)]
+    rand_bits = [b for b in rand_bits if not ((b & 0x7F800000) == 0x7F800000 and b & 0x7FFFFF)]
+    bits = edge_bits + rand_bits
+    xs = np.array([f32(b) for b in bits], dtype=np.float32)
+    got = bf16_round(xs)
+    want = np.array([_bf16_rne_bits(float(x)) for x in xs])
+    assert np.array_equal(got, want)
+    assert np.array_equal(np.signbit(got), np.signbit(want))      # -0 stays -0
+    assert np.isnan(bf16_round(np.array([np.nan], dtype=np.float32))[0])
+    # the checker itself distinguishes RNE from truncation and from ties-away
+    assert _bf16_rne_bits(f32(0x3F808000)) == 1.0                 # tie -> even (down)
+    assert _bf16_rne_bits(f32(0x3F818000)) == f32(0x3F820000)     # tie -> even (up)
+    assert math.isinf(_bf16_rne_bits(f32(0x7F7FFFFF)))
