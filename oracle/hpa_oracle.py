@@ -219,6 +219,34 @@ class OracleCache:
                 return set_id
         raise KeyError(f"unknown latent set {src_set_id}")
 
+    def fork(self, src_seq: int, n_prefix_rows: int, dst_seq: int) -> None:
+        """Prefix sharing ("regular KV cache including prefix KV
+        cache for user prompts"; reading A21): a new sequence dst_seq whose logical
+        content is the first n_prefix_rows rows of src_seq -- the same segments in the same
+        order (latent sets keep their set ids; dst's set counter continues from src's), the
+        segment holding row n_prefix_rows - 1 cut after it. A cut inside a latent set is
+        invalid (a latent set is one compressed memory). The model copies values; physical
+        sharing is the cache's business."""
+        if dst_seq in self.seqs:
+            raise KeyError(f"sequence {dst_seq} exists")
+        if not 0 <= n_prefix_rows <= self.seq_len(src_seq):
+            raise ValueError("n_prefix_rows outside [0, seq_len]")
+        segs, left = [], n_prefix_rows
+        for sg in self.seqs[src_seq]:
+            if left == 0:
+                break
+            if sg.rows <= left:
+                take = sg.rows
+            elif sg.kind == "latent":
+                raise ValueError("fork cut inside a latent set")
+            else:
+                take = left
+            q8 = None if sg.q8 is None else tuple(a[:, :take].copy() for a in sg.q8)
+            segs.append(_Segment(sg.kind, sg.set_id, sg.k[:, :take].copy(), sg.v[:, :take].copy(), q8))
+            left -= take
+        self.seqs[dst_seq] = segs
+        self.next_set[dst_seq] = self.next_set[src_seq]
+
     def remove(self, seq_id: int, set_id: int) -> None:
         segs = self.seqs[seq_id]
         for i, s in enumerate(segs):
