@@ -262,14 +262,24 @@ class OracleCache:
     def latent_rows(self, seq_id: int) -> int:
         return sum(s.rows for s in self.seqs[seq_id] if s.kind == "latent")
 
-    def logical_kv(self, seq_id: int, layer: int) -> Tuple[np.ndarray, np.ndarray]:
-        """Gather route 1: concatenate segments in order -> K, V [H_kv][Lb][d]."""
+    def logical_kv(self, seq_id: int, layer: int, fp8_staged: bool = False) -> Tuple[np.ndarray, np.ndarray]:
+        """Gather route 1: concatenate segments in order -> K, V [H_kv][Lb][d].
+
+        fp8_staged (fp8 token pages only): the rows chunked prefill attends over. Reading A20:
+        prefill reads token pages through bf16 staging pages holding bf16(fp32(code) * scale),
+        the same conversion as compress; decode reads code * scale directly (the default)."""
         segs = self.seqs[seq_id]
         if not segs:
             z = np.zeros((self.Hkv, 0, self.d))
             return z, z.copy()
-        k = np.concatenate([s.k[layer] for s in segs], axis=0)  # [Lb][H_kv][d]
-        v = np.concatenate([s.v[layer] for s in segs], axis=0)
+
+        def rows(s, which):
+            if fp8_staged and s.q8 is not None:
+                codes, scales = (s.q8[0], s.q8[1]) if which == 0 else (s.q8[2], s.q8[3])
+                return bf16_round(e4m3_values()[codes[layer]].astype(np.float32) * scales[layer][..., None])
+            return (s.k if which == 0 else s.v)[layer]
+        k = np.concatenate([rows(s, 0) for s in segs], axis=0)  # [Lb][H_kv][d]
+        v = np.concatenate([rows(s, 1) for s in segs], axis=0)
         return k.transpose(1, 0, 2).copy(), v.transpose(1, 0, 2).copy()
 
     def token_codes(self, seq_id: int, layer: int):

@@ -523,3 +523,26 @@ def test_bf16_round_matches_bit_level_rne():
     assert _bf16_rne_bits(f32(0x3F808000)) == 1.0                 # tie -> even (down)
     assert _bf16_rne_bits(f32(0x3F818000)) == f32(0x3F820000)     # tie -> even (up)
     assert math.isinf(_bf16_rne_bits(f32(0x7F7FFFFF)))
+
+
+def test_fp8_staged_logical_kv_is_the_compress_conversion():
+    """logical_kv(fp8_staged=True) (the rows prefill attends over, reading A20) equals, row by
+    row, the bf16 latent rows that compress produces from the same fp8 token rows (the
+    conversion pinned bit-exact against the GPU in test_gpu_fp8.py), and leaves latent rows
+    and the default (decode) view unchanged."""
+    from oracle import OracleCache
+    rng = np.random.default_rng(12)
+    c = OracleCache(1, 2, 1, 64, 16, token_fp8=True)
+    c.create_seq(0)
+    lat = _bf16(rng.standard_normal((1, 2, 16, 1, 64)))
+    c.install(0, -1, lat)
+    k, v = _bf16(rng.standard_normal((1, 40, 1, 64)) * 300), _bf16(rng.standard_normal((1, 40, 1, 64)))
+    c.append(0, k, v)
+    ks, vs = c.logical_kv(0, 0, fp8_staged=True)
+    kd, vd = c.logical_kv(0, 0)
+    assert np.array_equal(ks[:, :16], kd[:, :16]) and np.array_equal(vs[:, :16], vd[:, :16])
+    assert not np.array_equal(ks, kd)                              # staging really rounds
+    assert np.all(np.abs(ks - kd) <= 2.0 ** -8 * np.abs(kd))      # by at most a bf16 half-ulp
+    c.compress(0, 0, 40)                                           # the 40 token rows -> a latent set
+    kc, vc = c.logical_kv(0, 0)
+    assert np.array_equal(kc[:, 16:], ks[:, 16:]) and np.array_equal(vc[:, 16:], vs[:, 16:])
