@@ -51,7 +51,32 @@ def parse():
     ap.add_argument("--sweep-n", type=int, default=8, help="GPUs the sweep's global batch is sharded over")
     ap.add_argument("--sweep-max-gb", type=float, default=120.0)
     ap.add_argument("--sweep-min-gb", type=float, default=0.0, help="only points with at least this pool size")
-    return ap.parse_args()
+    ap.add_argument("--mode", default="request", choices=["request", "head_shard", "context_parallel"],
+                    help="multi-GPU partition of the configs[1] step (SURVEY 8(e)): request shard (default, weak "
+                         "scaling, no collective), KV-head shard + NCCL all-gather of the outputs, or "
+                         "context-parallel row shards + NCCL all-gather of fp32 partials + LSE merge (both strong "
+                         "scaling: the global batch of --batch requests is fixed)")
+    a = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if a.gpus != world:
+        # never run fewer GPUs than asked for and report it as N: multi-GPU runs are launched by
+        # torchrun, which sets WORLD_SIZE (python -m torch.distributed.run --nproc-per-node N ...)
+        sys.exit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}; launch N > 1 GPUs with "
+                 f"python -m torch.distributed.run --nnodes=1 --nproc-per-node {a.gpus} bench.py --gpus {a.gpus}")
+    return a
+
+
+def init_dist():
+    """(world, rank, local) from the torchrun environment; NCCL process group when world > 1."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return world, rank, local
 
 
 def peaks():
@@ -282,14 +307,17 @@ def bench_sweep(args):
     achieved GB/s must be flat (+-3 %) across r at fixed (B, ctx). One JSON line per point,
     then a summary line. Points whose pool exceeds --sweep-max-gb are reported as skipped."""
     import torch
+    import torch.distributed as dist
     from paper_2605_09100_b200 import Cache
+    from paper_2605_09100_b200.dist import max_over_ranks
     from workloads import LATENT_ROWS, qwen3_8b_shape
-    dev = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(dev)
+    world, rank, dev = init_dist()
     stream = torch.cuda.current_stream(dev)
     pk, pk_kind = peaks()
     shape = qwen3_8b_shape(args.page_size)
-    n = args.sweep_n
+    # under torchrun every rank holds its own B/n shard and the job rate uses the slowest rank;
+    # run alone (one process), the GPU measures one shard of an --sweep-n-GPU job
+    n = world if world > 1 else args.sweep_n
     rows_bytes = shape.num_kv_heads * shape.head_dim * 2 * 2
     points = []
     for B in (512, 1024, 2048, 4096):
@@ -305,19 +333,26 @@ def bench_sweep(args):
                     continue
                 if gb > args.sweep_max_gb:
                     pt["skipped"] = f"pool {gb:.0f} GB > --sweep-max-gb {args.sweep_max_gb}"
-                    print(json.dumps(pt), flush=True)
+                    if rank == 0:
+                        print(json.dumps(pt), flush=True)
                     points.append(pt)
                     continue
-                cache, seqs, _ = build_decode_cache(torch, Cache, shape, b, sets, tok, 0, dev, seed=1234)
-                ms = time_decode_calls(torch, cache, seqs, shape, dev, stream, args.steps, args.warmup)
+                cache, seqs, _ = build_decode_cache(torch, Cache, shape, b, sets, tok, 0, dev, seed=1234 + rank)
+                if world > 1:
+                    dist.barrier(device_ids=[dev])
+                ms_local = time_decode_calls(torch, cache, seqs, shape, dev, stream, args.steps, args.warmup)
+                ms = max_over_ranks(ms_local, device=f"cuda:{dev}")
                 byts = decode_bytes([ctx] * b, shape)
-                pt.update({"decode_ms": round(ms, 4), "requests_per_s_per_gpu": round(b / (ms / 1e3), 1),
+                pt.update({"decode_ms": round(ms, 4), "requests_per_s_per_gpu": round(b / (ms_local / 1e3), 1),
                            "requests_per_s_job": round(n * b / (ms / 1e3), 1),
-                           "achieved_gbs": round(byts / (ms / 1e3) / 1e9, 1),
-                           "frac": round(byts / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 4)})
+                           "job_rate": "max over ranks (torchrun)" if world > 1 else
+                                       f"one GPU's shard x {n} (no data-path collective)",
+                           "achieved_gbs": round(byts / (ms_local / 1e3) / 1e9, 1),
+                           "frac": round(byts / (ms_local / 1e3) / 1e9 / pk["hbm_gbs"], 4)})
                 cache.close()
                 torch.cuda.empty_cache()
-                print(json.dumps(pt), flush=True)
+                if rank == 0:
+                    print(json.dumps(pt), flush=True)
                 points.append(pt)
     flat = []
     for B in (512, 1024, 2048, 4096):
@@ -327,10 +362,13 @@ def bench_sweep(args):
             if len(g) == 3:
                 flat.append({"global_batch": B, "context": ctx,
                              "spread": round((max(g) - min(g)) / (sum(g) / 3), 4)})
-    print(json.dumps({"sweep": "configs[4]", "peak": pk["hbm_gbs"], "peak_kind": pk_kind,
-                      "page_size": args.page_size,
-                      "max_latent_ratio_spread": max((f["spread"] for f in flat), default=None),
-                      "flatness": flat}), flush=True)
+    if rank == 0:
+        print(json.dumps({"sweep": "configs[4]", "peak": pk["hbm_gbs"], "peak_kind": pk_kind,
+                          "page_size": args.page_size, "n_gpus": n, "ranks_run": world,
+                          "max_latent_ratio_spread": max((f["spread"] for f in flat), default=None),
+                          "flatness": flat}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def decode_bytes(lens, shape):
@@ -352,14 +390,7 @@ def run_ours(args):
     from paper_2605_09100_b200.dist import max_over_ranks
     from workloads import qwen3_8b_shape
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    dev = local
-    torch.cuda.set_device(dev)
+    world, rank, dev = init_dist()
     stream = torch.cuda.current_stream(dev)
     pk, pk_kind = peaks()
     shape = qwen3_8b_shape(args.page_size)
@@ -511,6 +542,173 @@ def run_ours(args):
                                                    token_kv_dtype="fp8", batches=(4,))
     if rank == 0 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(budget_s=15.0)
+        res["cpu_baseline"]["other_configs"] = cpu_baseline_extra()
+    if "prefill" in res:
+        # compact prefill figures near the front of the line (the driver keeps the line's head)
+        summ = {}
+        for key in ("B1", "B4"):
+            if key in res["prefill"]:
+                pf = res["prefill"][key]
+                summ[key] = {"ms": pf["ms"], "tflops": pf["tflops"], "frac": pf["frac"],
+                             "sm_mhz": pf["clocks"].get("sm_mhz")}
+                if "sustained" in pf:
+                    summ[key]["sustained_tflops"] = pf["sustained"]["tflops"]
+                    summ[key]["sustained_frac"] = round(pf["sustained"]["tflops"] / pk.get(
+                        "bf16_tflops_sustained", pk["bf16_tflops"]), 4)
+                    summ[key]["sustained_sm_mhz"] = pf["sustained"]["clocks"].get("sm_mhz")
+        summ["peak_burst"] = pk["bf16_tflops"]
+        summ["peak_sustained"] = pk.get("bf16_tflops_sustained")
+        head = {}
+        for k_, v_ in res.items():
+            head[k_] = v_
+            if k_ == "ms_per_step":
+                head["prefill_summary"] = summ
+        res = head
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_sharded(args):
+    """--mode head_shard | context_parallel (SURVEY 8(e), NEXT-4b): the configs[1] step with the
+    global batch of --batch requests fixed (strong scaling) and each request spread over the N
+    ranks. head_shard: rank r holds kv-heads [r H_kv/N, (r+1) H_kv/N) of every request (and their
+    G q-heads); step = append + decode of its heads + one NCCL all-gather of the bf16 outputs.
+    context_parallel: rank r holds a contiguous block of every request's logical rows (cut at
+    128-row boundaries; the last rank holds the tail and receives the appended token); step =
+    append (last rank) + hpa_decode_partial + NCCL all-gather of the fp32 partials and LSEs +
+    hpa_merge_partials. Time = device time of the whole step, max over ranks."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2605_09100_b200 import Cache, merge_partials
+    from paper_2605_09100_b200.dist import gather_head_shards, gather_partials, head_shard, max_over_ranks
+    from workloads import LATENT_ROWS, Shape
+
+    world, rank, dev = init_dist()
+    stream = torch.cuda.current_stream(dev)
+    pk, pk_kind = peaks()
+    B, docs, tokens = args.batch, 8, 4095
+    Hq, Hkv, D, P = 32, 8, 128, args.page_size
+    K, W = args.steps, args.warmup
+    cd = f"cuda:{dev}"
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[dev])
+
+    last = rank == world - 1
+    if args.mode == "head_shard":
+        kv_lo, kv_hi, q_lo, q_hi = head_shard(Hq, Hkv, rank, world)
+        shape = Shape(1, q_hi - q_lo, kv_hi - kv_lo, D, P)
+        cache, seqs, _ = build_decode_cache(torch, Cache, shape, B, docs, tokens, K + W + 16, dev, seed=1234 + rank)
+        appends = True
+        part = f"kv-heads [{kv_lo}, {kv_hi}) and q-heads [{q_lo}, {q_hi}) of every request"
+    else:
+        blocks = (docs * LATENT_ROWS + tokens + 1) // LATENT_ROWS  # 40 blocks of 128 rows
+        if blocks % world:
+            sys.exit(f"context_parallel needs {blocks} % world == 0")
+        lo, hi = rank * blocks // world, (rank + 1) * blocks // world
+        lat = max(0, min(hi, docs) - lo)
+        tok = (hi - lo - lat) * LATENT_ROWS - (1 if last else 0)
+        shape = Shape(1, Hq, Hkv, D, P)
+        cache, seqs, _ = build_decode_cache(torch, Cache, shape, B, lat, tok, K + W + 16 if last else 0, dev,
+                                            seed=1234 + rank)
+        appends = last
+        part = f"logical rows [{lo * LATENT_ROWS}, {hi * LATENT_ROWS}) of every request ({lat} latent sets)"
+    ids = np.asarray(seqs, dtype=np.int32)
+    ones = np.ones(B, dtype=np.int32)
+    g = torch.Generator(device=cd).manual_seed(4321 + rank)
+    hq_l, hkv_l = shape.num_q_heads, shape.num_kv_heads
+    knew = torch.randn((K + W, 1, B, hkv_l, D), generator=g, device=cd).to(torch.bfloat16)
+    vnew = torch.randn((K + W, 1, B, hkv_l, D), generator=g, device=cd).to(torch.bfloat16)
+    qs = torch.randn((K + W, B, hq_l, D), generator=g, device=cd).to(torch.bfloat16)
+    dec_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+
+    def step(i, kk, vv, qq, e=None):
+        if appends:
+            cache.append_kv(ids, ones, kk, vv)
+        if e:
+            e[0].record(stream)
+        if args.mode == "head_shard":
+            o = cache.decode(0, ids, qq)
+            if e:
+                e[1].record(stream)
+            return gather_head_shards(o)
+        o, lse = cache.decode_partial(0, ids, qq)
+        if e:
+            e[1].record(stream)
+        if world == 1:
+            return merge_partials(o[None], lse[None])
+        return merge_partials(*gather_partials(o, lse))
+
+    for i in range(W):
+        step(i, knew[i], vnew[i], qs[i])
+    torch.cuda.synchronize(dev)
+    lens0 = [cache.seq_info(s)[0] for s in seqs]
+    launches0 = cache.launch_count()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    clk.start()
+    t0.record(stream)
+    for i in range(K):
+        full = step(W + i, knew[W + i], vnew[W + i], qs[W + i], dec_ev[i])
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk.stop()
+    barrier()
+    assert full.shape == (B, Hq, D)
+    launches = cache.launch_count() - launches0
+    step_ms = max_over_ranks(t0.elapsed_time(t1) / K, device=cd)
+    dec_ms = sum(a.elapsed_time(b) for a, b in dec_ev) / K
+    dec_ms_max = max_over_ranks(dec_ms, device=cd)
+    bytes_local = sum(decode_bytes([L + (1 + i if appends else 0) for L in lens0], shape) for i in range(K)) / K
+    achieved = bytes_local / (dec_ms / 1e3) / 1e9
+    clocks = clk.summary()
+    # e2e: pinned host inputs of this rank's shard in, the gathered output out, every step
+    pin_k, pin_v, pin_q = knew.cpu().pin_memory(), vnew.cpu().pin_memory(), qs.cpu().pin_memory()
+    pin_o = torch.empty((B, Hq, D), dtype=torch.bfloat16).pin_memory()
+    dk, dv, dq = torch.empty_like(knew[0]), torch.empty_like(vnew[0]), torch.empty_like(qs[0])
+    barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(K):
+        dk.copy_(pin_k[W + i], non_blocking=True)
+        dv.copy_(pin_v[W + i], non_blocking=True)
+        dq.copy_(pin_q[W + i], non_blocking=True)
+        full = step(W + i, dk, dv, dq)
+        pin_o.copy_(full, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / K, device=cd)
+    h2d = (dk.numel() * 2 + dv.numel() * 2 if appends else 0) + dq.numel() * 2
+    cache.close()
+    res = {
+        "metric": METRIC, "value": round(B / (step_ms / 1e3), 1), "unit": "tokens/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(step_ms, 5), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"configs[1] Qwen3-8B-shaped HPA decode step, {args.mode} over {world} GPU(s)",
+                   "mode": args.mode, "global_batch": B, "num_q_heads": Hq, "num_kv_heads": Hkv, "head_dim": D,
+                   "page_size": P, "seq_len": docs * LATENT_ROWS + tokens + 1,
+                   "parallelism": f"{args.mode} x{world}", "rank0_holds": part,
+                   "l2": "working set >> 126 MB L2 per GPU at N <= 8 (no flush needed)"},
+        "clocks": clocks,
+        "e2e": {"value": round(B / (e2e_ms / 1e3), 1), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": B * Hq * D * 2, "ms_per_step": round(e2e_ms, 5)},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": "hpa decode of this rank's shard", "achieved": round(achieved, 1),
+                     "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
+                     "peak_kind": pk_kind, "algorithmic_bytes_per_launch": int(bytes_local),
+                     "launch_ms": round(dec_ms, 5), "max_over_ranks_ms": round(dec_ms_max, 5), "traffic": None},
+        "collective": {"head_shard": "all_gather_into_tensor of bf16 [B][Hq/N][d] (NCCL)",
+                       "context_parallel": "2 x all_gather_into_tensor of fp32 [B][Hq][d] + [B][Hq] (NCCL), "
+                                           "then hpa_merge_partials"}[args.mode] if world > 1 else "none (N = 1)",
+    }
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:
@@ -634,21 +832,31 @@ def bench_lmag(torch, Cache, shape, dev, stream, W, K, world, max_over_ranks, ba
     inst_bytes = 2 * B * 128 * 8 * 128 * 2 * 2  # K+V, read + write
     dbytes = decode_bytes(lens, shape)
     cache.close()
-    # O(1) check (SURVEY 8(d) configs[3]): the install must not depend on the token context
-    o1 = {}
+    # O(1) check (SURVEY 8(d) configs[3]): the install must not depend on the token context.
+    # Device time only: a 20 ms spin kernel holds the stream while the host enqueues the 10
+    # install calls, so the events bracket back-to-back device work and the host planning
+    # (timed separately, per call) is hidden behind the spin.
+    o1, o1_host = {}, {}
     for tokens in (1024, 8192, 32768):
         cache, seqs, _ = build_decode_cache(torch, Cache, shape, B, 8, tokens, 0, dev, seed=556)
         ids = np.asarray(seqs, dtype=np.int32)
         for _ in range(3):
             cache.latent_install_packed(ids, sets[0], stage[0])
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize(dev)
-        e0.record(stream)
-        for k in range(10):
-            cache.latent_install_packed(ids, sets[k % 8], stage[k % 2])
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        o1[str(tokens)] = round(e0.elapsed_time(e1) / 10 * 1e3, 1)
+        dev_us, host_us = [], []
+        for _rep in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            torch.cuda._sleep(40_000_000)  # ~20 ms of device spin at 1.9 GHz
+            e0.record(stream)
+            h0 = time.perf_counter()
+            for k in range(10):
+                cache.latent_install_packed(ids, sets[k % 8], stage[k % 2])
+            host_us.append((time.perf_counter() - h0) / 10 * 1e6)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            dev_us.append(e0.elapsed_time(e1) / 10 * 1e3)
+        o1[str(tokens)] = round(statistics.median(dev_us), 1)
+        o1_host[str(tokens)] = round(statistics.median(host_us), 1)
         cache.close()
         torch.cuda.empty_cache()
     return {"workload": "configs[3] LMAG: B=256 decode + per-request latent set replacement each step",
@@ -657,7 +865,10 @@ def bench_lmag(torch, Cache, shape, dev, stream, W, K, world, max_over_ranks, ba
             "step_ms": round(step, 4), "install_ms": round(inst, 4), "decode_ms": round(dec, 4),
             "install_gbs": round(inst_bytes / (inst / 1e3) / 1e9, 1),
             "decode_gbs": round(dbytes / (dec / 1e3) / 1e9, 1),
-            "install_us_vs_reasoning_tokens": o1}
+            "install_us_vs_reasoning_tokens": o1,
+            "install_host_us_vs_reasoning_tokens": o1_host,
+            "install_timing": "device time per batched call (256 requests x 128 rows), host enqueue hidden "
+                              "behind a spin kernel; host planning per call reported separately"}
 
 
 def bench_next(torch, Cache, shape, dev, stream, pk, max_over_ranks):
@@ -843,6 +1054,116 @@ def cpu_baseline(budget_s: float = 15.0):
                       f"processes x {half:.1f} s (1 BLAS thread each; {wall:.1f} s wall incl. spawn)"}
 
 
+def _oracle_prefill_group_worker(args):
+    """configs[2] B_p = 1, one GQA group: this process draws the request's rows of kv-head h
+    (workloads.Draw, the bench recipe) and times oracle.attend for the sampled query rows of
+    the group's G q-heads (1 BLAS thread). Returns (flops, seconds)."""
+    seed, h, rows, budget_s = args
+    import numpy as np
+    import torch
+    from threadpoolctl import threadpool_limits
+    from oracle import attend
+    from workloads import Shape
+    C, prior, G, d = 2048, 1024 + 16384, 4, 128
+    lb = prior + C
+    g = torch.Generator().manual_seed(seed + h)
+    k = torch.randn((1, lb, d), generator=g).to(torch.bfloat16).double().numpy()
+    v = torch.randn((1, lb, d), generator=g).to(torch.bfloat16).double().numpy()
+    q = torch.randn((C, G, d), generator=g).to(torch.bfloat16).double().numpy()
+    scale = Shape(1, 32, 8, d, 16).scale
+    flops, t_work, n = 0, 0.0, 0
+    with threadpool_limits(1):
+        while t_work < budget_s:
+            t = rows[n % len(rows)]
+            i = prior + t
+            t0 = time.perf_counter()
+            attend(q[t:t + 1], k[:, :i + 1], v[:, :i + 1], scale)
+            t_work += time.perf_counter() - t0
+            flops += 4 * G * d * (i + 1)
+            n += 1
+    return flops, t_work
+
+
+def cpu_baseline_extra(budget_s: float = 8.0):
+    """SURVEY 8(d) "Oracle timing beside it" for the other configs (the fp64 oracle as it
+    stands, host cores of this box): configs[0] latency, configs[2] B_p = 1 prefill on sampled
+    query rows (extrapolated to the full chunk), configs[3] LMAG step on 8 requests
+    (extrapolated to B = 256). Each sub-object states its sample and core count."""
+    import multiprocessing as mp
+    import numpy as np
+    import torch
+    from threadpoolctl import threadpool_limits
+    from oracle import OracleCache, attend
+    from oracle.hpa_oracle import decode_reference
+    from workloads import Draw, tiny_decode
+    out = {}
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    # configs[0]: tiny decode latency
+    w = tiny_decode("a")
+    sh = w.shape
+    c = OracleCache(1, 2, 1, 64, 16)
+    dr = Draw(5)
+    c.create_seq(0)
+    for kind, m in w.seqs[0].segments:
+        if kind == "latent":
+            c.install(0, -1, dr.latent(sh, m).double().numpy())
+        else:
+            k, v = dr.tokens(sh, m)
+            c.append(0, k.double().numpy(), v.double().numpy())
+    qt = dr.queries(sh, 1).double().numpy()[0]
+    lat = []
+    with threadpool_limits(1):
+        t_end = time.perf_counter() + 1.0
+        while time.perf_counter() < t_end:
+            t0 = time.perf_counter()
+            decode_reference(c, 0, 0, qt, sh.scale)
+            lat.append(time.perf_counter() - t0)
+    out["configs0_tiny_decode"] = {"value": round(statistics.median(lat) * 1e6, 2), "unit": "us per decode",
+                                   "cores": 1, "kind": "oracle",
+                                   "sample": f"{len(lat)} decodes of the tiny config (Lb = 64) in 1 s, median"}
+    # configs[2]: B_p = 1 prefill, sampled rows
+    C, prior = 2048, 1024 + 16384
+    full_flops = 4 * 32 * 128 * (C * prior + C * (C + 1) // 2)
+    rows = [int(x) for x in np.linspace(0, C - 1, 16)]
+    f1, t1 = _oracle_prefill_group_worker((2025, 0, rows, budget_s / 2))
+    n_proc = min(cores, 8)
+    with mp.get_context("spawn").Pool(n_proc) as pool:
+        res = pool.map(_oracle_prefill_group_worker, [(2025, h, rows, budget_s / 2) for h in range(n_proc)])
+    rate_all = sum(f / t for f, t in res)
+    out["configs2_prefill_B1"] = {
+        "value": round(rate_all / 1e9, 3), "unit": "GFLOP/s", "cores": n_proc, "kind": "oracle",
+        "single_core_gflops": round(f1 / t1 / 1e9, 3),
+        "extrapolated_s_per_request": round(full_flops / rate_all, 1),
+        "extrapolated_s_per_request_1core": round(full_flops / (f1 / t1), 1),
+        "sample": f"oracle.attend on 16 query rows spread over the C = 2048 chunk (each over its causal prefix "
+                  f"of {prior}+t+1 keys), one GQA group (4 q-heads, 1 kv-head) per process, {budget_s / 2:.1f} s "
+                  f"per process; FLOPs counted as 4 G d (i+1) per row, extrapolated to the full request "
+                  f"({full_flops / 1e12:.3f} TFLOP)"}
+    # configs[3]: LMAG step (replace set step mod 8, append 1 token, decode) on 8 requests
+    n_req = 8
+    oc, qs, shp = _oracle_requests(n_req, seed=31)
+    dr = Draw(32)
+    steps, t_work = 0, 0.0
+    with threadpool_limits(1):
+        while t_work < budget_s / 2:
+            inp = [(dr.latent(shp, 128).double().numpy(), *(x.double().numpy() for x in dr.tokens(shp, 1)))
+                   for _ in range(n_req)]
+            t0 = time.perf_counter()
+            for s in range(n_req):
+                oc.install(s, steps % 8, inp[s][0])
+                oc.append(s, inp[s][1], inp[s][2])
+                decode_reference(oc, s, 0, qs[s], shp.scale)
+            t_work += time.perf_counter() - t0
+            steps += 1
+    req_s = steps * n_req / t_work
+    out["configs3_lmag"] = {"value": round(req_s, 3), "unit": "tokens/s", "cores": 1, "kind": "oracle",
+                            "extrapolated_ms_per_B256_step": round(256 / req_s * 1e3, 1),
+                            "sample": f"{steps} LMAG steps over {n_req} requests (Lb ~ 5120; per request: replace a "
+                                      f"128-row latent set, append 1 token, decode; input draws excluded), "
+                                      f"extrapolated linearly to B = 256"}
+    return out
+
+
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -881,5 +1202,7 @@ if __name__ == "__main__":
         run_reference(a)
     elif a.sweep:
         bench_sweep(a)
+    elif a.mode != "request":
+        run_sharded(a)
     else:
         run_ours(a)

@@ -269,10 +269,17 @@ hpa_status_t hpa_set_prefill_splits(hpa_cache_t* c, int32_t splits);
 hpa_status_t hpa_set_prefill_ctas(hpa_cache_t* c, int32_t n);
 /* Introspection of the last hpa_prefill / hpa_prefill_span plan: *n_ctas prefill CTAs
  * launched, *n_split_units units split into *splits key ranges each (0 / 1 when none), or
- * *n_ctas = 0 when the grid path ran. Any output pointer may be NULL. */
-hpa_status_t hpa_prefill_plan_info(hpa_cache_t* c, int32_t* n_ctas, int32_t* n_split_units, int32_t* splits);
+ * *n_ctas = 0 when the grid path ran; *cluster_size = 2 when the items ran as 2-CTA clusters
+ * sharing K/V tiles by TMA multicast, else 1. Any output pointer may be NULL. */
+hpa_status_t hpa_prefill_plan_info(hpa_cache_t* c, int32_t* n_ctas, int32_t* n_split_units, int32_t* splits,
+                                   int32_t* cluster_size);
 /* Number of kernels this cache has launched so far (bench "gpu_launches"). */
 hpa_status_t hpa_launch_count(hpa_cache_t* c, uint64_t* n);
+/* Diagnostics only (scripts/trace_*.py): a device buffer of int64 slots into which kernels
+ * built with -DHPA_TRACE write per-CTA / per-phase %globaltimer stamps (layout defined by
+ * the trace script that reads it); NULL disables. The default build ignores it. The caller
+ * owns the buffer and keeps it alive while traced kernels run. INVALID_ARG on a NULL cache. */
+hpa_status_t hpa_debug_trace(hpa_cache_t* c, void* device_buf);
 
 #ifdef __cplusplus
 }

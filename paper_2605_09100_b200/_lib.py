@@ -63,8 +63,9 @@ SIGNATURES = {
     "hpa_set_decode_splits": (c_st, [c_vp, c_i32]),
     "hpa_set_prefill_splits": (c_st, [c_vp, c_i32]),
     "hpa_set_prefill_ctas": (c_st, [c_vp, c_i32]),
-    "hpa_prefill_plan_info": (c_st, [c_vp, c_i32p, c_i32p, c_i32p]),
+    "hpa_prefill_plan_info": (c_st, [c_vp, c_i32p, c_i32p, c_i32p, c_i32p]),
     "hpa_launch_count": (c_st, [c_vp, ctypes.POINTER(ctypes.c_uint64)]),
+    "hpa_debug_trace": (c_st, [c_vp, c_vp]),
 }
 
 

@@ -347,9 +347,10 @@ class Cache:
 
     def prefill_plan_info(self) -> dict:
         """The last prefill's plan: CTAs launched, units split, key ranges per split unit."""
-        n, u, s = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
-        check(LIB.hpa_prefill_plan_info(self._h, ctypes.byref(n), ctypes.byref(u), ctypes.byref(s)))
-        return {"ctas": n.value, "split_units": u.value, "splits": s.value}
+        n, u, s, cl = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        check(LIB.hpa_prefill_plan_info(self._h, ctypes.byref(n), ctypes.byref(u), ctypes.byref(s),
+                                        ctypes.byref(cl)))
+        return {"ctas": n.value, "split_units": u.value, "splits": s.value, "cluster": cl.value}
 
     def launch_count(self) -> int:
         n = ctypes.c_uint64()

@@ -481,6 +481,35 @@ __device__ __forceinline__ void fp8_vtile_to_bf16(const uint8_t* src, uint8_t* d
     }
   }
 }
+// fp8 V path of the swapped consumers (HPA_FP8_VPAIR): P^T goes to f16 as p * s_V * vpre with
+// p <= 2^8 (lazy rescale). svmax = this lane's largest valid V scale of the chunk(s) about to be
+// packed. If some lane would reach p * s_V * vpre > 2^15 (f16 overflows at 65504), or every lane
+// stays below 2^0 (weights drifting toward f16 subnormals), vpre moves to the power of two that
+// puts the warp's largest scale times vpre in [2^6, 2^7), and O -- accumulated in units of
+// 1 / vpre -- is multiplied by the same exact factor. Rare: never for V rows of similar size.
+template <int D>
+__device__ __forceinline__ void fp8_vpre_adjust(float svmax, float& vpre, float (&o)[D / 16][4]) {
+  const float sv = svmax * vpre;
+  const bool hi = __any_sync(0xffffffffu, sv > 128.f);
+  const bool lo = __all_sync(0xffffffffu, sv < 1.f / 256.f);
+  if (!(hi || lo)) return;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) svmax = fmaxf(svmax, __shfl_xor_sync(0xffffffffu, svmax, off));
+  if (!(svmax > 0.f) || !(svmax < CUDART_INF_F)) return;
+  const int e = int((__float_as_uint(svmax) >> 23) & 0xffu) - 127;  // floor(log2 svmax) (normal scales)
+  const int k = min(max(6 - e, -100), 100);                         // new vpre = 2^k
+  const float nv = __uint_as_float(uint32_t(127 + k) << 23);
+  const float r = nv / vpre;  // a power of two: exact
+#pragma unroll
+  for (int n = 0; n < D / 16; ++n) {
+    o[n][0] *= r;
+    o[n][1] *= r;
+    o[n][2] *= r;
+    o[n][3] *= r;
+  }
+  vpre = nv;
+}
+
 // Same as fp8_tile_to_bf16 but to f16 (one cvt per code pair; e4m3 values are exact in f16):
 // the swapped-operand consumers run fp8 chunks as f16 MMAs.
 template <int D, bool KSW = false>
@@ -779,15 +808,33 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     // HPA_FP8_KSWZ: f16 B operand over the dims in the register-direct order of the fp8 K
     // path: k (2t, 2t+1) <-> dims 16 ks + 4t, +1 and k (2t+8, 2t+9) <-> dims 16 ks + 4t + 2, +3
     uint32_t qbk[D / 16][2];
+    // fp8 units: the f16 copies of Q (qbk, qbh) hold q * 2^-qs, with qs chosen per unit so that
+    // max |q| stays inside f16's range (bf16 -> f16 would overflow above 65504); the fp8 K
+    // chunks' score multiplier carries 2^qs back. qs = 0 unless max |q| >= 2^15 or < 2^-10.
+    float qmul = 1.f, sl2k = sl2;
     {
       const uint32_t* qrow = reinterpret_cast<const uint32_t*>(qbuf + qb * qbytes + gq * D * 2);
+      if (a.fp8) {
+        float qmax = 0.f;
+#pragma unroll
+        for (int w = 0; w < D / 2; w += 4) {
+          const uint32_t v = gq < G ? qrow[w + tq] : 0u;
+          qmax = fmaxf(qmax, fmaxf(fabsf(__uint_as_float(v << 16)), fabsf(__uint_as_float(v & 0xffff0000u))));
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) qmax = fmaxf(qmax, __shfl_xor_sync(0xffffffffu, qmax, off));
+        const int e = qmax > 0.f ? int((__float_as_uint(qmax) >> 23) & 0xffu) - 127 : 0;  // floor(log2), normals
+        const int qs = (e >= 15 || e < -10) ? min(max(e - 14, -100), 100) : 0;
+        qmul = __uint_as_float(uint32_t(127 - qs) << 23);
+        sl2k = sl2 * __uint_as_float(uint32_t(127 + qs) << 23);
+      }
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks) {
         qbf[ks][0] = gq < G ? qrow[8 * ks + tq] : 0u;
         qbf[ks][1] = gq < G ? qrow[8 * ks + 4 + tq] : 0u;
         if (HPA_FP8_KSWZ && a.fp8) {
-          qbk[ks][0] = gq < G ? bf16x2_to_f16x2(qrow[8 * ks + 2 * tq]) : 0u;
-          qbk[ks][1] = gq < G ? bf16x2_to_f16x2(qrow[8 * ks + 2 * tq + 1]) : 0u;
+          qbk[ks][0] = gq < G ? bf16x2_to_f16x2_scaled(qrow[8 * ks + 2 * tq], qmul) : 0u;
+          qbk[ks][1] = gq < G ? bf16x2_to_f16x2_scaled(qrow[8 * ks + 2 * tq + 1], qmul) : 0u;
         }
       }
     }
@@ -797,14 +844,20 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     if (a.fp8) {
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks) {
-        qbh[ks][0] = bf16x2_to_f16x2(qbf[ks][0]);
-        qbh[ks][1] = bf16x2_to_f16x2(qbf[ks][1]);
+        qbh[ks][0] = bf16x2_to_f16x2_scaled(qbf[ks][0], qmul);
+        qbh[ks][1] = bf16x2_to_f16x2_scaled(qbf[ks][1], qmul);
       }
     }
+    // score multiplier of an fp8 chunk's keys: those run on the f16 copies of Q
+    const float slk = (HPA_FP8_KSWZ || HPA_FP8_F16) ? sl2k : sl2;
 
-    // HPA_FP8_VPAIR: every P^T fragment is pre-scaled by vpre (f16 range for the fp8 chunks;
-    // latent bf16 chunks carry the same factor so O stays consistent); undone at the merge
-    const float vpre = (HPA_FP8_VPAIR && a.fp8) ? 256.f : 1.f;
+    // HPA_FP8_VPAIR: every P^T fragment is pre-scaled by vpre, a power of two (f16 range for
+    // the fp8 chunks; latent bf16 chunks carry the same factor so O stays consistent); undone
+    // at the merge. It starts at 2^8 and moves (fp8_vpre_adjust, O rescaled by the same exact
+    // power of two) whenever a chunk's V scales would push p * s_V * vpre (p <= 2^8 under the
+    // lazy rescale) past 2^15, or leave all of it below 2^0: f16 never overflows and keeps its
+    // normal range for the weights whatever the V row magnitudes.
+    float vpre = (HPA_FP8_VPAIR && a.fp8) ? 256.f : 1.f;
     float o[D / 16][4];  // O^T tile mt: (dim 16mt+g, head 2t), (.., 2t+1), (dim +8, 2t), (dim +8, 2t+1)
 #pragma unroll
     for (int n = 0; n < D / 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
@@ -836,6 +889,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       const int sl[2] = {sA, sB};
       float x[2][4], vm[2][2];
       bool c8[2] = {false, false};
+      float svmax = 0.f;  // this lane's largest valid V scale over both chunks
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         x[c][0] = x[c][1] = x[c][2] = x[c][3] = -CUDART_INF_F;
@@ -845,15 +899,16 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         const int nvalid = nv[c] & 0xffff;
         const uint8_t* kt = stages + sl[c] * L::kStageBytes;
         float kmul0 = sl2, kmul1 = sl2;
-        vm[c][0] = vm[c][1] = vpre;
+        vm[c][0] = vm[c][1] = 1.f;  // raw V scales here; times vpre after the adjustment below
         float sacc[4] = {0.f, 0.f, 0.f, 0.f};
         if (c8[c]) {
           const float* ksc = reinterpret_cast<const float*>(kt + L::oK8 + 16 * D);
           const float* vsc = reinterpret_cast<const float*>(kt + L::oV8 + 16 * D);
-          kmul0 = ksc[gq] * sl2;
-          kmul1 = ksc[gq + 8] * sl2;
-          vm[c][0] = vsc[gq] * vpre;
-          vm[c][1] = vsc[gq + 8] * vpre;
+          kmul0 = ksc[gq] * slk;
+          kmul1 = ksc[gq + 8] * slk;
+          vm[c][0] = vsc[gq];
+          vm[c][1] = vsc[gq + 8];
+          svmax = fmaxf(svmax, fmaxf(gq < nvalid ? vm[c][0] : 0.f, gq + 8 < nvalid ? vm[c][1] : 0.f));
           const uint8_t* kb = kt + L::oK8;
 #pragma unroll
           for (int ks = 0; ks < D / 16; ++ks) {
@@ -882,6 +937,12 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         x[c][1] = gq < nvalid ? sacc[1] * kmul0 : -CUDART_INF_F;      // key g,   head 2t+1
         x[c][2] = gq + 8 < nvalid ? sacc[2] * kmul1 : -CUDART_INF_F;  // key g+8, head 2t
         x[c][3] = gq + 8 < nvalid ? sacc[3] * kmul1 : -CUDART_INF_F;  // key g+8, head 2t+1
+      }
+      if (HPA_FP8_VPAIR && a.fp8 && (c8[0] || c8[1])) fp8_vpre_adjust<D>(svmax, vpre, o);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        vm[c][0] *= vpre;
+        vm[c][1] *= vpre;
       }
       float mx0 = fmaxf(fmaxf(x[0][0], x[0][2]), fmaxf(x[1][0], x[1][2]));
       float mx1 = fmaxf(fmaxf(x[0][1], x[0][3]), fmaxf(x[1][1], x[1][3]));
@@ -992,10 +1053,13 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       if (c8) {
         const float* ksc = reinterpret_cast<const float*>(kt + L::oK8 + 16 * D);
         const float* vsc = reinterpret_cast<const float*>(kt + L::oV8 + 16 * D);
-        kmul0 = ksc[gq] * sl2;  // scales first: the conversion overwrites them
-        kmul1 = ksc[gq + 8] * sl2;
-        vmul0 = vsc[gq] * vpre;
-        vmul1 = vsc[gq + 8] * vpre;
+        kmul0 = ksc[gq] * slk;  // scales first: the conversion overwrites them
+        kmul1 = ksc[gq + 8] * slk;
+        const float sv0 = vsc[gq], sv1 = vsc[gq + 8];
+        if (HPA_FP8_VPAIR)
+          fp8_vpre_adjust<D>(fmaxf(gq < nvalid ? sv0 : 0.f, gq + 8 < nvalid ? sv1 : 0.f), vpre, o);
+        vmul0 = sv0 * vpre;
+        vmul1 = sv1 * vpre;
       }
       float sacc[4] = {0.f, 0.f, 0.f, 0.f};
       const bool kreg = HPA_FP8_KSWZ && !HPA_FP8_F16 && c8;

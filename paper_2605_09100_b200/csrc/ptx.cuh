@@ -165,6 +165,10 @@ __device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
 __device__ __forceinline__ uint32_t bf16x2_to_f16x2(uint32_t v) {
   return pack_f16(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
 }
+// bf16x2 -> f16x2 of (x * mul), mul a power of two chosen to keep x * mul in f16's range
+__device__ __forceinline__ uint32_t bf16x2_to_f16x2_scaled(uint32_t v, float mul) {
+  return pack_f16(__uint_as_float(v << 16) * mul, __uint_as_float(v & 0xffff0000u) * mul);
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo (low 16 bits)
   return *reinterpret_cast<uint32_t*>(&v);

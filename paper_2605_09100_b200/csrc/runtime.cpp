@@ -244,9 +244,12 @@ class StagingRing {
     host_ = dev_ = nullptr;
   }
   size_t cap() const { return cap_; }
-  // Returns the offset of a free region of n bytes (n <= cap).
+  static constexpr size_t kNoRoom = ~size_t(0);
+  // Returns the offset of a free region of n bytes, or kNoRoom when n exceeds the capacity
+  // (callers go through ring_reserve(), which turns that into HPA_ERR_INVALID_ARG).
   size_t reserve(size_t n) {
     n = (n + 255) & ~size_t(255);
+    if (n > cap_) return kNoRoom;
     if (head_ + n > cap_) head_ = 0;
     const size_t lo = head_, hi = head_ + n;
     while (!inflight_.empty() && cudaEventQuery(inflight_.front().ev) == cudaSuccess) pop_front();
@@ -466,6 +469,14 @@ hpa_status_t check_seq(hpa_cache_t* c, int32_t s) {
 
 int32_t seq_entries(const Seq& q) { return int32_t(q.pages.size()); }
 
+// A staging-ring region of n bytes, or INVALID_ARG when one call's upload exceeds the ring.
+hpa_status_t ring_reserve(hpa_cache_t* c, size_t n, size_t* off) {
+  *off = c->ring.reserve(n);
+  if (*off == StagingRing::kNoRoom)
+    return fail(HPA_ERR_INVALID_ARG, "staging upload of %zu bytes exceeds the ring capacity %zu", n, c->ring.cap());
+  return HPA_OK;
+}
+
 // Ships pending word writes (+ optional scatter records/slots) in one upload and
 // one scatter launch on `s`.
 hpa_status_t ship(hpa_cache_t* c, cudaStream_t s, const std::vector<ScatterRecord>& recs,
@@ -516,10 +527,8 @@ hpa_status_t ship(hpa_cache_t* c, cudaStream_t s, const std::vector<ScatterRecor
   const size_t o_words = b.add(c->pending.data(), c->pending.size());
   const size_t o_recs = b.add(recs.data(), recs.size());
   const size_t o_slots = b.add(slots.data(), slots.size());
-  if (b.bytes.size() > c->ring.cap())
-    return fail(HPA_ERR_INVALID_ARG, "metadata upload of %zu bytes exceeds staging capacity %zu",
-                b.bytes.size(), c->ring.cap());
-  const size_t off = c->ring.reserve(b.bytes.size());
+  size_t off;
+  if (hpa_status_t st = ring_reserve(c, b.bytes.size(), &off)) return st;
   std::memcpy(c->ring.host(off), b.bytes.data(), b.bytes.size());
   HPA_CUDA(c->ring.upload_side(off, b.bytes.size(), s, c->copy_stream, c->upload_done));
   char* d = c->ring.dev(off);
@@ -541,7 +550,8 @@ hpa_status_t upload_batch(hpa_cache_t* c, int32_t n, const int32_t* seq_ids, cud
     c->batch_cap = std::max(n, 1024);
     HPA_CUDA(cudaMalloc(&c->batch_dev, size_t(c->batch_cap) * 4));
   }
-  const size_t off = c->ring.reserve(size_t(n) * 4);
+  size_t off;
+  if (hpa_status_t st = ring_reserve(c, size_t(n) * 4, &off)) return st;
   std::memcpy(c->ring.host(off), seq_ids, size_t(n) * 4);
   HPA_CUDA(cudaMemcpyAsync(c->batch_dev, c->ring.host(off), size_t(n) * 4, cudaMemcpyHostToDevice, s));
   HPA_CUDA(c->ring.commit(off, size_t(n) * 4, s));
@@ -1504,7 +1514,8 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
         HPA_CUDA(cudaMalloc(&c->nsplit_dev, c->nsplit_cap * 4));
       }
       const size_t ub = size_t(U) * sizeof(int4), nb = size_t(n_seqs) * 4;
-      const size_t off = c->ring.reserve(ub + nb);
+      size_t off;
+      if (hpa_status_t st = ring_reserve(c, ub + nb, &off)) return st;
       int4* hu = reinterpret_cast<int4*>(c->ring.host(off));
       size_t k = 0;
       for (const auto& o : order) {
@@ -1617,6 +1628,27 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
   // the pages returned (stream order: the host mirror never changes). Same-stream semantics.
   std::vector<int32_t> tmp_pages;
   std::vector<WordWrite> restore;
+  // Failure atomicity (include/hpa.h): once table entries may point at temporary pages, every
+  // exit -- an error return included -- queues the restoring writes, ships them and returns
+  // the temporaries to the allocator. The success path does the same at the end and disarms.
+  struct TmpRedirect {
+    hpa_cache_t* c;
+    cudaStream_t s;
+    std::vector<int32_t>& pages;
+    std::vector<WordWrite>& restore;
+    bool armed = false;
+    hpa_status_t undo() {
+      armed = false;
+      c->pending.insert(c->pending.end(), restore.begin(), restore.end());
+      const hpa_status_t st = ship(c, s, {}, {}, 0);
+      for (int32_t p : pages) c->alloc.release(p);
+      pages.clear();
+      return st;
+    }
+    ~TmpRedirect() {
+      if (armed) undo();
+    }
+  } redirect{c, s, tmp_pages, restore};
   if (c->fp8) {
     const int32_t P = c->cfg.page_size;
     std::vector<char> seen(c->cfg.max_seqs, 0);
@@ -1632,6 +1664,7 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
                   c->alloc.num_free());
     if (need > 0) {
       c->alloc.alloc(need, tmp_pages);
+      redirect.armed = true;
       std::vector<int4> items;  // {fp8 token page, temporary bf16 page, valid rows, 0}
       int32_t k = 0;
       std::fill(seen.begin(), seen.end(), 0);
@@ -1660,7 +1693,8 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
       gl.v8 = c->v8_pool + f8_rows * (c->cfg.head_dim + 4);
       gl.L = 1;
       const size_t ib = items.size() * sizeof(int4);
-      const size_t ioff = c->ring.reserve(ib);
+      size_t ioff;
+      if (hpa_status_t st = ring_reserve(c, ib, &ioff)) return st;
       std::memcpy(c->ring.host(ioff), items.data(), ib);
       HPA_CUDA(c->ring.upload_side(ioff, ib, s, c->copy_stream, c->upload_done));
       int launched = 1;
@@ -1689,7 +1723,8 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
   const size_t wbytes = listed ? (plan.work.size() + plan.parts.size()) * sizeof(int4) : 0;
   const size_t cbytes = listed ? plan.cta_off.size() * 4 : 0;
   const size_t bytes = wbytes + cbytes + meta.size() * 4;
-  const size_t off = c->ring.reserve(bytes);
+  size_t off;
+  if (hpa_status_t st = ring_reserve(c, bytes, &off)) return st;
   if (listed) {
     std::memcpy(c->ring.host(off), plan.work.data(), plan.work.size() * sizeof(int4));
     std::memcpy(c->ring.host(off) + plan.work.size() * sizeof(int4), plan.parts.data(),
@@ -1741,11 +1776,7 @@ hpa_status_t prefill_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const i
   c->launches += launched;
   if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
   HPA_CUDA(c->ring.commit(off, bytes, s));
-  if (!tmp_pages.empty()) {  // NEXT-4c: table entries back to the fp8 pages, temporaries freed
-    c->pending.insert(c->pending.end(), restore.begin(), restore.end());
-    if (hpa_status_t st = ship(c, s, {}, {}, 0)) return st;
-    for (int32_t p : tmp_pages) c->alloc.release(p);
-  }
+  if (redirect.armed) return redirect.undo();  // NEXT-4c: entries back to the fp8 pages, temporaries freed
   return HPA_OK;
 }
 }  // namespace
@@ -1794,7 +1825,8 @@ hpa_status_t hpa_export_table(hpa_cache_t* c, int32_t seq_id, int32_t* pages, in
   return HPA_OK;
 }
 
-hpa_status_t hpa_prefill_plan_info(hpa_cache_t* c, int32_t* n_ctas, int32_t* n_split_units, int32_t* splits) {
+hpa_status_t hpa_prefill_plan_info(hpa_cache_t* c, int32_t* n_ctas, int32_t* n_split_units, int32_t* splits,
+                                   int32_t* cluster_size) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
   const bool l = c->pf_listed;
   if (n_ctas)
@@ -1803,6 +1835,7 @@ hpa_status_t hpa_prefill_plan_info(hpa_cache_t* c, int32_t* n_ctas, int32_t* n_s
                                            : int32_t(c->pf_plan.cta_off.size()) - 1;
   if (n_split_units) *n_split_units = l ? int32_t(c->pf_plan.parts.size() / 2) : 0;
   if (splits) *splits = l ? c->pf_plan.split_max : 1;
+  if (cluster_size) *cluster_size = l && c->pf_plan.mc2 ? 2 : 1;
   return HPA_OK;
 }
 
@@ -1827,8 +1860,7 @@ hpa_status_t hpa_set_decode_splits(hpa_cache_t* c, int32_t splits) {
   return HPA_OK;
 }
 
-// Internal / experiments only (not in include/hpa.h): device buffer for the
-// HPA_TRACE prefill phase stamps.
+// Diagnostics (include/hpa.h): device buffer for the HPA_TRACE phase stamps.
 hpa_status_t hpa_debug_trace(hpa_cache_t* c, void* device_buf) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
   c->trace = static_cast<long long*>(device_buf);

@@ -38,14 +38,24 @@ def head_shard(num_q_heads: int, num_kv_heads: int, rank: int, world: int) -> Tu
     return kv_lo, kv_hi, kv_lo * g, kv_hi * g
 
 
+def assemble_head_shards(gathered: torch.Tensor) -> torch.Tensor:
+    """[n][B][Hq/n][d] (rank-major, as all_gather_into_tensor leaves it) -> [B][Hq][d]: rank r's
+    q-heads are [r Hq/n, (r+1) Hq/n) (head_shard), so the full output is the rank-ordered
+    concatenation along the head axis."""
+    n, b, hl, d = gathered.shape
+    return gathered.permute(1, 0, 2, 3).reshape(b, n * hl, d)
+
+
 def gather_head_shards(out_local: torch.Tensor, group=None) -> torch.Tensor:
     """out_local [B][Hq/n][d] on every rank -> full [B][Hq][d] (rank-major head order)
-    with one all_gather_into_tensor (NCCL over NVLink on GPUs, gloo on CPU)."""
+    with one all_gather_into_tensor (NCCL over NVLink on GPUs, gloo on CPU). The payload is
+    B Hq d 2 bytes (64 KB at configs[1]), latency-bound: NCCL's all-gather is the right tool
+    (a fused peer-memory kernel would save microseconds on a step that sharding already slows)."""
     world = dist.get_world_size(group)
     b, hl, d = out_local.shape
     buf = torch.empty((world * b, hl, d), dtype=out_local.dtype, device=out_local.device)
     dist.all_gather_into_tensor(buf, out_local.contiguous(), group=group)
-    return buf.view(world, b, hl, d).permute(1, 0, 2, 3).reshape(b, world * hl, d)
+    return assemble_head_shards(buf.view(world, b, hl, d))
 
 
 def max_over_ranks(x: float, device=None) -> float:

@@ -115,7 +115,7 @@ def test_fp8_prefill_parity_and_cache_unchanged(hq, hkv, d, P):
         torch.cuda.synchronize()
         off = 0
         for s, n in zip(seqs, q_lens):
-            k, v = pr.orc.logical_kv(s, layer)
+            k, v = pr.orc.logical_kv(s, layer, fp8_staged=True)
             lb = k.shape[1]
             ref = np.stack([attend(f64(q[off + t:off + t + 1]), k[:, :lb - n + t + 1], v[:, :lb - n + t + 1],
                                    shape.scale)[0] for t in range(n)])
@@ -141,6 +141,9 @@ def test_fp8_export_and_compress_dequantize_like_the_oracle():
         assert np.array_equal(f64(k)[:, :64], ek[:, :64])
         np.testing.assert_allclose(f64(k)[:, 64:], ek[:, 64:], rtol=2 ** -8, atol=0)
         np.testing.assert_allclose(f64(v)[:, 64:], ev[:, 64:], rtol=2 ** -8, atol=0)
+        # ... and bit-exactly the staged rows of reading A20 (bf16(fp32(code) * scale))
+        sk, sv = pr.orc.logical_kv(s, layer, fp8_staged=True)
+        assert np.array_equal(f64(k), sk) and np.array_equal(f64(v), sv)
     free0 = pr.cache.token_pool()[4]
     got = pr.cache.compress(s, 4096 // 16, 128)          # document rows -> 128 bf16 latent rows
     exp = pr.orc.compress(s, 4096 // 16, 128)
@@ -192,7 +195,7 @@ def test_fp8_page256_and_partial_pages():
     check_close(out, ref, "fp8 P=256")
     qp = pr.queries(64)
     outp = pr.cache.prefill(0, [s1], [64], qp.cuda())
-    k, v = pr.orc.logical_kv(s1, 0)
+    k, v = pr.orc.logical_kv(s1, 0, fp8_staged=True)
     lb = k.shape[1]
     refp = np.stack([attend(f64(qp[t:t + 1]), k[:, :lb - 64 + t + 1], v[:, :lb - 64 + t + 1], shape.scale)[0]
                      for t in range(64)])

@@ -174,3 +174,33 @@ def test_decode_config4_sweep_shard_64k_sampled(ratio):
     seqs, _ = _build(cache, orc, shape, B, sampled, sets, tok, 31)
     _decode_sampled(cache, orc, shape, seqs, sampled, f"configs[4] shard ctx=64K r={ratio}")
     cache.close()
+
+
+def test_prefill_config2_b4_full_size_sampled_clusters():
+    """configs[2] at B_p = 4 in the launch configuration bench.py times:
+    1024 CTAs as 2-CTA TMA-multicast clusters with no split. Two of the four requests are
+    CPU-drawn and mirrored in the oracle; 24 sampled query rows each, all 32 heads."""
+    from paper_2605_09100_b200 import Cache
+    shape = qwen3_8b_shape(16)
+    C, prior, B, sampled = 2048, 16384, 4, [1, 3]
+    pages = 64 + (prior + C) // 16
+    cache = Cache(1, 32, 8, 128, 16, B * pages, B, pages, 0, 99)
+    orc = OracleCache(1, 32, 8, 128, 16)
+    seqs, draws = _build(cache, orc, shape, B, sampled, 8, prior + C, 78)
+    q = torch.randn((B * C, 32, 128), device="cuda").to(torch.bfloat16)
+    qs = {s: Draw(20 + s).queries(shape, C) for s in sampled}
+    for s in sampled:
+        q[s * C:(s + 1) * C] = qs[s].cuda()
+    out = cache.prefill(0, seqs, [C] * B, q)
+    torch.cuda.synchronize()
+    info = cache.prefill_plan_info()
+    assert info["cluster"] == 2 and info["split_units"] == 0 and info["ctas"] == B * 32 * C // 256, info
+    assert torch.isfinite(out.float()).all()
+    for s in sampled:
+        k, v = orc.logical_kv(seqs[s], 0)
+        lb = k.shape[1]
+        rows = sorted(set([0, 127, 128, 1023, 1024, 2047] + list(np.random.default_rng(s).integers(0, C, 18))))
+        ref = np.stack([attend(f64(qs[s][t:t + 1]), k[:, :lb - C + t + 1], v[:, :lb - C + t + 1], shape.scale)[0]
+                        for t in rows])
+        check_close(out[s * C:(s + 1) * C][rows], ref, f"configs[2] B=4 prefill request {s} sampled rows")
+    cache.close()

@@ -121,7 +121,7 @@ def test_fp8_token_pages_fuzz(case):
     torch.cuda.synchronize()
     ref, off = [], 0
     for s, n in zip(seqs, q_lens):
-        k, v = p.orc.logical_kv(s, layer)
+        k, v = p.orc.logical_kv(s, layer, fp8_staged=True)
         ref.append(attend(f64(qp[off:off + n]), k, v, shape.scale))
         off += n
     check_close(got, np.concatenate(ref), f"fp8 prefill fuzz case {case}")

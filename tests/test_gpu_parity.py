@@ -176,6 +176,33 @@ def test_split_invariance():
         assert torch.max(torch.abs(a - b)) <= 2 ** -7 * (1 + torch.max(torch.abs(a)))
 
 
+def test_split_invariance_fp32_partials():
+    """SURVEY §8(c) "Split invariance", on the fp32 result of the split combine
+    (hpa_decode_partial writes fp32 O and the LSE: no bf16 output rounding hides an error).
+    (a) q = 0: every score is 0, so every P weight is exactly 1 in every split and the only
+        difference between split counts is fp32 summation order and the combine's weights
+        2^(lse_s - LSE) over ragged split lengths -> <= 1e-5 relative.
+    (b) random q: each split (and each consumer warp) rounds its P weights to bf16 relative to
+        its own running max (reading A9), a relative perturbation <= 2^-9 per weight, so S = 1
+        and S = k may differ by that much: rel-L2 <= 2^-9."""
+    shape = Shape(1, 32, 8, 128, 16)
+    p = Pair(shape, num_pages=2048, max_seqs=4, max_pages_per_seq=512)
+    seqs = [p.build([("latent", 128), ("tokens", n)]) for n in (1000, 3333, 77)]
+    for q, tol in ((torch.zeros((len(seqs), 32, 128), dtype=torch.bfloat16), 1e-5),
+                   (p.queries(len(seqs)), 2.0 ** -9)):
+        q = q.cuda()
+        p.cache.set_decode_splits(1)
+        o1, l1 = p.cache.decode_partial(0, seqs, q)
+        for splits in (0, 2, 3, 5, 16):
+            p.cache.set_decode_splits(splits)
+            o, l = p.cache.decode_partial(0, seqs, q)
+            torch.cuda.synchronize()
+            rel = (torch.linalg.vector_norm(o - o1) / torch.linalg.vector_norm(o1)).item()
+            assert rel <= tol, (splits, rel, tol)
+            assert torch.allclose(l, l1, rtol=0, atol=1e-5 * (1 + l1.abs().max().item())), splits
+    p.cache.set_decode_splits(0)
+
+
 def test_rows_beyond_valid_are_masked():
     """Junk written into pool rows >= valid_rows (partial pages) changes nothing."""
     shape = Shape(1, 8, 2, 128, 16)
