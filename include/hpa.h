@@ -166,6 +166,19 @@ hpa_status_t hpa_latent_set_install_batch(hpa_cache_t* c, int32_t n, const int32
  * dst's new set id. Errors: HPA_ERR_UNKNOWN_SEQ / _UNKNOWN_SET / _SEQ_CAPACITY. */
 hpa_status_t hpa_latent_set_share(hpa_cache_t* c, int32_t dst_seq, int32_t src_seq, int32_t src_set_id,
                                   int32_t* set_id_out);
+/* Prefix sharing ("regular KV cache including prefix KV cache
+ * for user prompts"; reading A21): creates a new sequence (*dst_seq_out) whose
+ * logical rows are the first n_prefix_rows rows of src_seq -- the same segments in order,
+ * latent sets with their set ids (dst's set counter continues from src's), the segment
+ * holding row n_prefix_rows - 1 cut after it. The new sequence references src's physical
+ * pages (refcounts +1; O(pages) host work, no kernel, no copy). Appending to a sequence whose
+ * partial last page is shared copies that page first (copy-on-write, one page-copy launch
+ * before the append's scatter) unless the appender owns the page's claimed rows; replacing a
+ * shared latent set writes fresh pages (as hpa_latent_set_share). Either side can be released
+ * first. n_prefix_rows = 0 gives an empty sequence. Errors (cache unchanged): INVALID_ARG
+ * (n_prefix_rows outside [0, seq_len], or a cut inside a latent set), UNKNOWN_SEQ,
+ * SEQ_CAPACITY (no free sequence slot). */
+hpa_status_t hpa_seq_fork(hpa_cache_t* c, int32_t src_seq, int32_t n_prefix_rows, int32_t* dst_seq_out);
 /* Memory-server staging ("KV cache server for storing
  * and retrieving compressed document memories"): as hpa_latent_set_install_batch,
  * but payload i is in HOST memory (host_ptrs[i], [L][2][m_rows[i]][H_kv][d] bf16;

@@ -197,6 +197,13 @@ class Cache:
                                               _stream(self.device, stream), _p32(out)))
         return out
 
+    def seq_fork(self, src_seq: int, n_prefix_rows: int) -> int:
+        """hpa_seq_fork: a new sequence sharing the first n_prefix_rows rows of src_seq
+        (prefix pages referenced, copy-on-write on append). Returns the new sequence id."""
+        out = c_i32()
+        check(LIB.hpa_seq_fork(self._h, src_seq, n_prefix_rows, ctypes.byref(out)))
+        return out.value
+
     def latent_share(self, dst_seq: int, src_seq: int, src_set_id: int) -> int:
         """hpa_latent_set_share: dst gets a new LATENT set referencing src's pages."""
         out = c_i32()

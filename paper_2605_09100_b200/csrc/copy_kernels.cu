@@ -205,6 +205,41 @@ __global__ void __launch_bounds__(256) dequant_pages_kernel(PoolGeom g, const in
   }
 }
 
+// NEXT-2 copy-on-write of a token page shared by forked sequences (reading A21): item i =
+// {source page, destination page}; CTA (i, l) copies the page's whole layer-l region -- every
+// head, all P rows, K and V -- byte for byte: bf16 tiles [H][P][d], or the fp8 pool's 16-row
+// blocks [16 x d codes | 16 scales] (the K chunk swizzle and the V pair rows are functions of
+// the row index inside its block, so a raw block copy preserves them). Rows past the sharer's
+// valid rows are copied too; they stay masked by valid_rows.
+__global__ void __launch_bounds__(256) copy_pages_kernel(PoolGeom g, const __grid_constant__ CopyPagesMeta m) {
+  grid_dependency_wait();
+  grid_launch_dependents();
+  const int2 it = m.items[blockIdx.x];
+  const int64_t l = blockIdx.y;
+  int64_t bytes;
+  const int4 *ks, *vs;
+  int4 *kd, *vd;
+  if (m.fp8) {
+    bytes = int64_t(g.Hkv) * g.P / 16 * fp8_block_bytes(g.D);
+    const int64_t per_page = bytes;
+    ks = reinterpret_cast<const int4*>(g.k8 + (l * g.NPt + it.x) * per_page);
+    vs = reinterpret_cast<const int4*>(g.v8 + (l * g.NPt + it.x) * per_page);
+    kd = reinterpret_cast<int4*>(g.k8 + (l * g.NPt + it.y) * per_page);
+    vd = reinterpret_cast<int4*>(g.v8 + (l * g.NPt + it.y) * per_page);
+  } else {
+    bytes = int64_t(g.Hkv) * g.P * g.D * 2;
+    const int64_t per_page = bytes / 2;  // elements
+    ks = reinterpret_cast<const int4*>(static_cast<const __nv_bfloat16*>(g.k_pool) + (l * g.NP + it.x) * per_page);
+    vs = reinterpret_cast<const int4*>(static_cast<const __nv_bfloat16*>(g.v_pool) + (l * g.NP + it.x) * per_page);
+    kd = reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(g.k_pool) + (l * g.NP + it.y) * per_page);
+    vd = reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(g.v_pool) + (l * g.NP + it.y) * per_page);
+  }
+  for (int64_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) {
+    kd[i] = ks[i];
+    vd[i] = vs[i];
+  }
+}
+
 // Grid: x = table entry, y = kv head. Copies rows 0..valid-1 of the page tile
 // to out[h][pos0 + r][:].
 __global__ void __launch_bounds__(128) export_kernel(PoolGeom g, DevTables t, int32_t layer,
@@ -284,6 +319,11 @@ cudaError_t launch_dequant_pages(const PoolGeom& g, const int4* items, int32_t n
   const dim3 grid(unsigned(n), unsigned(g.Hkv));
   if (g.D == 128) return launch_pdl(dequant_pages_kernel<128>, grid, dim3(256), 0, s, g, items);
   return launch_pdl(dequant_pages_kernel<64>, grid, dim3(256), 0, s, g, items);
+}
+
+cudaError_t launch_copy_pages(const PoolGeom& g, const CopyPagesMeta& m, cudaStream_t s) {
+  if (m.n == 0) return cudaSuccess;
+  return launch_pdl(copy_pages_kernel, dim3(unsigned(m.n), unsigned(g.L)), dim3(256), 0, s, g, m);
 }
 
 cudaError_t launch_export(const PoolGeom& g, DevTables t, int32_t layer, int32_t seq,

@@ -94,6 +94,17 @@ cudaError_t launch_scatter_inline(const PoolGeom& g, int32_t* arena, const Inlin
 // items[n] = {fp8 token page, bf16 page, valid rows, 0} (device), g sliced to one layer.
 cudaError_t launch_dequant_pages(const PoolGeom& g, const int4* items, int32_t n, cudaStream_t s);
 
+// NEXT-2 copy-on-write: whole-page copies {source page, destination page} in every layer,
+// of the bf16 main pools (fp8 = 0) or the fp8 token pools (fp8 = 1). Items travel as kernel
+// parameters, kCopyPagesMax per launch.
+constexpr int kCopyPagesMax = 128;
+struct CopyPagesMeta {
+  int32_t n;
+  int32_t fp8;
+  int2 items[kCopyPagesMax];
+};
+cudaError_t launch_copy_pages(const PoolGeom& g, const CopyPagesMeta& m, cudaStream_t s);
+
 // Logical K/V export of one (layer, seq): out bf16 [H_kv][len][d].
 cudaError_t launch_export(const PoolGeom& g, DevTables t, int32_t layer, int32_t seq,
                           int32_t n_entries_host, void* k_out, void* v_out, cudaStream_t s);

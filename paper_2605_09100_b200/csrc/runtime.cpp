@@ -174,6 +174,7 @@ class PageAllocator {
  public:
   void init(int32_t num_pages, uint64_t seed) {
     refcnt_.assign(num_pages, 0);
+    high_.assign(num_pages, 0);
     free_.resize(num_pages);
     for (int32_t i = 0; i < num_pages; ++i) free_[i] = num_pages - 1 - i;  // pop_back -> page 0 first
     if (seed != 0) {
@@ -192,6 +193,7 @@ class PageAllocator {
       int32_t p = free_.back();
       free_.pop_back();
       refcnt_[p] = 1;
+      high_[p] = 0;
       out.push_back(p);
     }
   }
@@ -200,10 +202,16 @@ class PageAllocator {
   }
   void retain(int32_t p) { ++refcnt_[p]; }
   int32_t refcount(int32_t p) const { return refcnt_[p]; }
+  // Token pages shared by forked sequences (NEXT-2, reading A21): rows claimed so far. A sharer
+  // may append in place only when its valid rows equal the watermark (rows beyond it are then
+  // nobody's); any other sharer copies the page first.
+  int32_t high(int32_t p) const { return high_[p]; }
+  void set_high(int32_t p, int32_t rows) { high_[p] = rows; }
 
  private:
   std::vector<int32_t> free_;
   std::vector<int32_t> refcnt_;
+  std::vector<int32_t> high_;
 };
 
 struct Segment {
@@ -884,6 +892,27 @@ int32_t pages_for_append(const hpa_cache_t* c, const Seq& q, int32_t n) {
   return (n + P - 1) / P;
 }
 
+// Whether appending n rows to q must first copy its trailing token segment's last page: the
+// page is partial, shared (refcount > 1), and some sharer has claimed rows beyond q's valid rows
+// (watermark != valid; `claimed` holds watermarks raised earlier in the same call, and this
+// call's claim is recorded in it when q appends in place). NEXT-2, reading A21.
+bool append_needs_copy(const hpa_cache_t* c, const Seq& q, int32_t n,
+                       std::vector<std::pair<int32_t, int32_t>>& claimed) {
+  if (n <= 0 || q.segs.empty() || q.segs.back().latent) return false;
+  const int32_t P = c->cfg.page_size;
+  const Segment& g = q.segs.back();
+  const int32_t vl = g.rows % P;
+  if (vl == 0) return false;  // the last page is full: the rows go to fresh pages
+  const PageAllocator& tok = const_cast<hpa_cache_t*>(c)->pages_of(false);
+  const int32_t pl = g.pages.back();
+  int32_t high = tok.high(pl);
+  for (const auto& cl : claimed)
+    if (cl.first == pl) high = cl.second;
+  if (tok.refcount(pl) > 1 && high != vl) return true;
+  claimed.emplace_back(pl, std::min(P, vl + n));
+  return false;
+}
+
 bool valid_dims(const hpa_config_t* g) {
   auto p2 = [](int x) { return x == 16 || x == 32 || x == 64 || x == 128 || x == 256; };
   return (g->head_dim == 64 || g->head_dim == 128) && p2(g->page_size);
@@ -1141,18 +1170,42 @@ hpa_status_t hpa_append_kv(hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_id
   if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15)
     return fail(HPA_ERR_INVALID_ARG, "k / v must be 16-byte aligned");
   PageAllocator& tok = c->pages_of(false);
+  // copy-on-write of shared partial last pages (forked prefixes, reading A21), decided in call
+  // order with the watermarks this call claims: one more page per copied sequence
+  {
+    std::vector<std::pair<int32_t, int32_t>> claimed;  // (page, watermark) claimed by this call
+    for (int32_t i = 0; i < n_seqs; ++i) need += append_needs_copy(c, c->seqs[seq_ids[i]], n_new[i], claimed);
+  }
   if (need > tok.num_free())
     return fail(HPA_ERR_OUT_OF_PAGES, "append needs %d pages, %d free", need, tok.num_free());
   // ---- apply
   DeviceGuard dg(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int32_t P = c->cfg.page_size;
   std::vector<int32_t> slots;
   slots.reserve(size_t(total_rows));
+  CopyPagesMeta cow{};
+  cow.fp8 = c->fp8 ? 1 : 0;
   for (int32_t i = 0; i < n_seqs; ++i) {
     Seq& q = c->seqs[seq_ids[i]];
     int32_t n = n_new[i];
     if (n == 0) continue;
     const int32_t first_entry = std::max(0, seq_entries(q) - 1);
+    std::vector<std::pair<int32_t, int32_t>> none;
+    if (append_needs_copy(c, q, n, none)) {  // watermarks of earlier sequences are already applied
+      Segment& g = q.segs.back();
+      std::vector<int32_t> fresh;
+      tok.alloc(1, fresh);
+      const int32_t old = g.pages.back();
+      if (cow.n == kCopyPagesMax) {
+        HPA_CUDA(launch_copy_pages(c->geom(), cow, s));
+        c->launches += 1;
+        cow.n = 0;
+      }
+      cow.items[cow.n++] = make_int2(old, fresh[0]);
+      tok.release(old);
+      g.pages.back() = fresh[0];
+    }
     if (q.segs.empty() || q.segs.back().latent) q.segs.push_back(Segment{false, -1, 0, {}});
     Segment& g = q.segs.back();
     const int32_t np = pages_for_append(c, q, n);
@@ -1161,13 +1214,56 @@ hpa_status_t hpa_append_kv(hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_id
       const int32_t row = g.rows + r;
       slots.push_back(g.pages[row / P] * P + row % P);
     }
+    for (int32_t pg = g.rows / P; pg < int32_t(g.pages.size()); ++pg)  // watermarks of the written pages
+      tok.set_high(g.pages[pg], std::min(P, g.rows + n - pg * P));
     g.rows += n;
     c->rebuild(seq_ids[i], first_entry);
+  }
+  if (cow.n) {  // stream order: the copies land before the scatter writes the new rows
+    HPA_CUDA(launch_copy_pages(c->geom(), cow, s));
+    c->launches += 1;
   }
   const int64_t Hd = int64_t(c->cfg.num_kv_heads) * c->cfg.head_dim;
   std::vector<ScatterRecord> recs{
       ScatterRecord{k, v, total_rows * Hd, Hd, int32_t(total_rows), 0, 0, 0, 0, 0, c->fp8 ? 1 : 0, 0}};
-  return ship(c, static_cast<cudaStream_t>(stream), recs, slots, total_rows);
+  return ship(c, s, recs, slots, total_rows);
+}
+
+hpa_status_t hpa_seq_fork(hpa_cache_t* c, int32_t src_seq, int32_t n_prefix_rows, int32_t* dst_seq_out) {
+  if (!c || !dst_seq_out) return fail(HPA_ERR_INVALID_ARG, "null argument");
+  if (hpa_status_t st = check_seq(c, src_seq)) return st;
+  const Seq& src = c->seqs[src_seq];
+  if (n_prefix_rows < 0 || n_prefix_rows > src.len)
+    return fail(HPA_ERR_INVALID_ARG, "n_prefix_rows %d outside [0, %d]", n_prefix_rows, src.len);
+  const int32_t P = c->cfg.page_size;
+  std::vector<Segment> segs;
+  int32_t left = n_prefix_rows;
+  for (const Segment& g : src.segs) {
+    if (left == 0) break;
+    if (g.rows > left && g.latent)
+      return fail(HPA_ERR_INVALID_ARG, "fork cut at row %d falls inside latent set %d", n_prefix_rows, g.set_id);
+    const int32_t take = std::min(g.rows, left);
+    segs.push_back(Segment{g.latent, g.set_id, take,
+                           std::vector<int32_t>(g.pages.begin(), g.pages.begin() + (take + P - 1) / P)});
+    left -= take;
+  }
+  int32_t d = -1;
+  for (int32_t s = 0; s < c->cfg.max_seqs && d < 0; ++s)
+    if (!c->seqs[s].live) d = s;
+  if (d < 0) return fail(HPA_ERR_SEQ_CAPACITY, "all %d sequence slots are in use", c->cfg.max_seqs);
+  for (const Segment& g : segs)
+    for (int32_t p : g.pages) c->pages_of(g.latent).retain(p);
+  Seq& q = c->seqs[d];
+  q = Seq();
+  q.live = true;
+  q.next_set = c->seqs[src_seq].next_set;
+  q.segs = std::move(segs);
+  c->pending.push_back({int32_t(c->off_len() + d), 0});
+  c->pending.push_back({int32_t(c->off_nent() + d), 0});
+  c->rebuild(d, 0);
+  ++c->live;
+  *dst_seq_out = d;
+  return HPA_OK;
 }
 
 namespace {
@@ -1419,6 +1515,8 @@ hpa_status_t hpa_seq_compress(hpa_cache_t* c, int32_t seq_id, int32_t n_doc_rows
   for (size_t k = size_t(keep_pages); k < T.pages.size(); ++k) c->pages_of(false).release(T.pages[k]);
   T.pages.resize(size_t(keep_pages));
   T.rows = keep;
+  if (keep % P && c->pages_of(false).refcount(T.pages.back()) == 1)  // sole owner: rows past keep are free again
+    c->pages_of(false).set_high(T.pages.back(), keep % P);
   if (keep == 0) q.segs.pop_back();
   q.segs.push_back(std::move(L));
   c->rebuild(seq_id, n_before + std::max(0, keep_pages - 1));
