@@ -377,6 +377,11 @@ def decode_bytes(lens, shape):
     return sum(L * hkv * d * 2 * 2 + 2 * hq * d * 2 + 4 * math.ceil(L / P) for L in lens)
 
 
+def append_bytes(n, shape):
+    """Algorithmic bytes of appending one K and V row per request (every layer): read + write."""
+    return 2 * 2 * n * shape.num_layers * shape.num_kv_heads * shape.head_dim * 2
+
+
 def prefill_flops(prior, c, shape):
     """4 Hq d (C L_prior + C(C+1)/2) per request."""
     return 4 * shape.num_q_heads * shape.head_dim * (c * prior + c * (c + 1) // 2)
@@ -402,26 +407,28 @@ def run_ours(args):
             dist.barrier(device_ids=[dev])
 
     # ------------------------------------------------------------------ configs[1] decode step
-    cache, seqs, _ = build_decode_cache(torch, Cache, shape, B, docs, tokens, 2 * K + W + 16, dev,
+    # One step = hpa_append_decode: the current token's K/V row of every request written into
+    # its page slot (a1 + a2) and the split decode + combine (a4 + a5), one kernel launch
+    # (+ the combine). Region A (the `value`) has nothing but the steps between its two
+    # events; region B repeats the steps with an event pair around every call for the
+    # per-launch duration of the roofline (events between launches break the programmatic
+    # dependent launch overlap, so they stay out of region A).
+    cache, seqs, _ = build_decode_cache(torch, Cache, shape, B, docs, tokens, 3 * K + W + 16, dev,
                                         seed=1234 + rank)
     if args.splits:
         cache.set_decode_splits(args.splits)
     g = torch.Generator(device=f"cuda:{dev}").manual_seed(4321 + rank)
-    nsteps = K + W
+    nsteps = 2 * K + W
     knew = torch.randn((nsteps, 1, B, 8, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
     vnew = torch.randn((nsteps, 1, B, 8, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
     qs = torch.randn((nsteps, B, 32, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
     out = torch.empty((B, 32, 128), dtype=torch.bfloat16, device=f"cuda:{dev}")
-    ones = [1] * B
     import numpy as np
     ids = np.asarray(seqs, dtype=np.int32)
-    ones_np = np.ones(B, dtype=np.int32)
     for i in range(W):
-        cache.append_kv(ids, ones_np, knew[i], vnew[i])
-        cache.decode(0, ids, qs[i], out)
+        cache.append_decode(0, ids, knew[i], vnew[i], qs[i], out)
     torch.cuda.synchronize(dev)
     lens0 = [cache.seq_info(s)[0] for s in seqs]
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = cache.launch_count()
     clk = ClockSampler(dev)
@@ -430,24 +437,31 @@ def run_ours(args):
     clk.start()
     t0.record(stream)
     for i in range(K):
-        cache.append_kv(ids, ones_np, knew[W + i], vnew[W + i])
-        evs[i][0].record(stream)
-        cache.decode(0, ids, qs[W + i], out)
-        evs[i][1].record(stream)
+        cache.append_decode(0, ids, knew[W + i], vnew[W + i], qs[W + i], out)
     t1.record(stream)
     torch.cuda.synchronize(dev)
     clk.stop()
     barrier()
     launches = cache.launch_count() - launches0
     step_ms = t0.elapsed_time(t1) / K
-    dec_ms = [a.elapsed_time(b) for a, b in evs]
-    dec_mean = sum(dec_ms) / K
     step_ms_max = max_over_ranks(step_ms, device=f"cuda:{dev}")
-    dec_mean_max = max_over_ranks(dec_mean, device=f"cuda:{dev}")
     total_tokens = B * world
     value = total_tokens / (step_ms_max / 1e3)
-    # bytes per decode call, averaged over the timed steps (lengths grow by one per step)
-    bytes_per_call = sum(decode_bytes([L + 1 + i for L in lens0], shape) for i in range(K)) / K
+    # region B: per-call events (the launch duration for the roofline)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    torch.cuda.synchronize(dev)
+    for i in range(K):
+        evs[i][0].record(stream)
+        cache.append_decode(0, ids, knew[W + K + i], vnew[W + K + i], qs[W + K + i], out)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    dec_ms = [a.elapsed_time(b) for a, b in evs]
+    dec_mean = sum(dec_ms) / K
+    dec_mean_max = max_over_ranks(dec_mean, device=f"cuda:{dev}")
+    # algorithmic bytes per call, averaged over region B's calls (lengths grow by one per step):
+    # the decode's K/V + q + out + table, plus the appended rows (read once, written once)
+    app_bytes = append_bytes(B, shape)
+    bytes_per_call = sum(decode_bytes([L + K + 1 + i for L in lens0], shape) for i in range(K)) / K + app_bytes
     achieved = bytes_per_call / (dec_mean / 1e3) / 1e9
     clocks = clk.summary()
 
@@ -486,8 +500,7 @@ def run_ours(args):
         if i + 1 < K:
             h2d(i + 1)
         stream.wait_event(ev_in[sl])
-        cache.append_kv(ids, ones_np, dk[sl], dv[sl])
-        cache.decode(0, ids, dq[sl], do[sl])
+        cache.append_decode(0, ids, dk[sl], dv[sl], dq[sl], do[sl])
         ev_done[sl].record(stream)
         with torch.cuda.stream(cstream):
             cstream.wait_event(ev_done[sl])
@@ -507,7 +520,7 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": round(step_ms_max, 5), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "configs[1] Qwen3-8B-shaped HPA decode step (append 1 token + decode), one layer",
+        "config": {"workload": "configs[1] Qwen3-8B-shaped HPA decode step (append 1 token + decode, hpa_append_decode), one layer",
                    "requests_per_gpu": B, "global_batch": B * world, "num_q_heads": 32, "num_kv_heads": 8,
                    "head_dim": 128, "page_size": args.page_size, "latent_sets": docs, "latent_rows": 128,
                    "reasoning_tokens": tokens + 1, "seq_len": docs * 128 + tokens + 1,
@@ -519,7 +532,8 @@ def run_ours(args):
                 "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h,
                 "ms_per_step": round(e2e_ms, 5)},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "hpa decode split (+combine) per call",
+        "roofline": {"bound": "hbm", "kernel": "hpa_append_decode per call: fused append + split decode (+ combine)",
+                     "timing": "region B: an event pair around each call (region A, the value, has none)",
                      "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / pk["hbm_gbs"], 4), "peak_kind": pk_kind,
                      "frac_vs_nominal_8tbs": round(achieved / NOMINAL_HBM_GBS, 4),
@@ -800,7 +814,7 @@ def bench_lmag(torch, Cache, shape, dev, stream, W, K, world, max_over_ranks, ba
     request from a device staging buffer (one batched install), appends 1 token, decodes."""
     import numpy as np
     B = 256
-    cache, seqs, _ = build_decode_cache(torch, Cache, shape, B, 8, 4095, K + W + 8, dev, seed=555)
+    cache, seqs, _ = build_decode_cache(torch, Cache, shape, B, 8, 4095, 2 * K + W + 8, dev, seed=555)
     g = torch.Generator(device=f"cuda:{dev}").manual_seed(1)
     stage = torch.randn((2, B, 1, 2, 128, 8, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
     kn = torch.randn((1, B, 8, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
@@ -808,29 +822,36 @@ def bench_lmag(torch, Cache, shape, dev, stream, W, K, world, max_over_ranks, ba
     q = torch.randn((B, 32, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
     o = torch.empty_like(q)
     ids = np.asarray(seqs, dtype=np.int32)
-    ones = np.ones(B, dtype=np.int32)
     sets = [np.full(B, k, dtype=np.int32) for k in range(8)]
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
-    for i in range(W + K):
-        e = ev[i - W] if i >= W else None
-        if e:
-            e[0].record(stream)
+    # region A (the step rate): install + fused append/decode back to back, no events between;
+    # region B: the same steps with events around each call (install / decode breakdown)
+    for i in range(W):
         cache.latent_install_packed(ids, sets[i % 8], stage[i % 2])
-        if e:
-            e[1].record(stream)
-        cache.append_kv(ids, ones, kn, vn)
-        if e:
-            e[2].record(stream)
-        cache.decode(0, ids, q, o)
-        if e:
-            e[3].record(stream)
+        cache.append_decode(0, ids, kn, vn, q, o)
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize(dev)
+    a0.record(stream)
+    for i in range(W, W + K):
+        cache.latent_install_packed(ids, sets[i % 8], stage[i % 2])
+        cache.append_decode(0, ids, kn, vn, q, o)
+    a1.record(stream)
+    torch.cuda.synchronize(dev)
+    step = max_over_ranks(a0.elapsed_time(a1) / K, device=f"cuda:{dev}")
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    for i in range(K):
+        e = ev[i]
+        e[0].record(stream)
+        cache.latent_install_packed(ids, sets[i % 8], stage[i % 2])
+        e[1].record(stream)
+        cache.append_decode(0, ids, kn, vn, q, o)
+        e[2].record(stream)
     torch.cuda.synchronize(dev)
     inst = max_over_ranks(sum(a[0].elapsed_time(a[1]) for a in ev) / K, device=f"cuda:{dev}")
-    step = max_over_ranks(sum(a[0].elapsed_time(a[3]) for a in ev) / K, device=f"cuda:{dev}")
-    dec = max_over_ranks(sum(a[2].elapsed_time(a[3]) for a in ev) / K, device=f"cuda:{dev}")
+    dec = max_over_ranks(sum(a[1].elapsed_time(a[2]) for a in ev) / K, device=f"cuda:{dev}")
     lens = [cache.seq_info(s)[0] for s in seqs]
     inst_bytes = 2 * B * 128 * 8 * 128 * 2 * 2  # K+V, read + write
-    dbytes = decode_bytes(lens, shape)
+    dbytes = decode_bytes([L - K // 2 for L in lens], shape) + append_bytes(B, shape)
     cache.close()
     # O(1) check (SURVEY 8(d) configs[3]): the install must not depend on the token context.
     # Device time only: a 20 ms spin kernel holds the stream while the host enqueues the 10
@@ -863,6 +884,8 @@ def bench_lmag(torch, Cache, shape, dev, stream, W, K, world, max_over_ranks, ba
             "tokens_per_s": round(B * world / (step / 1e3), 1),
             "tokens_per_s_without_install": round(B * world / ((step - inst) / 1e3), 1),
             "step_ms": round(step, 4), "install_ms": round(inst, 4), "decode_ms": round(dec, 4),
+            "timing": "step: install + hpa_append_decode back to back; install / decode: separate pass "
+                      "with events around each call",
             "install_gbs": round(inst_bytes / (inst / 1e3) / 1e9, 1),
             "decode_gbs": round(dbytes / (dec / 1e3) / 1e9, 1),
             "install_us_vs_reasoning_tokens": o1,

@@ -219,6 +219,21 @@ hpa_status_t hpa_seq_compress(hpa_cache_t* c, int32_t seq_id, int32_t n_doc_rows
 hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
                         const void* q, void* out, float softmax_scale, hpa_stream_t stream);
 
+/* Decode step in one launch (a2 + a4 + a5): the per-token "store ... into the
+ * corresponding blocks" of regular KV fused with the decode that follows it.
+ * Result and cache state are exactly those of
+ *   hpa_append_kv(c, n_seqs, seq_ids, {1, ..., 1}, k, v, stream);
+ *   hpa_decode(c, layer, n_seqs, seq_ids, q, out, softmax_scale, stream);
+ * k, v: device bf16 [L][n_seqs][H_kv][d] (one new row per sequence, every layer);
+ * q, out as hpa_decode. The decode kernel writes each sequence's new row into its pool
+ * slot itself (no separate scatter launch) when the cache stores bf16 token pages and
+ * n_seqs <= 512; otherwise the call runs the two steps above. Argument errors
+ * (INVALID_ARG / OUT_OF_PAGES / SEQ_CAPACITY / UNKNOWN_SEQ) leave the cache unchanged;
+ * after HPA_ERR_CUDA the row is allocated but its contents are undefined. */
+hpa_status_t hpa_append_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
+                               const void* k, const void* v, const void* q, void* out,
+                               float softmax_scale, hpa_stream_t stream);
+
 /* Context-parallel decode (SURVEY §8(f) NEXT-4b: contexts beyond one GPU's pool,
  * pages sharded by row range across GPUs). As hpa_decode, but over the rows this
  * cache holds for each sequence (a shard of the logical sequence; the query is the

@@ -54,6 +54,7 @@ SIGNATURES = {
     "hpa_latent_set_install_host": (c_st, [c_vp, c_i32, c_i32p, c_i32p, c_i32p, ctypes.POINTER(c_vp), c_vp,
                                            c_i32p]),
     "hpa_decode": (c_st, [c_vp, c_i32, c_i32, c_i32p, c_vp, c_vp, ctypes.c_float, c_vp]),
+    "hpa_append_decode": (c_st, [c_vp, c_i32, c_i32, c_i32p, c_vp, c_vp, c_vp, c_vp, ctypes.c_float, c_vp]),
     "hpa_decode_partial": (c_st, [c_vp, c_i32, c_i32, c_i32p, c_vp, c_vp, c_vp, ctypes.c_float, c_vp]),
     "hpa_merge_partials": (c_st, [c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "hpa_prefill": (c_st, [c_vp, c_i32, c_i32, c_i32p, c_i32p, c_vp, c_vp, ctypes.c_float, c_vp]),

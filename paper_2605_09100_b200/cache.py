@@ -227,6 +227,24 @@ class Cache:
                              _stream(self.device, stream)))
         return out
 
+    def append_decode(self, layer: int, seq_ids: Sequence[int], k: torch.Tensor, v: torch.Tensor,
+                      q: torch.Tensor, out: Optional[torch.Tensor] = None, scale: float = 0.0,
+                      stream=None) -> torch.Tensor:
+        """One decode step (hpa_append_decode): append one row per sequence (k, v bf16
+        [L][n][H_kv][d]) and decode q bf16 [n][Hq][d] -> out, in one kernel launch."""
+        ids = seq_ids if isinstance(seq_ids, np.ndarray) and seq_ids.dtype == np.int32 else _i32(seq_ids)
+        n = ids.size
+        kp = self._dev_tensor(k, "k", (self.L, n, self.Hkv, self.d))
+        vp = self._dev_tensor(v, "v", (self.L, n, self.Hkv, self.d))
+        shape = (n, self.Hq, self.d)
+        qp = self._dev_tensor(q, "q", shape)
+        if out is None:
+            out = torch.empty(shape, dtype=torch.bfloat16, device=q.device)
+        op = self._dev_tensor(out, "out", shape)
+        check(LIB.hpa_append_decode(self._h, layer, n, _p32(ids), c_vp(kp), c_vp(vp), c_vp(qp), c_vp(op),
+                                    float(scale), _stream(self.device, stream)))
+        return out
+
     def decode_partial(self, layer: int, seq_ids: Sequence[int], q: torch.Tensor, scale: float = 0.0,
                        stream=None) -> Tuple[torch.Tensor, torch.Tensor]:
         """hpa_decode_partial: (o fp32 [n][Hq][d], lse2 fp32 [n][Hq]) over this cache's shard."""

@@ -566,10 +566,44 @@ struct PDecodeSmem {
   static int bytes(int G) { return oMerge(G) + kNCons * G * (D + 2) * 4; }
 };
 
-template <int D, bool SW>
+// Fused-append kernel parameters (AppendRows with the tail records by value); NA = 1 is the
+// plain decode (n = 0).
+template <int NA>
+struct AppendParams {
+  const __nv_bfloat16* k;  // new rows, bf16 [L][n][H_kv][d]
+  const __nv_bfloat16* v;
+  __nv_bfloat16* k_pool;   // bf16 [L][NP][H_kv][P][d]
+  __nv_bfloat16* v_pool;
+  int64_t stride_l;
+  int32_t n, L;
+  int4 tail[NA];           // {n_entries, page, meta, pos0} of each request's last entry
+};
+
+// One warp copies the new row of (request b, head h) into row (valid - 1) of the tail page,
+// in every layer: lanes [0, D/8) move K, [D/8, D/4) move V, 16 B each. Then the proxy fence:
+// the tile holding the row is read next by TMA (async proxy) after an mbarrier hand-off.
+template <int D, int NA>
+__device__ __forceinline__ void append_tail_row(const AppendParams<NA>& ap, const DecodeArgs& a, int b, int h,
+                                                int4 tl, int lane) {
+  constexpr int NV = D / 8;
+  if (lane < 2 * NV) {
+    const int vi = lane % NV;
+    const bool is_v = lane >= NV;
+    const int r = (tl.z & kMetaRowsMask) - 1;
+    const __nv_bfloat16* src = (is_v ? ap.v : ap.k) + (int64_t(b) * a.Hkv + h) * D + vi * 8;
+    __nv_bfloat16* dst = (is_v ? ap.v_pool : ap.k_pool) + (int64_t(tl.y) * a.Hkv + h) * a.P * D +
+                         int64_t(r) * D + vi * 8;
+    const int64_t lstride = int64_t(a.NP) * a.Hkv * a.P * D;
+    for (int l = 0; l < ap.L; ++l)
+      *reinterpret_cast<int4*>(dst + l * lstride) = *reinterpret_cast<const int4*>(src + l * ap.stride_l);
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+}
+
+template <int D, bool SW, int NA>
 __global__ void __launch_bounds__((kNCons + 2) * 32, HPA_DECODE_CTAS_PER_SM)
 decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                         const DecodeArgs a) {
+                         const DecodeArgs a, const __grid_constant__ AppendParams<NA> ap) {
   using L = PDecodeSmem<D>;
   extern __shared__ __align__(1024) uint8_t smem_pd[];
   uint8_t* smem = smem_pd;
@@ -650,7 +684,11 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       if (lane == 0) tn = HPA_DEC_DYNAMIC ? atomicAdd(a.sched, 1) : t + int(gridDim.x);
       const int4 ur = a.units[t];
       const int seq = ur.y, h = ur.z & 0xff, split = (ur.z >> 8) & 0xff, sb = ur.z >> 16;
-      const int ne = a.t.n_entries[seq];
+      // fused append (NA > 1): the request's last entry and entry count come from the tail
+      // record; the device table still holds the values from before this step's append
+      int4 tl = make_int4(0, 0, 0, 0);
+      if constexpr (NA > 1) tl = ap.tail[ur.x];
+      const int ne = NA > 1 ? tl.x : a.t.n_entries[seq];
       const int e0 = int(int64_t(split) * ne / sb);
       const int e1 = int(int64_t(split + 1) * ne / sb);
       const int32_t* bt = a.t.block_table + int64_t(seq) * a.t.max_pages;
@@ -658,12 +696,29 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       for (int e = e0, first = 1;; e += 31, first = 0) {
         const int cnt = min(31, e1 - e);
         const int last = e + cnt >= e1;
+        if constexpr (NA > 1) {
+          if (last && e1 == ne) {
+            // this unit holds the new row of (request, head h): write it into its pool slot
+            // (every layer) before the piece that loads its tile is published; the proxy
+            // fence orders these generic stores before the producer's TMA reads of the tile
+            append_tail_row<D>(ap, a, ur.x, h, tl, lane);
+            if (h == 0 && lane == 0) {  // write the entry back for later calls
+              const int64_t x = int64_t(seq) * a.t.max_pages + ne - 1;
+              a.t.block_table[x] = tl.y;
+              a.t.pos0[x] = tl.w;
+              a.t.meta[x] = tl.z;
+              a.t.seq_len[seq] = tl.w + (tl.z & kMetaRowsMask);
+              a.t.n_entries[seq] = ne;
+            }
+          }
+        }
         int2 item;
         if (lane == 0) {
           item = make_int2(ur.x, h | (split << 8) | (cnt << 16) | (first << 24) | (last << 25));
         } else if (lane <= cnt) {
-          const int page = bt[e + lane - 1];
-          const int mv = mt[e + lane - 1];
+          const bool tail_entry = NA > 1 && e + lane == ne;
+          const int page = tail_entry ? tl.y : bt[e + lane - 1];
+          const int mv = tail_entry ? tl.z : mt[e + lane - 1];
           const int f8 = a.fp8 && !(mv & kMetaLatent);  // fp8 token page (NEXT-4c)
           item = make_int2(((a.layer * (f8 ? a.NPt : a.NP) + page) * a.Hkv + h) * a.P,
                            (mv & kMetaRowsMask) | (f8 << 16));
@@ -710,7 +765,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         if ((hd.y >> 24) & 1) {  // first piece of a unit: its Q rows
           const int qb = ul & 1;
           if (ul >= 2) mbar_wait(&q_empty[qb], ((ul >> 1) - 1) & 1);
-          qmeta[qb] = make_int4(b, h, split, 0);
+          qmeta[qb] = make_int4(b, h, split, int(i % kNCons));  // ring position of the unit's first chunk
           mbar_arrive_expect_tx(&q_full[qb], uint32_t(G * D * 2));
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -798,6 +853,10 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       break;
     }
     const int b = um.x, h = um.y, split = um.z;
+    // merge slot = this consumer's chunk group within the unit (chunks j = cg mod kNCons):
+    // the unit's result then does not depend on where in the ring it started, i.e. on the
+    // dynamic unit schedule (run-to-run deterministic decode)
+    const int cg = (cw - um.w + kNCons) % kNCons;
     if constexpr (SW) {
     // ---- swapped operands (G <= 8): S^T = K Q^T with the chunk's 16 keys in M and the
     // G heads in N = 8; O^T = V^T P^T with 16 head dims per M tile. Half the MMAs of the
@@ -1202,17 +1261,17 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         const int d0 = 16 * mt + gq;
         const float ivp = 1.f / vpre;
         if (h0 < G) {
-          mo[(cw * G + h0) * D + d0] = o[mt][0] * ivp;
-          mo[(cw * G + h0) * D + d0 + 8] = o[mt][2] * ivp;
+          mo[(cg * G + h0) * D + d0] = o[mt][0] * ivp;
+          mo[(cg * G + h0) * D + d0 + 8] = o[mt][2] * ivp;
         }
         if (h1 < G) {
-          mo[(cw * G + h1) * D + d0] = o[mt][1] * ivp;
-          mo[(cw * G + h1) * D + d0 + 8] = o[mt][3] * ivp;
+          mo[(cg * G + h1) * D + d0] = o[mt][1] * ivp;
+          mo[(cg * G + h1) * D + d0 + 8] = o[mt][3] * ivp;
         }
       }
       if (gq == 0) {
-        if (h0 < G) { mm[cw * G + h0] = m_h[0]; ml[cw * G + h0] = l_h[0]; }
-        if (h1 < G) { mm[cw * G + h1] = m_h[1]; ml[cw * G + h1] = l_h[1]; }
+        if (h0 < G) { mm[cg * G + h0] = m_h[0]; ml[cg * G + h0] = l_h[0]; }
+        if (h1 < G) { mm[cg * G + h1] = m_h[1]; ml[cg * G + h1] = l_h[1]; }
       }
     }
     } else {
@@ -1364,17 +1423,17 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       for (int n = 0; n < D / 8; ++n) {
         const int dcol = n * 8 + 2 * (lane & 3);
         if (g0 < G) {
-          mo[(cw * G + g0) * D + dcol] = o[n][0];
-          mo[(cw * G + g0) * D + dcol + 1] = o[n][1];
+          mo[(cg * G + g0) * D + dcol] = o[n][0];
+          mo[(cg * G + g0) * D + dcol + 1] = o[n][1];
         }
         if (g1 < G) {
-          mo[(cw * G + g1) * D + dcol] = o[n][2];
-          mo[(cw * G + g1) * D + dcol + 1] = o[n][3];
+          mo[(cg * G + g1) * D + dcol] = o[n][2];
+          mo[(cg * G + g1) * D + dcol + 1] = o[n][3];
         }
       }
       if ((lane & 3) == 0) {
-        if (g0 < G) { mm[cw * G + g0] = m_r[0]; ml[cw * G + g0] = l_r[0]; }
-        if (g1 < G) { mm[cw * G + g1] = m_r[1]; ml[cw * G + g1] = l_r[1]; }
+        if (g0 < G) { mm[cg * G + g0] = m_r[0]; ml[cg * G + g0] = l_r[0]; }
+        if (g1 < G) { mm[cg * G + g1] = m_r[1]; ml[cg * G + g1] = l_r[1]; }
       }
     }
     }
@@ -1527,20 +1586,40 @@ __global__ void __launch_bounds__(D) merge_kernel(const float* __restrict__ o_pa
   out[r * D + threadIdx.x] = __float2bfloat16_rn(acc / W);
 }
 
+template <int D, int NA>
+cudaError_t launch_persistent(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,
+                              const AppendRows* ap, cudaStream_t s) {
+  AppendParams<NA> p{};
+  if (ap) {
+    p.k = static_cast<const __nv_bfloat16*>(ap->k);
+    p.v = static_cast<const __nv_bfloat16*>(ap->v);
+    p.k_pool = static_cast<__nv_bfloat16*>(ap->k_pool);
+    p.v_pool = static_cast<__nv_bfloat16*>(ap->v_pool);
+    p.stride_l = ap->stride_l;
+    p.n = ap->n;
+    p.L = ap->L;
+    for (int i = 0; i < ap->n; ++i) p.tail[i] = ap->tail[i];
+  }
+  const int smem = PDecodeSmem<D>::bytes(a.G);
+  const int grid = std::max(1, std::min(a.n_units, decode_slots(D, a.G)));
+  if (a.G <= 8 && HPA_DEC_SWAP)
+    return launch_pdl(decode_persistent_kernel<D, true, NA>, dim3(grid), dim3((kNCons + 2) * 32), smem, s, tm_k,
+                      tm_v, a, p);
+  return launch_pdl(decode_persistent_kernel<D, false, NA>, dim3(grid), dim3((kNCons + 2) * 32), smem, s, tm_k,
+                    tm_v, a, p);
+}
+
 template <int D>
 cudaError_t launch_decode_d(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,
-                            cudaStream_t s, int* launches) {
+                            cudaStream_t s, int* launches, const AppendRows* ap) {
   cudaError_t e;
   if (HPA_DECODE_PERSISTENT) {
-    const int smem = PDecodeSmem<D>::bytes(a.G);
-    const int grid = std::max(1, std::min(a.n_units, decode_slots(D, a.G)));
-    if (a.G <= 8 && HPA_DEC_SWAP)
-      e = launch_pdl(decode_persistent_kernel<D, true>, dim3(grid), dim3((kNCons + 2) * 32), smem, s, tm_k, tm_v,
-                     a);
-    else
-      e = launch_pdl(decode_persistent_kernel<D, false>, dim3(grid), dim3((kNCons + 2) * 32), smem, s, tm_k, tm_v,
-                     a);
+    if (!ap || ap->n == 0) e = launch_persistent<D, 1>(tm_k, tm_v, a, nullptr, s);
+    else if (ap->n != a.n_seqs || ap->n > kAppendFuseMax) return cudaErrorInvalidValue;
+    else if (ap->n <= kAppendFuseSmall) e = launch_persistent<D, kAppendFuseSmall>(tm_k, tm_v, a, ap, s);
+    else e = launch_persistent<D, kAppendFuseMax>(tm_k, tm_v, a, ap, s);
   } else {
+    if (ap && ap->n) return cudaErrorInvalidValue;
     const int smem = DecodeSmem<D>::kBytes;
     e = launch_pdl(decode_split_kernel<D>, dim3(a.splits, a.Hkv, a.n_seqs), dim3((kNCons + 1) * 32), smem, s,
                    tm_k, tm_v, a);
@@ -1578,6 +1657,22 @@ cudaError_t launch_merge(int32_t n_parts, int32_t n_rows, int32_t D, const float
   return cudaErrorInvalidValue;
 }
 
+template <int NA>
+cudaError_t set_persistent_attrs() {
+  auto cap = [](int bytes) { return std::min(bytes, 227 * 1024); };
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(decode_persistent_kernel<128, false, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cap(PDecodeSmem<128>::bytes(16)))) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(decode_persistent_kernel<64, false, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cap(PDecodeSmem<64>::bytes(16)))) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(decode_persistent_kernel<128, true, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cap(PDecodeSmem<128>::bytes(8)))) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(decode_persistent_kernel<64, true, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cap(PDecodeSmem<64>::bytes(8)))) != cudaSuccess)
+    return e;
+  return cudaSuccess;
+}
+
 cudaError_t decode_init_attributes() {
   // the opt-in maximum is 227 KB; configurations that need more fail at launch instead
   auto cap = [](int bytes) { return std::min(bytes, 227 * 1024); };
@@ -1586,14 +1681,8 @@ cudaError_t decode_init_attributes() {
                                 cap(DecodeSmem<128>::kBytes))) != cudaSuccess ||
       (e = cudaFuncSetAttribute(decode_split_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 cap(DecodeSmem<64>::kBytes))) != cudaSuccess ||
-      (e = cudaFuncSetAttribute(decode_persistent_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                cap(PDecodeSmem<128>::bytes(16)))) != cudaSuccess ||
-      (e = cudaFuncSetAttribute(decode_persistent_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                cap(PDecodeSmem<64>::bytes(16)))) != cudaSuccess ||
-      (e = cudaFuncSetAttribute(decode_persistent_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                cap(PDecodeSmem<128>::bytes(8)))) != cudaSuccess ||
-      (e = cudaFuncSetAttribute(decode_persistent_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                cap(PDecodeSmem<64>::bytes(8)))) != cudaSuccess)
+      (e = set_persistent_attrs<1>()) != cudaSuccess || (e = set_persistent_attrs<kAppendFuseSmall>()) != cudaSuccess ||
+      (e = set_persistent_attrs<kAppendFuseMax>()) != cudaSuccess)
     return e;
   return cudaSuccess;
 }
@@ -1619,10 +1708,10 @@ int decode_ctas_per_sm(int32_t D, int32_t /*G*/) {
 }
 
 cudaError_t launch_decode(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,
-                          int32_t D, cudaStream_t s, int* launches) {
+                          int32_t D, cudaStream_t s, int* launches, const AppendRows* ap) {
   if (a.n_seqs == 0) return cudaSuccess;
-  if (D == 128) return launch_decode_d<128>(tm_k, tm_v, a, s, launches);
-  if (D == 64) return launch_decode_d<64>(tm_k, tm_v, a, s, launches);
+  if (D == 128) return launch_decode_d<128>(tm_k, tm_v, a, s, launches, ap);
+  if (D == 64) return launch_decode_d<64>(tm_k, tm_v, a, s, launches, ap);
   return cudaErrorInvalidValue;
 }
 

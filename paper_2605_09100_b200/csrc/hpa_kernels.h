@@ -132,13 +132,30 @@ struct DecodeArgs {
   int32_t n_units;
   long long* trace;         // HPA_TRACE builds only: per-CTA {entry ns, last consumer exit ns, units}
 };
+// Fused decode-step append (hpa_append_decode): request b of the batch gains one token row,
+// written by the decode kernel itself before it reads that row's tile. tail[b] is the
+// request's LAST block-table entry after the append, {n_entries, page, meta, pos0}; the new
+// row is row (meta & kMetaRowsMask) - 1 of that page. The kernel reads these values instead
+// of the device table for that entry (which it writes back for later calls).
+struct AppendRows {
+  const void* k;        // bf16 [L][n][H_kv][d] (device)
+  const void* v;
+  void* k_pool;         // the cache's bf16 pools [L][NP][H_kv][P][d]
+  void* v_pool;
+  int64_t stride_l;     // elements between layers = n * H_kv * d
+  int32_t n, L;         // n == n_seqs of the decode call
+  const int4* tail;     // [n] (host; travels as kernel parameters)
+};
+constexpr int kAppendFuseSmall = 64;   // parameter-block variants: 1 KB and 8 KB of tail records
+constexpr int kAppendFuseMax = 512;
 // Merge of context-parallel partials: out[r][:] = sum_p 2^(lse_p - LSE) o_p / sum_p 2^(lse_p - LSE).
 cudaError_t launch_merge(int32_t n_parts, int32_t n_rows, int32_t D, const float* o_parts,
                          const float* lse_parts, void* out, cudaStream_t s);
 // tm_k / tm_v: 2-D tensor maps over the pools viewed as [L*NP*H_kv*P][d],
 // box {64, 16}, 128-B swizzle.
+// ap (or nullptr): the fused append of hpa_append_decode (persistent kernel, ap->n <= kAppendFuseMax).
 cudaError_t launch_decode(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const DecodeArgs& a,
-                          int32_t D, cudaStream_t s, int* launches);
+                          int32_t D, cudaStream_t s, int* launches, const AppendRows* ap = nullptr);
 int decode_ctas_per_sm(int32_t D, int32_t G);
 // Persistent decode kernel compiled in (HPA_DECODE_PERSISTENT) and its resident CTA count.
 bool decode_persistent();

@@ -1143,13 +1143,15 @@ hpa_status_t hpa_seq_release(hpa_cache_t* c, int32_t seq_id) {
   return HPA_OK;
 }
 
-hpa_status_t hpa_append_kv(hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, const int32_t* n_new,
-                           const void* k, const void* v, hpa_stream_t stream) {
-  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
-  if (n_seqs < 0) return fail(HPA_ERR_INVALID_ARG, "n_seqs < 0");
-  if (n_seqs == 0) return HPA_OK;
+namespace {
+// hpa_append_kv in two halves. append_check validates the call without mutating anything and
+// returns the number of rows; append_apply then allocates, updates the host tables (their
+// device words go to c->pending) and enqueues any copy-on-write page copies on `s`, filling
+// `slots` with each new row's pool slot.
+hpa_status_t append_check(hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, const int32_t* n_new,
+                          const void* k, const void* v, int64_t* rows_out) {
+  *rows_out = 0;
   if (!seq_ids || !n_new) return fail(HPA_ERR_INVALID_ARG, "null seq_ids / n_new");
-  // ---- check (no mutation)
   int64_t total_rows = 0;
   int32_t need = 0;
   std::vector<char> seen(c->cfg.max_seqs, 0);
@@ -1178,11 +1180,14 @@ hpa_status_t hpa_append_kv(hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_id
   }
   if (need > tok.num_free())
     return fail(HPA_ERR_OUT_OF_PAGES, "append needs %d pages, %d free", need, tok.num_free());
-  // ---- apply
-  DeviceGuard dg(c->cfg.device);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  *rows_out = total_rows;
+  return HPA_OK;
+}
+
+hpa_status_t append_apply(hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, const int32_t* n_new,
+                          int64_t total_rows, cudaStream_t s, std::vector<int32_t>& slots) {
+  PageAllocator& tok = c->pages_of(false);
   const int32_t P = c->cfg.page_size;
-  std::vector<int32_t> slots;
   slots.reserve(size_t(total_rows));
   CopyPagesMeta cow{};
   cow.fp8 = c->fp8 ? 1 : 0;
@@ -1223,6 +1228,22 @@ hpa_status_t hpa_append_kv(hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_id
     HPA_CUDA(launch_copy_pages(c->geom(), cow, s));
     c->launches += 1;
   }
+  return HPA_OK;
+}
+}  // namespace
+
+hpa_status_t hpa_append_kv(hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, const int32_t* n_new,
+                           const void* k, const void* v, hpa_stream_t stream) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (n_seqs < 0) return fail(HPA_ERR_INVALID_ARG, "n_seqs < 0");
+  if (n_seqs == 0) return HPA_OK;
+  int64_t total_rows = 0;
+  if (hpa_status_t st = append_check(c, n_seqs, seq_ids, n_new, k, v, &total_rows)) return st;
+  if (total_rows == 0) return HPA_OK;
+  DeviceGuard dg(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<int32_t> slots;
+  if (hpa_status_t st = append_apply(c, n_seqs, seq_ids, n_new, total_rows, s, slots)) return st;
   const int64_t Hd = int64_t(c->cfg.num_kv_heads) * c->cfg.head_dim;
   std::vector<ScatterRecord> recs{
       ScatterRecord{k, v, total_rows * Hd, Hd, int32_t(total_rows), 0, 0, 0, 0, 0, c->fp8 ? 1 : 0, 0}};
@@ -1527,13 +1548,75 @@ hpa_status_t hpa_seq_compress(hpa_cache_t* c, int32_t seq_id, int32_t n_doc_rows
 
 namespace {
 hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids, const void* q,
-                         void* out, float* part_o, float* part_lse, float softmax_scale, hpa_stream_t stream);
+                         void* out, float* part_o, float* part_lse, float softmax_scale, hpa_stream_t stream,
+                         const AppendRows* ap = nullptr);
 }
 
 hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids, const void* q,
                         void* out, float softmax_scale, hpa_stream_t stream) {
   if (!out) return fail(HPA_ERR_INVALID_ARG, "null out");
   return decode_impl(c, layer, n_seqs, seq_ids, q, out, nullptr, nullptr, softmax_scale, stream);
+}
+
+hpa_status_t hpa_append_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
+                               const void* k, const void* v, const void* q, void* out, float softmax_scale,
+                               hpa_stream_t stream) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (n_seqs < 0) return fail(HPA_ERR_INVALID_ARG, "n_seqs < 0");
+  if (n_seqs == 0) return HPA_OK;
+  // everything decode_impl would reject is checked before the append mutates the cache
+  if (layer < 0 || layer >= c->cfg.num_layers) return fail(HPA_ERR_INVALID_ARG, "layer %d out of range", layer);
+  if (n_seqs > c->cfg.max_seqs) return fail(HPA_ERR_INVALID_ARG, "n_seqs > max_seqs");
+  if (!seq_ids || !q || !out) return fail(HPA_ERR_INVALID_ARG, "null argument");
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(HPA_ERR_INVALID_ARG, "q / out must be 16-byte aligned");
+  if (c->fp8 && !decode_persistent())
+    return fail(HPA_ERR_UNSUPPORTED, "fp8 token pages need the persistent decode kernel");
+  if (decode_persistent() && c->cfg.num_kv_heads > 255)
+    return fail(HPA_ERR_UNSUPPORTED, "persistent decode supports H_kv <= 255");
+  const std::vector<int32_t> ones(size_t(n_seqs), 1);
+  int64_t rows = 0;
+  if (hpa_status_t st = append_check(c, n_seqs, seq_ids, ones.data(), k, v, &rows)) return st;
+  DeviceGuard dg(c->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // fp8 token pages quantize on append (copy_kernels.cu); larger batches exceed the kernel's
+  // parameter block: both take the two-launch path
+  const bool fuse = !c->fp8 && decode_persistent() && n_seqs <= kAppendFuseMax;
+  if (fuse) {
+    if (hpa_status_t st = ship(c, s, {}, {}, 0)) return st;  // earlier calls' table words first
+  }
+  std::vector<int32_t> slots;
+  if (hpa_status_t st = append_apply(c, n_seqs, seq_ids, ones.data(), rows, s, slots)) return st;
+  if (!fuse) {
+    const int64_t Hd = int64_t(c->cfg.num_kv_heads) * c->cfg.head_dim;
+    std::vector<ScatterRecord> recs{
+        ScatterRecord{k, v, rows * Hd, Hd, int32_t(rows), 0, 0, 0, 0, 0, c->fp8 ? 1 : 0, 0}};
+    if (hpa_status_t st = ship(c, s, recs, slots, rows)) return st;
+    return decode_impl(c, layer, n_seqs, seq_ids, q, out, nullptr, nullptr, softmax_scale, stream);
+  }
+  // The append changed only each sequence's last entry, its length and its entry count
+  // (rebuild from the old last entry); the kernel takes those from the tail records and
+  // writes them back, so the queued words are dropped -- unless something else is queued.
+  std::vector<int4> tail(static_cast<size_t>(n_seqs));
+  std::vector<int32_t> own;
+  own.reserve(size_t(n_seqs) * 5);
+  for (int32_t i = 0; i < n_seqs; ++i) {
+    const int32_t sid = seq_ids[i];
+    const Seq& sq = c->seqs[sid];
+    const int32_t e = seq_entries(sq) - 1;
+    tail[i] = make_int4(e + 1, sq.pages[e], sq.meta[e], sq.pos0[e]);
+    own.insert(own.end(), {int32_t(c->idx(sid, e)), int32_t(c->off_pos0() + c->idx(sid, e)),
+                           int32_t(c->off_meta() + c->idx(sid, e)), int32_t(c->off_len() + sid),
+                           int32_t(c->off_nent() + sid)});
+  }
+  std::sort(own.begin(), own.end());
+  bool only_own = true;
+  for (const WordWrite& w : c->pending) only_own = only_own && std::binary_search(own.begin(), own.end(), w.idx);
+  if (only_own) c->pending.clear();  // else decode_impl ships them (the same values) first
+  const PoolGeom g = c->geom();
+  const AppendRows ap{k, v, g.k_pool, g.v_pool, rows * c->cfg.num_kv_heads * c->cfg.head_dim, n_seqs,
+                      c->cfg.num_layers, tail.data()};
+  return decode_impl(c, layer, n_seqs, seq_ids, q, out, nullptr, nullptr, softmax_scale, stream, &ap);
 }
 
 hpa_status_t hpa_decode_partial(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
@@ -1557,7 +1640,8 @@ hpa_status_t hpa_merge_partials(int32_t n_parts, int32_t n_rows, int32_t head_di
 
 namespace {
 hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids, const void* q,
-                         void* out, float* part_o, float* part_lse, float softmax_scale, hpa_stream_t stream) {
+                         void* out, float* part_o, float* part_lse, float softmax_scale, hpa_stream_t stream,
+                         const AppendRows* ap) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
   if (layer < 0 || layer >= c->cfg.num_layers) return fail(HPA_ERR_INVALID_ARG, "layer %d out of range", layer);
   if (n_seqs < 0) return fail(HPA_ERR_INVALID_ARG, "n_seqs < 0");
@@ -1656,7 +1740,7 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
   if (c->fp8 && !decode_persistent())
     return fail(HPA_ERR_UNSUPPORTED, "fp8 token pages need the persistent decode kernel");
   int launched = 0;
-  cudaError_t e = launch_decode(c->tm_k_dec, c->tm_v_dec, a, D, s, &launched);
+  cudaError_t e = launch_decode(c->tm_k_dec, c->tm_v_dec, a, D, s, &launched, ap);
   c->launches += launched;
   if (e != cudaSuccess) return cuda_fail(e, "decode launch");
   return HPA_OK;

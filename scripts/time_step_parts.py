@@ -60,3 +60,16 @@ for splits in (0, 1, 2, 3, 4):
     print(f"S={splits}: decode only {loop(dec)} us; append+decode {loop(both)} us", flush=True)
 cache.set_decode_splits(0)
 print(f"append only {loop(app, n=100)} us", flush=True)
+
+# the bench's timed loop records an event between the append and the decode call
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+
+def both_ev():
+    app()
+    ev[0].record(st)
+    dec()
+    ev[1].record(st)
+
+
+print(f"append+decode with events (bench loop) {loop(both_ev)} us", flush=True)
