@@ -71,6 +71,9 @@ constexpr int kNCons = HPA_DEC_NCONS;  // consumer warps per CTA
 #ifndef HPA_DEC_VOTE_MAX
 #define HPA_DEC_VOTE_MAX 1  // swapped consumers: vote before the chunk-max reduction (skipped unless the max grows)
 #endif
+#ifndef HPA_DEC_F32
+#define HPA_DEC_F32 1  // fp8 token pages (G <= 8): 32-row fp8 chunks, two 16-row blocks per ring stage
+#endif
 #ifndef HPA_DEC_LAZY
 #define HPA_DEC_LAZY 1  // decode consumers: lazy running-max rescale (threshold 2^8)
 #endif
@@ -162,7 +165,7 @@ decode_split_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_const
           const int slot = i % kNSt;
           if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
           cmeta[slot] = min(kChunk, valid - sub * kChunk);
-          mbar_arrive_expect_tx(&full[slot], L::kStageBytes);
+          mbar_arrive_expect_tx(&full[slot], 2 * L::kTileBytes);
           uint8_t* kd = stages + slot * L::kStageBytes;
           uint8_t* vd = kd + L::kTileBytes;
           if (HPA_DEC_MAP3) {
@@ -542,23 +545,32 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 constexpr int kWB = 8;  // table-walker ring: pieces of one header + up to 31 page entries
 
-template <int D>
+// F32 (fp8 token pages, swapped consumers): a ring stage holds either one 16-row bf16 chunk
+// (K tile, V tile) or a 32-row fp8 chunk = two 16-row blocks [16 x D codes | 16 scales] of K
+// (A at 0, B at kBlk8) and of V (A at 2 kBlk8, B at 3 kBlk8): twice the keys per hand-off and per
+// softmax step, and twice the fp8 bytes in flight per stage. The stage stride stays 1024-B
+// aligned (128-B swizzled TMA tiles), so the ring is 8 stages deep instead of 12 (two CTAs per SM).
+template <int D, bool F32 = false>
 struct PDecodeSmem {
   static constexpr int kHalves = D / 64;
   static constexpr int kTileBytes = kChunk * D * 2;
-  static constexpr int kStageBytes = 2 * kTileBytes;
+  static constexpr int kBlk8 = 16 * D + 64;
+  static constexpr int kStageBytes =
+      F32 ? (((2 * kTileBytes > 4 * kBlk8 ? 2 * kTileBytes : 4 * kBlk8) + 1023) & ~1023) : 2 * kTileBytes;
+  static constexpr int kStages = F32 ? (D == 128 ? 8 : 12) : kNSt;
+  static_assert(kStages % kNCons == 0, "ring depth must be a multiple of the consumer count");
   static constexpr int oRing = 0;
   // full[NST], empty[NST], q_full[2], q_empty[2], w_full[WB], w_empty[WB]
-  static constexpr int oBar = kNSt * kStageBytes;
-  static constexpr int oMeta = oBar + (2 * kNSt + 4 + 2 * kWB) * 8;
-  static constexpr int oQMeta = (oMeta + kNSt * 4 + 15) & ~15;  // 2 x int4 {b, h, split, -}: unit of Q buffer
+  static constexpr int oBar = kStages * kStageBytes;
+  static constexpr int oMeta = oBar + (2 * kStages + 4 + 2 * kWB) * 8;
+  static constexpr int oQMeta = (oMeta + kStages * 4 + 15) & ~15;  // 2 x int4 {b, h, split, -}: unit of Q buffer
   static constexpr int oWalk = oQMeta + 32;                      // [WB][32] int2 pieces
   static constexpr int oZero = oWalk + kWB * 32 * 8;             // 16 zero bytes: A-operand rows >= G
   // fp8 chunk (NEXT-4c): the K and V blocks [16 x D codes | 16 scales] sit at the top of the
   // stage; the consumer reads the scales, then converts K to [0, kTile), V to [kTile, 2 kTile)
-  static constexpr int kBlk8 = 16 * D + 64;
-  static constexpr int oK8 = kStageBytes - 2 * kBlk8;
-  static constexpr int oV8 = kStageBytes - kBlk8;
+  // (F32: blocks at the bottom, see above; read in place, never converted)
+  static constexpr int oK8 = F32 ? 0 : kStageBytes - 2 * kBlk8;
+  static constexpr int oV8 = F32 ? 2 * kBlk8 : kStageBytes - kBlk8;
   static constexpr int oQ = oZero + 16;                          // 2 x [G][D] q rows (unswizzled)
   static __host__ __device__ int qbuf(int G) { return G * D * 2; }
   static __host__ __device__ int oMerge(int G) { return oQ + 2 * qbuf(G); }
@@ -600,11 +612,14 @@ __device__ __forceinline__ void append_tail_row(const AppendParams<NA>& ap, cons
   }
 }
 
-template <int D, bool SW, int NA>
+template <int D, bool SW, int NA, bool F32 = false>
 __global__ void __launch_bounds__((kNCons + 2) * 32, HPA_DECODE_CTAS_PER_SM)
 decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                          const DecodeArgs a, const __grid_constant__ AppendParams<NA> ap) {
-  using L = PDecodeSmem<D>;
+  static_assert(!F32 || (SW && NA == 1 && HPA_FP8_KSWZ && HPA_FP8_VPAIR && !HPA_FP8_F16 && !HPA_DEC_PAIR),
+                "32-row fp8 chunks: swapped consumers with the register-direct fp8 operands only");
+  using L = PDecodeSmem<D, F32>;
+  constexpr int kNSt = L::kStages;  // ring depth of this variant
   extern __shared__ __align__(1024) uint8_t smem_pd[];
   uint8_t* smem = smem_pd;
   if (smem_u32(smem) & 1023) {  // TMA 128-B swizzle needs 1024-B aligned stage buffers
@@ -749,6 +764,32 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       uint32_t i = 0, pc = 0;
       int ul = 0;
       const uint64_t pol = HPA_DEC_EVICT_FIRST ? l2_policy_evict_first() : 0;
+      // F32: one 32-row fp8 stage = blocks A (+ B): [K A | K B | V A | V B]
+      int64_t pend_blk = 0;
+      int pend_n = 0;  // rows of a held fp8 block A (0: none)
+      auto issue_f8 = [&](int64_t blk_a, int na, int64_t blk_b, int nb) {
+        const int slot = i % kNSt;
+        if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
+#if HPA_DEC_DEBUG_RING
+        dbg_tag[slot] = i;
+#endif
+        cmeta[slot] = na | (nb << 8) | (1 << 16);
+        uint8_t* kd = stages + slot * L::kStageBytes;
+        mbar_arrive_expect_tx(&full[slot], uint32_t((nb ? 4 : 2) * L::kBlk8));
+        bulk_g2s(kd, a.k8 + blk_a * L::kBlk8, L::kBlk8, &full[slot]);
+        bulk_g2s(kd + 2 * L::kBlk8, a.v8 + blk_a * L::kBlk8, L::kBlk8, &full[slot]);
+        if (nb) {
+          bulk_g2s(kd + L::kBlk8, a.k8 + blk_b * L::kBlk8, L::kBlk8, &full[slot]);
+          bulk_g2s(kd + 3 * L::kBlk8, a.v8 + blk_b * L::kBlk8, L::kBlk8, &full[slot]);
+        }
+        ++i;
+      };
+      auto flush_pend = [&]() {
+        if (pend_n) {
+          issue_f8(pend_blk, pend_n, 0, 0);
+          pend_n = 0;
+        }
+      };
       for (;;) {
         const int ws = pc % kWB;
         mbar_wait(&w_full[ws], (pc / kWB) & 1);
@@ -778,6 +819,25 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         for (int j = 1; j <= cnt; ++j) {
           const int2 en = it[j];
           const int rowbase = en.x, valid = en.y & 0xffff, f8 = en.y >> 16;
+          if constexpr (F32) {
+            if (f8) {
+              // fp8 token rows: 16-row blocks paired two per stage; a lone block is published
+              // alone when a bf16 chunk or the unit's end follows (flush_pend)
+              for (int sub = 0; sub * kChunk < valid; ++sub) {
+                const int nrows = min(kChunk, valid - sub * kChunk);
+                const int64_t blk = (int64_t(rowbase) + sub * kChunk) >> 4;
+                if (pend_n == 0) {
+                  pend_blk = blk;
+                  pend_n = nrows;
+                } else {
+                  issue_f8(pend_blk, pend_n, blk, nrows);
+                  pend_n = 0;
+                }
+              }
+              continue;
+            }
+            flush_pend();
+          }
           for (int sub = 0; sub * kChunk < valid; ++sub, ++i) {
             const int slot = i % kNSt;
             if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
@@ -796,7 +856,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
               bulk_g2s(kd + L::oV8, a.v8 + blk * L::kBlk8, L::kBlk8, &full[slot]);
               continue;
             }
-            mbar_arrive_expect_tx(&full[slot], L::kStageBytes);
+            mbar_arrive_expect_tx(&full[slot], 2 * L::kTileBytes);  // K and V tiles (F32 stages are larger)
             if (HPA_DEC_MAP3 && HPA_DEC_EVICT_FIRST) {
               tma_load_3d_hint(kd, &tm_k, &full[slot], 0, rowbase + sub * kChunk, 0, pol);
               tma_load_3d_hint(vd, &tm_v, &full[slot], 0, rowbase + sub * kChunk, 0, pol);
@@ -815,6 +875,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         mbar_arrive(&w_empty[ws]);
         ++pc;
         if (last) {
+          if constexpr (F32) flush_pend();
           for (int c = 0; c < kNCons; ++c, ++i) {  // end of unit: one sentinel per consumer
             const int slot = i % kNSt;
             if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
@@ -922,6 +983,162 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     for (int n = 0; n < D / 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
     float m_h[2] = {-CUDART_INF_F, -CUDART_INF_F};  // running max of heads 2t, 2t+1 (log2 domain)
     float l_h[2] = {0.f, 0.f};                       // partial sums over this lane's keys
+    if constexpr (F32) {
+      // 32-row fp8 chunks: blocks A and B of a stage give two independent QK^T chains, one
+      // softmax step over 32 keys and two PV k-steps; a 16-row bf16 (latent) chunk is block A only
+      for (;; i += kNCons) {
+        const int slot = i % kNSt;
+        mbar_wait(&full[slot], (i / kNSt) & 1);
+#if HPA_DEC_DEBUG_RING
+        if (dbg_tag[slot] != i) {
+          if (lane == 0)
+            printf("hpa decode ring: block %d consumer %d slot %d expected item %u, stage holds %u\n", blockIdx.x, cw,
+                   slot, i, dbg_tag[slot]);
+          __trap();
+        }
+#endif
+        const int meta = cmeta[slot];
+        if (meta <= 0) {  // sentinel: release the slot and finish the unit
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[slot]);
+          i += kNCons;
+          break;
+        }
+        const uint8_t* kt = stages + slot * L::kStageBytes;
+        const bool c8 = meta >= 0x10000;
+        const int nb0 = meta & 0xff, nb1 = (meta >> 8) & 0xff;
+        const bool two = c8 && nb1 > 0;
+        float x[2][4], vm[2][2];
+        float svmax = 0.f;  // this lane's largest valid V scale
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          x[c][0] = x[c][1] = x[c][2] = x[c][3] = -CUDART_INF_F;
+          vm[c][0] = vm[c][1] = 0.f;
+          if (c == 1 && !two) continue;
+          const int nv = c ? nb1 : nb0;
+          float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+          float kmul0 = sl2, kmul1 = sl2;
+          if (c8) {
+            const uint8_t* kb = kt + c * L::kBlk8;
+            const float* ksc = reinterpret_cast<const float*>(kb + 16 * D);
+            const float* vsc = reinterpret_cast<const float*>(kt + (2 + c) * L::kBlk8 + 16 * D);
+            kmul0 = ksc[gq] * slk;
+            kmul1 = ksc[gq + 8] * slk;
+            vm[c][0] = vsc[gq];
+            vm[c][1] = vsc[gq + 8];
+            svmax = fmaxf(svmax, fmaxf(gq < nv ? vm[c][0] : 0.f, gq + 8 < nv ? vm[c][1] : 0.f));
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {  // K fragments straight from the swizzled codes
+              const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + gq * D + fp8_kswz(ks * 16 + 4 * tq, gq, D));
+              const uint32_t w1 =
+                  *reinterpret_cast<const uint32_t*>(kb + (gq + 8) * D + fp8_kswz(ks * 16 + 4 * tq, gq + 8, D));
+              uint32_t ka[4];
+              ka[0] = f16x2_from_e4m3x2(w0);
+              ka[1] = f16x2_from_e4m3x2(w1);
+              ka[2] = f16x2_from_e4m3x2(w0 >> 16);
+              ka[3] = f16x2_from_e4m3x2(w1 >> 16);
+              mma_f16_16816(sacc, ka, qbk[ks][0], qbk[ks][1]);
+            }
+          } else {
+            vm[c][0] = vm[c][1] = 1.f;
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {  // A = K (16 keys x 16 dims), bf16 tile
+              const int mi = lane >> 3;
+              const int row = (lane & 7) + (mi & 1) * 8;
+              const int kc = ks * 2 + (mi >> 1);
+              uint32_t ka[4];
+              ldsm_x4(smem_u32(kt + (kc >> 3) * 2048 + sw128(row, kc & 7)), ka[0], ka[1], ka[2], ka[3]);
+              mma_bf16_16816(sacc, ka, qbf[ks][0], qbf[ks][1]);
+            }
+          }
+          x[c][0] = gq < nv ? sacc[0] * kmul0 : -CUDART_INF_F;      // key g,   head 2t
+          x[c][1] = gq < nv ? sacc[1] * kmul0 : -CUDART_INF_F;      // key g,   head 2t+1
+          x[c][2] = gq + 8 < nv ? sacc[2] * kmul1 : -CUDART_INF_F;  // key g+8, head 2t
+          x[c][3] = gq + 8 < nv ? sacc[3] * kmul1 : -CUDART_INF_F;  // key g+8, head 2t+1
+        }
+        if (c8) fp8_vpre_adjust<D>(svmax, vpre, o);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          vm[c][0] *= vpre;
+          vm[c][1] *= vpre;
+        }
+        float mx0 = fmaxf(fmaxf(x[0][0], x[0][2]), fmaxf(x[1][0], x[1][2]));
+        float mx1 = fmaxf(fmaxf(x[0][1], x[0][3]), fmaxf(x[1][1], x[1][3]));
+        const bool any_grow = __any_sync(0xffffffffu, mx0 > m_h[0] + 8.f || mx1 > m_h[1] + 8.f);
+        if (any_grow) {
+#pragma unroll
+          for (int off = 4; off < 32; off <<= 1) {  // over the 8 key-row lanes
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+          }
+        }
+        const bool g0 = any_grow && mx0 > m_h[0] + 8.f, g1 = any_grow && mx1 > m_h[1] + 8.f;
+        const float mn0 = g0 ? mx0 : m_h[0], mn1 = g1 ? mx1 : m_h[1];
+        float pp[2][4];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          pp[c][0] = fast_exp2(x[c][0] - mn0);
+          pp[c][1] = fast_exp2(x[c][1] - mn1);
+          pp[c][2] = fast_exp2(x[c][2] - mn0);
+          pp[c][3] = fast_exp2(x[c][3] - mn1);
+        }
+        const float s0 = (pp[0][0] + pp[0][2]) + (pp[1][0] + pp[1][2]);
+        const float s1 = (pp[0][1] + pp[0][3]) + (pp[1][1] + pp[1][3]);
+        if (!any_grow) {  // max unchanged: the factors are 1
+          l_h[0] += s0;
+          l_h[1] += s1;
+        } else {
+          const float al0 = fast_exp2(m_h[0] - mn0), al1 = fast_exp2(m_h[1] - mn1);
+          m_h[0] = mn0;
+          m_h[1] = mn1;
+          l_h[0] = l_h[0] * al0 + s0;
+          l_h[1] = l_h[1] * al1 + s1;
+#pragma unroll
+          for (int n = 0; n < D / 16; ++n) {
+            o[n][0] *= al0;
+            o[n][1] *= al1;
+            o[n][2] *= al0;
+            o[n][3] *= al1;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (c == 1 && !two) continue;
+          if (c8) {  // V^T fragments straight from the pair-row codes, P^T in f16 (x vpre)
+            const uint32_t pb0 = movmatrix_t(pack_f16(pp[c][0] * vm[c][0], pp[c][1] * vm[c][0]));
+            const uint32_t pb1 = movmatrix_t(pack_f16(pp[c][2] * vm[c][1], pp[c][3] * vm[c][1]));
+            const uint8_t* vb = kt + (2 + c) * L::kBlk8;
+#pragma unroll
+            for (int mt = 0; mt < D / 16; ++mt) {
+              const int d = 16 * mt + gq;
+              const uint32_t w0 = *reinterpret_cast<const uint32_t*>(vb + fp8_voff(2 * tq, d, D));
+              const uint32_t w1 = *reinterpret_cast<const uint32_t*>(vb + fp8_voff(2 * tq + 8, d, D));
+              uint32_t va[4];
+              va[0] = f16x2_from_e4m3x2(w0);
+              va[1] = f16x2_from_e4m3x2(w0 >> 16);
+              va[2] = f16x2_from_e4m3x2(w1);
+              va[3] = f16x2_from_e4m3x2(w1 >> 16);
+              mma_f16_16816(o[mt], va, pb0, pb1);
+            }
+          } else {
+            const uint32_t pb0 = movmatrix_t(pack_bf16(pp[c][0] * vm[c][0], pp[c][1] * vm[c][0]));
+            const uint32_t pb1 = movmatrix_t(pack_bf16(pp[c][2] * vm[c][1], pp[c][3] * vm[c][1]));
+            const uint8_t* vt = kt + L::kTileBytes;
+#pragma unroll
+            for (int mt = 0; mt < D / 16; ++mt) {  // A = V^T (16 dims x 16 keys)
+              const int mi = lane >> 3;
+              const int key = (lane & 7) + (mi >> 1) * 8;
+              const int dc = 2 * mt + (mi & 1);
+              uint32_t va[4];
+              ldsm_x4_t(smem_u32(vt + (dc >> 3) * 2048 + sw128(key, dc & 7)), va[0], va[1], va[2], va[3]);
+              mma_bf16_16816(o[mt], va, pb0, pb1);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+      }
+    } else {
 #if HPA_DEC_PAIR
     static_assert(HPA_FP8_KSWZ && HPA_FP8_VPAIR && !HPA_FP8_F16, "HPA_DEC_PAIR needs the register-direct fp8 paths");
     // HPA_DEC_PAIR: a consumer takes its next two chunks (items i, i + kNCons) together: two
@@ -1248,6 +1465,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       if (lane == 0) mbar_arrive(&empty[slot]);
     }
 #endif  // HPA_DEC_PAIR
+    }  // F32
     // ---------------------------------------------- merge the consumers' states
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
@@ -1602,6 +1820,11 @@ cudaError_t launch_persistent(const CUtensorMap& tm_k, const CUtensorMap& tm_v, 
   }
   const int smem = PDecodeSmem<D>::bytes(a.G);
   const int grid = std::max(1, std::min(a.n_units, decode_slots(D, a.G)));
+  if constexpr (NA == 1) {
+    if (HPA_DEC_F32 && a.fp8 && a.G <= 8 && HPA_DEC_SWAP)  // fp8 token pages: 32-row fp8 chunks
+      return launch_pdl(decode_persistent_kernel<D, true, 1, true>, dim3(grid), dim3((kNCons + 2) * 32),
+                        PDecodeSmem<D, true>::bytes(a.G), s, tm_k, tm_v, a, p);
+  }
   if (a.G <= 8 && HPA_DEC_SWAP)
     return launch_pdl(decode_persistent_kernel<D, true, NA>, dim3(grid), dim3((kNCons + 2) * 32), smem, s, tm_k,
                       tm_v, a, p);
@@ -1673,6 +1896,19 @@ cudaError_t set_persistent_attrs() {
   return cudaSuccess;
 }
 
+cudaError_t set_f32_attrs() {
+  auto cap = [](int bytes) { return std::min(bytes, 227 * 1024); };
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(decode_persistent_kernel<128, true, 1, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cap(PDecodeSmem<128, true>::bytes(8)))) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(decode_persistent_kernel<64, true, 1, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cap(PDecodeSmem<64, true>::bytes(8)))) != cudaSuccess)
+    return e;
+  return cudaSuccess;
+}
+
 cudaError_t decode_init_attributes() {
   // the opt-in maximum is 227 KB; configurations that need more fail at launch instead
   auto cap = [](int bytes) { return std::min(bytes, 227 * 1024); };
@@ -1682,7 +1918,7 @@ cudaError_t decode_init_attributes() {
       (e = cudaFuncSetAttribute(decode_split_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 cap(DecodeSmem<64>::kBytes))) != cudaSuccess ||
       (e = set_persistent_attrs<1>()) != cudaSuccess || (e = set_persistent_attrs<kAppendFuseSmall>()) != cudaSuccess ||
-      (e = set_persistent_attrs<kAppendFuseMax>()) != cudaSuccess)
+      (e = set_persistent_attrs<kAppendFuseMax>()) != cudaSuccess || (e = set_f32_attrs()) != cudaSuccess)
     return e;
   return cudaSuccess;
 }

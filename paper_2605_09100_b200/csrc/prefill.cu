@@ -140,6 +140,14 @@ __device__ __forceinline__ long long gtimer() {
 #ifndef HPA_PV_SPLIT
 #define HPA_PV_SPLIT 1    // publish P in two 64-key halves (PV starts on the first half)
 #endif
+#ifndef HPA_SM_SEQ
+#define HPA_SM_SEQ 0  // 1: the two slots' exp phases alternate per SMSP (MUFU hand-off barriers); measured slower (B=4 1253 vs 1266 TFLOP/s, profiles/r2_prefill_ab.log)
+#endif
+// MUFU hand-off (HPA_SM_SEQ): softmax warp q of slot 0 and warp q of slot 1 share SMSP q and its
+// MUFU. Their exp phases take turns -- slot 0 tile j, slot 1 tile j, slot 0 tile j+1, ... -- so
+// each runs at the full MUFU rate instead of both at half rate for longer: named barrier
+// kSeqBar0 + q (slot 1 -> slot 0) and kSeqBar1 + q (slot 0 -> slot 1), 64 threads each.
+constexpr uint32_t kSeqBar0 = 3, kSeqBar1 = 7;
 
 template <int D>
 struct PSmem {
@@ -349,7 +357,8 @@ template <int D>
 __device__ __forceinline__ void softmax_tile(const PrefillArgs& a, int s, int quarter, int row, int lane, int j,
                                              uint32_t tS, uint32_t tO, const int32_t* col, uint64_t* cfull,
                                              uint32_t cpar, uint64_t* cempty, uint64_t* pf, int my_i,
-                                             int span_from, float sl2, float& m_run, float& l_run) {
+                                             int span_from, float sl2, float& m_run, float& l_run,
+                                             bool seq = false, bool seq_last = false) {
   float x[kBN];
   constexpr int kLd0 = HPA_SPLIT_LD ? kBN / 2 : kBN;  // columns loaded before the first wait
 #pragma unroll
@@ -421,6 +430,9 @@ __device__ __forceinline__ void softmax_tile(const PrefillArgs& a, int s, int qu
   // exceeds it by > 2^8, so the result is exact whenever no row grew; otherwise the warp
   // redoes half 0 on the exact path below.
   uint32_t pk0[kBN / 4];
+  // MUFU turn: slot 0 waits for slot 1's previous exps (the first wait is pre-arrived), slot 1
+  // for slot 0's exps of this tile
+  if (HPA_SM_SEQ && seq) named_bar_sync((s == 0 ? kSeqBar0 : kSeqBar1) + quarter, 64);
   const bool opt = HPA_OPT_EXP && __all_sync(0xffffffffu, m_run != -CUDART_INF_F);
   bool p0_stored = false;  // P half 0 already in TMEM (not yet published)
   if (opt) {
@@ -491,6 +503,8 @@ __device__ __forceinline__ void softmax_tile(const PrefillArgs& a, int s, int qu
   {
     uint32_t pk1[kBN / 4];
     exps_half(1, m_use, pk1);
+    // hand the MUFU over (slot 1 skips its last hand-off: slot 0 has no tile left to wait for)
+    if (HPA_SM_SEQ && seq && !(s == 1 && seq_last)) named_bar_arrive((s == 0 ? kSeqBar1 : kSeqBar0) + quarter, 64);
     tc_st32(tS + 32, pk1);
     tc_wait_st();
     tc_fence_before();
@@ -1235,6 +1249,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const float sl2 = a.scale_log2;
     const bool live = s == 0 || slot1_live;
     float m_run = -CUDART_INF_F, l_run = 0.f;
+    const bool seq = HPA_SM_SEQ && slot1_live;  // both slots live: MUFU hand-off
+    if (seq && s == 1) named_bar_arrive(kSeqBar0 + quarter, 64);  // slot 0 goes first
     for (int j = 0; j < n_tiles; ++j) {
       const int cs = j % kNC;
       if (!live) {  // dead slot: still release the mask slot
@@ -1250,7 +1266,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #endif
       tc_fence_after();
       softmax_tile<D>(a, s, quarter, row, lane, j, tS, tO, sC + cs * (kBN + 4), &c_full[cs], (j / kNC) & 1,
-                      &c_empty[cs], &p_full[2 * s], my_i, span_from, sl2, m_run, l_run);
+                      &c_empty[cs], &p_full[2 * s], my_i, span_from, sl2, m_run, l_run, seq, j + 1 == n_tiles);
     }
 #ifdef HPA_TRACE
     if (threadIdx.x == 0) {
