@@ -615,9 +615,14 @@ int32_t plan_request_splits(const hpa_cache_t* c, int32_t n, const int32_t* seq_
     }
     return smax;
   }
-  // per-unit cost in chunks (Q load, merge, partial write) and the combine's fixed cost;
-  // HPA_PLAN_C0 / HPA_PLAN_COMBINE override them (tuning knobs, read once)
-  static const double c0 = std::getenv("HPA_PLAN_C0") ? std::atof(std::getenv("HPA_PLAN_C0")) : 0.5;
+  // per-unit cost in chunks (Q load, end-of-unit consumer barrier and merge, partial write) and
+  // the combine's fixed cost; HPA_PLAN_C0 / HPA_PLAN_COMBINE override them (tuning knobs, read
+  // once). c0 measured at configs[1] (profiles/r2_decode_plan_c0.log): bf16 0.5 (3.0 gave the
+  // fused step at most 1 % on one box, none in the bench, and cost 7 % at P = 64); an fp8 chunk
+  // costs ~0.6 of a bf16 one, so the per-unit time is several chunks there: 5.0 (S = 4 instead
+  // of 10 at configs[1]: 170 -> 152.6 us).
+  static const double c0_env = std::getenv("HPA_PLAN_C0") ? std::atof(std::getenv("HPA_PLAN_C0")) : -1.0;
+  const double c0 = c0_env >= 0.0 ? c0_env : (c->fp8 ? 5.0 : 0.5);
   static const double k_comb = std::getenv("HPA_PLAN_COMBINE") ? std::atof(std::getenv("HPA_PLAN_COMBINE")) : 4.0;
   const double hkv = c->cfg.num_kv_heads;
   const double part_chunks = double(c->cfg.num_q_heads) * (c->cfg.head_dim + 1) * 8 / 8192.0;

@@ -30,9 +30,12 @@ __device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes,
                : "memory");
 }
 
-// n_items stages; stage k reads granule perm[k] (and perm2[k] from pool 2 when pairs)
+// n_items stages; stage k reads granule g(k) (and g(k) from pool 2 when pairs); g(k) = perm[k]
+// (mode bit 0 clear: a dependent global load per stage) or a multiplicative hash of k (bit 0 set:
+// no load on the producer's path; n_items a power of two). Mode bit 1: the two copies of a pair
+// stage are issued by lanes 0 and 1 of the producer warp (one instruction) instead of one thread.
 __global__ void __launch_bounds__(64) ring_read(const uint8_t* pool, const uint8_t* pool2, const uint32_t* perm,
-                                                int n_items, int gbytes, int stride, int nst, int pairs) {
+                                                int n_items, int gbytes, int stride, int nst, int pairs, int mode) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const int sbytes = ((pairs ? 2 : 1) * gbytes + 127) & ~127;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + nst * sbytes);
@@ -47,13 +50,24 @@ __global__ void __launch_bounds__(64) ring_read(const uint8_t* pool, const uint8
   __syncthreads();
   const int per = (n_items + gridDim.x - 1) / gridDim.x;
   const int k0 = blockIdx.x * per, k1 = min(n_items, k0 + per);
-  if (threadIdx.x == 0) {
+  const int lane = threadIdx.x;
+  if ((mode & 2) && pairs && lane < 2) {
     for (int k = k0, i = 0; k < k1; ++k, ++i) {
       const int s = i % nst;
       if (i >= nst) mb_wait(&empty[s], ((i / nst) - 1) & 1);
+      if (lane == 0) mb_expect(&full[s], 2 * gbytes);
+      __syncwarp(3u);
+      const uint32_t g = (mode & 1) ? (uint32_t(k) * 2654435761u) & uint32_t(n_items - 1) : perm[k];
+      bulk(sm + s * sbytes + lane * gbytes, (lane ? pool2 : pool) + size_t(g) * stride, gbytes, &full[s]);
+    }
+  } else if (threadIdx.x == 0) {
+    for (int k = k0, i = 0; k < k1; ++k, ++i) {
+      const int s = i % nst;
+      if (i >= nst) mb_wait(&empty[s], ((i / nst) - 1) & 1);
+      const uint32_t g = (mode & 1) ? (uint32_t(k) * 2654435761u) & uint32_t(n_items - 1) : perm[k];
       mb_expect(&full[s], (pairs ? 2 : 1) * gbytes);
-      bulk(sm + s * sbytes, pool + size_t(perm[k]) * stride, gbytes, &full[s]);
-      if (pairs) bulk(sm + s * sbytes + gbytes, pool2 + size_t(perm[k]) * stride, gbytes, &full[s]);
+      bulk(sm + s * sbytes, pool + size_t(g) * stride, gbytes, &full[s]);
+      if (pairs) bulk(sm + s * sbytes + gbytes, pool2 + size_t(g) * stride, gbytes, &full[s]);
     }
   } else if (threadIdx.x == 32) {
     for (int k = k0, i = 0; k < k1; ++k, ++i) {
@@ -75,8 +89,7 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   struct Cfg { int g, stride, pairs; };
-  const Cfg cfgs[] = {{4096, 4096, 1}, {4096, 4096, 0}, {2112, 2112, 1}, {2112, 2112, 0}, {4224, 4224, 0},
-                      {8448, 8448, 0}, {1056, 1056, 1}, {2048, 2048, 1}};
+  const Cfg cfgs[] = {{4096, 4096, 1}, {2112, 2112, 1}, {2112, 2112, 0}, {4224, 4224, 0}, {1056, 1056, 1}};
   for (const Cfg& c : cfgs) {
     const int nit = int(bytes / c.stride) - 1;
     uint32_t* ph = new uint32_t[nit];
@@ -92,22 +105,26 @@ int main() {
     cudaMemcpy(perm, ph, size_t(nit) * 4, cudaMemcpyHostToDevice);
     delete[] ph;
     const int sbytes = ((c.pairs ? 2 : 1) * c.g + 127) & ~127;
-    for (int ctas : {2, 3}) for (int nst : {8, 12, 16, 24}) {
+    for (int mode = 0; mode < 4; ++mode) for (int ctas : {2, 3}) for (int nst : {8, 16}) {
+      if ((mode & 2) && !c.pairs) continue;
+      int nitm = nit;
+      if (mode & 1) { nitm = 1; while (2 * nitm <= nit) nitm *= 2; }
       const int smem = nst * sbytes + 2 * nst * 8;
       if (smem * ctas > 220 * 1024) continue;
       cudaFuncSetAttribute(ring_read, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       const int grid = 148 * ctas;
-      ring_read<<<grid, 64, smem>>>(p1, p2, perm, nit, c.g, c.stride, nst, c.pairs);
+      ring_read<<<grid, 64, smem>>>(p1, p2, perm, nitm, c.g, c.stride, nst, c.pairs, mode);
       cudaDeviceSynchronize();
       cudaEventRecord(a);
-      for (int r = 0; r < 3; ++r) ring_read<<<grid, 64, smem>>>(p1, p2, perm, nit, c.g, c.stride, nst, c.pairs);
+      for (int r = 0; r < 3; ++r) ring_read<<<grid, 64, smem>>>(p1, p2, perm, nitm, c.g, c.stride, nst, c.pairs, mode);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
       cudaEventElapsedTime(&ms, a, b);
-      const double moved = 3.0 * nit * c.g * (c.pairs ? 2 : 1);
-      printf("granule %5d B x %d pool(s), %d CTAs/SM, ring %2d (%6d B in flight/SM): %7.1f GB/s\n", c.g,
-             c.pairs ? 2 : 1, ctas, nst, ctas * nst * sbytes, moved / (ms / 1e3) / 1e9);
+      const double moved = 3.0 * nitm * c.g * (c.pairs ? 2 : 1);
+      printf("granule %5d B x %d pool(s), %s, %s, %d CTAs/SM, ring %2d: %7.1f GB/s\n", c.g, c.pairs ? 2 : 1,
+             (mode & 1) ? "hashed index" : "index load  ", (mode & 2) ? "2 lanes issue" : "1 thread     ", ctas, nst,
+             moved / (ms / 1e3) / 1e9);
     }
     cudaFree(perm);
   }
