@@ -215,7 +215,14 @@ hpa_status_t hpa_seq_compress(hpa_cache_t* c, int32_t seq_id, int32_t n_doc_rows
  * q: device bf16 [n_seqs][Hq][d]; out: device bf16 [n_seqs][Hq][d].
  * out[b][hq] = softmax(scale * K_log[h] q^T) V_log[h], h = floor(hq / G).
  * softmax_scale <= 0 selects 1/sqrt(d) (reading A5). Split-KV over pages +
- * LSE combine; the split count depends only on the batch's page counts. */
+ * LSE combine; the split count depends only on the batch's page counts.
+ * Cascade (NEXT-2; "prefix KV cache for user prompts"): requests of the batch whose
+ * block tables begin with the same run of pages (a prompt prefix shared by hpa_seq_fork,
+ * latent sets shared by hpa_latent_set_share and installed first) read that run once per
+ * group of up to 32/G requests -- one work unit holds the G query rows of every member --
+ * and each request's own remaining pages as usual; all partials merge in the combine. Same
+ * result up to fp32 rounding order; bf16 token pages, G <= 8, runs of >= 4 chunks
+ * (hpa_set_decode_cascade switches it off). */
 hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
                         const void* q, void* out, float softmax_scale, hpa_stream_t stream);
 
@@ -284,6 +291,14 @@ hpa_status_t hpa_export_table(hpa_cache_t* c, int32_t seq_id, int32_t* pages, in
                               uint16_t* meta, int32_t cap, int32_t* n_out);
 /* Testing / tuning hook: force the decode split count (0 = planner). */
 hpa_status_t hpa_set_decode_splits(hpa_cache_t* c, int32_t splits);
+/* Cascade decode of shared leading page runs in hpa_decode / hpa_append_decode /
+ * hpa_decode_partial: on = 1 (default), 0 = every request reads its whole table.
+ * INVALID_ARG on a NULL cache. */
+hpa_status_t hpa_set_decode_cascade(hpa_cache_t* c, int32_t on);
+/* Introspection of the last decode plan (persistent kernel): *n_units work units, of which
+ * *n_group_units are cascade group units, *splits_max partial slots per request (1 = no
+ * combine). Any output pointer may be NULL. INVALID_ARG on a NULL cache. */
+hpa_status_t hpa_decode_plan_info(hpa_cache_t* c, int32_t* n_units, int32_t* n_group_units, int32_t* splits_max);
 /* Testing / tuning hook for hpa_prefill / hpa_prefill_span: 0 = planner (split-KV only for
  * the units of an under-filled last wave), 1 = never split, 2..15 = split every unit's key
  * tiles into that many pieces (merged by LSE), 16 = no host work list (one CTA per unit of a

@@ -63,6 +63,8 @@ SIGNATURES = {
     "hpa_export_logical_kv": (c_st, [c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "hpa_export_table": (c_st, [c_vp, c_i32, c_i32p, c_i32p, c_u16p, c_i32, c_i32p]),
     "hpa_set_decode_splits": (c_st, [c_vp, c_i32]),
+    "hpa_set_decode_cascade": (c_st, [c_vp, c_i32]),
+    "hpa_decode_plan_info": (c_st, [c_vp, c_i32p, c_i32p, c_i32p]),
     "hpa_set_prefill_splits": (c_st, [c_vp, c_i32]),
     "hpa_set_prefill_ctas": (c_st, [c_vp, c_i32]),
     "hpa_prefill_plan_info": (c_st, [c_vp, c_i32p, c_i32p, c_i32p, c_i32p]),

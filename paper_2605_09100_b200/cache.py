@@ -360,6 +360,16 @@ class Cache:
     def set_decode_splits(self, splits: int) -> None:
         check(LIB.hpa_set_decode_splits(self._h, splits))
 
+    def set_decode_cascade(self, on: bool) -> None:
+        """Cascade decode of shared leading page runs (default on)."""
+        check(LIB.hpa_set_decode_cascade(self._h, 1 if on else 0))
+
+    def decode_plan_info(self) -> dict:
+        """The last decode's plan: work units, cascade group units, partial slots per request."""
+        u, g, s = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        check(LIB.hpa_decode_plan_info(self._h, ctypes.byref(u), ctypes.byref(g), ctypes.byref(s)))
+        return {"units": u.value, "group_units": g.value, "splits": s.value}
+
     def set_prefill_splits(self, splits: int) -> None:
         """0 = planner, 1 = never split, 2..15 = every unit split into that many key ranges,
         16 = the grid kernel without a host work list."""

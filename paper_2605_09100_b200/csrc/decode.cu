@@ -550,14 +550,17 @@ constexpr int kWB = 8;  // table-walker ring: pieces of one header + up to 31 pa
 // (A at 0, B at kBlk8) and of V (A at 2 kBlk8, B at 3 kBlk8): twice the keys per hand-off and per
 // softmax step, and twice the fp8 bytes in flight per stage. The stage stride stays 1024-B
 // aligned (128-B swizzled TMA tiles), so the ring is 8 stages deep instead of 12 (two CTAs per SM).
-template <int D, bool F32 = false>
+// CS (cascade decode, NEXT-2): the kernel also runs group units -- one shared run of entries
+// read once for up to 32 query rows of several requests (4 consumers x 8 columns): the Q buffers
+// hold 32 rows and the ring is 8 stages deep so two CTAs still fit on an SM.
+template <int D, bool F32 = false, bool CS = false>
 struct PDecodeSmem {
   static constexpr int kHalves = D / 64;
   static constexpr int kTileBytes = kChunk * D * 2;
   static constexpr int kBlk8 = 16 * D + 64;
   static constexpr int kStageBytes =
       F32 ? (((2 * kTileBytes > 4 * kBlk8 ? 2 * kTileBytes : 4 * kBlk8) + 1023) & ~1023) : 2 * kTileBytes;
-  static constexpr int kStages = F32 ? (D == 128 ? 8 : 12) : kNSt;
+  static constexpr int kStages = F32 ? (D == 128 ? 8 : 12) : (CS ? 8 : kNSt);
   static_assert(kStages % kNCons == 0, "ring depth must be a multiple of the consumer count");
   static constexpr int oRing = 0;
   // full[NST], empty[NST], q_full[2], q_empty[2], w_full[WB], w_empty[WB]
@@ -572,7 +575,8 @@ struct PDecodeSmem {
   static constexpr int oK8 = F32 ? 0 : kStageBytes - 2 * kBlk8;
   static constexpr int oV8 = F32 ? 2 * kBlk8 : kStageBytes - kBlk8;
   static constexpr int oQ = oZero + 16;                          // 2 x [G][D] q rows (unswizzled)
-  static __host__ __device__ int qbuf(int G) { return G * D * 2; }
+  static constexpr int kQRows = 32;  // CS: query rows of a group unit
+  static __host__ __device__ int qbuf(int G) { return (CS && G < kQRows ? kQRows : G) * D * 2; }
   static __host__ __device__ int oMerge(int G) { return oQ + 2 * qbuf(G); }
   // no alignment slack: the dynamic smem base is 1024-B aligned (checked in the kernel)
   static int bytes(int G) { return oMerge(G) + kNCons * G * (D + 2) * 4; }
@@ -612,13 +616,14 @@ __device__ __forceinline__ void append_tail_row(const AppendParams<NA>& ap, cons
   }
 }
 
-template <int D, bool SW, int NA, bool F32 = false>
+template <int D, bool SW, int NA, bool F32 = false, bool CS = false>
 __global__ void __launch_bounds__((kNCons + 2) * 32, HPA_DECODE_CTAS_PER_SM)
 decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                          const DecodeArgs a, const __grid_constant__ AppendParams<NA> ap) {
   static_assert(!F32 || (SW && NA == 1 && HPA_FP8_KSWZ && HPA_FP8_VPAIR && !HPA_FP8_F16 && !HPA_DEC_PAIR),
                 "32-row fp8 chunks: swapped consumers with the register-direct fp8 operands only");
-  using L = PDecodeSmem<D, F32>;
+  static_assert(!CS || (SW && NA == 1 && !F32 && !HPA_DEC_PAIR), "cascade units: swapped bf16 consumers only");
+  using L = PDecodeSmem<D, F32, CS>;
   constexpr int kNSt = L::kStages;  // ring depth of this variant
   extern __shared__ __align__(1024) uint8_t smem_pd[];
   uint8_t* smem = smem_pd;
@@ -656,7 +661,9 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
   if (threadIdx.x == 0) {
     for (int i = 0; i < kNSt; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      // CS: a group unit's stage is released by every consumer, a normal one by its consumer
+      // with an arrival count of kNCons
+      mbar_init(&empty[i], CS ? kNCons : 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
@@ -704,8 +711,16 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       int4 tl = make_int4(0, 0, 0, 0);
       if constexpr (NA > 1) tl = ap.tail[ur.x];
       const int ne = NA > 1 ? tl.x : a.t.n_entries[seq];
-      const int e0 = int(int64_t(split) * ne / sb);
-      const int e1 = int(int64_t(split + 1) * ne / sb);
+      int e0, e1;
+      if (CS && ur.x <= -2) {  // cascade group piece: a fixed entry range of the shared run
+        const int32_t* gr = a.groups + int64_t(-2 - ur.x) * kGroupRec;
+        e0 = gr[0];
+        e1 = gr[1];
+      } else {  // the request's own entries [r, ne) (r = ur.w: its cascaded shared run), split sb ways
+        const int r = ur.w;
+        e0 = r + int(int64_t(split) * (ne - r) / sb);
+        e1 = r + int(int64_t(split + 1) * (ne - r) / sb);
+      }
       const int32_t* bt = a.t.block_table + int64_t(seq) * a.t.max_pages;
       const int32_t* mt = a.t.meta + int64_t(seq) * a.t.max_pages;
       for (int e = e0, first = 1;; e += 31, first = 0) {
@@ -795,7 +810,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         mbar_wait(&w_full[ws], (pc / kWB) & 1);
         const int2* it = walk + ws * 32;
         const int2 hd = it[0];
-        if (hd.x < 0) {  // end of work: tell the consumers through the Q slot
+        if (hd.x == -1) {  // end of work: tell the consumers through the Q slot
           const int qb = ul & 1;
           if (ul >= 2) mbar_wait(&q_empty[qb], ((ul >> 1) - 1) & 1);
           qmeta[qb] = make_int4(-1, 0, 0, 0);
@@ -803,17 +818,29 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
           break;
         }
         const int b = hd.x, h = hd.y & 0xff, split = (hd.y >> 8) & 0xff, cnt = (hd.y >> 16) & 0xff;
+        const bool grp = CS && b <= -2;  // cascade group unit (b = -2 - group piece)
         if ((hd.y >> 24) & 1) {  // first piece of a unit: its Q rows
           const int qb = ul & 1;
           if (ul >= 2) mbar_wait(&q_empty[qb], ((ul >> 1) - 1) & 1);
-          qmeta[qb] = make_int4(b, h, split, int(i % kNCons));  // ring position of the unit's first chunk
-          mbar_arrive_expect_tx(&q_full[qb], uint32_t(G * D * 2));
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  smem_u32(qbuf + qb * qbytes)),
-              "l"(static_cast<const __nv_bfloat16*>(a.q) + (int64_t(b) * a.Hq + int64_t(h) * G) * D),
-              "r"(uint32_t(G * D * 2)), "r"(smem_u32(&q_full[qb]))
-              : "memory");
+          if (grp) {  // the G rows of every member request, stacked
+            const int32_t* gr = a.groups + int64_t(-2 - b) * kGroupRec;
+            const int nm = gr[2];
+            qmeta[qb] = make_int4(b, h, nm, int(i));
+            mbar_arrive_expect_tx(&q_full[qb], uint32_t(nm * G * D * 2));
+            for (int m = 0; m < nm; ++m)
+              bulk_g2s(qbuf + qb * qbytes + m * G * D * 2,
+                       static_cast<const __nv_bfloat16*>(a.q) + (int64_t(gr[4 + m]) * a.Hq + int64_t(h) * G) * D,
+                       uint32_t(G * D * 2), &q_full[qb]);
+          } else {
+            qmeta[qb] = make_int4(b, h, split, int(i));  // ring position of the unit's first chunk
+            mbar_arrive_expect_tx(&q_full[qb], uint32_t(G * D * 2));
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(qbuf + qb * qbytes)),
+                "l"(static_cast<const __nv_bfloat16*>(a.q) + (int64_t(b) * a.Hq + int64_t(h) * G) * D),
+                "r"(uint32_t(G * D * 2)), "r"(smem_u32(&q_full[qb]))
+                : "memory");
+          }
         }
         const int last = (hd.y >> 25) & 1;
         for (int j = 1; j <= cnt; ++j) {
@@ -876,7 +903,8 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         ++pc;
         if (last) {
           if constexpr (F32) flush_pend();
-          for (int c = 0; c < kNCons; ++c, ++i) {  // end of unit: one sentinel per consumer
+          // end of unit: one sentinel per consumer (a group unit's consumers all read one)
+          for (int c = 0; c < (grp ? 1 : kNCons); ++c, ++i) {
             const int slot = i % kNSt;
             if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
             cmeta[slot] = 0;
@@ -902,7 +930,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     const int qb = ul & 1;
     mbar_wait(&q_full[qb], (ul >> 1) & 1);
     const int4 um = qmeta[qb];
-    if (um.x < 0) {  // end of work
+    if (um.x == -1) {  // end of work (x <= -2: a cascade group unit)
 #ifdef HPA_TRACE
       if (a.trace && lane == 0) {
         long long t;
@@ -917,7 +945,26 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     // merge slot = this consumer's chunk group within the unit (chunks j = cg mod kNCons):
     // the unit's result then does not depend on where in the ring it started, i.e. on the
     // dynamic unit schedule (run-to-run deterministic decode)
-    const int cg = (cw - um.w + kNCons) % kNCons;
+    const int cg = (cw - int(uint32_t(um.w) % kNCons) + kNCons) % kNCons;
+    // CS group unit: every consumer reads every chunk of the unit for its own 8 query columns
+    // (rows 8 cw .. 8 cw + 7 of the stacked member rows) and finishes them itself
+    const bool grp = CS && b <= -2;
+    if (grp) i = uint32_t(um.w);
+    const uint32_t istep = grp ? 1u : uint32_t(kNCons);
+    auto release = [&](int slot) {
+      if (lane == 0) {
+        if (CS && !grp) mbar_arrive_cnt(&empty[slot], kNCons);
+        else mbar_arrive(&empty[slot]);
+      }
+    };
+    auto after_sentinel = [&]() {  // the consumer's next item: its own residue class again
+      if (grp) {
+        const uint32_t nx = i + 1;
+        i = nx + uint32_t((cw - int(nx % kNCons) + kNCons) % kNCons);
+      } else {
+        i += kNCons;
+      }
+    };
     if constexpr (SW) {
     // ---- swapped operands (G <= 8): S^T = K Q^T with the chunk's 16 keys in M and the
     // G heads in N = 8; O^T = V^T P^T with 16 head dims per M tile. Half the MMAs of the
@@ -933,12 +980,14 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     // chunks' score multiplier carries 2^qs back. qs = 0 unless max |q| >= 2^15 or < 2^-10.
     float qmul = 1.f, sl2k = sl2;
     {
-      const uint32_t* qrow = reinterpret_cast<const uint32_t*>(qbuf + qb * qbytes + gq * D * 2);
+      const int qr = grp ? 8 * cw + gq : gq;               // this lane's query row in the Q buffer
+      const bool qv = qr < (grp ? split * G : G);          // (group unit: split = member count)
+      const uint32_t* qrow = reinterpret_cast<const uint32_t*>(qbuf + qb * qbytes + qr * D * 2);
       if (a.fp8) {
         float qmax = 0.f;
 #pragma unroll
         for (int w = 0; w < D / 2; w += 4) {
-          const uint32_t v = gq < G ? qrow[w + tq] : 0u;
+          const uint32_t v = qv ? qrow[w + tq] : 0u;
           qmax = fmaxf(qmax, fmaxf(fabsf(__uint_as_float(v << 16)), fabsf(__uint_as_float(v & 0xffff0000u))));
         }
 #pragma unroll
@@ -950,11 +999,11 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       }
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks) {
-        qbf[ks][0] = gq < G ? qrow[8 * ks + tq] : 0u;
-        qbf[ks][1] = gq < G ? qrow[8 * ks + 4 + tq] : 0u;
+        qbf[ks][0] = qv ? qrow[8 * ks + tq] : 0u;
+        qbf[ks][1] = qv ? qrow[8 * ks + 4 + tq] : 0u;
         if (HPA_FP8_KSWZ && a.fp8) {
-          qbk[ks][0] = gq < G ? bf16x2_to_f16x2_scaled(qrow[8 * ks + 2 * tq], qmul) : 0u;
-          qbk[ks][1] = gq < G ? bf16x2_to_f16x2_scaled(qrow[8 * ks + 2 * tq + 1], qmul) : 0u;
+          qbk[ks][0] = qv ? bf16x2_to_f16x2_scaled(qrow[8 * ks + 2 * tq], qmul) : 0u;
+          qbk[ks][1] = qv ? bf16x2_to_f16x2_scaled(qrow[8 * ks + 2 * tq + 1], qmul) : 0u;
         }
       }
     }
@@ -986,7 +1035,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     if constexpr (F32) {
       // 32-row fp8 chunks: blocks A and B of a stage give two independent QK^T chains, one
       // softmax step over 32 keys and two PV k-steps; a 16-row bf16 (latent) chunk is block A only
-      for (;; i += kNCons) {
+      for (;; i += istep) {
         const int slot = i % kNSt;
         mbar_wait(&full[slot], (i / kNSt) & 1);
 #if HPA_DEC_DEBUG_RING
@@ -1000,8 +1049,8 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         const int meta = cmeta[slot];
         if (meta <= 0) {  // sentinel: release the slot and finish the unit
           __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[slot]);
-          i += kNCons;
+          release(slot);
+          after_sentinel();
           break;
         }
         const uint8_t* kt = stages + slot * L::kStageBytes;
@@ -1136,7 +1185,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
+        release(slot);
       }
     } else {
 #if HPA_DEC_PAIR
@@ -1303,7 +1352,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       if (!haveB) break;
     }
 #else
-    for (;; i += kNCons) {
+    for (;; i += istep) {
       const int slot = i % kNSt;
       mbar_wait(&full[slot], (i / kNSt) & 1);
 #if HPA_DEC_DEBUG_RING
@@ -1317,8 +1366,8 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       int nvalid = cmeta[slot];
       if (nvalid <= 0) {  // sentinel: release the slot and finish the unit
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
-        i += kNCons;
+        release(slot);
+        after_sentinel();
         break;
       }
       const bool c8 = nvalid >= 0x10000;  // fp8 chunk (NEXT-4c)
@@ -1462,7 +1511,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
+      release(slot);
     }
 #endif  // HPA_DEC_PAIR
     }  // F32
@@ -1471,6 +1520,28 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     for (int off = 4; off < 32; off <<= 1) {
       l_h[0] += __shfl_xor_sync(0xffffffffu, l_h[0], off);
       l_h[1] += __shfl_xor_sync(0xffffffffu, l_h[1], off);
+    }
+    if (CS && grp) {
+      // group unit: this consumer saw every key of the piece for its columns 2t, 2t+1, i.e.
+      // rows 8 cw + 2t (+1) = (member m, head) -> that member's partial slot of this piece
+      const int32_t* gr = a.groups + int64_t(-2 - b) * kGroupRec;
+      const int nrows = split * G;
+#pragma unroll
+      for (int c2 = 0; c2 < 2; ++c2) {
+        const int row = 8 * cw + 2 * tq + c2;
+        if (row < nrows) {
+          const int m = row / G, hq = h * G + row % G;
+          const int64_t pi = (int64_t(gr[4 + m]) * a.Hq + hq) * a.splits + gr[4 + kGroupMax + m];
+          const float inv = l_h[c2] > 0.f ? 1.f / (l_h[c2] * vpre) : 0.f;
+#pragma unroll
+          for (int mt = 0; mt < D / 16; ++mt) {
+            a.o_part[pi * D + 16 * mt + gq] = o[mt][c2] * inv;
+            a.o_part[pi * D + 16 * mt + gq + 8] = o[mt][2 + c2] * inv;
+          }
+          if (gq == 0) a.lse_part[pi] = l_h[c2] > 0.f ? m_h[c2] + __log2f(l_h[c2]) : -CUDART_INF_F;
+        }
+      }
+      continue;
     }
     {
       const int h0 = 2 * tq, h1 = 2 * tq + 1;
@@ -1510,7 +1581,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     for (int n = 0; n < D / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
     float m_r[2] = {-CUDART_INF_F, -CUDART_INF_F};
     float l_r[2] = {0.f, 0.f};
-    for (;; i += kNCons) {
+    for (;; i += istep) {
       const int slot = i % kNSt;
       mbar_wait(&full[slot], (i / kNSt) & 1);
 #if HPA_DEC_DEBUG_RING
@@ -1524,8 +1595,8 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       int nvalid = cmeta[slot];
       if (nvalid <= 0) {  // sentinel: release the slot and finish the unit
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
-        i += kNCons;
+        release(slot);
+        after_sentinel();
         break;
       }
       const bool c8 = nvalid >= 0x10000;  // fp8 chunk (NEXT-4c)
@@ -1628,7 +1699,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         mma_bf16_16816(o[2 * dp + 1], pa, v2, v3);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
+      release(slot);
     }
     // ---------------------------------------------- merge the consumers' states
     l_r[0] += __shfl_xor_sync(0xffffffffu, l_r[0], 1);
@@ -1824,6 +1895,13 @@ cudaError_t launch_persistent(const CUtensorMap& tm_k, const CUtensorMap& tm_v, 
     if (HPA_DEC_F32 && a.fp8 && a.G <= 8 && HPA_DEC_SWAP)  // fp8 token pages: 32-row fp8 chunks
       return launch_pdl(decode_persistent_kernel<D, true, 1, true>, dim3(grid), dim3((kNCons + 2) * 32),
                         PDecodeSmem<D, true>::bytes(a.G), s, tm_k, tm_v, a, p);
+    if (a.groups) {  // cascade group units in the plan (bf16, G <= 8)
+      if (a.fp8 || a.G > 8 || !HPA_DEC_SWAP || HPA_DEC_PAIR) return cudaErrorInvalidValue;
+      return launch_pdl(decode_persistent_kernel<D, true, 1, false, true>, dim3(grid), dim3((kNCons + 2) * 32),
+                        PDecodeSmem<D, false, true>::bytes(a.G), s, tm_k, tm_v, a, p);
+    }
+  } else {
+    if (a.groups) return cudaErrorInvalidValue;  // the fused append never runs a cascade plan
   }
   if (a.G <= 8 && HPA_DEC_SWAP)
     return launch_pdl(decode_persistent_kernel<D, true, NA>, dim3(grid), dim3((kNCons + 2) * 32), smem, s, tm_k,
@@ -1909,6 +1987,19 @@ cudaError_t set_f32_attrs() {
   return cudaSuccess;
 }
 
+cudaError_t set_cascade_attrs() {
+  auto cap = [](int bytes) { return std::min(bytes, 227 * 1024); };
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(decode_persistent_kernel<128, true, 1, false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cap(PDecodeSmem<128, false, true>::bytes(8)))) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(decode_persistent_kernel<64, true, 1, false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cap(PDecodeSmem<64, false, true>::bytes(8)))) != cudaSuccess)
+    return e;
+  return cudaSuccess;
+}
+
 cudaError_t decode_init_attributes() {
   // the opt-in maximum is 227 KB; configurations that need more fail at launch instead
   auto cap = [](int bytes) { return std::min(bytes, 227 * 1024); };
@@ -1918,7 +2009,8 @@ cudaError_t decode_init_attributes() {
       (e = cudaFuncSetAttribute(decode_split_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 cap(DecodeSmem<64>::kBytes))) != cudaSuccess ||
       (e = set_persistent_attrs<1>()) != cudaSuccess || (e = set_persistent_attrs<kAppendFuseSmall>()) != cudaSuccess ||
-      (e = set_persistent_attrs<kAppendFuseMax>()) != cudaSuccess || (e = set_f32_attrs()) != cudaSuccess)
+      (e = set_persistent_attrs<kAppendFuseMax>()) != cudaSuccess || (e = set_f32_attrs()) != cudaSuccess ||
+      (e = set_cascade_attrs()) != cudaSuccess)
     return e;
   return cudaSuccess;
 }

@@ -126,12 +126,20 @@ struct DecodeArgs {
   int32_t fp8, NPt;
   const uint8_t* k8;
   const uint8_t* v8;
-  const int4* units;        // [n_units] {request b, seq id, h | split << 8 | S_b << 16, 0}
+  const int4* units;        // [n_units] {request b, seq id, h | split << 8 | S_b << 16, r}: entries
+                            // [r, n_entries) split S_b ways (r: the request's cascaded shared run)
   const int32_t* nsplit;    // [n] per-request split count S_b (combine); nullptr = uniform `splits`
   int32_t* sched;           // [2] unit ticket / finished-CTA counters, zero between calls
   int32_t n_units;
   long long* trace;         // HPA_TRACE builds only: per-CTA {entry ns, last consumer exit ns, units}
+  // cascade decode (NEXT-2): group-piece records [kGroupRec] {e0, e1, n members, -, request
+  // index b[kGroupMax], partial slot[kGroupMax]}; a unit {-2 - record, representative seq, h, 0}
+  // reads entries [e0, e1) of the representative once for the G query rows of every member.
+  // nullptr: no group units in this plan.
+  const int32_t* groups;
 };
+constexpr int kGroupMax = 32;               // members per group record (rows = members x G <= 32)
+constexpr int kGroupRec = 4 + 2 * kGroupMax;
 // Fused decode-step append (hpa_append_decode): request b of the batch gains one token row,
 // written by the decode kernel itself before it reads that row's tile. tail[b] is the
 // request's LAST block-table entry after the append, {n_entries, page, meta, pos0}; the new

@@ -227,6 +227,10 @@ struct Seq {
   std::vector<Segment> segs;
   // host mirror of the table row (rebuilt from segs)
   std::vector<int32_t> pages, pos0, meta;
+  // cascade decode (NEXT-2): ph[k] = hash of entries [0, k] (page, meta), pch[k] = 16-row chunks
+  // in entries [0, k]; two sequences share their first k entries iff ph[k - 1] agree
+  std::vector<uint64_t> ph;
+  std::vector<int32_t> pch;
   int32_t len = 0;
   int32_t chunks = 0;  // number of 16-row decode chunks
 };
@@ -378,6 +382,12 @@ struct hpa_cache {
   size_t units_cap = 0, nsplit_cap = 0;
   int32_t plan_units = 0, plan_smax = 1;
   int32_t forced_splits = 0;
+  // cascade decode (NEXT-2): group-piece records of the current plan (device), on/off switch
+  bool cascade = true;
+  int32_t* groups_dev = nullptr;
+  size_t groups_cap = 0;
+  int32_t plan_group_units = 0;
+  bool plan_groups = false;
   // split-KV prefill: forced split count (0 = planner) and the partial workspace
   int32_t pf_forced_splits = 0;
   int32_t pf_ctas = -1;          // prefill CTAs: -1 = one per item (default), 0 = persistent on every SM, n > 0 = at most n
@@ -464,6 +474,19 @@ struct hpa_cache {
     q.meta.insert(q.meta.end(), tmeta.begin(), tmeta.end());
     q.len = pos;
     q.chunks += new_tail_chunks - old_tail_chunks;
+    q.ph.resize(size_t(from_entry));
+    q.pch.resize(size_t(from_entry));
+    for (int32_t k = from_entry; k < n; ++k) {
+      uint64_t h = (k ? q.ph[size_t(k - 1)] : 0x9e3779b97f4a7c15ull) ^
+                   (uint64_t(uint32_t(q.pages[size_t(k)])) << 20 ^ uint64_t(uint32_t(q.meta[size_t(k)])));
+      h ^= h >> 33;  // splitmix64 finalizer
+      h *= 0xff51afd7ed558ccdull;
+      h ^= h >> 33;
+      h *= 0xc4ceb9fe1a85ec53ull;
+      h ^= h >> 33;
+      q.ph.push_back(h);
+      q.pch.push_back((k ? q.pch[size_t(k - 1)] : 0) + ((q.meta[size_t(k)] & kMetaRowsMask) + 15) / 16);
+    }
   }
 };
 
@@ -596,15 +619,13 @@ int32_t plan_splits(hpa_cache_t* c, int32_t n, int32_t max_entries, int32_t max_
 //   cost = total / slots + max_unit / 2 + combine,   total = H_kv * sum_b (chunks_b + c0 * S_b).
 // The units go to the kernel longest first (it fetches them dynamically), so the tail is
 // about half a unit.  Returns S_max and fills splits[] (one per request).
-int32_t plan_request_splits(const hpa_cache_t* c, int32_t n, const int32_t* seq_ids, int32_t slots,
-                            std::vector<int32_t>& splits) {
+int32_t plan_splits_core(const hpa_cache_t* c, int32_t n, std::vector<int32_t> ch, std::vector<int32_t> ne,
+                         int32_t slots, std::vector<int32_t>& splits) {
   splits.assign(n, 1);
-  std::vector<int32_t> ch(n), ne(n);
   int32_t cmax = 0;
   for (int32_t i = 0; i < n; ++i) {
-    const Seq& q = c->seqs[seq_ids[i]];
-    ch[i] = std::max(1, q.chunks);
-    ne[i] = std::max(1, seq_entries(q));
+    ch[i] = std::max(1, ch[i]);
+    ne[i] = std::max(1, ne[i]);
     cmax = std::max(cmax, ch[i]);
   }
   if (c->forced_splits > 0) {
@@ -656,6 +677,101 @@ int32_t plan_request_splits(const hpa_cache_t* c, int32_t n, const int32_t* seq_
     smax = std::max(smax, splits[i]);
   }
   return smax;
+}
+
+int32_t plan_request_splits(const hpa_cache_t* c, int32_t n, const int32_t* seq_ids, int32_t slots,
+                            std::vector<int32_t>& splits) {
+  std::vector<int32_t> ch(n), ne(n);
+  for (int32_t i = 0; i < n; ++i) {
+    ch[i] = c->seqs[seq_ids[i]].chunks;
+    ne[i] = seq_entries(c->seqs[seq_ids[i]]);
+  }
+  return plan_splits_core(c, n, std::move(ch), std::move(ne), slots, splits);
+}
+
+// ---- cascade decode (NEXT-2: "prefix KV cache for user prompts"; shared latent sets)
+// Requests of one batch whose block tables start with the same entries (a forked prompt
+// prefix, shared latent sets installed first) read that run once per group of up to 32 / G
+// members: one group unit per (group, KV head, piece) holds the G query rows of every member
+// and writes each member a partial (O, LSE) of the run; the member's own entries [r, n) are
+// split as usual and the combine merges all partials (same LSE algebra as the split-KV a5).
+struct CGroup {
+  int32_t r = 0;    // shared run: entries [0, r)
+  int32_t rch = 0;  // its 16-row chunks
+  std::vector<int32_t> mem;  // batch indices; mem[0] is the representative
+  int32_t pieces = 1;
+};
+
+// longest common prefix (in entries) of two sequences' tables, from the prefix hashes
+int32_t lcp_entries(const Seq& a, const Seq& b) {
+  int32_t lo = 0, hi = int32_t(std::min(a.ph.size(), b.ph.size()));
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) / 2;
+    if (a.ph[size_t(mid - 1)] == b.ph[size_t(mid - 1)]) lo = mid;
+    else hi = mid - 1;
+  }
+  while (lo > 0 && (a.pages[size_t(lo - 1)] != b.pages[size_t(lo - 1)] || a.meta[size_t(lo - 1)] != b.meta[size_t(lo - 1)]))
+    --lo;  // (a 64-bit hash collision: never seen, kept exact anyway)
+  return lo;
+}
+
+constexpr int32_t kCascadeMinChunks = 4;  // shorter shared runs are decoded per request
+
+std::vector<CGroup> find_cascade_groups(const hpa_cache_t* c, int32_t n, const int32_t* seq_ids) {
+  std::vector<CGroup> out;
+  const int32_t G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
+  if (!c->cascade || c->fp8 || G > 8 || !decode_persistent()) return out;
+  std::vector<std::pair<int32_t, int32_t>> fp;  // (first page, batch index)
+  fp.reserve(size_t(n));
+  for (int32_t i = 0; i < n; ++i) {
+    const Seq& q = c->seqs[seq_ids[i]];
+    if (!q.pages.empty()) fp.emplace_back(q.pages[0], i);
+  }
+  std::sort(fp.begin(), fp.end());
+  const int32_t cap = std::min(kGroupMax, 32 / G);  // members per group unit (32 query rows)
+  for (size_t a = 0; a < fp.size();) {
+    size_t b = a;
+    while (b < fp.size() && fp[b].first == fp[a].first) ++b;
+    if (b - a >= 2) {
+      const Seq& rep = c->seqs[seq_ids[fp[a].second]];
+      std::vector<std::pair<int32_t, int32_t>> ls;  // (-lcp with the bucket's first, batch index)
+      for (size_t k = a; k < b; ++k)
+        ls.emplace_back(-(k == a ? int32_t(rep.pages.size()) : lcp_entries(rep, c->seqs[seq_ids[fp[k].second]])),
+                        fp[k].second);
+      std::sort(ls.begin(), ls.end());
+      // the members taken (longest shared prefixes first) and the run they all share, chosen to
+      // save the most chunk reads: cnt members reading rch chunks each vs once per group
+      int64_t best_gain = 0;
+      size_t best_cnt = 0;
+      for (size_t cnt = 2; cnt <= ls.size(); ++cnt) {
+        const int32_t r = -ls[cnt - 1].first;
+        if (r <= 0) break;
+        const int32_t rch = rep.pch[size_t(r - 1)];
+        const int64_t gain = int64_t(int64_t(cnt) - (int64_t(cnt) + cap - 1) / cap) * rch;
+        if (rch >= kCascadeMinChunks && gain > best_gain) {
+          best_gain = gain;
+          best_cnt = cnt;
+        }
+      }
+      if (best_cnt >= 2) {
+        const int32_t r = -ls[best_cnt - 1].first;
+        std::vector<int32_t> mem;
+        for (size_t k = 0; k < best_cnt; ++k) mem.push_back(ls[k].second);
+        std::sort(mem.begin(), mem.end());
+        for (size_t j = 0; j < mem.size(); j += size_t(cap)) {
+          const size_t e = std::min(mem.size(), j + size_t(cap));
+          if (e - j < 2) break;  // a lone member reads its run itself
+          CGroup g;
+          g.r = r;
+          g.rch = rep.pch[size_t(r - 1)];
+          g.mem.assign(mem.begin() + j, mem.begin() + e);
+          out.push_back(std::move(g));
+        }
+      }
+    }
+    a = b;
+  }
+  return out;
 }
 
 // Split-KV prefill plan. The prefill kernel owns all 512 TMEM columns, so one CTA runs per SM
@@ -1082,6 +1198,7 @@ hpa_status_t hpa_cache_destroy(hpa_cache_t* c) {
   if (c->counters) cudaFree(c->counters);
   if (c->units_dev) cudaFree(c->units_dev);
   if (c->nsplit_dev) cudaFree(c->nsplit_dev);
+  if (c->groups_dev) cudaFree(c->groups_dev);
   if (c->payload_dev) cudaFree(c->payload_dev);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->upload_done) cudaEventDestroy(c->upload_done);
@@ -1586,7 +1703,9 @@ hpa_status_t hpa_append_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, co
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // fp8 token pages quantize on append (copy_kernels.cu); larger batches exceed the kernel's
   // parameter block: both take the two-launch path
-  const bool fuse = !c->fp8 && decode_persistent() && n_seqs <= kAppendFuseMax;
+  // (a batch with cascade groups also takes it: the fused kernel has no group units)
+  const bool fuse = !c->fp8 && decode_persistent() && n_seqs <= kAppendFuseMax &&
+                    find_cascade_groups(c, n_seqs, seq_ids).empty();
   if (fuse) {
     if (hpa_status_t st = ship(c, s, {}, {}, 0)) return st;  // earlier calls' table words first
   }
@@ -1644,6 +1763,125 @@ hpa_status_t hpa_merge_partials(int32_t n_parts, int32_t n_rows, int32_t head_di
 }
 
 namespace {
+// Work list of a batch with cascade groups: own units {b, seq, h | split << 8 | S_b << 16, r_b}
+// over entries [r_b, n_b) and group units {-2 - record, representative, h, 0}, longest first;
+// a member's partial slots are its S_b own splits, then its group's pieces. Uploaded only when
+// the plan changes (key: batch, splits, runs, groups).
+hpa_status_t plan_cascade(hpa_cache_t* c, int32_t n, const int32_t* seq_ids, std::vector<CGroup>& groups,
+                          cudaStream_t s, int32_t* S_out) {
+  const int32_t D = c->cfg.head_dim, Hq = c->cfg.num_q_heads, Hkv = c->cfg.num_kv_heads;
+  const int32_t slots = decode_slots(D, Hq / Hkv);
+  std::vector<int32_t> r(size_t(n), 0), gof(size_t(n), -1);
+  std::vector<int32_t> ch(r.size()), ne(r.size());
+  for (size_t g = 0; g < groups.size(); ++g)
+    for (int32_t i : groups[g].mem) {
+      r[size_t(i)] = groups[g].r;
+      gof[size_t(i)] = int32_t(g);
+    }
+  for (int32_t i = 0; i < n; ++i) {
+    const Seq& q = c->seqs[seq_ids[i]];
+    ne[size_t(i)] = seq_entries(q) - r[size_t(i)];
+    ch[size_t(i)] = q.chunks - (r[size_t(i)] ? q.pch[size_t(r[size_t(i)] - 1)] : 0);
+  }
+  std::vector<int32_t> sp;
+  plan_splits_core(c, n, ch, ne, slots, sp);
+  int32_t E = kCascadeMinChunks;  // chunk budget of an own unit
+  for (int32_t i = 0; i < n; ++i) {
+    if (ne[size_t(i)] <= 0) sp[size_t(i)] = 0;  // nothing of its own: the group covers it
+    else E = std::max(E, (std::max(1, ch[size_t(i)]) + sp[size_t(i)] - 1) / sp[size_t(i)]);
+  }
+  // a group piece reads its chunks once but every consumer of the CTA works through all of
+  // them (for its own query columns): priced at 1.5 chunks per chunk
+  for (CGroup& g : groups) g.pieces = std::max(1, std::min({64, g.r, (3 * g.rch / 2 + E - 1) / E}));
+  if (const char* fp = std::getenv("HPA_CASC_PIECES"))  // debugging knob: forced pieces per group
+    for (CGroup& g : groups) g.pieces = std::max(1, std::min(g.r, std::atoi(fp)));
+  std::vector<int32_t> nsplit(r.size());
+  int32_t S = 2;  // every request goes through the combine
+  for (int32_t i = 0; i < n; ++i) {
+    nsplit[size_t(i)] = sp[size_t(i)] + (gof[size_t(i)] >= 0 ? groups[size_t(gof[size_t(i)])].pieces : 0);
+    S = std::max(S, nsplit[size_t(i)]);
+  }
+  if (S > 255) return fail(HPA_ERR_UNSUPPORTED, "cascade plan needs %d partial slots (max 255)", S);
+  std::vector<int32_t> key{-7, S};
+  key.insert(key.end(), seq_ids, seq_ids + n);
+  key.insert(key.end(), sp.begin(), sp.end());
+  key.insert(key.end(), r.begin(), r.end());
+  for (const CGroup& g : groups) {
+    key.push_back(g.pieces);
+    key.push_back(int32_t(g.mem.size()));
+    key.insert(key.end(), g.mem.begin(), g.mem.end());
+  }
+  *S_out = S;
+  if (key == c->plan_key) return HPA_OK;
+  std::vector<int32_t> rec;
+  std::vector<std::pair<double, int4>> list;
+  for (const CGroup& g : groups) {
+    const Seq& rep = c->seqs[seq_ids[g.mem[0]]];
+    for (int32_t pc = 0; pc < g.pieces; ++pc) {
+      const int32_t ri = int32_t(rec.size()) / kGroupRec;
+      const int32_t e0 = int32_t(int64_t(pc) * g.r / g.pieces), e1 = int32_t(int64_t(pc + 1) * g.r / g.pieces);
+      rec.resize(rec.size() + kGroupRec, 0);
+      int32_t* w = rec.data() + size_t(ri) * kGroupRec;
+      w[0] = e0;
+      w[1] = e1;
+      w[2] = int32_t(g.mem.size());
+      for (size_t m = 0; m < g.mem.size(); ++m) {
+        w[4 + m] = g.mem[m];
+        w[4 + kGroupMax + m] = sp[size_t(g.mem[m])] + pc;
+      }
+      const double cost = 1.5 * (rep.pch[size_t(e1 - 1)] - (e0 ? rep.pch[size_t(e0 - 1)] : 0));
+      for (int32_t h = 0; h < Hkv; ++h) list.emplace_back(-cost, int4{-2 - ri, seq_ids[g.mem[0]], h, 0});
+    }
+  }
+  for (int32_t i = 0; i < n; ++i) {
+    if (sp[size_t(i)] == 0) continue;
+    const double cost = double(std::max(1, ch[size_t(i)])) / sp[size_t(i)];
+    for (int32_t h = 0; h < Hkv; ++h)
+      for (int32_t k = 0; k < sp[size_t(i)]; ++k)
+        list.emplace_back(-cost, int4{i, seq_ids[i], h | (k << 8) | (sp[size_t(i)] << 16), r[size_t(i)]});
+  }
+  std::stable_sort(list.begin(), list.end(), [](const std::pair<double, int4>& x, const std::pair<double, int4>& y) {
+    return x.first < y.first;
+  });
+  const size_t U = list.size();
+  if (U > (size_t(1) << 30)) return fail(HPA_ERR_INVALID_ARG, "too many decode work units");
+  if (U > c->units_cap) {
+    if (c->units_dev) cudaFree(c->units_dev);
+    c->units_dev = nullptr;
+    c->units_cap = std::max<size_t>(U, 4096);
+    HPA_CUDA(cudaMalloc(&c->units_dev, c->units_cap * sizeof(int4)));
+  }
+  if (size_t(n) > c->nsplit_cap) {
+    if (c->nsplit_dev) cudaFree(c->nsplit_dev);
+    c->nsplit_dev = nullptr;
+    c->nsplit_cap = std::max<size_t>(size_t(n), 1024);
+    HPA_CUDA(cudaMalloc(&c->nsplit_dev, c->nsplit_cap * 4));
+  }
+  if (rec.size() > c->groups_cap) {
+    if (c->groups_dev) cudaFree(c->groups_dev);
+    c->groups_dev = nullptr;
+    c->groups_cap = std::max<size_t>(rec.size(), 64 * kGroupRec);
+    HPA_CUDA(cudaMalloc(&c->groups_dev, c->groups_cap * 4));
+  }
+  const size_t ub = U * sizeof(int4), nb = size_t(n) * 4, gb = rec.size() * 4;
+  size_t off;
+  if (hpa_status_t st = ring_reserve(c, ub + nb + gb, &off)) return st;
+  int4* hu = reinterpret_cast<int4*>(c->ring.host(off));
+  for (size_t k = 0; k < U; ++k) hu[k] = list[k].second;
+  std::memcpy(c->ring.host(off) + ub, nsplit.data(), nb);
+  std::memcpy(c->ring.host(off) + ub + nb, rec.data(), gb);
+  HPA_CUDA(cudaMemcpyAsync(c->units_dev, c->ring.host(off), ub, cudaMemcpyHostToDevice, s));
+  HPA_CUDA(cudaMemcpyAsync(c->nsplit_dev, c->ring.host(off) + ub, nb, cudaMemcpyHostToDevice, s));
+  HPA_CUDA(cudaMemcpyAsync(c->groups_dev, c->ring.host(off) + ub + nb, gb, cudaMemcpyHostToDevice, s));
+  HPA_CUDA(c->ring.commit(off, ub + nb + gb, s));
+  c->plan_key.swap(key);
+  c->plan_units = int32_t(U);
+  c->plan_smax = S;
+  c->plan_groups = true;
+  c->plan_group_units = int32_t(rec.size() / kGroupRec) * Hkv;
+  return HPA_OK;
+}
+
 hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids, const void* q,
                          void* out, float* part_o, float* part_lse, float softmax_scale, hpa_stream_t stream,
                          const AppendRows* ap) {
@@ -1671,11 +1909,18 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
   int32_t S = 1;
   if (decode_persistent()) {
     if (Hkv > 255) return fail(HPA_ERR_UNSUPPORTED, "persistent decode supports H_kv <= 255");
+    std::vector<CGroup> groups;
+    if (!ap) groups = find_cascade_groups(c, n_seqs, seq_ids);  // (the fused append never sees one)
     std::vector<int32_t> sp;
-    S = plan_request_splits(c, n_seqs, seq_ids, decode_slots(D, Hq / Hkv), sp);
-    std::vector<int32_t> key(seq_ids, seq_ids + n_seqs);
-    key.insert(key.end(), sp.begin(), sp.end());
-    if (key != c->plan_key) {
+    std::vector<int32_t> key;
+    if (!groups.empty()) {
+      if (hpa_status_t st = plan_cascade(c, n_seqs, seq_ids, groups, s, &S)) return st;
+    } else {
+      S = plan_request_splits(c, n_seqs, seq_ids, decode_slots(D, Hq / Hkv), sp);
+      key.assign(seq_ids, seq_ids + n_seqs);
+      key.insert(key.end(), sp.begin(), sp.end());
+    }
+    if (groups.empty() && key != c->plan_key) {
       // unit list, longest unit first (the kernel fetches units dynamically in this order)
       std::vector<std::pair<double, int32_t>> order;  // (-size, request)
       int64_t U = 0;
@@ -1719,6 +1964,8 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
       c->plan_key.swap(key);
       c->plan_units = int32_t(U);
       c->plan_smax = S;
+      c->plan_groups = false;
+      c->plan_group_units = 0;
     }
   } else {
     S = plan_splits(c, n_seqs, max_entries, max_chunks);
@@ -1741,7 +1988,8 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
                Hq / c->cfg.num_kv_heads, c->cfg.page_size, c->cfg.num_pages, layer, S,
                scale * 1.4426950408889634f, c->fp8 ? 1 : 0, c->fp8 ? c->cfg.num_token_pages : 0,
                c->k8_pool, c->v8_pool, c->units_dev, c->nsplit_dev,
-               c->counters + size_t(c->cfg.max_seqs) * Hkv, c->plan_units, c->trace};
+               c->counters + size_t(c->cfg.max_seqs) * Hkv, c->plan_units, c->trace,
+               decode_persistent() && c->plan_groups ? c->groups_dev : nullptr};
   if (c->fp8 && !decode_persistent())
     return fail(HPA_ERR_UNSUPPORTED, "fp8 token pages need the persistent decode kernel");
   int launched = 0;
@@ -2048,6 +2296,20 @@ hpa_status_t hpa_set_decode_splits(hpa_cache_t* c, int32_t splits) {
 }
 
 // Diagnostics (include/hpa.h): device buffer for the HPA_TRACE phase stamps.
+hpa_status_t hpa_set_decode_cascade(hpa_cache_t* c, int32_t on) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  c->cascade = on != 0;
+  return HPA_OK;
+}
+
+hpa_status_t hpa_decode_plan_info(hpa_cache_t* c, int32_t* n_units, int32_t* n_group_units, int32_t* splits_max) {
+  if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
+  if (n_units) *n_units = c->plan_units;
+  if (n_group_units) *n_group_units = c->plan_groups ? c->plan_group_units : 0;
+  if (splits_max) *splits_max = c->plan_smax;
+  return HPA_OK;
+}
+
 hpa_status_t hpa_debug_trace(hpa_cache_t* c, void* device_buf) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
   c->trace = static_cast<long long*>(device_buf);

@@ -1,0 +1,196 @@
+"""NEXT-2 cascade decode ("prefix KV cache for user prompts"; P:L63
+shared document memories) through the C ABI.
+
+Requests whose block tables begin with the same page run -- prompt prefixes shared by
+hpa_seq_fork, latent sets shared by hpa_latent_set_share and installed first -- are decoded as
+group units (the run read once for up to 32/G requests) plus per-request units over the rest,
+merged by the LSE combine. The oracle knows nothing about this: every output is compared with
+the plain definition (oracle.attend over the oracle's logical K/V of each request, fp64), and
+the plan introspection (hpa_decode_plan_info) proves the group units ran. Cascade off vs on
+must agree to fp32 rounding."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import attend
+from tests.hpa_testutil import Pair, check_close, f64
+from workloads import Shape
+
+pytestmark = pytest.mark.gpu
+
+
+def _shape(hq, hkv, d, P, L=2):
+    return Shape(num_layers=L, num_q_heads=hq, num_kv_heads=hkv, head_dim=d, page_size=P)
+
+
+def _fork(p, src, n):
+    d = p.cache.seq_fork(src, n)
+    p.orc.fork(src, n, d)
+    return d
+
+
+def _ref(p, seqs, q, layer):
+    return np.stack([attend(f64(q[i:i + 1]), *p.orc.logical_kv(s, layer), p.shape.scale)[0]
+                     for i, s in enumerate(seqs)])
+
+
+def _decode_both(p, seqs, q, layer, what):
+    """Cascade on (must plan group units) and off; both against the oracle, and each other."""
+    p.cache.set_decode_cascade(True)
+    on = p.cache.decode(layer, seqs, q.cuda())
+    torch.cuda.synchronize()
+    info = p.cache.decode_plan_info()
+    p.cache.set_decode_cascade(False)
+    off = p.cache.decode(layer, seqs, q.cuda())
+    torch.cuda.synchronize()
+    assert p.cache.decode_plan_info()["group_units"] == 0
+    p.cache.set_decode_cascade(True)
+    ref = _ref(p, seqs, q, layer)
+    check_close(on, ref, f"{what} cascade")
+    check_close(off, ref, f"{what} plain")
+    # both bf16 outputs of fp32 results that differ only in summation order
+    d = np.abs(f64(on) - f64(off)).max()
+    assert d <= 2.0 ** -7 * (1.0 + np.abs(f64(off)).max()), (what, d)
+    return info
+
+
+@pytest.mark.parametrize("hq,hkv,d,P", [(32, 8, 128, 16), (16, 2, 128, 32), (8, 8, 64, 16),
+                                        (16, 2, 64, 64), (8, 1, 128, 16)])
+def test_cascade_forked_prompt(hq, hkv, d, P):
+    """n requests forked from one prompt (latent set + tokens, cut inside a page), each with
+    its own continuation; group sizes 32/G -> several groups and a remainder."""
+    shape = _shape(hq, hkv, d, P)
+    G = hq // hkv
+    p = Pair(shape, 4096, 40, 400, seed=11)
+    src = p.build([("latent", 128), ("tokens", 40 * P + 5)])
+    n = 32 // G + 3  # one full group + a partial one
+    seqs = []
+    for i in range(n):
+        s = _fork(p, src, 128 + 40 * P + 5)
+        p.tokens([s], [1 + (7 * i) % (3 * P)])  # own rows: copy-on-write of the shared partial page
+        seqs.append(s)
+    q = p.queries(n)
+    for layer in (0, 1):
+        info = _decode_both(p, seqs, q, layer, f"fork hq={hq} hkv={hkv} d={d} P={P} L={layer}")
+        assert info["group_units"] > 0, info
+
+
+def test_cascade_mixed_batch_and_growth():
+    """Forks of two prompts, unrelated requests, a request that IS the shared prefix (no own
+    rows), a short shared run below the cascade threshold; then steps of appends (the plan is
+    rebuilt as own runs grow, and when the prefix owner's partial last page grows)."""
+    shape = _shape(32, 8, 128, 16)
+    p = Pair(shape, 8192, 48, 600, seed=5)
+    a = p.build([("tokens", 700)])
+    b = p.build([("latent", 256), ("tokens", 333)])
+    lone = p.build([("tokens", 900)])
+    short = p.build([("tokens", 40)])
+    seqs = [a, b, lone, short]
+    for i in range(9):
+        seqs.append(_fork(p, a, 700 - 16 * (i % 3)))    # different cut points: LCP differs
+    for i in range(5):
+        seqs.append(_fork(p, b, 256 + 333))
+    seqs.append(_fork(p, short, 40))                     # a 3-chunk run: below the threshold
+    for i, s in enumerate(seqs[4:]):
+        p.tokens([s], [3 + i])
+    for step in range(4):
+        q = p.queries(len(seqs))
+        info = _decode_both(p, seqs, q, step % 2, f"mixed step {step}")
+        assert info["group_units"] > 0, info
+        p.tokens(seqs, [1 + (step * 5 + i) % 17 for i in range(len(seqs))])
+
+
+def test_cascade_shared_latent_sets():
+    """Document memories shared by many requests (hpa_latent_set_share), installed first, then
+    each request's own tokens; one request also has a private set in between."""
+    shape = _shape(32, 8, 128, 16)
+    p = Pair(shape, 8192, 40, 300, seed=9)
+    owner = p.new_seq()
+    set0 = p.latent(owner, 128)
+    set1 = p.latent(owner, 96)
+    seqs = []
+    for i in range(12):
+        s = p.new_seq()
+        for sid in (set0, set1):
+            got = p.cache.latent_share(s, owner, sid)
+            assert got == p.orc.share(s, owner, sid)
+        if i == 3:
+            p.latent(s, 64)
+        p.tokens([s], [50 + 13 * i])
+        seqs.append(s)
+    q = p.queries(len(seqs))
+    info = _decode_both(p, seqs, q, 0, "shared sets")
+    assert info["group_units"] > 0, info
+
+
+def test_cascade_forced_splits_and_partial_api():
+    """Group units next to forced own splits, and through hpa_decode_partial (fp32 O + LSE of the
+    whole request) and hpa_append_decode (which then takes the two-launch path)."""
+    shape = _shape(16, 4, 128, 16)
+    p = Pair(shape, 4096, 24, 400, seed=21)
+    src = p.build([("tokens", 1500)])
+    seqs = [src] + [_fork(p, src, 1500) for _ in range(9)]
+    for i, s in enumerate(seqs):
+        p.tokens([s], [20 + 37 * i])
+    p.cache.set_decode_splits(3)
+    q = p.queries(len(seqs))
+    info = _decode_both(p, seqs, q, 0, "forced splits")
+    assert info["group_units"] > 0 and info["splits"] >= 4, info
+    p.cache.set_decode_splits(0)
+    o, lse = p.cache.decode_partial(0, seqs, q.cuda())
+    torch.cuda.synchronize()
+    assert p.cache.decode_plan_info()["group_units"] > 0
+    check_close(o, _ref(p, seqs, q, 0), "partial O")
+    # append + decode in one call == append, then decode
+    k, v = p.draw.tokens(shape, len(seqs))
+    out = torch.empty((len(seqs), 16, 128), dtype=torch.bfloat16, device="cuda")
+    p.cache.append_decode(1, seqs, k.cuda(), v.cuda(), q.cuda(), out)
+    for i, s in enumerate(seqs):
+        p.orc.append(s, f64(k[:, i:i + 1]), f64(v[:, i:i + 1]))
+    torch.cuda.synchronize()
+    assert p.cache.decode_plan_info()["group_units"] > 0
+    check_close(out, _ref(p, seqs, q, 1), "append_decode cascade")
+
+
+def test_cascade_off_for_fp8_and_large_groups_of_one():
+    """fp8 token caches never plan group units (decode stays correct); a batch without two
+    requests sharing a first page plans none either."""
+    shape = _shape(32, 8, 128, 16)
+    p = Pair(shape, 2048, 12, 300, seed=3, token_fp8=True, num_token_pages=2048)
+    src = p.build([("tokens", 600)])
+    seqs = [src] + [_fork(p, src, 600) for _ in range(4)]
+    q = p.queries(len(seqs))
+    out = p.cache.decode(0, seqs, q.cuda())
+    torch.cuda.synchronize()
+    assert p.cache.decode_plan_info()["group_units"] == 0
+    check_close(out, _ref(p, seqs, q, 0), "fp8 forks")
+    p2 = Pair(_shape(32, 8, 128, 16), 2048, 12, 300, seed=4)
+    seqs2 = [p2.build([("tokens", 300 + 50 * i)]) for i in range(5)]
+    q2 = p2.queries(5)
+    out2 = p2.cache.decode(0, seqs2, q2.cuda())
+    torch.cuda.synchronize()
+    assert p2.cache.decode_plan_info()["group_units"] == 0
+    check_close(out2, _ref(p2, seqs2, q2, 0), "no sharing")
+
+
+def test_cascade_fuzz():
+    """Random fork trees (forks of forks at random cuts), random own growth and batch subsets,
+    cascade on vs off vs oracle."""
+    rng = np.random.default_rng(1234)
+    shape = _shape(32, 8, 128, 16)
+    p = Pair(shape, 16384, 64, 800, seed=77)
+    roots = [p.build([("latent", 128), ("tokens", int(rng.integers(200, 1200)))]) for _ in range(3)]
+    live = list(roots)
+    for _ in range(30):
+        src = int(rng.choice(live))
+        L = p.orc.seq_len(src)
+        cut = int(rng.integers(129, L + 1))
+        s = _fork(p, src, cut)
+        p.tokens([s], [int(rng.integers(1, 40))])
+        live.append(s)
+    for it in range(6):
+        batch = sorted(rng.choice(live, size=int(rng.integers(8, len(live))), replace=False).tolist())
+        q = p.queries(len(batch))
+        _decode_both(p, batch, q, it % 2, f"fuzz {it}")
+        grow = [s for s in live if rng.random() < 0.5]
+        p.tokens(grow, [int(rng.integers(1, 30)) for _ in grow])
