@@ -939,22 +939,59 @@ def bench_next(torch, Cache, shape, dev, stream, pk, max_over_ranks):
     q = torch.randn((B, 32, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
     o = torch.empty_like(q)
     ids = np.asarray(seqs, dtype=np.int32)
-    for _ in range(3):
-        cache.decode(0, ids, q, o)
-    torch.cuda.synchronize(dev)
-    e0, e1 = ev(), ev()
-    e0.record(stream)
-    for _ in range(20):
-        cache.decode(0, ids, q, o)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    ms = e0.elapsed_time(e1) / 20
+
+    def time_decode(cascade, n=20):
+        cache.set_decode_cascade(cascade)
+        for _ in range(3):
+            cache.decode(0, ids, q, o)
+        torch.cuda.synchronize(dev)
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for _ in range(n):
+            cache.decode(0, ids, q, o)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / n, cache.decode_plan_info()
+
+    ms_off, _ = time_decode(False)
+    ms, plan = time_decode(True)
     lens = [cache.seq_info(s)[0] for s in seqs]
     out["shared_sets"] = {"workload": "B=64 decode, the same 8 latent sets shared by every request (stored once)",
                           "decode_ms": round(ms, 4), "tokens_per_s": round(B / (ms / 1e3), 1),
                           "logical_gbs": round(decode_bytes(lens, shape) / (ms / 1e3) / 1e9, 1),
+                          "cascade_group_units": plan["group_units"],
+                          "decode_ms_cascade_off": round(ms_off, 4),
                           "latent_pages_stored": 8 * (LATENT_ROWS // P),
                           "latent_pages_if_private": B * 8 * (LATENT_ROWS // P)}
+    cache.close()
+    # NEXT-2 cascade: B = 64 requests forked from one 16384-token prompt (hpa_seq_fork: the
+    # prompt's pages stored once), each with 1024 own tokens; the prompt is read once per group
+    # of 32 / G = 8 requests (cascade) or once per request (off)
+    B, n_prompt, n_own = 64, 16384, 1024
+    pages = n_prompt // P + B * (n_own // P + 2) + 64
+    cache = Cache(1, 32, 8, 128, P, pages, B + 1, (n_prompt + n_own) // P + 4, dev, 99)
+    src = cache.seq_create()
+    kp = torch.randn((1, n_prompt, 8, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+    cache.append_kv([src], [n_prompt], kp, kp.flip(1))
+    seqs = [cache.seq_fork(src, n_prompt) for _ in range(B)]
+    ko = torch.randn((1, B * n_own, 8, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+    cache.append_kv(seqs, [n_own] * B, ko, ko.flip(1))
+    ids = np.asarray(seqs, dtype=np.int32)
+    ms_off, plan_off = time_decode(False)
+    ms, plan = time_decode(True)
+    lens = [cache.seq_info(s)[0] for s in seqs]
+    row_bytes = shape.num_kv_heads * shape.head_dim * 2 * 2  # K + V of one row, all KV heads
+    groups = -(-B // (32 // (shape.num_q_heads // shape.num_kv_heads)))
+    phys = (groups * n_prompt + B * n_own) * row_bytes + 2 * B * shape.num_q_heads * shape.head_dim * 2
+    out["prefix_cascade"] = {
+        "workload": f"B={B} forks of one {n_prompt}-token prompt + {n_own} own tokens each (P:L251 prefix KV)",
+        "decode_ms": round(ms, 4), "tokens_per_s": round(B / (ms / 1e3), 1),
+        "decode_ms_cascade_off": round(ms_off, 4), "speedup_vs_off": round(ms_off / ms, 2),
+        "cascade_group_units": plan["group_units"], "units": plan["units"],
+        "logical_gbs": round(decode_bytes(lens, shape) / (ms / 1e3) / 1e9, 1),
+        "physical_bytes": phys, "physical_gbs": round(phys / (ms / 1e3) / 1e9, 1),
+        "physical_frac_of_copy_peak": round(phys / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 4),
+        "logical_gbs_cascade_off": round(decode_bytes(lens, shape) / (ms_off / 1e3) / 1e9, 1)}
     cache.close()
     # NEXT-3: LMAG-style replacement from pinned host payloads (copy stream) overlapped with decode
     B = 256

@@ -771,6 +771,15 @@ std::vector<CGroup> find_cascade_groups(const hpa_cache_t* c, int32_t n, const i
     }
     a = b;
   }
+  // worth it only when the reads saved are a real share of the batch's: a group chunk costs
+  // ~1.75 normal chunks of CTA time (every consumer works through it), and short shared runs
+  // are L2-resident for the plain path anyway (8 latent sets shared by 64 requests, 17 % of
+  // the reads: 7 % slower with cascade; a 2K prompt + 4K own, 29 %: 3 % slower; a 1K prompt +
+  // 1K own, 44 %: 1.12x faster; profiles/r2_cascade_cases.log)
+  int64_t saved = 0, total = 0;
+  for (const CGroup& g : out) saved += int64_t(g.mem.size() - 1) * g.rch;
+  for (int32_t i = 0; i < n; ++i) total += c->seqs[seq_ids[i]].chunks;
+  if (3 * saved < total) out.clear();
   return out;
 }
 
@@ -1791,9 +1800,30 @@ hpa_status_t plan_cascade(hpa_cache_t* c, int32_t n, const int32_t* seq_ids, std
     else E = std::max(E, (std::max(1, ch[size_t(i)]) + sp[size_t(i)] - 1) / sp[size_t(i)]);
   }
   // a group piece reads its chunks once but every consumer of the CTA works through all of
-  // them (for its own query columns): priced at 1.5 chunks per chunk
-  for (CGroup& g : groups) g.pieces = std::max(1, std::min({64, g.r, (3 * g.rch / 2 + E - 1) / E}));
-  if (const char* fp = std::getenv("HPA_CASC_PIECES"))  // debugging knob: forced pieces per group
+  // them (for its own query columns): ~1.75 chunk times per chunk (configs[1]-shaped forks,
+  // scripts/time_cascade.py). Pieces: no group unit longer than the per-slot share of the
+  // batch's work, and about one group unit per CTA slot (profiles/r2_cascade_pieces.log:
+  // fewer, longer pieces leave the group units on the critical path; more add partials)
+  double work = 0;
+  for (int32_t i = 0; i < n; ++i) work += double(std::max(0, ch[size_t(i)])) * Hkv;
+  for (const CGroup& g : groups) work += 1.75 * g.rch * Hkv;
+  // The group units run first (longest first) and all have about one length, so their count
+  // is kept just under a whole number k of CTA waves (320 units on 296 slots ran 1.3x slower
+  // than 256): the smallest k whose pieces are no longer than the per-slot share of the work.
+  const double share = std::max(double(E), work / slots);
+  const int32_t gh = std::max<int32_t>(1, int32_t(groups.size()) * Hkv);
+  int32_t rmax = 0;
+  for (const CGroup& g : groups) rmax = std::max(rmax, g.rch);
+  int32_t pk = 64;
+  for (int32_t k = 1; k <= 64; ++k) {
+    const int32_t p = std::max(1, k * slots / gh);
+    if (1.75 * rmax / p <= share || p >= 64) {
+      pk = std::min(64, p);
+      break;
+    }
+  }
+  for (CGroup& g : groups) g.pieces = std::max(1, std::min({pk, g.r, std::max(1, g.rch / 4)}));
+  if (const char* fp = std::getenv("HPA_CASC_PIECES"))  // tuning knob: forced pieces per group
     for (CGroup& g : groups) g.pieces = std::max(1, std::min(g.r, std::atoi(fp)));
   std::vector<int32_t> nsplit(r.size());
   int32_t S = 2;  // every request goes through the combine
@@ -1829,7 +1859,7 @@ hpa_status_t plan_cascade(hpa_cache_t* c, int32_t n, const int32_t* seq_ids, std
         w[4 + m] = g.mem[m];
         w[4 + kGroupMax + m] = sp[size_t(g.mem[m])] + pc;
       }
-      const double cost = 1.5 * (rep.pch[size_t(e1 - 1)] - (e0 ? rep.pch[size_t(e0 - 1)] : 0));
+      const double cost = 1.75 * (rep.pch[size_t(e1 - 1)] - (e0 ? rep.pch[size_t(e0 - 1)] : 0));
       for (int32_t h = 0; h < Hkv; ++h) list.emplace_back(-cost, int4{-2 - ri, seq_ids[g.mem[0]], h, 0});
     }
   }
@@ -1990,6 +2020,8 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
                c->k8_pool, c->v8_pool, c->units_dev, c->nsplit_dev,
                c->counters + size_t(c->cfg.max_seqs) * Hkv, c->plan_units, c->trace,
                decode_persistent() && c->plan_groups ? c->groups_dev : nullptr};
+  static const bool force_cs = std::getenv("HPA_FORCE_CS") != nullptr;  // A/B knob: the cascade kernel variant
+  if (force_cs && !a.groups && !c->fp8 && decode_persistent() && !ap) a.groups = reinterpret_cast<const int32_t*>(c->units_dev);
   if (c->fp8 && !decode_persistent())
     return fail(HPA_ERR_UNSUPPORTED, "fp8 token pages need the persistent decode kernel");
   int launched = 0;
