@@ -543,6 +543,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+// the same with an L2 cache-policy hint (evict-first for streamed K/V blocks)
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+#ifndef HPA_FP8_EVICT_FIRST
+#define HPA_FP8_EVICT_FIRST 1  // fp8 K/V blocks streamed with the evict-first L2 policy, like the bf16 tiles
+#endif
+
 constexpr int kWB = 8;  // table-walker ring: pieces of one header + up to 31 page entries
 
 // F32 (fp8 token pages, swapped consumers): a ring stage holds either one 16-row bf16 chunk
@@ -791,11 +804,20 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         cmeta[slot] = na | (nb << 8) | (1 << 16);
         uint8_t* kd = stages + slot * L::kStageBytes;
         mbar_arrive_expect_tx(&full[slot], uint32_t((nb ? 4 : 2) * L::kBlk8));
-        bulk_g2s(kd, a.k8 + blk_a * L::kBlk8, L::kBlk8, &full[slot]);
-        bulk_g2s(kd + 2 * L::kBlk8, a.v8 + blk_a * L::kBlk8, L::kBlk8, &full[slot]);
-        if (nb) {
-          bulk_g2s(kd + L::kBlk8, a.k8 + blk_b * L::kBlk8, L::kBlk8, &full[slot]);
-          bulk_g2s(kd + 3 * L::kBlk8, a.v8 + blk_b * L::kBlk8, L::kBlk8, &full[slot]);
+        if (HPA_FP8_EVICT_FIRST) {  // 148 vs 152 us at configs[1] (profiles/r2_fp8_evict_first_ab.log)
+          bulk_g2s_hint(kd, a.k8 + blk_a * L::kBlk8, L::kBlk8, &full[slot], pol);
+          bulk_g2s_hint(kd + 2 * L::kBlk8, a.v8 + blk_a * L::kBlk8, L::kBlk8, &full[slot], pol);
+          if (nb) {
+            bulk_g2s_hint(kd + L::kBlk8, a.k8 + blk_b * L::kBlk8, L::kBlk8, &full[slot], pol);
+            bulk_g2s_hint(kd + 3 * L::kBlk8, a.v8 + blk_b * L::kBlk8, L::kBlk8, &full[slot], pol);
+          }
+        } else {
+          bulk_g2s(kd, a.k8 + blk_a * L::kBlk8, L::kBlk8, &full[slot]);
+          bulk_g2s(kd + 2 * L::kBlk8, a.v8 + blk_a * L::kBlk8, L::kBlk8, &full[slot]);
+          if (nb) {
+            bulk_g2s(kd + L::kBlk8, a.k8 + blk_b * L::kBlk8, L::kBlk8, &full[slot]);
+            bulk_g2s(kd + 3 * L::kBlk8, a.v8 + blk_b * L::kBlk8, L::kBlk8, &full[slot]);
+          }
         }
         ++i;
       };
