@@ -74,6 +74,9 @@ constexpr int kNCons = HPA_DEC_NCONS;  // consumer warps per CTA
 #ifndef HPA_DEC_F32
 #define HPA_DEC_F32 1  // fp8 token pages (G <= 8): 32-row fp8 chunks, two 16-row blocks per ring stage
 #endif
+#ifndef HPA_DEC_F32_STAGES
+#define HPA_DEC_F32_STAGES 10  // ring depth of the 32-row fp8 variant (d = 128): 10 x 9 KB, two CTAs per SM (147.0 vs 148.2 us with 8, profiles/r2_fp8_ring10_ab.log)
+#endif
 #ifndef HPA_DEC_LAZY
 #define HPA_DEC_LAZY 1  // decode consumers: lazy running-max rescale (threshold 2^8)
 #endif
@@ -573,13 +576,18 @@ struct PDecodeSmem {
   static constexpr int kBlk8 = 16 * D + 64;
   static constexpr int kStageBytes =
       F32 ? (((2 * kTileBytes > 4 * kBlk8 ? 2 * kTileBytes : 4 * kBlk8) + 1023) & ~1023) : 2 * kTileBytes;
-  static constexpr int kStages = F32 ? (D == 128 ? 8 : 12) : (CS ? 8 : kNSt);
-  static_assert(kStages % kNCons == 0, "ring depth must be a multiple of the consumer count");
+  static constexpr int kStages = F32 ? (D == 128 ? HPA_DEC_F32_STAGES : 12) : (CS ? 8 : kNSt);
+  // a depth that is not a multiple of the consumer count puts successive items of one slot on
+  // different consumers, and a consumer could then take the slot's previous phase of the same
+  // parity for its item (mbarrier-parity ABA): every stage then carries its item index (ctag),
+  // which the consumer waits for before its parity wait
+  static constexpr bool kTags = kStages % kNCons != 0;
   static constexpr int oRing = 0;
   // full[NST], empty[NST], q_full[2], q_empty[2], w_full[WB], w_empty[WB]
   static constexpr int oBar = kStages * kStageBytes;
   static constexpr int oMeta = oBar + (2 * kStages + 4 + 2 * kWB) * 8;
-  static constexpr int oQMeta = (oMeta + kStages * 4 + 15) & ~15;  // 2 x int4 {b, h, split, -}: unit of Q buffer
+  static constexpr int oTag = oMeta + kStages * 4;               // [kStages] item index per stage (kTags)
+  static constexpr int oQMeta = (oTag + kStages * 4 + 15) & ~15;  // 2 x int4 {b, h, split, -}: unit of Q buffer
   static constexpr int oWalk = oQMeta + 32;                      // [WB][32] int2 pieces
   static constexpr int oZero = oWalk + kWB * 32 * 8;             // 16 zero bytes: A-operand rows >= G
   // fp8 chunk (NEXT-4c): the K and V blocks [16 x D codes | 16 scales] sit at the top of the
@@ -661,6 +669,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
   uint64_t* w_full = q_empty + 2;
   uint64_t* w_empty = w_full + kWB;
   volatile int32_t* cmeta = reinterpret_cast<int32_t*>(smem + L::oMeta);
+  volatile int32_t* ctag = reinterpret_cast<int32_t*>(smem + L::oTag);
   int4* qmeta = reinterpret_cast<int4*>(smem + L::oQMeta);
   int2* walk = reinterpret_cast<int2*>(smem + L::oWalk);
 #if HPA_DEC_DEBUG_RING
@@ -691,6 +700,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     tma_prefetch_desc(&tm_v);
   }
   if (threadIdx.x < 4) reinterpret_cast<uint32_t*>(zero)[threadIdx.x] = 0u;
+  if (L::kTags && threadIdx.x < kNSt) ctag[threadIdx.x] = -1;
   __syncthreads();
   grid_dependency_wait();  // PDL: everything above overlapped the previous kernel
   grid_launch_dependents();
@@ -802,6 +812,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         dbg_tag[slot] = i;
 #endif
         cmeta[slot] = na | (nb << 8) | (1 << 16);
+        if (L::kTags) ctag[slot] = int(i);
         uint8_t* kd = stages + slot * L::kStageBytes;
         mbar_arrive_expect_tx(&full[slot], uint32_t((nb ? 4 : 2) * L::kBlk8));
         if (HPA_FP8_EVICT_FIRST) {  // 148 vs 152 us at configs[1] (profiles/r2_fp8_evict_first_ab.log)
@@ -891,6 +902,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
             const int slot = i % kNSt;
             if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
             cmeta[slot] = min(kChunk, valid - sub * kChunk) | (f8 << 16);
+            if (L::kTags) ctag[slot] = int(i);
 #if HPA_DEC_DEBUG_RING
             dbg_tag[slot] = i;
 #endif
@@ -930,6 +942,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
             const int slot = i % kNSt;
             if (i >= kNSt) mbar_wait(&empty[slot], ((i / kNSt) - 1) & 1);
             cmeta[slot] = 0;
+            if (L::kTags) ctag[slot] = int(i);
 #if HPA_DEC_DEBUG_RING
             dbg_tag[slot] = i;
 #endif
@@ -1059,6 +1072,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       // softmax step over 32 keys and two PV k-steps; a 16-row bf16 (latent) chunk is block A only
       for (;; i += istep) {
         const int slot = i % kNSt;
+        if (L::kTags) while (ctag[slot] != int(i)) {}  // this stage holds item i (depth % consumers != 0)
         mbar_wait(&full[slot], (i / kNSt) & 1);
 #if HPA_DEC_DEBUG_RING
         if (dbg_tag[slot] != i) {
@@ -1376,7 +1390,8 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
 #else
     for (;; i += istep) {
       const int slot = i % kNSt;
-      mbar_wait(&full[slot], (i / kNSt) & 1);
+      if (L::kTags) while (ctag[slot] != int(i)) {}  // this stage holds item i (depth % consumers != 0)
+        mbar_wait(&full[slot], (i / kNSt) & 1);
 #if HPA_DEC_DEBUG_RING
       if (dbg_tag[slot] != i) {
         if (lane == 0)
@@ -1605,7 +1620,8 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     float l_r[2] = {0.f, 0.f};
     for (;; i += istep) {
       const int slot = i % kNSt;
-      mbar_wait(&full[slot], (i / kNSt) & 1);
+      if (L::kTags) while (ctag[slot] != int(i)) {}  // this stage holds item i (depth % consumers != 0)
+        mbar_wait(&full[slot], (i / kNSt) & 1);
 #if HPA_DEC_DEBUG_RING
       if (dbg_tag[slot] != i) {
         if (lane == 0)
