@@ -74,6 +74,12 @@ constexpr int kNCons = HPA_DEC_NCONS;  // consumer warps per CTA
 #ifndef HPA_DEC_F32
 #define HPA_DEC_F32 1  // fp8 token pages (G <= 8): 32-row fp8 chunks, two 16-row blocks per ring stage
 #endif
+#ifndef HPA_CS_PAIR
+#define HPA_CS_PAIR 1  // cascade group units: consumers take two chunks per softmax step
+#endif
+#ifndef HPA_DEC_CS_STAGES
+#define HPA_DEC_CS_STAGES 10  // ring depth of the cascade variant (its Q buffers hold 32 rows)
+#endif
 #ifndef HPA_DEC_F32_STAGES
 #define HPA_DEC_F32_STAGES 10  // ring depth of the 32-row fp8 variant (d = 128): 10 x 9 KB, two CTAs per SM (147.0 vs 148.2 us with 8, profiles/r2_fp8_ring10_ab.log)
 #endif
@@ -576,7 +582,7 @@ struct PDecodeSmem {
   static constexpr int kBlk8 = 16 * D + 64;
   static constexpr int kStageBytes =
       F32 ? (((2 * kTileBytes > 4 * kBlk8 ? 2 * kTileBytes : 4 * kBlk8) + 1023) & ~1023) : 2 * kTileBytes;
-  static constexpr int kStages = F32 ? (D == 128 ? HPA_DEC_F32_STAGES : 12) : (CS ? 8 : kNSt);
+  static constexpr int kStages = F32 ? (D == 128 ? HPA_DEC_F32_STAGES : 12) : (CS ? HPA_DEC_CS_STAGES : kNSt);
   // a depth that is not a multiple of the consumer count puts successive items of one slot on
   // different consumers, and a consumer could then take the slot's previous phase of the same
   // parity for its item (mbarrier-parity ABA): every stage then carries its item index (ctag),
@@ -1073,7 +1079,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       for (;; i += istep) {
         const int slot = i % kNSt;
         if (L::kTags) while (ctag[slot] != int(i)) {}  // this stage holds item i (depth % consumers != 0)
-        mbar_wait(&full[slot], (i / kNSt) & 1);
+      mbar_wait(&full[slot], (i / kNSt) & 1);
 #if HPA_DEC_DEBUG_RING
         if (dbg_tag[slot] != i) {
           if (lane == 0)
@@ -1388,10 +1394,117 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       if (!haveB) break;
     }
 #else
+    if (CS && grp && HPA_CS_PAIR) {
+      // Group unit (cascade): every consumer works through every chunk, so two chunks per step
+      // -- items i and i + 1, two independent QK^T chains, one softmax step over 32 keys and two
+      // PV k-steps -- halve the chain latency per chunk. Item i + 1 may be the unit's sentinel.
+      for (;;) {
+        const int sA = i % kNSt, sB = (i + 1) % kNSt;
+        if (L::kTags) while (ctag[sA] != int(i)) {}
+        mbar_wait(&full[sA], (i / kNSt) & 1);
+        const int nA = cmeta[sA];
+        if (nA <= 0) {
+          __syncwarp();
+          release(sA);
+          after_sentinel();
+          break;
+        }
+        if (L::kTags) while (ctag[sB] != int(i + 1)) {}
+        mbar_wait(&full[sB], ((i + 1) / kNSt) & 1);
+        const int nB = cmeta[sB];
+        const bool haveB = nB > 0;
+        float x[2][4];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          x[c][0] = x[c][1] = x[c][2] = x[c][3] = -CUDART_INF_F;
+          if (c == 1 && !haveB) continue;
+          const int nv = c ? nB : nA;
+          const uint8_t* kt = stages + (c ? sB : sA) * L::kStageBytes;
+          float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks) {  // A = K (16 keys x 16 dims)
+            const int mi = lane >> 3;
+            const int row = (lane & 7) + (mi & 1) * 8;
+            const int kc = ks * 2 + (mi >> 1);
+            uint32_t ka[4];
+            ldsm_x4(smem_u32(kt + (kc >> 3) * 2048 + sw128(row, kc & 7)), ka[0], ka[1], ka[2], ka[3]);
+            mma_bf16_16816(sacc, ka, qbf[ks][0], qbf[ks][1]);
+          }
+          x[c][0] = gq < nv ? sacc[0] * sl2 : -CUDART_INF_F;
+          x[c][1] = gq < nv ? sacc[1] * sl2 : -CUDART_INF_F;
+          x[c][2] = gq + 8 < nv ? sacc[2] * sl2 : -CUDART_INF_F;
+          x[c][3] = gq + 8 < nv ? sacc[3] * sl2 : -CUDART_INF_F;
+        }
+        float mx0 = fmaxf(fmaxf(x[0][0], x[0][2]), fmaxf(x[1][0], x[1][2]));
+        float mx1 = fmaxf(fmaxf(x[0][1], x[0][3]), fmaxf(x[1][1], x[1][3]));
+        const bool any_grow = __any_sync(0xffffffffu, mx0 > m_h[0] + 8.f || mx1 > m_h[1] + 8.f);
+        if (any_grow) {
+#pragma unroll
+          for (int off = 4; off < 32; off <<= 1) {
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+          }
+        }
+        const bool g0 = any_grow && mx0 > m_h[0] + 8.f, g1 = any_grow && mx1 > m_h[1] + 8.f;
+        const float mn0 = g0 ? mx0 : m_h[0], mn1 = g1 ? mx1 : m_h[1];
+        float pp[2][4];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          pp[c][0] = fast_exp2(x[c][0] - mn0);
+          pp[c][1] = fast_exp2(x[c][1] - mn1);
+          pp[c][2] = fast_exp2(x[c][2] - mn0);
+          pp[c][3] = fast_exp2(x[c][3] - mn1);
+        }
+        const float s0 = (pp[0][0] + pp[0][2]) + (pp[1][0] + pp[1][2]);
+        const float s1 = (pp[0][1] + pp[0][3]) + (pp[1][1] + pp[1][3]);
+        if (!any_grow) {
+          l_h[0] += s0;
+          l_h[1] += s1;
+        } else {
+          const float al0 = fast_exp2(m_h[0] - mn0), al1 = fast_exp2(m_h[1] - mn1);
+          m_h[0] = mn0;
+          m_h[1] = mn1;
+          l_h[0] = l_h[0] * al0 + s0;
+          l_h[1] = l_h[1] * al1 + s1;
+#pragma unroll
+          for (int n = 0; n < D / 16; ++n) {
+            o[n][0] *= al0;
+            o[n][1] *= al1;
+            o[n][2] *= al0;
+            o[n][3] *= al1;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (c == 1 && !haveB) continue;
+          const uint32_t pb0 = movmatrix_t(pack_bf16(pp[c][0] * vpre, pp[c][1] * vpre));
+          const uint32_t pb1 = movmatrix_t(pack_bf16(pp[c][2] * vpre, pp[c][3] * vpre));
+          const uint8_t* vt = stages + (c ? sB : sA) * L::kStageBytes + L::kTileBytes;
+#pragma unroll
+          for (int mt = 0; mt < D / 16; ++mt) {  // A = V^T (16 dims x 16 keys)
+            const int mi = lane >> 3;
+            const int key = (lane & 7) + (mi >> 1) * 8;
+            const int dc = 2 * mt + (mi & 1);
+            uint32_t va[4];
+            ldsm_x4_t(smem_u32(vt + (dc >> 3) * 2048 + sw128(key, dc & 7)), va[0], va[1], va[2], va[3]);
+            mma_bf16_16816(o[mt], va, pb0, pb1);
+          }
+        }
+        __syncwarp();
+        release(sA);
+        release(sB);
+        if (!haveB) {  // item i + 1 was the sentinel
+          i += 1;
+          after_sentinel();
+          break;
+        }
+        i += 2;
+      }
+    } else
     for (;; i += istep) {
       const int slot = i % kNSt;
       if (L::kTags) while (ctag[slot] != int(i)) {}  // this stage holds item i (depth % consumers != 0)
-        mbar_wait(&full[slot], (i / kNSt) & 1);
+      mbar_wait(&full[slot], (i / kNSt) & 1);
 #if HPA_DEC_DEBUG_RING
       if (dbg_tag[slot] != i) {
         if (lane == 0)
@@ -1621,7 +1734,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     for (;; i += istep) {
       const int slot = i % kNSt;
       if (L::kTags) while (ctag[slot] != int(i)) {}  // this stage holds item i (depth % consumers != 0)
-        mbar_wait(&full[slot], (i / kNSt) & 1);
+      mbar_wait(&full[slot], (i / kNSt) & 1);
 #if HPA_DEC_DEBUG_RING
       if (dbg_tag[slot] != i) {
         if (lane == 0)

@@ -779,7 +779,8 @@ std::vector<CGroup> find_cascade_groups(const hpa_cache_t* c, int32_t n, const i
   int64_t saved = 0, total = 0;
   for (const CGroup& g : out) saved += int64_t(g.mem.size() - 1) * g.rch;
   for (int32_t i = 0; i < n; ++i) total += c->seqs[seq_ids[i]].chunks;
-  if (3 * saved < total) out.clear();
+  static const double min_saved = std::getenv("HPA_CASC_MIN_SAVED") ? std::atof(std::getenv("HPA_CASC_MIN_SAVED")) : 1.0 / 3;
+  if (double(saved) < min_saved * double(total)) out.clear();
   return out;
 }
 
@@ -1806,7 +1807,8 @@ hpa_status_t plan_cascade(hpa_cache_t* c, int32_t n, const int32_t* seq_ids, std
   // fewer, longer pieces leave the group units on the critical path; more add partials)
   double work = 0;
   for (int32_t i = 0; i < n; ++i) work += double(std::max(0, ch[size_t(i)])) * Hkv;
-  for (const CGroup& g : groups) work += 1.75 * g.rch * Hkv;
+  static const double kappa = std::getenv("HPA_CASC_KAPPA") ? std::atof(std::getenv("HPA_CASC_KAPPA")) : 1.75;
+  for (const CGroup& g : groups) work += kappa * g.rch * Hkv;
   // The group units run first (longest first) and all have about one length, so their count
   // is kept just under a whole number k of CTA waves (320 units on 296 slots ran 1.3x slower
   // than 256): the smallest k whose pieces are no longer than the per-slot share of the work.
@@ -1817,7 +1819,7 @@ hpa_status_t plan_cascade(hpa_cache_t* c, int32_t n, const int32_t* seq_ids, std
   int32_t pk = 64;
   for (int32_t k = 1; k <= 64; ++k) {
     const int32_t p = std::max(1, k * slots / gh);
-    if (1.75 * rmax / p <= share || p >= 64) {
+    if (kappa * rmax / p <= share || p >= 64) {
       pk = std::min(64, p);
       break;
     }
@@ -1859,7 +1861,7 @@ hpa_status_t plan_cascade(hpa_cache_t* c, int32_t n, const int32_t* seq_ids, std
         w[4 + m] = g.mem[m];
         w[4 + kGroupMax + m] = sp[size_t(g.mem[m])] + pc;
       }
-      const double cost = 1.75 * (rep.pch[size_t(e1 - 1)] - (e0 ? rep.pch[size_t(e0 - 1)] : 0));
+      const double cost = kappa * (rep.pch[size_t(e1 - 1)] - (e0 ? rep.pch[size_t(e0 - 1)] : 0));
       for (int32_t h = 0; h < Hkv; ++h) list.emplace_back(-cost, int4{-2 - ri, seq_ids[g.mem[0]], h, 0});
     }
   }
