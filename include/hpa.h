@@ -221,8 +221,8 @@ hpa_status_t hpa_seq_compress(hpa_cache_t* c, int32_t seq_id, int32_t n_doc_rows
  * latent sets shared by hpa_latent_set_share and installed first) read that run once per
  * group of up to 32/G requests -- one work unit holds the G query rows of every member --
  * and each request's own remaining pages as usual; all partials merge in the combine. Same
- * result up to fp32 rounding order; bf16 token pages, G <= 8, runs of >= 4 chunks
- * (hpa_set_decode_cascade switches it off). */
+ * result up to fp32 rounding order; bf16 or fp8 token pages, G <= 8, runs of >= 4 chunks that
+ * save >= 1/3 of the batch's reads (hpa_set_decode_cascade switches it off). */
 hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
                         const void* q, void* out, float softmax_scale, hpa_stream_t stream);
 

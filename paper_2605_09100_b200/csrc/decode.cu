@@ -582,7 +582,8 @@ struct PDecodeSmem {
   static constexpr int kBlk8 = 16 * D + 64;
   static constexpr int kStageBytes =
       F32 ? (((2 * kTileBytes > 4 * kBlk8 ? 2 * kTileBytes : 4 * kBlk8) + 1023) & ~1023) : 2 * kTileBytes;
-  static constexpr int kStages = F32 ? (D == 128 ? HPA_DEC_F32_STAGES : 12) : (CS ? HPA_DEC_CS_STAGES : kNSt);
+  static constexpr int kStages =
+      F32 ? (CS ? 8 : (D == 128 ? HPA_DEC_F32_STAGES : 12)) : (CS ? HPA_DEC_CS_STAGES : kNSt);
   // a depth that is not a multiple of the consumer count puts successive items of one slot on
   // different consumers, and a consumer could then take the slot's previous phase of the same
   // parity for its item (mbarrier-parity ABA): every stage then carries its item index (ctag),
@@ -649,7 +650,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
                          const DecodeArgs a, const __grid_constant__ AppendParams<NA> ap) {
   static_assert(!F32 || (SW && NA == 1 && HPA_FP8_KSWZ && HPA_FP8_VPAIR && !HPA_FP8_F16 && !HPA_DEC_PAIR),
                 "32-row fp8 chunks: swapped consumers with the register-direct fp8 operands only");
-  static_assert(!CS || (SW && NA == 1 && !F32 && !HPA_DEC_PAIR), "cascade units: swapped bf16 consumers only");
+  static_assert(!CS || (SW && NA == 1 && !HPA_DEC_PAIR), "cascade units: swapped consumers only");
   using L = PDecodeSmem<D, F32, CS>;
   constexpr int kNSt = L::kStages;  // ring depth of this variant
   extern __shared__ __align__(1024) uint8_t smem_pd[];
@@ -2043,10 +2044,14 @@ cudaError_t launch_persistent(const CUtensorMap& tm_k, const CUtensorMap& tm_v, 
   const int smem = PDecodeSmem<D>::bytes(a.G);
   const int grid = std::max(1, std::min(a.n_units, decode_slots(D, a.G)));
   if constexpr (NA == 1) {
-    if (HPA_DEC_F32 && a.fp8 && a.G <= 8 && HPA_DEC_SWAP)  // fp8 token pages: 32-row fp8 chunks
+    if (HPA_DEC_F32 && a.fp8 && a.G <= 8 && HPA_DEC_SWAP) {  // fp8 token pages: 32-row fp8 chunks
+      if (a.groups)  // with cascade group units
+        return launch_pdl(decode_persistent_kernel<D, true, 1, true, true>, dim3(grid), dim3((kNCons + 2) * 32),
+                          PDecodeSmem<D, true, true>::bytes(a.G), s, tm_k, tm_v, a, p);
       return launch_pdl(decode_persistent_kernel<D, true, 1, true>, dim3(grid), dim3((kNCons + 2) * 32),
                         PDecodeSmem<D, true>::bytes(a.G), s, tm_k, tm_v, a, p);
-    if (a.groups) {  // cascade group units in the plan (bf16, G <= 8)
+    }
+    if (a.groups) {  // cascade group units in the plan (bf16 token pages here, G <= 8)
       if (a.fp8 || a.G > 8 || !HPA_DEC_SWAP || HPA_DEC_PAIR) return cudaErrorInvalidValue;
       return launch_pdl(decode_persistent_kernel<D, true, 1, false, true>, dim3(grid), dim3((kNCons + 2) * 32),
                         PDecodeSmem<D, false, true>::bytes(a.G), s, tm_k, tm_v, a, p);
@@ -2146,7 +2151,13 @@ cudaError_t set_cascade_attrs() {
                                 cap(PDecodeSmem<128, false, true>::bytes(8)))) != cudaSuccess ||
       (e = cudaFuncSetAttribute(decode_persistent_kernel<64, true, 1, false, true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                cap(PDecodeSmem<64, false, true>::bytes(8)))) != cudaSuccess)
+                                cap(PDecodeSmem<64, false, true>::bytes(8)))) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(decode_persistent_kernel<128, true, 1, true, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cap(PDecodeSmem<128, true, true>::bytes(8)))) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(decode_persistent_kernel<64, true, 1, true, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cap(PDecodeSmem<64, true, true>::bytes(8)))) != cudaSuccess)
     return e;
   return cudaSuccess;
 }

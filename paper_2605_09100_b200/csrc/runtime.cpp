@@ -720,7 +720,7 @@ constexpr int32_t kCascadeMinChunks = 4;  // shorter shared runs are decoded per
 std::vector<CGroup> find_cascade_groups(const hpa_cache_t* c, int32_t n, const int32_t* seq_ids) {
   std::vector<CGroup> out;
   const int32_t G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
-  if (!c->cascade || c->fp8 || G > 8 || !decode_persistent()) return out;
+  if (!c->cascade || G > 8 || !decode_persistent()) return out;
   std::vector<std::pair<int32_t, int32_t>> fp;  // (first page, batch index)
   fp.reserve(size_t(n));
   for (int32_t i = 0; i < n; ++i) {

@@ -17,7 +17,10 @@ cases = os.environ.get("CASES", "64:1024:1024,64:4096:1024,64:16384:1024,256:409
 for cs in cases.split(","):
     B, n_prompt, n_own = (int(x) for x in cs.split(":"))
     pages = n_prompt // P + B * (n_own // P + 2) + 64
-    cache = Cache(1, 32, 8, 128, P, pages, B + 1, (n_prompt + n_own) // P + 4, 0, 99)
+    if os.environ.get("DTYPE", "bf16") == "fp8":  # token pages in the fp8 pool (NEXT-4c)
+        cache = Cache(1, 32, 8, 128, P, 64, B + 1, (n_prompt + n_own) // P + 4, 0, 99, "fp8", pages)
+    else:
+        cache = Cache(1, 32, 8, 128, P, pages, B + 1, (n_prompt + n_own) // P + 4, 0, 99)
     src = cache.seq_create()
     kp = torch.randn((1, n_prompt, 8, 128), generator=g, device="cuda").to(torch.bfloat16)
     cache.append_kv([src], [n_prompt], kp, kp)
@@ -43,6 +46,6 @@ for cs in cases.split(","):
         if on:
             info = cache.decode_plan_info()
     off, on = min(res[False]), min(res[True])
-    print(f"B={B} prompt={n_prompt} own={n_own}: plain {off:.1f} us, cascade {on:.1f} us (x{off / on:.2f}), "
+    print(f"{os.environ.get('DTYPE', 'bf16')} B={B} prompt={n_prompt} own={n_own}: plain {off:.1f} us, cascade {on:.1f} us (x{off / on:.2f}), "
           f"plan {info}", flush=True)
     cache.close()

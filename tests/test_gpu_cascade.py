@@ -152,18 +152,25 @@ def test_cascade_forced_splits_and_partial_api():
     check_close(out, _ref(p, seqs, q, 1), "append_decode cascade")
 
 
-def test_cascade_off_for_fp8_and_large_groups_of_one():
-    """fp8 token caches never plan group units (decode stays correct); a batch without two
-    requests sharing a first page plans none either."""
-    shape = _shape(32, 8, 128, 16)
-    p = Pair(shape, 2048, 12, 300, seed=3, token_fp8=True, num_token_pages=2048)
-    src = p.build([("tokens", 600)])
-    seqs = [src] + [_fork(p, src, 600) for _ in range(4)]
+@pytest.mark.parametrize("hq,hkv,d,P", [(32, 8, 128, 16), (16, 2, 64, 32), (8, 1, 128, 64)])
+def test_cascade_fp8_token_pages(hq, hkv, d, P):
+    """fp8 token pages (NEXT-4c) with a forked prompt: group units on the 32-row fp8 kernel,
+    latent (bf16) and token (fp8) chunks in the shared run, own fp8 rows after it."""
+    shape = _shape(hq, hkv, d, P)
+    G = hq // hkv
+    p = Pair(shape, 2048, 24, 300, seed=3, token_fp8=True, num_token_pages=2048)
+    src = p.build([("latent", 64), ("tokens", 20 * P + 7)])
+    seqs = [src] + [_fork(p, src, 64 + 20 * P + 7) for _ in range(32 // G + 2)]
+    for i, s in enumerate(seqs):
+        p.tokens([s], [1 + (5 * i) % (2 * P)])
     q = p.queries(len(seqs))
-    out = p.cache.decode(0, seqs, q.cuda())
-    torch.cuda.synchronize()
-    assert p.cache.decode_plan_info()["group_units"] == 0
-    check_close(out, _ref(p, seqs, q, 0), "fp8 forks")
+    for layer in (0, 1):
+        info = _decode_both(p, seqs, q, layer, f"fp8 forks hq={hq} hkv={hkv} d={d} P={P} L={layer}")
+        assert info["group_units"] > 0, info
+
+
+def test_cascade_none_without_sharing():
+    """A batch without two requests sharing a first page plans no group units."""
     p2 = Pair(_shape(32, 8, 128, 16), 2048, 12, 300, seed=4)
     seqs2 = [p2.build([("tokens", 300 + 50 * i)]) for i in range(5)]
     q2 = p2.queries(5)
