@@ -980,6 +980,23 @@ def bench_next(torch, Cache, shape, dev, stream, pk, max_over_ranks):
     ms_off, plan_off = time_decode(False)
     ms, plan = time_decode(True)
     lens = [cache.seq_info(s)[0] for s in seqs]
+
+    def time_steps(cascade, n=20):  # the serving step: hpa_append_decode (append + decode, fused)
+        cache.set_decode_cascade(cascade)
+        kn = torch.randn((n + 3, 1, B, 8, 128), generator=g, device=f"cuda:{dev}").to(torch.bfloat16)
+        for i in range(3):
+            cache.append_decode(0, ids, kn[i], kn[i], q, o)
+        torch.cuda.synchronize(dev)
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for i in range(n):
+            cache.append_decode(0, ids, kn[3 + i], kn[3 + i], q, o)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / n
+
+    step_off = time_steps(False)
+    step_on = time_steps(True)
     row_bytes = shape.num_kv_heads * shape.head_dim * 2 * 2  # K + V of one row, all KV heads
     groups = -(-B // (32 // (shape.num_q_heads // shape.num_kv_heads)))
     phys = (groups * n_prompt + B * n_own) * row_bytes + 2 * B * shape.num_q_heads * shape.head_dim * 2
@@ -991,7 +1008,8 @@ def bench_next(torch, Cache, shape, dev, stream, pk, max_over_ranks):
         "logical_gbs": round(decode_bytes(lens, shape) / (ms / 1e3) / 1e9, 1),
         "physical_bytes": phys, "physical_gbs": round(phys / (ms / 1e3) / 1e9, 1),
         "physical_frac_of_copy_peak": round(phys / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 4),
-        "logical_gbs_cascade_off": round(decode_bytes(lens, shape) / (ms_off / 1e3) / 1e9, 1)}
+        "logical_gbs_cascade_off": round(decode_bytes(lens, shape) / (ms_off / 1e3) / 1e9, 1),
+        "append_decode_step_ms": round(step_on, 4), "append_decode_step_ms_cascade_off": round(step_off, 4)}
     cache.close()
     # NEXT-3: LMAG-style replacement from pinned host payloads (copy stream) overlapped with decode
     B = 256

@@ -650,7 +650,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
                          const DecodeArgs a, const __grid_constant__ AppendParams<NA> ap) {
   static_assert(!F32 || (SW && NA == 1 && HPA_FP8_KSWZ && HPA_FP8_VPAIR && !HPA_FP8_F16 && !HPA_DEC_PAIR),
                 "32-row fp8 chunks: swapped consumers with the register-direct fp8 operands only");
-  static_assert(!CS || (SW && NA == 1 && !HPA_DEC_PAIR), "cascade units: swapped consumers only");
+  static_assert(!CS || (SW && !HPA_DEC_PAIR), "cascade units: swapped consumers only");
   using L = PDecodeSmem<D, F32, CS>;
   constexpr int kNSt = L::kStages;  // ring depth of this variant
   extern __shared__ __align__(1024) uint8_t smem_pd[];
@@ -739,8 +739,11 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
       // fused append (NA > 1): the request's last entry and entry count come from the tail
       // record; the device table still holds the values from before this step's append
       int4 tl = make_int4(0, 0, 0, 0);
-      if constexpr (NA > 1) tl = ap.tail[ur.x];
-      const int ne = NA > 1 ? tl.x : a.t.n_entries[seq];
+      const bool gunit = CS && ur.x <= -2;  // cascade group unit: no tail record (its run is shared)
+      if constexpr (NA > 1) {
+        if (!gunit) tl = ap.tail[ur.x];
+      }
+      const int ne = NA > 1 && !gunit ? tl.x : a.t.n_entries[seq];
       int e0, e1;
       if (CS && ur.x <= -2) {  // cascade group piece: a fixed entry range of the shared run
         const int32_t* gr = a.groups + int64_t(-2 - ur.x) * kGroupRec;
@@ -757,7 +760,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         const int cnt = min(31, e1 - e);
         const int last = e + cnt >= e1;
         if constexpr (NA > 1) {
-          if (last && e1 == ne) {
+          if (last && e1 == ne && !gunit) {
             // this unit holds the new row of (request, head h): write it into its pool slot
             // (every layer) before the piece that loads its tile is published; the proxy
             // fence orders these generic stores before the producer's TMA reads of the tile
@@ -2057,7 +2060,11 @@ cudaError_t launch_persistent(const CUtensorMap& tm_k, const CUtensorMap& tm_v, 
                         PDecodeSmem<D, false, true>::bytes(a.G), s, tm_k, tm_v, a, p);
     }
   } else {
-    if (a.groups) return cudaErrorInvalidValue;  // the fused append never runs a cascade plan
+    if (a.groups) {  // fused append with cascade group units (bf16 token pages)
+      if (a.fp8 || a.G > 8 || !HPA_DEC_SWAP || HPA_DEC_PAIR) return cudaErrorInvalidValue;
+      return launch_pdl(decode_persistent_kernel<D, true, NA, false, true>, dim3(grid), dim3((kNCons + 2) * 32),
+                        PDecodeSmem<D, false, true>::bytes(a.G), s, tm_k, tm_v, a, p);
+    }
   }
   if (a.G <= 8 && HPA_DEC_SWAP)
     return launch_pdl(decode_persistent_kernel<D, true, NA>, dim3(grid), dim3((kNCons + 2) * 32), smem, s, tm_k,
@@ -2127,6 +2134,15 @@ cudaError_t set_persistent_attrs() {
       (e = cudaFuncSetAttribute(decode_persistent_kernel<64, true, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 cap(PDecodeSmem<64>::bytes(8)))) != cudaSuccess)
     return e;
+  if constexpr (NA > 1) {  // fused append with cascade group units
+    if ((e = cudaFuncSetAttribute(decode_persistent_kernel<128, true, NA, false, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  cap(PDecodeSmem<128, false, true>::bytes(8)))) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(decode_persistent_kernel<64, true, NA, false, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  cap(PDecodeSmem<64, false, true>::bytes(8)))) != cudaSuccess)
+      return e;
+  }
   return cudaSuccess;
 }
 

@@ -1713,9 +1713,7 @@ hpa_status_t hpa_append_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, co
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // fp8 token pages quantize on append (copy_kernels.cu); larger batches exceed the kernel's
   // parameter block: both take the two-launch path
-  // (a batch with cascade groups also takes it: the fused kernel has no group units)
-  const bool fuse = !c->fp8 && decode_persistent() && n_seqs <= kAppendFuseMax &&
-                    find_cascade_groups(c, n_seqs, seq_ids).empty();
+  const bool fuse = !c->fp8 && decode_persistent() && n_seqs <= kAppendFuseMax;
   if (fuse) {
     if (hpa_status_t st = ship(c, s, {}, {}, 0)) return st;  // earlier calls' table words first
   }
@@ -1942,7 +1940,7 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
   if (decode_persistent()) {
     if (Hkv > 255) return fail(HPA_ERR_UNSUPPORTED, "persistent decode supports H_kv <= 255");
     std::vector<CGroup> groups;
-    if (!ap) groups = find_cascade_groups(c, n_seqs, seq_ids);  // (the fused append never sees one)
+    groups = find_cascade_groups(c, n_seqs, seq_ids);
     std::vector<int32_t> sp;
     std::vector<int32_t> key;
     if (!groups.empty()) {
