@@ -779,7 +779,7 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         if (lane == 0) {
           item = make_int2(ur.x, h | (split << 8) | (cnt << 16) | (first << 24) | (last << 25));
         } else if (lane <= cnt) {
-          const bool tail_entry = NA > 1 && e + lane == ne;
+          const bool tail_entry = NA > 1 && !gunit && e + lane == ne;  // (a group unit has no tail record)
           const int page = tail_entry ? tl.y : bt[e + lane - 1];
           const int mv = tail_entry ? tl.z : mt[e + lane - 1];
           const int f8 = a.fp8 && !(mv & kMetaLatent);  // fp8 token page (NEXT-4c)

@@ -733,41 +733,73 @@ std::vector<CGroup> find_cascade_groups(const hpa_cache_t* c, int32_t n, const i
     size_t b = a;
     while (b < fp.size() && fp[b].first == fp[a].first) ++b;
     if (b - a >= 2) {
-      const Seq& rep = c->seqs[seq_ids[fp[a].second]];
-      std::vector<std::pair<int32_t, int32_t>> ls;  // (-lcp with the bucket's first, batch index)
-      for (size_t k = a; k < b; ++k)
-        ls.emplace_back(-(k == a ? int32_t(rep.pages.size()) : lcp_entries(rep, c->seqs[seq_ids[fp[k].second]])),
-                        fp[k].second);
-      std::sort(ls.begin(), ls.end());
-      // the members taken (longest shared prefixes first) and the run they all share, chosen to
-      // save the most chunk reads: cnt members reading rch chunks each vs once per group
-      int64_t best_gain = 0;
-      size_t best_cnt = 0;
-      for (size_t cnt = 2; cnt <= ls.size(); ++cnt) {
-        const int32_t r = -ls[cnt - 1].first;
-        if (r <= 0) break;
-        const int32_t rch = rep.pch[size_t(r - 1)];
-        const int64_t gain = int64_t(int64_t(cnt) - (int64_t(cnt) + cap - 1) / cap) * rch;
-        if (rch >= kCascadeMinChunks && gain > best_gain) {
-          best_gain = gain;
-          best_cnt = cnt;
+      // Members in lexicographic order of their tables: then the entries shared by members j..k
+      // are exactly min(adjacent LCPs between them), and groups are runs of that order.
+      std::vector<int32_t> mem;
+      for (size_t k = a; k < b; ++k) mem.push_back(fp[k].second);
+      auto lcp_of = [&](int32_t x, int32_t y) { return lcp_entries(c->seqs[seq_ids[x]], c->seqs[seq_ids[y]]); };
+      std::sort(mem.begin(), mem.end(), [&](int32_t x, int32_t y) {
+        const Seq& X = c->seqs[seq_ids[x]];
+        const Seq& Y = c->seqs[seq_ids[y]];
+        const int32_t l = lcp_of(x, y);
+        const int32_t nx = int32_t(X.pages.size()), ny = int32_t(Y.pages.size());
+        if (l == nx || l == ny) return nx != ny ? nx < ny : x < y;
+        if (X.pages[size_t(l)] != Y.pages[size_t(l)]) return X.pages[size_t(l)] < Y.pages[size_t(l)];
+        return X.meta[size_t(l)] < Y.meta[size_t(l)];
+      });
+      const size_t m = mem.size();
+      std::vector<int32_t> adj(m - 1);
+      for (size_t k = 0; k + 1 < m; ++k) adj[k] = lcp_of(mem[k], mem[k + 1]);
+      // chunks in the first r entries of member k (which has at least r entries)
+      auto chunks_of = [&](int32_t r, size_t k) { return r > 0 ? c->seqs[seq_ids[mem[k]]].pch[size_t(r - 1)] : 0; };
+      // the threshold t (entries) that saves the most chunk reads: runs of adjacent LCP >= t,
+      // each cut into groups of <= cap members sharing the run's minimum LCP
+      auto plan_t = [&](int32_t t, std::vector<CGroup>* outg) {
+        int64_t saved = 0;
+        size_t j = 0;
+        while (j + 1 < m) {
+          if (adj[j] < t) {
+            ++j;
+            continue;
+          }
+          size_t k = j;
+          while (k + 1 < m && adj[k] >= t) ++k;  // members j..k share >= t entries
+          for (size_t g0 = j; g0 <= k; g0 += size_t(cap)) {
+            const size_t g1 = std::min(k, g0 + size_t(cap) - 1);
+            if (g1 == g0) break;  // a lone member reads its run itself
+            int32_t r = adj[g0];
+            for (size_t q = g0; q < g1; ++q) r = std::min(r, adj[q]);
+            const int32_t rch = chunks_of(r, g0);
+            if (rch < kCascadeMinChunks) continue;
+            saved += int64_t(g1 - g0) * rch;
+            if (outg) {
+              CGroup g;
+              g.r = r;
+              g.rch = rch;
+              g.mem.assign(mem.begin() + int64_t(g0), mem.begin() + int64_t(g1) + 1);
+              std::sort(g.mem.begin(), g.mem.end());
+              outg->push_back(std::move(g));
+            }
+          }
+          j = k + 1;
+        }
+        return saved;
+      };
+      int64_t best = 0;
+      int32_t best_t = -1;
+      std::vector<int32_t> ts;
+      for (size_t k = 0; k + 1 < m; ++k)
+        if (adj[k] > 0 && chunks_of(adj[k], k) >= kCascadeMinChunks) ts.push_back(adj[k]);
+      std::sort(ts.begin(), ts.end());
+      ts.erase(std::unique(ts.begin(), ts.end()), ts.end());
+      for (int32_t t : ts) {
+        const int64_t sv = plan_t(t, nullptr);
+        if (sv > best) {
+          best = sv;
+          best_t = t;
         }
       }
-      if (best_cnt >= 2) {
-        const int32_t r = -ls[best_cnt - 1].first;
-        std::vector<int32_t> mem;
-        for (size_t k = 0; k < best_cnt; ++k) mem.push_back(ls[k].second);
-        std::sort(mem.begin(), mem.end());
-        for (size_t j = 0; j < mem.size(); j += size_t(cap)) {
-          const size_t e = std::min(mem.size(), j + size_t(cap));
-          if (e - j < 2) break;  // a lone member reads its run itself
-          CGroup g;
-          g.r = r;
-          g.rch = rep.pch[size_t(r - 1)];
-          g.mem.assign(mem.begin() + j, mem.begin() + e);
-          out.push_back(std::move(g));
-        }
-      }
+      if (best_t > 0) plan_t(best_t, &out);
     }
     a = b;
   }
@@ -780,6 +812,10 @@ std::vector<CGroup> find_cascade_groups(const hpa_cache_t* c, int32_t n, const i
   for (const CGroup& g : out) saved += int64_t(g.mem.size() - 1) * g.rch;
   for (int32_t i = 0; i < n; ++i) total += c->seqs[seq_ids[i]].chunks;
   static const double min_saved = std::getenv("HPA_CASC_MIN_SAVED") ? std::atof(std::getenv("HPA_CASC_MIN_SAVED")) : 1.0 / 3;
+  static const bool trace = std::getenv("HPA_CASC_TRACE") != nullptr;
+  if (trace && !out.empty())
+    std::fprintf(stderr, "cascade: %zu groups, saved %lld of %lld chunk reads (min %.3f)\n", out.size(),
+                 (long long)saved, (long long)total, min_saved);
   if (double(saved) < min_saved * double(total)) out.clear();
   return out;
 }
@@ -1713,7 +1749,8 @@ hpa_status_t hpa_append_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, co
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // fp8 token pages quantize on append (copy_kernels.cu); larger batches exceed the kernel's
   // parameter block: both take the two-launch path
-  const bool fuse = !c->fp8 && decode_persistent() && n_seqs <= kAppendFuseMax;
+  static const bool no_fuse = std::getenv("HPA_NO_FUSE") != nullptr;  // A/B knob: the two-launch step
+  const bool fuse = !c->fp8 && decode_persistent() && n_seqs <= kAppendFuseMax && !no_fuse;
   if (fuse) {
     if (hpa_status_t st = ship(c, s, {}, {}, 0)) return st;  // earlier calls' table words first
   }

@@ -29,6 +29,18 @@ def _fork(p, src, n):
     return d
 
 
+def _valid_cuts(orc, s):
+    """Fork cuts the reading allows (A21): any row boundary except strictly inside a latent set."""
+    cuts, pos = [0], 0
+    for sg in orc.seqs[s]:
+        if sg.kind == "token":
+            cuts += list(range(pos + 1, pos + sg.rows + 1))
+        else:
+            cuts.append(pos + sg.rows)
+        pos += sg.rows
+    return sorted(set(cuts))
+
+
 def _ref(p, seqs, q, layer):
     return np.stack([attend(f64(q[i:i + 1]), *p.orc.logical_kv(s, layer), p.shape.scale)[0]
                      for i, s in enumerate(seqs)])
@@ -201,3 +213,62 @@ def test_cascade_fuzz():
         _decode_both(p, batch, q, it % 2, f"fuzz {it}")
         grow = [s for s in live if rng.random() < 0.5]
         p.tokens(grow, [int(rng.integers(1, 30)) for _ in grow])
+
+
+@pytest.mark.parametrize("seed", range(2))
+def test_cascade_step_fuzz(seed):
+    """200 random ops on a fork tree -- forks at random cuts, fused decode steps
+    (hpa_append_decode) on random subsets, bulk appends, latent replacement in forked requests
+    (copy-on-write of shared latent pages) or new latent sets, releases -- with cascade decode vs
+    plain vs the oracle every 20 ops; the cascade must have run in some of the checks."""
+    import random
+
+    from paper_2605_09100_b200 import HPAError
+    import os
+    rng = random.Random(700 + seed)
+    shape = _shape(16, 4, 128, 16, L=1)
+    p = Pair(shape, 6000, 24, 300, seed=seed)
+    if os.environ.get("HPA_TEST_CASCADE_OFF"):
+        p.cache.set_decode_cascade(False)
+    roots = [p.build([("latent", 128), ("tokens", rng.randint(300, 900))]) for _ in range(2)]
+    live = list(roots)
+    grouped = 0
+    for step in range(200):
+        op = rng.random()
+        try:
+            if op < 0.25 and len(live) < 24:
+                src = rng.choice(live)
+                cuts = [c for c in _valid_cuts(p.orc, src) if c > 128]
+                if cuts:
+                    live.append(_fork(p, src, rng.choice(cuts)))
+            elif op < 0.55 and live:
+                ss = sorted(rng.sample(live, rng.randint(1, len(live))))
+                k, v = p.draw.tokens(shape, len(ss))
+                q = p.queries(len(ss))
+                out = p.cache.append_decode(0, ss, k.cuda(), v.cuda(), q.cuda())
+                for i, s in enumerate(ss):
+                    p.orc.append(s, f64(k[:, i:i + 1]), f64(v[:, i:i + 1]))
+                torch.cuda.synchronize()
+                check_close(out, _ref(p, ss, q, 0), f"fused step seed {seed} op {step}")
+            elif op < 0.75 and live:
+                ss = rng.sample(live, rng.randint(1, len(live)))
+                p.tokens(ss, [rng.randint(1, 40) for _ in ss])
+            elif op < 0.85 and live:
+                s = rng.choice(live)
+                ids = [sg.set_id for sg in p.orc.seqs[s] if sg.kind == "latent"]
+                if ids and rng.random() < 0.3:  # same size: in place, or copy-on-write if shared
+                    p.latent(s, 128, set_id=rng.choice(ids))
+                else:  # a new set at the end of the request
+                    p.latent(s, rng.choice([16, 40, 128]))
+            elif op < 0.92 and len(live) > 2:
+                s = live.pop(rng.randrange(len(live)))
+                p.cache.seq_release(s)
+                p.orc.release(s)
+        except HPAError as e:
+            assert e.name in ("HPA_ERR_OUT_OF_PAGES", "HPA_ERR_SEQ_CAPACITY"), e
+        if step % 20 == 19 and live:
+            batch = sorted(live)
+            q = p.queries(len(batch))
+            info = _decode_both(p, batch, q, 0, f"step fuzz seed {seed} op {step}")
+            grouped += info["group_units"] > 0
+    assert grouped > 0
