@@ -215,19 +215,21 @@ def test_cascade_fuzz():
         p.tokens(grow, [int(rng.integers(1, 30)) for _ in grow])
 
 
-@pytest.mark.parametrize("seed", range(2))
-def test_cascade_step_fuzz(seed):
+@pytest.mark.parametrize("seed,hq,hkv,d,P,fp8,need", [(0, 16, 4, 128, 16, False, True), (1, 16, 4, 128, 16, False, True),
+                                                       (2, 8, 8, 64, 32, False, True), (3, 32, 4, 128, 64, False, False),
+                                                       (4, 16, 4, 128, 16, True, False), (5, 8, 1, 128, 16, True, True)])
+def test_cascade_step_fuzz(seed, hq, hkv, d, P, fp8, need):
     """200 random ops on a fork tree -- forks at random cuts, fused decode steps
     (hpa_append_decode) on random subsets, bulk appends, latent replacement in forked requests
     (copy-on-write of shared latent pages) or new latent sets, releases -- with cascade decode vs
-    plain vs the oracle every 20 ops; the cascade must have run in some of the checks."""
+    plain vs the oracle every 20 ops; in most cases the cascade must have run in some checks."""
     import random
 
     from paper_2605_09100_b200 import HPAError
     import os
     rng = random.Random(700 + seed)
-    shape = _shape(16, 4, 128, 16, L=1)
-    p = Pair(shape, 6000, 24, 300, seed=seed)
+    shape = _shape(hq, hkv, d, P, L=1)
+    p = Pair(shape, 6000, 24, 4800 // P, seed=seed, token_fp8=fp8, num_token_pages=6000 if fp8 else 0)
     if os.environ.get("HPA_TEST_CASCADE_OFF"):
         p.cache.set_decode_cascade(False)
     roots = [p.build([("latent", 128), ("tokens", rng.randint(300, 900))]) for _ in range(2)]
@@ -271,4 +273,5 @@ def test_cascade_step_fuzz(seed):
             q = p.queries(len(batch))
             info = _decode_both(p, batch, q, 0, f"step fuzz seed {seed} op {step}")
             grouped += info["group_units"] > 0
-    assert grouped > 0
+    # (the random trees of some cases never pass the 1/3-of-reads rule; the others must cascade)
+    assert grouped > 0 or not need
