@@ -533,6 +533,9 @@ def run_ours(args):
                 "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h,
                 "ms_per_step": round(e2e_ms, 5)},
         "gpu_launches": launches,
+        # the value is one layer's decode; a Qwen3-8B token step runs 36 of them
+        "model_equivalent": {"layers": 36, "tokens_per_s": round(value / 36, 1),
+                             "note": "decode attention only (one call per layer), no other layer work"},
         "roofline": {"bound": "hbm", "kernel": "hpa_append_decode per call: fused append + split decode (+ combine)",
                      "timing": "region B: an event pair around each call (region A, the value, has none)",
                      "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
