@@ -506,6 +506,41 @@ def test_shared_latent_sets_refcount_and_copy_on_write():
 
 
 # ----------------------------------------------------------------------------- NEXT-3: host staging
+def test_install_from_host_payloads_scattered():
+    """hpa_latent_set_install_host with payloads of different sizes, some back to back in one
+    host buffer (coalesced into one copy) and some in separate buffers, in any order."""
+    import ctypes
+
+    from paper_2605_09100_b200._lib import LIB, check
+    shape = Shape(2, 32, 8, 128, 16)
+    p = Pair(shape, num_pages=2048, max_seqs=8, max_pages_per_seq=256)
+    seqs = [p.build([("latent", 128), ("tokens", 100 + 30 * i)]) for i in range(5)]
+    ms = [128, 40, 128, 16, 72]
+    kvs = [p.draw.latent(shape, m) for m in ms]                    # [L][2][m][Hkv][d]
+    joint = torch.cat([kvs[0].reshape(-1), kvs[1].reshape(-1)]).pin_memory()  # payloads 0, 1 back to back
+    sep = [kvs[i].contiguous().pin_memory() for i in (2, 3, 4)]
+    ptrs = [joint.data_ptr(), joint.data_ptr() + kvs[0].numel() * 2] + [t.data_ptr() for t in sep]
+    order = [3, 0, 1, 4, 2]                                         # request order != buffer order
+    ids = np.array([seqs[i] for i in order], np.int32)
+    sids = np.full(5, -1, np.int32)
+    mrows = np.array([ms[i] for i in order], np.int32)
+    hp = (ctypes.c_void_p * 5)(*[ptrs[i] for i in order])
+    out = np.zeros(5, np.int32)
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    check(LIB.hpa_latent_set_install_host(p.cache._h, 5, ids.ctypes.data_as(i32p), sids.ctypes.data_as(i32p),
+                                          mrows.ctypes.data_as(i32p), hp,
+                                          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream),
+                                          out.ctypes.data_as(i32p)))
+    for k, i in enumerate(order):
+        assert out[k] == p.orc.install(seqs[i], -1, f64(kvs[i]))
+    torch.cuda.synchronize()
+    for layer in (0, 1):
+        for s in seqs:
+            k1, v1 = p.orc.logical_kv(s, layer)
+            k2, v2 = p.cache.export_logical_kv(layer, s)
+            assert np.array_equal(k1, f64(k2)) and np.array_equal(v1, f64(v2))
+
+
 def test_install_from_host_payloads():
     """hpa_latent_set_install_host (pinned host payloads, internal copy stream) installs the
     same bits as the device-payload path; repeated calls reuse the staging buffer while
