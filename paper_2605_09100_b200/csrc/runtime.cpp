@@ -733,20 +733,34 @@ std::vector<CGroup> find_cascade_groups(const hpa_cache_t* c, int32_t n, const i
     size_t b = a;
     while (b < fp.size() && fp[b].first == fp[a].first) ++b;
     if (b - a >= 2) {
-      // Members in lexicographic order of their tables: then the entries shared by members j..k
-      // are exactly min(adjacent LCPs between them), and groups are runs of that order.
+      // Members ordered so that those sharing long prefixes are adjacent: by their common
+      // prefix with the bucket's longest table (desc), then by the entry where they leave it
+      // (in a fork tree: the fork point, then the branch). Any order is correct -- members j..k
+      // share min(adjacent LCPs) entries -- this one makes the shared runs long.
       std::vector<int32_t> mem;
       for (size_t k = a; k < b; ++k) mem.push_back(fp[k].second);
       auto lcp_of = [&](int32_t x, int32_t y) { return lcp_entries(c->seqs[seq_ids[x]], c->seqs[seq_ids[y]]); };
-      std::sort(mem.begin(), mem.end(), [&](int32_t x, int32_t y) {
+      int32_t ref = mem[0];
+      for (int32_t x : mem)
+        if (c->seqs[seq_ids[x]].pages.size() > c->seqs[seq_ids[ref]].pages.size()) ref = x;
+      struct Key {
+        int32_t lcp, page, meta, idx;
+      };
+      std::vector<Key> keys;
+      keys.reserve(mem.size());
+      for (int32_t x : mem) {
         const Seq& X = c->seqs[seq_ids[x]];
-        const Seq& Y = c->seqs[seq_ids[y]];
-        const int32_t l = lcp_of(x, y);
-        const int32_t nx = int32_t(X.pages.size()), ny = int32_t(Y.pages.size());
-        if (l == nx || l == ny) return nx != ny ? nx < ny : x < y;
-        if (X.pages[size_t(l)] != Y.pages[size_t(l)]) return X.pages[size_t(l)] < Y.pages[size_t(l)];
-        return X.meta[size_t(l)] < Y.meta[size_t(l)];
+        const int32_t l = x == ref ? int32_t(X.pages.size()) : lcp_of(ref, x);
+        const bool more = l < int32_t(X.pages.size());
+        keys.push_back({l, more ? X.pages[size_t(l)] : -1, more ? X.meta[size_t(l)] : -1, x});
+      }
+      std::sort(keys.begin(), keys.end(), [](const Key& x, const Key& y) {
+        if (x.lcp != y.lcp) return x.lcp > y.lcp;
+        if (x.page != y.page) return x.page < y.page;
+        if (x.meta != y.meta) return x.meta < y.meta;
+        return x.idx < y.idx;
       });
+      for (size_t k = 0; k < keys.size(); ++k) mem[k] = keys[k].idx;
       const size_t m = mem.size();
       std::vector<int32_t> adj(m - 1);
       for (size_t k = 0; k + 1 < m; ++k) adj[k] = lcp_of(mem[k], mem[k + 1]);
@@ -792,6 +806,12 @@ std::vector<CGroup> find_cascade_groups(const hpa_cache_t* c, int32_t n, const i
         if (adj[k] > 0 && chunks_of(adj[k], k) >= kCascadeMinChunks) ts.push_back(adj[k]);
       std::sort(ts.begin(), ts.end());
       ts.erase(std::unique(ts.begin(), ts.end()), ts.end());
+      if (ts.size() > 16) {  // at most 16 candidate thresholds (each costs a pass over the bucket)
+        std::vector<int32_t> sub;
+        for (size_t k = 0; k < 16; ++k) sub.push_back(ts[k * (ts.size() - 1) / 15]);
+        sub.erase(std::unique(sub.begin(), sub.end()), sub.end());
+        ts.swap(sub);
+      }
       for (int32_t t : ts) {
         const int64_t sv = plan_t(t, nullptr);
         if (sv > best) {
