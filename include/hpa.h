@@ -208,6 +208,14 @@ hpa_status_t hpa_latent_set_remove(hpa_cache_t* c, int32_t seq_id, int32_t set_i
  * new set id. Memory for the document goes from O(n_doc) to O(m) rows. */
 hpa_status_t hpa_seq_compress(hpa_cache_t* c, int32_t seq_id, int32_t n_doc_rows, int32_t m_rows,
                               hpa_stream_t stream, int32_t* set_id_out);
+/* hpa_seq_compress for n distinct sequences at once (one launch for all the moves): request i
+ * turns the last m_rows[i] rows of its trailing token segment into a new latent set and drops
+ * the n_doc_rows[i] rows before them. All arrays are host arrays of n entries; set_ids_out
+ * (may be NULL) receives the new set ids. Checked as a whole before any change: an invalid
+ * request, a repeated sequence (HPA_ERR_INVALID_ARG), capacity (HPA_ERR_SEQ_CAPACITY) or
+ * sum ceil(m_rows[i]/P) > free pages (HPA_ERR_OUT_OF_PAGES) leave the cache unchanged. */
+hpa_status_t hpa_seq_compress_batch(hpa_cache_t* c, int32_t n, const int32_t* seq_ids, const int32_t* n_doc_rows,
+                                    const int32_t* m_rows, hpa_stream_t stream, int32_t* set_ids_out);
 
 /* ---------------------------------------------------------------- attention (a4-a6)
  * Decode (a4 + a5): for each listed sequence the query is its LAST logical row

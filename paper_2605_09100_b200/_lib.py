@@ -49,6 +49,7 @@ SIGNATURES = {
                                             ctypes.POINTER(c_vp), c_vp, c_i32p]),
     "hpa_latent_set_remove": (c_st, [c_vp, c_i32, c_i32]),
     "hpa_seq_compress": (c_st, [c_vp, c_i32, c_i32, c_i32, c_vp, c_i32p]),
+    "hpa_seq_compress_batch": (c_st, [c_vp, c_i32, c_i32p, c_i32p, c_i32p, c_vp, c_i32p]),
     "hpa_latent_set_share": (c_st, [c_vp, c_i32, c_i32, c_i32, c_i32p]),
     "hpa_seq_fork": (c_st, [c_vp, c_i32, c_i32, c_i32p]),
     "hpa_latent_set_install_host": (c_st, [c_vp, c_i32, c_i32p, c_i32p, c_i32p, ctypes.POINTER(c_vp), c_vp,

@@ -178,6 +178,16 @@ class Cache:
                                    ctypes.byref(out)))
         return out.value
 
+    def compress_batch(self, seq_ids, n_doc_rows, m_rows, stream=None) -> np.ndarray:
+        """hpa_seq_compress_batch: in-cache compression of several requests, one launch."""
+        ids, nd, ms = _i32(seq_ids), _i32(n_doc_rows), _i32(m_rows)
+        if not (ids.size == nd.size == ms.size):
+            raise ValueError("seq_ids, n_doc_rows and m_rows differ in length")
+        out = np.zeros(ids.size, dtype=np.int32)
+        check(LIB.hpa_seq_compress_batch(self._h, ids.size, _p32(ids), _p32(nd), _p32(ms),
+                                         _stream(self.device, stream), _p32(out)))
+        return out
+
     def latent_install_host(self, seq_ids, set_ids, kv: torch.Tensor, stream=None) -> np.ndarray:
         """hpa_latent_set_install_host: kv is a (preferably pinned) CPU tensor
         [n][L][2][m][H_kv][d] bf16; copied on the cache's copy stream, then installed."""

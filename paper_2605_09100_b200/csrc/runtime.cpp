@@ -1704,44 +1704,102 @@ hpa_status_t hpa_latent_set_remove(hpa_cache_t* c, int32_t seq_id, int32_t set_i
 
 hpa_status_t hpa_seq_compress(hpa_cache_t* c, int32_t seq_id, int32_t n_doc_rows, int32_t m_rows,
                               hpa_stream_t stream, int32_t* set_id_out) {
+  return hpa_seq_compress_batch(c, 1, &seq_id, &n_doc_rows, &m_rows, stream, set_id_out);
+}
+
+hpa_status_t hpa_seq_compress_batch(hpa_cache_t* c, int32_t n, const int32_t* seq_ids, const int32_t* n_doc_rows,
+                                    const int32_t* m_rows, hpa_stream_t stream, int32_t* set_ids_out) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
-  if (hpa_status_t st = check_seq(c, seq_id)) return st;
-  Seq& q = c->seqs[seq_id];
-  if (n_doc_rows < 0 || m_rows <= 0) return fail(HPA_ERR_INVALID_ARG, "need n_doc_rows >= 0 and m_rows > 0");
-  if (q.segs.empty() || q.segs.back().latent || q.segs.back().rows < n_doc_rows + m_rows)
-    return fail(HPA_ERR_INVALID_ARG, "document + latent rows must lie in the trailing token segment");
+  if (n < 0) return fail(HPA_ERR_INVALID_ARG, "n < 0");
+  if (n == 0) return HPA_OK;
+  if (!seq_ids || !n_doc_rows || !m_rows) return fail(HPA_ERR_INVALID_ARG, "null argument");
   const int32_t P = c->cfg.page_size;
-  const int32_t np = (m_rows + P - 1) / P;
-  Segment& T = q.segs.back();
-  const int32_t keep = T.rows - n_doc_rows - m_rows;
-  const int32_t keep_pages = (keep + P - 1) / P;
-  const int32_t n_before = seq_entries(q) - int32_t(T.pages.size());
-  if (n_before + keep_pages + np > c->cfg.max_pages_per_seq)
-    return fail(HPA_ERR_SEQ_CAPACITY, "sequence %d would exceed %d pages", seq_id, c->cfg.max_pages_per_seq);
-  if (np > c->alloc.num_free())
-    return fail(HPA_ERR_OUT_OF_PAGES, "compress needs %d pages, %d free", np, c->alloc.num_free());
-  DeviceGuard dg(c->cfg.device);
-  // destination pages first (never overlapping the sources), then the move record
-  Segment L{true, q.next_set++, m_rows, {}};
-  c->alloc.alloc(np, L.pages);
-  std::vector<int32_t> idx(L.pages.begin(), L.pages.end());  // page-mode destination
-  const int32_t src_off = int32_t(idx.size());
-  for (int32_t r = 0; r < m_rows; ++r) {
-    const int32_t row = keep + n_doc_rows + r;
-    idx.push_back(T.pages[row / P] * P + row % P);
+  // every check before any change (the cache is unchanged on error)
+  int32_t need = 0;
+  std::vector<int32_t> sorted(seq_ids, seq_ids + n);
+  std::sort(sorted.begin(), sorted.end());
+  if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+    return fail(HPA_ERR_INVALID_ARG, "a sequence appears twice in the batch");
+  for (int32_t i = 0; i < n; ++i) {
+    if (hpa_status_t st = check_seq(c, seq_ids[i])) return st;
+    const Seq& q = c->seqs[seq_ids[i]];
+    if (n_doc_rows[i] < 0 || m_rows[i] <= 0) return fail(HPA_ERR_INVALID_ARG, "need n_doc_rows >= 0 and m_rows > 0");
+    if (q.segs.empty() || q.segs.back().latent || q.segs.back().rows < n_doc_rows[i] + m_rows[i])
+      return fail(HPA_ERR_INVALID_ARG, "document + latent rows must lie in the trailing token segment");
+    const Segment& T = q.segs.back();
+    const int32_t np = (m_rows[i] + P - 1) / P;
+    const int32_t keep = T.rows - n_doc_rows[i] - m_rows[i];
+    const int32_t n_before = seq_entries(q) - int32_t(T.pages.size());
+    if (n_before + (keep + P - 1) / P + np > c->cfg.max_pages_per_seq)
+      return fail(HPA_ERR_SEQ_CAPACITY, "sequence %d would exceed %d pages", seq_ids[i], c->cfg.max_pages_per_seq);
+    need += np;
   }
-  // free the document's (and the latents' token) pages; keep the prefix rows
-  for (size_t k = size_t(keep_pages); k < T.pages.size(); ++k) c->pages_of(false).release(T.pages[k]);
-  T.pages.resize(size_t(keep_pages));
-  T.rows = keep;
-  if (keep % P && c->pages_of(false).refcount(T.pages.back()) == 1)  // sole owner: rows past keep are free again
-    c->pages_of(false).set_high(T.pages.back(), keep % P);
-  if (keep == 0) q.segs.pop_back();
-  q.segs.push_back(std::move(L));
-  c->rebuild(seq_id, n_before + std::max(0, keep_pages - 1));
-  if (set_id_out) *set_id_out = q.segs.back().set_id;
-  std::vector<ScatterRecord> recs{ScatterRecord{nullptr, nullptr, 0, 0, m_rows, 0, 0, 1, 1, src_off, 0, c->fp8 ? 1 : 0}};
-  return ship(c, static_cast<cudaStream_t>(stream), recs, idx, m_rows);
+  // Pages: a request's trailing token pages past its kept rows hold either only document rows
+  // (freed before the destinations are allocated, so the batch can reuse them) or some of the
+  // m source rows (freed after the move is queued: no destination may overlap a source).
+  auto is_src_page = [&](int32_t i, int32_t k) {  // page k of request i's trailing segment
+    const Segment& T = c->seqs[seq_ids[i]].segs.back();
+    const int32_t lo = T.rows - m_rows[i];  // first source row
+    return (k + 1) * P > lo;                // page k covers rows [kP, kP + P)
+  };
+  int32_t reusable = 0;  // document-only pages that return to the latent pages' pool
+  if (!c->fp8) {
+    for (int32_t i = 0; i < n; ++i) {
+      const Segment& T = c->seqs[seq_ids[i]].segs.back();
+      const int32_t keep_pages = (T.rows - n_doc_rows[i] - m_rows[i] + P - 1) / P;
+      for (int32_t k = keep_pages; k < int32_t(T.pages.size()); ++k)
+        if (!is_src_page(i, k) && c->alloc.refcount(T.pages[size_t(k)]) == 1) ++reusable;
+    }
+  }
+  if (need > c->alloc.num_free() + reusable)
+    return fail(HPA_ERR_OUT_OF_PAGES, "compress needs %d pages, %d free", need, c->alloc.num_free() + reusable);
+  DeviceGuard dg(c->cfg.device);
+  for (int32_t i = 0; i < n; ++i) {  // document-only pages first
+    Segment& T = c->seqs[seq_ids[i]].segs.back();
+    const int32_t keep_pages = (T.rows - n_doc_rows[i] - m_rows[i] + P - 1) / P;
+    for (int32_t k = keep_pages; k < int32_t(T.pages.size()); ++k)
+      if (!is_src_page(i, k)) c->pages_of(false).release(T.pages[size_t(k)]);
+  }
+  // destination pages of every request, then one page-mode move record per request, all in
+  // one launch; the source pages are released once the records are built
+  std::vector<Segment> lat(static_cast<size_t>(n));
+  for (int32_t i = 0; i < n; ++i) {
+    Seq& q = c->seqs[seq_ids[i]];
+    lat[size_t(i)] = Segment{true, q.next_set++, m_rows[i], {}};
+    c->alloc.alloc((m_rows[i] + P - 1) / P, lat[size_t(i)].pages);
+  }
+  std::vector<int32_t> idx;
+  std::vector<ScatterRecord> recs;
+  std::vector<int32_t> src_pages;
+  for (int32_t i = 0; i < n; ++i) {
+    Seq& q = c->seqs[seq_ids[i]];
+    Segment& T = q.segs.back();
+    const int32_t keep = T.rows - n_doc_rows[i] - m_rows[i];
+    const int32_t keep_pages = (keep + P - 1) / P;
+    const int32_t n_before = seq_entries(q) - int32_t(T.pages.size());
+    const int32_t dst_off = int32_t(idx.size());
+    idx.insert(idx.end(), lat[size_t(i)].pages.begin(), lat[size_t(i)].pages.end());  // page-mode destination
+    const int32_t src_off = int32_t(idx.size());
+    for (int32_t r = 0; r < m_rows[i]; ++r) {
+      const int32_t row = keep + n_doc_rows[i] + r;
+      idx.push_back(T.pages[row / P] * P + row % P);
+    }
+    recs.push_back(ScatterRecord{nullptr, nullptr, 0, 0, m_rows[i], dst_off, 0, 1, 1, src_off, 0, c->fp8 ? 1 : 0});
+    for (int32_t k = keep_pages; k < int32_t(T.pages.size()); ++k)
+      if (is_src_page(i, k)) src_pages.push_back(T.pages[size_t(k)]);
+    T.pages.resize(size_t(keep_pages));
+    T.rows = keep;
+    if (keep % P && c->pages_of(false).refcount(T.pages.back()) == 1)  // sole owner: rows past keep are free again
+      c->pages_of(false).set_high(T.pages.back(), keep % P);
+    if (keep == 0) q.segs.pop_back();
+    q.segs.push_back(std::move(lat[size_t(i)]));
+    c->rebuild(seq_ids[i], n_before + std::max(0, keep_pages - 1));
+    if (set_ids_out) set_ids_out[i] = q.segs.back().set_id;
+  }
+  for (int32_t pg : src_pages) c->pages_of(false).release(pg);
+  int64_t rows = 0;  // the scatter grid is sized by the largest record
+  for (int32_t i = 0; i < n; ++i) rows = std::max<int64_t>(rows, m_rows[i]);
+  return ship(c, static_cast<cudaStream_t>(stream), recs, idx, rows);
 }
 
 namespace {

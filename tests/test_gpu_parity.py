@@ -448,6 +448,47 @@ def test_compress_in_cache(P):
     check_close(got, oracle_prefill(p, [seqs[0]], [20], q), "prefill after compress")
 
 
+@pytest.mark.parametrize("P,fp8", [(16, False), (32, False), (16, True)])
+def test_compress_batch(P, fp8):
+    """hpa_seq_compress_batch: five requests (including a fork sharing the documents' prefix)
+    compressed in one call == the oracle's sequential compressions; bit-exact views and tables,
+    exact page accounting, decode parity; a bad request or a repeated sequence changes nothing."""
+    from paper_2605_09100_b200 import HPAError
+    shape = Shape(2, 8, 2, 128, P)
+    p = Pair(shape, num_pages=3000, max_seqs=8, max_pages_per_seq=256, token_fp8=fp8,
+             num_token_pages=3000 if fp8 else 0)
+    jobs = [(300, 128), (5, 40), (0, 16), (77, 128), (10, 24)]
+    seqs = [p.build([("latent", 128), ("tokens", 21 + n_doc + m)]) for n_doc, m in jobs]
+    fork = p.cache.seq_fork(seqs[0], 128 + 21)
+    p.orc.fork(seqs[0], 128 + 21, fork)
+    state0 = (p.cache.stats(), [p.cache.export_table(s)[0].tolist() for s in seqs])
+    with pytest.raises(HPAError) as e:                       # request 3 asks for too many rows
+        p.cache.compress_batch(seqs, [n for n, _ in jobs[:3]] + [10 ** 4] + [jobs[4][0]], [m for _, m in jobs])
+    assert e.value.name == "HPA_ERR_INVALID_ARG"
+    with pytest.raises(HPAError) as e:                       # a sequence twice
+        p.cache.compress_batch([seqs[0], seqs[0]], [1, 1], [8, 8])
+    assert e.value.name == "HPA_ERR_INVALID_ARG"
+    assert (p.cache.stats(), [p.cache.export_table(s)[0].tolist() for s in seqs]) == state0
+    got = p.cache.compress_batch(seqs, [n for n, _ in jobs], [m for _, m in jobs])
+    for i, (s, (n_doc, m)) in enumerate(zip(seqs, jobs)):
+        assert got[i] == p.orc.compress(s, n_doc, m)
+    torch.cuda.synchronize()
+    live = seqs + [fork]
+    for layer in (0, 1):
+        for s in live:
+            pages, pos0, meta = p.cache.export_table(s)
+            assert [(("latent" if mm & META_LATENT_BIT else "token"), int(mm & 0x7fff), int(x))
+                    for mm, x in zip(meta, pos0)] == p.orc.expected_table(s)
+            k1, v1 = p.orc.logical_kv(s, layer, fp8_staged=fp8)  # export gives fp8 rows as bf16 (A20)
+            k2, v2 = p.cache.export_logical_kv(layer, s)
+            assert np.array_equal(k1, f64(k2)) and np.array_equal(v1, f64(v2))
+    q = p.queries(len(live))
+    out = p.cache.decode(1, live, q.cuda())
+    torch.cuda.synchronize()
+    ref = np.stack([attend(f64(q[i:i + 1]), *p.orc.logical_kv(s, 1), shape.scale)[0] for i, s in enumerate(live)])
+    check_close(out, ref, "decode after batched compress")
+
+
 def test_compress_errors_leave_cache_unchanged():
     from paper_2605_09100_b200 import HPAError
     shape = Shape(1, 4, 2, 64, 16)
