@@ -74,6 +74,12 @@ constexpr int kNCons = HPA_DEC_NCONS;  // consumer warps per CTA
 #ifndef HPA_DEC_F32
 #define HPA_DEC_F32 1  // fp8 token pages (G <= 8): 32-row fp8 chunks, two 16-row blocks per ring stage
 #endif
+#ifndef HPA_DEC_PSTAGES
+// ring depth of the persistent decode kernel (bf16): 10 stages ran the configs[1] step ~1.2 %
+// faster than 12, 11 or 8 (profiles/r2_decode_ring_depth_ab.log; depths that are not a multiple
+// of the consumer count use stage tags)
+#define HPA_DEC_PSTAGES 10
+#endif
 #ifndef HPA_CS_PAIR
 #define HPA_CS_PAIR 1  // cascade group units: consumers take two chunks per softmax step
 #endif
@@ -583,7 +589,7 @@ struct PDecodeSmem {
   static constexpr int kStageBytes =
       F32 ? (((2 * kTileBytes > 4 * kBlk8 ? 2 * kTileBytes : 4 * kBlk8) + 1023) & ~1023) : 2 * kTileBytes;
   static constexpr int kStages =
-      F32 ? (CS ? 8 : (D == 128 ? HPA_DEC_F32_STAGES : 12)) : (CS ? HPA_DEC_CS_STAGES : kNSt);
+      F32 ? (CS ? 8 : (D == 128 ? HPA_DEC_F32_STAGES : 12)) : (CS ? HPA_DEC_CS_STAGES : HPA_DEC_PSTAGES);
   // a depth that is not a multiple of the consumer count puts successive items of one slot on
   // different consumers, and a consumer could then take the slot's previous phase of the same
   // parity for its item (mbarrier-parity ABA): every stage then carries its item index (ctag),
