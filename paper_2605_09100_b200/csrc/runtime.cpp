@@ -643,7 +643,10 @@ int32_t plan_splits_core(const hpa_cache_t* c, int32_t n, std::vector<int32_t> c
   // costs ~0.6 of a bf16 one, so the per-unit time is several chunks there: 5.0 (S = 4 instead
   // of 10 at configs[1]: 170 -> 152.6 us).
   static const double c0_env = std::getenv("HPA_PLAN_C0") ? std::atof(std::getenv("HPA_PLAN_C0")) : -1.0;
-  const double c0 = c0_env >= 0.0 ? c0_env : (c->fp8 ? 5.0 : 0.5);
+  // round 2, with the 10-stage ring: bf16 P = 16 runs the configs[1] step 1.3 % and the ragged
+  // batch 1 % faster at 3.0 (S = 5) than at 0.5 (S = 10), while P = 64 runs 3.5 % slower there
+  // (profiles/r2_decode_plan_c0_ring10.log): 3.0 for pages of <= 32 rows, 0.5 above
+  const double c0 = c0_env >= 0.0 ? c0_env : (c->fp8 ? 5.0 : (c->cfg.page_size <= 32 ? 3.0 : 0.5));
   static const double k_comb = std::getenv("HPA_PLAN_COMBINE") ? std::atof(std::getenv("HPA_PLAN_COMBINE")) : 4.0;
   const double hkv = c->cfg.num_kv_heads;
   const double part_chunks = double(c->cfg.num_q_heads) * (c->cfg.head_dim + 1) * 8 / 8192.0;
