@@ -81,7 +81,10 @@ constexpr int kNCons = HPA_DEC_NCONS;  // consumer warps per CTA
 #define HPA_DEC_PSTAGES 10
 #endif
 #ifndef HPA_CS_PAIR
-#define HPA_CS_PAIR 1  // cascade group units: consumers take two chunks per softmax step
+#define HPA_CS_PAIR 1  // cascade group units: consumers take HPA_CS_STEP chunks per softmax step
+#endif
+#ifndef HPA_CS_STEP
+#define HPA_CS_STEP 2
 #endif
 #ifndef HPA_DEC_CS_STAGES
 #define HPA_DEC_CS_STAGES 10  // ring depth of the cascade variant (its Q buffers hold 32 rows)
@@ -1405,31 +1408,32 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
     }
 #else
     if (CS && grp && HPA_CS_PAIR) {
-      // Group unit (cascade): every consumer works through every chunk, so two chunks per step
-      // -- items i and i + 1, two independent QK^T chains, one softmax step over 32 keys and two
-      // PV k-steps -- halve the chain latency per chunk. Item i + 1 may be the unit's sentinel.
+      // Group unit (cascade): every consumer works through every chunk, so kCsStep chunks per
+      // step -- items i .. i + kCsStep - 1, independent QK^T chains, one softmax step over all
+      // their keys, then the PV k-steps -- cut the chain latency per chunk. Any item after the
+      // first may be the unit's sentinel.
+      constexpr int kCsStep = HPA_CS_STEP;
       for (;;) {
-        const int sA = i % kNSt, sB = (i + 1) % kNSt;
-        if (L::kTags) while (ctag[sA] != int(i)) {}
-        mbar_wait(&full[sA], (i / kNSt) & 1);
-        const int nA = cmeta[sA];
-        if (nA <= 0) {
-          __syncwarp();
-          release(sA);
-          after_sentinel();
-          break;
-        }
-        if (L::kTags) while (ctag[sB] != int(i + 1)) {}
-        mbar_wait(&full[sB], ((i + 1) / kNSt) & 1);
-        const int nB = cmeta[sB];
-        const bool haveB = nB > 0;
-        float x[2][4];
+        int sl[kCsStep], nv[kCsStep];
+        int nit = 0;  // chunks in this step (items before a sentinel)
+        bool ends = false;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < kCsStep; ++c) {
+          sl[c] = int((i + c) % kNSt);
+          nv[c] = 0;
+          if (ends) continue;
+          if (L::kTags) while (ctag[sl[c]] != int(i + c)) {}
+          mbar_wait(&full[sl[c]], ((i + c) / kNSt) & 1);
+          nv[c] = cmeta[sl[c]];
+          if (nv[c] <= 0) ends = true;
+          else nit = c + 1;
+        }
+        float x[kCsStep][4];
+#pragma unroll
+        for (int c = 0; c < kCsStep; ++c) {
           x[c][0] = x[c][1] = x[c][2] = x[c][3] = -CUDART_INF_F;
-          if (c == 1 && !haveB) continue;
-          const int nv = c ? nB : nA;
-          const uint8_t* kt = stages + (c ? sB : sA) * L::kStageBytes;
+          if (c >= nit) continue;
+          const uint8_t* kt = stages + sl[c] * L::kStageBytes;
           float sacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
           for (int ks = 0; ks < D / 16; ++ks) {  // A = K (16 keys x 16 dims)
@@ -1440,75 +1444,83 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
             ldsm_x4(smem_u32(kt + (kc >> 3) * 2048 + sw128(row, kc & 7)), ka[0], ka[1], ka[2], ka[3]);
             mma_bf16_16816(sacc, ka, qbf[ks][0], qbf[ks][1]);
           }
-          x[c][0] = gq < nv ? sacc[0] * sl2 : -CUDART_INF_F;
-          x[c][1] = gq < nv ? sacc[1] * sl2 : -CUDART_INF_F;
-          x[c][2] = gq + 8 < nv ? sacc[2] * sl2 : -CUDART_INF_F;
-          x[c][3] = gq + 8 < nv ? sacc[3] * sl2 : -CUDART_INF_F;
+          x[c][0] = gq < nv[c] ? sacc[0] * sl2 : -CUDART_INF_F;
+          x[c][1] = gq < nv[c] ? sacc[1] * sl2 : -CUDART_INF_F;
+          x[c][2] = gq + 8 < nv[c] ? sacc[2] * sl2 : -CUDART_INF_F;
+          x[c][3] = gq + 8 < nv[c] ? sacc[3] * sl2 : -CUDART_INF_F;
         }
-        float mx0 = fmaxf(fmaxf(x[0][0], x[0][2]), fmaxf(x[1][0], x[1][2]));
-        float mx1 = fmaxf(fmaxf(x[0][1], x[0][3]), fmaxf(x[1][1], x[1][3]));
-        const bool any_grow = __any_sync(0xffffffffu, mx0 > m_h[0] + 8.f || mx1 > m_h[1] + 8.f);
-        if (any_grow) {
+        if (nit > 0) {
+          float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
 #pragma unroll
-          for (int off = 4; off < 32; off <<= 1) {
-            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
-            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+          for (int c = 0; c < kCsStep; ++c) {
+            mx0 = fmaxf(mx0, fmaxf(x[c][0], x[c][2]));
+            mx1 = fmaxf(mx1, fmaxf(x[c][1], x[c][3]));
           }
-        }
-        const bool g0 = any_grow && mx0 > m_h[0] + 8.f, g1 = any_grow && mx1 > m_h[1] + 8.f;
-        const float mn0 = g0 ? mx0 : m_h[0], mn1 = g1 ? mx1 : m_h[1];
-        float pp[2][4];
+          const bool any_grow = __any_sync(0xffffffffu, mx0 > m_h[0] + 8.f || mx1 > m_h[1] + 8.f);
+          if (any_grow) {
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          pp[c][0] = fast_exp2(x[c][0] - mn0);
-          pp[c][1] = fast_exp2(x[c][1] - mn1);
-          pp[c][2] = fast_exp2(x[c][2] - mn0);
-          pp[c][3] = fast_exp2(x[c][3] - mn1);
-        }
-        const float s0 = (pp[0][0] + pp[0][2]) + (pp[1][0] + pp[1][2]);
-        const float s1 = (pp[0][1] + pp[0][3]) + (pp[1][1] + pp[1][3]);
-        if (!any_grow) {
-          l_h[0] += s0;
-          l_h[1] += s1;
-        } else {
-          const float al0 = fast_exp2(m_h[0] - mn0), al1 = fast_exp2(m_h[1] - mn1);
-          m_h[0] = mn0;
-          m_h[1] = mn1;
-          l_h[0] = l_h[0] * al0 + s0;
-          l_h[1] = l_h[1] * al1 + s1;
-#pragma unroll
-          for (int n = 0; n < D / 16; ++n) {
-            o[n][0] *= al0;
-            o[n][1] *= al1;
-            o[n][2] *= al0;
-            o[n][3] *= al1;
+            for (int off = 4; off < 32; off <<= 1) {
+              mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+              mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+            }
           }
-        }
+          const bool g0 = any_grow && mx0 > m_h[0] + 8.f, g1 = any_grow && mx1 > m_h[1] + 8.f;
+          const float mn0 = g0 ? mx0 : m_h[0], mn1 = g1 ? mx1 : m_h[1];
+          float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          if (c == 1 && !haveB) continue;
-          const uint32_t pb0 = movmatrix_t(pack_bf16(pp[c][0] * vpre, pp[c][1] * vpre));
-          const uint32_t pb1 = movmatrix_t(pack_bf16(pp[c][2] * vpre, pp[c][3] * vpre));
-          const uint8_t* vt = stages + (c ? sB : sA) * L::kStageBytes + L::kTileBytes;
+          for (int c = 0; c < kCsStep; ++c) {  // x becomes p (exp2 against the running max)
+            x[c][0] = fast_exp2(x[c][0] - mn0);
+            x[c][1] = fast_exp2(x[c][1] - mn1);
+            x[c][2] = fast_exp2(x[c][2] - mn0);
+            x[c][3] = fast_exp2(x[c][3] - mn1);
+            s0 += x[c][0] + x[c][2];
+            s1 += x[c][1] + x[c][3];
+          }
+          if (!any_grow) {
+            l_h[0] += s0;
+            l_h[1] += s1;
+          } else {
+            const float al0 = fast_exp2(m_h[0] - mn0), al1 = fast_exp2(m_h[1] - mn1);
+            m_h[0] = mn0;
+            m_h[1] = mn1;
+            l_h[0] = l_h[0] * al0 + s0;
+            l_h[1] = l_h[1] * al1 + s1;
 #pragma unroll
-          for (int mt = 0; mt < D / 16; ++mt) {  // A = V^T (16 dims x 16 keys)
-            const int mi = lane >> 3;
-            const int key = (lane & 7) + (mi >> 1) * 8;
-            const int dc = 2 * mt + (mi & 1);
-            uint32_t va[4];
-            ldsm_x4_t(smem_u32(vt + (dc >> 3) * 2048 + sw128(key, dc & 7)), va[0], va[1], va[2], va[3]);
-            mma_bf16_16816(o[mt], va, pb0, pb1);
+            for (int n = 0; n < D / 16; ++n) {
+              o[n][0] *= al0;
+              o[n][1] *= al1;
+              o[n][2] *= al0;
+              o[n][3] *= al1;
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < kCsStep; ++c) {
+            if (c >= nit) continue;
+            const uint32_t pb0 = movmatrix_t(pack_bf16(x[c][0] * vpre, x[c][1] * vpre));
+            const uint32_t pb1 = movmatrix_t(pack_bf16(x[c][2] * vpre, x[c][3] * vpre));
+            const uint8_t* vt = stages + sl[c] * L::kStageBytes + L::kTileBytes;
+#pragma unroll
+            for (int mt = 0; mt < D / 16; ++mt) {  // A = V^T (16 dims x 16 keys)
+              const int mi = lane >> 3;
+              const int key = (lane & 7) + (mi >> 1) * 8;
+              const int dc = 2 * mt + (mi & 1);
+              uint32_t va[4];
+              ldsm_x4_t(smem_u32(vt + (dc >> 3) * 2048 + sw128(key, dc & 7)), va[0], va[1], va[2], va[3]);
+              mma_bf16_16816(o[mt], va, pb0, pb1);
+            }
           }
         }
         __syncwarp();
-        release(sA);
-        release(sB);
-        if (!haveB) {  // item i + 1 was the sentinel
-          i += 1;
+        const int waited = ends ? nit + 1 : kCsStep;  // (the sentinel's stage too)
+#pragma unroll
+        for (int c = 0; c < kCsStep; ++c)
+          if (c < waited) release(sl[c]);
+        if (ends) {
+          i += nit;  // the sentinel's item
           after_sentinel();
           break;
         }
-        i += 2;
+        i += kCsStep;
       }
     } else
     for (;; i += istep) {
