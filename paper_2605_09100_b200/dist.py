@@ -51,6 +51,8 @@ def gather_head_shards(out_local: torch.Tensor, group=None) -> torch.Tensor:
     with one all_gather_into_tensor (NCCL over NVLink on GPUs, gloo on CPU). The payload is
     B Hq d 2 bytes (64 KB at configs[1]), latency-bound: NCCL's all-gather is the right tool
     (a fused peer-memory kernel would save microseconds on a step that sharding already slows)."""
+    if not dist.is_available() or not dist.is_initialized():  # one process: its shard is everything
+        return out_local
     world = dist.get_world_size(group)
     b, hl, d = out_local.shape
     buf = torch.empty((world * b, hl, d), dtype=out_local.dtype, device=out_local.device)
@@ -81,6 +83,8 @@ def context_parallel_decode(cache, layer: int, seq_ids, q: torch.Tensor, group=N
 def gather_partials(o: torch.Tensor, lse: torch.Tensor, group=None):
     """All-gathers every rank's partial (o [n][Hq][d], lse [n][Hq]) into rank-major
     [world][n][Hq][d] / [world][n][Hq] (two all_gather_into_tensor calls)."""
+    if not dist.is_available() or not dist.is_initialized():  # one process: world of one
+        return o.unsqueeze(0), lse.unsqueeze(0)
     world = dist.get_world_size(group)
     o_all = torch.empty((world,) + tuple(o.shape), dtype=o.dtype, device=o.device)
     l_all = torch.empty((world,) + tuple(lse.shape), dtype=lse.dtype, device=lse.device)

@@ -79,3 +79,17 @@ def test_head_shard_bounds():
     assert head_shard(32, 8, 3, 4) == (6, 8, 24, 32)
     with pytest.raises(ValueError):
         head_shard(32, 8, 0, 3)
+
+
+def test_gathers_without_process_group():
+    """One process (no torch.distributed group): the gathers return this process's data as the
+    whole (bench.py --mode head_shard | context_parallel at N = 1)."""
+    import torch
+
+    from paper_2605_09100_b200.dist import gather_head_shards, gather_partials
+    o = torch.randn(3, 8, 16)
+    assert gather_head_shards(o) is o
+    p, lse = torch.randn(3, 8, 16), torch.randn(3, 8)
+    pa, la = gather_partials(p, lse)
+    assert pa.shape == (1, 3, 8, 16) and la.shape == (1, 3, 8)
+    assert torch.equal(pa[0], p) and torch.equal(la[0], lse)
