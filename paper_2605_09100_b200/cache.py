@@ -18,8 +18,13 @@ def _p32(a: np.ndarray):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)  # the handle without a Stream object
+
+
 def _stream(device: int, stream) -> c_vp:
     if stream is None:
+        if _raw_stream is not None:
+            return c_vp(_raw_stream(device))
         stream = torch.cuda.current_stream(device)
     return c_vp(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
 
@@ -108,6 +113,10 @@ class Cache:
 
     # ------------------------------------------------------------------ checks
     def _dev_tensor(self, t: torch.Tensor, name: str, shape=None) -> int:
+        # fast path (one expression, the per-call cost of the decode step's four tensors)
+        if (type(t) is torch.Tensor and t.is_cuda and t.dtype is torch.bfloat16 and t.get_device() == self.device
+                and t.is_contiguous() and (shape is None or t.shape == shape)):
+            return t.data_ptr()
         if not isinstance(t, torch.Tensor) or t.device.type != "cuda" or t.device.index != self.device:
             raise ValueError(f"{name} must be a CUDA tensor on cuda:{self.device}")
         if t.dtype != torch.bfloat16:

@@ -12,7 +12,7 @@ import bench  # noqa: E402
 from paper_2605_09100_b200 import Cache  # noqa: E402
 from workloads import qwen3_8b_shape  # noqa: E402
 
-shape = qwen3_8b_shape(16)
+shape = qwen3_8b_shape(int(os.environ.get("P", "16")))
 B, K, W = 64, 50, 5
 st = torch.cuda.current_stream()
 cache, seqs, _ = bench.build_decode_cache(torch, Cache, shape, B, 8, 4095, 3 * K + W + 16, 0, seed=1234)
