@@ -48,7 +48,7 @@ constexpr int kNCons = HPA_DEC_NCONS;  // consumer warps per CTA
 #define HPA_DEC_ALLOW_ANY_DEPTH 0
 #endif
 #ifndef HPA_DEC_STAGES
-#define HPA_DEC_STAGES 12
+#define HPA_DEC_STAGES 12  // ring depth of the grid-per-split decode_split_kernel (HPA_DECODE_PERSISTENT=0); the persistent kernel uses HPA_DEC_PSTAGES
 #endif
 #ifndef HPA_DEC_DYNAMIC
 #define HPA_DEC_DYNAMIC 1  // 1: units fetched from a ticket counter; 0: static striding over the list
