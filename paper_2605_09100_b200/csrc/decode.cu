@@ -89,6 +89,10 @@ constexpr int kNCons = HPA_DEC_NCONS;  // consumer warps per CTA
 #ifndef HPA_DEC_CS_STAGES
 #define HPA_DEC_CS_STAGES 10  // ring depth of the cascade variant (its Q buffers hold 32 rows)
 #endif
+#ifndef HPA_WHATIF_EARLY_REL
+#define HPA_WHATIF_EARLY_REL 0  // timing what-if only (wrong results): 32-row chunks release their stage
+                                // 1: on arrival, 2: after QK^T (the bound for holding V in registers), 3: on arrival, no math
+#endif
 #ifndef HPA_DEC_F32_STAGES
 #define HPA_DEC_F32_STAGES 10  // ring depth of the 32-row fp8 variant (d = 128): 10 x 9 KB, two CTAs per SM (147.0 vs 148.2 us with 8, profiles/r2_fp8_ring10_ab.log)
 #endif
@@ -1112,6 +1116,11 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
         const bool c8 = meta >= 0x10000;
         const int nb0 = meta & 0xff, nb1 = (meta >> 8) & 0xff;
         const bool two = c8 && nb1 > 0;
+#if HPA_WHATIF_EARLY_REL == 1 || HPA_WHATIF_EARLY_REL == 3
+        __syncwarp();
+        release(slot);
+        if (HPA_WHATIF_EARLY_REL == 3) continue;  // 3: no math at all (the data-movement bound)
+#endif
         float x[2][4], vm[2][2];
         float svmax = 0.f;  // this lane's largest valid V scale
 #pragma unroll
@@ -1160,6 +1169,10 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
           x[c][2] = gq + 8 < nv ? sacc[2] * kmul1 : -CUDART_INF_F;  // key g+8, head 2t
           x[c][3] = gq + 8 < nv ? sacc[3] * kmul1 : -CUDART_INF_F;  // key g+8, head 2t+1
         }
+#if HPA_WHATIF_EARLY_REL == 2
+        __syncwarp();
+        release(slot);
+#endif
         if (c8) fp8_vpre_adjust<D>(svmax, vpre, o);
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -1239,8 +1252,10 @@ decode_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_
             }
           }
         }
+#if !HPA_WHATIF_EARLY_REL
         __syncwarp();
         release(slot);
+#endif
       }
     } else {
 #if HPA_DEC_PAIR
