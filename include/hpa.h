@@ -300,8 +300,10 @@ hpa_status_t hpa_export_table(hpa_cache_t* c, int32_t seq_id, int32_t* pages, in
 /* Testing / tuning hook: force the decode split count (0 = planner). */
 hpa_status_t hpa_set_decode_splits(hpa_cache_t* c, int32_t splits);
 /* Cascade decode of shared leading page runs in hpa_decode / hpa_append_decode /
- * hpa_decode_partial: on = 1 (default), 0 = every request reads its whole table.
- * INVALID_ARG on a NULL cache. */
+ * hpa_decode_partial: on = 1 (default: the planner's groups, kept when they save >= 1/3 of
+ * the batch's reads), 0 = every request reads its whole table, 2 = every group the planner
+ * finds regardless of the saving (testing hook). INVALID_ARG on a NULL cache or on outside
+ * [0, 2]. */
 hpa_status_t hpa_set_decode_cascade(hpa_cache_t* c, int32_t on);
 /* Introspection of the last decode plan (persistent kernel): *n_units work units, of which
  * *n_group_units are cascade group units, *splits_max partial slots per request (1 = no

@@ -379,9 +379,10 @@ class Cache:
     def set_decode_splits(self, splits: int) -> None:
         check(LIB.hpa_set_decode_splits(self._h, splits))
 
-    def set_decode_cascade(self, on: bool) -> None:
-        """Cascade decode of shared leading page runs (default on)."""
-        check(LIB.hpa_set_decode_cascade(self._h, 1 if on else 0))
+    def set_decode_cascade(self, on) -> None:
+        """Cascade decode of shared leading page runs: True / 1 = planner (default), False / 0 =
+        off, 2 = every group the planner finds, whatever it saves (testing hook)."""
+        check(LIB.hpa_set_decode_cascade(self._h, int(on)))
 
     def decode_plan_info(self) -> dict:
         """The last decode's plan: work units, cascade group units, partial slots per request."""

@@ -383,7 +383,7 @@ struct hpa_cache {
   int32_t plan_units = 0, plan_smax = 1;
   int32_t forced_splits = 0;
   // cascade decode (NEXT-2): group-piece records of the current plan (device), on/off switch
-  bool cascade = true;
+  int32_t cascade = 1;  // hpa_set_decode_cascade: 0 off, 1 planner, 2 every shared run
   int32_t* groups_dev = nullptr;
   size_t groups_cap = 0;
   int32_t plan_group_units = 0;
@@ -839,7 +839,7 @@ std::vector<CGroup> find_cascade_groups(const hpa_cache_t* c, int32_t n, const i
   if (trace && !out.empty())
     std::fprintf(stderr, "cascade: %zu groups, saved %lld of %lld chunk reads (min %.3f)\n", out.size(),
                  (long long)saved, (long long)total, min_saved);
-  if (double(saved) < min_saved * double(total)) out.clear();
+  if (c->cascade < 2 && double(saved) < min_saved * double(total)) out.clear();
   return out;
 }
 
@@ -2455,10 +2455,10 @@ hpa_status_t hpa_set_decode_splits(hpa_cache_t* c, int32_t splits) {
   return HPA_OK;
 }
 
-// Diagnostics (include/hpa.h): device buffer for the HPA_TRACE phase stamps.
 hpa_status_t hpa_set_decode_cascade(hpa_cache_t* c, int32_t on) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
-  c->cascade = on != 0;
+  if (on < 0 || on > 2) return fail(HPA_ERR_INVALID_ARG, "cascade mode %d outside [0, 2]", on);
+  c->cascade = on;
   return HPA_OK;
 }
 
@@ -2470,6 +2470,7 @@ hpa_status_t hpa_decode_plan_info(hpa_cache_t* c, int32_t* n_units, int32_t* n_g
   return HPA_OK;
 }
 
+// Diagnostics (include/hpa.h): device buffer for the HPA_TRACE phase stamps.
 hpa_status_t hpa_debug_trace(hpa_cache_t* c, void* device_buf) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
   c->trace = static_cast<long long*>(device_buf);

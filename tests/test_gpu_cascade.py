@@ -275,3 +275,28 @@ def test_cascade_step_fuzz(seed, hq, hkv, d, P, fp8, need):
             grouped += info["group_units"] > 0
     # (the random trees of some cases never pass the 1/3-of-reads rule; the others must cascade)
     assert grouped > 0 or not need
+
+
+def test_cascade_forced_mode_below_threshold():
+    """hpa_set_decode_cascade(c, 2) keeps groups the planner would drop for saving < 1/3 of the
+    reads: two requests forked from a 2K prompt, each with 6K rows of its own (saving 1/7) --
+    planner mode plans none, forced mode plans group units, both match the oracle; modes
+    outside [0, 2] are INVALID_ARG."""
+    from paper_2605_09100_b200 import HPAError
+    p = Pair(_shape(32, 8, 128, 16, L=1), 4096, 8, 600, seed=21)
+    src = p.build([("tokens", 2048)])
+    seqs = [src, _fork(p, src, 2048)]
+    p.tokens(seqs, [6144, 6144])
+    q = p.queries(2)
+    ref = _ref(p, seqs, q, 0)
+    got = {}
+    for mode in (1, 2):
+        p.cache.set_decode_cascade(mode)
+        got[mode] = p.cache.decode(0, seqs, q.cuda())
+        torch.cuda.synchronize()
+        n = p.cache.decode_plan_info()["group_units"]
+        assert (n > 0) == (mode == 2), (mode, n)
+        check_close(got[mode], ref, f"cascade mode {mode}")
+    for bad in (-1, 3):
+        with pytest.raises(HPAError):
+            p.cache.set_decode_cascade(bad)
