@@ -16,8 +16,20 @@ shape = qwen3_8b_shape(16)
 B, K = 64, 50
 st = torch.cuda.current_stream()
 cs = torch.cuda.Stream()
-cache, seqs, _ = bench.build_decode_cache(torch, Cache, shape, B, 8, 4095, 14 * K + 40, 0, seed=1234)
-ids = np.asarray(seqs, dtype=np.int32)
+cs2 = torch.cuda.Stream()  # ahead2: D2H on its own copy stream
+cache = ids = None
+
+
+def fresh():
+    """Every run starts from the same cache state (appends grow the sequences)."""
+    global cache, ids
+    if cache is not None and os.environ.get("NOFRESH"):
+        return
+    if cache is not None:
+        cache.close()
+        torch.cuda.empty_cache()
+    cache, seqs, _ = bench.build_decode_cache(torch, Cache, shape, B, 8, 4095, 20 * K + 40, 0, seed=1234)
+    ids = np.asarray(seqs, dtype=np.int32)
 g = torch.Generator(device="cuda").manual_seed(1)
 kvq_elems = 2 * B * 8 * 128 + B * 32 * 128
 host = torch.randn((K, kvq_elems), generator=g, device="cuda").to(torch.bfloat16).cpu().pin_memory()
@@ -36,6 +48,7 @@ def views(buf):
 def run(mode):
     """device: no copies; wait: a cross-stream event wait per step; ahead / ahead_noD2H: the
     bench's pipelining (step i+1's inputs copied while step i runs), one consolidated H2D."""
+    fresh()
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_done = [torch.cuda.Event() for _ in range(2)]
     dummy = torch.cuda.Event()
@@ -65,19 +78,25 @@ def run(mode):
         elif mode == "wait":
             dummy.record(cs)
             st.wait_event(dummy)
+        elif mode == "record":
+            dummy.record(st)
         k, v, q = views(dbuf[sl])
         cache.append_decode(0, ids, k, v, q, douts[sl])
         if ahead:
             ev_done[sl].record(st)
-            if mode == "ahead":
-                with torch.cuda.stream(cs):
-                    cs.wait_event(ev_done[sl])
+            if mode in ("ahead", "ahead2"):
+                ds = cs2 if mode == "ahead2" else cs
+                with torch.cuda.stream(ds):
+                    ds.wait_event(ev_done[sl])
                     pin_o[i].copy_(douts[sl], non_blocking=True)
+                if mode == "ahead2":  # the H2D into this slot two steps on waits for this D2H
+                    ev_done[sl].record(cs2)
     st.wait_stream(cs)
+    st.wait_stream(cs2)
     e1.record(st)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / K * 1e3
 
 
 for r in range(3):
-    print(" | ".join(f"{m} {run(m):.1f} us" for m in ("device", "wait", "ahead", "ahead_noD2H")), flush=True)
+    print(" | ".join(f"{m} {run(m):.1f} us" for m in ("device", "record", "wait", "ahead", "ahead2", "ahead_noD2H")), flush=True)
