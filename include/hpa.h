@@ -309,16 +309,20 @@ hpa_status_t hpa_set_decode_cascade(hpa_cache_t* c, int32_t on);
  * *n_group_units are cascade group units, *splits_max partial slots per request (1 = no
  * combine). Any output pointer may be NULL. INVALID_ARG on a NULL cache. */
 hpa_status_t hpa_decode_plan_info(hpa_cache_t* c, int32_t* n_units, int32_t* n_group_units, int32_t* splits_max);
-/* Testing / tuning hook for hpa_prefill / hpa_prefill_span: 0 = planner (split-KV only for
- * the units of an under-filled last wave), 1 = never split, 2..15 = split every unit's key
- * tiles into that many pieces (merged by LSE), 16 = no host work list (one CTA per unit of a
- * grid; each CTA searches the block table for its key-tile range). INVALID_ARG outside [0, 16]. */
+/* Testing / tuning hook for hpa_prefill / hpa_prefill_span: 0 = planner (stream-K shares, or
+ * split-KV for the units of an under-filled last wave; see hpa_set_prefill_ctas), 1 = never
+ * split, 2..15 = split every unit's key tiles into that many pieces (merged by LSE), 16 = no
+ * host work list (one CTA per unit of a grid; each CTA searches the block table for its
+ * key-tile range). INVALID_ARG outside [0, 16]. */
 hpa_status_t hpa_set_prefill_splits(hpa_cache_t* c, int32_t splits);
-/* Testing / tuning hook: prefill CTAs. -1 = one CTA per planned item (default; batches of
- * >= 4 waves with G % 4 == 0 run the items as 2-CTA clusters sharing K/V by multicast);
- * -2 = one CTA per item, clusters forced whenever G % 4 == 0; 0 = the persistent kernel, one
- * CTA per SM looping over the planned items; n > 0 = persistent with at most n CTAs.
- * INVALID_ARG below -2. */
+/* Testing / tuning hook: prefill CTAs. -1 = default: batches of >= 4 waves run one CTA per
+ * planned item (with G % 4 == 0 as 2-CTA clusters sharing K/V by multicast), smaller ones the
+ * persistent kernel on every SM with stream-K shares (whole units round-robin, the last
+ * partial wave's key tiles cut into equal-time pieces merged by LSE); -2 = one CTA per item,
+ * clusters forced whenever G % 4 == 0; -3 = one CTA per item at every batch size (the
+ * last wave's units split into equal pieces); 0 = the persistent kernel, one CTA per SM;
+ * n > 0 = persistent with at most n CTAs. With forced splits (hpa_set_prefill_splits 2..15)
+ * the persistent kernel takes the equal pieces instead of stream-K shares. INVALID_ARG below -3. */
 hpa_status_t hpa_set_prefill_ctas(hpa_cache_t* c, int32_t n);
 /* Introspection of the last hpa_prefill / hpa_prefill_span plan: *n_ctas prefill CTAs
  * launched, *n_split_units units split into *splits key ranges each (0 / 1 when none), or

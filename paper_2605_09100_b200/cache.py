@@ -396,8 +396,9 @@ class Cache:
         check(LIB.hpa_set_prefill_splits(self._h, splits))
 
     def set_prefill_ctas(self, n: int) -> None:
-        """-1 = one CTA per item (default), -2 = one CTA per item as forced 2-CTA clusters (G % 4 == 0),
-        0 = persistent prefill on every SM, n > 0 = at most n CTAs."""
+        """-1 = default (one CTA per item from 4 waves up, else the persistent kernel with stream-K
+        shares), -2 = one CTA per item as forced 2-CTA clusters (G % 4 == 0), -3 = one CTA per
+        item at every size, 0 = persistent prefill on every SM, n > 0 = at most n CTAs."""
         check(LIB.hpa_set_prefill_ctas(self._h, n))
 
     def prefill_plan_info(self) -> dict:

@@ -31,6 +31,7 @@
 #include <functional>
 #include <memory>
 #include <string>
+#include <tuple>
 #include <vector>
 
 using namespace hpa;
@@ -865,6 +866,114 @@ double list_schedule(std::vector<double>& heap, const double* items, size_t n) {
   return *std::max_element(heap.begin(), heap.end());
 }
 
+// Stream-K tail for the persistent prefill kernel (the default for batches under 4 waves:
+// configs[2] B = 1, 256 units on 148 SMs, 1202 vs 1174 TFLOP/s for the list-scheduled split
+// tail of one CTA per item; profiles/r2_prefill_streamk_ab.log). The first floor(nU / W) * W units (in
+// dispatch order) go round-robin to the W CTAs, whole -- as the hardware would dispatch them,
+// so the CTAs running at one time work on neighbouring units and share K/V tiles in L2. The
+// remaining nU mod W units are cut, in order, into W consecutive shares that fill every CTA
+// to the same estimated end time (tiles + per-item cost; water-filling over the CTAs' loads
+// after the whole units), so all CTAs finish together; a unit straddling share boundaries
+// becomes pieces merged by LSE (at most 15; none shorter than kMin tiles).
+// unit(k) -> (b, y, x, n, skip_a, n_skip).
+template <class UnitFn>
+bool plan_prefill_streamk(const hpa_cache_t* c, const int32_t* seq_ids, const int32_t* q_lens, const int32_t* q_off,
+                          int64_t nU, int32_t W, double o_item, double o_piece, UnitFn unit, PfPlan& plan) {
+  const int64_t R = nU % W, whole = nU - R;
+  std::vector<double> load(size_t(W), 0.0);
+  for (int64_t k = 0; k < whole; ++k) load[size_t(k % W)] += std::get<3>(unit(k)) + o_item;
+  int64_t Tt = 0;  // tail tiles
+  for (int64_t k = whole; k < nU; ++k) Tt += std::get<3>(unit(k));
+  const double per = o_piece * (1.0 + double(R) / W);  // piece cost per CTA (~1 + R/W pieces each)
+  // end time E: sum_c max(0, E - load_c - per) = Tt (bisection)
+  double lo = *std::min_element(load.begin(), load.end()),
+         hi = *std::max_element(load.begin(), load.end()) + double(Tt) + per;
+  for (int it = 0; it < 60; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    double f = 0;
+    for (double l : load) f += std::max(0.0, mid - l - per);
+    (f < double(Tt) ? lo : hi) = mid;
+  }
+  const double E = hi;
+  // shortest piece: 12 tiles, or the tail's per-CTA share when that is smaller (small batches)
+  const int32_t kMin = int32_t(std::max<int64_t>(4, std::min<int64_t>(12, Tt / W)));
+  struct Item { int32_t cta; int4 w0, w1, wq, wn; };
+  std::vector<Item> items;
+  plan.work.clear();
+  plan.parts.clear();
+  plan.mc2 = false;
+  plan.split_max = 1;
+  auto wq_of = [&](int32_t b) { return make_int4(seq_ids[b], q_lens[b], q_off[b], c->seqs[seq_ids[b]].len); };
+  auto wn_of = [&](int32_t b) { return make_int4(int32_t(c->seqs[seq_ids[b]].pages.size()), 0, 0, 0); };
+  for (int64_t k = 0; k < whole; ++k) {
+    const auto [b, y, x, n, skip_a, n_skip] = unit(k);
+    items.push_back({int32_t(k % W), make_int4(b, y, x, 1 << 4), make_int4(0, n, skip_a, n_skip), wq_of(b), wn_of(b)});
+  }
+  // CTA c takes tail tiles [bnd[c], bnd[c+1]) of the concatenated tail units: its room up to
+  // E minus about one piece's cost, scaled so the shares cover the tail exactly
+  std::vector<int64_t> bnd(size_t(W) + 1, 0);
+  {
+    std::vector<double> room(static_cast<size_t>(W));
+    double sum = 0;
+    for (int32_t i = 0; i < W; ++i) sum += room[size_t(i)] = std::max(0.0, E - load[size_t(i)] - per);
+    double acc = 0;
+    for (int32_t i = 0; i < W; ++i) {
+      acc += room[size_t(i)];
+      bnd[size_t(i) + 1] = sum > 0 ? int64_t(std::llround(acc / sum * double(Tt))) : Tt;
+    }
+    bnd[size_t(W)] = Tt;
+  }
+  int64_t g = 0;
+  std::vector<int4> pcs;  // {cta, first tile, tiles, -}
+  for (int64_t k = whole; k < nU; ++k) {
+    const auto [b, y, x, n, skip_a, n_skip] = unit(k);
+    const int64_t u0 = g, u1 = g + n;
+    g = u1;
+    pcs.clear();
+    int32_t ci = int32_t(std::upper_bound(bnd.begin(), bnd.end(), u0) - bnd.begin()) - 1;
+    for (; ci < W && bnd[size_t(ci)] < u1; ++ci) {
+      const int64_t lo = std::max(u0, bnd[size_t(ci)]), hi = std::min(u1, bnd[size_t(ci) + 1]);
+      if (hi > lo) pcs.push_back(make_int4(ci, int32_t(lo - u0), int32_t(hi - lo), 0));
+    }
+    // slivers shorter than kMin join their neighbour (at most 15 pieces)
+    for (size_t i = 0; pcs.size() > 1 && i < pcs.size();) {
+      if (pcs[i].z < kMin || pcs.size() > 15) {
+        if (i > 0) {
+          pcs[i - 1].z += pcs[i].z;
+        } else {
+          pcs[1].y = pcs[0].y;
+          pcs[1].z += pcs[0].z;
+        }
+        pcs.erase(pcs.begin() + std::ptrdiff_t(i));
+      } else {
+        ++i;
+      }
+    }
+    const int32_t ns = int32_t(pcs.size());
+    const int32_t part = int32_t(plan.parts.size() / 2);
+    if (ns > 1) {
+      plan.parts.push_back(make_int4(b, y, x, ns));
+      plan.parts.push_back(make_int4(q_lens[b], q_off[b], 0, 0));
+      plan.split_max = std::max(plan.split_max, ns);
+    }
+    for (int32_t p = 0; p < ns; ++p)
+      items.push_back({pcs[size_t(p)].x, make_int4(b, y, x, ns > 1 ? (p | (ns << 4) | (part << 8)) : (1 << 4)),
+                       make_int4(pcs[size_t(p)].y, pcs[size_t(p)].z, skip_a, n_skip), wq_of(b), wn_of(b)});
+  }
+  // each CTA's list: its whole units in dispatch order, then its tail pieces
+  std::stable_sort(items.begin(), items.end(), [](const Item& u, const Item& v) { return u.cta < v.cta; });
+  std::vector<int32_t> count(size_t(W), 0);
+  for (const Item& it : items) {
+    ++count[size_t(it.cta)];
+    plan.work.insert(plan.work.end(), {it.w0, it.w1, it.wq, it.wn});
+  }
+  int32_t n_ctas = W;
+  while (n_ctas > 1 && count[size_t(n_ctas) - 1] == 0) --n_ctas;
+  plan.cta_off.assign(size_t(n_ctas) + 1, 0);
+  for (int32_t i = 0; i < n_ctas; ++i) plan.cta_off[size_t(i) + 1] = plan.cta_off[size_t(i)] + count[size_t(i)];
+  return true;
+}
+
 // Key-tile iterations of every unit, computed here from the host mirror of the table exactly
 // as the kernel would (so the kernel needs no table search before its pipeline starts):
 // n = slot(i_max) / 128 + 1 tiles, minus the tiles wholly inside the GRC span when every
@@ -874,10 +983,10 @@ bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, 
                   const int32_t* q_off, const int32_t* span, PfPlan& plan) {
   const int32_t forced = c->pf_forced_splits;
   if (forced == 16 || !prefill_split_supported()) return false;
-  // persistent launch (one CTA per SM looping over its items) when selected with
-  // hpa_set_prefill_ctas(c, n >= 0); a positive value caps the CTA count. Not the default: it
-  // measured 2-3 % slower than one CTA per item
-  const bool persistent = c->pf_ctas >= 0;
+  // persistent launch (one CTA per SM looping over its items): selected with
+  // hpa_set_prefill_ctas(c, n >= 0) (a positive value caps the CTA count), and by default for
+  // batches of fewer than 4 waves (stream-K shares, below); larger batches run one CTA per item
+  // (2-3 % faster there, with 2-CTA clusters)
   const int32_t max_ctas = c->pf_ctas > 0 ? std::min(c->pf_ctas, c->num_sms) : c->num_sms;
   // per-item fixed cost in key tiles: a launched CTA (setup, pipeline fill, epilogue, CTA
   // switch; scripts/trace_prefill_ctas.py) vs a persistent item (Q reload bubble and the
@@ -919,6 +1028,7 @@ bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, 
   // tiles of one KV head read the same keys). Ordering units by length instead scattered a
   // wave over every (sequence, KV head) and re-read K/V from HBM (-4 % at configs[2] B = 4).
   const int64_t nU = int64_t(rows.size()) * Y;
+  const bool persistent = c->pf_ctas >= 0 || (c->pf_ctas == -1 && forced == 0 && nU < int64_t(4) * c->num_sms);
   const int32_t W = persistent ? max_ctas : c->num_sms;
   // The two head-pair units of a KV head as a 2-CTA cluster (consecutive work items, identical
   // key ranges) sharing every K/V box by TMA multicast: +1.3 % at configs[2] B=4, but pairing
@@ -942,6 +1052,11 @@ bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, 
     r0 = r1;
   }
   auto unit = [&](int64_t k) -> const U& { return rows[size_t(order[size_t(k)].first)]; };
+  if (persistent && forced == 0)
+    return plan_prefill_streamk(c, seq_ids, q_lens, q_off, nU, W, o_item_p, o_piece_p,
+                                [&](int64_t k) { return std::make_tuple(unit(k).b, order[size_t(k)].second, unit(k).x,
+                                                                        unit(k).n, unit(k).skip_a, unit(k).n_skip); },
+                                plan);
   int64_t best_tail = 0;
   int32_t best_s = 1;
   if (forced > 1) {
@@ -2436,7 +2551,7 @@ hpa_status_t hpa_prefill_plan_info(hpa_cache_t* c, int32_t* n_ctas, int32_t* n_s
 
 hpa_status_t hpa_set_prefill_ctas(hpa_cache_t* c, int32_t n) {
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
-  if (n < -2) return fail(HPA_ERR_INVALID_ARG, "prefill ctas %d < -2", n);
+  if (n < -3) return fail(HPA_ERR_INVALID_ARG, "prefill ctas %d < -3", n);
   c->pf_ctas = n;
   return HPA_OK;
 }

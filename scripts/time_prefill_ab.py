@@ -16,6 +16,8 @@ tag = os.path.basename(os.environ.get("HPA_LIB_PATH", "libhpa.so"))
 out = []
 for bp in [int(x) for x in os.environ.get("BATCHES", "4,1").split(",")]:
     cache, seqs, _ = build_decode_cache(torch, Cache, shape, bp, 8, 16384 + 2048, 0, 0, seed=777)
+    if os.environ.get("PF_CTAS"):  # prefill CTA mode (hpa_set_prefill_ctas): 0 = persistent
+        cache.set_prefill_ctas(int(os.environ["PF_CTAS"]))
     g = torch.Generator(device="cuda:0").manual_seed(99)
     q = torch.randn((bp * 2048, 32, 128), generator=g, device="cuda:0").to(torch.bfloat16)
     o = torch.empty_like(q)
@@ -34,4 +36,5 @@ for bp in [int(x) for x in os.environ.get("BATCHES", "4,1").split(",")]:
     ms = statistics.median(ws)
     out.append(f"B{bp} {ms:.4f} ms {bp * prefill_flops(17408, 2048, shape) / ms / 1e9:.1f} TFLOP/s")
     cache.close()
+tag += f" ctas={os.environ.get('PF_CTAS', '-1')} streamk={int('HPA_PF_STREAMK' in os.environ)}"
 print(tag, " | ".join(out), flush=True)

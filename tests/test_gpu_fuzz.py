@@ -46,7 +46,7 @@ def test_prefill_fuzz(case):
     q_lens = [min(int(rng.integers(1, L + 1)) if rng.random() < 0.7 else L, 900) for L in lens]
     layer = int(rng.integers(2))
     p.cache.set_prefill_splits(int(rng.choice([0, 0, 1, 2, 3, 5, 16])))
-    p.cache.set_prefill_ctas(int(rng.choice([-1, -1, -2, 0, 1, 3])))
+    p.cache.set_prefill_ctas(int(rng.choice([-1, -1, -2, -3, 0, 1, 3])))
     q = p.queries(sum(q_lens))
     use_span = rng.random() < 0.3
     if use_span:

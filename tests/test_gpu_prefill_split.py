@@ -75,12 +75,16 @@ def test_prefill_split_with_span(splits):
     check_close(got, np.concatenate(ref), f"prefill span split {splits}")
 
 
-def test_prefill_planner_small_batch_fills_sms():
-    """Planner (splits = 0) on a batch of fewer units than SMs: every unit is split; parity."""
+@pytest.mark.parametrize("ctas", [-3, -1])
+def test_prefill_planner_small_batch_fills_sms(ctas):
+    """Planner (splits = 0) on a batch of fewer units than SMs: every unit is split -- into
+    equal pieces of one CTA each (-3) or into stream-K shares of the persistent kernel (-1,
+    the default under 4 waves); parity."""
     shape = Shape(1, 8, 2, 128, 16)
     p = Pair(shape, num_pages=4096, max_seqs=2, max_pages_per_seq=1024)
     s = p.build([("latent", 128), ("tokens", 6000)])
     q = p.queries(512)
+    p.cache.set_prefill_ctas(ctas)
     p.cache.set_prefill_splits(1)
     p.cache.prefill(0, [s], [512], q.cuda())          # ships pending table writes
     before = p.cache.launch_count()
@@ -92,8 +96,10 @@ def test_prefill_planner_small_batch_fills_sms():
     torch.cuda.synchronize()
     assert p.cache.launch_count() - before == n_one + 1, "split plan: prefill + merge kernels"
     info = p.cache.prefill_plan_info()
-    assert info["split_units"] == 16 and info["splits"] >= 2 and 1 <= info["ctas"] <= 16 * info["splits"], info
-    check_close(got, _oracle_prefill(p, [s], [512], q), "prefill planner small batch")
+    assert info["split_units"] == 16 and info["splits"] >= 2, info
+    if ctas == -3:
+        assert 1 <= info["ctas"] <= 16 * info["splits"], info
+    check_close(got, _oracle_prefill(p, [s], [512], q), f"prefill planner small batch ctas={ctas}")
 
 
 def test_prefill_split_invalid_count():
