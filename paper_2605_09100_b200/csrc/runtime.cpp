@@ -935,6 +935,8 @@ bool plan_prefill_streamk(const hpa_cache_t* c, const int32_t* seq_ids, const in
       const int64_t lo = std::max(u0, bnd[size_t(ci)]), hi = std::min(u1, bnd[size_t(ci) + 1]);
       if (hi > lo) pcs.push_back(make_int4(ci, int32_t(lo - u0), int32_t(hi - lo), 0));
     }
+    if (pcs.empty())  // a unit without key tiles (not produced by the planner today) still writes its rows
+      pcs.push_back(make_int4(std::min(std::max(ci, 0), W - 1), 0, n, 0));
     // slivers shorter than kMin join their neighbour (at most 15 pieces)
     for (size_t i = 0; pcs.size() > 1 && i < pcs.size();) {
       if (pcs[i].z < kMin || pcs.size() > 15) {
