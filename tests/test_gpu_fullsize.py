@@ -96,6 +96,16 @@ def test_prefill_config2_full_size_sampled():
     ref = np.stack([attend(f64(q[t:t + 1]), k[:, :lb - C + t + 1], v[:, :lb - C + t + 1], shape.scale)[0]
                     for t in rows])
     check_close(out[rows], ref, "configs[2] prefill sampled rows")
+    # the bench's B=1 launch: stream-K shares on the persistent kernel (256 units, 1.73 waves);
+    # the one-CTA-per-item plan (-3) must agree everywhere up to fp32 summation order
+    info = cache.prefill_plan_info()
+    assert info["split_units"] > 0 and info["splits"] <= 15 and info["cluster"] == 1, info
+    cache.set_prefill_ctas(-3)
+    out2 = cache.prefill(0, seqs, [C], q.cuda())
+    torch.cuda.synchronize()
+    check_close(out2[rows], ref, "configs[2] prefill sampled rows, one CTA per item")
+    d = (out.float() - out2.float()).abs().max().item()
+    assert d <= 2.0 ** -7 * (1.0 + out2.float().abs().max().item()), d
     cache.close()
 
 
