@@ -1,6 +1,5 @@
 #!/bin/bash
-# configs[2] prefill: default (stream-K persistent under 4 waves) vs one CTA per item (-3) vs
-# persistent with equal split pieces (forced via -3 semantics is not possible: list only)
+# configs[2] prefill: default (stream-K persistent under 4 waves) vs one CTA per item (-3)
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 for r in 1 2 3; do
   python scripts/time_prefill_ab.py

@@ -36,5 +36,5 @@ for bp in [int(x) for x in os.environ.get("BATCHES", "4,1").split(",")]:
     ms = statistics.median(ws)
     out.append(f"B{bp} {ms:.4f} ms {bp * prefill_flops(17408, 2048, shape) / ms / 1e9:.1f} TFLOP/s")
     cache.close()
-tag += f" ctas={os.environ.get('PF_CTAS', '-1')} streamk={int('HPA_PF_STREAMK' in os.environ)}"
+tag += f" ctas={os.environ.get('PF_CTAS', '-1')}"
 print(tag, " | ".join(out), flush=True)
