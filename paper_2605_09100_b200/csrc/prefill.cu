@@ -34,8 +34,9 @@
 //  * Work: a host-planned list (plan_prefill in runtime.cpp) gives each CTA its unit and
 //    key-tile range; units of an under-filled last wave are split into key ranges whose
 //    fp32 O / l + LSE partials prefill_combine_kernel merges. The epilogue stages O in the
-//    idle K/V rings and writes it with TMA stores. prefill_persistent_kernel (opt-in) runs
-//    one CTA per SM over an item list instead.
+//    idle K/V rings and writes it with TMA stores. prefill_persistent_kernel runs one CTA per
+//    SM over a host-assigned item list instead (the default below 4 waves of units, with
+//    stream-K shares: plan_prefill_streamk in runtime.cpp).
 #include "hpa_kernels.h"
 #include "ptx.cuh"
 #include <cuda_bf16.h>
