@@ -1,4 +1,5 @@
 #!/bin/bash
+# (experiment record: the fused-merge build and its HPA_PF_SEP_MERGE knob were not kept; profiles/r2_prefill_fused_merge_ab.log)
 # persistent prefill: split units merged after each CTA's item list by the last-arriving piece
 # (default) vs the separate prefill_combine_kernel (HPA_PF_SEP_MERGE)
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
