@@ -895,6 +895,13 @@ bool plan_prefill_streamk(const hpa_cache_t* c, const int32_t* seq_ids, const in
     (f < double(Tt) ? lo : hi) = mid;
   }
   const double E = hi;
+  // a tail unit longer than 15 shares would need more pieces than the item format holds: the
+  // caller falls back to the list-scheduled plan (equal pieces of the last wave's units)
+  {
+    const double share = double(Tt) / W;
+    for (int64_t k = whole; k < nU; ++k)
+      if (double(std::get<3>(unit(k))) > 14.0 * std::max(1.0, share)) return false;
+  }
   // shortest piece: 12 tiles, or the tail's per-CTA share when that is smaller (small batches)
   const int32_t kMin = int32_t(std::max<int64_t>(4, std::min<int64_t>(12, Tt / W)));
   struct Item { int32_t cta; int4 w0, w1, wq, wn; };
@@ -1054,11 +1061,12 @@ bool plan_prefill(const hpa_cache_t* c, int32_t n_seqs, const int32_t* seq_ids, 
     r0 = r1;
   }
   auto unit = [&](int64_t k) -> const U& { return rows[size_t(order[size_t(k)].first)]; };
-  if (persistent && forced == 0)
-    return plan_prefill_streamk(c, seq_ids, q_lens, q_off, nU, W, o_item_p, o_piece_p,
+  if (persistent && forced == 0 &&
+      plan_prefill_streamk(c, seq_ids, q_lens, q_off, nU, W, o_item_p, o_piece_p,
                                 [&](int64_t k) { return std::make_tuple(unit(k).b, order[size_t(k)].second, unit(k).x,
                                                                         unit(k).n, unit(k).skip_a, unit(k).n_skip); },
-                                plan);
+                                plan))
+    return true;  // else (a unit would need more than 15 pieces) the list-scheduled plan below
   int64_t best_tail = 0;
   int32_t best_s = 1;
   if (forced > 1) {

@@ -255,3 +255,20 @@ def test_prefill_many_short_sequences_cluster_waves():
     got = p.cache.prefill(0, seqs, q_lens, q.cuda())
     torch.cuda.synchronize()
     check_close(got, _oracle_prefill(p, seqs, q_lens, q), "many short sequences")
+
+
+@pytest.mark.parametrize("hq,hkv,d,P,rows,ql", [(2, 1, 128, 16, 9000, 128), (3, 1, 64, 16, 7000, 200),
+                                                (4, 2, 128, 32, 6000, 300)])
+def test_prefill_default_plan_few_long_units(hq, hkv, d, P, rows, ql):
+    """Default plan on batches of a handful of very long units (few heads, one long sequence):
+    stream-K would cut a unit into more than 15 pieces, so the planner falls back to the
+    list-scheduled split plan of the persistent kernel; parity with the oracle either way."""
+    shape = Shape(1, hq, hkv, d, P)
+    p = Pair(shape, num_pages=rows // P + 64, max_seqs=2, max_pages_per_seq=rows // P + 32)
+    s = p.build([("latent", 128), ("tokens", rows)])
+    q = p.queries(ql)
+    got = p.cache.prefill(0, [s], [ql], q.cuda())
+    torch.cuda.synchronize()
+    info = p.cache.prefill_plan_info()
+    assert info["ctas"] >= 1 and info["splits"] <= 15, info
+    check_close(got, _oracle_prefill(p, [s], [ql], q), f"few long units {hq}/{hkv}/{d}/P{P}")
