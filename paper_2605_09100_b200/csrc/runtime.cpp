@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -1942,9 +1943,36 @@ hpa_status_t hpa_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int
   return decode_impl(c, layer, n_seqs, seq_ids, q, out, nullptr, nullptr, softmax_scale, stream);
 }
 
+#ifdef HPA_HOST_PROF  // diagnostics build: per-phase host time of hpa_append_decode, printed at exit
+namespace {
+struct HostProf {
+  double t[16] = {0};
+  long n = 0;
+  ~HostProf() {
+    if (n)
+      std::fprintf(stderr,
+                   "host prof (%ld calls, us): check %.2f ship %.2f apply %.2f tail %.2f decode %.2f "
+                   "[decode: checks+ship+batch %.2f groups %.2f splits %.2f upload %.2f launch %.2f]\n",
+                   n, t[0] / n, t[1] / n, t[2] / n, t[3] / n, t[4] / n, t[8] / n, t[9] / n, t[10] / n, t[11] / n,
+                   t[12] / n);
+  }
+} g_hprof;
+inline double hp_now() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+#define HP_MARK(i) do { const double _t = hp_now(); g_hprof.t[i] += _t - hp_last; hp_last = _t; } while (0)
+#else
+#define HP_MARK(i) do {} while (0)
+#endif
+
 hpa_status_t hpa_append_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
                                const void* k, const void* v, const void* q, void* out, float softmax_scale,
                                hpa_stream_t stream) {
+#ifdef HPA_HOST_PROF
+  double hp_last = hp_now();
+  ++g_hprof.n;
+#endif
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
   if (n_seqs < 0) return fail(HPA_ERR_INVALID_ARG, "n_seqs < 0");
   if (n_seqs == 0) return HPA_OK;
@@ -1961,6 +1989,7 @@ hpa_status_t hpa_append_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, co
   const std::vector<int32_t> ones(size_t(n_seqs), 1);
   int64_t rows = 0;
   if (hpa_status_t st = append_check(c, n_seqs, seq_ids, ones.data(), k, v, &rows)) return st;
+  HP_MARK(0);
   DeviceGuard dg(c->cfg.device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // fp8 token pages quantize on append (copy_kernels.cu); larger batches exceed the kernel's
@@ -1970,8 +1999,10 @@ hpa_status_t hpa_append_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, co
   if (fuse) {
     if (hpa_status_t st = ship(c, s, {}, {}, 0)) return st;  // earlier calls' table words first
   }
+  HP_MARK(1);
   std::vector<int32_t> slots;
   if (hpa_status_t st = append_apply(c, n_seqs, seq_ids, ones.data(), rows, s, slots)) return st;
+  HP_MARK(2);
   if (!fuse) {
     const int64_t Hd = int64_t(c->cfg.num_kv_heads) * c->cfg.head_dim;
     std::vector<ScatterRecord> recs{
@@ -2001,7 +2032,10 @@ hpa_status_t hpa_append_decode(hpa_cache_t* c, int32_t layer, int32_t n_seqs, co
   const PoolGeom g = c->geom();
   const AppendRows ap{k, v, g.k_pool, g.v_pool, rows * c->cfg.num_kv_heads * c->cfg.head_dim, n_seqs,
                       c->cfg.num_layers, tail.data()};
-  return decode_impl(c, layer, n_seqs, seq_ids, q, out, nullptr, nullptr, softmax_scale, stream, &ap);
+  HP_MARK(3);
+  const hpa_status_t st = decode_impl(c, layer, n_seqs, seq_ids, q, out, nullptr, nullptr, softmax_scale, stream, &ap);
+  HP_MARK(4);
+  return st;
 }
 
 hpa_status_t hpa_decode_partial(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids,
@@ -2168,6 +2202,9 @@ hpa_status_t plan_cascade(hpa_cache_t* c, int32_t n, const int32_t* seq_ids, std
 hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const int32_t* seq_ids, const void* q,
                          void* out, float* part_o, float* part_lse, float softmax_scale, hpa_stream_t stream,
                          const AppendRows* ap) {
+#ifdef HPA_HOST_PROF
+  double hp_last = hp_now();
+#endif
   if (!c) return fail(HPA_ERR_INVALID_ARG, "null cache");
   if (layer < 0 || layer >= c->cfg.num_layers) return fail(HPA_ERR_INVALID_ARG, "layer %d out of range", layer);
   if (n_seqs < 0) return fail(HPA_ERR_INVALID_ARG, "n_seqs < 0");
@@ -2188,12 +2225,14 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (hpa_status_t st = ship(c, s, {}, {}, 0)) return st;
   if (hpa_status_t st = upload_batch(c, n_seqs, seq_ids, s)) return st;
+  HP_MARK(8);
   const int32_t D = c->cfg.head_dim, Hq = c->cfg.num_q_heads, Hkv = c->cfg.num_kv_heads;
   int32_t S = 1;
   if (decode_persistent()) {
     if (Hkv > 255) return fail(HPA_ERR_UNSUPPORTED, "persistent decode supports H_kv <= 255");
     std::vector<CGroup> groups;
     groups = find_cascade_groups(c, n_seqs, seq_ids);
+    HP_MARK(9);
     std::vector<int32_t> sp;
     std::vector<int32_t> key;
     if (!groups.empty()) {
@@ -2203,6 +2242,7 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
       key.assign(seq_ids, seq_ids + n_seqs);
       key.insert(key.end(), sp.begin(), sp.end());
     }
+    HP_MARK(10);
     if (groups.empty() && key != c->plan_key) {
       // unit list, longest unit first (the kernel fetches units dynamically in this order)
       std::vector<std::pair<double, int32_t>> order;  // (-size, request)
@@ -2250,6 +2290,7 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
       c->plan_groups = false;
       c->plan_group_units = 0;
     }
+    HP_MARK(11);
   } else {
     S = plan_splits(c, n_seqs, max_entries, max_chunks);
   }
@@ -2279,6 +2320,7 @@ hpa_status_t decode_impl(hpa_cache_t* c, int32_t layer, int32_t n_seqs, const in
     return fail(HPA_ERR_UNSUPPORTED, "fp8 token pages need the persistent decode kernel");
   int launched = 0;
   cudaError_t e = launch_decode(c->tm_k_dec, c->tm_v_dec, a, D, s, &launched, ap);
+  HP_MARK(12);
   c->launches += launched;
   if (e != cudaSuccess) return cuda_fail(e, "decode launch");
   return HPA_OK;
