@@ -421,9 +421,10 @@ def run_ours(args):
     # One step = hpa_append_decode: the current token's K/V row of every request written into
     # its page slot (a1 + a2) and the split decode + combine (a4 + a5), one kernel launch
     # (+ the combine). Region A (the `value`) has nothing but the steps between its two
-    # events; region B repeats the steps with an event pair around every call for the
-    # per-launch duration of the roofline (events between launches break the programmatic
-    # dependent launch overlap, so they stay out of region A).
+    # events; then the e2e region (host copies, same lengths as region A); region B repeats the
+    # steps with an event pair around every call for the per-launch duration of the roofline
+    # (events between launches break the programmatic dependent launch overlap, so they stay
+    # out of region A).
     cache, seqs, _ = build_decode_cache(torch, Cache, shape, B, docs, tokens, 3 * K + W + 16, dev,
                                         seed=1234 + rank)
     if args.splits:
@@ -439,7 +440,6 @@ def run_ours(args):
     for i in range(W):
         cache.append_decode(0, ids, knew[i], vnew[i], qs[i], out)
     torch.cuda.synchronize(dev)
-    lens0 = [cache.seq_info(s)[0] for s in seqs]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = cache.launch_count()
     clk = ClockSampler(dev)
@@ -458,24 +458,6 @@ def run_ours(args):
     step_ms_max = max_over_ranks(step_ms, device=f"cuda:{dev}")
     total_tokens = B * world
     value = total_tokens / (step_ms_max / 1e3)
-    # region B: per-call events (the launch duration for the roofline)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    torch.cuda.synchronize(dev)
-    for i in range(K):
-        evs[i][0].record(stream)
-        cache.append_decode(0, ids, knew[W + K + i], vnew[W + K + i], qs[W + K + i], out)
-        evs[i][1].record(stream)
-    torch.cuda.synchronize(dev)
-    dec_ms = [a.elapsed_time(b) for a, b in evs]
-    dec_mean = sum(dec_ms) / K
-    dec_mean_max = max_over_ranks(dec_mean, device=f"cuda:{dev}")
-    # algorithmic bytes per call, averaged over region B's calls (lengths grow by one per step):
-    # the decode's K/V + q + out + table, plus the appended rows (read once, written once)
-    app_bytes = append_bytes(B, shape)
-    bytes_per_call = sum(decode_bytes([L + K + 1 + i for L in lens0], shape) for i in range(K)) / K + app_bytes
-    achieved = bytes_per_call / (dec_mean / 1e3) / 1e9
-    clocks = clk.summary()
-
     # ------------------------------------------------------------------ e2e through the public API
     # pinned host inputs -> device (copy stream, double-buffered) -> append + decode
     # (compute stream) -> output -> pinned host; all copies inside the timed region.
@@ -524,6 +506,26 @@ def run_ours(args):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / K, device=f"cuda:{dev}")
     h2d_bytes = dbuf[0].numel() * 2
     d2h = out.numel() * 2
+    # region B (after the e2e region, so that e2e runs at region A's lengths): per-call events
+    # (the launch duration for the roofline)
+    lensB = [cache.seq_info(s)[0] for s in seqs]
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    torch.cuda.synchronize(dev)
+    for i in range(K):
+        evs[i][0].record(stream)
+        cache.append_decode(0, ids, knew[W + K + i], vnew[W + K + i], qs[W + K + i], out)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    dec_ms = [a.elapsed_time(b) for a, b in evs]
+    dec_mean = sum(dec_ms) / K
+    dec_mean_max = max_over_ranks(dec_mean, device=f"cuda:{dev}")
+    # algorithmic bytes per call, averaged over region B's calls (lengths grow by one per step):
+    # the decode's K/V + q + out + table, plus the appended rows (read once, written once)
+    app_bytes = append_bytes(B, shape)
+    bytes_per_call = sum(decode_bytes([L + 1 + i for L in lensB], shape) for i in range(K)) / K + app_bytes
+    achieved = bytes_per_call / (dec_mean / 1e3) / 1e9
+    clocks = clk.summary()
+
     cache.close()
     del knew, vnew, qs, pin_in, pin_o
     torch.cuda.empty_cache()
