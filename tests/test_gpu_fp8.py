@@ -200,3 +200,36 @@ def test_fp8_page256_and_partial_pages():
     refp = np.stack([attend(f64(qp[t:t + 1]), k[:, :lb - 64 + t + 1], v[:, :lb - 64 + t + 1], shape.scale)[0]
                      for t in range(64)])
     check_close(outp, refp, "fp8 P=256 prefill")
+
+
+def test_fp8_prefill_config2_b4_full_size_sampled():
+    """configs[2] at B_p = 4 with fp8 token pages, as bench.py's next.fp8_prefill times it: the
+    batch's token pages dequantized into temporary bf16 pages, then the 1024-CTA cluster
+    launch. Two CPU-drawn requests mirrored in the oracle (prefill attends over the staged rows,
+    reading A20); 24 sampled query rows each, all 32 heads; the cache (fp8 codes, table, free
+    pages) unchanged afterwards is covered by test_fp8_prefill_parity_and_cache_unchanged."""
+    from tests.test_gpu_fullsize import _build
+    from oracle import OracleCache
+    from paper_2605_09100_b200 import Cache
+    from workloads import Draw
+    shape = qwen3_8b_shape(16)
+    C, prior, B, sampled = 2048, 16384, 4, [0, 2]
+    tok_pages = (prior + C) // 16
+    cache = Cache(1, 32, 8, 128, 16, B * (64 + tok_pages) + 64, B, 64 + tok_pages, 0, 99, "fp8", B * tok_pages + 64)
+    orc = OracleCache(1, 32, 8, 128, 16, token_fp8=True)
+    seqs, _ = _build(cache, orc, shape, B, sampled, 8, prior + C, 79)
+    q = torch.randn((B * C, 32, 128), device="cuda").to(torch.bfloat16)
+    qs = {s: Draw(30 + s).queries(shape, C) for s in sampled}
+    for s in sampled:
+        q[s * C:(s + 1) * C] = qs[s].cuda()
+    out = cache.prefill(0, seqs, [C] * B, q)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    for s in sampled:
+        k, v = orc.logical_kv(seqs[s], 0, fp8_staged=True)
+        lb = k.shape[1]
+        rows = sorted(set([0, 127, 128, 2047] + list(np.random.default_rng(s).integers(0, C, 20))))
+        ref = np.stack([attend(f64(qs[s][t:t + 1]), k[:, :lb - C + t + 1], v[:, :lb - C + t + 1], shape.scale)[0]
+                        for t in rows])
+        check_close(out[s * C:(s + 1) * C][rows], ref, f"configs[2] B=4 fp8 prefill request {s} sampled rows")
+    cache.close()
