@@ -300,3 +300,57 @@ def test_cascade_forced_mode_below_threshold():
     for bad in (-1, 3):
         with pytest.raises(HPAError):
             p.cache.set_decode_cascade(bad)
+
+
+def test_cascade_full_size_forked_prompt_sampled():
+    """bench.py's next.prefix_cascade at full size: B = 64 forks of one 16384-row prompt with
+    1024 rows of their own, decoded with the planner's cascade (group units present). Two forks
+    are mirrored in the oracle (the prompt and their own rows drawn on the CPU); the others get
+    GPU-drawn own rows and are checked for finiteness; cascade off must agree."""
+    from workloads import Draw, qwen3_8b_shape
+    from oracle import OracleCache
+    from paper_2605_09100_b200 import Cache
+    shape = qwen3_8b_shape(16)
+    B, prompt, own, sampled = 64, 16384, 1024, [0, 63]
+    cache = Cache(1, 32, 8, 128, 16, prompt // 16 + B * (own // 16 + 1) + 64, B + 1, prompt // 16 + own // 16 + 4,
+                  0, 99)
+    orc = OracleCache(1, 32, 8, 128, 16)
+    d = Draw(41)
+    src = cache.seq_create()
+    orc.create_seq(src)
+    k, v = d.tokens(shape, prompt)
+    cache.append_kv([src], [prompt], k.cuda(), v.cuda())
+    orc.append(src, f64(k), f64(v))
+    g = torch.Generator(device="cuda").manual_seed(42)
+    forks, ks, vs = [], [], []
+    for i in range(B):
+        f = cache.seq_fork(src, prompt)
+        forks.append(f)
+        if i in sampled:
+            orc.fork(src, prompt, f)
+            k, v = d.tokens(shape, own)
+            orc.append(f, f64(k), f64(v))
+            ks.append(k.cuda())
+            vs.append(v.cuda())
+        else:
+            ks.append(torch.randn((1, own, 8, 128), generator=g, device="cuda").to(torch.bfloat16))
+            vs.append(torch.randn((1, own, 8, 128), generator=g, device="cuda").to(torch.bfloat16))
+    cache.append_kv(forks, [own] * B, torch.cat(ks, 1), torch.cat(vs, 1))
+    q = torch.randn((B, 32, 128), generator=g, device="cuda").to(torch.bfloat16)
+    qs = d.queries(shape, len(sampled))
+    for i, s in enumerate(sampled):
+        q[s] = qs[i].cuda()
+    on = cache.decode(0, forks, q)
+    torch.cuda.synchronize()
+    assert cache.decode_plan_info()["group_units"] > 0
+    cache.set_decode_cascade(False)
+    off = cache.decode(0, forks, q)
+    torch.cuda.synchronize()
+    assert torch.isfinite(on.float()).all()
+    ref = np.stack([attend(f64(qs[i:i + 1]), *orc.logical_kv(forks[s], 0), shape.scale)[0]
+                    for i, s in enumerate(sampled)])
+    check_close(on[sampled], ref, "full-size forked prompt, cascade")
+    check_close(off[sampled], ref, "full-size forked prompt, plain")
+    dmax = (on.float() - off.float()).abs().max().item()
+    assert dmax <= 2.0 ** -7 * (1.0 + off.float().abs().max().item()), dmax
+    cache.close()
