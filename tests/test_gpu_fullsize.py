@@ -214,3 +214,28 @@ def test_prefill_config2_b4_full_size_sampled_clusters():
                         for t in rows])
         check_close(out[s * C:(s + 1) * C][rows], ref, f"configs[2] B=4 prefill request {s} sampled rows")
     cache.close()
+
+
+def test_span_prefill_config2_full_size_sampled():
+    """bench.py's next.span_prefill at full size: configs[2] B = 1 (the default stream-K plan on
+    the persistent kernel) with the GRC mask-out span over the first 8192 token rows (all C
+    queries are segment-3 rows); 12 sampled query rows, all 32 heads, against oracle.attend_span."""
+    from oracle import attend_span
+    from paper_2605_09100_b200 import Cache
+    shape = qwen3_8b_shape(16)
+    C, prior, n1 = 2048, 16384, 8192
+    cache = Cache(1, 32, 8, 128, 16, 1300, 1, 1300, 0, 99)
+    orc = OracleCache(1, 32, 8, 128, 16)
+    seqs, _ = _build(cache, orc, shape, 1, [0], 8, prior + C, 46)
+    q = Draw(47).queries(shape, C)
+    span = (1024, 1024 + n1, 1024 + prior)
+    out = cache.prefill_span(0, seqs, [C], [span], q.cuda())
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    k, v = orc.logical_kv(seqs[0], 0)
+    lb = k.shape[1]
+    rows = sorted(set([0, 127, 1024, 2047] + list(np.random.default_rng(5).integers(0, C, 8))))
+    ref = np.stack([attend_span(f64(q[t:t + 1]), k[:, :lb - C + t + 1], v[:, :lb - C + t + 1], shape.scale,
+                                *span)[0] for t in rows])
+    check_close(out[rows], ref, "configs[2] span prefill sampled rows")
+    cache.close()
