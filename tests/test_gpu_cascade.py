@@ -354,3 +354,56 @@ def test_cascade_full_size_forked_prompt_sampled():
     dmax = (on.float() - off.float()).abs().max().item()
     assert dmax <= 2.0 ** -7 * (1.0 + off.float().abs().max().item()), dmax
     cache.close()
+
+
+def test_shared_latent_sets_full_size_sampled():
+    """bench.py's next.shared_sets at full size: B = 64 requests sharing the same 8 latent sets
+    of 128 rows (stored once, refcounted) followed by 4096 token rows each; the planner decides
+    (the shared run is 1/5 of the reads: no group units at the default threshold), forced cascade
+    (mode 2) and cascade off must all match the oracle on two CPU-drawn requests."""
+    from workloads import Draw, LATENT_ROWS, qwen3_8b_shape
+    from oracle import OracleCache
+    from paper_2605_09100_b200 import Cache
+    shape = qwen3_8b_shape(16)
+    B, tokens, sampled = 64, 4096, [5, 40]
+    cache = Cache(1, 32, 8, 128, 16, 64 + B * (tokens // 16 + 1) + 64, B + 1, 64 + tokens // 16 + 4, 0, 99)
+    orc = OracleCache(1, 32, 8, 128, 16)
+    d = Draw(51)
+    owner = cache.seq_create()
+    orc.create_seq(owner)
+    for _ in range(8):
+        kv = d.latent(shape, LATENT_ROWS)
+        assert cache.latent_install(owner, -1, kv.cuda()) == orc.install(owner, -1, f64(kv))
+    seqs = [cache.seq_create() for _ in range(B)]
+    g = torch.Generator(device="cuda").manual_seed(52)
+    ks = []
+    for i, s in enumerate(seqs):
+        if i in sampled:
+            orc.create_seq(s)
+        for sid in range(8):
+            got = cache.latent_share(s, owner, sid)
+            if i in sampled:
+                assert got == orc.share(s, owner, sid)
+    for i, s in enumerate(seqs):
+        if i in sampled:
+            k, v = d.tokens(shape, tokens)
+            orc.append(s, f64(k), f64(v))
+            ks.append((k.cuda(), v.cuda()))
+        else:
+            ks.append((torch.randn((1, tokens, 8, 128), generator=g, device="cuda").to(torch.bfloat16),) * 2)
+    cache.append_kv(seqs, [tokens] * B, torch.cat([a for a, _ in ks], 1), torch.cat([b for _, b in ks], 1))
+    q = torch.randn((B, 32, 128), generator=g, device="cuda").to(torch.bfloat16)
+    qs = d.queries(shape, len(sampled))
+    for i, s in enumerate(sampled):
+        q[s] = qs[i].cuda()
+    ref = np.stack([attend(f64(qs[i:i + 1]), *orc.logical_kv(seqs[s], 0), shape.scale)[0]
+                    for i, s in enumerate(sampled)])
+    for mode in (1, 2, 0):
+        cache.set_decode_cascade(mode)
+        out = cache.decode(0, seqs, q)
+        torch.cuda.synchronize()
+        assert torch.isfinite(out.float()).all()
+        if mode == 2:
+            assert cache.decode_plan_info()["group_units"] > 0
+        check_close(out[sampled], ref, f"full-size shared latent sets, cascade mode {mode}")
+    cache.close()
