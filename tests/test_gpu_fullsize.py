@@ -10,6 +10,9 @@ configs[3]: B=256 LMAG step (batched latent replacement + append + decode);
 configs[1] ragged variant: reasoning rows ~ U[1K, 8K] per request.
 configs[4]: per-GPU shard of the 8-GPU sweep (B=512/8=64 requests) at ctx=64K
             with latent ratios 0.1 and 0.9; 2 sampled requests.
+NEXT rows as bench.py times them: the GRC span prefill (configs[2] B=1, 8192 masked rows)
+and the B=64 compress batch (4096-row documents -> 128-row latent sets); fp8 prefill at
+B=4 is in test_gpu_fp8.py, the full-size prefix cascade and shared sets in test_gpu_cascade.py.
 Sampled requests are drawn on the CPU (workloads.Draw); the rest of the batch
 is filled with GPU-drawn data of the same distribution (it only shapes the
 launch; its outputs are checked for finiteness)."""
@@ -238,4 +241,39 @@ def test_span_prefill_config2_full_size_sampled():
     ref = np.stack([attend_span(f64(q[t:t + 1]), k[:, :lb - C + t + 1], v[:, :lb - C + t + 1], shape.scale,
                                 *span)[0] for t in rows])
     check_close(out[rows], ref, "configs[2] span prefill sampled rows")
+    cache.close()
+
+
+def test_compress_batch_full_size_sampled():
+    """bench.py's next.compress at full size: B = 64 requests of 8 latent sets + a 4096-row
+    document + 128 meta-latent rows, one hpa_seq_compress_batch call turning the last 128 rows
+    of each into a latent set and dropping the document. Two requests mirrored in the oracle:
+    their logical K/V after the call is bit-exact, their decode matches; every request freed
+    its document pages (4096 / 16 - its kept partial page) and decodes finitely."""
+    from paper_2605_09100_b200 import Cache
+    shape = qwen3_8b_shape(16)
+    B, n_doc, m, sampled = 64, 4096, LATENT_ROWS, [3, 60]
+    pages = 64 + (n_doc + m) // 16 + 2
+    cache = Cache(1, 32, 8, 128, 16, B * pages + 64, B, pages, 0, 99)
+    orc = OracleCache(1, 32, 8, 128, 16)
+    seqs, _ = _build(cache, orc, shape, B, sampled, 8, n_doc + m, 80)
+    free0 = cache.stats()[0]
+    sets = cache.compress_batch(seqs, [n_doc] * B, [m] * B)
+    torch.cuda.synchronize()
+    for s in sampled:
+        assert sets[s] == orc.compress(seqs[s], n_doc, m)
+        k1, v1 = orc.logical_kv(seqs[s], 0)
+        k2, v2 = cache.export_logical_kv(0, seqs[s])
+        assert np.array_equal(k1, f64(k2)) and np.array_equal(v1, f64(v2)), s
+    assert cache.stats()[0] - free0 == B * (n_doc // 16), (cache.stats()[0], free0)
+    q = torch.randn((B, 32, 128), device="cuda").to(torch.bfloat16)
+    qs = Draw(81).queries(shape, len(sampled))
+    for i, s in enumerate(sampled):
+        q[s] = qs[i].cuda()
+    out = cache.decode(0, seqs, q)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    ref = np.stack([attend(f64(qs[i:i + 1]), *orc.logical_kv(seqs[s], 0), shape.scale)[0]
+                    for i, s in enumerate(sampled)])
+    check_close(out[sampled], ref, "decode after full-size compress batch")
     cache.close()
