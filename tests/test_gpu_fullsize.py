@@ -11,7 +11,8 @@ configs[1] ragged variant: reasoning rows ~ U[1K, 8K] per request.
 configs[4]: per-GPU shard of the 8-GPU sweep (B=512/8=64 requests) at ctx=64K
             with latent ratios 0.1 and 0.9; 2 sampled requests.
 NEXT rows as bench.py times them: the GRC span prefill (configs[2] B=1, 8192 masked rows)
-and the B=64 compress batch (4096-row documents -> 128-row latent sets); fp8 prefill at
+the B=64 compress batch (4096-row documents -> 128-row latent sets) and the B=256
+host-staged install; fp8 prefill at
 B=4 is in test_gpu_fp8.py, the full-size prefix cascade and shared sets in test_gpu_cascade.py.
 Sampled requests are drawn on the CPU (workloads.Draw); the rest of the batch
 is filled with GPU-drawn data of the same distribution (it only shapes the
@@ -276,4 +277,41 @@ def test_compress_batch_full_size_sampled():
     ref = np.stack([attend(f64(qs[i:i + 1]), *orc.logical_kv(seqs[s], 0), shape.scale)[0]
                     for i, s in enumerate(sampled)])
     check_close(out[sampled], ref, "decode after full-size compress batch")
+    cache.close()
+
+
+def test_host_staged_install_full_size_sampled():
+    """bench.py's next.host_staged_install at full size: B = 256 configs[1]-shaped requests, one
+    128-row latent set of each replaced from a pinned host payload in one
+    hpa_latent_set_install_host call (copy stream + scatter). Two requests mirrored in the
+    oracle: bit-exact logical views and decode parity afterwards."""
+    from paper_2605_09100_b200 import Cache
+    shape = qwen3_8b_shape(16)
+    B, sampled, tokens = 256, [7, 200], 4096
+    pages = 64 + tokens // 16 + 2
+    cache = Cache(1, 32, 8, 128, 16, B * pages + 64, B, pages, 0, 99)
+    orc = OracleCache(1, 32, 8, 128, 16)
+    seqs, _ = _build(cache, orc, shape, B, sampled, 8, tokens, 90)
+    d = Draw(91)
+    kv = torch.randn((B, 1, 2, LATENT_ROWS, 8, 128)).to(torch.bfloat16)
+    for s in sampled:
+        kv[s] = d.latent(shape, LATENT_ROWS)
+    kv = kv.pin_memory()
+    got = cache.latent_install_host(seqs, [3] * B, kv)
+    torch.cuda.synchronize()
+    for s in sampled:
+        assert got[s] == orc.install(seqs[s], 3, f64(kv[s]))
+        k1, v1 = orc.logical_kv(seqs[s], 0)
+        k2, v2 = cache.export_logical_kv(0, seqs[s])
+        assert np.array_equal(k1, f64(k2)) and np.array_equal(v1, f64(v2)), s
+    q = torch.randn((B, 32, 128), device="cuda").to(torch.bfloat16)
+    qs = Draw(92).queries(shape, len(sampled))
+    for i, s in enumerate(sampled):
+        q[s] = qs[i].cuda()
+    out = cache.decode(0, seqs, q)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    ref = np.stack([attend(f64(qs[i:i + 1]), *orc.logical_kv(seqs[s], 0), shape.scale)[0]
+                    for i, s in enumerate(sampled)])
+    check_close(out[sampled], ref, "decode after full-size host-staged install")
     cache.close()
